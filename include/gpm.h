@@ -1,0 +1,168 @@
+/* gpm.h — C ABI of the B200-native extend-reduce-filter engine (libgpm.so).
+ *
+ * Drop-in boundary for the Pangolin hot path (arXiv 1911.06969).  Every entry
+ * point names the reference interface it replaces.  Reference paths are
+ * relative to /root/reference:
+ *   proj/include/gpmine/graph.hpp, graph_io.hpp, embedding_list.hpp, error.hpp
+ *   SPEC.md (engine / apps / cli modules; the hot path exists only as spec)
+ *   PAPER.md (Alg. 1, Alg. 2, Listings 1-6)
+ *
+ * Conventions: plain pointers and sizes only; the caller owns input arrays
+ * (copied at create time); the library owns graphs/results until *_free.
+ * Exceptions never cross the ABI: every function returns a gpm_status and a
+ * thread-local message is available from gpm_last_error()
+ * (replaces gpmine::error / parse_error, error.hpp:10-25).
+ */
+#ifndef GPM_H_
+#define GPM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum gpm_status {
+  GPM_OK = 0,
+  GPM_EINVAL = 1,   /* bad argument / out-of-range id                 */
+  GPM_EPARSE = 2,   /* input text malformed (parse_error, error.hpp:16) */
+  GPM_ENOMEM = 3,   /* host or device allocation failed               */
+  GPM_ECUDA = 4,    /* CUDA runtime error / no device                 */
+  GPM_ENCCL = 5,    /* collective exchange callback failed            */
+  GPM_ECONFIG = 6   /* config conflict, e.g. chunking + filter */
+} gpm_status;
+
+typedef enum gpm_app {
+  GPM_APP_TC = 0,   /* triangle_count       */
+  GPM_APP_CF = 1,   /* clique_find(k)  SPEC.md:423-431, Listing 3 */
+  GPM_APP_MC = 2,   /* motif_count(k)  SPEC.md:432-440, Listing 4 */
+  GPM_APP_FSM = 3   /* fsm(k, sigma)   SPEC.md:441-449, Listing 5 */
+} gpm_app;
+
+typedef struct gpm_graph gpm_graph;
+typedef struct gpm_result gpm_result;
+
+/* Collective hook for multi-GPU runs (one process per GPU).  The library calls
+ * it with a DEVICE buffer on `stream`; the host side performs the exchange
+ * (torch.distributed / NCCL over NVLink) in place and returns 0 on success.
+ *   op 0 = sum over ranks (uint64 elements)
+ *   op 1 = bitwise OR over ranks (uint32 words; FSM domain bitmaps)
+ *   op 2 = all-gather: buf holds world*count elements, slot `rank` filled  */
+typedef int (*gpm_exchange_fn)(void* ctx, void* dev_buf, uint64_t count, int elem_bytes, int op, void* stream);
+
+/* EngineConfig + CliConfig knobs. */
+typedef struct gpm_config {
+  int app;                  /* gpm_app                                            */
+  int k;                    /* MAX_SIZE: vertices (TC/CF/MC); edges+1 (FSM)       */
+  uint64_t min_support;     /* sigma for FSM (to_prune = MNI < sigma)              */
+  uint64_t mem_budget;      /* device bytes for materialised levels; 0 = auto     */
+  int no_orient;            /* TC/CF: skip degree-ordered DAG orientation         */
+  int rank, world;          /* root-unit partition (degree-weighted static split) */
+  uint64_t root_lo, root_hi;/* explicit level-1 slice; root_hi=0 -> whole/split   */
+  void* stream;             /* cudaStream_t to launch on; NULL = library stream   */
+  gpm_exchange_fn exchange; /* optional collective hook (world > 1)               */
+  void* exchange_ctx;
+} gpm_config;
+
+void gpm_config_default(gpm_config* cfg);
+
+/* ---------------------------------------------------------------- graph core */
+
+/* Graph ctor (graph.hpp:29-55): validates strictly ascending lists, no
+ * self-loops, ids < n; uploads CSR (u64 offsets, u32 col, optional u32 labels)
+ * to `device`.  oriented != 0 marks a DAG input. */
+int gpm_graph_create_csr(const uint64_t* row_offsets, const uint32_t* col, const uint32_t* labels, uint32_t n,
+                         uint64_t m, int oriented, int device, gpm_graph** out);
+
+/* orient_dag (graph.hpp:121-132): keep u->v iff (deg u, u) < (deg v, v); runs
+ * on the device.  Errors if already oriented. */
+int gpm_graph_orient_dag(const gpm_graph* g, gpm_graph** out);
+
+/* num_vertices / num_edges / oriented (graph.hpp:60-72). */
+int gpm_graph_info(const gpm_graph* g, uint32_t* n, uint64_t* m, int* oriented, int* labeled);
+
+/* Copy the device CSR back (for tests of orient_dag). */
+int gpm_graph_download(const gpm_graph* g, uint64_t* row_offsets, uint32_t* col);
+
+/* is_connected (graph.hpp:93-97) batched on the device: out[i] = v_i in N(u_i). */
+int gpm_graph_is_connected(const gpm_graph* g, const uint32_t* us, const uint32_t* vs, uint64_t q, uint8_t* out);
+
+/* init_single_edges (embedding_list.hpp:178-192), vertex mode: level-1 idx/vid
+ * as built on the device (tests / listing). cap in entries. */
+int gpm_level1(const gpm_graph* g, uint32_t* idx, uint32_t* vid, uint64_t cap, uint64_t* n_out);
+
+void gpm_graph_free(gpm_graph* g);
+
+/* ---------------------------------------------------------------- engine */
+
+/* mine (Alg. 1) with the app's hooks
+ * (to_extend / to_add / get_pattern / to_prune) compiled into the kernels.
+ * TC/CF orient internally unless no_orient or the graph is already a DAG
+ * (apps).  Blocking; one in-flight job per graph. */
+int gpm_mine(const gpm_graph* g, const gpm_config* cfg, gpm_result** out);
+
+/* TC/CF total count (AppResult.total_count). */
+int gpm_result_total(const gpm_result* r, uint64_t* total);
+
+/* PatternMap: n patterns; text in the stable form
+ * "k=<n>;L=..;E=(i,j)..".  FSM patterns carry their level
+ * (edges) and MNI support; MC patterns carry counts (level = k). */
+int gpm_result_num_patterns(const gpm_result* r, uint64_t* n);
+int gpm_result_pattern(const gpm_result* r, uint64_t i, char* text, size_t cap, uint64_t* support, int* level);
+
+/* Stats record: per-level sizes (|L1|, accepted per extend level),
+ * candidates per extend level, FSM survivors per level, N_explored, B_alg
+ * and device ms per phase. Arrays are copied up to cap. */
+typedef struct gpm_stats {
+  int n_levels;
+  uint64_t level_sizes[16];
+  uint64_t candidates[16];
+  uint64_t survivors[16];
+  uint64_t n_explored;
+  double b_alg;
+  double ms_total;          /* device time of gpm_mine (events on its stream)    */
+  double ms_extend;         /* extend kernels (count/write/fused)                */
+  double ms_dominant;       /* the dominant extend kernel's total time           */
+  double b_dominant;        /* algorithmic bytes of the dominant kernel          */
+  uint64_t launches;        /* kernels launched by this gpm_mine call            */
+  uint64_t chunks;          /* planner chunks used                               */
+  char dominant[64];        /* name of the dominant kernel                       */
+} gpm_stats;
+int gpm_result_stats(const gpm_result* r, gpm_stats* out);
+
+void gpm_result_free(gpm_result* r);
+
+/* ---------------------------------------------------------------- host input
+ * Host-side loaders with the exact graph_io.hpp semantics (symmetrise, drop
+ * self-loops, dedup, ids compacted ascending; gSpan labels interned).  The
+ * returned arrays are malloc'd; release with gpm_csr_free. */
+typedef struct gpm_csr {
+  uint32_t n;
+  uint64_t m;
+  uint64_t* row_offsets;
+  uint32_t* col;
+  uint32_t* labels;        /* NULL for edge lists */
+  uint64_t* original_ids;  /* dense -> input id   */
+} gpm_csr;
+
+/* load_edge_list (graph_io.hpp:83-116); *err_line set on GPM_EPARSE. */
+int gpm_load_edge_list(const char* path, gpm_csr* out, uint64_t* err_line);
+/* load_labeled_graph (graph_io.hpp:126-211). */
+int gpm_load_labeled_graph(const char* path, gpm_csr* out, uint64_t* err_line);
+/* Build a cleaned CSR from an in-memory edge list (same cleaning rules). */
+int gpm_csr_from_edges(const uint64_t* src, const uint64_t* dst, uint64_t n_edges, gpm_csr* out);
+/* Seeded RMAT generator: m0 = round(ef * 2^scale) edges,
+ * quadrant probabilities (a,b,c,1-a-b-c), seeded vertex permutation, then
+ * load_edge_list cleaning; labels uniform in [0,n_labels) when n_labels > 0. */
+int gpm_generate_rmat(int scale, double edge_factor, double a, double b, double c, uint64_t seed,
+                      uint32_t n_labels, uint64_t label_seed, gpm_csr* out);
+void gpm_csr_free(gpm_csr* csr);
+
+const char* gpm_last_error(void);
+const char* gpm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPM_H_ */

@@ -1,0 +1,243 @@
+"""Host-side mirror of the reference interface, over the C ABI (libgpm.so).
+
+Reference surface mirrored here (paths relative to /root/reference):
+
+=====================================  ==========================================
+reference                              here
+=====================================  ==========================================
+``load_edge_list`` graph_io.hpp:83      :func:`load_edge_list`
+``load_labeled_graph`` graph_io.hpp:126 :func:`load_labeled_graph`
+``Graph`` graph.hpp:22                  :class:`HostGraph` (host CSR), :class:`Graph` (device)
+``orient_dag`` graph.hpp:121            :meth:`Graph.orient_dag`
+``is_connected`` graph.hpp:93           :meth:`Graph.is_connected`
+``init_single_edges`` emb_list.hpp:178  :meth:`Graph.level1`
+``mine`` SPEC.md:371                    :func:`mine` (EngineConfig SPEC.md:337)
+``triangle_count`` SPEC.md:414          :func:`triangle_count`
+``clique_find`` SPEC.md:423             :func:`clique_find`
+``motif_count`` SPEC.md:432             :func:`motif_count`
+``fsm`` SPEC.md:441                     :func:`fsm`
+``error`` / ``parse_error`` error.hpp   :class:`GpmError` / :class:`ParseError`
+=====================================  ==========================================
+
+All mining runs in the sm_100a kernels of libgpm.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+
+from . import _lib as _L
+from ._lib import GpmError, ParseError, check, lib
+
+APP_IDS = {"tc": _L.APP_TC, "cf": _L.APP_CF, "mc": _L.APP_MC, "fsm": _L.APP_FSM}
+
+
+def _p(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+@dataclass
+class HostGraph:
+    """Host CSR (graph.hpp:22-115): u64 row offsets, u32 ascending neighbour
+    lists, optional u32 labels, dense -> input id map."""
+    off: np.ndarray
+    col: np.ndarray
+    labels: Optional[np.ndarray] = None
+    original_ids: Optional[np.ndarray] = None
+    oriented: bool = False
+
+    @property
+    def n(self) -> int:
+        return len(self.off) - 1
+
+    @property
+    def m(self) -> int:
+        return len(self.col)
+
+    def degree(self) -> np.ndarray:
+        return np.diff(self.off.astype(np.int64))
+
+
+def _take_csr(cs: _L.CsrStruct) -> HostGraph:
+    n, m = cs.n, cs.m
+    off = np.ctypeslib.as_array(C.cast(cs.row_offsets, C.POINTER(C.c_uint64)), shape=(n + 1,)).copy()
+    col = (np.ctypeslib.as_array(C.cast(cs.col, C.POINTER(C.c_uint32)), shape=(m,)).copy()
+           if m else np.zeros(0, np.uint32))
+    lab = (np.ctypeslib.as_array(C.cast(cs.labels, C.POINTER(C.c_uint32)), shape=(n,)).copy()
+           if cs.labels and n else None)
+    ids = (np.ctypeslib.as_array(C.cast(cs.original_ids, C.POINTER(C.c_uint64)), shape=(n,)).copy()
+           if cs.original_ids and n else None)
+    lib().gpm_csr_free(C.byref(cs))
+    return HostGraph(off, col, lab, ids)
+
+
+def load_edge_list(path: str) -> HostGraph:
+    cs, line = _L.CsrStruct(), C.c_uint64(0)
+    rc = lib().gpm_load_edge_list(str(path).encode(), C.byref(cs), C.byref(line))
+    check(rc, line.value)
+    return _take_csr(cs)
+
+
+def load_labeled_graph(path: str) -> HostGraph:
+    cs, line = _L.CsrStruct(), C.c_uint64(0)
+    rc = lib().gpm_load_labeled_graph(str(path).encode(), C.byref(cs), C.byref(line))
+    check(rc, line.value)
+    return _take_csr(cs)
+
+
+def csr_from_edges(src, dst) -> HostGraph:
+    s = np.ascontiguousarray(src, dtype=np.uint64)
+    d = np.ascontiguousarray(dst, dtype=np.uint64)
+    cs = _L.CsrStruct()
+    check(lib().gpm_csr_from_edges(_p(s), _p(d), len(s), C.byref(cs)))
+    return _take_csr(cs)
+
+
+def generate_rmat(scale: int, edge_factor: float, a: float, b: float, c: float, seed: int = 1,
+                  n_labels: int = 0, label_seed: int = 101) -> HostGraph:
+    cs = _L.CsrStruct()
+    check(lib().gpm_generate_rmat(scale, edge_factor, a, b, c, seed, n_labels, label_seed, C.byref(cs)))
+    return _take_csr(cs)
+
+
+class Graph:
+    """Immutable device CSR (one per GPU; "safe for unrestricted
+    concurrent reads")."""
+
+    def __init__(self, host: HostGraph = None, device: int = 0, *, _handle=None):
+        L = lib()
+        if _handle is not None:
+            self._h = _handle
+        else:
+            off = np.ascontiguousarray(host.off, dtype=np.uint64)
+            col = np.ascontiguousarray(host.col, dtype=np.uint32)
+            lab = None if host.labels is None else np.ascontiguousarray(host.labels, dtype=np.uint32)
+            h = C.c_void_p()
+            check(L.gpm_graph_create_csr(_p(off), _p(col), _p(lab), host.n, host.m, int(host.oriented), device,
+                                         C.byref(h)))
+            self._h = h
+        n, m, o, lb = C.c_uint32(), C.c_uint64(), C.c_int(), C.c_int()
+        check(L.gpm_graph_info(self._h, C.byref(n), C.byref(m), C.byref(o), C.byref(lb)))
+        self.n, self.m, self.oriented, self.labeled = n.value, m.value, bool(o.value), bool(lb.value)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _L._lib is not None:
+            _L._lib.gpm_graph_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def orient_dag(self) -> "Graph":
+        h = C.c_void_p()
+        check(lib().gpm_graph_orient_dag(self._h, C.byref(h)))
+        return Graph(_handle=h)
+
+    def download(self) -> HostGraph:
+        off = np.zeros(self.n + 1, np.uint64)
+        col = np.zeros(max(self.m, 1), np.uint32)
+        check(lib().gpm_graph_download(self._h, _p(off), _p(col)))
+        return HostGraph(off, col[:self.m], oriented=self.oriented)
+
+    def is_connected(self, us, vs) -> np.ndarray:
+        u = np.ascontiguousarray(us, dtype=np.uint32).reshape(-1)
+        v = np.ascontiguousarray(vs, dtype=np.uint32).reshape(-1)
+        out = np.zeros(len(u), np.uint8)
+        check(lib().gpm_graph_is_connected(self._h, _p(u), _p(v), len(u), _p(out)))
+        return out.astype(bool)
+
+    def level1(self) -> Tuple[np.ndarray, np.ndarray]:
+        n = C.c_uint64()
+        check(lib().gpm_level1(self._h, None, None, 0, C.byref(n)))
+        idx = np.zeros(max(n.value, 1), np.uint32)
+        vid = np.zeros(max(n.value, 1), np.uint32)
+        check(lib().gpm_level1(self._h, _p(idx), _p(vid), n.value, C.byref(n)))
+        return idx[:n.value], vid[:n.value]
+
+
+@dataclass
+class MineResult:
+    """AppResult + engine stats."""
+    app: str
+    k: int
+    total: int
+    patterns: List[Tuple[int, str, int]]  # (level, canonical text, support)
+    stats: Dict = field(default_factory=dict)
+
+    def pattern_map(self) -> Dict[str, int]:
+        return {t: s for _, t, s in self.patterns}
+
+
+def make_config(app: str, k: int = 3, min_support: int = 0, *, mem_budget: int = 0, no_orient: bool = False,
+                rank: int = 0, world: int = 1, root_lo: int = 0, root_hi: int = 0, stream: int = 0,
+                exchange=None) -> _L.Config:
+    cfg = _L.Config()
+    lib().gpm_config_default(C.byref(cfg))
+    cfg.app = APP_IDS[app]
+    cfg.k = k
+    cfg.min_support = min_support
+    cfg.mem_budget = mem_budget
+    cfg.no_orient = int(no_orient)
+    cfg.rank, cfg.world = rank, world
+    cfg.root_lo, cfg.root_hi = root_lo, root_hi
+    cfg.stream = stream or None
+    if exchange is not None:
+        cfg.exchange = exchange
+    return cfg
+
+
+def mine(g: Graph, app: str, k: int = 3, min_support: int = 0, **kw) -> MineResult:
+    """mine(g, cfg): extend/reduce/filter level loop."""
+    cfg = make_config(app, k, min_support, **kw)
+    L = lib()
+    r = C.c_void_p()
+    check(L.gpm_mine(g.handle, C.byref(cfg), C.byref(r)))
+    try:
+        total = C.c_uint64()
+        check(L.gpm_result_total(r, C.byref(total)))
+        npat = C.c_uint64()
+        check(L.gpm_result_num_patterns(r, C.byref(npat)))
+        pats = []
+        buf = C.create_string_buffer(512)
+        for i in range(npat.value):
+            sup, lev = C.c_uint64(), C.c_int()
+            check(L.gpm_result_pattern(r, i, buf, 512, C.byref(sup), C.byref(lev)))
+            pats.append((lev.value, buf.value.decode(), sup.value))
+        st = _L.Stats()
+        check(L.gpm_result_stats(r, C.byref(st)))
+        nl = st.n_levels
+        stats = dict(level_sizes=list(st.level_sizes[:nl]), candidates=list(st.candidates[:nl]),
+                     survivors=list(st.survivors[:nl]), n_explored=st.n_explored, b_alg=st.b_alg,
+                     ms_total=st.ms_total, ms_extend=st.ms_extend, ms_dominant=st.ms_dominant,
+                     b_dominant=st.b_dominant, launches=st.launches, chunks=st.chunks,
+                     dominant=st.dominant.decode())
+    finally:
+        L.gpm_result_free(r)
+    if app == "fsm":
+        pats.sort(key=lambda x: (x[0], -x[2], x[1]))
+    return MineResult(app, k, total.value, pats, stats)
+
+
+def triangle_count(g: Graph, **kw) -> int:
+    """SPEC.md:414-422 / PAPER.md:982-984."""
+    return mine(g, "tc", 3, **kw).total
+
+
+def clique_find(g: Graph, k: int, **kw) -> int:
+    """SPEC.md:423-431 / Listing 3."""
+    return mine(g, "cf", k, **kw).total
+
+
+def motif_count(g: Graph, k: int, **kw) -> Dict[str, int]:
+    """SPEC.md:432-440 / Listings 4, 6."""
+    return mine(g, "mc", k, **kw).pattern_map()
+
+
+def fsm(g: Graph, k: int, sigma: int, **kw) -> List[Tuple[int, str, int]]:
+    """SPEC.md:441-449 / Listing 5: frequent patterns with up to k-1 edges."""
+    return mine(g, "fsm", k, sigma, **kw).patterns

@@ -1,0 +1,191 @@
+// api.cu — C ABI: mine(), results, stats, errors (include/gpm.h).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+
+#include "engine.hpp"
+#include "pattern.cuh"
+
+namespace gpm {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+// SPEC.md:252 stable text "k=<n>;L=<l0,...>;E=(i,j)(i,j)..."
+std::string canon_text(u64 key, int nv_hint, int label_bits, const std::vector<u32>* label_values) {
+  int nv = 0;
+  u32 lab[8] = {0};
+  u32 mask = 0;
+  pat::decode(key, label_bits, &nv, lab, &mask);
+  (void)nv_hint;
+  std::string s = "k=" + std::to_string(nv) + ";L=";
+  for (int i = 0; i < nv; ++i) {
+    if (i) s += ",";
+    u32 v = lab[i];
+    if (label_values && !label_values->empty()) v = (*label_values)[lab[i]];
+    s += std::to_string(v);
+  }
+  s += ";E=";
+  for (int a = 0; a < nv; ++a)
+    for (int b = a + 1; b < nv; ++b)
+      if (mask >> pat::pair_index(a, b, nv) & 1u) s += "(" + std::to_string(a) + "," + std::to_string(b) + ")";
+  return s;
+}
+
+// Sum a host u64 vector across ranks through the exchange hook.
+void exchange_sum_host(const gpm_config& cfg, std::vector<u64>& v, cudaStream_t s) {
+  if (cfg.world <= 1 || !cfg.exchange || v.empty()) return;
+  DBuf<u64> d(v.size(), s);
+  GPM_CUDA(cudaMemcpyAsync(d.get(), v.data(), sizeof(u64) * v.size(), cudaMemcpyHostToDevice, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  if (cfg.exchange(cfg.exchange_ctx, d.get(), v.size(), 8, 0, s) != 0) throw Error(GPM_ENCCL, "exchange(sum) failed");
+  GPM_CUDA(cudaMemcpyAsync(v.data(), d.get(), sizeof(u64) * v.size(), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+}
+
+void exchange_device(const gpm_config& cfg, void* dev, u64 count, int elem_bytes, int op, cudaStream_t s) {
+  if (cfg.world <= 1 || !cfg.exchange || count == 0) return;
+  GPM_CUDA(cudaStreamSynchronize(s));
+  if (cfg.exchange(cfg.exchange_ctx, dev, count, elem_bytes, op, s) != 0) throw Error(GPM_ENCCL, "exchange failed");
+}
+
+}  // namespace gpm
+
+using namespace gpm;
+
+extern "C" {
+
+const char* gpm_last_error(void) { return g_last_error.c_str(); }
+
+const char* gpm_version(void) { return "gpm-b200 0.1 (sm_100a)"; }
+
+void gpm_config_default(gpm_config* cfg) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->app = GPM_APP_TC;
+  cfg->k = 3;
+  cfg->world = 1;
+}
+
+int gpm_mine(const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
+  if (!g || !cfg || !out) {
+    set_last_error("gpm_mine: null argument");
+    return GPM_EINVAL;
+  }
+  *out = nullptr;
+  return guarded([&] {
+    if (cfg->app < GPM_APP_TC || cfg->app > GPM_APP_FSM) throw Error(GPM_EINVAL, "unknown app");
+    if (cfg->world < 0 || (cfg->world > 1 && (cfg->rank < 0 || cfg->rank >= cfg->world)))
+      throw Error(GPM_EINVAL, "bad rank/world");
+    GPM_CUDA(cudaSetDevice(g->device));
+    cudaStream_t s = cfg->stream ? (cudaStream_t)cfg->stream : g->stream;
+    if (cfg->stream) GPM_CUDA(cudaStreamSynchronize(g->stream));  // graph upload ordered before the caller's stream
+    auto res = std::make_unique<gpm_result>();
+    res->app = cfg->app;
+    res->k = cfg->k;
+    Stats st;
+    Timeline tl(s);
+    cudaEvent_t e0, e1;
+    GPM_CUDA(cudaEventCreate(&e0));
+    GPM_CUDA(cudaEventCreate(&e1));
+    GPM_CUDA(cudaEventRecord(e0, s));
+    try {
+      if (cfg->app == GPM_APP_FSM) mine_fsm(*g, *cfg, s, *res, st, tl);
+      else mine_vertex(*g, *cfg, s, *res, st, tl);
+    } catch (...) {
+      cudaStreamSynchronize(s);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      throw;
+    }
+    GPM_CUDA(cudaEventRecord(e1, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+    float ms = 0;
+    GPM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+
+    gpm_stats& S = res->stats;
+    std::memset(&S, 0, sizeof S);
+    S.n_levels = (int)std::min<size_t>(16, st.level_sizes.size());
+    for (int i = 0; i < S.n_levels; ++i) {
+      S.level_sizes[i] = st.level_sizes[i];
+      S.candidates[i] = i < (int)st.candidates.size() ? st.candidates[i] : 0;
+      S.survivors[i] = i < (int)st.survivors.size() ? st.survivors[i] : 0;
+    }
+    for (auto x : st.level_sizes) S.n_explored += x;
+    S.b_alg = st.balg;
+    S.ms_total = ms;
+    S.launches = tl.launches;
+    S.chunks = st.chunks;
+    std::map<std::string, std::pair<double, double>> per;  // name -> (ms, bytes)
+    for (auto& r : tl.recs) {
+      float t = 0;
+      GPM_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      per[r.name].first += t;
+      per[r.name].second += r.bytes;
+      S.ms_extend += t;
+    }
+    double best = -1;
+    for (auto& [name, v] : per)
+      if (v.first > best) {
+        best = v.first;
+        S.ms_dominant = v.first;
+        S.b_dominant = v.second;
+        std::snprintf(S.dominant, sizeof S.dominant, "%s", name.c_str());
+      }
+    *out = res.release();
+  });
+}
+
+int gpm_result_total(const gpm_result* r, uint64_t* total) {
+  if (!r || !total) {
+    set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  *total = r->total;
+  return GPM_OK;
+}
+
+int gpm_result_num_patterns(const gpm_result* r, uint64_t* n) {
+  if (!r || !n) {
+    set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  *n = r->patterns.size();
+  return GPM_OK;
+}
+
+int gpm_result_pattern(const gpm_result* r, uint64_t i, char* text, size_t cap, uint64_t* support, int* level) {
+  if (!r || i >= r->patterns.size()) {
+    set_last_error("pattern index out of range");
+    return GPM_EINVAL;
+  }
+  const auto& p = r->patterns[i];
+  if (text && cap) {
+    size_t c = std::min(cap - 1, p.text.size());
+    std::memcpy(text, p.text.data(), c);
+    text[c] = 0;
+  }
+  if (support) *support = p.support;
+  if (level) *level = p.level;
+  return GPM_OK;
+}
+
+int gpm_result_stats(const gpm_result* r, gpm_stats* out) {
+  if (!r || !out) {
+    set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  *out = r->stats;
+  return GPM_OK;
+}
+
+void gpm_result_free(gpm_result* r) { delete r; }
+
+}  // extern "C"

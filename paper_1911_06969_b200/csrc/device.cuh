@@ -1,0 +1,165 @@
+// device.cuh — device-side graph view, connectivity probes, memory + launch
+// helpers shared by the engine translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+
+namespace gpm {
+
+#define GPM_CUDA(x)                                                                                   \
+  do {                                                                                                \
+    cudaError_t e_ = (x);                                                                             \
+    if (e_ != cudaSuccess) {                                                                          \
+      if (e_ == cudaErrorMemoryAllocation) throw ::gpm::Error(GPM_ENOMEM, std::string(#x) + ": out of device memory"); \
+      throw ::gpm::Error(GPM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));                 \
+    }                                                                                                 \
+  } while (0)
+
+constexpr int kMaxLevels = 10;   // k <= 9 vertices (CF) -> 8 stored levels
+constexpr int kWarp = 32;
+
+// Immutable CSR in HBM (graph.hpp:22-115): u64 offsets, u32 ascending lists,
+// optional u32 dense label ranks.
+struct DevGraph {
+  const u64* __restrict__ off;
+  const u32* __restrict__ col;
+  const u32* __restrict__ lab;
+  u32 n;
+  u64 m;
+  int oriented;
+};
+
+__device__ __forceinline__ u32 ldg(const u32* p) { return __ldg(p); }
+__device__ __forceinline__ u64 ldg(const u64* p) { return __ldg(reinterpret_cast<const unsigned long long*>(p)); }
+
+// Binary-search membership over a sorted list (graph.hpp:101-104, PAPER.md
+// §5.4 "binary search for the connectivity check").
+__device__ __forceinline__ bool contains_sorted(const u32* __restrict__ a, u32 len, u32 key) {
+  const u32* base = a;
+  u32 n = len;
+  while (n > 1) {
+    u32 half = n >> 1;
+    base = (ldg(base + half - 1) < key) ? base + half : base;
+    n -= half;
+  }
+  return n == 1 && ldg(base) == key;
+}
+
+// Directed probe x -> u (on a DAG tests the oriented edge).
+__device__ __forceinline__ bool has_edge(const DevGraph& g, u32 x, u32 u) {
+  u64 b = ldg(g.off + x), e = ldg(g.off + x + 1);
+  return contains_sorted(g.col + b, (u32)(e - b), u);
+}
+
+// Undirected probe: search the shorter of the two lists (same answer by
+// symmetry), bounding the hub cost of power-law graphs.
+__device__ __forceinline__ bool has_edge_sym(const DevGraph& g, u32 x, u32 u) {
+  u64 bx = ldg(g.off + x), ex = ldg(g.off + x + 1);
+  u64 bu = ldg(g.off + u), eu = ldg(g.off + u + 1);
+  if (ex - bx <= eu - bu) return contains_sorted(g.col + bx, (u32)(ex - bx), u);
+  return contains_sorted(g.col + bu, (u32)(eu - bu), x);
+}
+
+// Last index i in [lo, hi) with W[i] <= key (W non-decreasing).
+__device__ __forceinline__ u64 upper_bound_prev(const u64* __restrict__ W, u64 lo, u64 hi, u64 key) {
+  // find first i in [lo,hi) with W[i] > key, return i-1
+  u64 l = lo, h = hi;
+  while (l < h) {
+    u64 mid = (l + h) >> 1;
+    if (ldg(W + mid) <= key) l = mid + 1;
+    else h = mid;
+  }
+  return l - 1;
+}
+
+__device__ __forceinline__ u32 lanemask_lt() {
+  u32 r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// Stream-ordered device buffer (cudaMallocAsync pool; released memory stays
+// cached in the pool across gpm_mine calls).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = 0;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) {
+      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        n = 0;
+        throw Error(GPM_ENOMEM, "device allocation of " + std::to_string(count * sizeof(T)) + " bytes failed");
+      }
+    }
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  T* get() const { return p; }
+};
+
+// Kernel timing + launch accounting for gpm_stats (CUDA events on the
+// engine's stream, resolved once at the end of gpm_mine).
+struct Timeline {
+  struct Rec {
+    std::string name;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  cudaStream_t s;
+  std::vector<Rec> recs;
+  u64 launches = 0;
+  explicit Timeline(cudaStream_t st) : s(st) {}
+  ~Timeline() {
+    for (auto& r : recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+  }
+  size_t begin(const std::string& name, double bytes) {
+    Rec r{name, nullptr, nullptr, bytes};
+    GPM_CUDA(cudaEventCreate(&r.a));
+    GPM_CUDA(cudaEventCreate(&r.b));
+    GPM_CUDA(cudaEventRecord(r.a, s));
+    recs.push_back(r);
+    return recs.size() - 1;
+  }
+  void end(size_t i) { GPM_CUDA(cudaEventRecord(recs[i].b, s)); }
+};
+
+inline int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+}  // namespace gpm

@@ -1,0 +1,77 @@
+// engine.hpp — internal (C++) engine interfaces behind the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "device.cuh"
+
+struct gpm_graph {
+  int device = 0;
+  gpm::u32 n = 0;
+  gpm::u64 m = 0;
+  bool oriented = false;
+  bool labeled = false;
+  gpm::u64* d_off = nullptr;
+  gpm::u32* d_col = nullptr;
+  gpm::u32* d_lab = nullptr;            // dense label ranks (order-preserving)
+  std::vector<gpm::u32> label_values;   // rank -> original label value
+  int label_bits = 0;
+  gpm::u32 max_deg = 0;
+  cudaStream_t stream = nullptr;        // library-owned stream
+  ~gpm_graph();
+  gpm::DevGraph view() const { return gpm::DevGraph{d_off, d_col, d_lab, n, m, oriented ? 1 : 0}; }
+};
+
+struct gpm_result {
+  int app = 0;
+  int k = 0;
+  gpm::u64 total = 0;
+  struct Pattern {
+    std::string text;
+    gpm::u64 support;
+    int level;
+  };
+  std::vector<Pattern> patterns;
+  gpm_stats stats{};
+};
+
+namespace gpm {
+
+struct Stats {
+  std::vector<u64> level_sizes, candidates, survivors;
+  double balg = 0;
+  u64 chunks = 0;
+  void ensure(size_t L) {
+    if (level_sizes.size() < L) level_sizes.resize(L, 0);
+    if (candidates.size() < L) candidates.resize(L, 0);
+    if (survivors.size() < L) survivors.resize(L, 0);
+  }
+};
+
+// Level-1 build on the device (embedding_list.hpp:178-192): DAG -> every
+// edge; undirected -> (u,v) with u<v.  idx[i] = first endpoint, vid[i] = second.
+void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl);
+
+// Degree-weighted static split of [0, n1) root units into `world` parts
+// (SURVEY §8e); weight = candidate count of each level-1 entry.
+void root_split(const gpm_graph& g, const u32* idx, const u32* vid, u64 n1, int app, int rank, int world, u64& lo,
+                u64& hi, cudaStream_t s, Timeline& tl);
+
+// Device orientation (graph.hpp:121-132).
+void orient_on_device(const gpm_graph& g, gpm_graph& out);
+
+void mine_vertex(const gpm_graph& g, const gpm_config& cfg, cudaStream_t s, gpm_result& res, Stats& st, Timeline& tl);
+void mine_fsm(const gpm_graph& g, const gpm_config& cfg, cudaStream_t s, gpm_result& res, Stats& st, Timeline& tl);
+
+// Collective hooks (multi-GPU, one process per GPU): sum a host vector or
+// exchange a device buffer in place through gpm_config.exchange.
+void exchange_sum_host(const gpm_config& cfg, std::vector<u64>& v, cudaStream_t s);
+void exchange_device(const gpm_config& cfg, void* dev, u64 count, int elem_bytes, int op, cudaStream_t s);
+
+// Canonical pattern text from a packed canonical key (pattern.cuh).
+std::string canon_text(u64 key, int nv, int label_bits, const std::vector<u32>* label_values);
+
+}  // namespace gpm

@@ -1,0 +1,412 @@
+// graph.cu — device CSR lifecycle: upload + validation (graph.hpp:29-55),
+// degree-ordered orientation (graph.hpp:121-132), level-1 init
+// (embedding_list.hpp:178-192), batched is_connected (graph.hpp:93-104) and
+// the degree-weighted root split.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+
+#include "engine.hpp"
+
+namespace gpm {
+namespace {
+
+// Warp per vertex: validates strictly ascending lists, ids < n, no loops.
+__global__ void validate_kernel(const u64* __restrict__ off, const u32* __restrict__ col, u32 n, u64 m,
+                                int* __restrict__ bad, u32* __restrict__ maxdeg) {
+  const int lane = threadIdx.x & 31;
+  const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+  const u64 nwarps = (gridDim.x * (u64)blockDim.x) >> 5;
+  for (u64 v = warp; v < n; v += nwarps) {
+    u64 b = off[v], e = off[v + 1];
+    if (e < b || e > m) {
+      if (lane == 0) atomicOr(bad, 1);
+      continue;
+    }
+    if (lane == 0) atomicMax(maxdeg, (u32)(e - b));
+    for (u64 i = b + lane; i < e; i += 32) {
+      u32 x = col[i];
+      bool ok = x < n && x != v && (i == b || col[i - 1] < x);
+      if (!ok) atomicOr(bad, 2);
+    }
+  }
+}
+
+// (deg, id) total order of graph.hpp:124-126
+__device__ __forceinline__ bool precedes(const u64* off, u32 a, u32 b) {
+  u64 da = off[a + 1] - off[a], db = off[b + 1] - off[b];
+  return da != db ? da < db : a < b;
+}
+
+template <bool WRITE>
+__global__ void orient_kernel(const u64* __restrict__ off, const u32* __restrict__ col, u32 n,
+                              u64* __restrict__ cnt_or_off, u32* __restrict__ out_col) {
+  const int lane = threadIdx.x & 31;
+  const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+  const u64 nwarps = (gridDim.x * (u64)blockDim.x) >> 5;
+  for (u64 u = warp; u < n; u += nwarps) {
+    const u64 b = off[u], e = off[u + 1];
+    u64 w = WRITE ? cnt_or_off[u] : 0;
+    u64 c = 0;
+    for (u64 i0 = b; i0 < e; i0 += 32) {
+      u64 i = i0 + lane;
+      bool keep = false;
+      u32 v = 0;
+      if (i < e) {
+        v = col[i];
+        keep = precedes(off, (u32)u, v);
+      }
+      u32 mask = __ballot_sync(0xffffffffu, keep);
+      if (WRITE && keep) out_col[w + __popc(mask & lanemask_lt())] = v;
+      w += __popc(mask);
+      c += __popc(mask);
+    }
+    if (!WRITE && lane == 0) cnt_or_off[u] = c;
+  }
+}
+
+// level 1 of an undirected graph: per vertex, entries v > u (u<v rule).
+__global__ void l1_count_kernel(const u64* __restrict__ off, const u32* __restrict__ col, u32 n,
+                                u64* __restrict__ cnt) {
+  u64 u = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  u64 b = off[u], e = off[u + 1];
+  // first position with col > u
+  u64 lo = b, hi = e;
+  while (lo < hi) {
+    u64 mid = (lo + hi) >> 1;
+    if (col[mid] <= u) lo = mid + 1;
+    else hi = mid;
+  }
+  cnt[u] = e - lo;
+}
+
+__global__ void l1_fill_kernel(const u64* __restrict__ off, const u32* __restrict__ col, u32 n, int oriented,
+                               const u64* __restrict__ pos, u32* __restrict__ idx, u32* __restrict__ vid) {
+  const int lane = threadIdx.x & 31;
+  const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+  const u64 nwarps = (gridDim.x * (u64)blockDim.x) >> 5;
+  for (u64 u = warp; u < n; u += nwarps) {
+    u64 b = off[u], e = off[u + 1];
+    u64 w = oriented ? b : pos[u];
+    u64 start = oriented ? b : e - (pos[u + 1] - pos[u]);
+    for (u64 i = start + lane; i < e; i += 32) {
+      idx[w + (i - start)] = (u32)u;
+      vid[w + (i - start)] = col[i];
+    }
+  }
+}
+
+__global__ void is_connected_kernel(DevGraph g, const u32* __restrict__ us, const u32* __restrict__ vs, u64 q,
+                                    u8* __restrict__ out) {
+  u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  if (i >= q) return;
+  out[i] = has_edge(g, us[i], vs[i]) ? 1 : 0;
+}
+
+__global__ void root_weight_kernel(const u64* __restrict__ off, const u32* __restrict__ idx,
+                                   const u32* __restrict__ vid, u64 n1, int both, u64* __restrict__ w) {
+  u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  if (i >= n1) return;
+  u32 a = idx[i], b = vid[i];
+  u64 x = off[b + 1] - off[b];
+  if (both) x += off[a + 1] - off[a];
+  w[i] = x + 1;  // +1: every root unit costs at least its own visit
+}
+
+__global__ void lower_bound_kernel(const u64* __restrict__ pre, u64 n, const u64* __restrict__ keys, int nk,
+                                   u64* __restrict__ out) {
+  int t = threadIdx.x;
+  if (t >= nk) return;
+  u64 key = keys[t], lo = 0, hi = n;
+  while (lo < hi) {
+    u64 mid = (lo + hi) >> 1;
+    if (pre[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  out[t] = lo;
+}
+
+void exclusive_scan_u64(u64* data, u64 n, cudaStream_t s) {
+  size_t tmp = 0;
+  GPM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, data, data, n, s));
+  DBuf<u8> t(tmp, s);
+  GPM_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, data, data, n, s));
+}
+
+inline unsigned grid_for(u64 items, int per_block) {
+  u64 g = (items + per_block - 1) / per_block;
+  return (unsigned)std::max<u64>(1, std::min<u64>(g, 1u << 20));
+}
+
+}  // namespace
+
+void scan_inplace(u64* data, u64 n, cudaStream_t s) { exclusive_scan_u64(data, n, s); }
+
+void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl) {
+  if (g.oriented) {
+    count = g.m;
+    idx.alloc(std::max<u64>(1, g.m), s);
+    vid.alloc(std::max<u64>(1, g.m), s);
+    if (g.m) {
+      ++tl.launches;
+      l1_fill_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, g.n, 1, nullptr, idx.get(),
+                                                                   vid.get());
+      GPM_CUDA(cudaGetLastError());
+    }
+    return;
+  }
+  DBuf<u64> pos(g.n + 1, s);
+  GPM_CUDA(cudaMemsetAsync(pos.get(), 0, sizeof(u64) * (g.n + 1), s));
+  if (g.n) {
+    ++tl.launches;
+    l1_count_kernel<<<grid_for(g.n, 256), 256, 0, s>>>(g.d_off, g.d_col, g.n, pos.get());
+    GPM_CUDA(cudaGetLastError());
+  }
+  exclusive_scan_u64(pos.get(), g.n + 1, s);
+  GPM_CUDA(cudaMemcpyAsync(&count, pos.get() + g.n, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  idx.alloc(std::max<u64>(1, count), s);
+  vid.alloc(std::max<u64>(1, count), s);
+  if (count) {
+    ++tl.launches;
+    l1_fill_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, g.n, 0, pos.get(), idx.get(),
+                                                                 vid.get());
+    GPM_CUDA(cudaGetLastError());
+  }
+}
+
+void root_split(const gpm_graph& g, const u32* idx, const u32* vid, u64 n1, int app, int rank, int world, u64& lo,
+                u64& hi, cudaStream_t s, Timeline& tl) {
+  if (world <= 1 || n1 == 0) {
+    lo = 0;
+    hi = n1;
+    return;
+  }
+  DBuf<u64> w(n1 + 1, s);
+  GPM_CUDA(cudaMemsetAsync(w.get() + n1, 0, sizeof(u64), s));
+  ++tl.launches;
+  root_weight_kernel<<<grid_for(n1, 256), 256, 0, s>>>(g.d_off, idx, vid, n1, app == GPM_APP_MC ? 1 : 0, w.get());
+  GPM_CUDA(cudaGetLastError());
+  exclusive_scan_u64(w.get(), n1 + 1, s);
+  u64 total = 0;
+  GPM_CUDA(cudaMemcpyAsync(&total, w.get() + n1, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  u64 keys[2] = {(u64)((unsigned __int128)total * (u64)rank / (u64)world),
+                 (u64)((unsigned __int128)total * (u64)(rank + 1) / (u64)world)};
+  DBuf<u64> dk(2, s), dout(2, s);
+  GPM_CUDA(cudaMemcpyAsync(dk.get(), keys, sizeof keys, cudaMemcpyHostToDevice, s));
+  ++tl.launches;
+  lower_bound_kernel<<<1, 32, 0, s>>>(w.get(), n1 + 1, dk.get(), 2, dout.get());
+  GPM_CUDA(cudaGetLastError());
+  u64 res[2];
+  GPM_CUDA(cudaMemcpyAsync(res, dout.get(), sizeof res, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  lo = std::min(res[0], n1);
+  hi = rank == world - 1 ? n1 : std::min(res[1], n1);
+}
+
+void orient_on_device(const gpm_graph& g, gpm_graph& out) {
+  cudaStream_t s = out.stream;
+  out.n = g.n;
+  out.oriented = true;
+  out.labeled = g.labeled;
+  out.label_values = g.label_values;
+  out.label_bits = g.label_bits;
+  GPM_CUDA(cudaMalloc(&out.d_off, sizeof(u64) * (g.n + 1)));
+  GPM_CUDA(cudaMemsetAsync(out.d_off, 0, sizeof(u64) * (g.n + 1), s));
+  // the source graph lives on g.stream; order it before our stream
+  GPM_CUDA(cudaStreamSynchronize(g.stream));
+  if (g.n) {
+    orient_kernel<false><<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, g.n, out.d_off, nullptr);
+    GPM_CUDA(cudaGetLastError());
+  }
+  exclusive_scan_u64(out.d_off, g.n + 1, s);
+  u64 m = 0;
+  GPM_CUDA(cudaMemcpyAsync(&m, out.d_off + g.n, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  out.m = m;
+  GPM_CUDA(cudaMalloc(&out.d_col, sizeof(u32) * std::max<u64>(1, m)));
+  if (g.n && m) {
+    orient_kernel<true><<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, g.n, out.d_off, out.d_col);
+    GPM_CUDA(cudaGetLastError());
+  }
+  if (g.labeled) {
+    GPM_CUDA(cudaMalloc(&out.d_lab, sizeof(u32) * std::max<u32>(1, g.n)));
+    GPM_CUDA(cudaMemcpyAsync(out.d_lab, g.d_lab, sizeof(u32) * g.n, cudaMemcpyDeviceToDevice, s));
+  }
+  // max out-degree (for planner heuristics)
+  DBuf<int> bad(1, s);
+  DBuf<u32> md(1, s);
+  GPM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+  GPM_CUDA(cudaMemsetAsync(md.get(), 0, sizeof(u32), s));
+  if (g.n) {
+    validate_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(out.d_off, out.d_col, g.n, m, bad.get(), md.get());
+    GPM_CUDA(cudaGetLastError());
+  }
+  GPM_CUDA(cudaMemcpyAsync(&out.max_deg, md.get(), sizeof(u32), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace gpm
+
+// ---------------------------------------------------------------- C ABI: graph
+using namespace gpm;
+
+gpm_graph::~gpm_graph() {
+  if (d_off) cudaFree(d_off);
+  if (d_col) cudaFree(d_col);
+  if (d_lab) cudaFree(d_lab);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+extern "C" int gpm_graph_create_csr(const uint64_t* row_offsets, const uint32_t* col, const uint32_t* labels,
+                                    uint32_t n, uint64_t m, int oriented, int device, gpm_graph** out) {
+  if (!out || !row_offsets || (m && !col)) {
+    set_last_error("gpm_graph_create_csr: null argument");
+    return GPM_EINVAL;
+  }
+  *out = nullptr;
+  return guarded([&] {
+    if (row_offsets[0] != 0 || row_offsets[n] != m) throw Error(GPM_EINVAL, "row_offsets must start at 0 and end at m");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw Error(GPM_ECUDA, "no CUDA device visible");
+    }
+    if (device < 0 || device >= ndev) throw Error(GPM_EINVAL, "device index out of range");
+    GPM_CUDA(cudaSetDevice(device));
+    auto g = std::make_unique<gpm_graph>();
+    g->device = device;
+    g->n = n;
+    g->m = m;
+    g->oriented = oriented != 0;
+    GPM_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    cudaStream_t s = g->stream;
+    GPM_CUDA(cudaMalloc(&g->d_off, sizeof(u64) * (n + 1)));
+    GPM_CUDA(cudaMalloc(&g->d_col, sizeof(u32) * std::max<u64>(1, m)));
+    GPM_CUDA(cudaMemcpyAsync(g->d_off, row_offsets, sizeof(u64) * (n + 1), cudaMemcpyHostToDevice, s));
+    if (m) GPM_CUDA(cudaMemcpyAsync(g->d_col, col, sizeof(u32) * m, cudaMemcpyHostToDevice, s));
+    if (labels) {
+      // order-preserving dense label ranks (canonical order is unchanged)
+      std::vector<u32> vals(labels, labels + n);
+      std::sort(vals.begin(), vals.end());
+      vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+      g->label_values = vals;
+      int lb = 0;
+      while ((u64(1) << lb) < std::max<size_t>(1, vals.size())) ++lb;
+      g->label_bits = lb;
+      std::vector<u32> ranks(n);
+      for (u32 v = 0; v < n; ++v)
+        ranks[v] = (u32)(std::lower_bound(vals.begin(), vals.end(), labels[v]) - vals.begin());
+      g->labeled = true;
+      GPM_CUDA(cudaMalloc(&g->d_lab, sizeof(u32) * std::max<u32>(1, n)));
+      GPM_CUDA(cudaMemcpyAsync(g->d_lab, ranks.data(), sizeof(u32) * n, cudaMemcpyHostToDevice, s));
+      GPM_CUDA(cudaStreamSynchronize(s));  // ranks is a host temporary
+    }
+    DBuf<int> bad(1, s);
+    DBuf<u32> md(1, s);
+    GPM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    GPM_CUDA(cudaMemsetAsync(md.get(), 0, sizeof(u32), s));
+    if (n) {
+      validate_kernel<<<grid_for((u64)n * 32, 256), 256, 0, s>>>(g->d_off, g->d_col, n, m, bad.get(), md.get());
+      GPM_CUDA(cudaGetLastError());
+    }
+    int hb = 0;
+    GPM_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaMemcpyAsync(&g->max_deg, md.get(), sizeof(u32), cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+    if (hb & 1) throw Error(GPM_EINVAL, "row_offsets not non-decreasing / out of range");
+    if (hb & 2) throw Error(GPM_EINVAL, "neighbor list not strictly ascending, self-loop, or id out of range");
+    *out = g.release();
+  });
+}
+
+extern "C" int gpm_graph_orient_dag(const gpm_graph* g, gpm_graph** out) {
+  if (!g || !out) {
+    set_last_error("gpm_graph_orient_dag: null argument");
+    return GPM_EINVAL;
+  }
+  *out = nullptr;
+  return guarded([&] {
+    if (g->oriented) throw Error(GPM_EINVAL, "orient_dag: graph is already oriented");
+    GPM_CUDA(cudaSetDevice(g->device));
+    auto o = std::make_unique<gpm_graph>();
+    o->device = g->device;
+    GPM_CUDA(cudaStreamCreateWithFlags(&o->stream, cudaStreamNonBlocking));
+    orient_on_device(*g, *o);
+    *out = o.release();
+  });
+}
+
+extern "C" int gpm_graph_info(const gpm_graph* g, uint32_t* n, uint64_t* m, int* oriented, int* labeled) {
+  if (!g) {
+    set_last_error("null graph");
+    return GPM_EINVAL;
+  }
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  if (oriented) *oriented = g->oriented;
+  if (labeled) *labeled = g->labeled;
+  return GPM_OK;
+}
+
+extern "C" int gpm_graph_download(const gpm_graph* g, uint64_t* row_offsets, uint32_t* col) {
+  if (!g || !row_offsets || (g->m && !col)) {
+    set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  return guarded([&] {
+    GPM_CUDA(cudaSetDevice(g->device));
+    GPM_CUDA(cudaMemcpyAsync(row_offsets, g->d_off, sizeof(u64) * (g->n + 1), cudaMemcpyDeviceToHost, g->stream));
+    if (g->m) GPM_CUDA(cudaMemcpyAsync(col, g->d_col, sizeof(u32) * g->m, cudaMemcpyDeviceToHost, g->stream));
+    GPM_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
+extern "C" int gpm_graph_is_connected(const gpm_graph* g, const uint32_t* us, const uint32_t* vs, uint64_t q,
+                                      uint8_t* out) {
+  if (!g || (q && (!us || !vs || !out))) {
+    set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  return guarded([&] {
+    for (u64 i = 0; i < q; ++i)
+      if (us[i] >= g->n || vs[i] >= g->n) throw Error(GPM_EINVAL, "is_connected: vertex id out of range");
+    if (!q) return;
+    GPM_CUDA(cudaSetDevice(g->device));
+    cudaStream_t s = g->stream;
+    DBuf<u32> du(q, s), dv(q, s);
+    DBuf<u8> dr(q, s);
+    GPM_CUDA(cudaMemcpyAsync(du.get(), us, sizeof(u32) * q, cudaMemcpyHostToDevice, s));
+    GPM_CUDA(cudaMemcpyAsync(dv.get(), vs, sizeof(u32) * q, cudaMemcpyHostToDevice, s));
+    is_connected_kernel<<<grid_for(q, 256), 256, 0, s>>>(g->view(), du.get(), dv.get(), q, dr.get());
+    GPM_CUDA(cudaGetLastError());
+    GPM_CUDA(cudaMemcpyAsync(out, dr.get(), q, cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+extern "C" int gpm_level1(const gpm_graph* g, uint32_t* idx, uint32_t* vid, uint64_t cap, uint64_t* n_out) {
+  if (!g || !n_out) {
+    set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  return guarded([&] {
+    GPM_CUDA(cudaSetDevice(g->device));
+    cudaStream_t s = g->stream;
+    Timeline tl(s);
+    DBuf<u32> di, dv;
+    u64 cnt = 0;
+    build_level1(*g, di, dv, cnt, s, tl);
+    *n_out = cnt;
+    u64 c = std::min<u64>(cap, cnt);
+    if (c && idx) GPM_CUDA(cudaMemcpyAsync(idx, di.get(), sizeof(u32) * c, cudaMemcpyDeviceToHost, s));
+    if (c && vid) GPM_CUDA(cudaMemcpyAsync(vid, dv.get(), sizeof(u32) * c, cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+extern "C" void gpm_graph_free(gpm_graph* g) { delete g; }

@@ -1,0 +1,451 @@
+// host_io.cpp — host input pipeline: text loaders with the exact semantics of
+// the reference loaders (graph_io.hpp:83-116 load_edge_list, :126-211
+// load_labeled_graph), a cleaned-CSR builder, and the seeded RMAT generator of
+// SURVEY.md §8d.  Parsing is a single pass over the file image with manual
+// digit scanning (no per-line istringstream, the reference's cost centre,
+// SURVEY §3 stack 1); CSR construction is counting-based and OpenMP-parallel.
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.hpp"
+
+namespace gpm {
+namespace {
+
+inline bool is_space(unsigned char c) { return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r'; }
+
+// graph_io.hpp:48-57 parse_u64: digits only, overflow rejected.
+inline bool parse_u64(const char* b, const char* e, u64& out) {
+  if (b == e) return false;
+  u64 v = 0;
+  for (const char* p = b; p != e; ++p) {
+    unsigned c = (unsigned char)*p - '0';
+    if (c > 9) return false;
+    if (v > (UINT64_MAX - c) / 10) return false;
+    v = v * 10 + c;
+  }
+  out = v;
+  return true;
+}
+
+std::string read_file(const char* path) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) throw Error(GPM_EINVAL, std::string("cannot open ") + path);
+  std::fseek(f, 0, SEEK_END);
+  long sz = std::ftell(f);
+  std::fseek(f, 0, SEEK_SET);
+  std::string buf(sz > 0 ? (size_t)sz : 0, '\0');
+  if (sz > 0 && std::fread(buf.data(), 1, (size_t)sz, f) != (size_t)sz) {
+    std::fclose(f);
+    throw Error(GPM_EINVAL, std::string("short read on ") + path);
+  }
+  std::fclose(f);
+  return buf;
+}
+
+struct Tok {
+  const char* b;
+  const char* e;
+};
+
+// Splits one line (without '\n') into whitespace tokens (istringstream >>
+// semantics); returns the number of tokens, storing up to `cap`.
+inline int tokenize(const char* b, const char* e, Tok* t, int cap) {
+  int n = 0;
+  const char* p = b;
+  while (p < e) {
+    while (p < e && is_space((unsigned char)*p)) ++p;
+    if (p >= e) break;
+    const char* s = p;
+    while (p < e && !is_space((unsigned char)*p)) ++p;
+    if (n < cap) t[n] = {s, p};
+    ++n;
+  }
+  return n;
+}
+
+// graph_io.hpp:32-41 blank / comment.
+inline bool blank_line(const char* b, const char* e) {
+  for (const char* p = b; p < e; ++p)
+    if (!is_space((unsigned char)*p)) return false;
+  return true;
+}
+inline bool comment_line(const char* b, const char* e) {
+  const char* p = b;
+  while (p < e && (*p == ' ' || *p == '\t')) ++p;
+  return p < e && (*p == '#' || *p == '%');
+}
+
+template <class F>
+void for_each_line(const std::string& buf, F&& f) {
+  const char* p = buf.data();
+  const char* end = p + buf.size();
+  u64 lineno = 0;
+  while (p < end) {
+    const char* nl = (const char*)std::memchr(p, '\n', end - p);
+    const char* le = nl ? nl : end;
+    ++lineno;
+    const char* ce = le;
+    if (ce > p && ce[-1] == '\r') --ce;  // chomp (graph_io.hpp:27-29)
+    f(p, ce, lineno);
+    p = nl ? nl + 1 : end;
+  }
+}
+
+// Dense ids ascending over `ids` (graph_io.hpp:57-66 compact_ids).  Returns the
+// sorted unique id list; `lookup` maps id -> dense index.
+struct Compactor {
+  std::vector<u64> uniq;
+  bool dense_range = false;
+  std::vector<u32> table;  // when ids are small: id -> dense
+  std::unordered_map<u64, u32> map;
+
+  void build(std::vector<u64> ids) {
+    u64 mx = 0;
+    for (u64 x : ids) mx = std::max(mx, x);
+    if (!ids.empty() && mx < (u64(1) << 32) && mx <= 4 * ids.size() + 1024) {
+      dense_range = true;
+      std::vector<u8> seen(mx + 1, 0);
+      for (u64 x : ids) seen[x] = 1;
+      table.assign(mx + 1, UINT32_MAX);
+      u32 d = 0;
+      for (u64 x = 0; x <= mx; ++x)
+        if (seen[x]) {
+          table[x] = d++;
+          uniq.push_back(x);
+        }
+    } else {
+      std::sort(ids.begin(), ids.end());
+      ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+      uniq = std::move(ids);
+      map.reserve(uniq.size() * 2);
+      for (size_t i = 0; i < uniq.size(); ++i) map.emplace(uniq[i], (u32)i);
+    }
+    if (uniq.size() >= (u64(1) << 32)) throw Error(GPM_EINVAL, "too many vertices for 32-bit ids");
+  }
+  u32 operator()(u64 id) const { return dense_range ? table[id] : map.at(id); }
+};
+
+// Symmetrise, sort, dedup (graph_io.hpp:68-73, :119-126).
+void build_csr(u32 n, const std::vector<u32>& su, const std::vector<u32>& sv, gpm_csr* out) {
+  const u64 ne = su.size();
+  std::vector<u64> deg(n + 1, 0);
+  for (u64 i = 0; i < ne; ++i) {
+    ++deg[su[i] + 1];
+    ++deg[sv[i] + 1];
+  }
+  for (u32 v = 0; v < n; ++v) deg[v + 1] += deg[v];
+  std::vector<u32> adj(deg[n]);
+  {
+    std::vector<u64> pos(deg.begin(), deg.end() - 1);
+    for (u64 i = 0; i < ne; ++i) {
+      adj[pos[su[i]]++] = sv[i];
+      adj[pos[sv[i]]++] = su[i];
+    }
+  }
+  std::vector<u64> cnt(n + 1, 0);
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (long long vv = 0; vv < (long long)n; ++vv) {
+    u32 v = (u32)vv;
+    auto b = adj.begin() + deg[v], e = adj.begin() + deg[v + 1];
+    std::sort(b, e);
+    cnt[v + 1] = (u64)(std::unique(b, e) - b);
+  }
+  for (u32 v = 0; v < n; ++v) cnt[v + 1] += cnt[v];
+  out->n = n;
+  out->m = cnt[n];
+  out->row_offsets = (u64*)std::malloc(sizeof(u64) * (n + 1));
+  out->col = (u32*)std::malloc(sizeof(u32) * std::max<u64>(1, cnt[n]));
+  if (!out->row_offsets || !out->col) throw Error(GPM_ENOMEM, "csr allocation failed");
+  std::memcpy(out->row_offsets, cnt.data(), sizeof(u64) * (n + 1));
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (long long vv = 0; vv < (long long)n; ++vv) {
+    u32 v = (u32)vv;
+    std::memcpy(out->col + cnt[v], adj.data() + deg[v], sizeof(u32) * (cnt[v + 1] - cnt[v]));
+  }
+}
+
+void finish_ids(const Compactor& C, gpm_csr* out) {
+  out->original_ids = (u64*)std::malloc(sizeof(u64) * std::max<size_t>(1, C.uniq.size()));
+  if (!out->original_ids) throw Error(GPM_ENOMEM, "id allocation failed");
+  std::memcpy(out->original_ids, C.uniq.data(), sizeof(u64) * C.uniq.size());
+}
+
+void csr_from_pairs(const std::vector<u64>& a, const std::vector<u64>& b, gpm_csr* out) {
+  std::vector<u64> ids;
+  ids.reserve(a.size() * 2);
+  ids.insert(ids.end(), a.begin(), a.end());
+  ids.insert(ids.end(), b.begin(), b.end());
+  Compactor C;
+  C.build(std::move(ids));
+  std::vector<u32> su(a.size()), sv(a.size());
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < (long long)a.size(); ++i) {
+    su[i] = C(a[i]);
+    sv[i] = C(b[i]);
+  }
+  build_csr((u32)C.uniq.size(), su, sv, out);
+  out->labels = nullptr;
+  finish_ids(C, out);
+}
+
+// splitmix64 (counter-based, reproducible across thread counts)
+inline u64 mix64(u64 x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+}  // namespace
+
+void load_edge_list(const char* path, gpm_csr* out) {
+  std::string buf = read_file(path);
+  std::vector<u64> a, b;
+  a.reserve(buf.size() / 12);
+  b.reserve(buf.size() / 12);
+  for_each_line(buf, [&](const char* lb, const char* le, u64 lineno) {
+    if (blank_line(lb, le) || comment_line(lb, le)) return;
+    Tok t[3];
+    int nt = tokenize(lb, le, t, 3);
+    u64 u, v;
+    if (nt != 2 || !parse_u64(t[0].b, t[0].e, u) || !parse_u64(t[1].b, t[1].e, v))
+      throw Error(GPM_EPARSE, "line " + std::to_string(lineno) + ": expected two non-negative integers", lineno);
+    if (u == v) return;  // self-loop
+    a.push_back(u);
+    b.push_back(v);
+  });
+  if (a.empty()) throw Error(GPM_EINVAL, "edge list is empty after cleaning");
+  csr_from_pairs(a, b, out);
+}
+
+void load_labeled_graph(const char* path, gpm_csr* out) {
+  std::string buf = read_file(path);
+  std::vector<std::pair<u64, std::string>> decls;
+  std::vector<u64> ea, eb, eline;
+  std::unordered_map<u64, size_t> declared;
+  for_each_line(buf, [&](const char* lb, const char* le, u64 lineno) {
+    if (blank_line(lb, le) || comment_line(lb, le)) return;
+    Tok t[5];
+    int nt = tokenize(lb, le, t, 5);
+    std::string tag(t[0].b, t[0].e);
+    if (tag == "t") return;  // gSpan transaction header
+    if (tag == "v") {
+      u64 id;
+      if (nt != 3 || !parse_u64(t[1].b, t[1].e, id))
+        throw Error(GPM_EPARSE, "line " + std::to_string(lineno) + ": expected 'v <id> <label>'", lineno);
+      if (!declared.emplace(id, decls.size()).second)
+        throw Error(GPM_EPARSE,
+                    "line " + std::to_string(lineno) + ": vertex " + std::string(t[1].b, t[1].e) + " declared twice",
+                    lineno);
+      decls.emplace_back(id, std::string(t[2].b, t[2].e));
+    } else if (tag == "e") {
+      u64 u, v;
+      if ((nt != 3 && nt != 4) || !parse_u64(t[1].b, t[1].e, u) || !parse_u64(t[2].b, t[2].e, v))
+        throw Error(GPM_EPARSE, "line " + std::to_string(lineno) + ": expected 'e <u> <v> [label]'", lineno);
+      if (u == v) return;
+      ea.push_back(u);
+      eb.push_back(v);
+      eline.push_back(lineno);
+    } else {
+      throw Error(GPM_EPARSE, "line " + std::to_string(lineno) + ": unknown line tag '" + tag + "'", lineno);
+    }
+  });
+  for (size_t i = 0; i < ea.size(); ++i)
+    for (u64 id : {ea[i], eb[i]})
+      if (!declared.count(id))
+        throw Error(GPM_EPARSE,
+                    "line " + std::to_string(eline[i]) + ": edge references undeclared vertex " + std::to_string(id),
+                    eline[i]);
+  if (ea.empty()) throw Error(GPM_EINVAL, "labeled graph has no edges after cleaning");
+
+  std::vector<u64> ids;
+  ids.reserve(decls.size());
+  for (auto& d : decls) ids.push_back(d.first);
+  Compactor C;
+  C.build(std::move(ids));
+  // numeric labels keep their value; other tokens interned above them,
+  // first-appearance order (graph_io.hpp:168-190)
+  u64 max_numeric = 0;
+  bool any_numeric = false;
+  for (auto& d : decls) {
+    u64 val;
+    if (parse_u64(d.second.data(), d.second.data() + d.second.size(), val)) {
+      if (val > 0xFFFFFFFFull) throw Error(GPM_EINVAL, "vertex label too large: " + d.second);
+      max_numeric = std::max(max_numeric, val);
+      any_numeric = true;
+    }
+  }
+  std::unordered_map<std::string, u32> interned;
+  u64 next_id = any_numeric ? max_numeric + 1 : 0;
+  const u32 n = (u32)C.uniq.size();
+  std::vector<u32> labels(n, 0);
+  for (auto& d : decls) {
+    u64 val;
+    u32 lab;
+    if (parse_u64(d.second.data(), d.second.data() + d.second.size(), val)) {
+      lab = (u32)val;
+    } else {
+      auto it = interned.find(d.second);
+      if (it == interned.end()) {
+        if (next_id > 0xFFFFFFFFull) throw Error(GPM_EINVAL, "too many distinct labels");
+        it = interned.emplace(d.second, (u32)next_id++).first;
+      }
+      lab = it->second;
+    }
+    labels[C(d.first)] = lab;
+  }
+  std::vector<u32> su(ea.size()), sv(ea.size());
+  for (size_t i = 0; i < ea.size(); ++i) {
+    su[i] = C(ea[i]);
+    sv[i] = C(eb[i]);
+  }
+  build_csr(n, su, sv, out);
+  out->labels = (u32*)std::malloc(sizeof(u32) * std::max<u32>(1, n));
+  if (!out->labels) throw Error(GPM_ENOMEM, "label allocation failed");
+  std::memcpy(out->labels, labels.data(), sizeof(u32) * n);
+  finish_ids(C, out);
+}
+
+void csr_from_edges(const u64* src, const u64* dst, u64 ne, gpm_csr* out) {
+  std::vector<u64> a, b;
+  a.reserve(ne);
+  b.reserve(ne);
+  for (u64 i = 0; i < ne; ++i) {
+    if (src[i] == dst[i]) continue;
+    a.push_back(src[i]);
+    b.push_back(dst[i]);
+  }
+  if (a.empty()) throw Error(GPM_EINVAL, "edge list is empty after cleaning");
+  csr_from_pairs(a, b, out);
+}
+
+// SURVEY.md §8d RMAT: for each edge and each bit, pick a quadrant with
+// probabilities (a, b, c, 1-a-b-c); then a seeded permutation of [0, 2^scale)
+// on both endpoints; then load_edge_list cleaning (ids compacted).
+void generate_rmat(int scale, double ef, double a, double b, double c, u64 seed, u32 n_labels, u64 label_seed,
+                   gpm_csr* out) {
+  if (scale < 1 || scale > 31) throw Error(GPM_EINVAL, "rmat scale must be in [1,31]");
+  if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0)) throw Error(GPM_EINVAL, "bad rmat probabilities");
+  const u64 N = u64(1) << scale;
+  const u64 m0 = (u64)std::llround(ef * (double)N);
+  std::vector<u64> perm(N);
+  std::iota(perm.begin(), perm.end(), 0);
+  u64 st = mix64(seed ^ 0x5EEDC0FFEEull);
+  for (u64 i = N - 1; i > 0; --i) {
+    st = mix64(st);
+    u64 j = st % (i + 1);
+    std::swap(perm[i], perm[j]);
+  }
+  const double ab = a + b, abc = a + b + c;
+  std::vector<u64> su(m0), sv(m0);
+#pragma omp parallel for schedule(static)
+  for (long long ii = 0; ii < (long long)m0; ++ii) {
+    u64 x = mix64(seed ^ mix64((u64)ii + 1));
+    u64 u = 0, v = 0;
+    for (int bit = 0; bit < scale; ++bit) {
+      x = mix64(x);
+      double r = (double)(x >> 11) * (1.0 / 9007199254740992.0);
+      u64 bu, bv;
+      if (r < a) { bu = 0; bv = 0; }
+      else if (r < ab) { bu = 0; bv = 1; }
+      else if (r < abc) { bu = 1; bv = 0; }
+      else { bu = 1; bv = 1; }
+      u = (u << 1) | bu;
+      v = (v << 1) | bv;
+    }
+    su[ii] = perm[u];
+    sv[ii] = perm[v];
+  }
+  // drop self-loops (load_edge_list semantics) then compact + clean
+  std::vector<u64> fa, fb;
+  fa.reserve(m0);
+  fb.reserve(m0);
+  for (u64 i = 0; i < m0; ++i)
+    if (su[i] != sv[i]) {
+      fa.push_back(su[i]);
+      fb.push_back(sv[i]);
+    }
+  su.clear();
+  su.shrink_to_fit();
+  sv.clear();
+  sv.shrink_to_fit();
+  if (fa.empty()) throw Error(GPM_EINVAL, "rmat produced no edges");
+  csr_from_pairs(fa, fb, out);
+  if (n_labels > 0) {
+    out->labels = (u32*)std::malloc(sizeof(u32) * std::max<u32>(1, out->n));
+    if (!out->labels) throw Error(GPM_ENOMEM, "label allocation failed");
+    for (u32 v = 0; v < out->n; ++v) out->labels[v] = (u32)(mix64(label_seed ^ mix64((u64)v + 0x1234567ull)) % n_labels);
+  }
+}
+
+}  // namespace gpm
+
+extern "C" {
+
+static void zero_csr(gpm_csr* out) { std::memset(out, 0, sizeof(*out)); }
+
+int gpm_load_edge_list(const char* path, gpm_csr* out, uint64_t* err_line) {
+  if (!path || !out) {
+    gpm::set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  zero_csr(out);
+  int rc = gpm::guarded([&] { gpm::load_edge_list(path, out); }, err_line);
+  if (rc != GPM_OK) gpm_csr_free(out);
+  return rc;
+}
+
+int gpm_load_labeled_graph(const char* path, gpm_csr* out, uint64_t* err_line) {
+  if (!path || !out) {
+    gpm::set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  zero_csr(out);
+  int rc = gpm::guarded([&] { gpm::load_labeled_graph(path, out); }, err_line);
+  if (rc != GPM_OK) gpm_csr_free(out);
+  return rc;
+}
+
+int gpm_csr_from_edges(const uint64_t* src, const uint64_t* dst, uint64_t n_edges, gpm_csr* out) {
+  if (!out || (n_edges && (!src || !dst))) {
+    gpm::set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  zero_csr(out);
+  int rc = gpm::guarded([&] { gpm::csr_from_edges(src, dst, n_edges, out); });
+  if (rc != GPM_OK) gpm_csr_free(out);
+  return rc;
+}
+
+int gpm_generate_rmat(int scale, double edge_factor, double a, double b, double c, uint64_t seed,
+                      uint32_t n_labels, uint64_t label_seed, gpm_csr* out) {
+  if (!out) {
+    gpm::set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  zero_csr(out);
+  int rc = gpm::guarded([&] { gpm::generate_rmat(scale, edge_factor, a, b, c, seed, n_labels, label_seed, out); });
+  if (rc != GPM_OK) gpm_csr_free(out);
+  return rc;
+}
+
+void gpm_csr_free(gpm_csr* csr) {
+  if (!csr) return;
+  std::free(csr->row_offsets);
+  std::free(csr->col);
+  std::free(csr->labels);
+  std::free(csr->original_ids);
+  std::memset(csr, 0, sizeof(*csr));
+}
+
+}  // extern "C"

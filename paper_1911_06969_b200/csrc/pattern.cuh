@@ -1,0 +1,117 @@
+// pattern.cuh — packed quick/canonical pattern codes, shared by the vertex
+// and edge engines (__host__ __device__).
+//
+// a pattern is (position labels, position edge set); the
+// canonical form is the lexicographic minimum of (labels, sorted edge list)
+// over all permutations, the first minimiser in next_permutation order giving
+// the PositionMap.  We pack a pattern into one u64 whose INTEGER order equals
+// that lexicographic order:
+//
+//   code = nv << 61 | labels << NP | E
+//   labels = L[0] << LB*(nv-1) | ... | L[nv-1]        (L[0] most significant)
+//   E      = ~M & (2^NP - 1),  M bit (NP-1-p) set iff pair p is an edge,
+//            pairs p in lexicographic order (0,1),(0,2),..,(nv-2,nv-1)
+//
+// For two sorted edge lists of equal length, the lexicographically smaller
+// list has the LARGER M (its first differing pair is a smaller pair, i.e. a
+// more significant bit), hence the smaller E.  So min(code) over permutations
+// == the SPEC's lexicographic minimum, and ties (automorphisms) keep the
+// first permutation.  The CPU oracle implements the literal vector compare;
+// tests hold the two to each other.
+#pragma once
+#include <cstdint>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#define __forceinline__ inline
+#endif
+
+namespace gpm {
+namespace pat {
+
+__host__ __device__ __forceinline__ int npairs(int nv) { return nv * (nv - 1) / 2; }
+
+__host__ __device__ __forceinline__ int pair_index(int i, int j, int nv) {
+  // i < j
+  return i * nv - i * (i + 1) / 2 + (j - i - 1);
+}
+
+// mask: bit p set iff pair p is an edge (natural bit order).
+__host__ __device__ __forceinline__ uint64_t make_code(int nv, const uint32_t* lab, uint32_t mask, int LB) {
+  const int NP = npairs(nv);
+  uint64_t lab_packed = 0;
+  for (int i = 0; i < nv; ++i) lab_packed = (lab_packed << LB) | (uint64_t)lab[i];
+  uint64_t M = 0;
+  for (int p = 0; p < NP; ++p)
+    if (mask >> p & 1u) M |= (uint64_t)1 << (NP - 1 - p);
+  const uint64_t E = (~M) & (((uint64_t)1 << NP) - 1);
+  return ((uint64_t)nv << 61) | (lab_packed << NP) | E;
+}
+
+__host__ __device__ __forceinline__ bool next_perm(uint8_t* a, int n) {
+  int i = n - 2;
+  while (i >= 0 && a[i] >= a[i + 1]) --i;
+  if (i < 0) return false;
+  int j = n - 1;
+  while (a[j] <= a[i]) --j;
+  uint8_t t = a[i];
+  a[i] = a[j];
+  a[j] = t;
+  for (int l = i + 1, r = n - 1; l < r; ++l, --r) {
+    t = a[l];
+    a[l] = a[r];
+    a[r] = t;
+  }
+  return true;
+}
+
+// canonicalize: returns canonical code; perm[i] = canonical
+// position of quick position i.
+__host__ __device__ inline uint64_t canonicalize(int nv, const uint32_t* lab, uint32_t mask, int LB, uint8_t* perm_out) {
+  uint8_t p[8];
+  for (int i = 0; i < nv; ++i) p[i] = (uint8_t)i;
+  uint64_t best = ~(uint64_t)0;
+  uint32_t pl[8];
+  do {
+    for (int i = 0; i < nv; ++i) pl[p[i]] = lab[i];
+    uint32_t pm = 0;
+    for (int a = 0; a < nv; ++a)
+      for (int b = a + 1; b < nv; ++b)
+        if (mask >> pair_index(a, b, nv) & 1u) {
+          int x = p[a], y = p[b];
+          if (x > y) { int t = x; x = y; y = t; }
+          pm |= 1u << pair_index(x, y, nv);
+        }
+    uint64_t c = make_code(nv, pl, pm, LB);
+    if (c < best) {
+      best = c;
+      if (perm_out)
+        for (int i = 0; i < nv; ++i) perm_out[i] = p[i];
+    }
+  } while (next_perm(p, nv));
+  return best;
+}
+
+__host__ __device__ __forceinline__ int code_nv(uint64_t code) { return (int)(code >> 61); }
+
+// Decode labels and natural-order edge mask from a code.
+__host__ __device__ inline void decode(uint64_t code, int LB, int* nv_out, uint32_t* lab, uint32_t* mask) {
+  const int nv = code_nv(code);
+  const int NP = npairs(nv);
+  const uint64_t E = code & (((uint64_t)1 << NP) - 1);
+  const uint64_t M = (~E) & (((uint64_t)1 << NP) - 1);
+  uint32_t m = 0;
+  for (int p = 0; p < NP; ++p)
+    if (M >> (NP - 1 - p) & 1u) m |= 1u << p;
+  uint64_t lp = (code & (((uint64_t)1 << 61) - 1)) >> NP;
+  for (int i = nv - 1; i >= 0; --i) {
+    lab[i] = LB ? (uint32_t)(lp & ((((uint64_t)1) << LB) - 1)) : 0u;
+    lp = LB ? (lp >> LB) : 0;
+  }
+  *nv_out = nv;
+  *mask = m;
+}
+
+}  // namespace pat
+}  // namespace gpm

@@ -1,0 +1,138 @@
+"""CPU tests of the product's host side: the C ABI library loads and exports
+every symbol in include/gpm.h, the loaders match the reference's own loaders
+(oracle/_ref), the RMAT generator is deterministic, and device calls fail
+loudly (no CPU fallback) where no GPU exists."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import bruteforce as BF
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_header_symbols():
+    import ctypes
+    from paper_1911_06969_b200 import _lib
+    hdr = open(os.path.join(ROOT, "include", "gpm.h")).read()
+    declared = set(re.findall(r"\b(gpm_[a-z0-9_]+)\s*\(", hdr)) - {"gpm_exchange_fn"}
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(L, name), f"libgpm.so does not export {name}"
+    assert declared <= set(_lib.EXPORTS) | {"gpm_exchange_fn"}
+
+
+def test_version_and_error_model():
+    import paper_1911_06969_b200 as P
+    assert b"sm_100a" in P.lib().gpm_version()
+
+
+def _write(tmp_path, name, text):
+    p = tmp_path / name
+    p.write_text(text)
+    return str(p)
+
+
+ref_only = pytest.mark.skipif(not __import__("pyoracle").ref_available(), reason="oracle/_ref not built")
+
+
+@ref_only
+@pytest.mark.parametrize("seed", range(5))
+def test_edge_list_loader_matches_reference(oracle, tmp_path, seed):
+    import paper_1911_06969_b200 as P
+    rng = np.random.default_rng(seed)
+    m = 400
+    ids = rng.choice(10**12, 120, replace=False) if seed % 2 else rng.integers(0, 150, 120)
+    u = ids[rng.integers(0, len(ids), m)]
+    v = ids[rng.integers(0, len(ids), m)]
+    lines = ["# header", "% other comment", ""]
+    for a, b in zip(u, v):
+        lines.append(f"{a}\t{b}" if rng.random() < 0.3 else f"  {a} {b} ")
+    text = "\r\n".join(lines) + "\n" if seed == 3 else "\n".join(lines)
+    path = _write(tmp_path, "g.el", text)
+    mine = P.load_edge_list(path)
+    ref = oracle.ref_load(path)
+    assert np.array_equal(mine.off, ref.off)
+    assert np.array_equal(mine.col, ref.col)
+    assert np.array_equal(mine.original_ids, ref.orig)
+
+
+@ref_only
+def test_labeled_loader_matches_reference(oracle, tmp_path):
+    import paper_1911_06969_b200 as P
+    text = "t # 0\nv 5 alpha\nv 1 7\nv 9 beta\nv 3 alpha\ne 5 1\ne 1 9 2\ne 9 9\ne 3 5\n"
+    path = _write(tmp_path, "g.lg", text)
+    mine = P.load_labeled_graph(path)
+    ref = oracle.ref_load(path, labeled=True)
+    assert np.array_equal(mine.off, ref.off) and np.array_equal(mine.col, ref.col)
+    assert np.array_equal(mine.labels, ref.labels)
+    assert np.array_equal(mine.original_ids, ref.orig)
+
+
+@ref_only
+@pytest.mark.parametrize("text,line", [("0 1\n1 x\n", 2), ("0 1\n\n1 2 3\n", 3), ("5\n", 1), ("0 -1\n", 1)])
+def test_parse_errors_match_reference(oracle, tmp_path, text, line):
+    import paper_1911_06969_b200 as P
+    path = _write(tmp_path, "bad.el", text)
+    with pytest.raises(P.ParseError) as e:
+        P.load_edge_list(path)
+    assert e.value.line == line
+    with pytest.raises(oracle.RefParseError) as r:
+        oracle.ref_load(path)
+    assert r.value.line == line
+
+
+def test_loader_spec_examples(tmp_path):
+    import paper_1911_06969_b200 as P
+    g = P.load_edge_list(_write(tmp_path, "t.el", "0 1\n1 2\n2 0\n"))
+    assert g.n == 3 and g.m == 6
+    g = P.load_edge_list(_write(tmp_path, "c.el", "0 0\n0 1\n1 0\n"))
+    assert g.n == 2 and g.m == 2
+    g = P.load_labeled_graph(_write(tmp_path, "l.lg", "v 0 1\nv 1 2\ne 0 1\n"))
+    assert list(g.labels) == [1, 2] and g.m == 2
+    with pytest.raises(P.ParseError):
+        P.load_labeled_graph(_write(tmp_path, "u.lg", "v 0 5\ne 0 1\n"))
+    with pytest.raises(P.ParseError):                                  # SPEC.md:50 declared twice
+        P.load_labeled_graph(_write(tmp_path, "d.lg", "v 0 5\nv 0 6\ne 0 0\n"))
+    with pytest.raises(P.GpmError):                                    # empty edge set
+        P.load_edge_list(_write(tmp_path, "e.el", "# nothing\n3 3\n"))
+
+
+def test_csr_from_edges_matches_python_cleaning(oracle):
+    import paper_1911_06969_b200 as P
+    E = BF.gnp(80, 0.1, 5)
+    src = np.array([a for a, b in E] + [3, 7], dtype=np.uint64)
+    dst = np.array([b for a, b in E] + [3, 2], dtype=np.uint64)
+    g = P.csr_from_edges(src, dst)
+    # compacted ids ascending; compare on the compacted id space
+    ids = np.unique(np.concatenate([src[src != dst], dst[src != dst]]))
+    remap = {int(x): i for i, x in enumerate(ids)}
+    e2 = [(remap[int(a)], remap[int(b)]) for a, b in zip(src, dst) if a != b]
+    ref = oracle.csr_from_edges(e2, len(ids))
+    assert np.array_equal(g.off, ref.off) and np.array_equal(g.col, ref.col)
+
+
+def test_rmat_deterministic_and_clean():
+    import paper_1911_06969_b200 as P
+    a = P.generate_rmat(10, 8, 0.57, 0.19, 0.19, seed=1, n_labels=32, label_seed=101)
+    b = P.generate_rmat(10, 8, 0.57, 0.19, 0.19, seed=1, n_labels=32, label_seed=101)
+    c = P.generate_rmat(10, 8, 0.57, 0.19, 0.19, seed=2)
+    assert np.array_equal(a.off, b.off) and np.array_equal(a.col, b.col) and np.array_equal(a.labels, b.labels)
+    assert not (a.m == c.m and np.array_equal(a.col, c.col))
+    assert a.labels.max() < 32
+    for v in range(a.n):
+        nb = a.col[a.off[v]:a.off[v + 1]]
+        assert (np.diff(nb.astype(np.int64)) > 0).all() and v not in nb
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    import torch
+    import paper_1911_06969_b200 as P
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    g = P.generate_rmat(6, 4, 0.57, 0.19, 0.19)
+    with pytest.raises(P.GpmError) as e:
+        P.Graph(g)
+    assert e.value.code == 4  # GPM_ECUDA: no silent CPU fallback
