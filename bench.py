@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""bench.py — embeddings explored/s for the Pangolin E-R-F hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--app cf4|tc|mc3|mc4|fsm] [--impl ours|reference]
+
+Headline workload (BASELINE.json configs[1]): 4-clique listing on the
+Patent-like synthetic RMAT (scale 22, edge factor 3.35, (a,b,c)=(.50,.20,.20),
+seed 1), degree-ordered DAG.  A step = one complete mine() of that workload.
+
+* value  = N_explored (summed over ranks) / device time per step, the DAG CSR
+           resident in HBM, L2 flushed between steps (256 MiB write).
+* e2e    = the same metric through the public C ABI from pinned HOST buffers:
+           every step uploads the undirected CSR, orients it on the device,
+           mines, and reads the result back.
+* roofline = the dominant extend kernel's algorithmic bytes (SURVEY §8d B_alg)
+           / its CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline = the C++/OpenMP oracle (oracle/liboracle.so) on this host.
+Multi-GPU (torchrun): root units split by degree weight, counts all-reduced
+over NCCL; time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (app, k, sigma, rmat args, description)
+    "cf4": ("cf", 4, 0, dict(scale=22, edge_factor=3.35, a=0.50, b=0.20, c=0.20, seed=1),
+            "4-CL on Patent-like RMAT-22 ef3.35 (.50,.20,.20) seed 1, degree-ordered DAG"),
+    "tc": ("tc", 3, 0, dict(scale=16, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1),
+           "TC on RMAT-16 ef16 (.57,.19,.19) seed 1, degree-ordered DAG"),
+    "mc3": ("mc", 3, 0, dict(scale=22, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1),
+            "3-MC on LiveJournal-sized RMAT-22 ef16 (.57,.19,.19) seed 1"),
+    "mc4": ("mc", 4, 0, dict(scale=22, edge_factor=8.6, a=0.45, b=0.15, c=0.15, seed=1),
+            "4-MC on power-law RMAT-22 ef8.6 (.45,.15,.15) seed 1"),
+    "fsm": ("fsm", 4, 300, dict(scale=17, edge_factor=11, a=0.45, b=0.15, c=0.15, seed=1, n_labels=32,
+                                 label_seed=101),
+            "3-edge FSM on Mico-like RMAT-17 ef11 (.45,.15,.15) 32 labels"),
+}
+METRIC = "embeddings explored/sec (N_explored = |L1| + accepted per extend level)"
+UNIT = "embeddings/s"
+
+
+def load_peaks():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons DURING the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def _oracle():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    return pyoracle
+
+
+def cpu_sample(hg, app, k, sigma, budget_s, threads):
+    """Chooses a bounded sample of the workload for the CPU oracle: a contiguous
+    prefix of level-1 root units grown x4 until it costs >= budget_s/4 (or is
+    the whole workload).  Returns (root_hi or None for all, description)."""
+    O = _oracle()
+    oc = O.Csr(hg.off, hg.col, hg.labels)
+    if app == "fsm":
+        return None, "full workload"
+    probe = 1 << 14
+    while True:
+        r = O.mine(oc, app, k, sigma, threads=threads, root_lo=0, root_hi=probe)
+        if r["level_sizes"][0] < probe:
+            return None, "full workload"
+        if r["ms"] / 1e3 >= budget_s / 4:
+            return probe, f"first {probe} level-1 root units (contiguous prefix)"
+        probe *= 4
+
+
+def cpu_run(hg, app, k, sigma, root_hi, threads):
+    O = _oracle()
+    oc = O.Csr(hg.off, hg.col, hg.labels)
+    return O.mine(oc, app, k, sigma, threads=threads, root_lo=0, root_hi=root_hi if root_hi else 2**64 - 1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--app", default="cf4", choices=sorted(WORKLOADS))
+    ap.add_argument("--sigma", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU oracle work for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    app, k, sigma, rmat, desc = WORKLOADS[args.app]
+    if args.sigma is not None:
+        sigma = args.sigma
+
+    import numpy as np
+    import paper_1911_06969_b200 as P
+
+    t0 = time.time()
+    hg = P.generate_rmat(rmat["scale"], rmat["edge_factor"], rmat["a"], rmat["b"], rmat["c"], rmat["seed"],
+                         rmat.get("n_labels", 0), rmat.get("label_seed", 101))
+    gen_s = time.time() - t0
+    config = {"workload": desc, "app": app, "k": k, "n": hg.n, "m_half_edges": hg.m,
+              "generator": "gpm_generate_rmat (splitmix64, seeded permutation, load_edge_list cleaning)",
+              "l2": "flushed between timed steps (256 MiB device write, outside the step events)"}
+    if app == "fsm":
+        config["min_support"] = sigma
+
+    if args.impl == "reference":
+        # reference arm: the CPU implementation of the path (oracle restatement of SPEC.md's
+        # engine; the reference's own engine exists only as spec text) on all host threads.
+        if rank != 0:
+            return
+        threads = os.cpu_count() or 1
+        times = []
+        r = None
+        sample = None
+        root_hi, sample = cpu_sample(hg, app, k, sigma, args.cpu_budget, threads)
+        for i in range(args.warmup + args.steps):
+            t = time.time()
+            r = cpu_run(hg, app, k, sigma, root_hi, threads)
+            if i >= args.warmup:
+                times.append(time.time() - t)
+        ms = 1e3 * sum(times) / len(times)
+        v = r["n_explored"] / (ms / 1e3)
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": config,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample + "; oracle/liboracle.so (C++/OpenMP restatement of SPEC.md engine)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "result": {"total": r.get("total"), "n_explored": r["n_explored"]},
+        }))
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1911_06969_b200.dist import make_exchange
+    exchange = make_exchange() if world > 1 else None
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- device-resident path (value)
+    g_und = P.Graph(hg, device=local)
+    g_in = g_und.orient_dag() if app in ("tc", "cf") else g_und   # preprocessing
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    kw = dict(rank=rank, world=world, stream=sp, exchange=exchange)
+    res = None
+    for _ in range(args.warmup):
+        res = P.mine(g_in, app, k, sigma, **kw)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    step_ms = []
+    dom_ms, dom_b, launches = [], [], 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        ev0.record(stream)
+        res = P.mine(g_in, app, k, sigma, **kw)
+        ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+        dom_ms.append(res.stats["ms_dominant"])
+        dom_b.append(res.stats["b_dominant"])
+        launches += res.stats["launches"]
+    barrier()
+    clock_rec = clocks.stop()
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = tot.item() / args.steps
+    n_explored = res.stats["n_explored"]   # already summed over ranks by the engine's exchange
+    value = n_explored / (ms_per_step / 1e3)
+
+    # ---------------- end-to-end through the public C ABI from pinned host buffers
+    off_p = torch.from_numpy(np.ascontiguousarray(hg.off, dtype=np.uint64).view(np.int64)).pin_memory()
+    col_p = torch.from_numpy(np.ascontiguousarray(hg.col, dtype=np.uint32).view(np.int32)).pin_memory()
+    lab_p = (torch.from_numpy(np.ascontiguousarray(hg.labels, dtype=np.uint32).view(np.int32)).pin_memory()
+             if hg.labels is not None else None)
+    pinned = P.HostGraph(off_p.numpy().view(np.uint64), col_p.numpy().view(np.uint32),
+                         None if lab_p is None else lab_p.numpy().view(np.uint32))
+    h2d = pinned.off.nbytes + pinned.col.nbytes + (0 if lab_p is None else pinned.labels.nbytes)
+    e2e_ms = []
+    er = None
+    for i in range(1 + args.steps):
+        barrier()
+        t = time.perf_counter()
+        g = P.Graph(pinned, device=local)
+        er = P.mine(g, app, k, sigma, rank=rank, world=world, exchange=exchange)
+        del g
+        torch.cuda.synchronize()
+        if i > 0:
+            e2e_ms.append(1e3 * (time.perf_counter() - t))
+    et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_ms_step = et.item() / args.steps
+    assert er.stats["n_explored"] == n_explored and er.total == res.total, "e2e result differs from device path"
+    d2h = 8 + 8 * len(er.patterns) + 8 * 16 * 3
+
+    peak, peak_kind = load_peaks()
+    dms = statistics.median(dom_ms)
+    achieved = (statistics.median(dom_b) / (dms / 1e3) / 1e9) if dms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.app}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": config,
+        "e2e": {"value": n_explored / (e2e_ms_step / 1e3), "unit": UNIT, "ms_per_step": e2e_ms_step,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": res.stats["dominant"],
+                     "kernel_ms": dms, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                     "bytes": "SURVEY §8d B_alg of that kernel: 8*l per parent + (16 + 4*deg) per extended position"},
+        "gpu_launches": launches,
+        "clocks": clock_rec,
+        "result": {"total": res.total, "n_explored": n_explored, "level_sizes": res.stats["level_sizes"],
+                   "candidates": res.stats["candidates"], "patterns": len(res.patterns)},
+        "gen_s": round(gen_s, 2),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        root_hi, sample = cpu_sample(hg, app, k, sigma, args.cpu_budget, threads)
+        r = cpu_run(hg, app, k, sigma, root_hi, threads)
+        out["cpu_baseline"] = {"value": r["n_explored"] / (r["ms"] / 1e3), "unit": UNIT, "cores": threads,
+                               "kind": "port", "sample": sample + " (oracle/liboracle.so, OpenMP)"}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -20,7 +20,8 @@ struct gpm_graph {
   std::vector<gpm::u32> label_values;   // rank -> original label value
   int label_bits = 0;
   gpm::u32 max_deg = 0;
-  cudaStream_t stream = nullptr;        // library-owned stream
+  cudaStream_t stream = nullptr;        // stream the arrays were allocated on
+  bool owns_stream = true;              // destroy `stream` with the graph
   ~gpm_graph();
   gpm::DevGraph view() const { return gpm::DevGraph{d_off, d_col, d_lab, n, m, oriented ? 1 : 0}; }
 };
@@ -59,6 +60,8 @@ void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count
 // (SURVEY §8e); weight = candidate count of each level-1 entry.
 void root_split(const gpm_graph& g, const u32* idx, const u32* vid, u64 n1, int app, int rank, int world, u64& lo,
                 u64& hi, cudaStream_t s, Timeline& tl);
+
+void keep_pool_warm(int device);
 
 // Device orientation (graph.hpp:121-132).
 void orient_on_device(const gpm_graph& g, gpm_graph& out);

@@ -19,18 +19,38 @@ __global__ void validate_kernel(const u64* __restrict__ off, const u32* __restri
   const int lane = threadIdx.x & 31;
   const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
   const u64 nwarps = (gridDim.x * (u64)blockDim.x) >> 5;
+  __shared__ u32 smax;
+  __shared__ int sbad;
+  if (threadIdx.x == 0) {
+    smax = 0;
+    sbad = 0;
+  }
+  __syncthreads();
+  u32 mymax = 0;
+  int mybad = 0;
   for (u64 v = warp; v < n; v += nwarps) {
     u64 b = off[v], e = off[v + 1];
     if (e < b || e > m) {
-      if (lane == 0) atomicOr(bad, 1);
+      mybad |= 1;
       continue;
     }
-    if (lane == 0) atomicMax(maxdeg, (u32)(e - b));
+    mymax = max(mymax, (u32)(e - b));
     for (u64 i = b + lane; i < e; i += 32) {
       u32 x = col[i];
       bool ok = x < n && x != v && (i == b || col[i - 1] < x);
-      if (!ok) atomicOr(bad, 2);
+      if (!ok) mybad |= 2;
     }
+  }
+  mymax = __reduce_max_sync(0xffffffffu, mymax);
+  mybad = (int)__reduce_or_sync(0xffffffffu, (unsigned)mybad);
+  if (lane == 0) {
+    atomicMax(&smax, mymax);
+    atomicOr(&sbad, mybad);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (smax) atomicMax(maxdeg, smax);
+    if (sbad) atomicOr(bad, sbad);
   }
 }
 
@@ -145,6 +165,21 @@ inline unsigned grid_for(u64 items, int per_block) {
 
 void scan_inplace(u64* data, u64 n, cudaStream_t s) { exclusive_scan_u64(data, n, s); }
 
+// Keep freed stream-ordered allocations cached in the device pool instead of
+// returning them to the driver at every synchronisation: level buffers are
+// re-allocated every gpm_mine call and every level.
+void keep_pool_warm(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    u64 thr = ~u64(0);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done[device] = true;
+}
+
 void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl) {
   if (g.oriented) {
     count = g.m;
@@ -215,7 +250,7 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
   out.labeled = g.labeled;
   out.label_values = g.label_values;
   out.label_bits = g.label_bits;
-  GPM_CUDA(cudaMalloc(&out.d_off, sizeof(u64) * (g.n + 1)));
+  GPM_CUDA(cudaMallocAsync((void**)&out.d_off, sizeof(u64) * (g.n + 1), s));
   GPM_CUDA(cudaMemsetAsync(out.d_off, 0, sizeof(u64) * (g.n + 1), s));
   // the source graph lives on g.stream; order it before our stream
   GPM_CUDA(cudaStreamSynchronize(g.stream));
@@ -228,13 +263,13 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
   GPM_CUDA(cudaMemcpyAsync(&m, out.d_off + g.n, sizeof(u64), cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaStreamSynchronize(s));
   out.m = m;
-  GPM_CUDA(cudaMalloc(&out.d_col, sizeof(u32) * std::max<u64>(1, m)));
+  GPM_CUDA(cudaMallocAsync((void**)&out.d_col, sizeof(u32) * std::max<u64>(1, m), s));
   if (g.n && m) {
     orient_kernel<true><<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, g.n, out.d_off, out.d_col);
     GPM_CUDA(cudaGetLastError());
   }
   if (g.labeled) {
-    GPM_CUDA(cudaMalloc(&out.d_lab, sizeof(u32) * std::max<u32>(1, g.n)));
+    GPM_CUDA(cudaMallocAsync((void**)&out.d_lab, sizeof(u32) * std::max<u32>(1, g.n), s));
     GPM_CUDA(cudaMemcpyAsync(out.d_lab, g.d_lab, sizeof(u32) * g.n, cudaMemcpyDeviceToDevice, s));
   }
   // max out-degree (for planner heuristics)
@@ -256,10 +291,15 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
 using namespace gpm;
 
 gpm_graph::~gpm_graph() {
-  if (d_off) cudaFree(d_off);
-  if (d_col) cudaFree(d_col);
-  if (d_lab) cudaFree(d_lab);
-  if (stream) cudaStreamDestroy(stream);
+  cudaSetDevice(device);
+  cudaStream_t s = stream ? stream : 0;
+  if (d_off) cudaFreeAsync(d_off, s);
+  if (d_col) cudaFreeAsync(d_col, s);
+  if (d_lab) cudaFreeAsync(d_lab, s);
+  if (stream) {
+    cudaStreamSynchronize(stream);
+    if (owns_stream) cudaStreamDestroy(stream);
+  }
 }
 
 extern "C" int gpm_graph_create_csr(const uint64_t* row_offsets, const uint32_t* col, const uint32_t* labels,
@@ -278,6 +318,7 @@ extern "C" int gpm_graph_create_csr(const uint64_t* row_offsets, const uint32_t*
     }
     if (device < 0 || device >= ndev) throw Error(GPM_EINVAL, "device index out of range");
     GPM_CUDA(cudaSetDevice(device));
+    keep_pool_warm(device);
     auto g = std::make_unique<gpm_graph>();
     g->device = device;
     g->n = n;
@@ -285,8 +326,8 @@ extern "C" int gpm_graph_create_csr(const uint64_t* row_offsets, const uint32_t*
     g->oriented = oriented != 0;
     GPM_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     cudaStream_t s = g->stream;
-    GPM_CUDA(cudaMalloc(&g->d_off, sizeof(u64) * (n + 1)));
-    GPM_CUDA(cudaMalloc(&g->d_col, sizeof(u32) * std::max<u64>(1, m)));
+    GPM_CUDA(cudaMallocAsync((void**)&g->d_off, sizeof(u64) * (n + 1), s));
+    GPM_CUDA(cudaMallocAsync((void**)&g->d_col, sizeof(u32) * std::max<u64>(1, m), s));
     GPM_CUDA(cudaMemcpyAsync(g->d_off, row_offsets, sizeof(u64) * (n + 1), cudaMemcpyHostToDevice, s));
     if (m) GPM_CUDA(cudaMemcpyAsync(g->d_col, col, sizeof(u32) * m, cudaMemcpyHostToDevice, s));
     if (labels) {
@@ -302,7 +343,7 @@ extern "C" int gpm_graph_create_csr(const uint64_t* row_offsets, const uint32_t*
       for (u32 v = 0; v < n; ++v)
         ranks[v] = (u32)(std::lower_bound(vals.begin(), vals.end(), labels[v]) - vals.begin());
       g->labeled = true;
-      GPM_CUDA(cudaMalloc(&g->d_lab, sizeof(u32) * std::max<u32>(1, n)));
+      GPM_CUDA(cudaMallocAsync((void**)&g->d_lab, sizeof(u32) * std::max<u32>(1, n), s));
       GPM_CUDA(cudaMemcpyAsync(g->d_lab, ranks.data(), sizeof(u32) * n, cudaMemcpyHostToDevice, s));
       GPM_CUDA(cudaStreamSynchronize(s));  // ranks is a host temporary
     }

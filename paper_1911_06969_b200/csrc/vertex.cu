@@ -27,6 +27,7 @@
 //    2^32-1 entries, the u32 idx limit of embedding_list.hpp:20) into batch
 //    ranges processed depth-first: generalised edge blocking.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <cstring>
@@ -69,8 +70,9 @@ __device__ __forceinline__ void reconstruct(const VLevels& L, u64 i, u32* emb) {
 struct ExtendArgs {
   DevGraph g;
   VLevels L;
-  const u64* Wp;   // exclusive work prefix over parents, np+1 entries
-  u64 np, W, B;
+  const u64* Wp;   // exclusive work prefix over compacted parents, np+1 entries
+  const u32* pidx; // compacted parent -> level index
+  u64 np, W, B;    // np = number of parents with non-zero work
   u64 b_begin, b_end;
   unsigned long long* ctr;
   u64* cnt;          // COUNT: accepted per batch (index b - b_begin)
@@ -78,6 +80,8 @@ struct ExtendArgs {
   u64 out_base;
   u32* out_idx;
   u32* out_vid;
+  u32* masks;        // COUNT writes / WRITE reads one ballot word per 32 candidates
+  u64 mask_base;     // batch index of masks[0]
   unsigned long long* hist;   // FUSED MC: per connectivity code
   unsigned long long* total;  // FUSED TC/CF
   int k;
@@ -101,10 +105,84 @@ __global__ void __launch_bounds__(kThreads) work_kernel(DevGraph g, VLevels L, u
   }
 }
 
+// Per-lane cursor over the candidate space: caches the parent embedding that
+// owns candidate j.  Parents are addressed in the COMPACTED index space of
+// parents with non-zero work (a.pidx maps back to level indices).
+template <int APP, int LEV, bool PMASK>
+struct Cursor {
+  static constexpr int S = LEV + 1;
+  static constexpr int NPOS = (APP == kAppMC) ? S : 1;
+  static constexpr int NPROBE = (APP == kAppMC) ? 1 : S - 1;
+  u64 cp = ~0ull, cWb = 0, cWe = 0;
+  u32 parent = 0;  // level index of the parent
+  u32 emb[S];
+  u64 pbeg[NPOS];
+  u32 pdeg[NPOS];
+  u64 qbeg[NPROBE];  // CF/TC: probe lists N+(emb[t]), t < S-1
+  u32 qdeg[NPROBE];
+  u32 pmask = 0;
+
+  __device__ __forceinline__ void load(const ExtendArgs& a, u64 p) {
+    if (p == cp) return;
+    cp = p;
+    cWb = ldg(a.Wp + p);
+    cWe = ldg(a.Wp + p + 1);
+    parent = ldg(a.pidx + p);
+    reconstruct<LEV>(a.L, parent, emb);
+    const DevGraph& g = a.g;
+    if (APP == kAppMC) {
+#pragma unroll
+      for (int t = 0; t < S; ++t) {
+        pbeg[t] = ldg(g.off + emb[t]);
+        pdeg[t] = (u32)(ldg(g.off + emb[t] + 1) - pbeg[t]);
+      }
+      if (PMASK) {
+        pmask = 1u << pat::pair_index(0, 1, S + 1);
+#pragma unroll
+        for (int bb = 2; bb < S; ++bb)
+#pragma unroll
+          for (int aa = 0; aa < bb; ++aa)
+            if (has_edge_sym(g, emb[aa], emb[bb])) pmask |= 1u << pat::pair_index(aa, bb, S + 1);
+      }
+    } else {
+      pbeg[0] = ldg(g.off + emb[S - 1]);
+      pdeg[0] = (u32)(ldg(g.off + emb[S - 1] + 1) - pbeg[0]);
+#pragma unroll
+      for (int t = 0; t < S - 1; ++t) {
+        qbeg[t] = ldg(g.off + emb[t]);
+        qdeg[t] = (u32)(ldg(g.off + emb[t] + 1) - qbeg[t]);
+      }
+    }
+  }
+
+  __device__ __forceinline__ void locate(const ExtendArgs& a, u64 j, u64 pa, u64 pb) {
+    if (cp != ~0ull && j < cWe && j >= cWb) return;
+    const u64 lo = (cp == ~0ull || j < cWb) ? pa : cp + 1;
+    load(a, upper_bound_prev(a.Wp, lo, pb + 1, j));
+  }
+
+  // candidate vertex u for j (after load/locate); pos = source position
+  __device__ __forceinline__ u32 candidate(const DevGraph& g, u64 j, int& pos) const {
+    u32 local = (u32)(j - cWb);
+    if (APP == kAppMC) {
+      pos = 0;
+#pragma unroll
+      for (int t = 0; t < S - 1; ++t)
+        if (pos == t && local >= pdeg[t]) {
+          local -= pdeg[t];
+          pos = t + 1;
+        }
+      return ldg(g.col + pbeg[pos] + local);
+    }
+    pos = S - 1;
+    return ldg(g.col + pbeg[0] + local);
+  }
+};
+
 template <int APP, int LEV, int MODE>
 __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
-  constexpr int S = LEV + 1;         // parent embedding size
-  constexpr int NPOS = (APP == kAppMC) ? S : 1;
+  constexpr int S = LEV + 1;  // parent embedding size
+  constexpr int kWords = (int)(kBatch / 32);
   extern __shared__ unsigned long long shist[];
   const int lane = threadIdx.x & 31;
   const DevGraph& g = a.g;
@@ -123,66 +201,64 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
     if (b >= a.b_end) break;
     const u64 j0 = b * a.B;
     const u64 j1 = min(a.W, j0 + a.B);
+    u64 wpos = 0;
+    if (MODE == kWrite) {
+      wpos = ldg(a.boffs + b);
+      if (ldg(a.boffs + b + 1) == wpos) continue;  // batch has no children
+      wpos -= a.out_base;
+    }
     u64 pr = 0;
     if (lane < 2) pr = upper_bound_prev(a.Wp, 0, a.np + 1, lane == 0 ? j0 : j1 - 1);
     const u64 pa = __shfl_sync(0xffffffffu, pr, 0);
     const u64 pb = __shfl_sync(0xffffffffu, pr, 1);
+    Cursor<APP, LEV, MODE == kFused> cur;
 
-    // per-lane parent cache
-    u64 cp = ~0ull, cWb = 0, cWe = 0;
-    u32 emb[S];
-    u64 pbeg[NPOS];
-    u32 pdeg[NPOS];
-    u32 pmask = 0;
-    u64 wpos = 0;
-    if (MODE == kWrite) wpos = a.boffs[b] - a.out_base;
+    if (MODE == kWrite && a.masks) {
+      // execution from the inspection's ballot masks: only accepted lanes work
+      const u32* mw = a.masks + (b - a.mask_base) * kWords;
+      const int nwords = (int)((j1 - j0 + 31) / 32);
+      for (int w0 = 0; w0 < nwords; w0 += 32) {
+        const u32 mine = (w0 + lane < nwords) ? ldg(mw + w0 + lane) : 0u;
+        const int lim = min(32, nwords - w0);
+        for (int t = 0; t < lim; ++t) {
+          const u32 m = __shfl_sync(0xffffffffu, mine, t);
+          if (!m) continue;
+          if (m >> lane & 1u) {
+            const u64 j = j0 + (u64)(w0 + t) * 32 + lane;
+            cur.locate(a, j, pa, pb);
+            int pos;
+            const u32 u = cur.candidate(g, j, pos);
+            const u64 o = wpos + __popc(m & lanemask_lt());
+            a.out_idx[o] = cur.parent;
+            a.out_vid[o] = u;
+          }
+          wpos += __popc(m);
+        }
+      }
+      continue;
+    }
+
     u32 c = 0;
-
-    for (u64 jb = j0; jb < j1; jb += 32) {
+    u32 myword = 0;
+    int it = 0;
+    u64 P0 = pa;  // compacted parent owning candidate jb
+    for (u64 jb = j0; jb < j1; jb += 32, ++it) {
       const u64 j = jb + lane;
+      // lane -> parent: every compacted parent owns >= 1 candidate, so the 32
+      // parents after P0 cover this step; one OR-reduction of their start
+      // offsets gives each lane its parent (no per-lane search).
+      const u64 x = (P0 + 1 + lane <= a.np) ? ldg(a.Wp + P0 + 1 + lane) : ~0ull;
+      const u32 bit = (x - jb < 32) ? (1u << (u32)(x - jb)) : 0u;
+      const u32 starts = __reduce_or_sync(0xffffffffu, bit);
+      const u64 myp = P0 + __popc(starts & (lanemask_lt() | (1u << lane)));
+      P0 += __popc(starts);
       bool ok = false;
       u32 u = 0, code = 0;
       if (j < j1) {
-        if (cp == ~0ull || j >= cWe) {
-          const u64 lo = (cp == ~0ull) ? pa : cp + 1;
-          cp = upper_bound_prev(a.Wp, lo, pb + 1, j);
-          cWb = ldg(a.Wp + cp);
-          cWe = ldg(a.Wp + cp + 1);
-          reconstruct<LEV>(a.L, cp, emb);
-          if (APP == kAppMC) {
-#pragma unroll
-            for (int t = 0; t < S; ++t) {
-              pbeg[t] = ldg(g.off + emb[t]);
-              pdeg[t] = (u32)(ldg(g.off + emb[t] + 1) - pbeg[t]);
-            }
-            if (MODE == kFused) {
-              pmask = 1u << pat::pair_index(0, 1, S + 1);
-#pragma unroll
-              for (int bb = 2; bb < S; ++bb)
-#pragma unroll
-                for (int aa = 0; aa < bb; ++aa)
-                  if (has_edge_sym(g, emb[aa], emb[bb])) pmask |= 1u << pat::pair_index(aa, bb, S + 1);
-            }
-          } else {
-            pbeg[0] = ldg(g.off + emb[S - 1]);
-            pdeg[0] = (u32)(ldg(g.off + emb[S - 1] + 1) - pbeg[0]);
-          }
-        }
-        u32 local = (u32)(j - cWb);
+        cur.load(a, myp);
         int pos;
-        if (APP == kAppMC) {
-          pos = 0;
-#pragma unroll
-          for (int t = 0; t < S - 1; ++t)
-            if (pos == t && local >= pdeg[t]) {
-              local -= pdeg[t];
-              pos = t + 1;
-            }
-          u = ldg(g.col + pbeg[pos] + local);
-        } else {
-          pos = S - 1;
-          u = ldg(g.col + pbeg[0] + local);
-        }
+        u = cur.candidate(g, j, pos);
+        const u32* emb = cur.emb;
         bool inemb = false;
 #pragma unroll
         for (int t = 0; t < S; ++t) inemb |= (emb[t] == u);
@@ -197,7 +273,7 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
             for (int t = 0; t < S - 1; ++t)
               if (ok && t < pos && has_edge_sym(g, emb[t], u)) ok = false;
             if (ok && MODE == kFused) {
-              code = pmask | (1u << pat::pair_index(pos, S, S + 1));
+              code = cur.pmask | (1u << pat::pair_index(pos, S, S + 1));
 #pragma unroll
               for (int t = 1; t < S; ++t)
                 if (t > pos && has_edge_sym(g, emb[t], u)) code |= 1u << pat::pair_index(t, S, S + 1);
@@ -207,17 +283,23 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
             ok = true;
 #pragma unroll
             for (int t = 0; t < S - 1; ++t)
-              if (ok && !has_edge(g, emb[t], u)) ok = false;
+              if (ok && !contains_sorted(g.col + cur.qbeg[t], cur.qdeg[t], u)) ok = false;
           }
         }
       }
       const u32 mask = __ballot_sync(0xffffffffu, ok);
       if (MODE == kCount) {
         c += __popc(mask);
+        if (a.masks) {
+          if ((it & 31) == lane) myword = mask;
+          if ((it & 31) == 31) {
+            a.masks[(b - a.mask_base) * kWords + (it - 31) + lane] = myword;
+          }
+        }
       } else if (MODE == kWrite) {
         if (ok) {
           const u64 o = wpos + __popc(mask & lanemask_lt());
-          a.out_idx[o] = (u32)cp;
+          a.out_idx[o] = cur.parent;
           a.out_vid[o] = u;
         }
         wpos += __popc(mask);
@@ -233,7 +315,10 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
         }
       }
     }
-    if (MODE == kCount && lane == 0) a.cnt[b - a.b_begin] = c;
+    if (MODE == kCount) {
+      if (a.masks && (it & 31) != 0 && lane < (it & 31)) a.masks[(b - a.mask_base) * kWords + (it & ~31) + lane] = myword;
+      if (lane == 0) a.cnt[b - a.b_begin] = c;
+    }
   }
   if (MODE == kFused) {
     if (APP == kAppMC) {
@@ -244,6 +329,16 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
       atomicAdd(a.total, wtotal);
     }
   }
+}
+
+struct NonZeroW {
+  const u64* w;
+  __device__ __forceinline__ bool operator()(const u32& i) const { return w[i] != 0; }
+};
+
+__global__ void gather_kernel(const u64* __restrict__ w, const u32* __restrict__ pidx, u64 nz, u64* __restrict__ Wp) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nz; i += (u64)gridDim.x * blockDim.x)
+    Wp[i] = w[pidx[i]];
 }
 
 // Canonical code of every connectivity mask over k positions (reduce step 2:
@@ -265,6 +360,7 @@ struct Ctx {
   Stats* st;
   int sms;
   u64 cap_entries;
+  u64 mask_budget;
   unsigned long long* d_total;
   unsigned long long* d_hist;
   unsigned long long* d_ctr;
@@ -274,9 +370,11 @@ template <int APP, int LEV, int MODE>
 void launch_extend(Ctx& c, ExtendArgs& a, const char* what, double bytes) {
   auto kern = extend_kernel<APP, LEV, MODE>;
   size_t smem = (MODE == kFused && APP == kAppMC) ? sizeof(unsigned long long) * (size_t(1) << pat::npairs(c.k)) : 0;
-  int occ = 0;
-  GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
-  occ = std::max(1, occ);
+  static int occ = 0;  // per template instantiation
+  if (occ == 0) {
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
+    occ = std::max(1, occ);
+  }
   const u64 nb = a.b_end - a.b_begin;
   const u64 warps_needed = nb;
   u64 blocks = std::min<u64>((u64)c.sms * occ, (warps_needed * 32 + kThreads - 1) / kThreads);
@@ -322,13 +420,34 @@ void process(Ctx& c, VLevels L, u64 np) {
   const bool last = (LEV == c.k - 2);
   Stats& st = *c.st;
   if (np == 0) return;
-  // ---- work pass + scan: candidate space
-  DBuf<u64> Wp(np + 1, c.s);
-  GPM_CUDA(cudaMemsetAsync(Wp.get() + np, 0, sizeof(u64), c.s));
-  run_work<APP, LEV>(c, L, np, Wp.get());
-  scan_inplace(Wp.get(), np + 1, c.s);
+  // ---- work pass, compaction of parents with work, scan: candidate space
+  u64 nz = 0;
+  DBuf<u32> pidx;
+  DBuf<u64> Wp;
+  {
+    DBuf<u64> w(np, c.s);
+    run_work<APP, LEV>(c, L, np, w.get());
+    pidx.alloc(np, c.s);
+    DBuf<u64> nsel(1, c.s);
+    size_t tmp = 0;
+    thrust::counting_iterator<u32> it(0);
+    GPM_CUDA(cub::DeviceSelect::If(nullptr, tmp, it, pidx.get(), nsel.get(), (int64_t)np, NonZeroW{w.get()}, c.s));
+    DBuf<u8> t(tmp, c.s);
+    GPM_CUDA(cub::DeviceSelect::If(t.get(), tmp, it, pidx.get(), nsel.get(), (int64_t)np, NonZeroW{w.get()}, c.s));
+    GPM_CUDA(cudaMemcpyAsync(&nz, nsel.get(), sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+    GPM_CUDA(cudaStreamSynchronize(c.s));
+    Wp.alloc(nz + 1, c.s);
+    GPM_CUDA(cudaMemsetAsync(Wp.get() + nz, 0, sizeof(u64), c.s));
+    if (nz) {
+      gather_kernel<<<(unsigned)std::min<u64>((nz + 255) / 256, 1u << 20), 256, 0, c.s>>>(w.get(), pidx.get(), nz,
+                                                                                          Wp.get());
+      GPM_CUDA(cudaGetLastError());
+      c.tl->launches += 2;
+    }
+  }
+  scan_inplace(Wp.get(), nz + 1, c.s);
   u64 W = 0;
-  GPM_CUDA(cudaMemcpyAsync(&W, Wp.get() + np, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+  GPM_CUDA(cudaMemcpyAsync(&W, Wp.get() + nz, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
   GPM_CUDA(cudaStreamSynchronize(c.s));
   st.candidates[LEV] += W;
   const double bytes_in = 8.0 * LEV * np + 16.0 * NPOS * np + 4.0 * W;
@@ -339,7 +458,8 @@ void process(Ctx& c, VLevels L, u64 np) {
   a.g = c.g;
   a.L = L;
   a.Wp = Wp.get();
-  a.np = np;
+  a.pidx = pidx.get();
+  a.np = nz;
   a.W = W;
   a.B = kBatch;
   a.b_begin = 0;
@@ -355,6 +475,15 @@ void process(Ctx& c, VLevels L, u64 np) {
   DBuf<u64> cnt(nb + 1, c.s);
   GPM_CUDA(cudaMemsetAsync(cnt.get() + nb, 0, sizeof(u64), c.s));
   a.cnt = cnt.get();
+  // keep the inspection's ballot masks (1 bit per candidate) when affordable,
+  // so the execution pass touches accepted candidates only
+  DBuf<u32> masks;
+  const u64 mask_words = nb * (kBatch / 32);
+  if (mask_words * 4 <= c.mask_budget) {
+    masks.alloc(mask_words, c.s);
+    a.masks = masks.get();
+    a.mask_base = 0;
+  }
   launch_extend<APP, LEV, kCount>(c, a, "extend_count", bytes_in);
   scan_inplace(cnt.get(), nb + 1, c.s);
   u64 T = 0;
@@ -396,8 +525,10 @@ void process(Ctx& c, VLevels L, u64 np) {
     w.out_base = base;
     w.out_idx = oi.get();
     w.out_vid = ov.get();
+    // execution from masks reads 1 bit per candidate + the accepted candidates' parents
     const double frac = (double)(b1 - b0) / (double)nb;
-    launch_extend<APP, LEV, kWrite>(c, w, "extend_write", bytes_in * frac + 8.0 * Tc);
+    const double wbytes = a.masks ? (double)(b1 - b0) * kBatch / 8.0 + 24.0 * Tc : bytes_in * frac;
+    launch_extend<APP, LEV, kWrite>(c, w, "extend_write", wbytes + 8.0 * Tc);
     VLevels nl = L;
     nl.idx[LEV] = oi.get();
     nl.vid[LEV] = ov.get();
@@ -423,9 +554,8 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   if (app != GPM_APP_MC && !G0.oriented && !cfg.no_orient) {
     dag = std::make_unique<gpm_graph>();
     dag->device = G0.device;
-    dag->stream = nullptr;
-    GPM_CUDA(cudaStreamCreateWithFlags(&dag->stream, cudaStreamNonBlocking));
-    GPM_CUDA(cudaStreamSynchronize(s));
+    dag->stream = s;            // orient on the engine stream; freed on it too
+    dag->owns_stream = false;
     orient_on_device(G0, *dag);
     tl.launches += 4;
     G = dag.get();
@@ -463,6 +593,7 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   u64 budget = cfg.mem_budget ? cfg.mem_budget : (u64)(0.6 * (double)freeb);
   const int mat_levels = std::max(1, k - 3);
   c.cap_entries = std::max<u64>(kBatch, std::min<u64>((u64(1) << 32) - 1, budget / 16 / mat_levels));
+  c.mask_budget = budget / 4;
   const int nbins = (app == GPM_APP_MC) ? (1 << pat::npairs(k)) : 1;
   DBuf<unsigned long long> d_total(1, s), d_hist(nbins, s), d_ctr(1, s);
   GPM_CUDA(cudaMemsetAsync(d_total.get(), 0, sizeof(unsigned long long), s));
