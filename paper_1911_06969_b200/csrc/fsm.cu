@@ -1,11 +1,1011 @@
-// fsm.cu — edge-induced FSM engine (placeholder until the edge engine lands).
+// fsm.cu — edge-induced extend-reduce-filter engine: frequent subgraph mining
+// with canonical-mapping MNI support, on sm_100a.
+//
+// Reference: Listing 5, Alg. 1 with the level-1
+// reduce+filter before the loop
+// (is_auto_canonical_edge), :193-210 (quick/canonical pattern), :276-302
+// (domain support, merge, MNI), :362-370 (filter), :441-449 (fsm app).
+//
+// Per level:
+//   A  extend + quick code: every accepted child's quick code (nv, position
+//      labels, position-pair edge mask; pattern.cuh) is inserted into an
+//      open-addressing device hash table with warp-aggregated counts.
+//   C  canonicalize each distinct quick code once (<= 5! permutations),
+//      sort-reduce canonical codes -> dense pattern ids + counts.  Patterns
+//      whose embedding count < sigma cannot reach MNI >= sigma (MNI <= count),
+//      so only count-frequent patterns get domain bitmaps.
+//   B  extend again: OR each child's vertices into bitmap[pattern][perm[i]]
+//      (atomicOr on u32 words, canonical positions via the PositionMap).
+//   M  popcount per (pattern, position), min -> MNI.
+//   F  filter (not on the last level): inspection-execution over children
+//      whose pattern has MNI >= sigma -> next SoA level (idx, vid, his).
+// The last level is never materialised.  Multi-GPU: pattern keys are
+// all-gathered and bitmaps OR-exchanged through gpm_config.exchange.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+
 #include "engine.hpp"
+#include "pattern.cuh"
 
 namespace gpm {
 
+void scan_inplace(u64* data, u64 n, cudaStream_t s);
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr u64 kBatch = 2048;
+constexpr int kMaxEdges = 5;  // k <= 6
+enum { kQC = 0, kDomain = 1, kSCount = 2, kSWrite = 3 };
+
+struct ELevels {
+  const u32* idx[kMaxEdges + 1];
+  const u32* vid[kMaxEdges + 1];
+  const u8* his[kMaxEdges + 1];
+};
+
+// Edge-mode embedding with LEV edges (embedding_list.hpp:73-115 edge branch).
+template <int LEV>
+struct EEmb {
+  static constexpr int MAXV = LEV + 1;
+  int nv;
+  u32 v[MAXV];
+  u32 lab[MAXV];
+  u8 slot[MAXV];
+  u8 step[MAXV];
+  u32 e0[LEV], e1[LEV];   // normalised vertex pairs e_1..e_LEV
+  u8 pa[LEV], pb[LEV];    // position pairs
+};
+
+template <int LEV>
+__device__ __forceinline__ void reconstruct_e(const ELevels& L, const DevGraph& g, u64 i, EEmb<LEV>& E) {
+  u32 chain[LEV + 1];
+  u8 his[LEV + 1];
+  u64 p = i;
+#pragma unroll
+  for (int k = LEV; k >= 2; --k) {
+    chain[k] = ldg(L.vid[k - 1] + p);
+    his[k] = L.his[k - 1][p];
+    p = ldg(L.idx[k - 1] + p);
+  }
+  chain[0] = ldg(L.idx[0] + p);
+  chain[1] = ldg(L.vid[0] + p);
+  his[1] = 0;
+  u8 slotpos[LEV + 1];
+  E.nv = 0;
+#pragma unroll
+  for (int j = 0; j <= LEV; ++j) {
+    int at = E.nv;
+#pragma unroll
+    for (int q = 0; q < LEV + 1; ++q)
+      if (q < E.nv && E.v[q] == chain[j] && at == E.nv) at = q;
+    if (at == E.nv) {
+#pragma unroll
+      for (int q = 0; q < LEV + 1; ++q)
+        if (q == E.nv) {
+          E.v[q] = chain[j];
+          E.slot[q] = (u8)j;
+          E.step[q] = (u8)(j < 1 ? 1 : j);
+        }
+      ++E.nv;
+    }
+    slotpos[j] = (u8)at;
+  }
+#pragma unroll
+  for (int q = 0; q < LEV + 1; ++q)
+    if (q < E.nv) E.lab[q] = ldg(g.lab + E.v[q]);
+#pragma unroll
+  for (int j = 1; j <= LEV; ++j) {
+    u32 a = chain[his[j]], b = chain[j];
+    E.e0[j - 1] = min(a, b);
+    E.e1[j - 1] = max(a, b);
+    E.pa[j - 1] = slotpos[his[j]];
+    E.pb[j - 1] = slotpos[j];
+  }
+}
+
+__device__ __forceinline__ bool pair_gt(u32 a0, u32 a1, u32 b0, u32 b1) { return a0 != b0 ? a0 > b0 : a1 > b1; }
+
+// is_auto_canonical_edge + closing edge from its earlier-inserted
+// endpoint only.  r = position of w in the embedding or nv if new.
+template <int LEV>
+__device__ __forceinline__ bool edge_to_add(const EEmb<LEV>& E, int q, u32 w, int r) {
+  const u32 x = E.v[q];
+  const u32 n0 = min(x, w), n1 = max(x, w);
+  bool dup = false;
+#pragma unroll
+  for (int j = 0; j < LEV; ++j) dup |= (E.e0[j] == n0 && E.e1[j] == n1);
+  if (dup) return false;
+  if (r < E.nv && r < q) return false;
+  if (!pair_gt(n0, n1, E.e0[0], E.e1[0])) return false;
+  int p = E.step[q];
+  if (r < E.nv) p = min(p, (int)E.step[r]);
+#pragma unroll
+  for (int s = 2; s <= LEV; ++s)
+    if (s > p && !pair_gt(n0, n1, E.e0[s - 1], E.e1[s - 1])) return false;
+  return true;
+}
+
+// Quick code of the child (parent + edge (q, w)); fills child vertices.
+template <int LEV>
+__device__ __forceinline__ u64 child_code(const EEmb<LEV>& E, const DevGraph& g, int q, u32 w, int r, int LB,
+                                          u32* cv, int& cnv) {
+  u32 lab[LEV + 2];
+  cnv = E.nv;
+#pragma unroll
+  for (int i = 0; i < LEV + 1; ++i)
+    if (i < E.nv) {
+      cv[i] = E.v[i];
+      lab[i] = E.lab[i];
+    }
+  int wp = r;
+  if (r == E.nv) {
+#pragma unroll
+    for (int i = 0; i < LEV + 2; ++i)
+      if (i == E.nv) {
+        cv[i] = w;
+        lab[i] = ldg(g.lab + w);
+      }
+    wp = E.nv;
+    ++cnv;
+  }
+  u32 mask = 0;
+#pragma unroll
+  for (int j = 0; j < LEV; ++j) {
+    int a = min(E.pa[j], E.pb[j]), b = max(E.pa[j], E.pb[j]);
+    mask |= 1u << pat::pair_index(a, b, cnv);
+  }
+  mask |= 1u << pat::pair_index(min(q, wp), max(q, wp), cnv);
+  return pat::make_code(cnv, lab, mask, LB);
+}
+
+struct Hash {
+  unsigned long long* keys;    // 0 = empty
+  unsigned long long* counts;
+  u64 mask;                    // capacity - 1
+  unsigned long long* used;    // inserted keys
+  int* overflow;
+};
+
+__device__ __forceinline__ u64 hash64(u64 x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+
+__device__ __forceinline__ void hash_add(const Hash& H, u64 key, unsigned long long c) {
+  u64 h = hash64(key) & H.mask;
+  for (u64 probe = 0; probe <= H.mask; ++probe) {
+    unsigned long long cur = H.keys[h];
+    if (cur == key) {
+      atomicAdd(H.counts + h, c);
+      return;
+    }
+    if (cur == 0) {
+      unsigned long long prev = atomicCAS(H.keys + h, 0ull, (unsigned long long)key);
+      if (prev == 0ull) {
+        unsigned long long n = atomicAdd(H.used, 1ull);
+        if (n * 2 >= H.mask) atomicOr(H.overflow, 1);
+        atomicAdd(H.counts + h, c);
+        return;
+      }
+      if (prev == key) {
+        atomicAdd(H.counts + h, c);
+        return;
+      }
+    }
+    h = (h + 1) & H.mask;
+  }
+  atomicOr(H.overflow, 2);
+}
+
+__device__ __forceinline__ u64 hash_find(const Hash& H, u64 key) {
+  u64 h = hash64(key) & H.mask;
+  for (u64 probe = 0; probe <= H.mask; ++probe) {
+    unsigned long long cur = H.keys[h];
+    if (cur == key) return h;
+    if (cur == 0) return ~0ull;
+    h = (h + 1) & H.mask;
+  }
+  return ~0ull;
+}
+
+struct FsmArgs {
+  DevGraph g;
+  ELevels L;
+  const u64* Wp;
+  const u32* pidx;
+  u64 np, W, B, b_begin, b_end;
+  unsigned long long* ctr;
+  int LB;
+  Hash H;
+  const u32* slot_pid;    // hash slot -> pattern id
+  const u32* slot_perm;   // hash slot -> packed PositionMap (3 bits / position)
+  const u32* bslot;       // pattern -> bitmap slot or ~0
+  u32* bitmaps;
+  u64 words;
+  int kpos;
+  u32 round_lo, round_hi;
+  const u8* frequent;     // pattern -> MNI >= sigma
+  u64* cnt;
+  const u64* boffs;
+  u64 out_base;
+  u32* out_idx;
+  u32* out_vid;
+  u8* out_his;
+  unsigned long long* accepted;
+};
+
+__device__ __forceinline__ void domain_or(const FsmArgs& a, u64 slot, const u32* cv, int cnv) {
+  const u32 pid = a.slot_pid[slot];
+  const u32 bs = a.bslot[pid];
+  if (bs < a.round_lo || bs >= a.round_hi) return;
+  const u32 perm = a.slot_perm[slot];
+  u32* base = a.bitmaps + (u64)(bs - a.round_lo) * a.kpos * a.words;
+  for (int i = 0; i < cnv; ++i) {
+    const u32 cp = (perm >> (3 * i)) & 7u;
+    const u32 v = cv[i];
+    atomicOr(base + (u64)cp * a.words + (v >> 5), 1u << (v & 31));
+  }
+}
+
+// Work per parent: sum of deg over all positions (to_extend default true).
+template <int LEV>
+__global__ void __launch_bounds__(kThreads) ework_kernel(DevGraph g, ELevels L, u64 np, u64* __restrict__ W,
+                                                         unsigned long long* __restrict__ nvsum) {
+  unsigned long long mine = 0;
+  for (u64 p = blockIdx.x * (u64)blockDim.x + threadIdx.x; p < np; p += (u64)gridDim.x * blockDim.x) {
+    EEmb<LEV> E;
+    reconstruct_e<LEV>(L, g, p, E);
+    u64 w = 0;
+#pragma unroll
+    for (int q = 0; q < LEV + 1; ++q)
+      if (q < E.nv) w += ldg(g.off + E.v[q] + 1) - ldg(g.off + E.v[q]);
+    W[p] = w;
+    mine += E.nv;
+  }
+  mine = __reduce_add_sync(0xffffffffu, (unsigned)mine);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(nvsum, mine);
+}
+
+template <int LEV>
+struct ECursor {
+  u64 cp = ~0ull, cWb = 0, cWe = 0;
+  u32 parent = 0;
+  EEmb<LEV> E;
+  u64 pbeg[LEV + 1];
+  u32 pdeg[LEV + 1];
+  __device__ __forceinline__ void load(const FsmArgs& a, u64 p) {
+    if (p == cp) return;
+    cp = p;
+    cWb = ldg(a.Wp + p);
+    cWe = ldg(a.Wp + p + 1);
+    parent = ldg(a.pidx + p);
+    reconstruct_e<LEV>(a.L, a.g, parent, E);
+#pragma unroll
+    for (int q = 0; q < LEV + 1; ++q) {
+      if (q < E.nv) {
+        pbeg[q] = ldg(a.g.off + E.v[q]);
+        pdeg[q] = (u32)(ldg(a.g.off + E.v[q] + 1) - pbeg[q]);
+      } else {
+        pbeg[q] = 0;
+        pdeg[q] = 0;
+      }
+    }
+  }
+  __device__ __forceinline__ void locate(const FsmArgs& a, u64 j, u64 pa, u64 pb) {
+    if (cp != ~0ull && j < cWe && j >= cWb) return;
+    const u64 lo = (cp == ~0ull || j < cWb) ? pa : cp + 1;
+    load(a, upper_bound_prev(a.Wp, lo, pb + 1, j));
+  }
+  __device__ __forceinline__ u32 candidate(const DevGraph& g, u64 j, int& q) const {
+    u32 local = (u32)(j - cWb);
+    q = 0;
+#pragma unroll
+    for (int t = 0; t < LEV; ++t)
+      if (q == t && local >= pdeg[t]) {
+        local -= pdeg[t];
+        q = t + 1;
+      }
+    return ldg(g.col + pbeg[q] + local);
+  }
+};
+
+template <int LEV, int MODE>
+__global__ void __launch_bounds__(kThreads) eextend_kernel(FsmArgs a) {
+  const int lane = threadIdx.x & 31;
+  const DevGraph& g = a.g;
+  unsigned long long acc = 0;
+  for (;;) {
+    u64 b = 0;
+    if (lane == 0) b = atomicAdd(a.ctr, 1ull) + a.b_begin;
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (b >= a.b_end) break;
+    const u64 j0 = b * a.B;
+    const u64 j1 = min(a.W, j0 + a.B);
+    u64 wpos = 0;
+    if (MODE == kSWrite) {
+      wpos = ldg(a.boffs + b);
+      if (ldg(a.boffs + b + 1) == wpos) continue;
+      wpos -= a.out_base;
+    }
+    u64 pr = 0;
+    if (lane == 0) pr = upper_bound_prev(a.Wp, 0, a.np + 1, j0);
+    u64 P0 = __shfl_sync(0xffffffffu, pr, 0);
+    ECursor<LEV> cur;
+    u32 c = 0;
+    for (u64 jb = j0; jb < j1; jb += 32) {
+      const u64 j = jb + lane;
+      const u64 x = (P0 + 1 + lane <= a.np) ? ldg(a.Wp + P0 + 1 + lane) : ~0ull;
+      const u32 bit = (x - jb < 32) ? (1u << (u32)(x - jb)) : 0u;
+      const u32 starts = __reduce_or_sync(0xffffffffu, bit);
+      const u64 myp = P0 + __popc(starts & (lanemask_lt() | (1u << lane)));
+      P0 += __popc(starts);
+      bool ok = false;
+      u64 code = 0;
+      u32 w = 0;
+      int q = 0, r = 0;
+      u32 cv[LEV + 2];
+      int cnv = 0;
+      if (j < j1) {
+        cur.load(a, myp);
+        w = cur.candidate(g, j, q);
+        r = cur.E.nv;
+#pragma unroll
+        for (int i = 0; i < LEV + 1; ++i)
+          if (i < cur.E.nv && cur.E.v[i] == w) r = i;
+        ok = edge_to_add<LEV>(cur.E, q, w, r);
+        if (ok) code = child_code<LEV>(cur.E, g, q, w, r, a.LB, cv, cnv);
+      }
+      if (MODE == kQC) {
+        const u32 mask = __ballot_sync(0xffffffffu, ok);
+        acc += __popc(mask);
+        if (mask) {
+          const unsigned long long key = ok ? code : ~0ull;
+          const u32 peers = __match_any_sync(0xffffffffu, key);
+          if (ok && lane == __ffs(peers) - 1) hash_add(a.H, code, __popc(peers));
+        }
+      } else if (MODE == kDomain) {
+        if (ok) {
+          const u64 slot = hash_find(a.H, code);
+          domain_or(a, slot, cv, cnv);
+        }
+      } else {
+        bool keep = false;
+        if (ok) {
+          const u64 slot = hash_find(a.H, code);
+          keep = a.frequent[a.slot_pid[slot]] != 0;
+        }
+        const u32 mask = __ballot_sync(0xffffffffu, keep);
+        if (MODE == kSCount) {
+          c += __popc(mask);
+        } else {
+          if (keep) {
+            const u64 o = wpos + __popc(mask & lanemask_lt());
+            a.out_idx[o] = cur.parent;
+            a.out_vid[o] = w;
+            a.out_his[o] = cur.E.slot[q];
+          }
+          wpos += __popc(mask);
+        }
+      }
+    }
+    if (MODE == kSCount && lane == 0) a.cnt[b - a.b_begin] = c;
+  }
+  if (MODE == kQC && lane == 0 && acc) atomicAdd(a.accepted, acc);
+}
+
+// ---- level 1 (single edges): reduce + filter before the loop
+__device__ __forceinline__ u64 l1_code(const DevGraph& g, u32 u, u32 v, int LB) {
+  u32 lab[2] = {ldg(g.lab + u), ldg(g.lab + v)};
+  return pat::make_code(2, lab, 1u, LB);
+}
+
+template <int MODE>
+__global__ void l1_kernel(FsmArgs a, const u32* __restrict__ idx, const u32* __restrict__ vid, u64 n,
+                          u8* __restrict__ keep) {
+  const int lane = threadIdx.x & 31;
+  for (u64 i0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; i0 < n; i0 += (u64)gridDim.x * blockDim.x) {
+    const u64 i = i0 + lane;
+    const bool act = i < n;
+    u32 u = 0, v = 0;
+    u64 code = 0;
+    if (act) {
+      u = idx[i];
+      v = vid[i];
+      code = l1_code(a.g, u, v, a.LB);
+    }
+    if (MODE == kQC) {
+      const unsigned long long key = act ? code : ~0ull;
+      const u32 peers = __match_any_sync(0xffffffffu, key);
+      if (act && lane == __ffs(peers) - 1) hash_add(a.H, code, __popc(peers));
+    } else if (MODE == kDomain) {
+      if (act) {
+        u32 cv[2] = {u, v};
+        domain_or(a, hash_find(a.H, code), cv, 2);
+      }
+    } else if (act) {
+      keep[i] = a.frequent[a.slot_pid[hash_find(a.H, code)]];
+    }
+  }
+}
+
+// canonicalize every occupied hash slot once (reduce step 2)
+__global__ void canon_slots_kernel(const unsigned long long* __restrict__ keys, u64 cap, int LB,
+                                   u64* __restrict__ canon, u32* __restrict__ perm) {
+  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < cap; s += (u64)gridDim.x * blockDim.x) {
+    const u64 key = keys[s];
+    if (!key) {
+      canon[s] = ~0ull;
+      continue;
+    }
+    int nv;
+    u32 lab[8], mask;
+    pat::decode(key, LB, &nv, lab, &mask);
+    u8 p[8];
+    canon[s] = pat::canonicalize(nv, lab, mask, LB, p);
+    u32 pk = 0;
+    for (int i = 0; i < nv; ++i) pk |= (u32)p[i] << (3 * i);
+    perm[s] = pk;
+  }
+}
+
+__global__ void slot_pid_kernel(const u64* __restrict__ canon, u64 cap, const u64* __restrict__ gkeys, u64 P,
+                                u32* __restrict__ slot_pid) {
+  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < cap; s += (u64)gridDim.x * blockDim.x) {
+    const u64 c = canon[s];
+    if (c == ~0ull) continue;
+    u64 lo = 0, hi = P;
+    while (lo < hi) {
+      u64 mid = (lo + hi) >> 1;
+      if (gkeys[mid] < c) lo = mid + 1;
+      else hi = mid;
+    }
+    slot_pid[s] = (u32)lo;
+  }
+}
+
+// popcount per (pattern, canonical position); MNI = min over positions
+__global__ void mni_kernel(const u32* __restrict__ bitmaps, u64 words, int kpos, const u64* __restrict__ gkeys,
+                           const u32* __restrict__ bs_to_pid, u32 round_lo, u32 round_n,
+                           unsigned long long* __restrict__ mni) {
+  const u32 r = blockIdx.x;  // bitmap pattern within round
+  if (r >= round_n) return;
+  const u32 pid = bs_to_pid[round_lo + r];
+  const int nv = pat::code_nv(gkeys[pid]);
+  __shared__ unsigned long long part[32];
+  __shared__ unsigned long long best;
+  if (threadIdx.x == 0) best = ~0ull;
+  __syncthreads();
+  for (int pos = 0; pos < nv; ++pos) {
+    const u32* bm = bitmaps + ((u64)r * kpos + pos) * words;
+    unsigned long long c = 0;
+    for (u64 w = threadIdx.x; w < words; w += blockDim.x) c += __popc(bm[w]);
+    c = __reduce_add_sync(0xffffffffu, (unsigned)c);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
+      best = min(best, t);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) mni[pid] = best;
+}
+
+struct NonZeroW {
+  const u64* w;
+  __device__ __forceinline__ bool operator()(const u32& i) const { return w[i] != 0; }
+};
+
+__global__ void egather_kernel(const u64* __restrict__ w, const u32* __restrict__ pidx, u64 nz, u64* __restrict__ Wp) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nz; i += (u64)gridDim.x * blockDim.x)
+    Wp[i] = w[pidx[i]];
+}
+
+inline unsigned grid1(u64 items) { return (unsigned)std::max<u64>(1, std::min<u64>((items + 255) / 256, 1u << 20)); }
+
+// ------------------------------------------------------------------ host driver
+struct Fsm {
+  const gpm_graph& G;
+  const gpm_config& cfg;
+  DevGraph g;
+  cudaStream_t s;
+  Stats& st;
+  Timeline& tl;
+  gpm_result& res;
+  int k;
+  u64 sigma;
+  int LB;
+  int sms;
+  u64 budget;
+  DBuf<unsigned long long> d_ctr;
+
+  Fsm(const gpm_graph& G_, const gpm_config& c_, cudaStream_t s_, Stats& st_, Timeline& tl_, gpm_result& r_)
+      : G(G_), cfg(c_), g(G_.view()), s(s_), st(st_), tl(tl_), res(r_) {}
+
+  void sync() { GPM_CUDA(cudaStreamSynchronize(s)); }
+  template <class T>
+  T d2h(const T* p) {
+    T v;
+    GPM_CUDA(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, s));
+    sync();
+    return v;
+  }
+
+  // Reduce state for one level
+  struct Level {
+    u64 cap = 0;
+    DBuf<unsigned long long> keys, counts, used;
+    DBuf<int> overflow;
+    DBuf<u64> canon;
+    DBuf<u32> perm, slot_pid, bslot, bs_to_pid;
+    DBuf<u8> frequent;
+    std::vector<u64> gkeys_h, gcount_h, mni_h;
+    DBuf<u64> gkeys;
+    u64 P = 0;
+    u64 NB = 0;
+  };
+
+  Hash hash_of(Level& R) {
+    return Hash{R.keys.get(), R.counts.get(), R.cap - 1, R.used.get(), R.overflow.get()};
+  }
+
+  void alloc_hash(Level& R, u64 cap) {
+    R.cap = cap;
+    R.keys.alloc(cap, s);
+    R.counts.alloc(cap, s);
+    R.used.alloc(1, s);
+    R.overflow.alloc(1, s);
+    GPM_CUDA(cudaMemsetAsync(R.keys.get(), 0, sizeof(unsigned long long) * cap, s));
+    GPM_CUDA(cudaMemsetAsync(R.counts.get(), 0, sizeof(unsigned long long) * cap, s));
+    GPM_CUDA(cudaMemsetAsync(R.used.get(), 0, sizeof(unsigned long long), s));
+    GPM_CUDA(cudaMemsetAsync(R.overflow.get(), 0, sizeof(int), s));
+  }
+
+  // After pass A: canonicalize slots, global pattern table (+exchange), pids,
+  // count pre-filter, bitmap slots.
+  void canon_and_group(Level& R) {
+    R.canon.alloc(R.cap, s);
+    R.perm.alloc(R.cap, s);
+    R.slot_pid.alloc(R.cap, s);
+    canon_slots_kernel<<<grid1(R.cap), 256, 0, s>>>(R.keys.get(), R.cap, LB, R.canon.get(), R.perm.get());
+    GPM_CUDA(cudaGetLastError());
+    ++tl.launches;
+    // compact (canon, count) of occupied slots, sort by canon, reduce by key
+    DBuf<u64> ck(R.cap, s), ck2(R.cap, s);
+    DBuf<unsigned long long> cc(R.cap, s), cc2(R.cap, s);
+    GPM_CUDA(cudaMemcpyAsync(ck.get(), R.canon.get(), sizeof(u64) * R.cap, cudaMemcpyDeviceToDevice, s));
+    GPM_CUDA(cudaMemcpyAsync(cc.get(), R.counts.get(), sizeof(u64) * R.cap, cudaMemcpyDeviceToDevice, s));
+    size_t tmp = 0;
+    GPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ck.get(), ck2.get(), cc.get(), cc2.get(), (int64_t)R.cap, 0,
+                                             64, s));
+    DBuf<u8> t(tmp, s);
+    GPM_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, ck.get(), ck2.get(), cc.get(), cc2.get(), (int64_t)R.cap, 0,
+                                             64, s));
+    // occupied slots are the first U entries (empty = ~0 sorts last)
+    const u64 U = d2h(R.used.get());
+    std::vector<u64> keys(U), cnts(U);
+    if (U) {
+      GPM_CUDA(cudaMemcpyAsync(keys.data(), ck2.get(), sizeof(u64) * U, cudaMemcpyDeviceToHost, s));
+      GPM_CUDA(cudaMemcpyAsync(cnts.data(), cc2.get(), sizeof(u64) * U, cudaMemcpyDeviceToHost, s));
+      sync();
+    }
+    // multi-GPU: all-gather every rank's (canonical key, count) list
+    if (cfg.world > 1 && cfg.exchange) {
+      const int W = cfg.world;
+      std::vector<u64> lens(W, 0);
+      lens[cfg.rank] = U;
+      exchange_sum_host(cfg, lens, s);
+      u64 mx = *std::max_element(lens.begin(), lens.end());
+      std::vector<u64> buf(2 * mx * W, 0);
+      for (u64 i = 0; i < U; ++i) {
+        buf[(u64)cfg.rank * 2 * mx + i] = keys[i];
+        buf[(u64)cfg.rank * 2 * mx + mx + i] = cnts[i];
+      }
+      exchange_sum_host(cfg, buf, s);  // disjoint slots: sum == all-gather
+      keys.clear();
+      cnts.clear();
+      for (int r = 0; r < W; ++r)
+        for (u64 i = 0; i < lens[r]; ++i) {
+          keys.push_back(buf[(u64)r * 2 * mx + i]);
+          cnts.push_back(buf[(u64)r * 2 * mx + mx + i]);
+        }
+      std::vector<size_t> ord(keys.size());
+      for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+      std::sort(ord.begin(), ord.end(), [&](size_t x, size_t y) { return keys[x] < keys[y]; });
+      std::vector<u64> k2, c2;
+      for (size_t i : ord) {
+        k2.push_back(keys[i]);
+        c2.push_back(cnts[i]);
+      }
+      keys.swap(k2);
+      cnts.swap(c2);
+    }
+    // reduce by canonical key (sorted)
+    R.gkeys_h.clear();
+    R.gcount_h.clear();
+    for (size_t i = 0; i < keys.size(); ++i) {
+      if (R.gkeys_h.empty() || R.gkeys_h.back() != keys[i]) {
+        R.gkeys_h.push_back(keys[i]);
+        R.gcount_h.push_back(0);
+      }
+      R.gcount_h.back() += cnts[i];
+    }
+    R.P = R.gkeys_h.size();
+    R.gkeys.alloc(std::max<u64>(1, R.P), s);
+    if (R.P)
+      GPM_CUDA(cudaMemcpyAsync(R.gkeys.get(), R.gkeys_h.data(), sizeof(u64) * R.P, cudaMemcpyHostToDevice, s));
+    slot_pid_kernel<<<grid1(R.cap), 256, 0, s>>>(R.canon.get(), R.cap, R.gkeys.get(), R.P, R.slot_pid.get());
+    GPM_CUDA(cudaGetLastError());
+    ++tl.launches;
+    // count pre-filter -> bitmap slots (MNI <= count)
+    std::vector<u32> bslot(std::max<u64>(1, R.P), ~0u), bs_to_pid;
+    for (u64 p = 0; p < R.P; ++p)
+      if (R.gcount_h[p] >= sigma) {
+        bslot[p] = (u32)bs_to_pid.size();
+        bs_to_pid.push_back((u32)p);
+      }
+    R.NB = bs_to_pid.size();
+    R.bslot.alloc(bslot.size(), s);
+    GPM_CUDA(cudaMemcpyAsync(R.bslot.get(), bslot.data(), sizeof(u32) * bslot.size(), cudaMemcpyHostToDevice, s));
+    R.bs_to_pid.alloc(std::max<u64>(1, R.NB), s);
+    if (R.NB)
+      GPM_CUDA(cudaMemcpyAsync(R.bs_to_pid.get(), bs_to_pid.data(), sizeof(u32) * R.NB, cudaMemcpyHostToDevice, s));
+    sync();  // host vectors above are temporaries
+  }
+
+  // Domain pass in rounds that fit the bitmap budget; MNI; frequent flags.
+  template <class DomainFn>
+  void domains_and_mni(Level& R, int kpos, DomainFn&& run_domain) {
+    const u64 words = (G.n + 31) / 32;
+    const u64 per_pat = (u64)kpos * words * 4;
+    const u64 per_round = std::max<u64>(1, std::min<u64>(R.NB, budget / 2 / std::max<u64>(1, per_pat)));
+    DBuf<unsigned long long> mni(std::max<u64>(1, R.P), s);
+    GPM_CUDA(cudaMemsetAsync(mni.get(), 0, sizeof(unsigned long long) * std::max<u64>(1, R.P), s));
+    if (R.NB) {
+      DBuf<u32> bm(per_round * kpos * words, s);
+      for (u64 lo = 0; lo < R.NB; lo += per_round) {
+        const u64 n = std::min(per_round, R.NB - lo);
+        GPM_CUDA(cudaMemsetAsync(bm.get(), 0, sizeof(u32) * n * kpos * words, s));
+        run_domain(bm.get(), words, kpos, (u32)lo, (u32)(lo + n));
+        // multi-GPU: OR the packed domain bitmaps across ranks (SURVEY §5 route ii)
+        exchange_device(cfg, bm.get(), n * kpos * words, 4, 1, s);
+        mni_kernel<<<(unsigned)n, 256, 0, s>>>(bm.get(), words, kpos, R.gkeys.get(), R.bs_to_pid.get(), (u32)lo,
+                                               (u32)n, mni.get());
+        GPM_CUDA(cudaGetLastError());
+        ++tl.launches;
+      }
+    }
+    R.mni_h.assign(R.P, 0);
+    if (R.P)
+      GPM_CUDA(cudaMemcpyAsync(R.mni_h.data(), mni.get(), sizeof(u64) * R.P, cudaMemcpyDeviceToHost, s));
+    sync();
+    std::vector<u8> freq(std::max<u64>(1, R.P), 0);
+    for (u64 p = 0; p < R.P; ++p) freq[p] = (R.gcount_h[p] >= sigma && R.mni_h[p] >= sigma) ? 1 : 0;
+    R.frequent.alloc(freq.size(), s);
+    GPM_CUDA(cudaMemcpyAsync(R.frequent.get(), freq.data(), freq.size(), cudaMemcpyHostToDevice, s));
+    sync();
+  }
+
+  void record(Level& R, int level) {
+    for (u64 p = 0; p < R.P; ++p)
+      if (R.gcount_h[p] >= sigma && R.mni_h[p] >= sigma)
+        res.patterns.push_back({canon_text(R.gkeys_h[p], 0, LB, &G.label_values), R.mni_h[p], level});
+  }
+
+  FsmArgs base_args(Level& R) {
+    FsmArgs a{};
+    a.g = g;
+    a.LB = LB;
+    a.H = hash_of(R);
+    a.ctr = d_ctr.get();
+    return a;
+  }
+
+  // ---------------------------------------------------------- level 1
+  void level1(DBuf<u32>& idx, DBuf<u32>& vid, u64& n1) {
+    Level R;
+    u64 cap = 1024;
+    while (cap < 4 * std::min<u64>(n1, u64(1) << 22)) cap <<= 1;
+    for (;;) {
+      alloc_hash(R, cap);
+      FsmArgs a = base_args(R);
+      if (n1) {
+        l1_kernel<kQC><<<grid1(n1), 256, 0, s>>>(a, idx.get(), vid.get(), n1, nullptr);
+        GPM_CUDA(cudaGetLastError());
+        ++tl.launches;
+      }
+      if (d2h(R.overflow.get()) == 0) break;
+      cap <<= 3;
+    }
+    canon_and_group(R);
+    domains_and_mni(R, 2, [&](u32* bm, u64 words, int kpos, u32 lo, u32 hi) {
+      FsmArgs a = base_args(R);
+      a.slot_pid = R.slot_pid.get();
+      a.slot_perm = R.perm.get();
+      a.bslot = R.bslot.get();
+      a.bitmaps = bm;
+      a.words = words;
+      a.kpos = kpos;
+      a.round_lo = lo;
+      a.round_hi = hi;
+      if (n1) {
+        l1_kernel<kDomain><<<grid1(n1), 256, 0, s>>>(a, idx.get(), vid.get(), n1, nullptr);
+        GPM_CUDA(cudaGetLastError());
+        ++tl.launches;
+      }
+    });
+    record(R, 1);
+    // filter: keep entries whose pattern is frequent
+    if (!n1) return;
+    DBuf<u8> keep(n1, s);
+    {
+      FsmArgs a = base_args(R);
+      a.slot_pid = R.slot_pid.get();
+      a.frequent = R.frequent.get();
+      l1_kernel<kSCount><<<grid1(n1), 256, 0, s>>>(a, idx.get(), vid.get(), n1, keep.get());
+      GPM_CUDA(cudaGetLastError());
+      ++tl.launches;
+    }
+    DBuf<u32> ni(n1, s), nvv(n1, s);
+    DBuf<u64> nsel(1, s);
+    size_t tmp = 0;
+    GPM_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, idx.get(), keep.get(), ni.get(), nsel.get(), (int64_t)n1, s));
+    DBuf<u8> t(tmp, s);
+    GPM_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, idx.get(), keep.get(), ni.get(), nsel.get(), (int64_t)n1, s));
+    GPM_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, vid.get(), keep.get(), nvv.get(), nsel.get(), (int64_t)n1, s));
+    n1 = d2h(nsel.get());
+    idx = std::move(ni);
+    vid = std::move(nvv);
+    st.survivors[0] = n1;
+  }
+
+  // ---------------------------------------------------------- extend levels
+  template <int LEV>
+  void launch(FsmArgs& a, int mode, const char* name, double bytes) {
+    void (*kern)(FsmArgs) = nullptr;
+    switch (mode) {
+      case kQC: kern = eextend_kernel<LEV, kQC>; break;
+      case kDomain: kern = eextend_kernel<LEV, kDomain>; break;
+      case kSCount: kern = eextend_kernel<LEV, kSCount>; break;
+      default: kern = eextend_kernel<LEV, kSWrite>; break;
+    }
+    int occ = 0;
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
+    occ = std::max(1, occ);
+    const u64 nb = a.b_end - a.b_begin;
+    u64 blocks = std::max<u64>(1, std::min<u64>((u64)sms * occ, (nb * 32 + kThreads - 1) / kThreads));
+    GPM_CUDA(cudaMemsetAsync(d_ctr.get(), 0, sizeof(unsigned long long), s));
+    size_t ev = tl.begin(std::string(name) + "_L" + std::to_string(LEV), bytes);
+    kern<<<(unsigned)blocks, kThreads, 0, s>>>(a);
+    GPM_CUDA(cudaGetLastError());
+    tl.end(ev);
+    ++tl.launches;
+  }
+
+  // Extends level LEV (np parents) -> reduce (+ filter into out arrays unless last)
+  template <int LEV>
+  void extend_level(const ELevels& L, u64 np, bool last, DBuf<u32>& oi, DBuf<u32>& ov, DBuf<u8>& oh, u64& nout) {
+    nout = 0;
+    // work + compaction + scan
+    DBuf<u64> w(std::max<u64>(1, np), s);
+    DBuf<unsigned long long> nvsum(1, s);
+    GPM_CUDA(cudaMemsetAsync(nvsum.get(), 0, sizeof(unsigned long long), s));
+    if (np) {
+      ework_kernel<LEV><<<grid1(np), kThreads, 0, s>>>(g, L, np, w.get(), nvsum.get());
+      GPM_CUDA(cudaGetLastError());
+      ++tl.launches;
+    }
+    DBuf<u32> pidx(std::max<u64>(1, np), s);
+    DBuf<u64> nsel(1, s);
+    u64 nz = 0;
+    if (np) {
+      size_t tmp = 0;
+      thrust::counting_iterator<u32> it(0);
+      GPM_CUDA(cub::DeviceSelect::If(nullptr, tmp, it, pidx.get(), nsel.get(), (int64_t)np, NonZeroW{w.get()}, s));
+      DBuf<u8> t(tmp, s);
+      GPM_CUDA(cub::DeviceSelect::If(t.get(), tmp, it, pidx.get(), nsel.get(), (int64_t)np, NonZeroW{w.get()}, s));
+      nz = d2h(nsel.get());
+    }
+    DBuf<u64> Wp(nz + 1, s);
+    GPM_CUDA(cudaMemsetAsync(Wp.get() + nz, 0, sizeof(u64), s));
+    if (nz) {
+      egather_kernel<<<grid1(nz), 256, 0, s>>>(w.get(), pidx.get(), nz, Wp.get());
+      GPM_CUDA(cudaGetLastError());
+      ++tl.launches;
+    }
+    scan_inplace(Wp.get(), nz + 1, s);
+    const u64 W = d2h(Wp.get() + nz);
+    const u64 nvs = d2h(nvsum.get());
+    st.candidates[LEV] += W;
+    const double bytes_in = 8.0 * LEV * np + 16.0 * nvs + 4.0 * W;
+    st.balg += bytes_in;
+    const u64 nb = (W + kBatch - 1) / kBatch;
+
+    Level R;
+    DBuf<unsigned long long> accepted(1, s);
+    auto args = [&](Level& RR) {
+      FsmArgs a = base_args(RR);
+      a.L = L;
+      a.Wp = Wp.get();
+      a.pidx = pidx.get();
+      a.np = nz;
+      a.W = W;
+      a.B = kBatch;
+      a.b_begin = 0;
+      a.b_end = nb;
+      a.accepted = accepted.get();
+      return a;
+    };
+    u64 cap = 1u << 14;
+    for (;;) {
+      alloc_hash(R, cap);
+      GPM_CUDA(cudaMemsetAsync(accepted.get(), 0, sizeof(unsigned long long), s));
+      if (nb) {
+        FsmArgs a = args(R);
+        launch<LEV>(a, kQC, "fsm_extend_qc", bytes_in);
+      }
+      if (d2h(R.overflow.get()) == 0) break;
+      cap <<= 3;
+    }
+    u64 acc = d2h(accepted.get());
+    if (cfg.world > 1 && cfg.exchange) {
+      std::vector<u64> v{acc};
+      exchange_sum_host(cfg, v, s);
+      acc = v[0];
+    }
+    st.level_sizes[LEV] += acc;
+    canon_and_group(R);
+    domains_and_mni(R, LEV + 2, [&](u32* bm, u64 words, int kpos, u32 lo, u32 hi) {
+      if (!nb) return;
+      FsmArgs a = args(R);
+      a.slot_pid = R.slot_pid.get();
+      a.slot_perm = R.perm.get();
+      a.bslot = R.bslot.get();
+      a.bitmaps = bm;
+      a.words = words;
+      a.kpos = kpos;
+      a.round_lo = lo;
+      a.round_hi = hi;
+      launch<LEV>(a, kDomain, "fsm_extend_domain", bytes_in);
+    });
+    record(R, LEV + 1);
+    if (last || !nb) return;
+    // filter + write survivors (inspection-execution)
+    DBuf<u64> cnt(nb + 1, s);
+    GPM_CUDA(cudaMemsetAsync(cnt.get() + nb, 0, sizeof(u64), s));
+    {
+      FsmArgs a = args(R);
+      a.slot_pid = R.slot_pid.get();
+      a.frequent = R.frequent.get();
+      a.cnt = cnt.get();
+      launch<LEV>(a, kSCount, "fsm_extend_filter_count", bytes_in);
+    }
+    scan_inplace(cnt.get(), nb + 1, s);
+    const u64 T = d2h(cnt.get() + nb);
+    if (T >= (u64(1) << 32)) throw Error(GPM_ENOMEM, "fsm level exceeds 2^32 embeddings");
+    nout = T;
+    oi.alloc(std::max<u64>(1, T), s);
+    ov.alloc(std::max<u64>(1, T), s);
+    oh.alloc(std::max<u64>(1, T), s);
+    if (T) {
+      FsmArgs a = args(R);
+      a.slot_pid = R.slot_pid.get();
+      a.frequent = R.frequent.get();
+      a.boffs = cnt.get();
+      a.out_base = 0;
+      a.out_idx = oi.get();
+      a.out_vid = ov.get();
+      a.out_his = oh.get();
+      launch<LEV>(a, kSWrite, "fsm_extend_filter_write", bytes_in + 9.0 * T);
+    }
+    st.survivors[LEV] = T;
+    st.balg += 9.0 * T;
+  }
+
+  void run() {
+    k = cfg.k;
+    sigma = cfg.min_support;
+    if (!G.labeled) throw Error(GPM_EINVAL, "fsm: graph is unlabeled");
+    if (G.oriented) throw Error(GPM_EINVAL, "fsm: graph must be undirected");
+    if (k < 2 || k > kMaxEdges + 1) throw Error(GPM_EINVAL, "fsm: k must be in [2,6]");
+    LB = std::max(1, G.label_bits);
+    if (k * LB + pat::npairs(k) > 61)
+      throw Error(GPM_EINVAL, "fsm: too many distinct labels for a packed pattern code at this k");
+    sms = sm_count();
+    size_t freeb = 0, totalb = 0;
+    GPM_CUDA(cudaMemGetInfo(&freeb, &totalb));
+    budget = cfg.mem_budget ? cfg.mem_budget : (u64)(0.5 * (double)freeb);
+    d_ctr.alloc(1, s);
+    const int levels = k - 1;
+    st.ensure(levels);
+    DBuf<u32> l1i, l1v;
+    u64 n1 = 0;
+    build_level1(G, l1i, l1v, n1, s, tl);
+    u64 lo = 0, hi = n1;
+    if (cfg.root_hi > 0) {
+      lo = std::min(cfg.root_lo, n1);
+      hi = std::max(lo, std::min(cfg.root_hi, n1));
+    } else {
+      root_split(G, l1i.get(), l1v.get(), n1, GPM_APP_MC, cfg.rank, std::max(1, cfg.world), lo, hi, s, tl);
+    }
+    // slice level 1 into owned arrays
+    u64 nr = hi - lo;
+    {
+      DBuf<u32> a(std::max<u64>(1, nr), s), b(std::max<u64>(1, nr), s);
+      if (nr) {
+        GPM_CUDA(cudaMemcpyAsync(a.get(), l1i.get() + lo, sizeof(u32) * nr, cudaMemcpyDeviceToDevice, s));
+        GPM_CUDA(cudaMemcpyAsync(b.get(), l1v.get() + lo, sizeof(u32) * nr, cudaMemcpyDeviceToDevice, s));
+      }
+      l1i = std::move(a);
+      l1v = std::move(b);
+    }
+    u64 nl1 = nr;
+    if (cfg.world > 1 && cfg.exchange) {
+      std::vector<u64> v{nr};
+      exchange_sum_host(cfg, v, s);
+      nl1 = v[0];
+    }
+    st.level_sizes[0] = nl1;
+    level1(l1i, l1v, nr);
+    DBuf<u8> l1h(std::max<u64>(1, nr), s);
+    GPM_CUDA(cudaMemsetAsync(l1h.get(), 0, std::max<u64>(1, nr), s));
+    std::vector<DBuf<u32>> li(levels), lv(levels);
+    std::vector<DBuf<u8>> lh(levels);
+    li[0] = std::move(l1i);
+    lv[0] = std::move(l1v);
+    lh[0] = std::move(l1h);
+    u64 np = nr;
+    ELevels L{};
+    for (int lev = 1; lev <= levels - 1; ++lev) {
+      L.idx[lev - 1] = li[lev - 1].get();
+      L.vid[lev - 1] = lv[lev - 1].get();
+      L.his[lev - 1] = lh[lev - 1].get();
+      const bool last = (lev == levels - 1);
+      u64 nout = 0;
+      switch (lev) {
+        case 1: extend_level<1>(L, np, last, li[lev], lv[lev], lh[lev], nout); break;
+        case 2: extend_level<2>(L, np, last, li[lev], lv[lev], lh[lev], nout); break;
+        case 3: extend_level<3>(L, np, last, li[lev], lv[lev], lh[lev], nout); break;
+        case 4: extend_level<4>(L, np, last, li[lev], lv[lev], lh[lev], nout); break;
+        default: throw Error(GPM_EINVAL, "fsm: level out of range");
+      }
+      np = nout;
+    }
+    if (cfg.world > 1 && cfg.exchange) {
+      // level sizes except the already-reduced accepted counts: survivors per rank
+      std::vector<u64> v(st.survivors.begin(), st.survivors.end());
+      std::vector<u64> c(st.candidates.begin(), st.candidates.end());
+      v.insert(v.end(), c.begin(), c.end());
+      v.push_back((u64)st.balg);
+      exchange_sum_host(cfg, v, s);
+      const size_t L2 = st.survivors.size();
+      for (size_t i = 0; i < L2; ++i) st.survivors[i] = v[i];
+      for (size_t i = 0; i < st.candidates.size(); ++i) st.candidates[i] = v[L2 + i];
+      st.balg = (double)v.back();
+    }
+    std::sort(res.patterns.begin(), res.patterns.end(), [](const gpm_result::Pattern& x, const gpm_result::Pattern& y) {
+      if (x.level != y.level) return x.level < y.level;
+      if (x.support != y.support) return x.support > y.support;
+      return x.text < y.text;
+    });
+  }
+};
+
+}  // namespace
+
 void mine_fsm(const gpm_graph& g, const gpm_config& cfg, cudaStream_t s, gpm_result& res, Stats& st, Timeline& tl) {
-  (void)g; (void)cfg; (void)s; (void)res; (void)st; (void)tl;
-  throw Error(GPM_EINVAL, "fsm: not built yet");
+  Fsm f(g, cfg, s, st, tl, res);
+  f.run();
 }
 
 }  // namespace gpm

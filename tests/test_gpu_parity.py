@@ -176,3 +176,54 @@ def test_edge_cases(P, oracle):
         P.Graph(P.HostGraph(np.array([0, 1], np.uint64), np.array([0], np.uint32)))        # self-loop
     with pytest.raises(P.GpmError):
         P.mine(P.Graph(host(P, oracle, [(0, 1)], 2)), "mc", 7)
+
+
+# ----------------------------------------------------------------- FSM (edge-induced)
+def test_fsm_golden(P, oracle, golden):
+    for rec in golden:
+        if rec["labels"] is None:
+            continue
+        g = P.Graph(host(P, oracle, [tuple(e) for e in rec["edges"]], rec["n"], rec["labels"]))
+        for key, want in rec["bf_fsm"].items():
+            k, sigma = map(int, key.split(","))
+            r = P.mine(g, "fsm", k, sigma)
+            assert [list(p) for p in r.patterns] == want["patterns"], (rec["name"], key)
+            assert r.stats["level_sizes"][:len(want["level_sizes"])] == want["level_sizes"], (rec["name"], key)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fsm_gnp_parity(P, oracle, seed):
+    rng = np.random.default_rng(700 + seed)
+    n = int(rng.integers(30, 120))
+    lab = rng.integers(0, [2, 3, 5][seed % 3], n)
+    hg = host(P, oracle, BF.gnp(n, 0.08, 700 + seed), n, lab)
+    g = P.Graph(hg)
+    oc = oracle.Csr(hg.off, hg.col, hg.labels)
+    for k in (2, 3, 4, 5):
+        for sigma in (0, 2, 5):
+            r = P.mine(g, "fsm", k, sigma)
+            o = oracle.mine(oc, "fsm", k, sigma)
+            assert [tuple(p) for p in r.patterns] == [tuple(p) for p in o["patterns"]], (k, sigma)
+            same(r, o, ("level_sizes", "candidates", "survivors", "n_explored", "b_alg"))
+
+
+@pytest.mark.parametrize("labels,sigma", [(4, 20), (8, 40), (32, 5)])
+def test_fsm_rmat_parity(P, oracle, labels, sigma):
+    hg = P.generate_rmat(12, 6, 0.45, 0.15, 0.15, seed=labels, n_labels=labels, label_seed=101)
+    g = P.Graph(hg)
+    oc = oracle.Csr(hg.off, hg.col, hg.labels)
+    r = P.mine(g, "fsm", 4, sigma)
+    o = oracle.mine(oc, "fsm", 4, sigma)
+    assert [tuple(p) for p in r.patterns] == [tuple(p) for p in o["patterns"]]
+    same(r, o, ("level_sizes", "candidates", "survivors", "n_explored", "b_alg"))
+
+
+def test_fsm_errors_and_sparse_labels(P, oracle):
+    g = P.Graph(host(P, oracle, [(0, 1), (1, 2)], 3))
+    with pytest.raises(P.GpmError):
+        P.mine(g, "fsm", 3, 1)                                   # unlabeled
+    # large, sparse label values keep their identity in the pattern text
+    hg = host(P, oracle, [(0, 1), (1, 2), (2, 3), (3, 0)], 4, [7, 1000000, 7, 1000000])
+    r = P.mine(P.Graph(hg), "fsm", 3, 1)
+    o = oracle.mine(oracle.Csr(hg.off, hg.col, hg.labels), "fsm", 3, 1)
+    assert [tuple(p) for p in r.patterns] == [tuple(p) for p in o["patterns"]]
