@@ -126,8 +126,6 @@ def cpu_sample(hg, app, k, sigma, budget_s, threads):
     the whole workload).  Returns (root_hi or None for all, description)."""
     O = _oracle()
     oc = O.Csr(hg.off, hg.col, hg.labels)
-    if app == "fsm":
-        return None, "full workload"
     probe = 1 << 14
     while True:
         r = O.mine(oc, app, k, sigma, threads=threads, root_lo=0, root_hi=probe)

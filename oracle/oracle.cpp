@@ -661,7 +661,7 @@ static int pid_of(const ReduceState& RS, const Graph& g, const EEmb& E) {
   return RS.qinfo.at(quick_key(g, E)).first;
 }
 
-FResult mine_fsm(const Graph& g, int k, u64 sigma) {
+FResult mine_fsm(const Graph& g, int k, u64 sigma, u64 root_lo = 0, u64 root_hi = ~u64(0)) {
   if (g.lab.empty()) throw std::runtime_error("fsm: graph is unlabeled");
   if (g.oriented) throw std::runtime_error("fsm: graph must be undirected");
   if (k < 2 || k > 6) throw std::runtime_error("fsm: k must be in [2,6]");
@@ -677,6 +677,16 @@ FResult mine_fsm(const Graph& g, int k, u64 sigma) {
       L[0].vid.push_back(v);
       L[0].his.push_back(0);
     }
+  // optional level-1 slice (bounded CPU samples / partition tests)
+  root_hi = std::min<u64>(root_hi, L[0].size());
+  root_lo = std::min(root_lo, root_hi);
+  if (root_lo > 0 || root_hi < L[0].size()) {
+    ELevel S;
+    S.idx.assign(L[0].idx.begin() + root_lo, L[0].idx.begin() + root_hi);
+    S.vid.assign(L[0].vid.begin() + root_lo, L[0].vid.begin() + root_hi);
+    S.his.assign(root_hi - root_lo, 0);
+    L[0] = std::move(S);
+  }
   R.st.level_sizes[0] = L[0].size();
   const int nthr = omp_get_max_threads();
 
@@ -887,7 +897,7 @@ char* oracle_mine_json(const std::uint64_t* off, const std::uint32_t* col, const
     auto t0 = std::chrono::steady_clock::now();
     double ms = 0;
     if (app == orc::FSM) {
-      auto R = orc::mine_fsm(g, k, min_support);
+      auto R = orc::mine_fsm(g, k, min_support, root_lo, root_hi);
       ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       std::sort(R.patterns.begin(), R.patterns.end(), [](const orc::FSMPattern& a, const orc::FSMPattern& b) {
         if (a.level != b.level) return a.level < b.level;

@@ -1,6 +1,7 @@
 // api.cu — C ABI: mine(), results, stats, errors (include/gpm.h).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -124,9 +125,12 @@ int gpm_mine(const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
     S.launches = tl.launches;
     S.chunks = st.chunks;
     std::map<std::string, std::pair<double, double>> per;  // name -> (ms, bytes)
+    static const bool trace = std::getenv("GPM_TRACE") != nullptr;
+    if (trace) std::fprintf(stderr, "[gpm] mine app=%d k=%d total %.3f ms, %zu timed launches\n", cfg->app, cfg->k, ms, tl.recs.size());
     for (auto& r : tl.recs) {
       float t = 0;
       GPM_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      if (trace) std::fprintf(stderr, "[gpm]   %-28s %10.3f ms  %12.4g B_alg\n", r.name.c_str(), t, r.bytes);
       per[r.name].first += t;
       per[r.name].second += r.bytes;
       S.ms_extend += t;

@@ -25,6 +25,9 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 
@@ -180,9 +183,15 @@ __device__ __forceinline__ u64 hash64(u64 x) {
   return x;
 }
 
+constexpr int kMaxProbe = 256;
+
+// Insert-or-add with bounded linear probing.  Once the table is flagged as
+// overflowing (load > 1/2 or a probe run > kMaxProbe) inserts stop at once;
+// the host regrows the table and re-runs the pass.
 __device__ __forceinline__ void hash_add(const Hash& H, u64 key, unsigned long long c) {
+  if (*(volatile int*)H.overflow) return;
   u64 h = hash64(key) & H.mask;
-  for (u64 probe = 0; probe <= H.mask; ++probe) {
+  for (int probe = 0; probe < kMaxProbe; ++probe) {
     unsigned long long cur = H.keys[h];
     if (cur == key) {
       atomicAdd(H.counts + h, c);
@@ -208,7 +217,7 @@ __device__ __forceinline__ void hash_add(const Hash& H, u64 key, unsigned long l
 
 __device__ __forceinline__ u64 hash_find(const Hash& H, u64 key) {
   u64 h = hash64(key) & H.mask;
-  for (u64 probe = 0; probe <= H.mask; ++probe) {
+  for (int probe = 0; probe < kMaxProbe; ++probe) {
     unsigned long long cur = H.keys[h];
     if (cur == key) return h;
     if (cur == 0) return ~0ull;
@@ -252,7 +261,12 @@ __device__ __forceinline__ void domain_or(const FsmArgs& a, u64 slot, const u32*
   for (int i = 0; i < cnv; ++i) {
     const u32 cp = (perm >> (3 * i)) & 7u;
     const u32 v = cv[i];
-    atomicOr(base + (u64)cp * a.words + (v >> 5), 1u << (v & 31));
+    u32* wp = base + (u64)cp * a.words + (v >> 5);
+    const u32 bit = 1u << (v & 31);
+    // domains saturate quickly: test before the read-modify-write so most
+    // embeddings cost a cached load instead of an L2 atomic (a stale read only
+    // causes a redundant, still-correct atomicOr)
+    if (!(*wp & bit)) atomicOr(wp, bit);
   }
 }
 
@@ -527,12 +541,22 @@ struct Fsm {
   int LB;
   int sms;
   u64 budget;
+  u64 prev_unique = 1024;
   DBuf<unsigned long long> d_ctr;
 
   Fsm(const gpm_graph& G_, const gpm_config& c_, cudaStream_t s_, Stats& st_, Timeline& tl_, gpm_result& r_)
       : G(G_), cfg(c_), g(G_.view()), s(s_), st(st_), tl(tl_), res(r_) {}
 
   void sync() { GPM_CUDA(cudaStreamSynchronize(s)); }
+  // host-side phase trace (GPM_TRACE=1)
+  void trace(const char* what, double a = 0, double b = 0) {
+    static const bool on = std::getenv("GPM_TRACE") != nullptr;
+    if (!on) return;
+    sync();
+    static auto t0 = std::chrono::steady_clock::now();
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[gpm fsm] %10.1f ms  %-24s %.6g %.6g\n", ms, what, a, b);
+  }
   template <class T>
   T d2h(const T* p) {
     T v;
@@ -593,6 +617,7 @@ struct Fsm {
                                              64, s));
     // occupied slots are the first U entries (empty = ~0 sorts last)
     const u64 U = d2h(R.used.get());
+    trace("canon+sort", (double)U, (double)R.cap);
     std::vector<u64> keys(U), cnts(U);
     if (U) {
       GPM_CUDA(cudaMemcpyAsync(keys.data(), ck2.get(), sizeof(u64) * U, cudaMemcpyDeviceToHost, s));
@@ -661,6 +686,7 @@ struct Fsm {
     if (R.NB)
       GPM_CUDA(cudaMemcpyAsync(R.bs_to_pid.get(), bs_to_pid.data(), sizeof(u32) * R.NB, cudaMemcpyHostToDevice, s));
     sync();  // host vectors above are temporaries
+    trace("group", (double)R.P, (double)R.NB);
   }
 
   // Domain pass in rounds that fit the bitmap budget; MNI; frequent flags.
@@ -679,6 +705,7 @@ struct Fsm {
         run_domain(bm.get(), words, kpos, (u32)lo, (u32)(lo + n));
         // multi-GPU: OR the packed domain bitmaps across ranks (SURVEY §5 route ii)
         exchange_device(cfg, bm.get(), n * kpos * words, 4, 1, s);
+        trace("domain round", (double)lo, (double)n);
         mni_kernel<<<(unsigned)n, 256, 0, s>>>(bm.get(), words, kpos, R.gkeys.get(), R.bs_to_pid.get(), (u32)lo,
                                                (u32)n, mni.get());
         GPM_CUDA(cudaGetLastError());
@@ -727,6 +754,7 @@ struct Fsm {
       if (d2h(R.overflow.get()) == 0) break;
       cap <<= 3;
     }
+    prev_unique = d2h(R.used.get());
     canon_and_group(R);
     domains_and_mni(R, 2, [&](u32* bm, u64 words, int kpos, u32 lo, u32 hi) {
       FsmArgs a = base_args(R);
@@ -846,7 +874,9 @@ struct Fsm {
       a.accepted = accepted.get();
       return a;
     };
-    u64 cap = 1u << 14;
+    // first guess: previous level's distinct quick codes x fan-out, grown x8 on overflow
+    u64 cap = 1u << 16;
+    while (cap < std::min<u64>(u64(1) << 26, 64 * prev_unique)) cap <<= 1;
     for (;;) {
       alloc_hash(R, cap);
       GPM_CUDA(cudaMemsetAsync(accepted.get(), 0, sizeof(unsigned long long), s));
@@ -858,6 +888,8 @@ struct Fsm {
       cap <<= 3;
     }
     u64 acc = d2h(accepted.get());
+    prev_unique = d2h(R.used.get());
+    trace("pass A (qc)", (double)acc, (double)R.cap);
     if (cfg.world > 1 && cfg.exchange) {
       std::vector<u64> v{acc};
       exchange_sum_host(cfg, v, s);
@@ -879,6 +911,7 @@ struct Fsm {
       launch<LEV>(a, kDomain, "fsm_extend_domain", bytes_in);
     });
     record(R, LEV + 1);
+    trace("mni+record", (double)R.P);
     if (last || !nb) return;
     // filter + write survivors (inspection-execution)
     DBuf<u64> cnt(nb + 1, s);
