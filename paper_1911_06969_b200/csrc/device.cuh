@@ -3,7 +3,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -154,6 +157,18 @@ struct Timeline {
   }
   void end(size_t i) { GPM_CUDA(cudaEventRecord(recs[i].b, s)); }
 };
+
+// Host-side phase trace (GPM_TRACE=1): synchronises the stream and prints the
+// wall time since the previous trace point.
+inline void htrace(cudaStream_t s, const char* what) {
+  static const bool on = std::getenv("GPM_TRACE") != nullptr;
+  if (!on) return;
+  cudaStreamSynchronize(s);
+  static auto t0 = std::chrono::steady_clock::now();
+  auto t1 = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[gpm host] %8.3f ms  %s\n", std::chrono::duration<double, std::milli>(t1 - t0).count(), what);
+  t0 = t1;
+}
 
 inline int sm_count() {
   int dev = 0, n = 0;

@@ -54,7 +54,8 @@ struct Stats {
 
 // Level-1 build on the device (embedding_list.hpp:178-192): DAG -> every
 // edge; undirected -> (u,v) with u<v.  idx[i] = first endpoint, vid[i] = second.
-void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl);
+void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl,
+                  const u32** vid_view = nullptr);
 
 // Degree-weighted static split of [0, n1) root units into `world` parts
 // (SURVEY §8e); weight = candidate count of each level-1 entry.

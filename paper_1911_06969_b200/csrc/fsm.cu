@@ -232,6 +232,7 @@ struct FsmArgs {
   const u64* Wp;
   const u32* pidx;
   u64 np, W, B, b_begin, b_end;
+  u64 grab;
   unsigned long long* ctr;
   int LB;
   Hash H;
@@ -337,10 +338,16 @@ __global__ void __launch_bounds__(kThreads) eextend_kernel(FsmArgs a) {
   const int lane = threadIdx.x & 31;
   const DevGraph& g = a.g;
   unsigned long long acc = 0;
+  u64 bgrab = 0, bleft = 0;
   for (;;) {
-    u64 b = 0;
-    if (lane == 0) b = atomicAdd(a.ctr, 1ull) + a.b_begin;
-    b = __shfl_sync(0xffffffffu, b, 0);
+    if (bleft == 0) {  // 4 batches per atomic: one global counter serialises at L2
+      u64 b_ = 0;
+      if (lane == 0) b_ = atomicAdd(a.ctr, (unsigned long long)a.grab) + a.b_begin;
+      bgrab = __shfl_sync(0xffffffffu, b_, 0);
+      bleft = a.grab;
+    }
+    const u64 b = bgrab++;
+    --bleft;
     if (b >= a.b_end) break;
     const u64 j0 = b * a.B;
     const u64 j1 = min(a.W, j0 + a.B);
@@ -812,6 +819,7 @@ struct Fsm {
     occ = std::max(1, occ);
     const u64 nb = a.b_end - a.b_begin;
     u64 blocks = std::max<u64>(1, std::min<u64>((u64)sms * occ, (nb * 32 + kThreads - 1) / kThreads));
+    a.grab = std::max<u64>(1, std::min<u64>(4, nb / (blocks * (kThreads / 32) * 64)));
     GPM_CUDA(cudaMemsetAsync(d_ctr.get(), 0, sizeof(unsigned long long), s));
     size_t ev = tl.begin(std::string(name) + "_L" + std::to_string(LEV), bytes);
     kern<<<(unsigned)blocks, kThreads, 0, s>>>(a);

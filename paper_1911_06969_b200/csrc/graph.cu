@@ -119,6 +119,11 @@ __global__ void l1_fill_kernel(const u64* __restrict__ off, const u32* __restric
   }
 }
 
+__global__ void l1_idx_kernel(const u64* __restrict__ off, u32 n, u32* __restrict__ idx) {
+  for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < n; v += (u64)gridDim.x * blockDim.x)
+    for (u64 e = off[v], ee = off[v + 1]; e < ee; ++e) idx[e] = (u32)v;
+}
+
 __global__ void is_connected_kernel(DevGraph g, const u32* __restrict__ us, const u32* __restrict__ vs, u64 q,
                                     u8* __restrict__ out) {
   u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
@@ -180,19 +185,26 @@ void keep_pool_warm(int device) {
   done[device] = true;
 }
 
-void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl) {
+void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl,
+                  const u32** vid_view) {
   if (g.oriented) {
+    // level 1 of a DAG is the CSR edge range itself: vid aliases col (no copy)
     count = g.m;
     idx.alloc(std::max<u64>(1, g.m), s);
-    vid.alloc(std::max<u64>(1, g.m), s);
-    if (g.m) {
+    if (vid_view) {
+      *vid_view = g.d_col;
+    } else {
+      vid.alloc(std::max<u64>(1, g.m), s);
+      if (g.m) GPM_CUDA(cudaMemcpyAsync(vid.get(), g.d_col, sizeof(u32) * g.m, cudaMemcpyDeviceToDevice, s));
+    }
+    if (g.m && g.n) {
       ++tl.launches;
-      l1_fill_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, g.n, 1, nullptr, idx.get(),
-                                                                   vid.get());
+      l1_idx_kernel<<<grid_for(g.n, 256), 256, 0, s>>>(g.d_off, g.n, idx.get());
       GPM_CUDA(cudaGetLastError());
     }
     return;
   }
+  if (vid_view) *vid_view = nullptr;
   DBuf<u64> pos(g.n + 1, s);
   GPM_CUDA(cudaMemsetAsync(pos.get(), 0, sizeof(u64) * (g.n + 1), s));
   if (g.n) {
@@ -272,16 +284,6 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
     GPM_CUDA(cudaMallocAsync((void**)&out.d_lab, sizeof(u32) * std::max<u32>(1, g.n), s));
     GPM_CUDA(cudaMemcpyAsync(out.d_lab, g.d_lab, sizeof(u32) * g.n, cudaMemcpyDeviceToDevice, s));
   }
-  // max out-degree (for planner heuristics)
-  DBuf<int> bad(1, s);
-  DBuf<u32> md(1, s);
-  GPM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
-  GPM_CUDA(cudaMemsetAsync(md.get(), 0, sizeof(u32), s));
-  if (g.n) {
-    validate_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(out.d_off, out.d_col, g.n, m, bad.get(), md.get());
-    GPM_CUDA(cudaGetLastError());
-  }
-  GPM_CUDA(cudaMemcpyAsync(&out.max_deg, md.get(), sizeof(u32), cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -30,6 +30,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -48,6 +49,13 @@ enum { kCount = 1, kWrite = 2, kFused = 3 };
 
 constexpr int kThreads = 256;
 constexpr u64 kBatch = 2048;  // candidates per warp batch
+
+constexpr u64 kItemGrab = 8;        // root-kernel work items per atomic grab
+constexpr u64 kBatchGrab = 4;       // generic-engine batches per atomic grab
+constexpr u32 kFilterWords = 128;   // 4096-bit per-warp hash filter
+constexpr u32 kFilterMax = 512;     // lists longer than this skip the filter
+
+__device__ __forceinline__ u32 filter_hash(u32 v) { return (v * 0x9E3779B1u) >> 20; }
 
 struct VLevels {
   const u32* idx[kMaxLevels];
@@ -72,8 +80,13 @@ struct ExtendArgs {
   VLevels L;
   const u64* Wp;   // exclusive work prefix over compacted parents, np+1 entries
   const u32* pidx; // compacted parent -> level index
+  // CF/TC on a DAG: per compacted parent, candidate-list begin and packed probe
+  // lists (begin | deg << 40) of emb[0..S-2]; replaces the reconstruct chain
+  const u64* dcbeg;
+  const u64* dq[kMaxLevels];
   u64 np, W, B;    // np = number of parents with non-zero work
   u64 b_begin, b_end;
+  u64 grab;          // batches per atomic grab
   unsigned long long* ctr;
   u64* cnt;          // COUNT: accepted per batch (index b - b_begin)
   const u64* boffs;  // WRITE: exclusive offsets per batch (absolute b)
@@ -128,6 +141,16 @@ struct Cursor {
     cWb = ldg(a.Wp + p);
     cWe = ldg(a.Wp + p + 1);
     parent = ldg(a.pidx + p);
+    if (APP != kAppMC && a.dcbeg) {  // descriptor path: independent loads, no chain
+      pbeg[0] = ldg(a.dcbeg + p);
+#pragma unroll
+      for (int t = 0; t < S - 1; ++t) {
+        const u64 q = ldg(a.dq[t] + p);
+        qbeg[t] = q & ((u64(1) << 40) - 1);
+        qdeg[t] = (u32)(q >> 40);
+      }
+      return;
+    }
     reconstruct<LEV>(a.L, parent, emb);
     const DevGraph& g = a.g;
     if (APP == kAppMC) {
@@ -184,7 +207,9 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
   constexpr int S = LEV + 1;  // parent embedding size
   constexpr int kWords = (int)(kBatch / 32);
   extern __shared__ unsigned long long shist[];
+  __shared__ __align__(16) u32 s_filter[(APP != kAppMC) ? kThreads / 32 : 1][kFilterWords];
   const int lane = threadIdx.x & 31;
+  u32* filt = s_filter[(APP != kAppMC) ? (threadIdx.x >> 5) : 0];
   const DevGraph& g = a.g;
   int nbins = 0;
   if (MODE == kFused && APP == kAppMC) {
@@ -194,10 +219,16 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
   }
   unsigned long long wtotal = 0;
 
+  u64 bgrab = 0, bleft = 0;
   for (;;) {
-    u64 b = 0;
-    if (lane == 0) b = atomicAdd(a.ctr, 1ull) + a.b_begin;
-    b = __shfl_sync(0xffffffffu, b, 0);
+    if (bleft == 0) {
+      u64 b_ = 0;
+      if (lane == 0) b_ = atomicAdd(a.ctr, (unsigned long long)a.grab) + a.b_begin;
+      bgrab = __shfl_sync(0xffffffffu, b_, 0);
+      bleft = a.grab;
+    }
+    const u64 b = bgrab++;
+    --bleft;
     if (b >= a.b_end) break;
     const u64 j0 = b * a.B;
     const u64 j1 = min(a.W, j0 + a.B);
@@ -241,6 +272,8 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
     u32 c = 0;
     u32 myword = 0;
     int it = 0;
+    u64 fkey = ~0ull;  // begin of the root out-list held in the filter
+    bool fok = false;
     u64 P0 = pa;  // compacted parent owning candidate jb
     for (u64 jb = j0; jb < j1; jb += 32, ++it) {
       const u64 j = jb + lane;
@@ -254,14 +287,41 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
       P0 += __popc(starts);
       bool ok = false;
       u32 u = 0, code = 0;
+      if (j < j1) cur.load(a, myp);
+      if (APP != kAppMC) {
+        // warp-shared 4096-bit hash filter of N+(emb[0]) (the root's out-list,
+        // shared by all parents of one root): most rejected candidates cost one
+        // shared-memory load instead of a global binary search
+        const u32 act = __ballot_sync(0xffffffffu, j < j1);
+        const int leader = __ffs(act) - 1;
+        const u64 key = __shfl_sync(0xffffffffu, cur.qbeg[0] | ((u64)cur.qdeg[0] << 40), leader);
+        if (key != fkey) {
+          fkey = key;
+          const u32 d = (u32)(key >> 40);
+          const u64 qb = key & ((u64(1) << 40) - 1);
+          fok = d <= kFilterMax;
+          if (fok) {
+            reinterpret_cast<uint4*>(filt)[lane] = make_uint4(0u, 0u, 0u, 0u);
+            __syncwarp();
+            for (u32 i = lane; i < d; i += 32) {
+              const u32 h = filter_hash(ldg(g.col + qb + i));
+              atomicOr(&filt[h >> 5], 1u << (h & 31));
+            }
+            __syncwarp();
+          }
+        }
+      }
       if (j < j1) {
-        cur.load(a, myp);
         int pos;
         u = cur.candidate(g, j, pos);
         const u32* emb = cur.emb;
         bool inemb = false;
+        // SPEC.md:392.  On the DAG descriptor path every emb[t] precedes u in
+        // the orientation order (u in N+(emb[S-1])), so u cannot be in emb.
+        if (APP == kAppMC || !a.dcbeg) {
 #pragma unroll
-        for (int t = 0; t < S; ++t) inemb |= (emb[t] == u);
+          for (int t = 0; t < S; ++t) inemb |= (emb[t] == u);
+        }
         if (!inemb) {
           if (APP == kAppMC) {
             // is_auto_canonical_vertex + source position
@@ -281,6 +341,10 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
           } else {
             // Listing 3 / TC: connected (directed) to every earlier vertex
             ok = true;
+            if (fok && (cur.qbeg[0] | ((u64)cur.qdeg[0] << 40)) == fkey) {
+              const u32 h = filter_hash(u);
+              ok = (filt[h >> 5] >> (h & 31)) & 1u;
+            }
 #pragma unroll
             for (int t = 0; t < S - 1; ++t)
               if (ok && !contains_sorted(g.col + cur.qbeg[t], cur.qdeg[t], u)) ok = false;
@@ -341,6 +405,241 @@ __global__ void gather_kernel(const u64* __restrict__ w, const u32* __restrict__
     Wp[i] = w[pidx[i]];
 }
 
+template <int LEV>
+__global__ void desc_kernel(DevGraph g, VLevels L, const u32* __restrict__ pidx, u64 nz, u64* __restrict__ cbeg,
+                            ExtendArgs a) {
+  constexpr int S = LEV + 1;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nz; i += (u64)gridDim.x * blockDim.x) {
+    u32 emb[S];
+    reconstruct<LEV>(L, pidx[i], emb);
+    cbeg[i] = ldg(g.off + emb[S - 1]);
+#pragma unroll
+    for (int t = 0; t < S - 1; ++t) {
+      const u64 b = ldg(g.off + emb[t]), e = ldg(g.off + emb[t] + 1);
+      const_cast<u64*>(a.dq[t])[i] = b | ((e - b) << 40);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Root-centric kernel for the first extension of TC / CF on the DAG
+// (Listing 3: parents are level-1 edges (v0, v1); candidates u in N+(v1);
+// to_add = u in N+(v0)).  One warp per root v0: the 32-wide chunk of N+(v0)
+// (the parents) lives in registers/shared memory, an in-register scan of
+// d+(v1) gives the chunk's candidate space, lanes map to parents with one
+// REDUX over start offsets held in shared memory (all 32-bit), and probes hit
+// the warp's hash filter of N+(v0).  Same output order as the generic engine.
+struct RootArgs {
+  DevGraph g;
+  u64 lo, hi;          // level-1 slice (edge indices of the DAG CSR)
+  u32 vlo, vhi;        // roots owning the slice (inclusive)
+  const u64* item_start;  // per root (r - vlo): first work item; nr+1 entries
+  const u32* item_root;   // per item: root (r - vlo)
+  u64 nitems, ibeg, iend; // items processed by this launch: [ibeg, iend)
+  u64 grab;               // items per atomic grab
+  unsigned long long* ctr;
+  u64* cnt;            // COUNT: accepted per item
+  const u64* offs;     // WRITE: exclusive offsets per item (absolute index)
+  u64 out_base;
+  u32* out_idx;
+  u32* out_vid;
+  u32* masks;          // COUNT writes / WRITE reads ballot words (bump-allocated)
+  u64* moff;           // per item: word offset into masks, or ~0 (no masks)
+  unsigned long long* mtop;
+  u64 mcap;
+  unsigned long long* total;  // FUSED
+  unsigned long long* cand;   // candidates streamed (stats)
+};
+
+// work items = (root, 32-parent chunk) so hub roots spread over warps
+__global__ void root_items_kernel(const u64* __restrict__ off, u64 lo, u64 hi, u32 vlo, u32 nr,
+                                  u64* __restrict__ items) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nr; i += (u64)gridDim.x * blockDim.x) {
+    const u32 r = vlo + (u32)i;
+    const u64 eb = max(off[r], lo), ee = min(off[r + 1], hi);
+    items[i] = ee > eb ? (ee - eb + 31) / 32 : 0;
+  }
+}
+
+__global__ void item_root_kernel(const u64* __restrict__ items, u32 nr, u32* __restrict__ item_root) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nr; i += (u64)gridDim.x * blockDim.x)
+    for (u64 t = items[i], te = items[i + 1]; t < te; ++t) item_root[t] = (u32)i;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) root_kernel(RootArgs a) {
+  __shared__ __align__(16) u32 s_filter[kThreads / 32][kFilterWords];
+  __shared__ u64 s_cb[kThreads / 32][32];
+  __shared__ u32 s_ex[kThreads / 32][33];
+  __shared__ u32 s_ei[kThreads / 32][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  u32* filt = s_filter[wid];
+  u64* scb = s_cb[wid];
+  u32* sex = s_ex[wid];
+  u32* sei = s_ei[wid];
+  const DevGraph& g = a.g;
+  unsigned long long acc_total = 0, acc_cand = 0;
+  u32 froot = 0xffffffffu;  // root whose out-list is in the filter
+  u64 grab = 0, grab_left = 0;
+  for (;;) {
+    // one atomic per kItemGrab items: a single global counter serialises at L2
+    if (grab_left == 0) {
+      u64 it_ = 0;
+      if (lane == 0) it_ = atomicAdd(a.ctr, (unsigned long long)a.grab) + a.ibeg;
+      grab = __shfl_sync(0xffffffffu, it_, 0);
+      grab_left = a.grab;
+    }
+    const u64 item = grab++;
+    --grab_left;
+    if (item >= a.iend) break;
+    u64 wpos = 0, mo = ~0ull;
+    if (MODE == kWrite) {
+      wpos = ldg(a.offs + item);
+      if (ldg(a.offs + item + 1) == wpos) continue;
+      wpos -= a.out_base;
+      mo = ldg(a.moff + item);
+    }
+    // root owning the item
+    const u32 rr = ldg(a.item_root + item);
+    const u32 r = a.vlo + rr;
+    const u64 ob = ldg(g.off + r), oe = ldg(g.off + r + 1);
+    const u64 eb = max(ob, a.lo), ee = min(oe, a.hi);
+    const u64 c0 = eb + 32 * (item - ldg(a.item_start + rr));
+    const u32 d0 = (u32)(oe - ob);
+    const bool use_filter = d0 <= kFilterMax;
+    const bool from_masks = (MODE == kWrite) && mo != ~0ull;
+    if (use_filter && !from_masks && r != froot) {
+      froot = r;
+      reinterpret_cast<uint4*>(filt)[lane] = make_uint4(0u, 0u, 0u, 0u);
+      __syncwarp();
+      for (u32 i = lane; i < d0; i += 32) {
+        const u32 h = filter_hash(ldg(g.col + ob + i));
+        atomicOr(&filt[h >> 5], 1u << (h & 31));
+      }
+      __syncwarp();
+    }
+    // the item's 32 parents (v0, v1): candidate lists N+(v1)
+    const u64 e = c0 + lane;
+    const bool valid = e < ee;
+    u64 cb = 0;
+    u32 w = 0;
+    if (valid) {
+      const u32 v1 = ldg(g.col + e);
+      cb = ldg(g.off + v1);
+      w = (u32)(ldg(g.off + v1 + 1) - cb);
+    }
+    u32 incl = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+    if (MODE != kWrite) acc_cand += total;
+    if (total == 0) {
+      if (MODE == kCount && lane == 0) {
+        a.cnt[item] = 0;
+        a.moff[item] = ~0ull;
+      }
+      continue;
+    }
+    const u32 nzmask = __ballot_sync(0xffffffffu, w > 0);
+    const u32 rank = __popc(nzmask & lanemask_lt());
+    if (w > 0) {
+      scb[rank] = cb;
+      sex[rank] = incl - w;
+      sei[rank] = (u32)(e - a.lo);
+    }
+    const u32 nnz = __popc(nzmask);
+    __syncwarp();
+    const u32 nwords = (total + 31) / 32;
+    if (MODE == kCount) {
+      u64 m = ~0ull;
+      if (lane == 0 && a.masks) {
+        const unsigned long long t = atomicAdd(a.mtop, (unsigned long long)nwords);
+        if (t + nwords <= a.mcap) m = t;
+      }
+      mo = __shfl_sync(0xffffffffu, m, 0);
+    }
+    u32 P = 0, c = 0, myword = 0;
+    u32 wi = 0;
+    for (u32 jb = 0; jb < total; jb += 32, ++wi) {
+      const u32 j = jb + lane;
+      const u32 x = (P + 1 + lane < nnz) ? sex[P + 1 + lane] : 0xffffffffu;
+      const u32 bit = (x - jb < 32u) ? (1u << (x - jb)) : 0u;
+      const u32 starts = __reduce_or_sync(0xffffffffu, bit);
+      const u32 myp = P + __popc(starts & (lanemask_lt() | (1u << lane)));
+      P += __popc(starts);
+      if (from_masks) {
+        const u32 m = ldg(a.masks + mo + wi);
+        if (m) {
+          if (m >> lane & 1u) {
+            const u64 o = wpos + __popc(m & lanemask_lt());
+            a.out_idx[o] = sei[myp];
+            a.out_vid[o] = ldg(g.col + scb[myp] + (j - sex[myp]));
+          }
+          wpos += __popc(m);
+        }
+        continue;
+      }
+      bool ok = false;
+      u32 u = 0;
+      if (j < total) {
+        u = ldg(g.col + scb[myp] + (j - sex[myp]));
+        if (use_filter) {
+          const u32 h = filter_hash(u);
+          ok = (filt[h >> 5] >> (h & 31)) & 1u;
+          if (ok) ok = contains_sorted(g.col + ob, d0, u);
+        } else {
+          ok = contains_sorted(g.col + ob, d0, u);
+        }
+      }
+      const u32 mask = __ballot_sync(0xffffffffu, ok);
+      if (MODE == kWrite) {
+        if (ok) {
+          const u64 o = wpos + __popc(mask & lanemask_lt());
+          a.out_idx[o] = sei[myp];
+          a.out_vid[o] = u;
+        }
+        wpos += __popc(mask);
+      } else {
+        c += __popc(mask);
+        if (MODE == kCount && mo != ~0ull) {
+          if ((wi & 31) == (u32)lane) myword = mask;
+          if ((wi & 31) == 31) a.masks[mo + (wi - 31) + lane] = myword;
+        }
+      }
+    }
+    if (MODE == kCount) {
+      if (mo != ~0ull && (wi & 31) != 0 && (u32)lane < (wi & 31)) a.masks[mo + (wi & ~31u) + lane] = myword;
+      if (lane == 0) {
+        a.cnt[item] = c;
+        a.moff[item] = mo;
+      }
+    }
+    if (MODE == kFused) acc_total += c;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (MODE == kFused && acc_total) atomicAdd(a.total, acc_total);
+    if (MODE != kWrite && acc_cand) atomicAdd(a.cand, acc_cand);
+  }
+}
+
+__global__ void edge_source_kernel(const u64* __restrict__ off, u32 n, u64 e0, u64 e1, u32* __restrict__ out) {
+  // out[0] = vertex owning edge e0, out[1] = vertex owning edge e1
+  const int t = threadIdx.x;
+  if (t > 1) return;
+  const u64 e = t == 0 ? e0 : e1;
+  u64 lo = 0, hi = n;  // last v with off[v] <= e
+  while (lo < hi) {
+    u64 mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  out[t] = (u32)lo;
+}
+
 // Canonical code of every connectivity mask over k positions (reduce step 2:
 // canonicalize once per quick pattern).
 __global__ void canon_masks_kernel(int k, u64* __restrict__ keys) {
@@ -379,6 +678,7 @@ void launch_extend(Ctx& c, ExtendArgs& a, const char* what, double bytes) {
   const u64 warps_needed = nb;
   u64 blocks = std::min<u64>((u64)c.sms * occ, (warps_needed * 32 + kThreads - 1) / kThreads);
   blocks = std::max<u64>(1, blocks);
+  a.grab = std::max<u64>(1, std::min<u64>(kBatchGrab, nb / (blocks * (kThreads / 32) * 64)));
   GPM_CUDA(cudaMemsetAsync(c.d_ctr, 0, sizeof(unsigned long long), c.s));
   a.ctr = c.d_ctr;
   size_t ev = c.tl->begin(std::string(what) + "_L" + std::to_string(LEV), bytes);
@@ -452,6 +752,7 @@ void process(Ctx& c, VLevels L, u64 np) {
   st.candidates[LEV] += W;
   const double bytes_in = 8.0 * LEV * np + 16.0 * NPOS * np + 4.0 * W;
   st.balg += bytes_in;
+  htrace(c.s, "generic: work+select+scan");
   if (W == 0) return;
   const u64 nb = (W + kBatch - 1) / kBatch;
   ExtendArgs a{};
@@ -461,6 +762,17 @@ void process(Ctx& c, VLevels L, u64 np) {
   a.pidx = pidx.get();
   a.np = nz;
   a.W = W;
+  DBuf<u64> dcbeg, dq;
+  if (APP != kAppMC && c.g.oriented && c.G->m < (u64(1) << 40)) {
+    dcbeg.alloc(nz, c.s);
+    dq.alloc(nz * (S - 1), c.s);
+    for (int t = 0; t < S - 1; ++t) a.dq[t] = dq.get() + (u64)t * nz;
+    a.dcbeg = dcbeg.get();
+    desc_kernel<LEV><<<(unsigned)std::min<u64>((nz + 255) / 256, 1u << 20), 256, 0, c.s>>>(c.g, L, pidx.get(), nz,
+                                                                                       dcbeg.get(), a);
+    GPM_CUDA(cudaGetLastError());
+    ++c.tl->launches;
+  }
   a.B = kBatch;
   a.b_begin = 0;
   a.b_end = nb;
@@ -469,6 +781,7 @@ void process(Ctx& c, VLevels L, u64 np) {
     a.hist = c.d_hist;
     a.total = c.d_total;
     launch_extend<APP, LEV, kFused>(c, a, "extend_fused", bytes_in);
+    htrace(c.s, "generic: fused");
     return;
   }
   // ---- inspection: children per batch
@@ -536,9 +849,152 @@ void process(Ctx& c, VLevels L, u64 np) {
   }
 }
 
+template <int MODE>
+void launch_root(Ctx& c, RootArgs& a, const char* what, double bytes) {
+  auto kern = root_kernel<MODE>;
+  static int occ = 0;
+  if (occ == 0) {
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
+    occ = std::max(1, occ);
+  }
+  const u64 ni = a.iend - a.ibeg;
+  u64 blocks = std::max<u64>(1, std::min<u64>((u64)c.sms * occ, (ni * 32 + kThreads - 1) / kThreads));
+  // coarse grabs only when every warp gets many items (tail balance first)
+  a.grab = std::max<u64>(1, std::min<u64>(kItemGrab, ni / (blocks * (kThreads / 32) * 64)));
+  GPM_CUDA(cudaMemsetAsync(c.d_ctr, 0, sizeof(unsigned long long), c.s));
+  a.ctr = c.d_ctr;
+  size_t ev = c.tl->begin(what, bytes);
+  kern<<<(unsigned)blocks, kThreads, 0, c.s>>>(a);
+  GPM_CUDA(cudaGetLastError());
+  c.tl->end(ev);
+  ++c.tl->launches;
+}
+
+// First extension of TC/CF on a DAG through the root-centric kernel; deeper
+// levels continue in the generic engine.
+void process_root_cf(Ctx& c, const VLevels& L, u64 lo, u64 hi) {
+  Stats& st = *c.st;
+  const u64 np = hi - lo;
+  if (np == 0) return;
+  const bool last = (c.k == 3);
+  DBuf<u32> vv(2, c.s);
+  edge_source_kernel<<<1, 32, 0, c.s>>>(c.G->d_off, c.G->n, lo, hi - 1, vv.get());
+  GPM_CUDA(cudaGetLastError());
+  u32 vr[2];
+  GPM_CUDA(cudaMemcpyAsync(vr, vv.get(), sizeof vr, cudaMemcpyDeviceToHost, c.s));
+  GPM_CUDA(cudaStreamSynchronize(c.s));
+  const u32 nr = vr[1] - vr[0] + 1;
+  DBuf<u64> items(nr + 1, c.s);
+  GPM_CUDA(cudaMemsetAsync(items.get() + nr, 0, sizeof(u64), c.s));
+  root_items_kernel<<<(unsigned)std::min<u64>((nr + 255) / 256, 1u << 20), 256, 0, c.s>>>(c.G->d_off, lo, hi, vr[0],
+                                                                                       nr, items.get());
+  GPM_CUDA(cudaGetLastError());
+  c.tl->launches += 2;
+  scan_inplace(items.get(), nr + 1, c.s);
+  DBuf<unsigned long long> cand(1, c.s);
+  GPM_CUDA(cudaMemsetAsync(cand.get(), 0, sizeof(unsigned long long), c.s));
+  u64 NI = 0;
+  GPM_CUDA(cudaMemcpyAsync(&NI, items.get() + nr, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+  GPM_CUDA(cudaStreamSynchronize(c.s));
+  DBuf<u32> iroot(std::max<u64>(1, NI), c.s);
+  item_root_kernel<<<(unsigned)std::min<u64>((nr + 255) / 256, 1u << 20), 256, 0, c.s>>>(items.get(), nr, iroot.get());
+  GPM_CUDA(cudaGetLastError());
+  ++c.tl->launches;
+  RootArgs a{};
+  a.g = c.g;
+  a.lo = lo;
+  a.hi = hi;
+  a.vlo = vr[0];
+  a.vhi = vr[1];
+  a.item_start = items.get();
+  a.item_root = iroot.get();
+  a.nitems = NI;
+  a.ibeg = 0;
+  a.iend = NI;
+  a.cand = cand.get();
+  if (last) {
+    a.total = c.d_total;
+    size_t rec = c.tl->recs.size();
+    launch_root<kFused>(c, a, "extend_fused_L1", 0.0);
+    unsigned long long W = 0;
+    GPM_CUDA(cudaMemcpyAsync(&W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, c.s));
+    GPM_CUDA(cudaStreamSynchronize(c.s));
+    const double bytes = 8.0 * np + 16.0 * np + 4.0 * W;
+    c.tl->recs[rec].bytes = bytes;
+    st.candidates[1] += W;
+    st.balg += bytes;
+    return;
+  }
+  DBuf<u64> cnt(NI + 1, c.s), moff(NI + 1, c.s);
+  GPM_CUDA(cudaMemsetAsync(cnt.get() + NI, 0, sizeof(u64), c.s));
+  // ballot masks: 1 bit per candidate, bump-allocated per item
+  const u64 mcap = std::max<u64>(1, std::min<u64>(c.mask_budget / 4, u64(1) << 28));
+  DBuf<u32> masks(mcap, c.s);
+  DBuf<unsigned long long> mtop(1, c.s);
+  GPM_CUDA(cudaMemsetAsync(mtop.get(), 0, sizeof(unsigned long long), c.s));
+  a.cnt = cnt.get();
+  a.moff = moff.get();
+  a.masks = masks.get();
+  a.mtop = mtop.get();
+  a.mcap = mcap;
+  size_t rec = c.tl->recs.size();
+  launch_root<kCount>(c, a, "extend_count_L1", 0.0);
+  scan_inplace(cnt.get(), NI + 1, c.s);
+  unsigned long long W = 0;
+  u64 T = 0;
+  GPM_CUDA(cudaMemcpyAsync(&W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, c.s));
+  GPM_CUDA(cudaMemcpyAsync(&T, cnt.get() + NI, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+  GPM_CUDA(cudaStreamSynchronize(c.s));
+  const double bytes_in = 8.0 * np + 16.0 * np + 4.0 * W;
+  c.tl->recs[rec].bytes = bytes_in;
+  st.candidates[1] += W;
+  st.balg += bytes_in + 8.0 * T;
+  st.level_sizes[1] += T;
+  if (T == 0) return;
+  std::vector<std::pair<u64, u64>> chunks;  // item ranges
+  if (T <= c.cap_entries) {
+    chunks.emplace_back(0, NI);
+  } else {
+    std::vector<u64> h(NI + 1);
+    GPM_CUDA(cudaMemcpyAsync(h.data(), cnt.get(), sizeof(u64) * (NI + 1), cudaMemcpyDeviceToHost, c.s));
+    GPM_CUDA(cudaStreamSynchronize(c.s));
+    u64 r0 = 0;
+    while (r0 < NI) {
+      u64 key = h[r0] + c.cap_entries;
+      u64 r1 = (u64)(std::upper_bound(h.begin() + r0 + 1, h.end(), key) - h.begin()) - 1;
+      if (r1 <= r0) r1 = r0 + 1;
+      chunks.emplace_back(r0, r1);
+      r0 = r1;
+    }
+  }
+  st.chunks += chunks.size() - 1;
+  for (auto [r0, r1] : chunks) {
+    u64 base = 0, end = 0;
+    GPM_CUDA(cudaMemcpyAsync(&base, cnt.get() + r0, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+    GPM_CUDA(cudaMemcpyAsync(&end, cnt.get() + r1, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+    GPM_CUDA(cudaStreamSynchronize(c.s));
+    const u64 Tc = end - base;
+    if (Tc == 0) continue;
+    DBuf<u32> oi(Tc, c.s), ov(Tc, c.s);
+    RootArgs w = a;
+    w.ibeg = r0;
+    w.iend = r1;
+    w.offs = cnt.get();
+    w.out_base = base;
+    w.out_idx = oi.get();
+    w.out_vid = ov.get();
+    const double frac = (double)(r1 - r0) / (double)NI;
+    launch_root<kWrite>(c, w, "extend_write_L1", frac * (double)W / 8.0 + 24.0 * Tc);
+    htrace(c.s, "root: write");
+    VLevels nl = L;
+    nl.idx[1] = oi.get();
+    nl.vid[1] = ov.get();
+    process_dispatch<kAppCF>(c, 2, nl, Tc);
+  }
+}
+
 }  // namespace
 
-void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl);
 
 void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm_result& res, Stats& st,
                  Timeline& tl) {
@@ -564,18 +1020,22 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
 
   const int levels = k - 1;
   st.ensure(levels);
+  htrace(s, "mine_vertex: start (orient done)");
   DBuf<u32> l1i, l1v;
   u64 n1 = 0;
-  build_level1(*G, l1i, l1v, n1, s, tl);
+  const u32* l1vid = nullptr;
+  build_level1(*G, l1i, l1v, n1, s, tl, &l1vid);
+  if (!l1vid) l1vid = l1v.get();
   u64 lo = 0, hi = n1;
   if (cfg.root_hi > 0) {
     lo = std::min(cfg.root_lo, n1);
     hi = std::min(cfg.root_hi, n1);
     if (hi < lo) hi = lo;
   } else {
-    root_split(*G, l1i.get(), l1v.get(), n1, app, cfg.rank, std::max(1, cfg.world), lo, hi, s, tl);
+    root_split(*G, l1i.get(), l1vid, n1, app, cfg.rank, std::max(1, cfg.world), lo, hi, s, tl);
   }
   const u64 nroot = hi - lo;
+  htrace(s, "level1 built");
   if (nroot >= (u64(1) << 32)) throw Error(GPM_EINVAL, "level 1 exceeds 2^32 entries");
   st.level_sizes[0] = nroot;
 
@@ -602,18 +1062,22 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   c.d_hist = d_hist.get();
   c.d_ctr = d_ctr.get();
 
+  htrace(s, "setup (meminfo, counters)");
   VLevels L{};
   L.idx[0] = l1i.get() + lo;
-  L.vid[0] = l1v.get() + lo;
+  L.vid[0] = l1vid + lo;
   const int appk = (app == GPM_APP_MC) ? kAppMC : kAppCF;  // TC == CF with k=3 (Listing 3)
   if (k == 2 || nroot == 0) {
     res.total = (k == 2) ? nroot : 0;
   } else if (appk == kAppMC) {
     process_dispatch<kAppMC>(c, 1, L, nroot);
+  } else if (G->oriented && !std::getenv("GPM_GENERIC_L1")) {
+    process_root_cf(c, L, lo, hi);
   } else {
     process_dispatch<kAppCF>(c, 1, L, nroot);
   }
 
+  htrace(s, "levels processed");
   // multi-GPU: the only collectives are the per-pattern counts and the
   // per-level size vectors
   if (cfg.world > 1 && cfg.exchange) {
