@@ -262,7 +262,8 @@ def main():
     for i in range(1 + args.steps):
         barrier()
         t = time.perf_counter()
-        g = P.Graph(pinned, device=local)
+        # TC/CF need the degree-ordered DAG: fused pipelined upload + orientation
+        g = P.Graph(pinned, device=local, orient=app in ("tc", "cf"))
         er = P.mine(g, app, k, sigma, rank=rank, world=world, exchange=exchange)
         del g
         torch.cuda.synchronize()

@@ -75,6 +75,13 @@ void gpm_config_default(gpm_config* cfg);
 int gpm_graph_create_csr(const uint64_t* row_offsets, const uint32_t* col, const uint32_t* labels, uint32_t n,
                          uint64_t m, int oriented, int device, gpm_graph** out);
 
+/* Graph ctor + orient_dag fused (graph.hpp:29-55, :121-132): uploads an
+ * UNDIRECTED host CSR and returns the degree-ordered DAG, overlapping the
+ * chunked host->device copy with validation and orientation on the device.
+ * Same result as gpm_graph_create_csr followed by gpm_graph_orient_dag. */
+int gpm_graph_create_dag_csr(const uint64_t* row_offsets, const uint32_t* col, const uint32_t* labels, uint32_t n,
+                             uint64_t m, int device, gpm_graph** out);
+
 /* orient_dag (graph.hpp:121-132): keep u->v iff (deg u, u) < (deg v, v); runs
  * on the device.  Errors if already oriented. */
 int gpm_graph_orient_dag(const gpm_graph* g, gpm_graph** out);

@@ -18,7 +18,7 @@ APP_TC, APP_CF, APP_MC, APP_FSM = range(4)
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_void_p)
 
 EXPORTS = [
-    "gpm_config_default", "gpm_graph_create_csr", "gpm_graph_orient_dag", "gpm_graph_info", "gpm_graph_download",
+    "gpm_config_default", "gpm_graph_create_csr", "gpm_graph_create_dag_csr", "gpm_graph_orient_dag", "gpm_graph_info", "gpm_graph_download",
     "gpm_graph_is_connected", "gpm_level1", "gpm_graph_free", "gpm_mine", "gpm_result_total",
     "gpm_result_num_patterns", "gpm_result_pattern", "gpm_result_stats", "gpm_result_free",
     "gpm_load_edge_list", "gpm_load_labeled_graph", "gpm_csr_from_edges", "gpm_generate_rmat", "gpm_csr_free",
@@ -73,6 +73,7 @@ def lib():
     sig = {
         "gpm_config_default": (None, [C.POINTER(Config)]),
         "gpm_graph_create_csr": (i32, [vp, vp, vp, u32, u64, i32, i32, C.POINTER(vp)]),
+        "gpm_graph_create_dag_csr": (i32, [vp, vp, vp, u32, u64, i32, C.POINTER(vp)]),
         "gpm_graph_orient_dag": (i32, [vp, C.POINTER(vp)]),
         "gpm_graph_info": (i32, [vp, C.POINTER(u32), C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]),
         "gpm_graph_download": (i32, [vp, vp, vp]),

@@ -107,10 +107,19 @@ class Graph:
     """Immutable device CSR (one per GPU; "safe for unrestricted
     concurrent reads")."""
 
-    def __init__(self, host: HostGraph = None, device: int = 0, *, _handle=None):
+    def __init__(self, host: HostGraph = None, device: int = 0, *, orient: bool = False, _handle=None):
+        """Uploads `host`.  orient=True returns the degree-ordered DAG directly
+        (pipelined upload + orientation, == Graph(host).orient_dag())."""
         L = lib()
         if _handle is not None:
             self._h = _handle
+        elif orient:
+            off = np.ascontiguousarray(host.off, dtype=np.uint64)
+            col = np.ascontiguousarray(host.col, dtype=np.uint32)
+            lab = None if host.labels is None else np.ascontiguousarray(host.labels, dtype=np.uint32)
+            h = C.c_void_p()
+            check(L.gpm_graph_create_dag_csr(_p(off), _p(col), _p(lab), host.n, host.m, device, C.byref(h)))
+            self._h = h
         else:
             off = np.ascontiguousarray(host.off, dtype=np.uint64)
             col = np.ascontiguousarray(host.col, dtype=np.uint32)

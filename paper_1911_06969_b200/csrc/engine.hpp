@@ -66,6 +66,7 @@ void keep_pool_warm(int device);
 
 // Device orientation (graph.hpp:121-132).
 void orient_on_device(const gpm_graph& g, gpm_graph& out);
+void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels, u32 n, u64 m, gpm_graph& out);
 
 void mine_vertex(const gpm_graph& g, const gpm_config& cfg, cudaStream_t s, gpm_result& res, Stats& st, Timeline& tl);
 void mine_fsm(const gpm_graph& g, const gpm_config& cfg, cudaStream_t s, gpm_result& res, Stats& st, Timeline& tl);

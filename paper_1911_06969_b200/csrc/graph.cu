@@ -87,6 +87,65 @@ __global__ void orient_kernel(const u64* __restrict__ off, const u32* __restrict
   }
 }
 
+// Orientation pass 1 over vertices [vb, ve): optional validation (graph.hpp:
+// 29-55), out-degree in the (deg, id) order, and a keep flag per half-edge so
+// pass 2 needs no second degree gather.
+__global__ void orient_count_kernel(const u64* __restrict__ off, const u32* __restrict__ col, u32 n, u64 m, u32 vb,
+                                    u32 ve, int validate, u64* __restrict__ cnt, u8* __restrict__ keep,
+                                    int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+  const u64 nwarps = (gridDim.x * (u64)blockDim.x) >> 5;
+  int mybad = 0;
+  for (u64 uu = vb + warp; uu < ve; uu += nwarps) {
+    const u32 u = (u32)uu;
+    const u64 b = off[u], e = off[u + 1];
+    if (e < b || e > m) {
+      mybad |= 1;
+      if (lane == 0) cnt[u] = 0;
+      continue;
+    }
+    const u64 du = e - b;
+    u64 c = 0;
+    for (u64 i0 = b; i0 < e; i0 += 32) {
+      const u64 i = i0 + lane;
+      bool k = false;
+      if (i < e) {
+        const u32 v = col[i];
+        if (validate && !(v < n && v != u && (i == b || col[i - 1] < v))) mybad |= 2;
+        if (v < n) {
+          const u64 dv = off[v + 1] - off[v];
+          k = du != dv ? du < dv : u < v;
+        }
+        keep[i] = k ? 1 : 0;
+      }
+      c += __popc(__ballot_sync(0xffffffffu, k));
+    }
+    if (lane == 0) cnt[u] = c;
+  }
+  mybad = (int)__reduce_or_sync(0xffffffffu, (unsigned)mybad);
+  if (lane == 0 && mybad) atomicOr(bad, mybad);
+}
+
+__global__ void orient_write_kernel(const u64* __restrict__ off, const u32* __restrict__ col,
+                                    const u8* __restrict__ keep, u32 n, const u64* __restrict__ doff,
+                                    u32* __restrict__ dcol) {
+  const int lane = threadIdx.x & 31;
+  const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+  const u64 nwarps = (gridDim.x * (u64)blockDim.x) >> 5;
+  for (u64 u = warp; u < n; u += nwarps) {
+    const u64 b = off[u], e = off[u + 1];
+    u64 w = doff[u];
+    for (u64 i0 = b; i0 < e; i0 += 32) {
+      const u64 i = i0 + lane;
+      const bool k = i < e && keep[i];
+      const u32 mask = __ballot_sync(0xffffffffu, k);
+      if (k) dcol[w + __popc(mask & lanemask_lt())] = col[i];
+      w += __popc(mask);
+    }
+  }
+}
+
 // level 1 of an undirected graph: per vertex, entries v > u (u<v rule).
 __global__ void l1_count_kernel(const u64* __restrict__ off, const u32* __restrict__ col, u32 n,
                                 u64* __restrict__ cnt) {
@@ -262,12 +321,15 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
   out.labeled = g.labeled;
   out.label_values = g.label_values;
   out.label_bits = g.label_bits;
+  GPM_CUDA(cudaStreamSynchronize(g.stream));  // source graph ordered before our stream
   GPM_CUDA(cudaMallocAsync((void**)&out.d_off, sizeof(u64) * (g.n + 1), s));
-  GPM_CUDA(cudaMemsetAsync(out.d_off, 0, sizeof(u64) * (g.n + 1), s));
-  // the source graph lives on g.stream; order it before our stream
-  GPM_CUDA(cudaStreamSynchronize(g.stream));
+  GPM_CUDA(cudaMemsetAsync(out.d_off + g.n, 0, sizeof(u64), s));
+  DBuf<u8> keep(std::max<u64>(1, g.m), s);
+  DBuf<int> bad(1, s);
+  GPM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
   if (g.n) {
-    orient_kernel<false><<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, g.n, out.d_off, nullptr);
+    orient_count_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, g.n, g.m, 0, g.n, 0,
+                                                                    out.d_off, keep.get(), bad.get());
     GPM_CUDA(cudaGetLastError());
   }
   exclusive_scan_u64(out.d_off, g.n + 1, s);
@@ -277,12 +339,83 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
   out.m = m;
   GPM_CUDA(cudaMallocAsync((void**)&out.d_col, sizeof(u32) * std::max<u64>(1, m), s));
   if (g.n && m) {
-    orient_kernel<true><<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, g.n, out.d_off, out.d_col);
+    orient_write_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, keep.get(), g.n, out.d_off,
+                                                                    out.d_col);
     GPM_CUDA(cudaGetLastError());
   }
   if (g.labeled) {
     GPM_CUDA(cudaMallocAsync((void**)&out.d_lab, sizeof(u32) * std::max<u32>(1, g.n), s));
     GPM_CUDA(cudaMemcpyAsync(out.d_lab, g.d_lab, sizeof(u32) * g.n, cudaMemcpyDeviceToDevice, s));
+  }
+  GPM_CUDA(cudaStreamSynchronize(s));
+}
+
+// Host CSR -> device DAG in one pipelined call: the column array is copied in
+// vertex-range chunks on a copy stream while a compute stream validates and
+// counts the orientation of every chunk that has landed (graph.hpp:29-55 +
+// :121-132).  The undirected copy is dropped afterwards.
+void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels, u32 n, u64 m, gpm_graph& out) {
+  cudaStream_t s = out.stream;
+  cudaStream_t cs;
+  GPM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t x;
+    ~StreamGuard() { cudaStreamSynchronize(x); cudaStreamDestroy(x); }
+  } guard{cs};
+  DBuf<u64> uoff(n + 1, s);
+  DBuf<u32> ucol(std::max<u64>(1, m), s);
+  DBuf<u8> keep(std::max<u64>(1, m), s);
+  DBuf<int> bad(1, s);
+  GPM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+  GPM_CUDA(cudaMallocAsync((void**)&out.d_off, sizeof(u64) * (n + 1), s));
+  GPM_CUDA(cudaMemsetAsync(out.d_off + n, 0, sizeof(u64), s));
+  cudaEvent_t ready;
+  GPM_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  GPM_CUDA(cudaEventRecord(ready, s));  // allocations visible to the copy stream
+  GPM_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+  GPM_CUDA(cudaMemcpyAsync(uoff.get(), h_off, sizeof(u64) * (n + 1), cudaMemcpyHostToDevice, cs));
+  const int K = m > (u64(1) << 22) ? 8 : 1;
+  std::vector<cudaEvent_t> evs;
+  u32 vb = 0;
+  for (int k = 0; k < K && vb < n; ++k) {
+    // vertex range whose edges end near (k+1)/K of m
+    const u64 target = (k == K - 1) ? m : m / K * (k + 1);
+    const u32 ve = (k == K - 1) ? n : (u32)(std::upper_bound(h_off, h_off + n + 1, target) - h_off - 1);
+    const u32 vend = std::max(ve, vb + 1 <= n ? vb + 1 : n);
+    const u64 eb = h_off[vb], ee = h_off[vend];
+    if (ee > eb)
+      GPM_CUDA(cudaMemcpyAsync(ucol.get() + eb, h_col + eb, sizeof(u32) * (ee - eb), cudaMemcpyHostToDevice, cs));
+    cudaEvent_t ev;
+    GPM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    GPM_CUDA(cudaEventRecord(ev, cs));
+    evs.push_back(ev);
+    GPM_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    orient_count_kernel<<<grid_for((u64)(vend - vb) * 32, 256), 256, 0, s>>>(uoff.get(), ucol.get(), n, m, vb, vend, 1,
+                                                                            out.d_off, keep.get(), bad.get());
+    GPM_CUDA(cudaGetLastError());
+    vb = vend;
+  }
+  if (labels) {
+    GPM_CUDA(cudaMallocAsync((void**)&out.d_lab, sizeof(u32) * std::max<u32>(1, n), s));
+  }
+  exclusive_scan_u64(out.d_off, n + 1, s);
+  u64 dm = 0;
+  int hb = 0;
+  GPM_CUDA(cudaMemcpyAsync(&dm, out.d_off + n, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  for (auto e : evs) cudaEventDestroy(e);
+  cudaEventDestroy(ready);
+  if (hb & 1) throw Error(GPM_EINVAL, "row_offsets not non-decreasing / out of range");
+  if (hb & 2) throw Error(GPM_EINVAL, "neighbor list not strictly ascending, self-loop, or id out of range");
+  out.n = n;
+  out.m = dm;
+  out.oriented = true;
+  GPM_CUDA(cudaMallocAsync((void**)&out.d_col, sizeof(u32) * std::max<u64>(1, dm), s));
+  if (n && dm) {
+    orient_write_kernel<<<grid_for((u64)n * 32, 256), 256, 0, s>>>(uoff.get(), ucol.get(), keep.get(), n, out.d_off,
+                                                                  out.d_col);
+    GPM_CUDA(cudaGetLastError());
   }
   GPM_CUDA(cudaStreamSynchronize(s));
 }
@@ -363,6 +496,49 @@ extern "C" int gpm_graph_create_csr(const uint64_t* row_offsets, const uint32_t*
     GPM_CUDA(cudaStreamSynchronize(s));
     if (hb & 1) throw Error(GPM_EINVAL, "row_offsets not non-decreasing / out of range");
     if (hb & 2) throw Error(GPM_EINVAL, "neighbor list not strictly ascending, self-loop, or id out of range");
+    *out = g.release();
+  });
+}
+
+extern "C" int gpm_graph_create_dag_csr(const uint64_t* row_offsets, const uint32_t* col, const uint32_t* labels,
+                                        uint32_t n, uint64_t m, int device, gpm_graph** out) {
+  if (!out || !row_offsets || (m && !col)) {
+    set_last_error("gpm_graph_create_dag_csr: null argument");
+    return GPM_EINVAL;
+  }
+  *out = nullptr;
+  return guarded([&] {
+    if (row_offsets[0] != 0 || row_offsets[n] != m) throw Error(GPM_EINVAL, "row_offsets must start at 0 and end at m");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw Error(GPM_ECUDA, "no CUDA device visible");
+    }
+    if (device < 0 || device >= ndev) throw Error(GPM_EINVAL, "device index out of range");
+    GPM_CUDA(cudaSetDevice(device));
+    keep_pool_warm(device);
+    auto g = std::make_unique<gpm_graph>();
+    g->device = device;
+    GPM_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    if (labels) {
+      std::vector<u32> vals(labels, labels + n);
+      std::sort(vals.begin(), vals.end());
+      vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+      g->label_values = vals;
+      int lb = 0;
+      while ((u64(1) << lb) < std::max<size_t>(1, vals.size())) ++lb;
+      g->label_bits = lb;
+      g->labeled = true;
+    }
+    create_dag_pipelined(row_offsets, col, labels, n, m, *g);
+    if (labels) {
+      std::vector<u32> ranks(n);
+      for (u32 v = 0; v < n; ++v)
+        ranks[v] = (u32)(std::lower_bound(g->label_values.begin(), g->label_values.end(), labels[v]) -
+                         g->label_values.begin());
+      GPM_CUDA(cudaMemcpyAsync(g->d_lab, ranks.data(), sizeof(u32) * n, cudaMemcpyHostToDevice, g->stream));
+      GPM_CUDA(cudaStreamSynchronize(g->stream));
+    }
     *out = g.release();
   });
 }

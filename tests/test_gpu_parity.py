@@ -162,6 +162,18 @@ def test_is_connected_and_orient(P, oracle):
         P.Graph(hg).orient_dag().orient_dag()
 
 
+def test_create_dag_matches_orient(P, oracle):
+    for hg in (P.generate_rmat(14, 8, 0.57, 0.19, 0.19, seed=2), host(P, oracle, BF.gnp(90, 0.1, 3), 90),
+               P.generate_rmat(12, 4, 0.45, 0.15, 0.15, seed=3, n_labels=5)):
+        a = P.Graph(hg).orient_dag().download()
+        gd = P.Graph(hg, orient=True)
+        b = gd.download()
+        assert gd.oriented and np.array_equal(a.off, b.off) and np.array_equal(a.col, b.col)
+        assert P.triangle_count(gd) == P.triangle_count(P.Graph(hg))
+    with pytest.raises(P.GpmError):
+        P.Graph(P.HostGraph(np.array([0, 2, 2], np.uint64), np.array([1, 1], np.uint32)), orient=True)
+
+
 def test_edge_cases(P, oracle):
     # no edges / isolated vertices / single edge
     empty = P.HostGraph(np.zeros(4, np.uint64), np.zeros(0, np.uint32))

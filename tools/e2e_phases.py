@@ -17,4 +17,7 @@ for it in range(4):
     r, t3 = t(lambda: P.mine(d, a, k))
     _, t4 = t(lambda: (g.__del__(), d.__del__()))
     r2, t5 = t(lambda: P.mine(P.Graph(ph), a, k))
-    print(f"create {t1:.2f}  orient {t2:.2f}  mine {t3:.2f} (dev {r.stats['ms_total']:.2f})  free {t4:.2f} | e2e-one-call {t5:.2f} (dev {r2.stats['ms_total']:.2f})")
+    gd, t6 = t(lambda: P.Graph(ph, orient=True))
+    r3, t7 = t(lambda: P.mine(gd, a, k))
+    del gd
+    print(f"create {t1:.2f}  orient {t2:.2f}  mine {t3:.2f} (dev {r.stats['ms_total']:.2f})  free {t4:.2f} | e2e-one-call {t5:.2f} (dev {r2.stats['ms_total']:.2f}) | create_dag {t6:.2f} + mine {t7:.2f}")
