@@ -84,7 +84,14 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
-    def stop(self):
+    def wait_samples(self, n, timeout=5.0):
+        """Blocks until n samples have arrived (the sampler's first lines lag
+        its start; short timed regions would otherwise see none)."""
+        t = time.time()
+        while self.proc and len(self.lines) < n and time.time() - t < timeout:
+            time.sleep(0.02)
+
+    def stop(self, first=0):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -94,7 +101,7 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[first:]:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -226,6 +233,8 @@ def main():
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
+    clocks.wait_samples(1)
+    n_before = len(clocks.lines)
     step_ms = []
     dom_ms, dom_b, launches = [], [], 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -241,7 +250,13 @@ def main():
         dom_b.append(res.stats["b_dominant"])
         launches += res.stats["launches"]
     barrier()
-    clock_rec = clocks.stop()
+    # a short timed region may fall between two 100 ms samples: keep the GPU
+    # busy with further (untimed) steps until one sample lands after it began
+    t_extra = time.time()
+    while len(clocks.lines) <= n_before + 1 and time.time() - t_extra < 3.0:
+        P.mine(g_in, app, k, sigma, **kw)
+        torch.cuda.synchronize()
+    clock_rec = clocks.stop(first=n_before)
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)

@@ -68,6 +68,46 @@ __device__ __forceinline__ bool has_edge_sym(const DevGraph& g, u32 x, u32 u) {
   return contains_sorted(g.col + bu, (u32)(eu - bu), x);
 }
 
+// Open-addressing set of distinct u32 vertex ids in shared memory (linear
+// probing, multiplicative hash, capacity a power of two >= 2 x keys): the
+// on-chip staging of a source adjacency list.  sh = 32 -
+// log2(capacity).
+constexpr u32 kEmpty = 0xffffffffu;
+constexpr u32 kHashMul = 0x9E3779B1u;
+__device__ __forceinline__ void hs_insert(u32* T, u32 sh, u32 mask, u32 v) {
+  u32 h = (v * kHashMul) >> sh;
+  for (;;) {
+    const u32 old = atomicCAS(T + h, kEmpty, v);
+    if (old == kEmpty || old == v) return;
+    h = (h + 1) & mask;
+  }
+}
+__device__ __forceinline__ bool hs_has(const u32* T, u32 sh, u32 mask, u32 v) {
+  u32 h = (v * kHashMul) >> sh;
+  for (;;) {
+    const u32 x = T[h];
+    if (x == v) return true;
+    if (x == kEmpty) return false;
+    h = (h + 1) & mask;
+  }
+}
+// Warp-collective: stages col[b, b+len) (len <= cap/2) into T with the
+// smallest power-of-two capacity >= max(64, 2 len); returns (sh, mask).
+__device__ __forceinline__ void hs_stage_warp(u32* T, const u32* __restrict__ col, u64 b, u32 len, u32& sh,
+                                              u32& mask) {
+  const int lane = threadIdx.x & 31;
+  u32 cap = 64;
+  while (cap < 2 * len) cap <<= 1;
+  mask = cap - 1;
+  sh = 32 - (31 - __clz(cap));
+  __syncwarp();
+  for (u32 i = lane * 4; i < cap; i += 128)
+    *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+  __syncwarp();
+  for (u32 i = lane; i < len; i += 32) hs_insert(T, sh, mask, __ldg(col + b + i));
+  __syncwarp();
+}
+
 // Last index i in [lo, hi) with W[i] <= key (W non-decreasing).
 __device__ __forceinline__ u64 upper_bound_prev(const u64* __restrict__ W, u64 lo, u64 hi, u64 key) {
   // find first i in [lo,hi) with W[i] > key, return i-1

@@ -54,8 +54,20 @@ struct Stats {
 
 // Level-1 build on the device (embedding_list.hpp:178-192): DAG -> every
 // edge; undirected -> (u,v) with u<v.  idx[i] = first endpoint, vid[i] = second.
+// Undirected graphs: *l1_start (optional) receives the exclusive prefix over
+// vertices of |{v in N(u) : v > u}|, i.e. the first level-1 index of root u.
 void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl,
-                  const u32** vid_view = nullptr);
+                  const u32** vid_view = nullptr, DBuf<u64>* l1_start = nullptr);
+
+// Last extension of 3-MC with the root's upper adjacency staged on chip
+// (mc_staged.cu): adds the 3-vertex connectivity-code counts of the level-1
+// slice [lo, hi) into d_hist (8 bins) and the candidates / B_alg to st.
+void mc3_staged(const gpm_graph& g, const u64* l1_start, u64 lo, u64 hi, unsigned long long* d_hist, cudaStream_t s,
+                Timeline& tl, Stats& st);
+// Last extension of 4-MC over a materialised level 2 (idx2 -> level-1 index,
+// vid2 = v2) with S0 / S1 staged on chip; adds 6-pair code counts to d_hist.
+void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u32* idx2, const u32* vid2, u64 np,
+                     unsigned long long* d_hist, cudaStream_t s, Timeline& tl, Stats& st);
 
 // Degree-weighted static split of [0, n1) root units into `world` parts
 // (SURVEY §8e); weight = candidate count of each level-1 entry.

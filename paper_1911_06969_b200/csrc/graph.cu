@@ -245,7 +245,7 @@ void keep_pool_warm(int device) {
 }
 
 void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl,
-                  const u32** vid_view) {
+                  const u32** vid_view, DBuf<u64>* l1_start) {
   if (g.oriented) {
     // level 1 of a DAG is the CSR edge range itself: vid aliases col (no copy)
     count = g.m;
@@ -282,6 +282,7 @@ void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count
                                                                  vid.get());
     GPM_CUDA(cudaGetLastError());
   }
+  if (l1_start) *l1_start = std::move(pos);
 }
 
 void root_split(const gpm_graph& g, const u32* idx, const u32* vid, u64 n1, int app, int rank, int world, u64& lo,

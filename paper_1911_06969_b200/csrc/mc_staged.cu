@@ -1,0 +1,729 @@
+// mc_staged.cu — the last extension of 3-motif counting with the root's
+// adjacency staged on chip (sm_100a).
+//
+// Reference: extend (Alg. 2) with MC's
+// to_add = is_auto_canonical_vertex (Listing 4) and reduce by
+// connectivity code (Listing 6), fused on the last level
+// (PAPER.md:742-744).  DESIGN.md §3a.
+//
+// Level 1 of MC is every edge (v0, v1) with v0 < v1 (embedding_list.hpp:
+// 178-192); the parents of one root v0 are S0 = {v in N(v0) : v > v0}, the
+// upper suffix of v0's sorted CSR list.  Every 3-vertex candidate u satisfies
+// u > v0, so only S0 matters for the membership tests.  Per parent (v0, v1):
+//   pos 0: u in N(v0), u > v1          -> always accepted;
+//          triangle iff u in N(v1), else wedge centred at v0
+//   pos 1: u in N(v1), u > v0          -> accepted iff u not in N(v0);
+//          wedge centred at v1
+// The pos-1 candidates are streamed from HBM (coalesced, one lane per
+// candidate) and tested against S0 held in a shared-memory hash set; a hit is
+// the pair predicate adj(v0,u) = adj(v1,u) for the same u, which also decides
+// the class of the pos-0 candidate u (u > v1).  So one streamed pass over the
+// pos-1 candidates evaluates every candidate's to_add and pattern predicate:
+//   tri(v0,v1)   = #{u in N(v1) ∩ S0 : u > v1}
+//   X(v0,v1)     = #{u in N(v1) ∩ S0}
+//   wedge@v0     = #{u in S0 : u > v1} - tri
+//   wedge@v1     = #{u in N(v1) : u > v0} - X
+// Roots with |S0| <= kWKeys stage S0 per warp (warp kernel); larger roots
+// stage S0 per CTA in tiles of kBKeys (block kernel), each tile owning an id
+// range so that every pos-1 candidate is streamed exactly once.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "engine.hpp"
+#include "pattern.cuh"
+
+namespace gpm {
+
+void scan_inplace(u64* data, u64 n, cudaStream_t s);
+
+namespace {
+
+constexpr int kT = 256;
+constexpr int kWarps = kT / 32;
+constexpr u32 kWSlots = 1024;   // per-warp hash slots (4 KB)
+constexpr u32 kWKeys = 512;     // roots with |S0| <= this use the warp kernel
+constexpr u32 kBSlots = 16384;  // per-CTA hash slots (64 KB)
+constexpr u32 kBKeys = 8192;    // S0 tile size of the block kernel
+constexpr u32 kPB = 32 * kWarps;  // parents per block item
+// first index i in [b, e) with col[i] >= key
+__device__ __forceinline__ u64 lower_bound_col(const u32* __restrict__ col, u64 b, u64 e, u32 key) {
+  while (b < e) {
+    const u64 mid = (b + e) >> 1;
+    if (ldg(col + mid) < key) b = mid + 1;
+    else e = mid;
+  }
+  return b;
+}
+
+struct Mc3Args {
+  DevGraph g;
+  const u64* l1s;        // first level-1 index per vertex (n+1 entries)
+  u64 lo, hi;            // level-1 slice
+  u32 vlo;               // root of level-1 index lo
+  const u64* istart;     // per root (r - vlo): first item; nr+1 entries
+  const u32* iroot;      // per item: r - vlo
+  u64 nitems;
+  u64 grab;
+  unsigned long long* ctr;
+  unsigned long long* hist;
+  unsigned long long* cand;
+  u32 codeT, codeW0, codeW1;
+};
+
+// Per-root item counts.  small: |S0| <= kWKeys -> ceil(npar/32) warp items;
+// big: ntiles * ceil(npar/kPB) block items.
+__global__ void mc3_items_kernel(const u64* __restrict__ l1s, u64 lo, u64 hi, u32 vlo, u32 nr,
+                                 u64* __restrict__ small, u64* __restrict__ big) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nr; i += (u64)gridDim.x * blockDim.x) {
+    const u32 r = vlo + (u32)i;
+    const u64 s = l1s[r], e = l1s[r + 1];
+    const u64 ns = e - s;
+    const u64 pa = max(s, lo), pb = min(e, hi);
+    const u64 np = pb > pa ? pb - pa : 0;
+    u64 cs = 0, cb = 0;
+    if (np) {
+      if (ns <= kWKeys) cs = (np + 31) / 32;
+      else cb = ((ns + kBKeys - 1) / kBKeys) * ((np + kPB - 1) / kPB);
+    }
+    small[i] = cs;
+    big[i] = cb;
+  }
+}
+
+__global__ void mc3_iroot_kernel(const u64* __restrict__ istart, u32 nr, u32* __restrict__ iroot) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nr; i += (u64)gridDim.x * blockDim.x)
+    for (u64 t = istart[i], te = istart[i + 1]; t < te; ++t) iroot[t] = (u32)i;
+}
+
+// root owning level-1 index e: last r with l1s[r] <= e
+__global__ void mc3_root_of_kernel(const u64* __restrict__ l1s, u32 n, u64 e0, u64 e1, u32* __restrict__ out) {
+  const int t = threadIdx.x;
+  if (t > 1) return;
+  const u64 e = t == 0 ? e0 : e1;
+  u64 lo = 0, hi = n;
+  while (lo < hi) {
+    const u64 mid = (lo + hi + 1) >> 1;
+    if (l1s[mid] <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  out[t] = (u32)lo;
+}
+
+// Streams the concatenated pos-1 candidate ranges of <= 32 parents (one per
+// lane: range [st, st+len) of col, parent vertex v1) against the staged set.
+// Returns (X, tri) counts for the warp (uniform across lanes).
+__device__ __forceinline__ void stream_parents(const u32* __restrict__ col, const u32* T, u32 sh, u32 mask, u64 st,
+                                               u32 len, u32 v1, u64* scb, u32* sex, u32* sv1, unsigned long long& X,
+                                               unsigned long long& tri) {
+  const int lane = threadIdx.x & 31;
+  u32 incl = len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return;
+  const u32 nz = __ballot_sync(0xffffffffu, len > 0);
+  const u32 rank = __popc(nz & lanemask_lt());
+  __syncwarp();
+  if (len > 0) {
+    scb[rank] = st;
+    sex[rank] = incl - len;
+    sv1[rank] = v1;
+  }
+  const u32 nnz = __popc(nz);
+  __syncwarp();
+  u32 P = 0;
+  u32 cx = 0, ct = 0;
+  for (u32 jb = 0; jb < total; jb += 32) {
+    const u32 j = jb + lane;
+    // lane -> parent by one OR-reduction over the parents' start offsets
+    const u32 x = (P + 1 + lane < nnz) ? sex[P + 1 + lane] : 0xffffffffu;
+    const u32 bit = (x - jb < 32u) ? (1u << (x - jb)) : 0u;
+    const u32 starts = __reduce_or_sync(0xffffffffu, bit);
+    const u32 myp = P + __popc(starts & (lanemask_lt() | (1u << lane)));
+    P += __popc(starts);
+    bool hit = false, t = false;
+    if (j < total) {
+      const u32 u = ldg(col + scb[myp] + (j - sex[myp]));
+      hit = hs_has(T, sh, mask, u);
+      t = hit && u > sv1[myp];
+    }
+    cx += __popc(__ballot_sync(0xffffffffu, hit));
+    ct += __popc(__ballot_sync(0xffffffffu, t));
+  }
+  X += cx;
+  tri += ct;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kT) mc3_warp_kernel(Mc3Args a) {
+  __shared__ __align__(16) u32 s_tab[kWarps][kWSlots];
+  __shared__ u64 s_cb[kWarps][32];
+  __shared__ u32 s_ex[kWarps][32];
+  __shared__ u32 s_v1[kWarps][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  u32* T = s_tab[wid];
+  const DevGraph& g = a.g;
+  unsigned long long aX = 0, aTri = 0, aC0 = 0, aLen = 0, aCand = 0;
+  u32 troot = 0xffffffffu, sh = 0, mask = 0;
+  u64 grab = 0, left = 0;
+  for (;;) {
+    if (left == 0) {
+      u64 g_ = 0;
+      if (lane == 0) g_ = atomicAdd(a.ctr, (unsigned long long)a.grab);
+      grab = __shfl_sync(0xffffffffu, g_, 0);
+      left = a.grab;
+    }
+    const u64 item = grab++;
+    --left;
+    if (item >= a.nitems) break;
+    const u32 rr = ldg(a.iroot + item);
+    const u32 r = a.vlo + rr;
+    const u64 s = ldg(a.l1s + r), e = ldg(a.l1s + r + 1);
+    const u32 ns = (u32)(e - s);
+    const u64 ob = ldg(g.off + r), oe = ldg(g.off + r + 1);
+    const u64 sb = oe - ns;  // S0 = col[sb, oe)
+    if (r != troot) {
+      troot = r;
+      u32 cap = 64;
+      while (cap < 2 * ns) cap <<= 1;
+      mask = cap - 1;
+      sh = 32 - (31 - __clz(cap));
+      for (u32 i = lane * 4; i < cap; i += 128) *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+      __syncwarp();
+      for (u32 i = lane; i < ns; i += 32) hs_insert(T, sh, mask, ldg(g.col + sb + i));
+      __syncwarp();
+    }
+    const u64 pa0 = max(s, a.lo);
+    const u64 pa = pa0 + 32 * (item - ldg(a.istart + rr));
+    const u64 pb = min(min(e, a.hi), pa + 32);
+    const u64 p = pa + lane;
+    u64 st = 0;
+    u32 len = 0, v1 = 0;
+    if (p < pb) {
+      const u32 ip = (u32)(p - s);
+      v1 = ldg(g.col + sb + ip);
+      const u64 b1 = ldg(g.off + v1), e1 = ldg(g.off + v1 + 1);
+      st = lower_bound_col(g.col, b1, e1, r + 1);
+      len = (u32)(e1 - st);
+      aC0 += ns - ip - 1;
+      aLen += len;
+      aCand += (oe - ob) + (e1 - b1);
+    }
+    stream_parents(g.col, T, sh, mask, st, len, v1, s_cb[wid], s_ex[wid], s_v1[wid], aX, aTri);
+  }
+  // per-lane partials (aC0, aLen, aCand) + warp-uniform (aX, aTri)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    aC0 += __shfl_xor_sync(0xffffffffu, aC0, o);
+    aLen += __shfl_xor_sync(0xffffffffu, aLen, o);
+    aCand += __shfl_xor_sync(0xffffffffu, aCand, o);
+  }
+  if (lane == 0) {
+    if (aTri) atomicAdd(a.hist + a.codeT, aTri);
+    if (aC0 - aTri) atomicAdd(a.hist + a.codeW0, aC0 - aTri);
+    if (aLen - aX) atomicAdd(a.hist + a.codeW1, aLen - aX);
+    if (aCand) atomicAdd(a.cand, aCand);
+  }
+}
+
+// Roots with |S0| > kWKeys: item = (root, S0 tile, chunk of kPB parents); the
+// CTA stages the tile, each warp streams 32 parents' candidates inside the
+// tile's id range [idlo, idhi).
+__global__ void __launch_bounds__(kT) mc3_block_kernel(Mc3Args a) {
+  extern __shared__ __align__(16) u32 s_btab[];
+  __shared__ u64 s_cb[kWarps][32];
+  __shared__ u32 s_ex[kWarps][32];
+  __shared__ u32 s_v1[kWarps][32];
+  __shared__ u64 s_item;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const DevGraph& g = a.g;
+  constexpr u32 mask = kBSlots - 1;
+  const u32 sh = 32 - (31 - __clz(kBSlots));
+  unsigned long long aX = 0, aTri = 0, aC0 = 0, aLen = 0, aCand = 0;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(a.ctr, 1ull);
+    __syncthreads();
+    const u64 item = s_item;
+    if (item >= a.nitems) break;
+    const u32 rr = ldg(a.iroot + item);
+    const u32 r = a.vlo + rr;
+    const u64 s = ldg(a.l1s + r), e = ldg(a.l1s + r + 1);
+    const u32 ns = (u32)(e - s);
+    const u64 ob = ldg(g.off + r), oe = ldg(g.off + r + 1);
+    const u64 sb = oe - ns;
+    const u64 pa0 = max(s, a.lo), pe = min(e, a.hi);
+    const u64 nch = (pe - pa0 + kPB - 1) / kPB;
+    const u32 ntiles = (ns + kBKeys - 1) / kBKeys;
+    const u64 q = item - ldg(a.istart + rr);
+    const u32 t = (u32)(q / nch);
+    const u64 c = q % nch;
+    const u32 k0 = t * kBKeys, k1 = min(ns, k0 + kBKeys);
+    for (u32 i = threadIdx.x * 4; i < kBSlots; i += kT * 4)
+      *reinterpret_cast<uint4*>(s_btab + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    __syncthreads();
+    for (u32 i = k0 + threadIdx.x; i < k1; i += kT) hs_insert(s_btab, sh, mask, ldg(g.col + sb + i));
+    __syncthreads();
+    const u32 idlo = (t == 0) ? r + 1 : ldg(g.col + sb + k0);
+    const bool last_tile = (t + 1 == ntiles);
+    const u32 idhi = last_tile ? 0xffffffffu : ldg(g.col + sb + k1);
+    const u64 p = pa0 + c * kPB + (u64)wid * 32 + lane;
+    const u64 pb = min(pe, pa0 + (c + 1) * kPB);
+    u64 st = 0;
+    u32 len = 0, v1 = 0;
+    if (p < pb) {
+      const u32 ip = (u32)(p - s);
+      v1 = ldg(g.col + sb + ip);
+      const u64 b1 = ldg(g.off + v1), e1 = ldg(g.off + v1 + 1);
+      st = lower_bound_col(g.col, b1, e1, idlo);
+      const u64 en = last_tile ? e1 : lower_bound_col(g.col, st, e1, idhi);
+      len = (u32)(en - st);
+      aLen += len;
+      if (t == 0) {
+        aC0 += ns - ip - 1;
+        aCand += (oe - ob) + (e1 - b1);
+      }
+    }
+    stream_parents(g.col, s_btab, sh, mask, st, len, v1, s_cb[wid], s_ex[wid], s_v1[wid], aX, aTri);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    aC0 += __shfl_xor_sync(0xffffffffu, aC0, o);
+    aLen += __shfl_xor_sync(0xffffffffu, aLen, o);
+    aCand += __shfl_xor_sync(0xffffffffu, aCand, o);
+  }
+  if (lane == 0) {
+    if (aTri) atomicAdd(a.hist + a.codeT, aTri);
+    if (aC0 - aTri) atomicAdd(a.hist + a.codeW0, aC0 - aTri);  // mod 2^64: partial sums may be negative
+    if (aLen - aX) atomicAdd(a.hist + a.codeW1, aLen - aX);
+    if (aCand) atomicAdd(a.cand, aCand);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 4-MC last extension.  Parents are level-2 embeddings (v0, v1, v2) whose
+// level-1 parent q = (v0, v1) groups them (the level is written in parent
+// order).  With S_i = N(v_i) ∩ (>v0), m = max(v1, v2), the candidates are
+//   pos 0: u in S0, u > m                 -> accepted; class by (u~v1, u~v2)
+//   pos 1: u in S1, u > v2, u not in S0   -> accepted; class by u~v2
+//   pos 2: u in S2, u not in S0 ∪ S1      -> accepted
+// (SPEC.md:214 + "emit u only from its first adjacent position").  The warp
+// stages S0 (per root) and S1 (per group) as shared-memory hash sets and
+// I01 = S0 ∩ S1 (sorted, per-warp scratch); each child streams S2 from HBM,
+// one lane per candidate, probing both sets:
+//   e2  = #{u in S2 : u !in S0, u !in S1}
+//   e11 = #{u in S2 : u in S0, u in S1, u > m}
+//   e01 = #{u in S2 : u in S0, u !in S1, u > m}
+//   e12 = #{u in S2 : u in S1, u !in S0, u > v2}
+// and the classes follow from the same predicates:
+//   pos0 (v1,v2 adj) e11 | (v1) #I01>m - e11 | (v2) e01 | () #S0>m - #I01>m - e01
+//   pos1 (v2 adj) e12    | () #S1>v2 - #I01>v2 - e12          pos2: e2
+// Sets larger than the hash capacity are probed by binary search in HBM.
+constexpr int kT4 = 256;
+constexpr int kW4 = kT4 / 32;
+constexpr u32 k4Slots = 1024;
+constexpr u32 k4Keys = 512;
+constexpr u64 k4Item = 512;  // level-2 entries per warp work item
+
+struct Mc4Args {
+  DevGraph g;
+  const u32* l1i;   // level-1 v0 (slice-relative)
+  const u32* l1v;   // level-1 v1
+  const u32* idx2;  // level-2 -> level-1 index
+  const u32* vid2;  // level-2 v2
+  u64 np;
+  u64 nitems;
+  unsigned long long* ctr;
+  unsigned long long* hist;   // 64 bins
+  unsigned long long* cand;
+  u32* scratch;               // per warp: max_deg entries for I01
+  u64 scratch_stride;
+  u32 pm_bits[4];             // pmask value for (v0~v2, v1~v2)
+  u32 cl_bits[7];
+};
+
+struct HSet {
+  const u32* T;    // smem table (or nullptr -> sorted list in HBM)
+  const u32* lst;  // sorted list in HBM
+  u32 len, sh, mask;
+  __device__ __forceinline__ bool has(u32 v) const {
+    if (T) return hs_has(T, sh, mask, v);
+    return contains_sorted(lst, len, v);
+  }
+};
+
+// stage the sorted list col[b, b+len) into T when it fits; warp-collective
+__device__ __forceinline__ HSet stage_set(u32* T, const u32* __restrict__ col, u64 b, u32 len) {
+  const int lane = threadIdx.x & 31;
+  HSet h;
+  h.lst = col + b;
+  h.len = len;
+  if (len > k4Keys) {
+    h.T = nullptr;
+    h.sh = h.mask = 0;
+    return h;
+  }
+  u32 cap = 64;
+  while (cap < 2 * len) cap <<= 1;
+  h.mask = cap - 1;
+  h.sh = 32 - (31 - __clz(cap));
+  __syncwarp();
+  for (u32 i = lane * 4; i < cap; i += 128) *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+  __syncwarp();
+  for (u32 i = lane; i < len; i += 32) hs_insert(T, h.sh, h.mask, ldg(col + b + i));
+  __syncwarp();
+  h.T = T;
+  return h;
+}
+
+// #{x in sorted a[0, n) : x > key}
+__device__ __forceinline__ u32 count_gt_global(const u32* __restrict__ a, u32 n, u32 key) {
+  u32 lo = 0, hi = n;
+  while (lo < hi) {
+    const u32 mid = (lo + hi) >> 1;
+    if (ldg(a + mid) <= key) lo = mid + 1;
+    else hi = mid;
+  }
+  return n - lo;
+}
+__device__ __forceinline__ u32 count_gt_plain(const u32* a, u32 n, u32 key) {
+  u32 lo = 0, hi = n;
+  while (lo < hi) {
+    const u32 mid = (lo + hi) >> 1;
+    if (a[mid] <= key) lo = mid + 1;
+    else hi = mid;
+  }
+  return n - lo;
+}
+
+__global__ void __launch_bounds__(kT4) mc4_last_kernel(Mc4Args a) {
+  extern __shared__ __align__(16) u32 s_dyn4[];  // [2][kW4][k4Slots] hash tables
+  u32 (*s_t0)[k4Slots] = reinterpret_cast<u32 (*)[k4Slots]>(s_dyn4);
+  u32 (*s_t1)[k4Slots] = reinterpret_cast<u32 (*)[k4Slots]>(s_dyn4 + kW4 * k4Slots);
+  __shared__ u64 s_cb[kW4][32];
+  __shared__ u32 s_ex[kW4][32];
+  __shared__ u32 s_v2[kW4][32];
+  __shared__ u32 s_ev[kW4][4][32];
+  __shared__ unsigned long long s_h[kW4][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const DevGraph& g = a.g;
+  u32* I01 = a.scratch + (blockIdx.x * (u64)kW4 + wid) * a.scratch_stride;
+  s_h[wid][lane] = 0;
+  unsigned long long aCand = 0;
+  u32 cur_v0 = 0xffffffffu;
+  u64 cur_q = ~0ull;
+  HSet h0{}, h1{};
+  u64 s0b = 0, s1b = 0;
+  u32 v0 = 0, v1 = 0, n01 = 0;
+  for (;;) {
+    u64 it_ = 0;
+    if (lane == 0) it_ = atomicAdd(a.ctr, 1ull);
+    const u64 item = __shfl_sync(0xffffffffu, it_, 0);
+    if (item >= a.nitems) break;
+    u64 cur = item * k4Item;
+    const u64 iend = min(a.np, cur + k4Item);
+    while (cur < iend) {
+      // children of one level-1 parent q among the next 32 entries
+      const u64 e = cur + lane;
+      const u64 qi = e < iend ? (u64)ldg(a.idx2 + e) : ~0ull;
+      const u64 q = __shfl_sync(0xffffffffu, qi, 0);
+      const u32 same = __ballot_sync(0xffffffffu, qi == q);
+      const u32 nstep = __popc(same);  // a prefix: idx2 is non-decreasing
+      if (q != cur_q) {
+        cur_q = q;
+        const u32 nv0 = ldg(a.l1i + q);
+        v1 = ldg(a.l1v + q);
+        if (nv0 != cur_v0) {
+          cur_v0 = nv0;
+          v0 = nv0;
+          const u64 b0 = ldg(g.off + v0), e0 = ldg(g.off + v0 + 1);
+          s0b = lower_bound_col(g.col, b0, e0, v0 + 1);
+          h0 = stage_set(s_t0[wid], g.col, s0b, (u32)(e0 - s0b));
+        }
+        const u64 b1 = ldg(g.off + v1), e1 = ldg(g.off + v1 + 1);
+        s1b = lower_bound_col(g.col, b1, e1, v0 + 1);
+        h1 = stage_set(s_t1[wid], g.col, s1b, (u32)(e1 - s1b));
+        // I01 = S1 ∩ S0 in ascending order (stream S1, probe S0)
+        n01 = 0;
+        for (u32 jb = 0; jb < h1.len; jb += 32) {
+          const u32 j = jb + lane;
+          u32 u = 0;
+          bool hit = false;
+          if (j < h1.len) {
+            u = ldg(g.col + s1b + j);
+            hit = h0.has(u);
+          }
+          const u32 bm = __ballot_sync(0xffffffffu, hit);
+          if (hit) I01[n01 + __popc(bm & lanemask_lt())] = u;
+          n01 += __popc(bm);
+        }
+        __syncwarp();
+      }
+      // per-child setup: lane c < nstep owns child cur + c
+      u32 v2 = 0, len = 0, pmv = 0;
+      u64 st = 0;
+      const bool valid = lane < (int)nstep;
+      if (valid) {
+        v2 = ldg(a.vid2 + cur + lane);
+        const u64 b2 = ldg(g.off + v2), e2 = ldg(g.off + v2 + 1);
+        st = lower_bound_col(g.col, b2, e2, v0 + 1);
+        len = (u32)(e2 - st);
+        pmv = (h0.has(v2) ? 1u : 0u) | (h1.has(v2) ? 2u : 0u);
+        aCand += (ldg(g.off + v0 + 1) - ldg(g.off + v0)) + (ldg(g.off + v1 + 1) - ldg(g.off + v1)) + (e2 - b2);
+      }
+      const u32 m = max(v1, v2);
+      // concatenated stream of the children's S2 ranges
+      u32 incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+      s_cb[wid][lane] = st;
+      s_ex[wid][lane] = incl - len;
+      s_v2[wid][lane] = v2;
+#pragma unroll
+      for (int ev = 0; ev < 4; ++ev) s_ev[wid][ev][lane] = 0;
+      __syncwarp();
+      u32 P = 0;  // child owning candidate jb (children with len 0 are skipped by the scan)
+      for (u32 jb = 0; jb < total; jb += 32) {
+        const u32 j = jb + lane;
+        // lane -> child: last c with ex[c] <= j and len[c] > 0 (binary search over 32)
+        u32 c = 0;
+        if (j < total) {
+          u32 lo_ = P, hi_ = nstep - 1;
+          while (lo_ < hi_) {
+            const u32 mid = (lo_ + hi_ + 1) >> 1;
+            if (s_ex[wid][mid] <= j) lo_ = mid;
+            else hi_ = mid - 1;
+          }
+          c = lo_;
+        }
+        bool f2 = false, f11 = false, f01 = false, f12 = false;
+        if (j < total) {
+          const u32 u = ldg(g.col + s_cb[wid][c] + (j - s_ex[wid][c]));
+          const bool i0 = h0.has(u), i1 = h1.has(u);
+          const u32 c_v2 = s_v2[wid][c];  // thresholds of child c
+          const u32 c_m = max(v1, c_v2);
+          f2 = !i0 && !i1;
+          f11 = i0 && i1 && u > c_m;
+          f01 = i0 && !i1 && u > c_m;
+          f12 = i1 && !i0 && u > c_v2;
+        }
+        // segmented per-child counts: head lane of each child segment adds popc
+        const u32 b2_ = __ballot_sync(0xffffffffu, f2), b11 = __ballot_sync(0xffffffffu, f11);
+        const u32 b01 = __ballot_sync(0xffffffffu, f01), b12 = __ballot_sync(0xffffffffu, f12);
+        const u32 cprev = __shfl_up_sync(0xffffffffu, c, 1);
+        const bool head = (j < total) && (lane == 0 || cprev != c);
+        const u32 heads = __ballot_sync(0xffffffffu, head);
+        if (head) {
+          const u32 above = heads & ~((2u << lane) - 1u);  // heads after this lane
+          const u32 endl = above ? (__ffs(above) - 1) : 32u;
+          const u32 seg = (endl >= 32 ? 0xffffffffu : ((1u << endl) - 1u)) & ~((1u << lane) - 1u);
+          s_ev[wid][0][c] += __popc(b2_ & seg);
+          s_ev[wid][1][c] += __popc(b11 & seg);
+          s_ev[wid][2][c] += __popc(b01 & seg);
+          s_ev[wid][3][c] += __popc(b12 & seg);
+        }
+        P = __shfl_sync(0xffffffffu, c, 31);  // j of lane 31 < total unless this is the last step
+        __syncwarp();
+      }
+      __syncwarp();
+      // per-child class values, reduced per parent-mask value
+      u32 val[7] = {0, 0, 0, 0, 0, 0, 0};
+      if (valid) {
+        const u32 e2c = s_ev[wid][0][lane], e11 = s_ev[wid][1][lane], e01 = s_ev[wid][2][lane],
+                  e12 = s_ev[wid][3][lane];
+        const u32 A0 = count_gt_global(g.col + s0b, h0.len, m);
+        const u32 B1 = count_gt_global(g.col + s1b, h1.len, v2);
+        const u32 Im = count_gt_plain(I01, n01, m);
+        const u32 I2 = count_gt_plain(I01, n01, v2);
+        val[0] = e11;
+        val[1] = Im - e11;
+        val[2] = e01;
+        val[3] = A0 - Im - e01;
+        val[4] = e12;
+        val[5] = B1 - I2 - e12;
+        val[6] = e2c;
+      }
+#pragma unroll
+      for (u32 pv = 0; pv < 4; ++pv) {
+        const bool mine = valid && pmv == pv;
+        if (__ballot_sync(0xffffffffu, mine) == 0) continue;
+#pragma unroll
+        for (int cl = 0; cl < 7; ++cl) {
+          const u32 sum = __reduce_add_sync(0xffffffffu, mine ? val[cl] : 0u);
+          if (lane == 0) s_h[wid][pv * 8 + cl] += sum;
+        }
+      }
+      __syncwarp();
+      cur += nstep;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) aCand += __shfl_xor_sync(0xffffffffu, aCand, o);
+  {
+    const u32 pv = lane >> 3, cl = lane & 7;
+    const unsigned long long v = s_h[wid][lane];
+    if (cl < 7 && v) atomicAdd(a.hist + (a.pm_bits[pv] | a.cl_bits[cl]), v);
+  }
+  if (lane == 0 && aCand) atomicAdd(a.cand, aCand);
+}
+
+inline unsigned grid1(u64 items) { return (unsigned)std::max<u64>(1, std::min<u64>((items + 255) / 256, 1u << 20)); }
+
+}  // namespace
+
+void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned long long* d_hist, cudaStream_t s,
+                Timeline& tl, Stats& st) {
+  if (hi <= lo) return;
+  const u64 np = hi - lo;
+  DBuf<u32> vv(2, s);
+  mc3_root_of_kernel<<<1, 32, 0, s>>>(l1s, G.n, lo, hi - 1, vv.get());
+  GPM_CUDA(cudaGetLastError());
+  u32 vr[2];
+  GPM_CUDA(cudaMemcpyAsync(vr, vv.get(), sizeof vr, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  const u32 nr = vr[1] - vr[0] + 1;
+  DBuf<u64> ismall(nr + 1, s), ibig(nr + 1, s);
+  GPM_CUDA(cudaMemsetAsync(ismall.get() + nr, 0, sizeof(u64), s));
+  GPM_CUDA(cudaMemsetAsync(ibig.get() + nr, 0, sizeof(u64), s));
+  mc3_items_kernel<<<grid1(nr), 256, 0, s>>>(l1s, lo, hi, vr[0], nr, ismall.get(), ibig.get());
+  GPM_CUDA(cudaGetLastError());
+  scan_inplace(ismall.get(), nr + 1, s);
+  scan_inplace(ibig.get(), nr + 1, s);
+  u64 NS = 0, NB = 0;
+  GPM_CUDA(cudaMemcpyAsync(&NS, ismall.get() + nr, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaMemcpyAsync(&NB, ibig.get() + nr, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  tl.launches += 6;
+  DBuf<u32> rs(std::max<u64>(1, NS), s), rb(std::max<u64>(1, NB), s);
+  if (NS) mc3_iroot_kernel<<<grid1(nr), 256, 0, s>>>(ismall.get(), nr, rs.get());
+  if (NB) mc3_iroot_kernel<<<grid1(nr), 256, 0, s>>>(ibig.get(), nr, rb.get());
+  GPM_CUDA(cudaGetLastError());
+  DBuf<unsigned long long> ctr(2, s), cand(1, s);
+  GPM_CUDA(cudaMemsetAsync(ctr.get(), 0, 2 * sizeof(unsigned long long), s));
+  GPM_CUDA(cudaMemsetAsync(cand.get(), 0, sizeof(unsigned long long), s));
+
+  Mc3Args a{};
+  a.g = G.view();
+  a.l1s = l1s;
+  a.lo = lo;
+  a.hi = hi;
+  a.vlo = vr[0];
+  a.hist = d_hist;
+  a.cand = cand.get();
+  a.codeT = (1u << pat::pair_index(0, 1, 3)) | (1u << pat::pair_index(0, 2, 3)) | (1u << pat::pair_index(1, 2, 3));
+  a.codeW0 = (1u << pat::pair_index(0, 1, 3)) | (1u << pat::pair_index(0, 2, 3));
+  a.codeW1 = (1u << pat::pair_index(0, 1, 3)) | (1u << pat::pair_index(1, 2, 3));
+  const int sms = sm_count();
+  size_t rec = tl.recs.size();
+  if (NS) {
+    static int occ = 0;
+    if (!occ) {
+      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mc3_warp_kernel, kT, 0));
+      occ = std::max(1, occ);
+    }
+    const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sms * occ, (NS + kWarps - 1) / kWarps));
+    Mc3Args w = a;
+    w.istart = ismall.get();
+    w.iroot = rs.get();
+    w.nitems = NS;
+    w.ctr = ctr.get();
+    w.grab = std::max<u64>(1, std::min<u64>(4, NS / (blocks * kWarps * 64)));
+    size_t ev = tl.begin("extend_fused_L1", 0.0);
+    mc3_warp_kernel<<<(unsigned)blocks, kT, 0, s>>>(w);
+    GPM_CUDA(cudaGetLastError());
+    tl.end(ev);
+    ++tl.launches;
+  }
+  if (NB) {
+    const size_t smem = kBSlots * sizeof(u32);
+    static int occb = 0;
+    if (!occb) {
+      GPM_CUDA(cudaFuncSetAttribute(mc3_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occb, mc3_block_kernel, kT, smem));
+      occb = std::max(1, occb);
+    }
+    const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sms * occb, NB));
+    Mc3Args b = a;
+    b.istart = ibig.get();
+    b.iroot = rb.get();
+    b.nitems = NB;
+    b.ctr = ctr.get() + 1;
+    size_t ev = tl.begin("extend_fused_L1", 0.0);
+    mc3_block_kernel<<<(unsigned)blocks, kT, smem, s>>>(b);
+    GPM_CUDA(cudaGetLastError());
+    tl.end(ev);
+    ++tl.launches;
+  }
+  unsigned long long W = 0;
+  GPM_CUDA(cudaMemcpyAsync(&W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  // SURVEY §8d B_alg of the level: 8*l per parent + (16 + 4 deg) per position
+  const double bytes = 8.0 * np + 16.0 * 2 * np + 4.0 * (double)W;
+  if (rec < tl.recs.size()) tl.recs[rec].bytes = bytes;
+  st.candidates[1] += W;
+  st.balg += bytes;
+}
+
+void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u32* idx2, const u32* vid2, u64 np,
+                     unsigned long long* d_hist, cudaStream_t s, Timeline& tl, Stats& st) {
+  if (np == 0) return;
+  const size_t smem = 2ull * kW4 * k4Slots * sizeof(u32);
+  static int occ = 0;
+  if (!occ) {
+    GPM_CUDA(cudaFuncSetAttribute(mc4_last_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mc4_last_kernel, kT4, smem));
+    occ = std::max(1, occ);
+  }
+  const u64 nitems = (np + k4Item - 1) / k4Item;
+  const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sm_count() * occ, (nitems + kW4 - 1) / kW4));
+  const u64 stride = std::max<u64>(32, ((u64)G.max_deg + 31) / 32 * 32);
+  DBuf<u32> scratch(blocks * kW4 * stride, s);
+  DBuf<unsigned long long> ctr(1, s), cand(1, s);
+  GPM_CUDA(cudaMemsetAsync(ctr.get(), 0, sizeof(unsigned long long), s));
+  GPM_CUDA(cudaMemsetAsync(cand.get(), 0, sizeof(unsigned long long), s));
+  Mc4Args a{};
+  a.g = G.view();
+  a.l1i = l1i;
+  a.l1v = l1v;
+  a.idx2 = idx2;
+  a.vid2 = vid2;
+  a.np = np;
+  a.nitems = nitems;
+  a.ctr = ctr.get();
+  a.hist = d_hist;
+  a.cand = cand.get();
+  a.scratch = scratch.get();
+  a.scratch_stride = stride;
+  auto P = [](int i, int j) { return 1u << pat::pair_index(i, j, 4); };
+  for (u32 pv = 0; pv < 4; ++pv) a.pm_bits[pv] = P(0, 1) | ((pv & 1) ? P(0, 2) : 0u) | ((pv & 2) ? P(1, 2) : 0u);
+  a.cl_bits[0] = P(0, 3) | P(1, 3) | P(2, 3);
+  a.cl_bits[1] = P(0, 3) | P(1, 3);
+  a.cl_bits[2] = P(0, 3) | P(2, 3);
+  a.cl_bits[3] = P(0, 3);
+  a.cl_bits[4] = P(1, 3) | P(2, 3);
+  a.cl_bits[5] = P(1, 3);
+  a.cl_bits[6] = P(2, 3);
+  size_t ev = tl.begin("extend_fused_L2", 0.0);
+  mc4_last_kernel<<<(unsigned)blocks, kT4, smem, s>>>(a);
+  GPM_CUDA(cudaGetLastError());
+  tl.end(ev);
+  tl.launches += 1;
+  unsigned long long W = 0;
+  GPM_CUDA(cudaMemcpyAsync(&W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  const double bytes = 8.0 * 2 * np + 16.0 * 3 * np + 4.0 * (double)W;
+  tl.recs[ev].bytes = bytes;
+  st.candidates[2] += W;
+  st.balg += bytes;
+}
+
+}  // namespace gpm

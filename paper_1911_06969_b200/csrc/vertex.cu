@@ -52,10 +52,8 @@ constexpr u64 kBatch = 2048;  // candidates per warp batch
 
 constexpr u64 kItemGrab = 8;        // root-kernel work items per atomic grab
 constexpr u64 kBatchGrab = 4;       // generic-engine batches per atomic grab
-constexpr u32 kFilterWords = 128;   // 4096-bit per-warp hash filter
-constexpr u32 kFilterMax = 512;     // lists longer than this skip the filter
-
-__device__ __forceinline__ u32 filter_hash(u32 v) { return (v * 0x9E3779B1u) >> 20; }
+constexpr u32 kHashSlots = 1024;    // per-warp exact hash set of the root's out-list (4 KB)
+constexpr u32 kFilterMax = 512;     // out-lists longer than this are probed by binary search
 
 struct VLevels {
   const u32* idx[kMaxLevels];
@@ -207,9 +205,10 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
   constexpr int S = LEV + 1;  // parent embedding size
   constexpr int kWords = (int)(kBatch / 32);
   extern __shared__ unsigned long long shist[];
-  __shared__ __align__(16) u32 s_filter[(APP != kAppMC) ? kThreads / 32 : 1][kFilterWords];
+  __shared__ __align__(16) u32 s_hash[(APP != kAppMC) ? kThreads / 32 : 1][(APP != kAppMC) ? kHashSlots : 4];
   const int lane = threadIdx.x & 31;
-  u32* filt = s_filter[(APP != kAppMC) ? (threadIdx.x >> 5) : 0];
+  u32* filt = s_hash[(APP != kAppMC) ? (threadIdx.x >> 5) : 0];
+  u32 fsh = 0, fmask = 0;
   const DevGraph& g = a.g;
   int nbins = 0;
   if (MODE == kFused && APP == kAppMC) {
@@ -272,7 +271,7 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
     u32 c = 0;
     u32 myword = 0;
     int it = 0;
-    u64 fkey = ~0ull;  // begin of the root out-list held in the filter
+    u64 fkey = ~0ull;  // begin of the root out-list held in the hash set
     bool fok = false;
     u64 P0 = pa;  // compacted parent owning candidate jb
     for (u64 jb = j0; jb < j1; jb += 32, ++it) {
@@ -289,9 +288,9 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
       u32 u = 0, code = 0;
       if (j < j1) cur.load(a, myp);
       if (APP != kAppMC) {
-        // warp-shared 4096-bit hash filter of N+(emb[0]) (the root's out-list,
-        // shared by all parents of one root): most rejected candidates cost one
-        // shared-memory load instead of a global binary search
+        // warp-shared exact hash set of N+(emb[0]) (the root's out-list,
+        // shared by all parents of one root): the emb[0] probe costs one or
+        // two shared-memory loads instead of a global binary search
         const u32 act = __ballot_sync(0xffffffffu, j < j1);
         const int leader = __ffs(act) - 1;
         const u64 key = __shfl_sync(0xffffffffu, cur.qbeg[0] | ((u64)cur.qdeg[0] << 40), leader);
@@ -300,15 +299,7 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
           const u32 d = (u32)(key >> 40);
           const u64 qb = key & ((u64(1) << 40) - 1);
           fok = d <= kFilterMax;
-          if (fok) {
-            reinterpret_cast<uint4*>(filt)[lane] = make_uint4(0u, 0u, 0u, 0u);
-            __syncwarp();
-            for (u32 i = lane; i < d; i += 32) {
-              const u32 h = filter_hash(ldg(g.col + qb + i));
-              atomicOr(&filt[h >> 5], 1u << (h & 31));
-            }
-            __syncwarp();
-          }
+          if (fok) hs_stage_warp(filt, g.col, qb, d, fsh, fmask);
         }
       }
       if (j < j1) {
@@ -341,13 +332,14 @@ __global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
           } else {
             // Listing 3 / TC: connected (directed) to every earlier vertex
             ok = true;
+            int t0 = 0;
             if (fok && (cur.qbeg[0] | ((u64)cur.qdeg[0] << 40)) == fkey) {
-              const u32 h = filter_hash(u);
-              ok = (filt[h >> 5] >> (h & 31)) & 1u;
+              ok = hs_has(filt, fsh, fmask, u);  // exact: emb[0] needs no further probe
+              t0 = 1;
             }
 #pragma unroll
             for (int t = 0; t < S - 1; ++t)
-              if (ok && !contains_sorted(g.col + cur.qbeg[t], cur.qdeg[t], u)) ok = false;
+              if (t >= t0 && ok && !contains_sorted(g.col + cur.qbeg[t], cur.qdeg[t], u)) ok = false;
           }
         }
       }
@@ -468,12 +460,13 @@ __global__ void item_root_kernel(const u64* __restrict__ items, u32 nr, u32* __r
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) root_kernel(RootArgs a) {
-  __shared__ __align__(16) u32 s_filter[kThreads / 32][kFilterWords];
+  extern __shared__ __align__(16) u32 s_rhash[];  // [kThreads/32][kHashSlots]
   __shared__ u64 s_cb[kThreads / 32][32];
   __shared__ u32 s_ex[kThreads / 32][33];
   __shared__ u32 s_ei[kThreads / 32][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  u32* filt = s_filter[wid];
+  u32* filt = s_rhash + wid * kHashSlots;
+  u32 fsh = 0, fmask = 0;
   u64* scb = s_cb[wid];
   u32* sex = s_ex[wid];
   u32* sei = s_ei[wid];
@@ -510,13 +503,7 @@ __global__ void __launch_bounds__(kThreads) root_kernel(RootArgs a) {
     const bool from_masks = (MODE == kWrite) && mo != ~0ull;
     if (use_filter && !from_masks && r != froot) {
       froot = r;
-      reinterpret_cast<uint4*>(filt)[lane] = make_uint4(0u, 0u, 0u, 0u);
-      __syncwarp();
-      for (u32 i = lane; i < d0; i += 32) {
-        const u32 h = filter_hash(ldg(g.col + ob + i));
-        atomicOr(&filt[h >> 5], 1u << (h & 31));
-      }
-      __syncwarp();
+      hs_stage_warp(filt, g.col, ob, d0, fsh, fmask);
     }
     // the item's 32 parents (v0, v1): candidate lists N+(v1)
     const u64 e = c0 + lane;
@@ -587,9 +574,7 @@ __global__ void __launch_bounds__(kThreads) root_kernel(RootArgs a) {
       if (j < total) {
         u = ldg(g.col + scb[myp] + (j - sex[myp]));
         if (use_filter) {
-          const u32 h = filter_hash(u);
-          ok = (filt[h >> 5] >> (h & 31)) & 1u;
-          if (ok) ok = contains_sorted(g.col + ob, d0, u);
+          ok = hs_has(filt, fsh, fmask, u);
         } else {
           ok = contains_sorted(g.col + ob, d0, u);
         }
@@ -663,6 +648,7 @@ struct Ctx {
   unsigned long long* d_total;
   unsigned long long* d_hist;
   unsigned long long* d_ctr;
+  bool generic_mc;   // GPM_GENERIC_MC: per-candidate binary-search path for MC
 };
 
 template <int APP, int LEV, int MODE>
@@ -720,6 +706,12 @@ void process(Ctx& c, VLevels L, u64 np) {
   const bool last = (LEV == c.k - 2);
   Stats& st = *c.st;
   if (np == 0) return;
+  if constexpr (APP == kAppMC && LEV == 2) {
+    if (last && c.k == 4 && !c.generic_mc) {
+      mc4_last_staged(*c.G, L.idx[0], L.vid[0], L.idx[1], L.vid[1], np, c.d_hist, c.s, *c.tl, st);
+      return;
+    }
+  }
   // ---- work pass, compaction of parents with work, scan: candidate space
   u64 nz = 0;
   DBuf<u32> pidx;
@@ -852,9 +844,11 @@ void process(Ctx& c, VLevels L, u64 np) {
 template <int MODE>
 void launch_root(Ctx& c, RootArgs& a, const char* what, double bytes) {
   auto kern = root_kernel<MODE>;
+  const size_t smem = (size_t)(kThreads / 32) * kHashSlots * sizeof(u32);
   static int occ = 0;
   if (occ == 0) {
-    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
+    GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
     occ = std::max(1, occ);
   }
   const u64 ni = a.iend - a.ibeg;
@@ -864,7 +858,7 @@ void launch_root(Ctx& c, RootArgs& a, const char* what, double bytes) {
   GPM_CUDA(cudaMemsetAsync(c.d_ctr, 0, sizeof(unsigned long long), c.s));
   a.ctr = c.d_ctr;
   size_t ev = c.tl->begin(what, bytes);
-  kern<<<(unsigned)blocks, kThreads, 0, c.s>>>(a);
+  kern<<<(unsigned)blocks, kThreads, smem, c.s>>>(a);
   GPM_CUDA(cudaGetLastError());
   c.tl->end(ev);
   ++c.tl->launches;
@@ -1022,9 +1016,10 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   st.ensure(levels);
   htrace(s, "mine_vertex: start (orient done)");
   DBuf<u32> l1i, l1v;
+  DBuf<u64> l1s;
   u64 n1 = 0;
   const u32* l1vid = nullptr;
-  build_level1(*G, l1i, l1v, n1, s, tl, &l1vid);
+  build_level1(*G, l1i, l1v, n1, s, tl, &l1vid, &l1s);
   if (!l1vid) l1vid = l1v.get();
   u64 lo = 0, hi = n1;
   if (cfg.root_hi > 0) {
@@ -1048,6 +1043,7 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   c.tl = &tl;
   c.st = &st;
   c.sms = sm_count();
+  c.generic_mc = std::getenv("GPM_GENERIC_MC") != nullptr;
   size_t freeb = 0, totalb = 0;
   GPM_CUDA(cudaMemGetInfo(&freeb, &totalb));
   u64 budget = cfg.mem_budget ? cfg.mem_budget : (u64)(0.6 * (double)freeb);
@@ -1069,6 +1065,8 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   const int appk = (app == GPM_APP_MC) ? kAppMC : kAppCF;  // TC == CF with k=3 (Listing 3)
   if (k == 2 || nroot == 0) {
     res.total = (k == 2) ? nroot : 0;
+  } else if (appk == kAppMC && k == 3 && l1s.get() && !c.generic_mc) {
+    mc3_staged(*G, l1s.get(), lo, hi, c.d_hist, s, tl, st);
   } else if (appk == kAppMC) {
     process_dispatch<kAppMC>(c, 1, L, nroot);
   } else if (G->oriented && !std::getenv("GPM_GENERIC_L1")) {
