@@ -137,29 +137,44 @@ __device__ __forceinline__ void stream_parents(const u32* __restrict__ col, cons
   __syncwarp();
   u32 P = 0;
   u32 cx = 0, ct = 0;
-  for (u32 jb = 0; jb < total; jb += 32) {
-    const u32 j = jb + lane;
-    // lane -> parent by one OR-reduction over the parents' start offsets
-    const u32 x = (P + 1 + lane < nnz) ? sex[P + 1 + lane] : 0xffffffffu;
-    const u32 bit = (x - jb < 32u) ? (1u << (x - jb)) : 0u;
-    const u32 starts = __reduce_or_sync(0xffffffffu, bit);
-    const u32 myp = P + __popc(starts & (lanemask_lt() | (1u << lane)));
-    P += __popc(starts);
-    bool hit = false, t = false;
-    if (j < total) {
-      const u32 u = ldg(col + scb[myp] + (j - sex[myp]));
-      hit = hs_has(T, sh, mask, u);
-      t = hit && u > sv1[myp];
+  // two 32-candidate steps per iteration: both loads are in flight before
+  // either probe (memory-level parallelism for the L2/HBM latency)
+  for (u32 jb = 0; jb < total; jb += 64) {
+    u32 myp[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const u32 jh = jb + 32 * h;
+      // lane -> parent by one OR-reduction over the parents' start offsets
+      const u32 x = (P + 1 + lane < nnz) ? sex[P + 1 + lane] : 0xffffffffu;
+      const u32 bit = (x - jh < 32u) ? (1u << (x - jh)) : 0u;
+      const u32 starts = __reduce_or_sync(0xffffffffu, bit);
+      myp[h] = min(P + __popc(starts & (lanemask_lt() | (1u << lane))), nnz - 1);
+      P += __popc(starts);
     }
-    cx += __popc(__ballot_sync(0xffffffffu, hit));
-    ct += __popc(__ballot_sync(0xffffffffu, t));
+    u32 u[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const u32 j = jb + 32 * h + lane;
+      u[h] = j < total ? ldg(col + scb[myp[h]] + (j - sex[myp[h]])) : 0u;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const u32 j = jb + 32 * h + lane;
+      bool hit = false, t = false;
+      if (j < total) {
+        hit = hs_has(T, sh, mask, u[h]);
+        t = hit && u[h] > sv1[myp[h]];
+      }
+      cx += __popc(__ballot_sync(0xffffffffu, hit));
+      ct += __popc(__ballot_sync(0xffffffffu, t));
+    }
   }
   X += cx;
   tri += ct;
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(kT) mc3_warp_kernel(Mc3Args a) {
+__global__ void __launch_bounds__(kT, 4) mc3_warp_kernel(Mc3Args a) {
   __shared__ __align__(16) u32 s_tab[kWarps][kWSlots];
   __shared__ u64 s_cb[kWarps][32];
   __shared__ u32 s_ex[kWarps][32];
@@ -233,7 +248,7 @@ __global__ void __launch_bounds__(kT) mc3_warp_kernel(Mc3Args a) {
 // Roots with |S0| > kWKeys: item = (root, S0 tile, chunk of kPB parents); the
 // CTA stages the tile, each warp streams 32 parents' candidates inside the
 // tile's id range [idlo, idhi).
-__global__ void __launch_bounds__(kT) mc3_block_kernel(Mc3Args a) {
+__global__ void __launch_bounds__(kT, 3) mc3_block_kernel(Mc3Args a) {
   extern __shared__ __align__(16) u32 s_btab[];
   __shared__ u64 s_cb[kWarps][32];
   __shared__ u32 s_ex[kWarps][32];
@@ -325,9 +340,9 @@ __global__ void __launch_bounds__(kT) mc3_block_kernel(Mc3Args a) {
 // Sets larger than the hash capacity are probed by binary search in HBM.
 constexpr int kT4 = 256;
 constexpr int kW4 = kT4 / 32;
-constexpr u32 k4Slots = 1024;
-constexpr u32 k4Keys = 512;
-constexpr u64 k4Item = 512;  // level-2 entries per warp work item
+constexpr u32 k4Slots = 1024;  // per-warp union table S0 ∪ S1 (4 KB)
+constexpr u32 k4Keys = 512;    // |S0| + |S1| above this -> binary search in HBM
+constexpr u64 k4Item = 512;    // level-2 entries per warp work item
 
 struct Mc4Args {
   DevGraph g;
@@ -346,38 +361,32 @@ struct Mc4Args {
   u32 cl_bits[7];
 };
 
-struct HSet {
-  const u32* T;    // smem table (or nullptr -> sorted list in HBM)
-  const u32* lst;  // sorted list in HBM
-  u32 len, sh, mask;
-  __device__ __forceinline__ bool has(u32 v) const {
-    if (T) return hs_has(T, sh, mask, v);
-    return contains_sorted(lst, len, v);
+// Union hash set of S0 and S1: slot = (id << 2) | (in S0) | (in S1) << 1
+// (ids < 2^30).  One probe answers both memberships.
+__device__ __forceinline__ u32 us_flags(const u32* T, u32 sh, u32 mask, u32 v) {
+  u32 h = (v * kHashMul) >> sh;
+  for (;;) {
+    const u32 x = T[h];
+    if (x == kEmpty) return 0;
+    if ((x >> 2) == v) return x & 3u;
+    h = (h + 1) & mask;
   }
-};
-
-// stage the sorted list col[b, b+len) into T when it fits; warp-collective
-__device__ __forceinline__ HSet stage_set(u32* T, const u32* __restrict__ col, u64 b, u32 len) {
-  const int lane = threadIdx.x & 31;
-  HSet h;
-  h.lst = col + b;
-  h.len = len;
-  if (len > k4Keys) {
-    h.T = nullptr;
-    h.sh = h.mask = 0;
-    return h;
+}
+// insert v with flag f; if v is present OR the flag in; returns true if present
+__device__ __forceinline__ bool us_add(u32* T, u32 sh, u32 mask, u32 v, u32 f) {
+  u32 h = (v * kHashMul) >> sh;
+  for (;;) {
+    u32 x = T[h];
+    if (x == kEmpty) {
+      x = atomicCAS(T + h, kEmpty, (v << 2) | f);
+      if (x == kEmpty) return false;
+    }
+    if ((x >> 2) == v) {
+      atomicOr(T + h, f);
+      return true;
+    }
+    h = (h + 1) & mask;
   }
-  u32 cap = 64;
-  while (cap < 2 * len) cap <<= 1;
-  h.mask = cap - 1;
-  h.sh = 32 - (31 - __clz(cap));
-  __syncwarp();
-  for (u32 i = lane * 4; i < cap; i += 128) *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-  __syncwarp();
-  for (u32 i = lane; i < len; i += 32) hs_insert(T, h.sh, h.mask, ldg(col + b + i));
-  __syncwarp();
-  h.T = T;
-  return h;
 }
 
 // #{x in sorted a[0, n) : x > key}
@@ -400,10 +409,19 @@ __device__ __forceinline__ u32 count_gt_plain(const u32* a, u32 n, u32 key) {
   return n - lo;
 }
 
-__global__ void __launch_bounds__(kT4) mc4_last_kernel(Mc4Args a) {
-  extern __shared__ __align__(16) u32 s_dyn4[];  // [2][kW4][k4Slots] hash tables
-  u32 (*s_t0)[k4Slots] = reinterpret_cast<u32 (*)[k4Slots]>(s_dyn4);
-  u32 (*s_t1)[k4Slots] = reinterpret_cast<u32 (*)[k4Slots]>(s_dyn4 + kW4 * k4Slots);
+struct UnionSet {
+  const u32* T;      // nullptr -> probe the sorted lists in HBM
+  const u32* s0;
+  const u32* s1;
+  u32 n0, n1, sh, mask;
+  __device__ __forceinline__ u32 flags(u32 v) const {
+    if (T) return us_flags(T, sh, mask, v);
+    return (contains_sorted(s0, n0, v) ? 1u : 0u) | (contains_sorted(s1, n1, v) ? 2u : 0u);
+  }
+};
+
+__global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
+  __shared__ __align__(16) u32 s_tab[kW4][k4Slots];
   __shared__ u64 s_cb[kW4][32];
   __shared__ u32 s_ex[kW4][32];
   __shared__ u32 s_v2[kW4][32];
@@ -411,13 +429,14 @@ __global__ void __launch_bounds__(kT4) mc4_last_kernel(Mc4Args a) {
   __shared__ unsigned long long s_h[kW4][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const DevGraph& g = a.g;
+  u32* T = s_tab[wid];
   u32* I01 = a.scratch + (blockIdx.x * (u64)kW4 + wid) * a.scratch_stride;
   s_h[wid][lane] = 0;
   unsigned long long aCand = 0;
   u32 cur_v0 = 0xffffffffu;
   u64 cur_q = ~0ull;
-  HSet h0{}, h1{};
-  u64 s0b = 0, s1b = 0;
+  UnionSet U{};
+  u64 s0b = 0;
   u32 v0 = 0, v1 = 0, n01 = 0;
   for (;;) {
     u64 it_ = 0;
@@ -431,39 +450,53 @@ __global__ void __launch_bounds__(kT4) mc4_last_kernel(Mc4Args a) {
       const u64 e = cur + lane;
       const u64 qi = e < iend ? (u64)ldg(a.idx2 + e) : ~0ull;
       const u64 q = __shfl_sync(0xffffffffu, qi, 0);
-      const u32 same = __ballot_sync(0xffffffffu, qi == q);
-      const u32 nstep = __popc(same);  // a prefix: idx2 is non-decreasing
+      const u32 nstep = __popc(__ballot_sync(0xffffffffu, qi == q));  // a prefix: idx2 is sorted
       if (q != cur_q) {
+        // ---- stage S0 ∪ S1 (flags) and I01 = S0 ∩ S1 in ascending order
         cur_q = q;
         const u32 nv0 = ldg(a.l1i + q);
         v1 = ldg(a.l1v + q);
         if (nv0 != cur_v0) {
-          cur_v0 = nv0;
-          v0 = nv0;
+          cur_v0 = v0 = nv0;
           const u64 b0 = ldg(g.off + v0), e0 = ldg(g.off + v0 + 1);
           s0b = lower_bound_col(g.col, b0, e0, v0 + 1);
-          h0 = stage_set(s_t0[wid], g.col, s0b, (u32)(e0 - s0b));
+          U.s0 = g.col + s0b;
+          U.n0 = (u32)(e0 - s0b);
         }
         const u64 b1 = ldg(g.off + v1), e1 = ldg(g.off + v1 + 1);
-        s1b = lower_bound_col(g.col, b1, e1, v0 + 1);
-        h1 = stage_set(s_t1[wid], g.col, s1b, (u32)(e1 - s1b));
-        // I01 = S1 ∩ S0 in ascending order (stream S1, probe S0)
+        const u64 s1b = lower_bound_col(g.col, b1, e1, v0 + 1);
+        U.s1 = g.col + s1b;
+        U.n1 = (u32)(e1 - s1b);
+        const bool fits = U.n0 + U.n1 <= k4Keys;
+        if (fits) {
+          u32 cap = 64;
+          while (cap < 2 * (U.n0 + U.n1)) cap <<= 1;
+          U.mask = cap - 1;
+          U.sh = 32 - (31 - __clz(cap));
+          __syncwarp();
+          for (u32 i = lane * 4; i < cap; i += 128)
+            *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+          __syncwarp();
+          for (u32 i = lane; i < U.n0; i += 32) us_add(T, U.sh, U.mask, ldg(U.s0 + i), 1u);
+          __syncwarp();
+        }
         n01 = 0;
-        for (u32 jb = 0; jb < h1.len; jb += 32) {
+        for (u32 jb = 0; jb < U.n1; jb += 32) {
           const u32 j = jb + lane;
           u32 u = 0;
           bool hit = false;
-          if (j < h1.len) {
-            u = ldg(g.col + s1b + j);
-            hit = h0.has(u);
+          if (j < U.n1) {
+            u = ldg(U.s1 + j);
+            hit = fits ? us_add(T, U.sh, U.mask, u, 2u) : contains_sorted(U.s0, U.n0, u);
           }
           const u32 bm = __ballot_sync(0xffffffffu, hit);
           if (hit) I01[n01 + __popc(bm & lanemask_lt())] = u;
           n01 += __popc(bm);
         }
+        U.T = fits ? T : nullptr;
         __syncwarp();
       }
-      // per-child setup: lane c < nstep owns child cur + c
+      // ---- per-child setup: lane c < nstep owns child cur + c
       u32 v2 = 0, len = 0, pmv = 0;
       u64 st = 0;
       const bool valid = lane < (int)nstep;
@@ -472,11 +505,10 @@ __global__ void __launch_bounds__(kT4) mc4_last_kernel(Mc4Args a) {
         const u64 b2 = ldg(g.off + v2), e2 = ldg(g.off + v2 + 1);
         st = lower_bound_col(g.col, b2, e2, v0 + 1);
         len = (u32)(e2 - st);
-        pmv = (h0.has(v2) ? 1u : 0u) | (h1.has(v2) ? 2u : 0u);
-        aCand += (ldg(g.off + v0 + 1) - ldg(g.off + v0)) + (ldg(g.off + v1 + 1) - ldg(g.off + v1)) + (e2 - b2);
+        pmv = U.flags(v2);  // bit 0: v2 ~ v0, bit 1: v2 ~ v1
+        aCand += (u64)(ldg(g.off + v0 + 1) - ldg(g.off + v0)) + (ldg(g.off + v1 + 1) - ldg(g.off + v1)) + (e2 - b2);
       }
-      const u32 m = max(v1, v2);
-      // concatenated stream of the children's S2 ranges
+      // ---- concatenated stream of the non-empty children's S2 ranges
       u32 incl = len;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -484,63 +516,65 @@ __global__ void __launch_bounds__(kT4) mc4_last_kernel(Mc4Args a) {
         if (lane >= o) incl += t;
       }
       const u32 total = __shfl_sync(0xffffffffu, incl, 31);
-      s_cb[wid][lane] = st;
-      s_ex[wid][lane] = incl - len;
-      s_v2[wid][lane] = v2;
+      const u32 nz = __ballot_sync(0xffffffffu, len > 0);
+      const u32 rank = __popc(nz & lanemask_lt());
+      const u32 nnz = __popc(nz);
+      if (len > 0) {
+        s_cb[wid][rank] = st;
+        s_ex[wid][rank] = incl - len;
+        s_v2[wid][rank] = v2;
+      }
 #pragma unroll
       for (int ev = 0; ev < 4; ++ev) s_ev[wid][ev][lane] = 0;
       __syncwarp();
-      u32 P = 0;  // child owning candidate jb (children with len 0 are skipped by the scan)
+      u32 P = 0;
       for (u32 jb = 0; jb < total; jb += 32) {
         const u32 j = jb + lane;
-        // lane -> child: last c with ex[c] <= j and len[c] > 0 (binary search over 32)
-        u32 c = 0;
-        if (j < total) {
-          u32 lo_ = P, hi_ = nstep - 1;
-          while (lo_ < hi_) {
-            const u32 mid = (lo_ + hi_ + 1) >> 1;
-            if (s_ex[wid][mid] <= j) lo_ = mid;
-            else hi_ = mid - 1;
-          }
-          c = lo_;
-        }
+        // lane -> child by one OR-reduction over the children's start offsets
+        const u32 x = (P + 1 + lane < nnz) ? s_ex[wid][P + 1 + lane] : 0xffffffffu;
+        const u32 bit = (x - jb < 32u) ? (1u << (x - jb)) : 0u;
+        const u32 starts = __reduce_or_sync(0xffffffffu, bit);
+        const u32 c = P + __popc(starts & (lanemask_lt() | (1u << lane)));
+        P += __popc(starts);
         bool f2 = false, f11 = false, f01 = false, f12 = false;
         if (j < total) {
           const u32 u = ldg(g.col + s_cb[wid][c] + (j - s_ex[wid][c]));
-          const bool i0 = h0.has(u), i1 = h1.has(u);
-          const u32 c_v2 = s_v2[wid][c];  // thresholds of child c
-          const u32 c_m = max(v1, c_v2);
-          f2 = !i0 && !i1;
-          f11 = i0 && i1 && u > c_m;
-          f01 = i0 && !i1 && u > c_m;
-          f12 = i1 && !i0 && u > c_v2;
+          const u32 cv2 = s_v2[wid][c];
+          const u32 cm = max(v1, cv2);
+          const u32 f = U.flags(u);
+          f2 = f == 0;
+          f11 = f == 3 && u > cm;
+          f01 = f == 1 && u > cm;
+          f12 = f == 2 && u > cv2;
         }
-        // segmented per-child counts: head lane of each child segment adds popc
+        // segmented per-child counts: each segment's first lane adds its popcounts
         const u32 b2_ = __ballot_sync(0xffffffffu, f2), b11 = __ballot_sync(0xffffffffu, f11);
         const u32 b01 = __ballot_sync(0xffffffffu, f01), b12 = __ballot_sync(0xffffffffu, f12);
-        const u32 cprev = __shfl_up_sync(0xffffffffu, c, 1);
-        const bool head = (j < total) && (lane == 0 || cprev != c);
-        const u32 heads = __ballot_sync(0xffffffffu, head);
-        if (head) {
-          const u32 above = heads & ~((2u << lane) - 1u);  // heads after this lane
-          const u32 endl = above ? (__ffs(above) - 1) : 32u;
+        const u32 heads = starts | 1u;
+        if ((heads >> lane & 1u) && j < total) {
+          const u32 above = heads & ~((2u << lane) - 1u);
+          const u32 endl = above ? (u32)(__ffs(above) - 1) : 32u;
           const u32 seg = (endl >= 32 ? 0xffffffffu : ((1u << endl) - 1u)) & ~((1u << lane) - 1u);
           s_ev[wid][0][c] += __popc(b2_ & seg);
           s_ev[wid][1][c] += __popc(b11 & seg);
           s_ev[wid][2][c] += __popc(b01 & seg);
           s_ev[wid][3][c] += __popc(b12 & seg);
         }
-        P = __shfl_sync(0xffffffffu, c, 31);  // j of lane 31 < total unless this is the last step
         __syncwarp();
       }
-      __syncwarp();
-      // per-child class values, reduced per parent-mask value
+      // ---- per-child class values, reduced per parent-mask value
       u32 val[7] = {0, 0, 0, 0, 0, 0, 0};
       if (valid) {
-        const u32 e2c = s_ev[wid][0][lane], e11 = s_ev[wid][1][lane], e01 = s_ev[wid][2][lane],
-                  e12 = s_ev[wid][3][lane];
-        const u32 A0 = count_gt_global(g.col + s0b, h0.len, m);
-        const u32 B1 = count_gt_global(g.col + s1b, h1.len, v2);
+        u32 e2c = 0, e11 = 0, e01 = 0, e12 = 0;
+        if (len > 0) {
+          e2c = s_ev[wid][0][rank];
+          e11 = s_ev[wid][1][rank];
+          e01 = s_ev[wid][2][rank];
+          e12 = s_ev[wid][3][rank];
+        }
+        const u32 m = max(v1, v2);
+        const u32 A0 = count_gt_global(U.s0, U.n0, m);
+        const u32 B1 = count_gt_global(U.s1, U.n1, v2);
         const u32 Im = count_gt_plain(I01, n01, m);
         const u32 I2 = count_gt_plain(I01, n01, v2);
         val[0] = e11;
@@ -676,11 +710,9 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
 void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u32* idx2, const u32* vid2, u64 np,
                      unsigned long long* d_hist, cudaStream_t s, Timeline& tl, Stats& st) {
   if (np == 0) return;
-  const size_t smem = 2ull * kW4 * k4Slots * sizeof(u32);
   static int occ = 0;
   if (!occ) {
-    GPM_CUDA(cudaFuncSetAttribute(mc4_last_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mc4_last_kernel, kT4, smem));
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mc4_last_kernel, kT4, 0));
     occ = std::max(1, occ);
   }
   const u64 nitems = (np + k4Item - 1) / k4Item;
@@ -713,7 +745,7 @@ void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u
   a.cl_bits[5] = P(1, 3);
   a.cl_bits[6] = P(2, 3);
   size_t ev = tl.begin("extend_fused_L2", 0.0);
-  mc4_last_kernel<<<(unsigned)blocks, kT4, smem, s>>>(a);
+  mc4_last_kernel<<<(unsigned)blocks, kT4, 0, s>>>(a);
   GPM_CUDA(cudaGetLastError());
   tl.end(ev);
   tl.launches += 1;

@@ -201,7 +201,7 @@ struct Cursor {
 };
 
 template <int APP, int LEV, int MODE>
-__global__ void __launch_bounds__(kThreads) extend_kernel(ExtendArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) extend_kernel(ExtendArgs a) {
   constexpr int S = LEV + 1;  // parent embedding size
   constexpr int kWords = (int)(kBatch / 32);
   extern __shared__ unsigned long long shist[];
@@ -459,7 +459,7 @@ __global__ void item_root_kernel(const u64* __restrict__ items, u32 nr, u32* __r
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) root_kernel(RootArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) root_kernel(RootArgs a) {
   extern __shared__ __align__(16) u32 s_rhash[];  // [kThreads/32][kHashSlots]
   __shared__ u64 s_cb[kThreads / 32][32];
   __shared__ u32 s_ex[kThreads / 32][33];
@@ -550,14 +550,20 @@ __global__ void __launch_bounds__(kThreads) root_kernel(RootArgs a) {
     }
     u32 P = 0, c = 0, myword = 0;
     u32 wi = 0;
-    for (u32 jb = 0; jb < total; jb += 32, ++wi) {
-      const u32 j = jb + lane;
+    // lane -> parent for the step at jb: one OR-reduction over the parents'
+    // start offsets (every listed parent owns >= 1 candidate)
+    auto map_step = [&](u32 jb) -> u32 {
       const u32 x = (P + 1 + lane < nnz) ? sex[P + 1 + lane] : 0xffffffffu;
       const u32 bit = (x - jb < 32u) ? (1u << (x - jb)) : 0u;
       const u32 starts = __reduce_or_sync(0xffffffffu, bit);
       const u32 myp = P + __popc(starts & (lanemask_lt() | (1u << lane)));
       P += __popc(starts);
-      if (from_masks) {
+      return min(myp, nnz - 1);
+    };
+    if (from_masks) {
+      for (u32 jb = 0; jb < total; jb += 32, ++wi) {
+        const u32 j = jb + lane;
+        const u32 myp = map_step(jb);
         const u32 m = ldg(a.masks + mo + wi);
         if (m) {
           if (m >> lane & 1u) {
@@ -567,31 +573,39 @@ __global__ void __launch_bounds__(kThreads) root_kernel(RootArgs a) {
           }
           wpos += __popc(m);
         }
-        continue;
       }
-      bool ok = false;
-      u32 u = 0;
-      if (j < total) {
-        u = ldg(g.col + scb[myp] + (j - sex[myp]));
-        if (use_filter) {
-          ok = hs_has(filt, fsh, fmask, u);
-        } else {
-          ok = contains_sorted(g.col + ob, d0, u);
+    } else {
+      // two steps per iteration: both candidate loads in flight before the probes
+      for (u32 jb = 0; jb < total; jb += 64) {
+        u32 myp[2], u[2];
+        myp[0] = map_step(jb);
+        myp[1] = map_step(jb + 32);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const u32 j = jb + 32 * h + lane;
+          u[h] = j < total ? ldg(g.col + scb[myp[h]] + (j - sex[myp[h]])) : 0u;
         }
-      }
-      const u32 mask = __ballot_sync(0xffffffffu, ok);
-      if (MODE == kWrite) {
-        if (ok) {
-          const u64 o = wpos + __popc(mask & lanemask_lt());
-          a.out_idx[o] = sei[myp];
-          a.out_vid[o] = u;
-        }
-        wpos += __popc(mask);
-      } else {
-        c += __popc(mask);
-        if (MODE == kCount && mo != ~0ull) {
-          if ((wi & 31) == (u32)lane) myword = mask;
-          if ((wi & 31) == 31) a.masks[mo + (wi - 31) + lane] = myword;
+#pragma unroll
+        for (int h = 0; h < 2; ++h, ++wi) {
+          const u32 j = jb + 32 * h + lane;
+          if (jb + 32 * h >= total) break;
+          bool ok = false;
+          if (j < total) ok = use_filter ? hs_has(filt, fsh, fmask, u[h]) : contains_sorted(g.col + ob, d0, u[h]);
+          const u32 mask = __ballot_sync(0xffffffffu, ok);
+          if (MODE == kWrite) {
+            if (ok) {
+              const u64 o = wpos + __popc(mask & lanemask_lt());
+              a.out_idx[o] = sei[myp[h]];
+              a.out_vid[o] = u[h];
+            }
+            wpos += __popc(mask);
+          } else {
+            c += __popc(mask);
+            if (MODE == kCount && mo != ~0ull) {
+              if ((wi & 31) == (u32)lane) myword = mask;
+              if ((wi & 31) == 31) a.masks[mo + (wi - 31) + lane] = myword;
+            }
+          }
         }
       }
     }
@@ -707,7 +721,7 @@ void process(Ctx& c, VLevels L, u64 np) {
   Stats& st = *c.st;
   if (np == 0) return;
   if constexpr (APP == kAppMC && LEV == 2) {
-    if (last && c.k == 4 && !c.generic_mc) {
+    if (last && c.k == 4 && !c.generic_mc && c.G->n < (1u << 30)) {  // union-set tags need ids < 2^30
       mc4_last_staged(*c.G, L.idx[0], L.vid[0], L.idx[1], L.vid[1], np, c.d_hist, c.s, *c.tl, st);
       return;
     }

@@ -9,6 +9,9 @@ W = {
     "mc3s": ("mc", 3, 0, (19, 16, .57, .19, .19, 1, 0)),
     "mc4s": ("mc", 4, 0, (19, 8.6, .45, .15, .15, 1, 0)),
     "fsms": ("fsm", 4, 100, (15, 11, .45, .15, .15, 1, 32)),
+    "mc3": ("mc", 3, 0, (22, 16, .57, .19, .19, 1, 0)),
+    "mc4": ("mc", 4, 0, (22, 8.6, .45, .15, .15, 1, 0)),
+    "fsm": ("fsm", 4, 300, (17, 11, .45, .15, .15, 1, 32)),
 }
 app, k, sigma, (sc, ef, a, b, c, seed, nl) = W[sys.argv[1]]
 hg = P.generate_rmat(sc, ef, a, b, c, seed, nl, 101)
