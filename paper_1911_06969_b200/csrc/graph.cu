@@ -147,6 +147,15 @@ __global__ void orient_write_kernel(const u64* __restrict__ off, const u32* __re
 }
 
 // level 1 of an undirected graph: per vertex, entries v > u (u<v rule).
+// max_v (off[v+1] - off[v]) -> *md (atomicMax per warp)
+__global__ void max_degree_kernel(const u64* __restrict__ off, u32 n, u32* __restrict__ md) {
+  u32 best = 0;
+  for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < n; v += (u64)gridDim.x * blockDim.x)
+    best = max(best, (u32)(off[v + 1] - off[v]));
+  best = __reduce_max_sync(0xffffffffu, best);
+  if ((threadIdx.x & 31) == 0 && best) atomicMax(md, best);
+}
+
 __global__ void l1_count_kernel(const u64* __restrict__ off, const u32* __restrict__ col, u32 n,
                                 u64* __restrict__ cnt) {
   u64 u = blockIdx.x * (u64)blockDim.x + threadIdx.x;
@@ -315,6 +324,18 @@ void root_split(const gpm_graph& g, const u32* idx, const u32* vid, u64 n1, int 
   hi = rank == world - 1 ? n1 : std::min(res[1], n1);
 }
 
+// out-degree maximum of a freshly built device CSR (sets gpm_graph::max_deg)
+void set_max_degree(gpm_graph& out, cudaStream_t s) {
+  DBuf<u32> md(1, s);
+  GPM_CUDA(cudaMemsetAsync(md.get(), 0, sizeof(u32), s));
+  if (out.n) {
+    max_degree_kernel<<<std::min<unsigned>(grid_for(out.n, 256), 1184u), 256, 0, s>>>(out.d_off, out.n, md.get());
+    GPM_CUDA(cudaGetLastError());
+  }
+  GPM_CUDA(cudaMemcpyAsync(&out.max_deg, md.get(), sizeof(u32), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+}
+
 void orient_on_device(const gpm_graph& g, gpm_graph& out) {
   cudaStream_t s = out.stream;
   out.n = g.n;
@@ -348,7 +369,7 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
     GPM_CUDA(cudaMallocAsync((void**)&out.d_lab, sizeof(u32) * std::max<u32>(1, g.n), s));
     GPM_CUDA(cudaMemcpyAsync(out.d_lab, g.d_lab, sizeof(u32) * g.n, cudaMemcpyDeviceToDevice, s));
   }
-  GPM_CUDA(cudaStreamSynchronize(s));
+  set_max_degree(out, s);
 }
 
 // Host CSR -> device DAG in one pipelined call: the column array is copied in
@@ -418,7 +439,7 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
                                                                   out.d_col);
     GPM_CUDA(cudaGetLastError());
   }
-  GPM_CUDA(cudaStreamSynchronize(s));
+  set_max_degree(out, s);
 }
 
 }  // namespace gpm

@@ -41,11 +41,12 @@ namespace {
 
 constexpr int kT = 256;
 constexpr int kWarps = kT / 32;
-constexpr u32 kWSlots = 1024;   // per-warp hash slots (4 KB)
-constexpr u32 kWKeys = 512;     // roots with |S0| <= this use the warp kernel
+constexpr u32 kWSlots = 2048;   // per-warp hash slots (8 KB): load <= 1/8 up to kWKeys
+constexpr u32 kWKeys = 256;     // roots with |S0| <= this use the warp kernel
 constexpr u32 kBSlots = 16384;  // per-CTA hash slots (64 KB)
-constexpr u32 kBKeys = 8192;    // S0 tile size of the block kernel
-constexpr u32 kPB = 32 * kWarps;  // parents per block item
+constexpr u32 kBKeys = 2048;    // S0 tile of the block kernel (load 1/8)
+constexpr u32 kPB = 1024;       // parents per block item (warps grab 32 at a time)
+
 // first index i in [b, e) with col[i] >= key
 __device__ __forceinline__ u64 lower_bound_col(const u32* __restrict__ col, u64 b, u64 e, u32 key) {
   while (b < e) {
@@ -110,77 +111,91 @@ __global__ void mc3_root_of_kernel(const u64* __restrict__ l1s, u32 n, u64 e0, u
   out[t] = (u32)lo;
 }
 
-// Streams the concatenated pos-1 candidate ranges of <= 32 parents (one per
-// lane: range [st, st+len) of col, parent vertex v1) against the staged set.
-// Returns (X, tri) counts for the warp (uniform across lanes).
+// Streams the pos-1 candidate ranges of <= 32 parents (lane i: col[st, st+len),
+// parent vertex v1) against the staged set; adds the warp's hits (X) and hits
+// above v1 (tri).  Segments of >= 32 candidates are streamed one at a time
+// (warp-uniform parent, coalesced, two loads in flight); shorter ones are
+// packed 32 candidates per step with the OR-reduction lane -> parent map.
 __device__ __forceinline__ void stream_parents(const u32* __restrict__ col, const u32* T, u32 sh, u32 mask, u64 st,
                                                u32 len, u32 v1, u64* scb, u32* sex, u32* sv1, unsigned long long& X,
                                                unsigned long long& tri) {
   const int lane = threadIdx.x & 31;
-  u32 incl = len;
+  u32 cx = 0, ct = 0;
+  // ---- long segments, one after the other
+  u32 todo = __ballot_sync(0xffffffffu, len >= 32);
+  while (todo) {
+    const int i = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const u64 b = __shfl_sync(0xffffffffu, st, i);
+    const u32 L = __shfl_sync(0xffffffffu, len, i);
+    const u32 w = __shfl_sync(0xffffffffu, v1, i);
+    u32 j = 0;
+    for (; j + 64 <= L; j += 64) {
+      const u32 u0 = ldg(col + b + j + lane);
+      const u32 u1 = ldg(col + b + j + 32 + lane);
+      const bool h0 = hs_has(T, sh, mask, u0);
+      const bool h1 = hs_has(T, sh, mask, u1);
+      cx += __popc(__ballot_sync(0xffffffffu, h0)) + __popc(__ballot_sync(0xffffffffu, h1));
+      ct += __popc(__ballot_sync(0xffffffffu, h0 && u0 > w)) + __popc(__ballot_sync(0xffffffffu, h1 && u1 > w));
+    }
+    for (; j < L; j += 32) {
+      const bool v = j + lane < L;
+      const u32 u0 = v ? ldg(col + b + j + lane) : 0u;
+      const bool h0 = v && hs_has(T, sh, mask, u0);
+      cx += __popc(__ballot_sync(0xffffffffu, h0));
+      ct += __popc(__ballot_sync(0xffffffffu, h0 && u0 > w));
+    }
+  }
+  // ---- short segments, packed
+  const u32 sl = len < 32 ? len : 0u;
+  u32 incl = sl;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += t;
   }
   const u32 total = __shfl_sync(0xffffffffu, incl, 31);
-  if (total == 0) return;
-  const u32 nz = __ballot_sync(0xffffffffu, len > 0);
-  const u32 rank = __popc(nz & lanemask_lt());
-  __syncwarp();
-  if (len > 0) {
-    scb[rank] = st;
-    sex[rank] = incl - len;
-    sv1[rank] = v1;
-  }
-  const u32 nnz = __popc(nz);
-  __syncwarp();
-  u32 P = 0;
-  u32 cx = 0, ct = 0;
-  // two 32-candidate steps per iteration: both loads are in flight before
-  // either probe (memory-level parallelism for the L2/HBM latency)
-  for (u32 jb = 0; jb < total; jb += 64) {
-    u32 myp[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const u32 jh = jb + 32 * h;
-      // lane -> parent by one OR-reduction over the parents' start offsets
+  if (total) {
+    const u32 nz = __ballot_sync(0xffffffffu, sl > 0);
+    const u32 rank = __popc(nz & lanemask_lt());
+    __syncwarp();
+    if (sl > 0) {
+      scb[rank] = st;
+      sex[rank] = incl - sl;
+      sv1[rank] = v1;
+    }
+    const u32 nnz = __popc(nz);
+    __syncwarp();
+    u32 P = 0;
+    for (u32 jb = 0; jb < total; jb += 32) {
+      const u32 jj = jb + lane;
       const u32 x = (P + 1 + lane < nnz) ? sex[P + 1 + lane] : 0xffffffffu;
-      const u32 bit = (x - jh < 32u) ? (1u << (x - jh)) : 0u;
+      const u32 bit = (x - jb < 32u) ? (1u << (x - jb)) : 0u;
       const u32 starts = __reduce_or_sync(0xffffffffu, bit);
-      myp[h] = min(P + __popc(starts & (lanemask_lt() | (1u << lane))), nnz - 1);
+      const u32 myp = min(P + __popc(starts & (lanemask_lt() | (1u << lane))), nnz - 1);
       P += __popc(starts);
-    }
-    u32 u[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const u32 j = jb + 32 * h + lane;
-      u[h] = j < total ? ldg(col + scb[myp[h]] + (j - sex[myp[h]])) : 0u;
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const u32 j = jb + 32 * h + lane;
       bool hit = false, t = false;
-      if (j < total) {
-        hit = hs_has(T, sh, mask, u[h]);
-        t = hit && u[h] > sv1[myp[h]];
+      if (jj < total) {
+        const u32 u = ldg(col + scb[myp] + (jj - sex[myp]));
+        hit = hs_has(T, sh, mask, u);
+        t = hit && u > sv1[myp];
       }
       cx += __popc(__ballot_sync(0xffffffffu, hit));
       ct += __popc(__ballot_sync(0xffffffffu, t));
     }
+    __syncwarp();
   }
   X += cx;
   tri += ct;
-  __syncwarp();
 }
 
-__global__ void __launch_bounds__(kT, 4) mc3_warp_kernel(Mc3Args a) {
-  __shared__ __align__(16) u32 s_tab[kWarps][kWSlots];
+__global__ void __launch_bounds__(kT, 3) mc3_warp_kernel(Mc3Args a) {
+  extern __shared__ __align__(16) u32 s_wtab[];  // [kWarps][kWSlots]
   __shared__ u64 s_cb[kWarps][32];
   __shared__ u32 s_ex[kWarps][32];
   __shared__ u32 s_v1[kWarps][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  u32* T = s_tab[wid];
+  u32* T = s_wtab + wid * kWSlots;
   const DevGraph& g = a.g;
   unsigned long long aX = 0, aTri = 0, aC0 = 0, aLen = 0, aCand = 0;
   u32 troot = 0xffffffffu, sh = 0, mask = 0;
@@ -204,7 +219,7 @@ __global__ void __launch_bounds__(kT, 4) mc3_warp_kernel(Mc3Args a) {
     if (r != troot) {
       troot = r;
       u32 cap = 64;
-      while (cap < 2 * ns) cap <<= 1;
+      while (cap < 8 * ns && cap < kWSlots) cap <<= 1;
       mask = cap - 1;
       sh = 32 - (31 - __clz(cap));
       for (u32 i = lane * 4; i < cap; i += 128) *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
@@ -245,15 +260,16 @@ __global__ void __launch_bounds__(kT, 4) mc3_warp_kernel(Mc3Args a) {
   }
 }
 
-// Roots with |S0| > kWKeys: item = (root, S0 tile, chunk of kPB parents); the
-// CTA stages the tile, each warp streams 32 parents' candidates inside the
-// tile's id range [idlo, idhi).
+// Roots with |S0| > kWKeys: item = (root, S0 tile, chunk of <= kPB parents).
+// The CTA stages the tile; warps grab 32 parents at a time from the chunk and
+// stream their candidates inside the tile's id range [idlo, idhi).
 __global__ void __launch_bounds__(kT, 3) mc3_block_kernel(Mc3Args a) {
   extern __shared__ __align__(16) u32 s_btab[];
   __shared__ u64 s_cb[kWarps][32];
   __shared__ u32 s_ex[kWarps][32];
   __shared__ u32 s_v1[kWarps][32];
   __shared__ u64 s_item;
+  __shared__ u32 s_next;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const DevGraph& g = a.g;
   constexpr u32 mask = kBSlots - 1;
@@ -261,7 +277,10 @@ __global__ void __launch_bounds__(kT, 3) mc3_block_kernel(Mc3Args a) {
   unsigned long long aX = 0, aTri = 0, aC0 = 0, aLen = 0, aCand = 0;
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_item = atomicAdd(a.ctr, 1ull);
+    if (threadIdx.x == 0) {
+      s_item = atomicAdd(a.ctr, 1ull);
+      s_next = 0;
+    }
     __syncthreads();
     const u64 item = s_item;
     if (item >= a.nitems) break;
@@ -286,24 +305,31 @@ __global__ void __launch_bounds__(kT, 3) mc3_block_kernel(Mc3Args a) {
     const u32 idlo = (t == 0) ? r + 1 : ldg(g.col + sb + k0);
     const bool last_tile = (t + 1 == ntiles);
     const u32 idhi = last_tile ? 0xffffffffu : ldg(g.col + sb + k1);
-    const u64 p = pa0 + c * kPB + (u64)wid * 32 + lane;
-    const u64 pb = min(pe, pa0 + (c + 1) * kPB);
-    u64 st = 0;
-    u32 len = 0, v1 = 0;
-    if (p < pb) {
-      const u32 ip = (u32)(p - s);
-      v1 = ldg(g.col + sb + ip);
-      const u64 b1 = ldg(g.off + v1), e1 = ldg(g.off + v1 + 1);
-      st = lower_bound_col(g.col, b1, e1, idlo);
-      const u64 en = last_tile ? e1 : lower_bound_col(g.col, st, e1, idhi);
-      len = (u32)(en - st);
-      aLen += len;
-      if (t == 0) {
-        aC0 += ns - ip - 1;
-        aCand += (oe - ob) + (e1 - b1);
+    const u64 cb = pa0 + c * kPB;
+    const u32 cn = (u32)(min(pe, cb + kPB) - cb);
+    for (;;) {
+      u32 sub = 0;
+      if (lane == 0) sub = atomicAdd(&s_next, 32u);
+      sub = __shfl_sync(0xffffffffu, sub, 0);
+      if (sub >= cn) break;
+      const u64 p = cb + sub + lane;
+      u64 st = 0;
+      u32 len = 0, v1 = 0;
+      if (sub + lane < cn) {
+        const u32 ip = (u32)(p - s);
+        v1 = ldg(g.col + sb + ip);
+        const u64 b1 = ldg(g.off + v1), e1 = ldg(g.off + v1 + 1);
+        st = lower_bound_col(g.col, b1, e1, idlo);
+        const u64 en = last_tile ? e1 : lower_bound_col(g.col, st, e1, idhi);
+        len = (u32)(en - st);
+        aLen += len;
+        if (t == 0) {
+          aC0 += ns - ip - 1;
+          aCand += (oe - ob) + (e1 - b1);
+        }
       }
+      stream_parents(g.col, s_btab, sh, mask, st, len, v1, s_cb[wid], s_ex[wid], s_v1[wid], aX, aTri);
     }
-    stream_parents(g.col, s_btab, sh, mask, st, len, v1, s_cb[wid], s_ex[wid], s_v1[wid], aX, aTri);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -470,7 +496,7 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
         const bool fits = U.n0 + U.n1 <= k4Keys;
         if (fits) {
           u32 cap = 64;
-          while (cap < 2 * (U.n0 + U.n1)) cap <<= 1;
+          while (cap < 8 * (U.n0 + U.n1) && cap < k4Slots) cap <<= 1;  // load <= 1/8 while it fits
           U.mask = cap - 1;
           U.sh = 32 - (31 - __clz(cap));
           __syncwarp();
@@ -659,9 +685,11 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
   const int sms = sm_count();
   size_t rec = tl.recs.size();
   if (NS) {
+    const size_t wsmem = (size_t)kWarps * kWSlots * sizeof(u32);
     static int occ = 0;
     if (!occ) {
-      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mc3_warp_kernel, kT, 0));
+      GPM_CUDA(cudaFuncSetAttribute(mc3_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mc3_warp_kernel, kT, wsmem));
       occ = std::max(1, occ);
     }
     const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sms * occ, (NS + kWarps - 1) / kWarps));
@@ -672,7 +700,7 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
     w.ctr = ctr.get();
     w.grab = std::max<u64>(1, std::min<u64>(4, NS / (blocks * kWarps * 64)));
     size_t ev = tl.begin("extend_fused_L1", 0.0);
-    mc3_warp_kernel<<<(unsigned)blocks, kT, 0, s>>>(w);
+    mc3_warp_kernel<<<(unsigned)blocks, kT, wsmem, s>>>(w);
     GPM_CUDA(cudaGetLastError());
     tl.end(ev);
     ++tl.launches;

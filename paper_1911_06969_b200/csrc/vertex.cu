@@ -441,6 +441,7 @@ struct RootArgs {
   u64 mcap;
   unsigned long long* total;  // FUSED
   unsigned long long* cand;   // candidates streamed (stats)
+  u32 hstride;                // per-warp hash slots (>= 2 x max out-degree, <= kHashSlots)
 };
 
 // work items = (root, 32-parent chunk) so hub roots spread over warps
@@ -459,13 +460,13 @@ __global__ void item_root_kernel(const u64* __restrict__ items, u32 nr, u32* __r
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 2) root_kernel(RootArgs a) {
+__global__ void __launch_bounds__(kThreads, 6) root_kernel(RootArgs a) {
   extern __shared__ __align__(16) u32 s_rhash[];  // [kThreads/32][kHashSlots]
   __shared__ u64 s_cb[kThreads / 32][32];
   __shared__ u32 s_ex[kThreads / 32][33];
   __shared__ u32 s_ei[kThreads / 32][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  u32* filt = s_rhash + wid * kHashSlots;
+  u32* filt = s_rhash + wid * a.hstride;
   u32 fsh = 0, fmask = 0;
   u64* scb = s_cb[wid];
   u32* sex = s_ex[wid];
@@ -858,10 +859,15 @@ void process(Ctx& c, VLevels L, u64 np) {
 template <int MODE>
 void launch_root(Ctx& c, RootArgs& a, const char* what, double bytes) {
   auto kern = root_kernel<MODE>;
-  const size_t smem = (size_t)(kThreads / 32) * kHashSlots * sizeof(u32);
-  static int occ = 0;
+  // hash capacity for the largest staged out-list (<= kFilterMax keys)
+  u32 hs = 64;
+  while (hs < 2 * std::min<u32>(c.G->max_deg ? c.G->max_deg : kFilterMax, kFilterMax)) hs <<= 1;
+  a.hstride = hs;
+  const size_t smem = (size_t)(kThreads / 32) * hs * sizeof(u32);
+  static int occ_by_hs[16] = {0};
+  int& occ = occ_by_hs[31 - __builtin_clz(hs)];
   if (occ == 0) {
-    GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kThreads / 32 * kHashSlots * 4)));
     GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
     occ = std::max(1, occ);
   }
