@@ -24,18 +24,44 @@ std::string canon_text(u64 key, int nv_hint, int label_bits, const std::vector<u
   u32 mask = 0;
   pat::decode(key, label_bits, &nv, lab, &mask);
   (void)nv_hint;
-  std::string s = "k=" + std::to_string(nv) + ";L=";
+  // "k=<n>;L=l0,l1,..;E=(i,j)..", formatted without iostreams:
+  // FSM can emit ~10^6 patterns per call
+  char buf[256];
+  char* o = buf;
+  auto put_u = [&](u32 v) {
+    char t[12];
+    int n = 0;
+    do {
+      t[n++] = (char)('0' + v % 10);
+      v /= 10;
+    } while (v);
+    while (n) *o++ = t[--n];
+  };
+  *o++ = 'k';
+  *o++ = '=';
+  put_u((u32)nv);
+  *o++ = ';';
+  *o++ = 'L';
+  *o++ = '=';
   for (int i = 0; i < nv; ++i) {
-    if (i) s += ",";
+    if (i) *o++ = ',';
     u32 v = lab[i];
     if (label_values && !label_values->empty()) v = (*label_values)[lab[i]];
-    s += std::to_string(v);
+    put_u(v);
   }
-  s += ";E=";
+  *o++ = ';';
+  *o++ = 'E';
+  *o++ = '=';
   for (int a = 0; a < nv; ++a)
     for (int b = a + 1; b < nv; ++b)
-      if (mask >> pat::pair_index(a, b, nv) & 1u) s += "(" + std::to_string(a) + "," + std::to_string(b) + ")";
-  return s;
+      if (mask >> pat::pair_index(a, b, nv) & 1u) {
+        *o++ = '(';
+        put_u((u32)a);
+        *o++ = ',';
+        put_u((u32)b);
+        *o++ = ')';
+      }
+  return std::string(buf, o);
 }
 
 // Sum a host u64 vector across ranks through the exchange hook.

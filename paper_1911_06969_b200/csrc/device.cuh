@@ -91,13 +91,14 @@ __device__ __forceinline__ bool hs_has(const u32* T, u32 sh, u32 mask, u32 v) {
     h = (h + 1) & mask;
   }
 }
-// Warp-collective: stages col[b, b+len) (len <= cap/2) into T with the
-// smallest power-of-two capacity >= max(64, 2 len); returns (sh, mask).
-__device__ __forceinline__ void hs_stage_warp(u32* T, const u32* __restrict__ col, u64 b, u32 len, u32& sh,
-                                              u32& mask) {
+// Warp-collective: stages col[b, b+len) into T (maxcap >= 2 len slots) with
+// the smallest power-of-two capacity >= 8 len (load <= 1/8, short probe runs)
+// that fits maxcap; returns (sh, mask).
+__device__ __forceinline__ void hs_stage_warp(u32* T, const u32* __restrict__ col, u64 b, u32 len, u32 maxcap,
+                                              u32& sh, u32& mask) {
   const int lane = threadIdx.x & 31;
   u32 cap = 64;
-  while (cap < 2 * len) cap <<= 1;
+  while (cap < 8 * len && cap < maxcap) cap <<= 1;
   mask = cap - 1;
   sh = 32 - (31 - __clz(cap));
   __syncwarp();

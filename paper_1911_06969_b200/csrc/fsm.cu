@@ -25,6 +25,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <parallel/algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -166,9 +167,11 @@ __device__ __forceinline__ u64 child_code(const EEmb<LEV>& E, const DevGraph& g,
   return pat::make_code(cnv, lab, mask, LB);
 }
 
+// Open-addressing table of quick codes; entry = {key, val} in 16 B so a probe
+// touches one sector.  val = embedding count during pass A, then
+// (pattern id << 32 | packed PositionMap) once the level is canonicalised.
 struct Hash {
-  unsigned long long* keys;    // 0 = empty
-  unsigned long long* counts;
+  unsigned long long* ent;     // 2 x capacity: ent[2h] key (0 = empty), ent[2h+1] val
   u64 mask;                    // capacity - 1
   unsigned long long* used;    // inserted keys
   int* overflow;
@@ -192,21 +195,21 @@ __device__ __forceinline__ void hash_add(const Hash& H, u64 key, unsigned long l
   if (*(volatile int*)H.overflow) return;
   u64 h = hash64(key) & H.mask;
   for (int probe = 0; probe < kMaxProbe; ++probe) {
-    unsigned long long cur = H.keys[h];
+    unsigned long long cur = H.ent[2 * h];
     if (cur == key) {
-      atomicAdd(H.counts + h, c);
+      atomicAdd(H.ent + 2 * h + 1, c);
       return;
     }
     if (cur == 0) {
-      unsigned long long prev = atomicCAS(H.keys + h, 0ull, (unsigned long long)key);
+      unsigned long long prev = atomicCAS(H.ent + 2 * h, 0ull, (unsigned long long)key);
       if (prev == 0ull) {
         unsigned long long n = atomicAdd(H.used, 1ull);
         if (n * 2 >= H.mask) atomicOr(H.overflow, 1);
-        atomicAdd(H.counts + h, c);
+        atomicAdd(H.ent + 2 * h + 1, c);
         return;
       }
       if (prev == key) {
-        atomicAdd(H.counts + h, c);
+        atomicAdd(H.ent + 2 * h + 1, c);
         return;
       }
     }
@@ -215,10 +218,12 @@ __device__ __forceinline__ void hash_add(const Hash& H, u64 key, unsigned long l
   atomicOr(H.overflow, 2);
 }
 
+__device__ __forceinline__ u64 hash_info(const Hash& H, u64 slot) { return H.ent[2 * slot + 1]; }
+
 __device__ __forceinline__ u64 hash_find(const Hash& H, u64 key) {
   u64 h = hash64(key) & H.mask;
   for (int probe = 0; probe < kMaxProbe; ++probe) {
-    unsigned long long cur = H.keys[h];
+    unsigned long long cur = H.ent[2 * h];
     if (cur == key) return h;
     if (cur == 0) return ~0ull;
     h = (h + 1) & H.mask;
@@ -236,8 +241,6 @@ struct FsmArgs {
   unsigned long long* ctr;
   int LB;
   Hash H;
-  const u32* slot_pid;    // hash slot -> pattern id
-  const u32* slot_perm;   // hash slot -> packed PositionMap (3 bits / position)
   const u32* bslot;       // pattern -> bitmap slot or ~0
   u32* bitmaps;
   u64 words;
@@ -253,11 +256,11 @@ struct FsmArgs {
   unsigned long long* accepted;
 };
 
-__device__ __forceinline__ void domain_or(const FsmArgs& a, u64 slot, const u32* cv, int cnv) {
-  const u32 pid = a.slot_pid[slot];
+__device__ __forceinline__ void domain_or(const FsmArgs& a, u64 info, const u32* cv, int cnv) {
+  const u32 pid = (u32)(info >> 32);
   const u32 bs = a.bslot[pid];
   if (bs < a.round_lo || bs >= a.round_hi) return;
-  const u32 perm = a.slot_perm[slot];
+  const u32 perm = (u32)info;
   u32* base = a.bitmaps + (u64)(bs - a.round_lo) * a.kpos * a.words;
   for (int i = 0; i < cnv; ++i) {
     const u32 cp = (perm >> (3 * i)) & 7u;
@@ -395,14 +398,12 @@ __global__ void __launch_bounds__(kThreads) eextend_kernel(FsmArgs a) {
         }
       } else if (MODE == kDomain) {
         if (ok) {
-          const u64 slot = hash_find(a.H, code);
-          domain_or(a, slot, cv, cnv);
+          domain_or(a, hash_info(a.H, hash_find(a.H, code)), cv, cnv);
         }
       } else {
         bool keep = false;
         if (ok) {
-          const u64 slot = hash_find(a.H, code);
-          keep = a.frequent[a.slot_pid[slot]] != 0;
+          keep = a.frequent[hash_info(a.H, hash_find(a.H, code)) >> 32] != 0;
         }
         const u32 mask = __ballot_sync(0xffffffffu, keep);
         if (MODE == kSCount) {
@@ -450,19 +451,20 @@ __global__ void l1_kernel(FsmArgs a, const u32* __restrict__ idx, const u32* __r
     } else if (MODE == kDomain) {
       if (act) {
         u32 cv[2] = {u, v};
-        domain_or(a, hash_find(a.H, code), cv, 2);
+        domain_or(a, hash_info(a.H, hash_find(a.H, code)), cv, 2);
       }
     } else if (act) {
-      keep[i] = a.frequent[a.slot_pid[hash_find(a.H, code)]];
+      keep[i] = a.frequent[hash_info(a.H, hash_find(a.H, code)) >> 32];
     }
   }
 }
 
 // canonicalize every occupied hash slot once (reduce step 2)
-__global__ void canon_slots_kernel(const unsigned long long* __restrict__ keys, u64 cap, int LB,
-                                   u64* __restrict__ canon, u32* __restrict__ perm) {
+__global__ void canon_slots_kernel(const unsigned long long* __restrict__ ent, u64 cap, int LB,
+                                   u64* __restrict__ canon, u32* __restrict__ perm, u64* __restrict__ counts) {
   for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < cap; s += (u64)gridDim.x * blockDim.x) {
-    const u64 key = keys[s];
+    const u64 key = ent[2 * s];
+    counts[s] = ent[2 * s + 1];
     if (!key) {
       canon[s] = ~0ull;
       continue;
@@ -479,7 +481,7 @@ __global__ void canon_slots_kernel(const unsigned long long* __restrict__ keys, 
 }
 
 __global__ void slot_pid_kernel(const u64* __restrict__ canon, u64 cap, const u64* __restrict__ gkeys, u64 P,
-                                u32* __restrict__ slot_pid) {
+                                const u32* __restrict__ perm, unsigned long long* __restrict__ ent) {
   for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < cap; s += (u64)gridDim.x * blockDim.x) {
     const u64 c = canon[s];
     if (c == ~0ull) continue;
@@ -489,7 +491,7 @@ __global__ void slot_pid_kernel(const u64* __restrict__ canon, u64 cap, const u6
       if (gkeys[mid] < c) lo = mid + 1;
       else hi = mid;
     }
-    slot_pid[s] = (u32)lo;
+    ent[2 * s + 1] = ((unsigned long long)lo << 32) | perm[s];
   }
 }
 
@@ -575,10 +577,10 @@ struct Fsm {
   // Reduce state for one level
   struct Level {
     u64 cap = 0;
-    DBuf<unsigned long long> keys, counts, used;
+    DBuf<unsigned long long> ent, used;
     DBuf<int> overflow;
     DBuf<u64> canon;
-    DBuf<u32> perm, slot_pid, bslot, bs_to_pid;
+    DBuf<u32> perm, bslot, bs_to_pid;
     DBuf<u8> frequent;
     std::vector<u64> gkeys_h, gcount_h, mni_h;
     DBuf<u64> gkeys;
@@ -587,17 +589,15 @@ struct Fsm {
   };
 
   Hash hash_of(Level& R) {
-    return Hash{R.keys.get(), R.counts.get(), R.cap - 1, R.used.get(), R.overflow.get()};
+    return Hash{R.ent.get(), R.cap - 1, R.used.get(), R.overflow.get()};
   }
 
   void alloc_hash(Level& R, u64 cap) {
     R.cap = cap;
-    R.keys.alloc(cap, s);
-    R.counts.alloc(cap, s);
+    R.ent.alloc(2 * cap, s);
     R.used.alloc(1, s);
     R.overflow.alloc(1, s);
-    GPM_CUDA(cudaMemsetAsync(R.keys.get(), 0, sizeof(unsigned long long) * cap, s));
-    GPM_CUDA(cudaMemsetAsync(R.counts.get(), 0, sizeof(unsigned long long) * cap, s));
+    GPM_CUDA(cudaMemsetAsync(R.ent.get(), 0, sizeof(unsigned long long) * 2 * cap, s));
     GPM_CUDA(cudaMemsetAsync(R.used.get(), 0, sizeof(unsigned long long), s));
     GPM_CUDA(cudaMemsetAsync(R.overflow.get(), 0, sizeof(int), s));
   }
@@ -607,15 +607,14 @@ struct Fsm {
   void canon_and_group(Level& R) {
     R.canon.alloc(R.cap, s);
     R.perm.alloc(R.cap, s);
-    R.slot_pid.alloc(R.cap, s);
-    canon_slots_kernel<<<grid1(R.cap), 256, 0, s>>>(R.keys.get(), R.cap, LB, R.canon.get(), R.perm.get());
+    DBuf<unsigned long long> cc(R.cap, s), cc2(R.cap, s);
+    canon_slots_kernel<<<grid1(R.cap), 256, 0, s>>>(R.ent.get(), R.cap, LB, R.canon.get(), R.perm.get(),
+                                                    reinterpret_cast<u64*>(cc.get()));
     GPM_CUDA(cudaGetLastError());
     ++tl.launches;
     // compact (canon, count) of occupied slots, sort by canon, reduce by key
     DBuf<u64> ck(R.cap, s), ck2(R.cap, s);
-    DBuf<unsigned long long> cc(R.cap, s), cc2(R.cap, s);
     GPM_CUDA(cudaMemcpyAsync(ck.get(), R.canon.get(), sizeof(u64) * R.cap, cudaMemcpyDeviceToDevice, s));
-    GPM_CUDA(cudaMemcpyAsync(cc.get(), R.counts.get(), sizeof(u64) * R.cap, cudaMemcpyDeviceToDevice, s));
     size_t tmp = 0;
     GPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ck.get(), ck2.get(), cc.get(), cc2.get(), (int64_t)R.cap, 0,
                                              64, s));
@@ -676,7 +675,7 @@ struct Fsm {
     R.gkeys.alloc(std::max<u64>(1, R.P), s);
     if (R.P)
       GPM_CUDA(cudaMemcpyAsync(R.gkeys.get(), R.gkeys_h.data(), sizeof(u64) * R.P, cudaMemcpyHostToDevice, s));
-    slot_pid_kernel<<<grid1(R.cap), 256, 0, s>>>(R.canon.get(), R.cap, R.gkeys.get(), R.P, R.slot_pid.get());
+    slot_pid_kernel<<<grid1(R.cap), 256, 0, s>>>(R.canon.get(), R.cap, R.gkeys.get(), R.P, R.perm.get(), R.ent.get());
     GPM_CUDA(cudaGetLastError());
     ++tl.launches;
     // count pre-filter -> bitmap slots (MNI <= count)
@@ -731,9 +730,14 @@ struct Fsm {
   }
 
   void record(Level& R, int level) {
+    std::vector<u64> sel;
     for (u64 p = 0; p < R.P; ++p)
-      if (R.gcount_h[p] >= sigma && R.mni_h[p] >= sigma)
-        res.patterns.push_back({canon_text(R.gkeys_h[p], 0, LB, &G.label_values), R.mni_h[p], level});
+      if (R.gcount_h[p] >= sigma && R.mni_h[p] >= sigma) sel.push_back(p);
+    const size_t base = res.patterns.size();
+    res.patterns.resize(base + sel.size());
+#pragma omp parallel for schedule(static)
+    for (size_t i = 0; i < sel.size(); ++i)
+      res.patterns[base + i] = {canon_text(R.gkeys_h[sel[i]], 0, LB, &G.label_values), R.mni_h[sel[i]], level};
   }
 
   FsmArgs base_args(Level& R) {
@@ -765,8 +769,6 @@ struct Fsm {
     canon_and_group(R);
     domains_and_mni(R, 2, [&](u32* bm, u64 words, int kpos, u32 lo, u32 hi) {
       FsmArgs a = base_args(R);
-      a.slot_pid = R.slot_pid.get();
-      a.slot_perm = R.perm.get();
       a.bslot = R.bslot.get();
       a.bitmaps = bm;
       a.words = words;
@@ -785,7 +787,6 @@ struct Fsm {
     DBuf<u8> keep(n1, s);
     {
       FsmArgs a = base_args(R);
-      a.slot_pid = R.slot_pid.get();
       a.frequent = R.frequent.get();
       l1_kernel<kSCount><<<grid1(n1), 256, 0, s>>>(a, idx.get(), vid.get(), n1, keep.get());
       GPM_CUDA(cudaGetLastError());
@@ -883,8 +884,10 @@ struct Fsm {
       return a;
     };
     // first guess: previous level's distinct quick codes x fan-out, grown x8 on overflow
+    // distinct quick codes <= accepted <= candidates W: size for 2 W (capped at
+    // 2^26 entries = 1 GB) so the pass rarely has to regrow and re-run
     u64 cap = 1u << 16;
-    while (cap < std::min<u64>(u64(1) << 26, 64 * prev_unique)) cap <<= 1;
+    while (cap < std::min<u64>(u64(1) << 26, std::max<u64>(2 * W, 64 * prev_unique))) cap <<= 1;
     for (;;) {
       alloc_hash(R, cap);
       GPM_CUDA(cudaMemsetAsync(accepted.get(), 0, sizeof(unsigned long long), s));
@@ -908,8 +911,6 @@ struct Fsm {
     domains_and_mni(R, LEV + 2, [&](u32* bm, u64 words, int kpos, u32 lo, u32 hi) {
       if (!nb) return;
       FsmArgs a = args(R);
-      a.slot_pid = R.slot_pid.get();
-      a.slot_perm = R.perm.get();
       a.bslot = R.bslot.get();
       a.bitmaps = bm;
       a.words = words;
@@ -926,7 +927,6 @@ struct Fsm {
     GPM_CUDA(cudaMemsetAsync(cnt.get() + nb, 0, sizeof(u64), s));
     {
       FsmArgs a = args(R);
-      a.slot_pid = R.slot_pid.get();
       a.frequent = R.frequent.get();
       a.cnt = cnt.get();
       launch<LEV>(a, kSCount, "fsm_extend_filter_count", bytes_in);
@@ -940,7 +940,6 @@ struct Fsm {
     oh.alloc(std::max<u64>(1, T), s);
     if (T) {
       FsmArgs a = args(R);
-      a.slot_pid = R.slot_pid.get();
       a.frequent = R.frequent.get();
       a.boffs = cnt.get();
       a.out_base = 0;
@@ -1034,7 +1033,7 @@ struct Fsm {
       for (size_t i = 0; i < st.candidates.size(); ++i) st.candidates[i] = v[L2 + i];
       st.balg = (double)v.back();
     }
-    std::sort(res.patterns.begin(), res.patterns.end(), [](const gpm_result::Pattern& x, const gpm_result::Pattern& y) {
+    __gnu_parallel::sort(res.patterns.begin(), res.patterns.end(), [](const gpm_result::Pattern& x, const gpm_result::Pattern& y) {
       if (x.level != y.level) return x.level < y.level;
       if (x.support != y.support) return x.support > y.support;
       return x.text < y.text;

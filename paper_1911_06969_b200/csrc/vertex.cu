@@ -54,6 +54,7 @@ constexpr u64 kItemGrab = 8;        // root-kernel work items per atomic grab
 constexpr u64 kBatchGrab = 4;       // generic-engine batches per atomic grab
 constexpr u32 kHashSlots = 1024;    // per-warp exact hash set of the root's out-list (4 KB)
 constexpr u32 kFilterMax = 512;     // out-lists longer than this are probed by binary search
+constexpr u64 kMaskChunk = 4096;    // ballot-mask words a warp reserves at a time
 
 struct VLevels {
   const u32* idx[kMaxLevels];
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 2) extend_kernel(ExtendArgs a) {
           const u32 d = (u32)(key >> 40);
           const u64 qb = key & ((u64(1) << 40) - 1);
           fok = d <= kFilterMax;
-          if (fok) hs_stage_warp(filt, g.col, qb, d, fsh, fmask);
+          if (fok) hs_stage_warp(filt, g.col, qb, d, kHashSlots, fsh, fmask);
         }
       }
       if (j < j1) {
@@ -414,69 +415,64 @@ __global__ void desc_kernel(DevGraph g, VLevels L, const u32* __restrict__ pidx,
 }
 
 // ---------------------------------------------------------------------------
-// Root-centric kernel for the first extension of TC / CF on the DAG
-// (Listing 3: parents are level-1 edges (v0, v1); candidates u in N+(v1);
-// to_add = u in N+(v0)).  One warp per root v0: the 32-wide chunk of N+(v0)
-// (the parents) lives in registers/shared memory, an in-register scan of
-// d+(v1) gives the chunk's candidate space, lanes map to parents with one
-// REDUX over start offsets held in shared memory (all 32-bit), and probes hit
-// the warp's hash filter of N+(v0).  Same output order as the generic engine.
-struct RootArgs {
+// First extension of TC / CF on the DAG (Listing 3: parents are level-1 edges
+// (v0, v1); candidates u in N+(v1); to_add = u in N+(v0)).  Work item = 32
+// consecutive level-1 edges (one per lane), which may span several roots v0.
+// The warp stages the out-lists of the item's distinct roots in ONE exact
+// shared-memory hash set keyed (u << 5 | root slot), streams the concatenated
+// candidate lists N+(v1) 32 at a time (lanes -> parents by one OR-reduction
+// over start offsets) and probes each candidate with its parent's root slot.
+// Fixed-size edge items keep the per-item cost amortised over ~all 32 lanes
+// even when most roots own only a handful of out-edges (power-law DAGs).
+// Output order = sequential (parent, candidate) order, as the generic engine.
+struct EdgeArgs {
   DevGraph g;
+  const u32* src;      // level-1 v0 per DAG edge (absolute edge index)
   u64 lo, hi;          // level-1 slice (edge indices of the DAG CSR)
-  u32 vlo, vhi;        // roots owning the slice (inclusive)
-  const u64* item_start;  // per root (r - vlo): first work item; nr+1 entries
-  const u32* item_root;   // per item: root (r - vlo)
-  u64 nitems, ibeg, iend; // items processed by this launch: [ibeg, iend)
-  u64 grab;               // items per atomic grab
+  u64 ibeg, iend;      // items processed by this launch: [ibeg, iend), item = 32 edges
+  u64 grab;            // items per atomic grab
   unsigned long long* ctr;
   u64* cnt;            // COUNT: accepted per item
   const u64* offs;     // WRITE: exclusive offsets per item (absolute index)
   u64 out_base;
   u32* out_idx;
   u32* out_vid;
-  u32* masks;          // COUNT writes / WRITE reads ballot words (bump-allocated)
+  u32* masks;          // COUNT writes / WRITE reads ballot words (per-warp chunks)
   u64* moff;           // per item: word offset into masks, or ~0 (no masks)
   unsigned long long* mtop;
   u64 mcap;
   unsigned long long* total;  // FUSED
   unsigned long long* cand;   // candidates streamed (stats)
-  u32 hstride;                // per-warp hash slots (>= 2 x max out-degree, <= kHashSlots)
+  u32 hstride;                // per-warp hash slots (power of two)
 };
 
-// work items = (root, 32-parent chunk) so hub roots spread over warps
-__global__ void root_items_kernel(const u64* __restrict__ off, u64 lo, u64 hi, u32 vlo, u32 nr,
-                                  u64* __restrict__ items) {
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nr; i += (u64)gridDim.x * blockDim.x) {
-    const u32 r = vlo + (u32)i;
-    const u64 eb = max(off[r], lo), ee = min(off[r + 1], hi);
-    items[i] = ee > eb ? (ee - eb + 31) / 32 : 0;
-  }
-}
-
-__global__ void item_root_kernel(const u64* __restrict__ items, u32 nr, u32* __restrict__ item_root) {
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nr; i += (u64)gridDim.x * blockDim.x)
-    for (u64 t = items[i], te = items[i + 1]; t < te; ++t) item_root[t] = (u32)i;
-}
-
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 6) root_kernel(RootArgs a) {
-  extern __shared__ __align__(16) u32 s_rhash[];  // [kThreads/32][kHashSlots]
-  __shared__ u64 s_cb[kThreads / 32][32];
-  __shared__ u32 s_ex[kThreads / 32][33];
-  __shared__ u32 s_ei[kThreads / 32][32];
+__global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
+  extern __shared__ __align__(16) u32 s_rhash[];  // [kThreads/32][hstride]
+  __shared__ u64 s_cp[kThreads / 32][64];   // per parent rank: &col[cb] - 4 * exclusive start (byte address)
+  __shared__ u32 s_ex[kThreads / 32][64];   // per parent rank: exclusive candidate start; ~0 past nnz
+  __shared__ u32 s_ei[kThreads / 32][64];   // per parent rank: parent index (slice-relative)
+  __shared__ u32 s_sl[kThreads / 32][64];   // per parent rank: root slot
+  __shared__ u64 s_rb[kThreads / 32][32];   // per root slot: out-list begin
+  __shared__ u32 s_rk[kThreads / 32][64];   // per root slot: exclusive key start; ~0 past the roots
+  __shared__ u32 s_rd[kThreads / 32][32];   // per root slot: out-degree
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  u32* filt = s_rhash + wid * a.hstride;
-  u32 fsh = 0, fmask = 0;
-  u64* scb = s_cb[wid];
-  u32* sex = s_ex[wid];
-  u32* sei = s_ei[wid];
+  const u32 lemask = lanemask_lt() | (1u << lane);
+  u32* T = s_rhash + wid * a.hstride;
+  u64* const scp = s_cp[wid];
+  u32* const sex = s_ex[wid];
+  u32* const sei = s_ei[wid];
+  u32* const ssl = s_sl[wid];
+  u64* const srb = s_rb[wid];
+  u32* const srk = s_rk[wid];
+  u32* const srd = s_rd[wid];
+  sex[32 + lane] = 0xffffffffu;
+  srk[32 + lane] = 0xffffffffu;
   const DevGraph& g = a.g;
   unsigned long long acc_total = 0, acc_cand = 0;
-  u32 froot = 0xffffffffu;  // root whose out-list is in the filter
+  u32 mbase = 0, mend = 0;  // this warp's chunk of ballot-mask words (mcap <= 2^28)
   u64 grab = 0, grab_left = 0;
   for (;;) {
-    // one atomic per kItemGrab items: a single global counter serialises at L2
     if (grab_left == 0) {
       u64 it_ = 0;
       if (lane == 0) it_ = atomicAdd(a.ctr, (unsigned long long)a.grab) + a.ibeg;
@@ -493,26 +489,68 @@ __global__ void __launch_bounds__(kThreads, 6) root_kernel(RootArgs a) {
       wpos -= a.out_base;
       mo = ldg(a.moff + item);
     }
-    // root owning the item
-    const u32 rr = ldg(a.item_root + item);
-    const u32 r = a.vlo + rr;
-    const u64 ob = ldg(g.off + r), oe = ldg(g.off + r + 1);
-    const u64 eb = max(ob, a.lo), ee = min(oe, a.hi);
-    const u64 c0 = eb + 32 * (item - ldg(a.item_start + rr));
-    const u32 d0 = (u32)(oe - ob);
-    const bool use_filter = d0 <= kFilterMax;
     const bool from_masks = (MODE == kWrite) && mo != ~0ull;
-    if (use_filter && !from_masks && r != froot) {
-      froot = r;
-      hs_stage_warp(filt, g.col, ob, d0, fsh, fmask);
+    const u64 e = a.lo + item * 32 + lane;
+    const bool valid = e < a.hi;
+    const u32 v0 = valid ? ldg(a.src + e) : 0xffffffffu;
+    const u32 v1 = valid ? ldg(g.col + e) : 0u;
+    // distinct roots of the item (edges are sorted by v0): slot = root rank
+    const u32 vprev = __shfl_up_sync(0xffffffffu, v0, 1);
+    const bool lead = valid && (lane == 0 || v0 != vprev);
+    const u32 lmask = __ballot_sync(0xffffffffu, lead);
+    const u32 slot = __popc(lmask & lemask) - 1;
+    bool use_hash = false;
+    u32 sh = 0, hmask = 0;
+    if (!from_masks) {
+      // ---- stage the roots' out-lists, key = u << 5 | slot
+      u64 rb = 0;
+      u32 rd = 0;
+      if (lead) {
+        rb = ldg(g.off + v0);
+        rd = (u32)(ldg(g.off + v0 + 1) - rb);
+      }
+      u32 kin = rd;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, kin, o);
+        if (lane >= o) kin += t;
+      }
+      const u32 K = __shfl_sync(0xffffffffu, kin, 31);
+      const u32 nr = __popc(lmask);
+      __syncwarp();
+      srk[lane] = 0xffffffffu;
+      __syncwarp();
+      if (lead) {
+        srb[slot] = rb;
+        srk[slot] = kin - rd;
+        srd[slot] = rd;
+      }
+      __syncwarp();
+      use_hash = 2 * K <= a.hstride;
+      if (use_hash) {
+        u32 cap = 64;
+        while (cap < 8 * K && cap < a.hstride) cap <<= 1;
+        hmask = cap - 1;
+        sh = 32 - (31 - __clz(cap));
+        for (u32 i = lane * 4; i < cap; i += 128)
+          *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        __syncwarp();
+        u32 R = 0;  // root owning key kb
+        for (u32 kb = 0; kb < K; kb += 32) {
+          const u32 d = srk[R + 1 + lane] - kb;
+          const u32 starts = __reduce_or_sync(0xffffffffu, d < 32u ? (1u << d) : 0u);
+          const u32 r = min(R + __popc(starts & lemask), nr - 1);
+          R += __popc(starts);
+          const u32 k = kb + lane;
+          if (k < K) hs_insert(T, sh, hmask, (ldg(g.col + srb[r] + (k - srk[r])) << 5) | r);
+        }
+        __syncwarp();
+      }
     }
-    // the item's 32 parents (v0, v1): candidate lists N+(v1)
-    const u64 e = c0 + lane;
-    const bool valid = e < ee;
+    // ---- parents' candidate lists N+(v1), concatenated
     u64 cb = 0;
     u32 w = 0;
     if (valid) {
-      const u32 v1 = ldg(g.col + e);
       cb = ldg(g.off + v1);
       w = (u32)(ldg(g.off + v1 + 1) - cb);
     }
@@ -533,81 +571,98 @@ __global__ void __launch_bounds__(kThreads, 6) root_kernel(RootArgs a) {
     }
     const u32 nzmask = __ballot_sync(0xffffffffu, w > 0);
     const u32 rank = __popc(nzmask & lanemask_lt());
+    __syncwarp();
+    sex[lane] = 0xffffffffu;
+    __syncwarp();
     if (w > 0) {
-      scb[rank] = cb;
+      scp[rank] = reinterpret_cast<u64>(g.col) + 4 * (cb - (u64)(incl - w));
       sex[rank] = incl - w;
       sei[rank] = (u32)(e - a.lo);
+      ssl[rank] = slot;
     }
-    const u32 nnz = __popc(nzmask);
     __syncwarp();
     const u32 nwords = (total + 31) / 32;
-    if (MODE == kCount) {
-      u64 m = ~0ull;
-      if (lane == 0 && a.masks) {
-        const unsigned long long t = atomicAdd(a.mtop, (unsigned long long)nwords);
-        if (t + nwords <= a.mcap) m = t;
+    if (MODE == kCount && a.masks) {
+      // ballot words come from a per-warp chunk (one global atomic per chunk)
+      if (mbase + nwords > mend) {
+        const u32 want = kMaskChunk > nwords ? (u32)kMaskChunk : nwords;
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(a.mtop, (unsigned long long)want);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t + want <= a.mcap) {
+          mbase = (u32)t;
+          mend = (u32)t + want;
+        } else {
+          mbase = mend = 0;
+        }
       }
-      mo = __shfl_sync(0xffffffffu, m, 0);
+      mo = ~0ull;
+      if (mbase + nwords <= mend) {
+        mo = mbase;
+        mbase += nwords;
+      }
     }
-    u32 P = 0, c = 0, myword = 0;
-    u32 wi = 0;
-    // lane -> parent for the step at jb: one OR-reduction over the parents'
-    // start offsets (every listed parent owns >= 1 candidate)
+    u32 P = 0, c = 0, myword = 0, wi = 0;
+    // lane -> parent for the step at jb: one OR-reduction over the next
+    // parents' start offsets (sex is padded with ~0 past the last parent)
     auto map_step = [&](u32 jb) -> u32 {
-      const u32 x = (P + 1 + lane < nnz) ? sex[P + 1 + lane] : 0xffffffffu;
-      const u32 bit = (x - jb < 32u) ? (1u << (x - jb)) : 0u;
-      const u32 starts = __reduce_or_sync(0xffffffffu, bit);
-      const u32 myp = P + __popc(starts & (lanemask_lt() | (1u << lane)));
+      const u32 d = sex[P + 1 + lane] - jb;
+      const u32 starts = __reduce_or_sync(0xffffffffu, d < 32u ? (1u << d) : 0u);
+      const u32 myp = P + __popc(starts & lemask);
       P += __popc(starts);
-      return min(myp, nnz - 1);
+      return myp;
     };
     if (from_masks) {
       for (u32 jb = 0; jb < total; jb += 32, ++wi) {
-        const u32 j = jb + lane;
         const u32 myp = map_step(jb);
         const u32 m = ldg(a.masks + mo + wi);
         if (m) {
           if (m >> lane & 1u) {
             const u64 o = wpos + __popc(m & lanemask_lt());
             a.out_idx[o] = sei[myp];
-            a.out_vid[o] = ldg(g.col + scb[myp] + (j - sex[myp]));
+            a.out_vid[o] = ldg(reinterpret_cast<const u32*>(scp[myp]) + jb + lane);
           }
           wpos += __popc(m);
         }
       }
     } else {
-      // two steps per iteration: both candidate loads in flight before the probes
-      for (u32 jb = 0; jb < total; jb += 64) {
-        u32 myp[2], u[2];
-        myp[0] = map_step(jb);
-        myp[1] = map_step(jb + 32);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const u32 j = jb + 32 * h + lane;
-          u[h] = j < total ? ldg(g.col + scb[myp[h]] + (j - sex[myp[h]])) : 0u;
+      // software pipeline: the next step's candidate load is in flight while
+      // the current one is probed
+      u32 myp = map_step(0);
+      u32 u = lane < total ? ldg(reinterpret_cast<const u32*>(scp[myp]) + lane) : 0u;
+      for (u32 jb = 0; jb < total; jb += 32, ++wi) {
+        const u32 j = jb + lane;
+        u32 nmyp = 0, nu = 0;
+        if (jb + 32 < total) {
+          nmyp = map_step(jb + 32);
+          if (j + 32 < total) nu = ldg(reinterpret_cast<const u32*>(scp[nmyp]) + j + 32);
         }
-#pragma unroll
-        for (int h = 0; h < 2; ++h, ++wi) {
-          const u32 j = jb + 32 * h + lane;
-          if (jb + 32 * h >= total) break;
-          bool ok = false;
-          if (j < total) ok = use_filter ? hs_has(filt, fsh, fmask, u[h]) : contains_sorted(g.col + ob, d0, u[h]);
-          const u32 mask = __ballot_sync(0xffffffffu, ok);
-          if (MODE == kWrite) {
-            if (ok) {
-              const u64 o = wpos + __popc(mask & lanemask_lt());
-              a.out_idx[o] = sei[myp[h]];
-              a.out_vid[o] = u[h];
-            }
-            wpos += __popc(mask);
+        bool ok = false;
+        if (j < total) {
+          if (use_hash) {
+            ok = hs_has(T, sh, hmask, (u << 5) | ssl[myp]);
           } else {
-            c += __popc(mask);
-            if (MODE == kCount && mo != ~0ull) {
-              if ((wi & 31) == (u32)lane) myword = mask;
-              if ((wi & 31) == 31) a.masks[mo + (wi - 31) + lane] = myword;
-            }
+            const u32 r = ssl[myp];
+            ok = contains_sorted(g.col + srb[r], srd[r], u);
           }
         }
+        const u32 mask = __ballot_sync(0xffffffffu, ok);
+        if (MODE == kWrite) {
+          if (ok) {
+            const u64 o = wpos + __popc(mask & lanemask_lt());
+            a.out_idx[o] = sei[myp];
+            a.out_vid[o] = u;
+          }
+          wpos += __popc(mask);
+        } else {
+          c += __popc(mask);
+          if (MODE == kCount && mo != ~0ull) {
+            if ((wi & 31) == (u32)lane) myword = mask;
+            if ((wi & 31) == 31) a.masks[mo + (wi - 31) + lane] = myword;
+          }
+        }
+        myp = nmyp;
+        u = nu;
       }
     }
     if (MODE == kCount) {
@@ -624,20 +679,6 @@ __global__ void __launch_bounds__(kThreads, 6) root_kernel(RootArgs a) {
     if (MODE == kFused && acc_total) atomicAdd(a.total, acc_total);
     if (MODE != kWrite && acc_cand) atomicAdd(a.cand, acc_cand);
   }
-}
-
-__global__ void edge_source_kernel(const u64* __restrict__ off, u32 n, u64 e0, u64 e1, u32* __restrict__ out) {
-  // out[0] = vertex owning edge e0, out[1] = vertex owning edge e1
-  const int t = threadIdx.x;
-  if (t > 1) return;
-  const u64 e = t == 0 ? e0 : e1;
-  u64 lo = 0, hi = n;  // last v with off[v] <= e
-  while (lo < hi) {
-    u64 mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= e) lo = mid;
-    else hi = mid - 1;
-  }
-  out[t] = (u32)lo;
 }
 
 // Canonical code of every connectivity mask over k positions (reduce step 2:
@@ -857,11 +898,12 @@ void process(Ctx& c, VLevels L, u64 np) {
 }
 
 template <int MODE>
-void launch_root(Ctx& c, RootArgs& a, const char* what, double bytes) {
-  auto kern = root_kernel<MODE>;
-  // hash capacity for the largest staged out-list (<= kFilterMax keys)
-  u32 hs = 64;
-  while (hs < 2 * std::min<u32>(c.G->max_deg ? c.G->max_deg : kFilterMax, kFilterMax)) hs <<= 1;
+void launch_edge(Ctx& c, EdgeArgs& a, const char* what, double bytes) {
+  auto kern = edge_chunk_kernel<MODE>;
+  // hash capacity: keys of one item <= 32 + 2 x max out-degree in practice
+  const u32 md = c.G->max_deg ? c.G->max_deg : kFilterMax;
+  u32 hs = 256;
+  while (hs < 2 * (32 + 2 * std::min<u32>(md, kFilterMax)) && hs < kHashSlots) hs <<= 1;
   a.hstride = hs;
   const size_t smem = (size_t)(kThreads / 32) * hs * sizeof(u32);
   static int occ_by_hs[16] = {0};
@@ -884,52 +926,28 @@ void launch_root(Ctx& c, RootArgs& a, const char* what, double bytes) {
   ++c.tl->launches;
 }
 
-// First extension of TC/CF on a DAG through the root-centric kernel; deeper
-// levels continue in the generic engine.
-void process_root_cf(Ctx& c, const VLevels& L, u64 lo, u64 hi) {
+// First extension of TC/CF on a DAG through the edge-chunk kernel; deeper
+// levels continue in the generic engine.  src = level-1 v0 (absolute index).
+void process_l1_cf(Ctx& c, const VLevels& L, const u32* src, u64 lo, u64 hi) {
   Stats& st = *c.st;
   const u64 np = hi - lo;
   if (np == 0) return;
   const bool last = (c.k == 3);
-  DBuf<u32> vv(2, c.s);
-  edge_source_kernel<<<1, 32, 0, c.s>>>(c.G->d_off, c.G->n, lo, hi - 1, vv.get());
-  GPM_CUDA(cudaGetLastError());
-  u32 vr[2];
-  GPM_CUDA(cudaMemcpyAsync(vr, vv.get(), sizeof vr, cudaMemcpyDeviceToHost, c.s));
-  GPM_CUDA(cudaStreamSynchronize(c.s));
-  const u32 nr = vr[1] - vr[0] + 1;
-  DBuf<u64> items(nr + 1, c.s);
-  GPM_CUDA(cudaMemsetAsync(items.get() + nr, 0, sizeof(u64), c.s));
-  root_items_kernel<<<(unsigned)std::min<u64>((nr + 255) / 256, 1u << 20), 256, 0, c.s>>>(c.G->d_off, lo, hi, vr[0],
-                                                                                       nr, items.get());
-  GPM_CUDA(cudaGetLastError());
-  c.tl->launches += 2;
-  scan_inplace(items.get(), nr + 1, c.s);
+  const u64 NI = (np + 31) / 32;
   DBuf<unsigned long long> cand(1, c.s);
   GPM_CUDA(cudaMemsetAsync(cand.get(), 0, sizeof(unsigned long long), c.s));
-  u64 NI = 0;
-  GPM_CUDA(cudaMemcpyAsync(&NI, items.get() + nr, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
-  GPM_CUDA(cudaStreamSynchronize(c.s));
-  DBuf<u32> iroot(std::max<u64>(1, NI), c.s);
-  item_root_kernel<<<(unsigned)std::min<u64>((nr + 255) / 256, 1u << 20), 256, 0, c.s>>>(items.get(), nr, iroot.get());
-  GPM_CUDA(cudaGetLastError());
-  ++c.tl->launches;
-  RootArgs a{};
+  EdgeArgs a{};
   a.g = c.g;
+  a.src = src;
   a.lo = lo;
   a.hi = hi;
-  a.vlo = vr[0];
-  a.vhi = vr[1];
-  a.item_start = items.get();
-  a.item_root = iroot.get();
-  a.nitems = NI;
   a.ibeg = 0;
   a.iend = NI;
   a.cand = cand.get();
   if (last) {
     a.total = c.d_total;
     size_t rec = c.tl->recs.size();
-    launch_root<kFused>(c, a, "extend_fused_L1", 0.0);
+    launch_edge<kFused>(c, a, "extend_fused_L1", 0.0);
     unsigned long long W = 0;
     GPM_CUDA(cudaMemcpyAsync(&W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, c.s));
     GPM_CUDA(cudaStreamSynchronize(c.s));
@@ -941,7 +959,7 @@ void process_root_cf(Ctx& c, const VLevels& L, u64 lo, u64 hi) {
   }
   DBuf<u64> cnt(NI + 1, c.s), moff(NI + 1, c.s);
   GPM_CUDA(cudaMemsetAsync(cnt.get() + NI, 0, sizeof(u64), c.s));
-  // ballot masks: 1 bit per candidate, bump-allocated per item
+  // ballot masks: 1 bit per candidate, per-warp chunks
   const u64 mcap = std::max<u64>(1, std::min<u64>(c.mask_budget / 4, u64(1) << 28));
   DBuf<u32> masks(mcap, c.s);
   DBuf<unsigned long long> mtop(1, c.s);
@@ -952,7 +970,7 @@ void process_root_cf(Ctx& c, const VLevels& L, u64 lo, u64 hi) {
   a.mtop = mtop.get();
   a.mcap = mcap;
   size_t rec = c.tl->recs.size();
-  launch_root<kCount>(c, a, "extend_count_L1", 0.0);
+  launch_edge<kCount>(c, a, "extend_count_L1", 0.0);
   scan_inplace(cnt.get(), NI + 1, c.s);
   unsigned long long W = 0;
   u64 T = 0;
@@ -990,7 +1008,7 @@ void process_root_cf(Ctx& c, const VLevels& L, u64 lo, u64 hi) {
     const u64 Tc = end - base;
     if (Tc == 0) continue;
     DBuf<u32> oi(Tc, c.s), ov(Tc, c.s);
-    RootArgs w = a;
+    EdgeArgs w = a;
     w.ibeg = r0;
     w.iend = r1;
     w.offs = cnt.get();
@@ -998,8 +1016,8 @@ void process_root_cf(Ctx& c, const VLevels& L, u64 lo, u64 hi) {
     w.out_idx = oi.get();
     w.out_vid = ov.get();
     const double frac = (double)(r1 - r0) / (double)NI;
-    launch_root<kWrite>(c, w, "extend_write_L1", frac * (double)W / 8.0 + 24.0 * Tc);
-    htrace(c.s, "root: write");
+    launch_edge<kWrite>(c, w, "extend_write_L1", frac * (double)W / 8.0 + 24.0 * Tc);
+    htrace(c.s, "l1: write");
     VLevels nl = L;
     nl.idx[1] = oi.get();
     nl.vid[1] = ov.get();
@@ -1089,8 +1107,8 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
     mc3_staged(*G, l1s.get(), lo, hi, c.d_hist, s, tl, st);
   } else if (appk == kAppMC) {
     process_dispatch<kAppMC>(c, 1, L, nroot);
-  } else if (G->oriented && !std::getenv("GPM_GENERIC_L1")) {
-    process_root_cf(c, L, lo, hi);
+  } else if (G->oriented && G->n < (1u << 27) && !std::getenv("GPM_GENERIC_L1")) {  // key = u << 5 | slot
+    process_l1_cf(c, L, l1i.get(), lo, hi);
   } else {
     process_dispatch<kAppCF>(c, 1, L, nroot);
   }
