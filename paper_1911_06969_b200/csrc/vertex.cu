@@ -55,6 +55,7 @@ constexpr u64 kBatchGrab = 4;       // generic-engine batches per atomic grab
 constexpr u32 kHashSlots = 1024;    // per-warp exact hash set of the root's out-list (4 KB)
 constexpr u32 kFilterMax = 512;     // out-lists longer than this are probed by binary search
 constexpr u64 kMaskChunk = 4096;    // ballot-mask words a warp reserves at a time
+constexpr u32 kSparseWords = 64;    // non-zero (step, ballot) pairs kept per CF item
 
 struct VLevels {
   const u32* idx[kMaxLevels];
@@ -456,6 +457,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
   __shared__ u64 s_rb[kThreads / 32][32];   // per root slot: out-list begin
   __shared__ u32 s_rk[kThreads / 32][64];   // per root slot: exclusive key start; ~0 past the roots
   __shared__ u32 s_rd[kThreads / 32][32];   // per root slot: out-degree
+  __shared__ u32 s_mw[kThreads / 32][2 * kSparseWords];  // COUNT: (step, ballot) of non-zero steps
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const u32 lemask = lanemask_lt() | (1u << lane);
   u32* T = s_rhash + wid * a.hstride;
@@ -466,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
   u64* const srb = s_rb[wid];
   u32* const srk = s_rk[wid];
   u32* const srd = s_rd[wid];
+  u32* const smw = s_mw[wid];
   sex[32 + lane] = 0xffffffffu;
   srk[32 + lane] = 0xffffffffu;
   const DevGraph& g = a.g;
@@ -571,6 +574,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
     }
     const u32 nzmask = __ballot_sync(0xffffffffu, w > 0);
     const u32 rank = __popc(nzmask & lanemask_lt());
+    const u32 nnz = __popc(nzmask);
     __syncwarp();
     sex[lane] = 0xffffffffu;
     __syncwarp();
@@ -581,28 +585,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
       ssl[rank] = slot;
     }
     __syncwarp();
-    const u32 nwords = (total + 31) / 32;
-    if (MODE == kCount && a.masks) {
-      // ballot words come from a per-warp chunk (one global atomic per chunk)
-      if (mbase + nwords > mend) {
-        const u32 want = kMaskChunk > nwords ? (u32)kMaskChunk : nwords;
-        unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(a.mtop, (unsigned long long)want);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t + want <= a.mcap) {
-          mbase = (u32)t;
-          mend = (u32)t + want;
-        } else {
-          mbase = mend = 0;
-        }
-      }
-      mo = ~0ull;
-      if (mbase + nwords <= mend) {
-        mo = mbase;
-        mbase += nwords;
-      }
-    }
-    u32 P = 0, c = 0, myword = 0, wi = 0;
+    u32 P = 0, c = 0, wi = 0, nzw = 0;
     // lane -> parent for the step at jb: one OR-reduction over the next
     // parents' start offsets (sex is padded with ~0 past the last parent)
     auto map_step = [&](u32 jb) -> u32 {
@@ -613,17 +596,26 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
       return myp;
     };
     if (from_masks) {
-      for (u32 jb = 0; jb < total; jb += 32, ++wi) {
-        const u32 myp = map_step(jb);
-        const u32 m = ldg(a.masks + mo + wi);
-        if (m) {
-          if (m >> lane & 1u) {
-            const u64 o = wpos + __popc(m & lanemask_lt());
-            a.out_idx[o] = sei[myp];
-            a.out_vid[o] = ldg(reinterpret_cast<const u32*>(scp[myp]) + jb + lane);
+      // execution from the inspection's sparse ballots: only steps with
+      // accepted candidates are visited; lane -> parent by binary search
+      const u32 nw = (u32)(mo & 0xff);
+      const u64 mb = mo >> 8;
+      for (u32 i = 0; i < nw; ++i) {
+        const u32 jb = 32 * ldg(a.masks + mb + 2 * i);
+        const u32 m = ldg(a.masks + mb + 2 * i + 1);
+        if (m >> lane & 1u) {
+          const u32 j = jb + lane;
+          u32 lo_ = 0, hi_ = nnz - 1;  // last rank with sex[rank] <= j
+          while (lo_ < hi_) {
+            const u32 mid = (lo_ + hi_ + 1) >> 1;
+            if (sex[mid] <= j) lo_ = mid;
+            else hi_ = mid - 1;
           }
-          wpos += __popc(m);
+          const u64 o = wpos + __popc(m & lanemask_lt());
+          a.out_idx[o] = sei[lo_];
+          a.out_vid[o] = ldg(reinterpret_cast<const u32*>(scp[lo_]) + j);
         }
+        wpos += __popc(m);
       }
     } else {
       // software pipeline: the next step's candidate load is in flight while
@@ -656,9 +648,12 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
           wpos += __popc(mask);
         } else {
           c += __popc(mask);
-          if (MODE == kCount && mo != ~0ull) {
-            if ((wi & 31) == (u32)lane) myword = mask;
-            if ((wi & 31) == 31) a.masks[mo + (wi - 31) + lane] = myword;
+          if (MODE == kCount && mask) {
+            if (lane == 0 && nzw < kSparseWords) {
+              smw[2 * nzw] = wi;
+              smw[2 * nzw + 1] = mask;
+            }
+            ++nzw;
           }
         }
         myp = nmyp;
@@ -666,7 +661,28 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
       }
     }
     if (MODE == kCount) {
-      if (mo != ~0ull && (wi & 31) != 0 && (u32)lane < (wi & 31)) a.masks[mo + (wi & ~31u) + lane] = myword;
+      // keep the non-zero ballots (step, mask) when they fit; the execution
+      // pass then touches accepted candidates only (else it recomputes)
+      mo = ~0ull;
+      if (nzw && nzw <= kSparseWords && a.masks) {
+        if (mbase + 2 * nzw > mend) {  // per-warp chunk: one global atomic per chunk
+          unsigned long long t = 0;
+          if (lane == 0) t = atomicAdd(a.mtop, (unsigned long long)kMaskChunk);
+          t = __shfl_sync(0xffffffffu, t, 0);
+          if (t + kMaskChunk <= a.mcap) {
+            mbase = (u32)t;
+            mend = (u32)(t + kMaskChunk);
+          } else {
+            mbase = mend = 0;
+          }
+        }
+        if (mbase + 2 * nzw <= mend) {
+          __syncwarp();
+          for (u32 i = lane; i < 2 * nzw; i += 32) a.masks[mbase + i] = smw[i];
+          mo = ((u64)mbase << 8) | nzw;
+          mbase += 2 * nzw;
+        }
+      }
       if (lane == 0) {
         a.cnt[item] = c;
         a.moff[item] = mo;
