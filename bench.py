@@ -214,7 +214,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1911_06969_b200.dist import make_exchange
     exchange = make_exchange() if world > 1 else None
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the engine launches every kernel on it
+    # and the step events are recorded on it, so they bracket the device work
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
 
     def barrier():

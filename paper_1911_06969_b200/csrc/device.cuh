@@ -211,6 +211,25 @@ inline void htrace(cudaStream_t s, const char* what) {
   t0 = t1;
 }
 
+// Device bytes available to the engine: free memory plus what the stream-
+// ordered pool holds reserved but unused (the pool keeps released blocks,
+// keep_pool_warm), so the planner's budget does not shrink from call to call.
+inline size_t device_free_bytes() {
+  size_t freeb = 0, totalb = 0;
+  GPM_CUDA(cudaMemGetInfo(&freeb, &totalb));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long reserved = 0, used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+      freeb += (size_t)(reserved - used);
+  }
+  cudaGetLastError();
+  return freeb;
+}
+
 inline int sm_count() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);

@@ -963,7 +963,8 @@ struct Fsm {
       throw Error(GPM_EINVAL, "fsm: too many distinct labels for a packed pattern code at this k");
     sms = sm_count();
     size_t freeb = 0, totalb = 0;
-    GPM_CUDA(cudaMemGetInfo(&freeb, &totalb));
+    freeb = device_free_bytes();
+    (void)totalb;
     budget = cfg.mem_budget ? cfg.mem_budget : (u64)(0.5 * (double)freeb);
     d_ctr.alloc(1, s);
     const int levels = k - 1;

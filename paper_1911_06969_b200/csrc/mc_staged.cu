@@ -534,70 +534,111 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
         pmv = U.flags(v2);  // bit 0: v2 ~ v0, bit 1: v2 ~ v1
         aCand += (u64)(ldg(g.off + v0 + 1) - ldg(g.off + v0)) + (ldg(g.off + v1 + 1) - ldg(g.off + v1)) + (e2 - b2);
       }
-      // ---- concatenated stream of the non-empty children's S2 ranges
-      u32 incl = len;
+      // ---- event counts of every child: e2c / e11 / e01 / e12 (see above)
+      u32 e2c = 0, e11 = 0, e01 = 0, e12 = 0;
+      // long S2 ranges (>= 32 candidates): one child at a time, warp-uniform
+      // thresholds, coalesced loads, two in flight
+      u32 todo = __ballot_sync(0xffffffffu, len >= 32);
+      while (todo) {
+        const int i = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const u64 b = __shfl_sync(0xffffffffu, st, i);
+        const u32 L = __shfl_sync(0xffffffffu, len, i);
+        const u32 cv2 = __shfl_sync(0xffffffffu, v2, i);
+        const u32 cm = max(v1, cv2);
+        u32 c2 = 0, c11 = 0, c01 = 0, c12 = 0;
+        u32 j = 0;
+        for (; j + 64 <= L; j += 64) {
+          const u32 u0 = ldg(g.col + b + j + lane);
+          const u32 u1 = ldg(g.col + b + j + 32 + lane);
+          const u32 f0 = U.flags(u0), f1 = U.flags(u1);
+          c2 += __popc(__ballot_sync(0xffffffffu, f0 == 0)) + __popc(__ballot_sync(0xffffffffu, f1 == 0));
+          c11 += __popc(__ballot_sync(0xffffffffu, f0 == 3 && u0 > cm)) + __popc(__ballot_sync(0xffffffffu, f1 == 3 && u1 > cm));
+          c01 += __popc(__ballot_sync(0xffffffffu, f0 == 1 && u0 > cm)) + __popc(__ballot_sync(0xffffffffu, f1 == 1 && u1 > cm));
+          c12 += __popc(__ballot_sync(0xffffffffu, f0 == 2 && u0 > cv2)) + __popc(__ballot_sync(0xffffffffu, f1 == 2 && u1 > cv2));
+        }
+        for (; j < L; j += 32) {
+          const bool ok = j + lane < L;
+          const u32 u0 = ok ? ldg(g.col + b + j + lane) : 0u;
+          const u32 f0 = ok ? U.flags(u0) : 4u;
+          c2 += __popc(__ballot_sync(0xffffffffu, f0 == 0));
+          c11 += __popc(__ballot_sync(0xffffffffu, f0 == 3 && u0 > cm));
+          c01 += __popc(__ballot_sync(0xffffffffu, f0 == 1 && u0 > cm));
+          c12 += __popc(__ballot_sync(0xffffffffu, f0 == 2 && u0 > cv2));
+        }
+        if (lane == i) {
+          e2c = c2;
+          e11 = c11;
+          e01 = c01;
+          e12 = c12;
+        }
+      }
+      // short S2 ranges: packed 32 candidates per step (OR-reduction lane ->
+      // child map), per-child counts by the first lane of each segment
+      const u32 sl = len < 32 ? len : 0u;
+      u32 incl = sl;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += t;
       }
       const u32 total = __shfl_sync(0xffffffffu, incl, 31);
-      const u32 nz = __ballot_sync(0xffffffffu, len > 0);
+      const u32 nz = __ballot_sync(0xffffffffu, sl > 0);
       const u32 rank = __popc(nz & lanemask_lt());
       const u32 nnz = __popc(nz);
-      if (len > 0) {
-        s_cb[wid][rank] = st;
-        s_ex[wid][rank] = incl - len;
-        s_v2[wid][rank] = v2;
-      }
-#pragma unroll
-      for (int ev = 0; ev < 4; ++ev) s_ev[wid][ev][lane] = 0;
-      __syncwarp();
-      u32 P = 0;
-      for (u32 jb = 0; jb < total; jb += 32) {
-        const u32 j = jb + lane;
-        // lane -> child by one OR-reduction over the children's start offsets
-        const u32 x = (P + 1 + lane < nnz) ? s_ex[wid][P + 1 + lane] : 0xffffffffu;
-        const u32 bit = (x - jb < 32u) ? (1u << (x - jb)) : 0u;
-        const u32 starts = __reduce_or_sync(0xffffffffu, bit);
-        const u32 c = P + __popc(starts & (lanemask_lt() | (1u << lane)));
-        P += __popc(starts);
-        bool f2 = false, f11 = false, f01 = false, f12 = false;
-        if (j < total) {
-          const u32 u = ldg(g.col + s_cb[wid][c] + (j - s_ex[wid][c]));
-          const u32 cv2 = s_v2[wid][c];
-          const u32 cm = max(v1, cv2);
-          const u32 f = U.flags(u);
-          f2 = f == 0;
-          f11 = f == 3 && u > cm;
-          f01 = f == 1 && u > cm;
-          f12 = f == 2 && u > cv2;
+      if (total) {
+        if (sl > 0) {
+          s_cb[wid][rank] = st;
+          s_ex[wid][rank] = incl - sl;
+          s_v2[wid][rank] = v2;
         }
-        // segmented per-child counts: each segment's first lane adds its popcounts
-        const u32 b2_ = __ballot_sync(0xffffffffu, f2), b11 = __ballot_sync(0xffffffffu, f11);
-        const u32 b01 = __ballot_sync(0xffffffffu, f01), b12 = __ballot_sync(0xffffffffu, f12);
-        const u32 heads = starts | 1u;
-        if ((heads >> lane & 1u) && j < total) {
-          const u32 above = heads & ~((2u << lane) - 1u);
-          const u32 endl = above ? (u32)(__ffs(above) - 1) : 32u;
-          const u32 seg = (endl >= 32 ? 0xffffffffu : ((1u << endl) - 1u)) & ~((1u << lane) - 1u);
-          s_ev[wid][0][c] += __popc(b2_ & seg);
-          s_ev[wid][1][c] += __popc(b11 & seg);
-          s_ev[wid][2][c] += __popc(b01 & seg);
-          s_ev[wid][3][c] += __popc(b12 & seg);
+#pragma unroll
+        for (int ev = 0; ev < 4; ++ev) s_ev[wid][ev][lane] = 0;
+        __syncwarp();
+        u32 P = 0;
+        for (u32 jb = 0; jb < total; jb += 32) {
+          const u32 j = jb + lane;
+          const u32 x = (P + 1 + lane < nnz) ? s_ex[wid][P + 1 + lane] : 0xffffffffu;
+          const u32 bit = (x - jb < 32u) ? (1u << (x - jb)) : 0u;
+          const u32 starts = __reduce_or_sync(0xffffffffu, bit);
+          const u32 c = P + __popc(starts & (lanemask_lt() | (1u << lane)));
+          P += __popc(starts);
+          bool f2 = false, f11 = false, f01 = false, f12 = false;
+          if (j < total) {
+            const u32 u = ldg(g.col + s_cb[wid][c] + (j - s_ex[wid][c]));
+            const u32 cv2 = s_v2[wid][c];
+            const u32 cm = max(v1, cv2);
+            const u32 f = U.flags(u);
+            f2 = f == 0;
+            f11 = f == 3 && u > cm;
+            f01 = f == 1 && u > cm;
+            f12 = f == 2 && u > cv2;
+          }
+          const u32 b2_ = __ballot_sync(0xffffffffu, f2), b11 = __ballot_sync(0xffffffffu, f11);
+          const u32 b01 = __ballot_sync(0xffffffffu, f01), b12 = __ballot_sync(0xffffffffu, f12);
+          const u32 heads = starts | 1u;
+          if ((heads >> lane & 1u) && j < total) {
+            const u32 above = heads & ~((2u << lane) - 1u);
+            const u32 endl = above ? (u32)(__ffs(above) - 1) : 32u;
+            const u32 seg = (endl >= 32 ? 0xffffffffu : ((1u << endl) - 1u)) & ~((1u << lane) - 1u);
+            s_ev[wid][0][c] += __popc(b2_ & seg);
+            s_ev[wid][1][c] += __popc(b11 & seg);
+            s_ev[wid][2][c] += __popc(b01 & seg);
+            s_ev[wid][3][c] += __popc(b12 & seg);
+          }
+          __syncwarp();
+        }
+        if (sl > 0) {
+          e2c = s_ev[wid][0][rank];
+          e11 = s_ev[wid][1][rank];
+          e01 = s_ev[wid][2][rank];
+          e12 = s_ev[wid][3][rank];
         }
         __syncwarp();
       }
       // ---- per-child class values, reduced per parent-mask value
       u32 val[7] = {0, 0, 0, 0, 0, 0, 0};
       if (valid) {
-        u32 e2c = 0, e11 = 0, e01 = 0, e12 = 0;
-        if (len > 0) {
-          e2c = s_ev[wid][0][rank];
-          e11 = s_ev[wid][1][rank];
-          e01 = s_ev[wid][2][rank];
-          e12 = s_ev[wid][3][rank];
-        }
         const u32 m = max(v1, v2);
         const u32 A0 = count_gt_global(U.s0, U.n0, m);
         const u32 B1 = count_gt_global(U.s1, U.n1, v2);

@@ -1099,7 +1099,8 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   c.sms = sm_count();
   c.generic_mc = std::getenv("GPM_GENERIC_MC") != nullptr;
   size_t freeb = 0, totalb = 0;
-  GPM_CUDA(cudaMemGetInfo(&freeb, &totalb));
+  freeb = device_free_bytes();
+  (void)totalb;
   u64 budget = cfg.mem_budget ? cfg.mem_budget : (u64)(0.6 * (double)freeb);
   const int mat_levels = std::max(1, k - 3);
   c.cap_entries = std::max<u64>(kBatch, std::min<u64>((u64(1) << 32) - 1, budget / 16 / mat_levels));

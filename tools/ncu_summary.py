@@ -1,7 +1,7 @@
 """Summarise ncu --set full reports: python tools/ncu_summary.py rep1.ncu-rep ..."""
 import csv, io, subprocess, sys
 WANT = [
-    ("gpu__time_duration.sum", "time_us", 1e-3),
+    ("gpu__time_duration.sum", "time_ms", "time"),
     ("dram__bytes_read.sum", "dram_rd_MB", None),
     ("dram__bytes_write.sum", "dram_wr_MB", None),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct", 1),
@@ -36,8 +36,8 @@ def rows(rep):
                 continue
             if scale is None:
                 v *= UNITS.get(units[i], 1)
-            elif name == "time_us":
-                v *= {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(units[i], 1e-3) / 1e-3 * 1e-3
+            elif scale == "time":
+                v *= {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1, "ms": 1}.get(units[i], 1)
             d[name] = round(v, 2)
         yield d
 
