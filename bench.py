@@ -159,6 +159,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU oracle work for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-steal", action="store_true", help="N>1: static split only (no work-stealing tail)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     app, k, sigma, rmat, desc = WORKLOADS[args.app]
@@ -230,9 +231,28 @@ def main():
     g_in = g_und.orient_dag() if app in ("tc", "cf") else g_und   # preprocessing
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     kw = dict(rank=rank, world=world, stream=sp, exchange=exchange)
+    # N > 1: degree-weighted static split + device-side work-stealing tail
+    # over counters peer-mapped from rank 0's GPU (FSM levels exchange anyway)
+    steal = None
+    if world > 1 and app != "fsm" and not args.no_steal:
+        try:
+            from paper_1911_06969_b200.dist import StealCounters
+            steal = StealCounters()
+        except Exception as e:  # static split only
+            print(f"[bench] work stealing disabled: {e!r}", file=sys.stderr)
+            steal = None
+    config["partition"] = "degree-weighted static split" + (" + device work-stealing tail" if steal else "")
+
+    def mine_step(g, **extra):
+        skw = {}
+        if steal is not None:
+            steal.reset()
+            skw = dict(steal_ctrs=steal.ptr)
+        return P.mine(g, app, k, sigma, **extra, **skw)
+
     res = None
     for _ in range(args.warmup):
-        res = P.mine(g_in, app, k, sigma, **kw)
+        res = mine_step(g_in, **kw)
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -244,8 +264,10 @@ def main():
     barrier()
     for _ in range(args.steps):
         flush.zero_()
+        if steal is not None:
+            steal.reset()
         ev0.record(stream)
-        res = P.mine(g_in, app, k, sigma, **kw)
+        res = P.mine(g_in, app, k, sigma, **kw, **({"steal_ctrs": steal.ptr} if steal else {}))
         ev1.record(stream)
         ev1.synchronize()
         step_ms.append(ev0.elapsed_time(ev1))
@@ -257,7 +279,7 @@ def main():
     # busy with further (untimed) steps until one sample lands after it began
     t_extra = time.time()
     while len(clocks.lines) <= n_before + 1 and time.time() - t_extra < 3.0:
-        P.mine(g_in, app, k, sigma, **kw)
+        mine_step(g_in, **kw)
         torch.cuda.synchronize()
     clock_rec = clocks.stop(first=n_before)
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
@@ -278,11 +300,14 @@ def main():
     e2e_ms = []
     er = None
     for i in range(1 + args.steps):
+        if steal is not None:
+            steal.reset()
         barrier()
         t = time.perf_counter()
         # TC/CF need the degree-ordered DAG: fused pipelined upload + orientation
         g = P.Graph(pinned, device=local, orient=app in ("tc", "cf"))
-        er = P.mine(g, app, k, sigma, rank=rank, world=world, exchange=exchange)
+        er = P.mine(g, app, k, sigma, rank=rank, world=world, exchange=exchange,
+                    **({"steal_ctrs": steal.ptr} if steal else {}))
         del g
         torch.cuda.synchronize()
         if i > 0:
@@ -328,6 +353,8 @@ def main():
                                "kind": "port", "sample": sample + " (oracle/liboracle.so, OpenMP)"}
     if rank == 0:
         print(json.dumps(out))
+    if steal is not None:
+        steal.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -63,9 +63,26 @@ typedef struct gpm_config {
   void* stream;             /* cudaStream_t to launch on; NULL = library stream   */
   gpm_exchange_fn exchange; /* optional collective hook (world > 1)               */
   void* exchange_ctx;
+  /* Device-side work-stealing tail (world > 1, TC/CF/MC): device
+   * pointer, valid on this rank's GPU, to `world` uint64 counters shared by all
+   * ranks (gpm_steal_create / gpm_steal_open) and zeroed before the call
+   * (gpm_steal_reset + a barrier).  Each rank mines the head of its static
+   * range, then claims chunks of every rank's tail with system-scope atomics
+   * on the counters (own tail first).  NULL = static split only. */
+  void* steal_ctrs;
+  uint64_t steal_chunk;     /* level-1 entries per stolen chunk; 0 = auto          */
 } gpm_config;
 
 void gpm_config_default(gpm_config* cfg);
+
+/* Shared steal counters for gpm_config.steal_ctrs.  One rank creates them on
+ * its device and exports a CUDA IPC handle (64 bytes) that the other ranks open
+ * (peer mapping over NVLink); ranks in one process may share the pointer.
+ * reset zeroes the `world` counters on `stream` (NULL = legacy stream). */
+int gpm_steal_create(int device, int world, void** dev_ptr, void* ipc_handle_out);
+int gpm_steal_open(int device, const void* ipc_handle, void** dev_ptr);
+int gpm_steal_reset(void* dev_ptr, int world, void* stream);
+int gpm_steal_release(void* dev_ptr, int opened);
 
 /* ---------------------------------------------------------------- graph core */
 

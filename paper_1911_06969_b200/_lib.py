@@ -22,7 +22,7 @@ EXPORTS = [
     "gpm_graph_is_connected", "gpm_level1", "gpm_graph_free", "gpm_mine", "gpm_result_total",
     "gpm_result_num_patterns", "gpm_result_pattern", "gpm_result_stats", "gpm_result_free",
     "gpm_load_edge_list", "gpm_load_labeled_graph", "gpm_csr_from_edges", "gpm_generate_rmat", "gpm_csr_free",
-    "gpm_last_error", "gpm_version",
+    "gpm_last_error", "gpm_version", "gpm_steal_create", "gpm_steal_open", "gpm_steal_reset", "gpm_steal_release",
 ]
 
 
@@ -30,7 +30,7 @@ class Config(C.Structure):
     _fields_ = [("app", C.c_int), ("k", C.c_int), ("min_support", C.c_uint64), ("mem_budget", C.c_uint64),
                 ("no_orient", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("root_lo", C.c_uint64),
                 ("root_hi", C.c_uint64), ("stream", C.c_void_p), ("exchange", EXCHANGE_FN),
-                ("exchange_ctx", C.c_void_p)]
+                ("exchange_ctx", C.c_void_p), ("steal_ctrs", C.c_void_p), ("steal_chunk", C.c_uint64)]
 
 
 class Stats(C.Structure):
@@ -93,6 +93,10 @@ def lib():
                                     C.POINTER(CsrStruct)]),
         "gpm_csr_free": (None, [C.POINTER(CsrStruct)]),
         "gpm_last_error": (C.c_char_p, []),
+        "gpm_steal_create": (i32, [i32, i32, C.POINTER(vp), vp]),
+        "gpm_steal_open": (i32, [i32, vp, C.POINTER(vp)]),
+        "gpm_steal_reset": (i32, [vp, i32, vp]),
+        "gpm_steal_release": (i32, [vp, i32]),
         "gpm_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():

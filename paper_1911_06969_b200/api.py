@@ -184,7 +184,7 @@ class MineResult:
 
 def make_config(app: str, k: int = 3, min_support: int = 0, *, mem_budget: int = 0, no_orient: bool = False,
                 rank: int = 0, world: int = 1, root_lo: int = 0, root_hi: int = 0, stream: int = 0,
-                exchange=None) -> _L.Config:
+                exchange=None, steal_ctrs: int = 0, steal_chunk: int = 0) -> _L.Config:
     cfg = _L.Config()
     lib().gpm_config_default(C.byref(cfg))
     cfg.app = APP_IDS[app]
@@ -197,6 +197,8 @@ def make_config(app: str, k: int = 3, min_support: int = 0, *, mem_budget: int =
     cfg.stream = stream or None
     if exchange is not None:
         cfg.exchange = exchange
+    cfg.steal_ctrs = steal_ctrs or None
+    cfg.steal_chunk = steal_chunk
     return cfg
 
 

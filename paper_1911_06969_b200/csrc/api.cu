@@ -99,6 +99,58 @@ void gpm_config_default(gpm_config* cfg) {
   cfg->world = 1;
 }
 
+int gpm_steal_create(int device, int world, void** dev_ptr, void* ipc_handle_out) {
+  if (!dev_ptr || world < 1) {
+    set_last_error("gpm_steal_create: bad argument");
+    return GPM_EINVAL;
+  }
+  return guarded([&] {
+    GPM_CUDA(cudaSetDevice(device));
+    void* p = nullptr;
+    GPM_CUDA(cudaMalloc(&p, sizeof(unsigned long long) * world));  // not pooled: IPC-exportable
+    GPM_CUDA(cudaMemset(p, 0, sizeof(unsigned long long) * world));
+    if (ipc_handle_out) {
+      cudaIpcMemHandle_t h;
+      GPM_CUDA(cudaIpcGetMemHandle(&h, p));
+      std::memcpy(ipc_handle_out, &h, sizeof h);
+    }
+    *dev_ptr = p;
+  });
+}
+
+int gpm_steal_open(int device, const void* ipc_handle, void** dev_ptr) {
+  if (!ipc_handle || !dev_ptr) {
+    set_last_error("gpm_steal_open: null argument");
+    return GPM_EINVAL;
+  }
+  return guarded([&] {
+    GPM_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, sizeof h);
+    GPM_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int gpm_steal_reset(void* dev_ptr, int world, void* stream) {
+  if (!dev_ptr || world < 1) {
+    set_last_error("gpm_steal_reset: bad argument");
+    return GPM_EINVAL;
+  }
+  return guarded([&] {
+    cudaStream_t s = (cudaStream_t)stream;
+    GPM_CUDA(cudaMemsetAsync(dev_ptr, 0, sizeof(unsigned long long) * world, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int gpm_steal_release(void* dev_ptr, int opened) {
+  if (!dev_ptr) return GPM_OK;
+  return guarded([&] {
+    if (opened) GPM_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+    else GPM_CUDA(cudaFree(dev_ptr));
+  });
+}
+
 int gpm_mine(const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
   if (!g || !cfg || !out) {
     set_last_error("gpm_mine: null argument");

@@ -73,6 +73,13 @@ void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u
 // (SURVEY §8e); weight = candidate count of each level-1 entry.
 void root_split(const gpm_graph& g, const u32* idx, const u32* vid, u64 n1, int app, int rank, int world, u64& lo,
                 u64& hi, cudaStream_t s, Timeline& tl);
+// The same split for every rank: bounds[r]..bounds[r+1] (world+1 entries).
+void root_split_bounds(const gpm_graph& g, const u32* idx, const u32* vid, u64 n1, int app, int world,
+                       std::vector<u64>& bounds, cudaStream_t s, Timeline& tl);
+// Device-side work-stealing grab over the ranks' tail ranges [tlo, thi)
+// (gpm_config.steal_ctrs); [lo, hi) = claimed chunk, lo == hi when all done.
+void steal_grab(unsigned long long* ctrs, const u64* d_tlo, const u64* d_thi, int world, int rank, u64 chunk,
+                u64* d_out, u64& lo, u64& hi, cudaStream_t s);
 
 void keep_pool_warm(int device);
 

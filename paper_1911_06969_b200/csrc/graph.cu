@@ -294,13 +294,11 @@ void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count
   if (l1_start) *l1_start = std::move(pos);
 }
 
-void root_split(const gpm_graph& g, const u32* idx, const u32* vid, u64 n1, int app, int rank, int world, u64& lo,
-                u64& hi, cudaStream_t s, Timeline& tl) {
-  if (world <= 1 || n1 == 0) {
-    lo = 0;
-    hi = n1;
-    return;
-  }
+void root_split_bounds(const gpm_graph& g, const u32* idx, const u32* vid, u64 n1, int app, int world,
+                       std::vector<u64>& bounds, cudaStream_t s, Timeline& tl) {
+  bounds.assign(world + 1, n1);
+  bounds[0] = 0;
+  if (world <= 1 || n1 == 0) return;
   DBuf<u64> w(n1 + 1, s);
   GPM_CUDA(cudaMemsetAsync(w.get() + n1, 0, sizeof(u64), s));
   ++tl.launches;
@@ -310,18 +308,56 @@ void root_split(const gpm_graph& g, const u32* idx, const u32* vid, u64 n1, int 
   u64 total = 0;
   GPM_CUDA(cudaMemcpyAsync(&total, w.get() + n1, sizeof(u64), cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaStreamSynchronize(s));
-  u64 keys[2] = {(u64)((unsigned __int128)total * (u64)rank / (u64)world),
-                 (u64)((unsigned __int128)total * (u64)(rank + 1) / (u64)world)};
-  DBuf<u64> dk(2, s), dout(2, s);
-  GPM_CUDA(cudaMemcpyAsync(dk.get(), keys, sizeof keys, cudaMemcpyHostToDevice, s));
+  std::vector<u64> keys(world - 1);
+  for (int r = 1; r < world; ++r) keys[r - 1] = (u64)((unsigned __int128)total * (u64)r / (u64)world);
+  DBuf<u64> dk(world - 1, s), dout(world - 1, s);
+  GPM_CUDA(cudaMemcpyAsync(dk.get(), keys.data(), sizeof(u64) * (world - 1), cudaMemcpyHostToDevice, s));
   ++tl.launches;
-  lower_bound_kernel<<<1, 32, 0, s>>>(w.get(), n1 + 1, dk.get(), 2, dout.get());
+  lower_bound_kernel<<<(world + 31) / 32, 32, 0, s>>>(w.get(), n1 + 1, dk.get(), world - 1, dout.get());
   GPM_CUDA(cudaGetLastError());
-  u64 res[2];
-  GPM_CUDA(cudaMemcpyAsync(res, dout.get(), sizeof res, cudaMemcpyDeviceToHost, s));
+  std::vector<u64> res(world - 1);
+  GPM_CUDA(cudaMemcpyAsync(res.data(), dout.get(), sizeof(u64) * (world - 1), cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaStreamSynchronize(s));
-  lo = std::min(res[0], n1);
-  hi = rank == world - 1 ? n1 : std::min(res[1], n1);
+  for (int r = 1; r < world; ++r) bounds[r] = std::min(std::max(res[r - 1], bounds[r - 1]), n1);
+}
+
+void root_split(const gpm_graph& g, const u32* idx, const u32* vid, u64 n1, int app, int rank, int world, u64& lo,
+                u64& hi, cudaStream_t s, Timeline& tl) {
+  std::vector<u64> b;
+  root_split_bounds(g, idx, vid, n1, app, world, b, s, tl);
+  lo = b[rank];
+  hi = b[rank + 1];
+}
+
+// Work-stealing grab (device side): one thread walks the ranks' tail counters
+// from its own rank on and claims the next chunk with a system-scope atomic on
+// the (possibly NVLink-peer-mapped) counter.  out = [lo, hi) or [0, 0).
+__global__ void steal_grab_kernel(unsigned long long* ctrs, const u64* __restrict__ tlo, const u64* __restrict__ thi,
+                                  int world, int rank, u64 chunk, u64* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int k = 0; k < world; ++k) {
+    const int v = (rank + k) % world;
+    const u64 len = thi[v] - tlo[v];
+    if (*(volatile unsigned long long*)(ctrs + v) >= len) continue;
+    const u64 t = atomicAdd_system(ctrs + v, (unsigned long long)chunk);
+    if (t < len) {
+      out[0] = tlo[v] + t;
+      out[1] = tlo[v] + min(t + chunk, len);
+      return;
+    }
+  }
+  out[0] = out[1] = 0;
+}
+
+void steal_grab(unsigned long long* ctrs, const u64* d_tlo, const u64* d_thi, int world, int rank, u64 chunk,
+                u64* d_out, u64& lo, u64& hi, cudaStream_t s) {
+  steal_grab_kernel<<<1, 32, 0, s>>>(ctrs, d_tlo, d_thi, world, rank, chunk, d_out);
+  GPM_CUDA(cudaGetLastError());
+  u64 r[2];
+  GPM_CUDA(cudaMemcpyAsync(r, d_out, sizeof r, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  lo = r[0];
+  hi = r[1];
 }
 
 // out-degree maximum of a freshly built device CSR (sets gpm_graph::max_deg)

@@ -1075,18 +1075,22 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   const u32* l1vid = nullptr;
   build_level1(*G, l1i, l1v, n1, s, tl, &l1vid, &l1s);
   if (!l1vid) l1vid = l1v.get();
+  // root units of this rank: an explicit slice, the degree-weighted static
+  // split, or (steal_ctrs set) the split's head + a device-side stealing tail
+  const int world = std::max(1, cfg.world);
+  const bool steal = world > 1 && cfg.steal_ctrs && cfg.root_hi == 0;
   u64 lo = 0, hi = n1;
+  std::vector<u64> bounds;
   if (cfg.root_hi > 0) {
     lo = std::min(cfg.root_lo, n1);
     hi = std::min(cfg.root_hi, n1);
     if (hi < lo) hi = lo;
-  } else {
-    root_split(*G, l1i.get(), l1vid, n1, app, cfg.rank, std::max(1, cfg.world), lo, hi, s, tl);
+  } else if (world > 1) {
+    root_split_bounds(*G, l1i.get(), l1vid, n1, app, world, bounds, s, tl);
+    lo = bounds[cfg.rank];
+    hi = bounds[cfg.rank + 1];
   }
-  const u64 nroot = hi - lo;
   htrace(s, "level1 built");
-  if (nroot >= (u64(1) << 32)) throw Error(GPM_EINVAL, "level 1 exceeds 2^32 entries");
-  st.level_sizes[0] = nroot;
 
   Ctx c{};
   c.G = G;
@@ -1114,21 +1118,59 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   c.d_ctr = d_ctr.get();
 
   htrace(s, "setup (meminfo, counters)");
-  VLevels L{};
-  L.idx[0] = l1i.get() + lo;
-  L.vid[0] = l1vid + lo;
   const int appk = (app == GPM_APP_MC) ? kAppMC : kAppCF;  // TC == CF with k=3 (Listing 3)
-  if (k == 2 || nroot == 0) {
-    res.total = (k == 2) ? nroot : 0;
-  } else if (appk == kAppMC && k == 3 && l1s.get() && !c.generic_mc) {
-    mc3_staged(*G, l1s.get(), lo, hi, c.d_hist, s, tl, st);
-  } else if (appk == kAppMC) {
-    process_dispatch<kAppMC>(c, 1, L, nroot);
-  } else if (G->oriented && G->n < (1u << 27) && !std::getenv("GPM_GENERIC_L1")) {  // key = u << 5 | slot
-    process_l1_cf(c, L, l1i.get(), lo, hi);
+  u64 nroot = 0;  // level-1 entries processed by this rank
+  auto run_slice = [&](u64 slo, u64 shi) {
+    const u64 np = shi - slo;
+    if (np >= (u64(1) << 32)) throw Error(GPM_EINVAL, "level 1 exceeds 2^32 entries");
+    nroot += np;
+    st.level_sizes[0] += np;
+    if (k == 2 || np == 0) return;
+    VLevels L{};
+    L.idx[0] = l1i.get() + slo;
+    L.vid[0] = l1vid + slo;
+    if (appk == kAppMC && k == 3 && l1s.get() && !c.generic_mc) {
+      mc3_staged(*G, l1s.get(), slo, shi, c.d_hist, s, tl, st);
+    } else if (appk == kAppMC) {
+      process_dispatch<kAppMC>(c, 1, L, np);
+    } else if (G->oriented && G->n < (1u << 27) && !std::getenv("GPM_GENERIC_L1")) {  // key = u << 5 | slot
+      process_l1_cf(c, L, l1i.get(), slo, shi);
+    } else {
+      process_dispatch<kAppCF>(c, 1, L, np);
+    }
+  };
+  if (!steal) {
+    run_slice(lo, hi);
   } else {
-    process_dispatch<kAppCF>(c, 1, L, nroot);
+    // head: the first (1 - tail) of the own static range, no contention;
+    // tails: every rank's remainder, claimed in chunks through the shared
+    // counters (own tail first, then the others'), so a rank that finishes
+    // early drains the slow ranks' work.
+    const double tail = 0.25;
+    std::vector<u64> tlo(world), thi(world);
+    u64 tsum = 0;
+    for (int r = 0; r < world; ++r) {
+      const u64 len = bounds[r + 1] - bounds[r];
+      tlo[r] = bounds[r] + (u64)((1.0 - tail) * (double)len);
+      thi[r] = bounds[r + 1];
+      tsum += thi[r] - tlo[r];
+    }
+    run_slice(lo, tlo[cfg.rank]);
+    const u64 chunk = cfg.steal_chunk ? cfg.steal_chunk : std::max<u64>(1024, tsum / ((u64)world * 32));
+    DBuf<u64> d_t(2 * world, s), d_out(2, s);
+    GPM_CUDA(cudaMemcpyAsync(d_t.get(), tlo.data(), sizeof(u64) * world, cudaMemcpyHostToDevice, s));
+    GPM_CUDA(cudaMemcpyAsync(d_t.get() + world, thi.data(), sizeof(u64) * world, cudaMemcpyHostToDevice, s));
+    for (;;) {
+      u64 clo = 0, chi = 0;
+      steal_grab(reinterpret_cast<unsigned long long*>(cfg.steal_ctrs), d_t.get(), d_t.get() + world, world,
+                 cfg.rank, chunk, d_out.get(), clo, chi, s);
+      ++tl.launches;
+      if (clo >= chi) break;
+      ++st.chunks;
+      run_slice(clo, chi);
+    }
   }
+  if (k == 2) res.total = nroot;
 
   htrace(s, "levels processed");
   // multi-GPU: the only collectives are the per-pattern counts and the
@@ -1171,7 +1213,7 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
               [](const gpm_result::Pattern& x, const gpm_result::Pattern& y) { return x.text < y.text; });
     st.level_sizes[levels - 1] += acc;
     res.total = acc;
-  } else if (k > 2 && nroot > 0) {
+  } else if (k > 2) {
     unsigned long long t = 0;
     GPM_CUDA(cudaMemcpyAsync(&t, d_total.get(), sizeof t, cudaMemcpyDeviceToHost, s));
     GPM_CUDA(cudaStreamSynchronize(s));

@@ -10,12 +10,18 @@ exchanges are:
           reduction, so it is an all-gather of the packed words followed by an
           OR-reduction on the device
   * op 2  all-gather (FSM pattern-key union)
+
+Load balance beyond the static split: ``StealCounters`` creates the shared
+work-stealing counters of gpm_config.steal_ctrs (one uint64 per rank on rank
+0's GPU, exported by CUDA IPC and peer-mapped over NVLink by the other ranks);
+the engine claims chunks of every rank's tail with device-side system-scope
+atomics once its own head is done.
 """
 from __future__ import annotations
 
 import ctypes as C
 
-from ._lib import EXCHANGE_FN
+from ._lib import EXCHANGE_FN, check, lib
 
 _TYPESTR = {1: "|u1", 4: "<u4", 8: "<u8"}
 
@@ -73,3 +79,49 @@ def make_exchange(group=None):
             return 1
 
     return EXCHANGE_FN(_cb)
+
+
+class StealCounters:
+    """Shared steal counters for one process per GPU (gpm_steal_* in gpm.h).
+
+    Rank 0 allocates ``world`` counters on its device and broadcasts the CUDA
+    IPC handle; every other rank opens it (peer mapping).  Call ``reset()``
+    (collective) before each mine; pass ``ptr`` as ``steal_ctrs``."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        dev = torch.cuda.current_device()
+        L = lib()
+        handle = (C.c_char * 64)()
+        ptr = C.c_void_p()
+        if self.rank == 0:
+            check(L.gpm_steal_create(dev, self.world, C.byref(ptr), handle))
+        on_cuda = dist.get_backend(group) == "nccl"
+        h = torch.tensor(list(bytes(handle)), dtype=torch.uint8, device="cuda" if on_cuda else "cpu")
+        dist.broadcast(h, 0, group=group)
+        if self.rank != 0:
+            raw = bytes(h.cpu().tolist())
+            check(L.gpm_steal_open(dev, raw, C.byref(ptr)))
+        self._opened = int(self.rank != 0)
+        self.ptr = ptr.value
+
+    def reset(self):
+        import torch.distributed as dist
+        dist.barrier(group=self.group)
+        if self.rank == 0:
+            check(lib().gpm_steal_reset(self.ptr, self.world, None))
+        dist.barrier(group=self.group)
+
+    def close(self):
+        import torch.distributed as dist
+        dist.barrier(group=self.group)   # peers unmap before the owner frees
+        if self._opened and self.ptr:
+            check(lib().gpm_steal_release(self.ptr, 1))
+        dist.barrier(group=self.group)
+        if not self._opened and self.ptr:
+            check(lib().gpm_steal_release(self.ptr, 0))
+        self.ptr = None

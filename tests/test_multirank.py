@@ -130,7 +130,7 @@ class ThreadedExchange:
         return EXCHANGE_FN(cb)
 
 
-def _run_ranks(P, hg, app, k, sigma, world):
+def _run_ranks(P, hg, app, k, sigma, world, steal=None, steal_chunk=0):
     ex = ThreadedExchange(world)
     out = [None] * world
     errs = []
@@ -139,7 +139,8 @@ def _run_ranks(P, hg, app, k, sigma, world):
     def run(r):
         try:
             g = P.Graph(hg)
-            out[r] = P.mine(g, app, k, sigma, rank=r, world=world, exchange=fns[r])
+            kw = dict(steal_ctrs=steal.data_ptr(), steal_chunk=steal_chunk) if steal is not None else {}
+            out[r] = P.mine(g, app, k, sigma, rank=r, world=world, exchange=fns[r], **kw)
         except Exception as e:
             errs.append(e)
             ex.barrier.abort()
@@ -168,3 +169,89 @@ def test_threaded_ranks_match_single(world):
             assert r.patterns == base.patterns, (app, k)
             assert r.stats["n_explored"] == base.stats["n_explored"], (app, k)
             assert r.stats["level_sizes"] == base.stats["level_sizes"], (app, k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,chunk", [(2, 0), (3, 97), (4, 1024)])
+def test_threaded_work_stealing_tail(world, chunk):
+    """Device-side stealing over shared counters (gpm_config.steal_ctrs): every
+    level-1 root unit is mined exactly once whatever the interleaving, so the
+    reduced result equals the single-rank one."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1911_06969_b200 as P
+    hg = P.generate_rmat(13, 8, 0.57, 0.19, 0.19, seed=6)
+    for app, k in (("tc", 3), ("cf", 4), ("cf", 5), ("mc", 3), ("mc", 4)):
+        base = P.mine(P.Graph(hg), app, k)
+        ctrs = torch.zeros(world, dtype=torch.int64, device="cuda")
+        outs = _run_ranks(P, hg, app, k, 0, world, steal=ctrs, steal_chunk=chunk)
+        for r in outs:
+            assert r.total == base.total, (app, k)
+            assert r.patterns == base.patterns, (app, k)
+            assert r.stats["n_explored"] == base.stats["n_explored"], (app, k)
+            assert r.stats["level_sizes"] == base.stats["level_sizes"], (app, k)
+            assert r.stats["candidates"] == base.stats["candidates"], (app, k)
+        # every tail was drained: counters >= the tail lengths
+        assert int(ctrs.min().item()) > 0
+
+
+def _ipc_worker(rank, world, port, q):
+    """One process per rank on the same GPU: the steal counters live on rank
+    0's allocation and are opened by the other ranks through CUDA IPC (the
+    multi-GPU path peer-maps them over NVLink the same way)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1911_06969_b200 as P
+        from paper_1911_06969_b200._lib import EXCHANGE_FN
+        from paper_1911_06969_b200.dist import StealCounters, _DevArray, exchange_op
+
+        def cb(ctx, ptr, count, eb, op, stream):  # device buffer -> host gloo collective -> device
+            t = torch.as_tensor(_DevArray(ptr, count, eb), device="cuda")
+            t = t.view(torch.int64) if eb == 8 else t.view(torch.int32)
+            h = t.cpu()
+            exchange_op(h, op)
+            t.copy_(h.to("cuda"))
+            torch.cuda.synchronize()
+            return 0
+
+        fn = EXCHANGE_FN(cb)
+        steal = StealCounters()
+        hg = P.generate_rmat(13, 8, 0.57, 0.19, 0.19, seed=8)
+        out = {}
+        for app, k in (("tc", 3), ("cf", 4), ("mc", 3)):
+            steal.reset()
+            r = P.mine(P.Graph(hg), app, k, rank=rank, world=world, exchange=fn, steal_ctrs=steal.ptr, steal_chunk=64)
+            out[f"{app}{k}"] = (r.total, r.stats["n_explored"], sorted(r.patterns))
+        steal.close()
+        q.put((rank, out))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_ipc_steal_counters_two_processes():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1911_06969_b200 as P
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    hg = P.generate_rmat(13, 8, 0.57, 0.19, 0.19, seed=8)
+    for r in range(world):
+        assert isinstance(res[r], dict), res[r]
+        for app, k in (("tc", 3), ("cf", 4), ("mc", 3)):
+            base = P.mine(P.Graph(hg), app, k)
+            assert res[r][f"{app}{k}"] == (base.total, base.stats["n_explored"], sorted(base.patterns)), (app, k)
