@@ -168,8 +168,9 @@ __device__ __forceinline__ u64 child_code(const EEmb<LEV>& E, const DevGraph& g,
 }
 
 // Open-addressing table of quick codes; entry = {key, val} in 16 B so a probe
-// touches one sector.  val = embedding count during pass A, then
-// (pattern id << 32 | packed PositionMap) once the level is canonicalised.
+// touches one sector.  During pass A val = (dense quick-code id << 40 | count)
+// (ids 1.. in insertion order); once the level is canonicalised val is
+// overwritten with (pattern id << 32 | packed PositionMap).
 struct Hash {
   unsigned long long* ent;     // 2 x capacity: ent[2h] key (0 = empty), ent[2h+1] val
   u64 mask;                    // capacity - 1
@@ -191,31 +192,34 @@ constexpr int kMaxProbe = 256;
 // Insert-or-add with bounded linear probing.  Once the table is flagged as
 // overflowing (load > 1/2 or a probe run > kMaxProbe) inserts stop at once;
 // the host regrows the table and re-runs the pass.
-__device__ __forceinline__ void hash_add(const Hash& H, u64 key, unsigned long long c) {
-  if (*(volatile int*)H.overflow) return;
+constexpr u64 kCountMask = (u64(1) << 40) - 1;
+
+// Returns the key's dense id (>= 1), or 0 once the table overflowed.
+__device__ __forceinline__ u32 hash_add(const Hash& H, u64 key, unsigned long long c) {
+  if (*(volatile int*)H.overflow) return 0;
   u64 h = hash64(key) & H.mask;
   for (int probe = 0; probe < kMaxProbe; ++probe) {
     unsigned long long cur = H.ent[2 * h];
-    if (cur == key) {
-      atomicAdd(H.ent + 2 * h + 1, c);
-      return;
-    }
     if (cur == 0) {
       unsigned long long prev = atomicCAS(H.ent + 2 * h, 0ull, (unsigned long long)key);
       if (prev == 0ull) {
-        unsigned long long n = atomicAdd(H.used, 1ull);
+        const unsigned long long n = atomicAdd(H.used, 1ull);
         if (n * 2 >= H.mask) atomicOr(H.overflow, 1);
-        atomicAdd(H.ent + 2 * h + 1, c);
-        return;
+        atomicAdd(H.ent + 2 * h + 1, ((unsigned long long)(n + 1) << 40) + c);
+        return (u32)(n + 1);
       }
-      if (prev == key) {
-        atomicAdd(H.ent + 2 * h + 1, c);
-        return;
-      }
+      cur = prev;
+    }
+    if (cur == key) {
+      unsigned long long v = atomicAdd(H.ent + 2 * h + 1, c);
+      // the inserting thread publishes the id right after its CAS
+      while ((v >> 40) == 0) v = *(volatile unsigned long long*)(H.ent + 2 * h + 1);
+      return (u32)(v >> 40);
     }
     h = (h + 1) & H.mask;
   }
   atomicOr(H.overflow, 2);
+  return 0;
 }
 
 __device__ __forceinline__ u64 hash_info(const Hash& H, u64 slot) { return H.ent[2 * slot + 1]; }
@@ -244,6 +248,10 @@ struct FsmArgs {
   const u32* bslot;       // pattern -> bitmap slot or ~0
   u32* bitmaps;
   u64 words;
+  const u32* lrank;       // vertex -> rank within its label class (label-local bitmap index)
+  u32* qbm;               // fused last level: domain bitmaps per quick-code id (quick positions)
+  u64 qcap;               // ids with a bitmap
+  int* qover;             // set when an id >= qcap appeared (host falls back to a domain pass)
   int kpos;
   u32 round_lo, round_hi;
   const u8* frequent;     // pattern -> MNI >= sigma
@@ -265,8 +273,9 @@ __device__ __forceinline__ void domain_or(const FsmArgs& a, u64 info, const u32*
   for (int i = 0; i < cnv; ++i) {
     const u32 cp = (perm >> (3 * i)) & 7u;
     const u32 v = cv[i];
-    u32* wp = base + (u64)cp * a.words + (v >> 5);
-    const u32 bit = 1u << (v & 31);
+    const u32 lr = ldg(a.lrank + v);  // all vertices at one position share its label
+    u32* wp = base + (u64)cp * a.words + (lr >> 5);
+    const u32 bit = 1u << (lr & 31);
     // domains saturate quickly: test before the read-modify-write so most
     // embeddings cost a cached load instead of an L2 atomic (a stale read only
     // causes a redundant, still-correct atomicOr)
@@ -394,7 +403,27 @@ __global__ void __launch_bounds__(kThreads) eextend_kernel(FsmArgs a) {
         if (mask) {
           const unsigned long long key = ok ? code : ~0ull;
           const u32 peers = __match_any_sync(0xffffffffu, key);
-          if (ok && lane == __ffs(peers) - 1) hash_add(a.H, code, __popc(peers));
+          const int leader = __ffs(peers) - 1;
+          u32 id = 0;
+          if (ok && lane == leader) id = hash_add(a.H, code, __popc(peers));
+          if (a.qbm) {
+            // fused last level: OR the child's vertices into its quick code's
+            // domain bitmaps (quick positions; merged per canonical pattern later)
+            id = __shfl_sync(0xffffffffu, id, leader);
+            if (ok && id) {
+              if (id - 1 < a.qcap) {
+                u32* base = a.qbm + (u64)(id - 1) * a.kpos * a.words;
+                for (int i = 0; i < cnv; ++i) {
+                  const u32 lr = ldg(a.lrank + cv[i]);
+                  u32* wp = base + (u64)i * a.words + (lr >> 5);
+                  const u32 bit = 1u << (lr & 31);
+                  if (!(*wp & bit)) atomicOr(wp, bit);
+                }
+              } else {
+                *a.qover = 1;
+              }
+            }
+          }
         }
       } else if (MODE == kDomain) {
         if (ok) {
@@ -461,10 +490,12 @@ __global__ void l1_kernel(FsmArgs a, const u32* __restrict__ idx, const u32* __r
 
 // canonicalize every occupied hash slot once (reduce step 2)
 __global__ void canon_slots_kernel(const unsigned long long* __restrict__ ent, u64 cap, int LB,
-                                   u64* __restrict__ canon, u32* __restrict__ perm, u64* __restrict__ counts) {
+                                   u64* __restrict__ canon, u32* __restrict__ perm, u64* __restrict__ counts,
+                                   u32* __restrict__ ids) {
   for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < cap; s += (u64)gridDim.x * blockDim.x) {
     const u64 key = ent[2 * s];
-    counts[s] = ent[2 * s + 1];
+    counts[s] = ent[2 * s + 1] & kCountMask;
+    ids[s] = (u32)(ent[2 * s + 1] >> 40);
     if (!key) {
       canon[s] = ~0ull;
       continue;
@@ -477,6 +508,52 @@ __global__ void canon_slots_kernel(const unsigned long long* __restrict__ ent, u
     u32 pk = 0;
     for (int i = 0; i < nv; ++i) pk |= (u32)p[i] << (3 * i);
     perm[s] = pk;
+  }
+}
+
+// occupied slots -> (canonical key, count) in any order (sorted afterwards)
+__global__ void compact_slots_kernel(const u64* __restrict__ canon, const u64* __restrict__ counts, u64 cap,
+                                     unsigned long long* __restrict__ top, u64* __restrict__ ok,
+                                     u64* __restrict__ oc) {
+  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < cap; s += (u64)gridDim.x * blockDim.x) {
+    const u64 c = canon[s];
+    if (c == ~0ull) continue;
+    const u64 i = atomicAdd(top, 1ull);
+    ok[i] = c;
+    oc[i] = counts[s];
+  }
+}
+
+// Fused last level: OR each quick code's position bitmaps into its canonical
+// pattern's bitmaps through the PositionMap (one warp per quick code).
+__global__ void merge_qbm_kernel(const u32* __restrict__ qbm, const u64* __restrict__ canon,
+                                 const u32* __restrict__ ids, const u32* __restrict__ perm, u64 cap,
+                                 const u64* __restrict__ gkeys, u64 P, const u32* __restrict__ bslot, u32 round_lo,
+                                 u32 round_hi, u32* __restrict__ bitmaps, u64 words, int kpos) {
+  const int lane = threadIdx.x & 31;
+  for (u64 sl = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; sl < cap;
+       sl += ((u64)gridDim.x * blockDim.x) >> 5) {
+    const u64 c = canon[sl];
+    if (c == ~0ull) continue;
+    u64 lo = 0, hi = P;  // pattern id of the canonical key
+    while (lo < hi) {
+      const u64 mid = (lo + hi) >> 1;
+      if (gkeys[mid] < c) lo = mid + 1;
+      else hi = mid;
+    }
+    const u32 bs = bslot[lo];
+    if (bs < round_lo || bs >= round_hi) continue;
+    const int nv = pat::code_nv(c);
+    const u32 pm = perm[sl];
+    const u32* q = qbm + (u64)(ids[sl] - 1) * kpos * words;
+    u32* b = bitmaps + (u64)(bs - round_lo) * kpos * words;
+    for (int i = 0; i < nv; ++i) {
+      const u32 cp = (pm >> (3 * i)) & 7u;
+      for (u64 w = lane; w < words; w += 32) {
+        const u32 v = q[(u64)i * words + w];
+        if (v) atomicOr(b + (u64)cp * words + w, v);
+      }
+    }
   }
 }
 
@@ -534,6 +611,28 @@ __global__ void egather_kernel(const u64* __restrict__ w, const u32* __restrict_
     Wp[i] = w[pidx[i]];
 }
 
+__global__ void iota_kernel(u32* __restrict__ v, u32 n) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) v[i] = (u32)i;
+}
+
+// sorted (label, vertex) -> rank of each vertex within its label class; the
+// largest class size -> *mx
+__global__ void lrank_kernel(const u32* __restrict__ lab, const u32* __restrict__ vid, u32 n, u32* __restrict__ lrank,
+                             unsigned long long* __restrict__ mx) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    // class start: first index with the same label (binary search)
+    u64 lo = 0, hi = i;
+    const u32 L = lab[i];
+    while (lo < hi) {
+      const u64 mid = (lo + hi) >> 1;
+      if (lab[mid] < L) lo = mid + 1;
+      else hi = mid;
+    }
+    lrank[vid[i]] = (u32)(i - lo);
+    if (i + 1 == n || lab[i + 1] != L) atomicMax(mx, (unsigned long long)(i - lo + 1));
+  }
+}
+
 inline unsigned grid1(u64 items) { return (unsigned)std::max<u64>(1, std::min<u64>((items + 255) / 256, 1u << 20)); }
 
 // ------------------------------------------------------------------ host driver
@@ -552,6 +651,30 @@ struct Fsm {
   u64 budget;
   u64 prev_unique = 1024;
   DBuf<unsigned long long> d_ctr;
+  DBuf<u32> lrank;   // vertex -> rank within its label class
+  u64 max_class = 1;
+
+  // lrank[v] = #{u < v : lab[u] == lab[v]} via a stable sort of (label, v)
+  void label_ranks() {
+    const u32 n = G.n;
+    lrank.alloc(std::max<u32>(1, n), s);
+    if (!n) return;
+    DBuf<u32> lab2(n, s), vid(n, s), vid2(n, s);
+    iota_kernel<<<grid1(n), 256, 0, s>>>(vid.get(), n);
+    GPM_CUDA(cudaGetLastError());
+    size_t tmp = 0;
+    GPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, G.d_lab, lab2.get(), vid.get(), vid2.get(), (int64_t)n, 0,
+                                             std::max(1, LB), s));
+    DBuf<u8> t(tmp, s);
+    GPM_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, G.d_lab, lab2.get(), vid.get(), vid2.get(), (int64_t)n, 0,
+                                             std::max(1, LB), s));
+    DBuf<unsigned long long> mx(1, s);
+    GPM_CUDA(cudaMemsetAsync(mx.get(), 0, sizeof(unsigned long long), s));
+    lrank_kernel<<<grid1(n), 256, 0, s>>>(lab2.get(), vid2.get(), n, lrank.get(), mx.get());
+    GPM_CUDA(cudaGetLastError());
+    tl.launches += 4;
+    max_class = std::max<u64>(1, d2h(mx.get()));
+  }
 
   Fsm(const gpm_graph& G_, const gpm_config& c_, cudaStream_t s_, Stats& st_, Timeline& tl_, gpm_result& r_)
       : G(G_), cfg(c_), g(G_.view()), s(s_), st(st_), tl(tl_), res(r_) {}
@@ -580,7 +703,7 @@ struct Fsm {
     DBuf<unsigned long long> ent, used;
     DBuf<int> overflow;
     DBuf<u64> canon;
-    DBuf<u32> perm, bslot, bs_to_pid;
+    DBuf<u32> perm, bslot, bs_to_pid, ids;
     DBuf<u8> frequent;
     std::vector<u64> gkeys_h, gcount_h, mni_h;
     DBuf<u64> gkeys;
@@ -607,38 +730,56 @@ struct Fsm {
   void canon_and_group(Level& R) {
     R.canon.alloc(R.cap, s);
     R.perm.alloc(R.cap, s);
-    DBuf<unsigned long long> cc(R.cap, s), cc2(R.cap, s);
+    DBuf<unsigned long long> cc(R.cap, s);
+    R.ids.alloc(R.cap, s);
     canon_slots_kernel<<<grid1(R.cap), 256, 0, s>>>(R.ent.get(), R.cap, LB, R.canon.get(), R.perm.get(),
-                                                    reinterpret_cast<u64*>(cc.get()));
+                                                    reinterpret_cast<u64*>(cc.get()), R.ids.get());
     GPM_CUDA(cudaGetLastError());
     ++tl.launches;
-    // compact (canon, count) of occupied slots, sort by canon, reduce by key
-    DBuf<u64> ck(R.cap, s), ck2(R.cap, s);
-    GPM_CUDA(cudaMemcpyAsync(ck.get(), R.canon.get(), sizeof(u64) * R.cap, cudaMemcpyDeviceToDevice, s));
-    size_t tmp = 0;
-    GPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ck.get(), ck2.get(), cc.get(), cc2.get(), (int64_t)R.cap, 0,
-                                             64, s));
-    DBuf<u8> t(tmp, s);
-    GPM_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, ck.get(), ck2.get(), cc.get(), cc2.get(), (int64_t)R.cap, 0,
-                                             64, s));
-    // occupied slots are the first U entries (empty = ~0 sorts last)
+    // compact (canon, count) of the U occupied slots, sort by canon, reduce by
+    // key on the device: only the distinct canonical patterns come back
     const u64 U = d2h(R.used.get());
-    trace("canon+sort", (double)U, (double)R.cap);
-    std::vector<u64> keys(U), cnts(U);
+    DBuf<u64> ck(std::max<u64>(1, U), s), ck2(std::max<u64>(1, U), s);
+    DBuf<unsigned long long> cc3(std::max<u64>(1, U), s), cc4(std::max<u64>(1, U), s);
+    DBuf<unsigned long long> top(1, s);
+    GPM_CUDA(cudaMemsetAsync(top.get(), 0, sizeof(unsigned long long), s));
+    compact_slots_kernel<<<grid1(R.cap), 256, 0, s>>>(R.canon.get(), reinterpret_cast<const u64*>(cc.get()), R.cap,
+                                                      top.get(), ck.get(), reinterpret_cast<u64*>(cc3.get()));
+    GPM_CUDA(cudaGetLastError());
+    ++tl.launches;
+    std::vector<u64> keys, cnts;
     if (U) {
-      GPM_CUDA(cudaMemcpyAsync(keys.data(), ck2.get(), sizeof(u64) * U, cudaMemcpyDeviceToHost, s));
-      GPM_CUDA(cudaMemcpyAsync(cnts.data(), cc2.get(), sizeof(u64) * U, cudaMemcpyDeviceToHost, s));
+      size_t tmp = 0;
+      GPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ck.get(), ck2.get(), cc3.get(), cc4.get(), (int64_t)U, 0,
+                                               64, s));
+      DBuf<u8> t(tmp, s);
+      GPM_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, ck.get(), ck2.get(), cc3.get(), cc4.get(), (int64_t)U, 0,
+                                               64, s));
+      DBuf<u64> nuniq(1, s);
+      size_t tmp2 = 0;
+      GPM_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, tmp2, ck2.get(), ck.get(), cc4.get(), cc3.get(), nuniq.get(),
+                                              cuda::std::plus<unsigned long long>{}, (int64_t)U, s));
+      DBuf<u8> t2(tmp2, s);
+      GPM_CUDA(cub::DeviceReduce::ReduceByKey(t2.get(), tmp2, ck2.get(), ck.get(), cc4.get(), cc3.get(), nuniq.get(),
+                                              cuda::std::plus<unsigned long long>{}, (int64_t)U, s));
+      const u64 PU = d2h(nuniq.get());
+      keys.resize(PU);
+      cnts.resize(PU);
+      GPM_CUDA(cudaMemcpyAsync(keys.data(), ck.get(), sizeof(u64) * PU, cudaMemcpyDeviceToHost, s));
+      GPM_CUDA(cudaMemcpyAsync(cnts.data(), cc3.get(), sizeof(u64) * PU, cudaMemcpyDeviceToHost, s));
       sync();
     }
+    trace("canon+sort", (double)U, (double)R.cap);
     // multi-GPU: all-gather every rank's (canonical key, count) list
     if (cfg.world > 1 && cfg.exchange) {
       const int W = cfg.world;
+      const u64 nk = keys.size();
       std::vector<u64> lens(W, 0);
-      lens[cfg.rank] = U;
+      lens[cfg.rank] = nk;
       exchange_sum_host(cfg, lens, s);
       u64 mx = *std::max_element(lens.begin(), lens.end());
       std::vector<u64> buf(2 * mx * W, 0);
-      for (u64 i = 0; i < U; ++i) {
+      for (u64 i = 0; i < nk; ++i) {
         buf[(u64)cfg.rank * 2 * mx + i] = keys[i];
         buf[(u64)cfg.rank * 2 * mx + mx + i] = cnts[i];
       }
@@ -698,7 +839,10 @@ struct Fsm {
   // Domain pass in rounds that fit the bitmap budget; MNI; frequent flags.
   template <class DomainFn>
   void domains_and_mni(Level& R, int kpos, DomainFn&& run_domain) {
-    const u64 words = (G.n + 31) / 32;
+    // label-local domain bitmaps: a position's vertices all carry its label,
+    // so bits are indexed by the rank within the label class (n/#labels bits
+    // per position instead of n)
+    const u64 words = (max_class + 31) / 32;
     const u64 per_pat = (u64)kpos * words * 4;
     const u64 per_round = std::max<u64>(1, std::min<u64>(R.NB, budget / 2 / std::max<u64>(1, per_pat)));
     DBuf<unsigned long long> mni(std::max<u64>(1, R.P), s);
@@ -772,6 +916,7 @@ struct Fsm {
       a.bslot = R.bslot.get();
       a.bitmaps = bm;
       a.words = words;
+      a.lrank = lrank.get();
       a.kpos = kpos;
       a.round_lo = lo;
       a.round_hi = hi;
@@ -888,16 +1033,43 @@ struct Fsm {
     // 2^26 entries = 1 GB) so the pass rarely has to regrow and re-run
     u64 cap = 1u << 16;
     while (cap < std::min<u64>(u64(1) << 26, std::max<u64>(2 * W, 64 * prev_unique))) cap <<= 1;
+    // Last level: fuse the domain pass into pass A.  Children OR their vertices
+    // into per-quick-code bitmaps (label-local, quick positions); after
+    // canonicalisation these are merged into the canonical patterns' bitmaps
+    // through the PositionMaps, so the level is extended once, not twice.
+    const int kposL = LEV + 2;
+    const u64 wordsL = (max_class + 31) / 32;
+    const u64 per_id = (u64)kposL * wordsL * 4;
+    DBuf<u32> qbm;
+    DBuf<int> qover(1, s);
+    u64 qcap = 0;
+    if (last && nb && !std::getenv("GPM_FSM_TWO_PASS")) {
+      qcap = std::min<u64>(cap / 2, budget / 4 / std::max<u64>(1, per_id));
+      if (qcap >= 1024) qbm.alloc(qcap * kposL * wordsL, s);
+      else qcap = 0;
+    }
     for (;;) {
       alloc_hash(R, cap);
       GPM_CUDA(cudaMemsetAsync(accepted.get(), 0, sizeof(unsigned long long), s));
+      GPM_CUDA(cudaMemsetAsync(qover.get(), 0, sizeof(int), s));
+      if (qcap) GPM_CUDA(cudaMemsetAsync(qbm.get(), 0, sizeof(u32) * qcap * kposL * wordsL, s));
       if (nb) {
         FsmArgs a = args(R);
-        launch<LEV>(a, kQC, "fsm_extend_qc", bytes_in);
+        if (qcap) {
+          a.qbm = qbm.get();
+          a.qcap = qcap;
+          a.qover = qover.get();
+          a.kpos = kposL;
+          a.words = wordsL;
+          a.lrank = lrank.get();
+        }
+        launch<LEV>(a, kQC, qcap ? "fsm_extend_qc_domain" : "fsm_extend_qc", bytes_in);
       }
       if (d2h(R.overflow.get()) == 0) break;
       cap <<= 3;
     }
+    const bool fused = qcap && d2h(qover.get()) == 0;
+    if (!fused) qbm.release();  // more quick codes than bitmaps: separate domain pass
     u64 acc = d2h(accepted.get());
     prev_unique = d2h(R.used.get());
     trace("pass A (qc)", (double)acc, (double)R.cap);
@@ -910,10 +1082,18 @@ struct Fsm {
     canon_and_group(R);
     domains_and_mni(R, LEV + 2, [&](u32* bm, u64 words, int kpos, u32 lo, u32 hi) {
       if (!nb) return;
+      if (fused) {
+        merge_qbm_kernel<<<grid1(R.cap * 32), 256, 0, s>>>(qbm.get(), R.canon.get(), R.ids.get(), R.perm.get(), R.cap,
+                                                           R.gkeys.get(), R.P, R.bslot.get(), lo, hi, bm, words, kpos);
+        GPM_CUDA(cudaGetLastError());
+        ++tl.launches;
+        return;
+      }
       FsmArgs a = args(R);
       a.bslot = R.bslot.get();
       a.bitmaps = bm;
       a.words = words;
+      a.lrank = lrank.get();
       a.kpos = kpos;
       a.round_lo = lo;
       a.round_hi = hi;
@@ -967,6 +1147,7 @@ struct Fsm {
     (void)totalb;
     budget = cfg.mem_budget ? cfg.mem_budget : (u64)(0.5 * (double)freeb);
     d_ctr.alloc(1, s);
+    label_ranks();
     const int levels = k - 1;
     st.ensure(levels);
     DBuf<u32> l1i, l1v;
