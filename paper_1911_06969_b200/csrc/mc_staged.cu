@@ -272,8 +272,6 @@ __global__ void __launch_bounds__(kT, 3) mc3_block_kernel(Mc3Args a) {
   __shared__ u32 s_next;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const DevGraph& g = a.g;
-  constexpr u32 mask = kBSlots - 1;
-  const u32 sh = 32 - (31 - __clz(kBSlots));
   unsigned long long aX = 0, aTri = 0, aC0 = 0, aLen = 0, aCand = 0;
   for (;;) {
     __syncthreads();
@@ -297,7 +295,11 @@ __global__ void __launch_bounds__(kT, 3) mc3_block_kernel(Mc3Args a) {
     const u32 t = (u32)(q / nch);
     const u64 c = q % nch;
     const u32 k0 = t * kBKeys, k1 = min(ns, k0 + kBKeys);
-    for (u32 i = threadIdx.x * 4; i < kBSlots; i += kT * 4)
+    u32 cap = 1024;  // table sized to the tile: load <= 1/8, cleared in O(cap)
+    while (cap < 8 * (k1 - k0) && cap < kBSlots) cap <<= 1;
+    const u32 mask = cap - 1;
+    const u32 sh = 32 - (31 - __clz(cap));
+    for (u32 i = threadIdx.x * 4; i < cap; i += kT * 4)
       *reinterpret_cast<uint4*>(s_btab + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     __syncthreads();
     for (u32 i = k0 + threadIdx.x; i < k1; i += kT) hs_insert(s_btab, sh, mask, ldg(g.col + sb + i));
