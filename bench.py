@@ -339,6 +339,7 @@ def main():
                      "frac": achieved / peak, "traffic": traffic, "kernel": res.stats["dominant"],
                      "kernel_ms": dms, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                      "bytes": "SURVEY §8d B_alg of that kernel: 8*l per parent + (16 + 4*deg) per extended position"},
+        "step_ms": [round(x, 4) for x in step_ms],
         "gpu_launches": launches,
         "clocks": clock_rec,
         "result": {"total": res.total, "n_explored": n_explored, "level_sizes": res.stats["level_sizes"],

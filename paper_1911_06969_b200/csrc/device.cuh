@@ -215,10 +215,20 @@ inline void htrace(cudaStream_t s, const char* what) {
 // ordered pool holds reserved but unused (the pool keeps released blocks,
 // keep_pool_warm), so the planner's budget does not shrink from call to call.
 inline size_t device_free_bytes() {
-  size_t freeb = 0, totalb = 0;
-  GPM_CUDA(cudaMemGetInfo(&freeb, &totalb));
+  // cudaMemGetInfo costs up to ~1 ms of host time: reuse a reading taken in
+  // the last 50 ms on this device (back-to-back mine calls)
   int dev = 0;
   cudaGetDevice(&dev);
+  struct Cached {
+    int dev = -1;
+    size_t bytes = 0;
+    std::chrono::steady_clock::time_point at;
+  };
+  static thread_local Cached cache;
+  const auto now = std::chrono::steady_clock::now();
+  if (cache.dev == dev && now - cache.at < std::chrono::milliseconds(50)) return cache.bytes;
+  size_t freeb = 0, totalb = 0;
+  GPM_CUDA(cudaMemGetInfo(&freeb, &totalb));
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     unsigned long long reserved = 0, used = 0;
@@ -227,6 +237,9 @@ inline size_t device_free_bytes() {
       freeb += (size_t)(reserved - used);
   }
   cudaGetLastError();
+  cache.dev = dev;
+  cache.bytes = freeb;
+  cache.at = now;
   return freeb;
 }
 

@@ -55,7 +55,7 @@ constexpr u64 kBatchGrab = 4;       // generic-engine batches per atomic grab
 constexpr u32 kHashSlots = 1024;    // per-warp exact hash set of the root's out-list (4 KB)
 constexpr u32 kFilterMax = 512;     // out-lists longer than this are probed by binary search
 constexpr u64 kMaskChunk = 4096;    // ballot-mask words a warp reserves at a time
-constexpr u32 kSparseWords = 64;    // non-zero (step, ballot) pairs kept per CF item
+constexpr u32 kSparseWords = 64;    // accepted (parent, u) children recorded per CF item
 
 struct VLevels {
   const u32* idx[kMaxLevels];
@@ -445,9 +445,15 @@ struct EdgeArgs {
   unsigned long long* total;  // FUSED
   unsigned long long* cand;   // candidates streamed (stats)
   u32 hstride;                // per-warp hash slots (power of two)
+  const u32* wv;              // SIB: new vertex per entry (level vid array)
 };
 
-template <int MODE>
+// SIB = false: level-1 edges (src = v0, new vertex col[e], root list N+(v0)).
+// SIB = true: last CF level (k >= 4): entries of a materialised level, src =
+// parent index (sorted), new vertex w = wv[e], "root list" = the parent's
+// children wv[group] (= the common out-neighbours of the parent embedding, so
+// u ~ every earlier vertex <=> u in the group; Listing 3), FUSED only.
+template <int MODE, bool SIB>
 __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
   extern __shared__ __align__(16) u32 s_rhash[];  // [kThreads/32][hstride]
   __shared__ u64 s_cp[kThreads / 32][64];   // per parent rank: &col[cb] - 4 * exclusive start (byte address)
@@ -457,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
   __shared__ u64 s_rb[kThreads / 32][32];   // per root slot: out-list begin
   __shared__ u32 s_rk[kThreads / 32][64];   // per root slot: exclusive key start; ~0 past the roots
   __shared__ u32 s_rd[kThreads / 32][32];   // per root slot: out-degree
-  __shared__ u32 s_mw[kThreads / 32][2 * kSparseWords];  // COUNT: (step, ballot) of non-zero steps
+  __shared__ __align__(8) u32 s_mw[kThreads / 32][2 * kSparseWords];  // COUNT: accepted (parent, u) pairs
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const u32 lemask = lanemask_lt() | (1u << lane);
   u32* T = s_rhash + wid * a.hstride;
@@ -475,28 +481,51 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
   unsigned long long acc_total = 0, acc_cand = 0;
   u32 mbase = 0, mend = 0;  // this warp's chunk of ballot-mask words (mcap <= 2^28)
   u64 grab = 0, grab_left = 0;
+  // WRITE items are (mostly) a copy of recorded children: uniform cost, so
+  // warps take them in a static stride instead of contending on the counter
+  const u64 gwarp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  u64 sitem = a.ibeg + gwarp;
   for (;;) {
-    if (grab_left == 0) {
-      u64 it_ = 0;
-      if (lane == 0) it_ = atomicAdd(a.ctr, (unsigned long long)a.grab) + a.ibeg;
-      grab = __shfl_sync(0xffffffffu, it_, 0);
-      grab_left = a.grab;
+    u64 item;
+    if (MODE == kWrite) {
+      item = sitem;
+      sitem += nwarps;
+    } else {
+      if (grab_left == 0) {
+        u64 it_ = 0;
+        if (lane == 0) it_ = atomicAdd(a.ctr, (unsigned long long)a.grab) + a.ibeg;
+        grab = __shfl_sync(0xffffffffu, it_, 0);
+        grab_left = a.grab;
+      }
+      item = grab++;
+      --grab_left;
     }
-    const u64 item = grab++;
-    --grab_left;
     if (item >= a.iend) break;
     u64 wpos = 0, mo = ~0ull;
     if (MODE == kWrite) {
       wpos = ldg(a.offs + item);
-      if (ldg(a.offs + item + 1) == wpos) continue;
-      wpos -= a.out_base;
+      const u64 wend = ldg(a.offs + item + 1);
+      if (wend == wpos) continue;
       mo = ldg(a.moff + item);
+      wpos -= a.out_base;
+      if (mo != ~0ull) {
+        // execution from the inspection's recorded children: a coalesced copy
+        const u32 nc = (u32)(wend - (wpos + a.out_base));
+        for (u32 i = lane; i < nc; i += 32) {
+          const uint2 pr = reinterpret_cast<const uint2*>(a.masks + mo)[i];
+          a.out_idx[wpos + i] = pr.x;
+          a.out_vid[wpos + i] = pr.y;
+        }
+        continue;
+      }
     }
-    const bool from_masks = (MODE == kWrite) && mo != ~0ull;
+    constexpr bool from_masks = false;
     const u64 e = a.lo + item * 32 + lane;
     const bool valid = e < a.hi;
     const u32 v0 = valid ? ldg(a.src + e) : 0xffffffffu;
-    const u32 v1 = valid ? ldg(g.col + e) : 0u;
+    const u32* const keysrc = SIB ? a.wv : g.col;
+    const u32 v1 = valid ? ldg(keysrc + e) : 0u;
     // distinct roots of the item (edges are sorted by v0): slot = root rank
     const u32 vprev = __shfl_up_sync(0xffffffffu, v0, 1);
     const bool lead = valid && (lane == 0 || v0 != vprev);
@@ -509,8 +538,26 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
       u64 rb = 0;
       u32 rd = 0;
       if (lead) {
-        rb = ldg(g.off + v0);
-        rd = (u32)(ldg(g.off + v0 + 1) - rb);
+        if (SIB) {  // the parent's whole child group [gb, ge) (may extend past the item)
+          u64 lo_ = 0, hi_ = e;
+          while (lo_ < hi_) {
+            const u64 mid = (lo_ + hi_) >> 1;
+            if (ldg(a.src + mid) < v0) lo_ = mid + 1;
+            else hi_ = mid;
+          }
+          rb = lo_;
+          lo_ = e + 1;
+          hi_ = a.hi;
+          while (lo_ < hi_) {
+            const u64 mid = (lo_ + hi_) >> 1;
+            if (ldg(a.src + mid) <= v0) lo_ = mid + 1;
+            else hi_ = mid;
+          }
+          rd = (u32)(lo_ - rb);
+        } else {
+          rb = ldg(g.off + v0);
+          rd = (u32)(ldg(g.off + v0 + 1) - rb);
+        }
       }
       u32 kin = rd;
 #pragma unroll
@@ -545,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
           const u32 r = min(R + __popc(starts & lemask), nr - 1);
           R += __popc(starts);
           const u32 k = kb + lane;
-          if (k < K) hs_insert(T, sh, hmask, (ldg(g.col + srb[r] + (k - srk[r])) << 5) | r);
+          if (k < K) hs_insert(T, sh, hmask, (ldg(keysrc + srb[r] + (k - srk[r])) << 5) | r);
         }
         __syncwarp();
       }
@@ -585,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
       ssl[rank] = slot;
     }
     __syncwarp();
-    u32 P = 0, c = 0, wi = 0, nzw = 0;
+    u32 P = 0, c = 0, wi = 0;
     // lane -> parent for the step at jb: one OR-reduction over the next
     // parents' start offsets (sex is padded with ~0 past the last parent)
     auto map_step = [&](u32 jb) -> u32 {
@@ -595,29 +642,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
       P += __popc(starts);
       return myp;
     };
-    if (from_masks) {
-      // execution from the inspection's sparse ballots: only steps with
-      // accepted candidates are visited; lane -> parent by binary search
-      const u32 nw = (u32)(mo & 0xff);
-      const u64 mb = mo >> 8;
-      for (u32 i = 0; i < nw; ++i) {
-        const u32 jb = 32 * ldg(a.masks + mb + 2 * i);
-        const u32 m = ldg(a.masks + mb + 2 * i + 1);
-        if (m >> lane & 1u) {
-          const u32 j = jb + lane;
-          u32 lo_ = 0, hi_ = nnz - 1;  // last rank with sex[rank] <= j
-          while (lo_ < hi_) {
-            const u32 mid = (lo_ + hi_ + 1) >> 1;
-            if (sex[mid] <= j) lo_ = mid;
-            else hi_ = mid - 1;
-          }
-          const u64 o = wpos + __popc(m & lanemask_lt());
-          a.out_idx[o] = sei[lo_];
-          a.out_vid[o] = ldg(reinterpret_cast<const u32*>(scp[lo_]) + j);
-        }
-        wpos += __popc(m);
-      }
-    } else {
+    {
       // software pipeline: the next step's candidate load is in flight while
       // the current one is probed
       u32 myp = map_step(0);
@@ -635,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
             ok = hs_has(T, sh, hmask, (u << 5) | ssl[myp]);
           } else {
             const u32 r = ssl[myp];
-            ok = contains_sorted(g.col + srb[r], srd[r], u);
+            ok = contains_sorted(keysrc + srb[r], srd[r], u);
           }
         }
         const u32 mask = __ballot_sync(0xffffffffu, ok);
@@ -647,14 +672,15 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
           }
           wpos += __popc(mask);
         } else {
-          c += __popc(mask);
           if (MODE == kCount && mask) {
-            if (lane == 0 && nzw < kSparseWords) {
-              smw[2 * nzw] = wi;
-              smw[2 * nzw + 1] = mask;
+            // record the accepted children (sequential order) for execution
+            const u32 slot = c + __popc(mask & lanemask_lt());
+            if (ok && slot < kSparseWords) {
+              smw[2 * slot] = sei[myp];
+              smw[2 * slot + 1] = u;
             }
-            ++nzw;
           }
+          c += __popc(mask);
         }
         myp = nmyp;
         u = nu;
@@ -664,6 +690,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
       // keep the non-zero ballots (step, mask) when they fit; the execution
       // pass then touches accepted candidates only (else it recomputes)
       mo = ~0ull;
+      const u32 nzw = c;
       if (nzw && nzw <= kSparseWords && a.masks) {
         if (mbase + 2 * nzw > mend) {  // per-warp chunk: one global atomic per chunk
           unsigned long long t = 0;
@@ -679,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
         if (mbase + 2 * nzw <= mend) {
           __syncwarp();
           for (u32 i = lane; i < 2 * nzw; i += 32) a.masks[mbase + i] = smw[i];
-          mo = ((u64)mbase << 8) | nzw;
+          mo = mbase;
           mbase += 2 * nzw;
         }
       }
@@ -720,6 +747,7 @@ struct Ctx {
   unsigned long long* d_total;
   unsigned long long* d_hist;
   unsigned long long* d_ctr;
+  bool siblings_complete;   // every child of each level parent is in this chunk
   bool generic_mc;   // GPM_GENERIC_MC: per-candidate binary-search path for MC
 };
 
@@ -754,6 +782,8 @@ void run_work(Ctx& c, const VLevels& L, u64 np, u64* W) {
   ++c.tl->launches;
 }
 
+void cf_last_siblings(Ctx& c, const u32* idx, const u32* vid, u64 np, int lev);
+
 template <int APP, int LEV>
 void process(Ctx& c, VLevels L, u64 np);
 
@@ -781,6 +811,12 @@ void process(Ctx& c, VLevels L, u64 np) {
   if constexpr (APP == kAppMC && LEV == 2) {
     if (last && c.k == 4 && !c.generic_mc && c.G->n < (1u << 30)) {  // union-set tags need ids < 2^30
       mc4_last_staged(*c.G, L.idx[0], L.vid[0], L.idx[1], L.vid[1], np, c.d_hist, c.s, *c.tl, st);
+      return;
+    }
+  }
+  if constexpr (APP == kAppCF && LEV >= 2) {
+    if (last && c.g.oriented && c.siblings_complete && c.G->n < (1u << 27) && !std::getenv("GPM_GENERIC_CF")) {
+      cf_last_siblings(c, L.idx[LEV - 1], L.vid[LEV - 1], np, LEV);
       return;
     }
   }
@@ -909,13 +945,14 @@ void process(Ctx& c, VLevels L, u64 np) {
     VLevels nl = L;
     nl.idx[LEV] = oi.get();
     nl.vid[LEV] = ov.get();
+    c.siblings_complete = chunks.size() == 1;  // planner chunks may split a parent's children
     process_dispatch<APP>(c, LEV + 1, nl, Tc);
   }
 }
 
-template <int MODE>
-void launch_edge(Ctx& c, EdgeArgs& a, const char* what, double bytes) {
-  auto kern = edge_chunk_kernel<MODE>;
+template <int MODE, bool SIB = false>
+void launch_edge(Ctx& c, EdgeArgs& a, const std::string& what, double bytes) {
+  auto kern = edge_chunk_kernel<MODE, SIB>;
   // hash capacity: keys of one item <= 32 + 2 x max out-degree in practice
   const u32 md = c.G->max_deg ? c.G->max_deg : kFilterMax;
   u32 hs = 256;
@@ -940,6 +977,33 @@ void launch_edge(Ctx& c, EdgeArgs& a, const char* what, double bytes) {
   GPM_CUDA(cudaGetLastError());
   c.tl->end(ev);
   ++c.tl->launches;
+}
+
+// Last extension of CF (k >= 4) over a complete materialised level: the
+// edge-chunk kernel in sibling mode (one probe into the parent's child group
+// replaces the LEV binary searches of the generic to_add).
+void cf_last_siblings(Ctx& c, const u32* idx, const u32* vid, u64 np, int lev) {
+  DBuf<unsigned long long> cand(1, c.s);
+  GPM_CUDA(cudaMemsetAsync(cand.get(), 0, sizeof(unsigned long long), c.s));
+  EdgeArgs a{};
+  a.g = c.g;
+  a.src = idx;
+  a.wv = vid;
+  a.lo = 0;
+  a.hi = np;
+  a.ibeg = 0;
+  a.iend = (np + 31) / 32;
+  a.total = c.d_total;
+  a.cand = cand.get();
+  size_t rec = c.tl->recs.size();
+  launch_edge<kFused, true>(c, a, "extend_fused_L" + std::to_string(lev), 0.0);
+  unsigned long long W = 0;
+  GPM_CUDA(cudaMemcpyAsync(&W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, c.s));
+  GPM_CUDA(cudaStreamSynchronize(c.s));
+  const double bytes = 8.0 * lev * np + 16.0 * np + 4.0 * (double)W;  // SURVEY §8d (one extended position)
+  c.tl->recs[rec].bytes = bytes;
+  c.st->candidates[lev] += W;
+  c.st->balg += bytes;
 }
 
 // First extension of TC/CF on a DAG through the edge-chunk kernel; deeper
@@ -976,7 +1040,9 @@ void process_l1_cf(Ctx& c, const VLevels& L, const u32* src, u64 lo, u64 hi) {
   DBuf<u64> cnt(NI + 1, c.s), moff(NI + 1, c.s);
   GPM_CUDA(cudaMemsetAsync(cnt.get() + NI, 0, sizeof(u64), c.s));
   // ballot masks: 1 bit per candidate, per-warp chunks
-  const u64 mcap = std::max<u64>(1, std::min<u64>(c.mask_budget / 4, u64(1) << 28));
+  // recorded children: <= kSparseWords pairs per item + one chunk of slack per warp
+  const u64 mwant = 2 * kSparseWords * NI + (u64)c.sms * 64 * kMaskChunk;
+  const u64 mcap = std::max<u64>(1, std::min<u64>({c.mask_budget / 4, u64(1) << 28, mwant}));
   DBuf<u32> masks(mcap, c.s);
   DBuf<unsigned long long> mtop(1, c.s);
   GPM_CUDA(cudaMemsetAsync(mtop.get(), 0, sizeof(unsigned long long), c.s));
@@ -1037,6 +1103,7 @@ void process_l1_cf(Ctx& c, const VLevels& L, const u32* src, u64 lo, u64 hi) {
     VLevels nl = L;
     nl.idx[1] = oi.get();
     nl.vid[1] = ov.get();
+    c.siblings_complete = true;  // item-aligned chunks never split an edge's children
     process_dispatch<kAppCF>(c, 2, nl, Tc);
   }
 }
