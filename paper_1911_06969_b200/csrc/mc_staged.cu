@@ -4,7 +4,7 @@
 // Reference: extend (Alg. 2) with MC's
 // to_add = is_auto_canonical_vertex (Listing 4) and reduce by
 // connectivity code (Listing 6), fused on the last level
-// (PAPER.md:742-744).  DESIGN.md §3a.
+// (PAPER.md:742-744).  DESIGN.md §3b.
 //
 // Level 1 of MC is every edge (v0, v1) with v0 < v1 (embedding_list.hpp:
 // 178-192); the parents of one root v0 are S0 = {v in N(v0) : v > v0}, the
@@ -371,6 +371,7 @@ constexpr int kW4 = kT4 / 32;
 constexpr u32 k4Slots = 1024;  // per-warp union table S0 ∪ S1 (4 KB)
 constexpr u32 k4Keys = 512;    // |S0| + |S1| above this -> binary search in HBM
 constexpr u64 k4Item = 512;    // level-2 entries per warp work item
+constexpr u64 kShortList = 0;  // lists up to this length skip the lower-bound search (64 measured slower on MC4)
 
 struct Mc4Args {
   DevGraph g;
@@ -531,7 +532,9 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
       if (valid) {
         v2 = ldg(a.vid2 + cur + lane);
         const u64 b2 = ldg(g.off + v2), e2 = ldg(g.off + v2 + 1);
-        st = lower_bound_col(g.col, b2, e2, v0 + 1);
+        // short lists are streamed whole (the u > v0 test is applied per
+        // candidate below) instead of paying a dependent binary search
+        st = (e2 - b2 <= kShortList) ? b2 : lower_bound_col(g.col, b2, e2, v0 + 1);
         len = (u32)(e2 - st);
         pmv = U.flags(v2);  // bit 0: v2 ~ v0, bit 1: v2 ~ v1
         aCand += (u64)(ldg(g.off + v0 + 1) - ldg(g.off + v0)) + (ldg(g.off + v1 + 1) - ldg(g.off + v1)) + (e2 - b2);
@@ -554,7 +557,7 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
           const u32 u0 = ldg(g.col + b + j + lane);
           const u32 u1 = ldg(g.col + b + j + 32 + lane);
           const u32 f0 = U.flags(u0), f1 = U.flags(u1);
-          c2 += __popc(__ballot_sync(0xffffffffu, f0 == 0)) + __popc(__ballot_sync(0xffffffffu, f1 == 0));
+          c2 += __popc(__ballot_sync(0xffffffffu, f0 == 0 && u0 > v0)) + __popc(__ballot_sync(0xffffffffu, f1 == 0 && u1 > v0));
           c11 += __popc(__ballot_sync(0xffffffffu, f0 == 3 && u0 > cm)) + __popc(__ballot_sync(0xffffffffu, f1 == 3 && u1 > cm));
           c01 += __popc(__ballot_sync(0xffffffffu, f0 == 1 && u0 > cm)) + __popc(__ballot_sync(0xffffffffu, f1 == 1 && u1 > cm));
           c12 += __popc(__ballot_sync(0xffffffffu, f0 == 2 && u0 > cv2)) + __popc(__ballot_sync(0xffffffffu, f1 == 2 && u1 > cv2));
@@ -563,7 +566,7 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
           const bool ok = j + lane < L;
           const u32 u0 = ok ? ldg(g.col + b + j + lane) : 0u;
           const u32 f0 = ok ? U.flags(u0) : 4u;
-          c2 += __popc(__ballot_sync(0xffffffffu, f0 == 0));
+          c2 += __popc(__ballot_sync(0xffffffffu, f0 == 0 && u0 > v0));
           c11 += __popc(__ballot_sync(0xffffffffu, f0 == 3 && u0 > cm));
           c01 += __popc(__ballot_sync(0xffffffffu, f0 == 1 && u0 > cm));
           c12 += __popc(__ballot_sync(0xffffffffu, f0 == 2 && u0 > cv2));
@@ -611,7 +614,7 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
             const u32 cv2 = s_v2[wid][c];
             const u32 cm = max(v1, cv2);
             const u32 f = U.flags(u);
-            f2 = f == 0;
+            f2 = f == 0 && u > v0;
             f11 = f == 3 && u > cm;
             f01 = f == 1 && u > cm;
             f12 = f == 2 && u > cv2;
