@@ -41,10 +41,10 @@ namespace {
 
 constexpr int kT = 256;
 constexpr int kWarps = kT / 32;
-constexpr u32 kWSlots = 2048;   // per-warp hash slots (8 KB): load <= 1/8 up to kWKeys
-constexpr u32 kWKeys = 256;     // roots with |S0| <= this use the warp kernel
-constexpr u32 kBSlots = 16384;  // per-CTA hash slots (64 KB)
-constexpr u32 kBKeys = 2048;    // S0 tile of the block kernel (load 1/8)
+constexpr u32 kWSlots = 1024;   // per-warp hash slots (4 KB): load <= 1/8 up to kWKeys
+constexpr u32 kWKeys = 256;     // roots with |S0| <= this use the warp kernel (load <= 1/4)
+constexpr u32 kBSlots = 8192;   // per-CTA hash slots (32 KB)
+constexpr u32 kBKeys = 1024;    // S0 tile of the block kernel (load 1/8)
 constexpr u32 kPB = 1024;       // parents per block item (warps grab 32 at a time)
 
 // first index i in [b, e) with col[i] >= key
@@ -130,6 +130,28 @@ __device__ __forceinline__ void stream_parents(const u32* __restrict__ col, cons
     const u32 L = __shfl_sync(0xffffffffu, len, i);
     const u32 w = __shfl_sync(0xffffffffu, v1, i);
     u32 j = 0;
+    for (; j + 256 <= L; j += 256) {  // eight loads in flight per lane
+      u32 u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) u[q] = ldg(col + b + j + 32 * q + lane);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const bool h = hs_has(T, sh, mask, u[q]);
+        cx += __popc(__ballot_sync(0xffffffffu, h));
+        ct += __popc(__ballot_sync(0xffffffffu, h && u[q] > w));
+      }
+    }
+    for (; j + 128 <= L; j += 128) {  // four loads in flight per lane
+      u32 u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) u[q] = ldg(col + b + j + 32 * q + lane);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool h = hs_has(T, sh, mask, u[q]);
+        cx += __popc(__ballot_sync(0xffffffffu, h));
+        ct += __popc(__ballot_sync(0xffffffffu, h && u[q] > w));
+      }
+    }
     for (; j + 64 <= L; j += 64) {
       const u32 u0 = ldg(col + b + j + lane);
       const u32 u1 = ldg(col + b + j + 32 + lane);
@@ -189,7 +211,7 @@ __device__ __forceinline__ void stream_parents(const u32* __restrict__ col, cons
   tri += ct;
 }
 
-__global__ void __launch_bounds__(kT, 3) mc3_warp_kernel(Mc3Args a) {
+__global__ void __launch_bounds__(kT, 4) mc3_warp_kernel(Mc3Args a) {
   extern __shared__ __align__(16) u32 s_wtab[];  // [kWarps][kWSlots]
   __shared__ u64 s_cb[kWarps][32];
   __shared__ u32 s_ex[kWarps][32];
@@ -263,7 +285,7 @@ __global__ void __launch_bounds__(kT, 3) mc3_warp_kernel(Mc3Args a) {
 // Roots with |S0| > kWKeys: item = (root, S0 tile, chunk of <= kPB parents).
 // The CTA stages the tile; warps grab 32 parents at a time from the chunk and
 // stream their candidates inside the tile's id range [idlo, idhi).
-__global__ void __launch_bounds__(kT, 3) mc3_block_kernel(Mc3Args a) {
+__global__ void __launch_bounds__(kT, 4) mc3_block_kernel(Mc3Args a) {
   extern __shared__ __align__(16) u32 s_btab[];
   __shared__ u64 s_cb[kWarps][32];
   __shared__ u32 s_ex[kWarps][32];
@@ -553,6 +575,19 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
         const u32 cm = max(v1, cv2);
         u32 c2 = 0, c11 = 0, c01 = 0, c12 = 0;
         u32 j = 0;
+        for (; j + 128 <= L; j += 128) {  // four loads in flight per lane
+          u32 u[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) u[q] = ldg(g.col + b + j + 32 * q + lane);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const u32 f = U.flags(u[q]);
+            c2 += __popc(__ballot_sync(0xffffffffu, f == 0 && u[q] > v0));
+            c11 += __popc(__ballot_sync(0xffffffffu, f == 3 && u[q] > cm));
+            c01 += __popc(__ballot_sync(0xffffffffu, f == 1 && u[q] > cm));
+            c12 += __popc(__ballot_sync(0xffffffffu, f == 2 && u[q] > cv2));
+          }
+        }
         for (; j + 64 <= L; j += 64) {
           const u32 u0 = ldg(g.col + b + j + lane);
           const u32 u1 = ldg(g.col + b + j + 32 + lane);
