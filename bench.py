@@ -338,7 +338,11 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": res.stats["dominant"],
                      "kernel_ms": dms, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                     "bytes": "SURVEY §8d B_alg of that kernel: 8*l per parent + (16 + 4*deg) per extended position"},
+                     "bytes": "SURVEY §8d B_alg of that kernel: 8*l per parent + (16 + 4*deg) per extended position",
+                     "note": ("B_alg counts 4 B for every candidate of every position; staged source "
+                              "lists are read on chip once per root/group, and L2-resident CSRs are "
+                              "re-read from L2, so B_alg/t can exceed the HBM copy rate. traffic = ncu "
+                              "dram bytes of one captured launch (profiles/traffic_<app>.json)")},
         "step_ms": [round(x, 4) for x in step_ms],
         "gpu_launches": launches,
         "clocks": clock_rec,

@@ -91,6 +91,38 @@ __device__ __forceinline__ bool hs_has(const u32* T, u32 sh, u32 mask, u32 v) {
     h = (h + 1) & mask;
   }
 }
+// Bucketised variant (4 slots = 16 B per bucket): a lookup is one LDS.128 and
+// four compares; the next bucket is visited only when a bucket is full, which
+// at load <= 1/4 almost never happens for any lane of a warp (linear probing
+// sends most warps round a second probe).  Buckets fill left to right, so an
+// empty last slot ends the search.  sh = 32 - log2(capacity / 4).
+__device__ __forceinline__ void hb_insert(u32* T, u32 sh, u32 bmask, u32 v) {
+  u32 b = (v * kHashMul) >> sh;
+  for (;;) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const u32 old = atomicCAS(T + 4 * b + k, kEmpty, v);
+      if (old == kEmpty || old == v) return;
+    }
+    b = (b + 1) & bmask;
+  }
+}
+__device__ __forceinline__ bool hb_has(const u32* T, u32 sh, u32 bmask, u32 v) {
+  u32 b = (v * kHashMul) >> sh;
+  for (;;) {
+    const uint4 x = *reinterpret_cast<const uint4*>(T + 4 * b);
+    if (x.x == v || x.y == v || x.z == v || x.w == v) return true;
+    if (x.w == kEmpty) return false;
+    b = (b + 1) & bmask;
+  }
+}
+// (sh, bmask) of a bucketised table of cap slots (cap a power of two >= 64)
+__device__ __forceinline__ void hb_geom(u32 cap, u32& sh, u32& bmask) {
+  const u32 nb = cap >> 2;
+  bmask = nb - 1;
+  sh = 32 - (31 - __clz(nb));
+}
+
 // Warp-collective: stages col[b, b+len) into T (maxcap >= 2 len slots) with
 // the smallest power-of-two capacity >= 8 len (load <= 1/8, short probe runs)
 // that fits maxcap; returns (sh, mask).

@@ -45,7 +45,7 @@ constexpr u32 kWSlots = 1024;   // per-warp hash slots (4 KB): load <= 1/8 up to
 constexpr u32 kWKeys = 256;     // roots with |S0| <= this use the warp kernel (load <= 1/4)
 constexpr u32 kBSlots = 8192;   // per-CTA hash slots (32 KB)
 constexpr u32 kBKeys = 1024;    // S0 tile of the block kernel (load 1/8)
-constexpr u32 kPB = 1024;       // parents per block item (warps grab 32 at a time)
+constexpr u32 kPB = 4096;       // parents per block item (warps grab 32 at a time)
 
 // first index i in [b, e) with col[i] >= key
 __device__ __forceinline__ u64 lower_bound_col(const u32* __restrict__ col, u64 b, u64 e, u32 key) {
@@ -136,7 +136,7 @@ __device__ __forceinline__ void stream_parents(const u32* __restrict__ col, cons
       for (int q = 0; q < 8; ++q) u[q] = ldg(col + b + j + 32 * q + lane);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const bool h = hs_has(T, sh, mask, u[q]);
+        const bool h = hb_has(T, sh, mask, u[q]);
         cx += __popc(__ballot_sync(0xffffffffu, h));
         ct += __popc(__ballot_sync(0xffffffffu, h && u[q] > w));
       }
@@ -147,7 +147,7 @@ __device__ __forceinline__ void stream_parents(const u32* __restrict__ col, cons
       for (int q = 0; q < 4; ++q) u[q] = ldg(col + b + j + 32 * q + lane);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const bool h = hs_has(T, sh, mask, u[q]);
+        const bool h = hb_has(T, sh, mask, u[q]);
         cx += __popc(__ballot_sync(0xffffffffu, h));
         ct += __popc(__ballot_sync(0xffffffffu, h && u[q] > w));
       }
@@ -155,15 +155,15 @@ __device__ __forceinline__ void stream_parents(const u32* __restrict__ col, cons
     for (; j + 64 <= L; j += 64) {
       const u32 u0 = ldg(col + b + j + lane);
       const u32 u1 = ldg(col + b + j + 32 + lane);
-      const bool h0 = hs_has(T, sh, mask, u0);
-      const bool h1 = hs_has(T, sh, mask, u1);
+      const bool h0 = hb_has(T, sh, mask, u0);
+      const bool h1 = hb_has(T, sh, mask, u1);
       cx += __popc(__ballot_sync(0xffffffffu, h0)) + __popc(__ballot_sync(0xffffffffu, h1));
       ct += __popc(__ballot_sync(0xffffffffu, h0 && u0 > w)) + __popc(__ballot_sync(0xffffffffu, h1 && u1 > w));
     }
     for (; j < L; j += 32) {
       const bool v = j + lane < L;
       const u32 u0 = v ? ldg(col + b + j + lane) : 0u;
-      const bool h0 = v && hs_has(T, sh, mask, u0);
+      const bool h0 = v && hb_has(T, sh, mask, u0);
       cx += __popc(__ballot_sync(0xffffffffu, h0));
       ct += __popc(__ballot_sync(0xffffffffu, h0 && u0 > w));
     }
@@ -199,7 +199,7 @@ __device__ __forceinline__ void stream_parents(const u32* __restrict__ col, cons
       bool hit = false, t = false;
       if (jj < total) {
         const u32 u = ldg(col + scb[myp] + (jj - sex[myp]));
-        hit = hs_has(T, sh, mask, u);
+        hit = hb_has(T, sh, mask, u);
         t = hit && u > sv1[myp];
       }
       cx += __popc(__ballot_sync(0xffffffffu, hit));
@@ -242,11 +242,10 @@ __global__ void __launch_bounds__(kT, 4) mc3_warp_kernel(Mc3Args a) {
       troot = r;
       u32 cap = 64;
       while (cap < 8 * ns && cap < kWSlots) cap <<= 1;
-      mask = cap - 1;
-      sh = 32 - (31 - __clz(cap));
+      hb_geom(cap, sh, mask);  // bucketised table: mask = bucket mask
       for (u32 i = lane * 4; i < cap; i += 128) *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
       __syncwarp();
-      for (u32 i = lane; i < ns; i += 32) hs_insert(T, sh, mask, ldg(g.col + sb + i));
+      for (u32 i = lane; i < ns; i += 32) hb_insert(T, sh, mask, ldg(g.col + sb + i));
       __syncwarp();
     }
     const u64 pa0 = max(s, a.lo);
@@ -319,12 +318,12 @@ __global__ void __launch_bounds__(kT, 4) mc3_block_kernel(Mc3Args a) {
     const u32 k0 = t * kBKeys, k1 = min(ns, k0 + kBKeys);
     u32 cap = 1024;  // table sized to the tile: load <= 1/8, cleared in O(cap)
     while (cap < 8 * (k1 - k0) && cap < kBSlots) cap <<= 1;
-    const u32 mask = cap - 1;
-    const u32 sh = 32 - (31 - __clz(cap));
+    u32 sh, mask;
+    hb_geom(cap, sh, mask);
     for (u32 i = threadIdx.x * 4; i < cap; i += kT * 4)
       *reinterpret_cast<uint4*>(s_btab + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     __syncthreads();
-    for (u32 i = k0 + threadIdx.x; i < k1; i += kT) hs_insert(s_btab, sh, mask, ldg(g.col + sb + i));
+    for (u32 i = k0 + threadIdx.x; i < k1; i += kT) hb_insert(s_btab, sh, mask, ldg(g.col + sb + i));
     __syncthreads();
     const u32 idlo = (t == 0) ? r + 1 : ldg(g.col + sb + k0);
     const bool last_tile = (t + 1 == ntiles);
@@ -414,29 +413,36 @@ struct Mc4Args {
 
 // Union hash set of S0 and S1: slot = (id << 2) | (in S0) | (in S1) << 1
 // (ids < 2^30).  One probe answers both memberships.
-__device__ __forceinline__ u32 us_flags(const u32* T, u32 sh, u32 mask, u32 v) {
-  u32 h = (v * kHashMul) >> sh;
+__device__ __forceinline__ u32 us_flags(const u32* T, u32 sh, u32 bmask, u32 v) {
+  u32 b = (v * kHashMul) >> sh;  // bucketised (4 slots, one LDS.128), see hb_has
   for (;;) {
-    const u32 x = T[h];
-    if (x == kEmpty) return 0;
-    if ((x >> 2) == v) return x & 3u;
-    h = (h + 1) & mask;
+    const uint4 x = *reinterpret_cast<const uint4*>(T + 4 * b);
+    if ((x.x >> 2) == v && x.x != kEmpty) return x.x & 3u;
+    if ((x.y >> 2) == v && x.y != kEmpty) return x.y & 3u;
+    if ((x.z >> 2) == v && x.z != kEmpty) return x.z & 3u;
+    if ((x.w >> 2) == v && x.w != kEmpty) return x.w & 3u;
+    if (x.w == kEmpty) return 0;
+    b = (b + 1) & bmask;
   }
 }
 // insert v with flag f; if v is present OR the flag in; returns true if present
-__device__ __forceinline__ bool us_add(u32* T, u32 sh, u32 mask, u32 v, u32 f) {
-  u32 h = (v * kHashMul) >> sh;
+// (keys inserted concurrently are distinct, so a lost CAS just moves on)
+__device__ __forceinline__ bool us_add(u32* T, u32 sh, u32 bmask, u32 v, u32 f) {
+  u32 b = (v * kHashMul) >> sh;
   for (;;) {
-    u32 x = T[h];
-    if (x == kEmpty) {
-      x = atomicCAS(T + h, kEmpty, (v << 2) | f);
-      if (x == kEmpty) return false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      u32 x = T[4 * b + k];
+      if (x == kEmpty) {
+        x = atomicCAS(T + 4 * b + k, kEmpty, (v << 2) | f);
+        if (x == kEmpty) return false;
+      }
+      if ((x >> 2) == v) {
+        atomicOr(T + 4 * b + k, f);
+        return true;
+      }
     }
-    if ((x >> 2) == v) {
-      atomicOr(T + h, f);
-      return true;
-    }
-    h = (h + 1) & mask;
+    b = (b + 1) & bmask;
   }
 }
 
@@ -522,8 +528,7 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
         if (fits) {
           u32 cap = 64;
           while (cap < 8 * (U.n0 + U.n1) && cap < k4Slots) cap <<= 1;  // load <= 1/8 while it fits
-          U.mask = cap - 1;
-          U.sh = 32 - (31 - __clz(cap));
+          hb_geom(cap, U.sh, U.mask);
           __syncwarp();
           for (u32 i = lane * 4; i < cap; i += 128)
             *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);

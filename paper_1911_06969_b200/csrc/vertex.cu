@@ -580,8 +580,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
       if (use_hash) {
         u32 cap = 64;
         while (cap < 8 * K && cap < a.hstride) cap <<= 1;
-        hmask = cap - 1;
-        sh = 32 - (31 - __clz(cap));
+        hb_geom(cap, sh, hmask);  // bucketised: one LDS.128 per probe
         for (u32 i = lane * 4; i < cap; i += 128)
           *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
         __syncwarp();
@@ -592,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
           const u32 r = min(R + __popc(starts & lemask), nr - 1);
           R += __popc(starts);
           const u32 k = kb + lane;
-          if (k < K) hs_insert(T, sh, hmask, (ldg(keysrc + srb[r] + (k - srk[r])) << 5) | r);
+          if (k < K) hb_insert(T, sh, hmask, (ldg(keysrc + srb[r] + (k - srk[r])) << 5) | r);
         }
         __syncwarp();
       }
@@ -657,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
         bool ok = false;
         if (j < total) {
           if (use_hash) {
-            ok = hs_has(T, sh, hmask, (u << 5) | ssl[myp]);
+            ok = hb_has(T, sh, hmask, (u << 5) | ssl[myp]);
           } else {
             const u32 r = ssl[myp];
             ok = contains_sorted(keysrc + srb[r], srd[r], u);

@@ -16,7 +16,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
 out = os.path.join(ROOT, "profiles", rnd)
 os.makedirs(out, exist_ok=True)
-DOMINANT = {"cf4": "edge_chunk", "tc": "edge_chunk", "mc3": "mc3_block", "mc4": "mc4_last", "fsm": "eextend"}
+# dominant timeline record per bench workload -> the kernels it is made of
+# (3-MC's "extend_fused_L1" is the warp kernel + the tiled block kernel)
+DOMINANT = {"cf4": ["edge_chunk"], "tc": ["edge_chunk"], "mc3": ["mc3_warp", "mc3_block"], "mc4": ["mc4_last"],
+            "fsm": ["eextend"]}
+traffic = {}
 
 
 def raw(rep):
@@ -73,10 +77,13 @@ for rep in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "full_*.ncu-rep")))
         lines.append("  stalls " + ", ".join(f"{k.replace('smsp__pcsamp_warps_issue_stalled_', '')} {100 * float(v) / tot:.1f}%"
                                            for k, v in top))
         app = tag.split("_")[0]
-        if app in DOMINANT and DOMINANT[app] in kname and t:
-            with open(os.path.join(ROOT, "profiles", f"traffic_{app}.json"), "w") as f:
-                json.dump({"kernel": kname, "dram_bytes_per_launch": rd + wr, "duration_ms_ncu": t * 1e3,
-                           "source": f"profiles/{rnd}/ncu_{tag}.txt"}, f)
+        if app in DOMINANT and any(k in kname for k in DOMINANT[app]) and t:
+            e = traffic.setdefault(app, {"kernels": [], "dram_bytes_per_launch": 0.0, "duration_ms_ncu": 0.0,
+                                         "sources": []})
+            e["kernels"].append(kname)
+            e["dram_bytes_per_launch"] += rd + wr
+            e["duration_ms_ncu"] += t * 1e3
+            e["sources"].append(f"profiles/{rnd}/ncu_{tag}.txt")
     src = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_source.py"), rep, tag.split("_", 1)[1], "0", "15"],
                          capture_output=True, text=True).stdout
     lines.append("top source lines (stall share, instruction share):")
@@ -84,6 +91,10 @@ for rep in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "full_*.ncu-rep")))
     with open(os.path.join(out, f"ncu_{tag}.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
     print("wrote", f"ncu_{tag}.txt")
+
+for app, e in traffic.items():
+    with open(os.path.join(ROOT, "profiles", f"traffic_{app}.json"), "w") as f:
+        json.dump(e, f, indent=1)
 
 lc = os.path.join(ROOT, "gpurun_out", "launches_cf4.csv")
 if os.path.exists(lc):
