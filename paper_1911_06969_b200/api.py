@@ -169,14 +169,41 @@ class Graph:
         return idx[:n.value], vid[:n.value]
 
 
-@dataclass
 class MineResult:
-    """AppResult + engine stats."""
-    app: str
-    k: int
-    total: int
-    patterns: List[Tuple[int, str, int]]  # (level, canonical text, support)
-    stats: Dict = field(default_factory=dict)
+    """AppResult + engine stats.  The PatternMap is copied
+    out of the library result lazily, on first access of ``patterns`` (FSM can
+    return ~10^6 patterns; callers timing gpm_mine do not pay for it)."""
+
+    def __init__(self, app: str, k: int, total: int, stats: Dict, handle, npat: int):
+        self.app, self.k, self.total, self.stats = app, k, total, stats
+        self._handle, self._npat, self._patterns = handle, npat, None
+
+    @property
+    def patterns(self) -> List[Tuple[int, str, int]]:  # (level, canonical text, support)
+        if self._patterns is None:
+            L = lib()
+            pats = []
+            buf = C.create_string_buffer(512)
+            for i in range(self._npat):
+                sup, lev = C.c_uint64(), C.c_int()
+                check(L.gpm_result_pattern(self._handle, i, buf, 512, C.byref(sup), C.byref(lev)))
+                pats.append((lev.value, buf.value.decode(), sup.value))
+            if self.app == "fsm":
+                pats.sort(key=lambda x: (x[0], -x[2], x[1]))
+            self._patterns = pats
+            self._release()
+        return self._patterns
+
+    def _release(self):
+        if self._handle is not None:
+            lib().gpm_result_free(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self._release()
+        except Exception:
+            pass
 
     def pattern_map(self) -> Dict[str, int]:
         return {t: s for _, t, s in self.patterns}
@@ -213,12 +240,6 @@ def mine(g: Graph, app: str, k: int = 3, min_support: int = 0, **kw) -> MineResu
         check(L.gpm_result_total(r, C.byref(total)))
         npat = C.c_uint64()
         check(L.gpm_result_num_patterns(r, C.byref(npat)))
-        pats = []
-        buf = C.create_string_buffer(512)
-        for i in range(npat.value):
-            sup, lev = C.c_uint64(), C.c_int()
-            check(L.gpm_result_pattern(r, i, buf, 512, C.byref(sup), C.byref(lev)))
-            pats.append((lev.value, buf.value.decode(), sup.value))
         st = _L.Stats()
         check(L.gpm_result_stats(r, C.byref(st)))
         nl = st.n_levels
@@ -227,11 +248,10 @@ def mine(g: Graph, app: str, k: int = 3, min_support: int = 0, **kw) -> MineResu
                      ms_total=st.ms_total, ms_extend=st.ms_extend, ms_dominant=st.ms_dominant,
                      b_dominant=st.b_dominant, launches=st.launches, chunks=st.chunks,
                      dominant=st.dominant.decode())
-    finally:
+    except Exception:
         L.gpm_result_free(r)
-    if app == "fsm":
-        pats.sort(key=lambda x: (x[0], -x[2], x[1]))
-    return MineResult(app, k, total.value, pats, stats)
+        raise
+    return MineResult(app, k, total.value, stats, r, npat.value)
 
 
 def triangle_count(g: Graph, **kw) -> int:

@@ -128,13 +128,14 @@ __global__ void orient_count_kernel(const u64* __restrict__ off, const u32* __re
 }
 
 __global__ void orient_write_kernel(const u64* __restrict__ off, const u32* __restrict__ col,
-                                    const u8* __restrict__ keep, u32 n, const u64* __restrict__ doff,
-                                    u32* __restrict__ dcol) {
+                                    const u8* __restrict__ keep, u32 vb, u32 ve, u64 m,
+                                    const u64* __restrict__ doff, u32* __restrict__ dcol) {
   const int lane = threadIdx.x & 31;
   const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
   const u64 nwarps = (gridDim.x * (u64)blockDim.x) >> 5;
-  for (u64 u = warp; u < n; u += nwarps) {
+  for (u64 u = vb + warp; u < ve; u += nwarps) {
     const u64 b = off[u], e = off[u + 1];
+    if (e < b || e > m) continue;  // invalid offsets: flagged by the count pass
     u64 w = doff[u];
     for (u64 i0 = b; i0 < e; i0 += 32) {
       const u64 i = i0 + lane;
@@ -144,6 +145,23 @@ __global__ void orient_write_kernel(const u64* __restrict__ off, const u32* __re
       w += __popc(mask);
     }
   }
+}
+
+// chunk [vb, ve) of a running exclusive scan: doff[v] += doff[vb-1] + cnt[vb-1]
+__global__ void add_base_kernel(u64* __restrict__ doff, const u64* __restrict__ cnt, u32 vb, u32 ve) {
+  const u64 base = vb ? doff[vb - 1] + cnt[vb - 1] : 0;
+  for (u64 v = vb + blockIdx.x * (u64)blockDim.x + threadIdx.x; v < ve; v += (u64)gridDim.x * blockDim.x)
+    doff[v] += base;
+}
+// doff[n] = total; md = max out-degree
+__global__ void finish_offsets_kernel(u64* __restrict__ doff, const u64* __restrict__ cnt, u32 n,
+                                      u32* __restrict__ md) {
+  u32 best = 0;
+  for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < n; v += (u64)gridDim.x * blockDim.x)
+    best = max(best, (u32)cnt[v]);
+  best = __reduce_max_sync(0xffffffffu, best);
+  if ((threadIdx.x & 31) == 0 && best) atomicMax(md, best);
+  if (blockIdx.x == 0 && threadIdx.x == 0) doff[n] = n ? doff[n - 1] + cnt[n - 1] : 0;
 }
 
 // level 1 of an undirected graph: per vertex, entries v > u (u<v rule).
@@ -397,8 +415,8 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
   out.m = m;
   GPM_CUDA(cudaMallocAsync((void**)&out.d_col, sizeof(u32) * std::max<u64>(1, m), s));
   if (g.n && m) {
-    orient_write_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, keep.get(), g.n, out.d_off,
-                                                                    out.d_col);
+    orient_write_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, keep.get(), 0, g.n, g.m,
+                                                                    out.d_off, out.d_col);
     GPM_CUDA(cudaGetLastError());
   }
   if (g.labeled) {
@@ -413,6 +431,10 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
 // counts the orientation of every chunk that has landed (graph.hpp:29-55 +
 // :121-132).  The undirected copy is dropped afterwards.
 void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels, u32 n, u64 m, gpm_graph& out) {
+  // Per column chunk (vertex range) as soon as it lands: validate + count the
+  // kept out-edges, scan the chunk onto the running offsets (no host round
+  // trip: the base is read on the device) and write its DAG lists, so the
+  // whole orientation overlaps the host->device copy of the later chunks.
   cudaStream_t s = out.stream;
   cudaStream_t cs;
   GPM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -423,10 +445,14 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
   DBuf<u64> uoff(n + 1, s);
   DBuf<u32> ucol(std::max<u64>(1, m), s);
   DBuf<u8> keep(std::max<u64>(1, m), s);
+  DBuf<u64> cnt(std::max<u32>(1, n), s);
   DBuf<int> bad(1, s);
+  DBuf<u32> md(1, s);
   GPM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+  GPM_CUDA(cudaMemsetAsync(md.get(), 0, sizeof(u32), s));
   GPM_CUDA(cudaMallocAsync((void**)&out.d_off, sizeof(u64) * (n + 1), s));
-  GPM_CUDA(cudaMemsetAsync(out.d_off + n, 0, sizeof(u64), s));
+  // a valid undirected CSR keeps exactly m/2 entries; m bounds any input
+  GPM_CUDA(cudaMallocAsync((void**)&out.d_col, sizeof(u32) * std::max<u64>(1, m), s));
   cudaEvent_t ready;
   GPM_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   GPM_CUDA(cudaEventRecord(ready, s));  // allocations visible to the copy stream
@@ -434,6 +460,7 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
   GPM_CUDA(cudaMemcpyAsync(uoff.get(), h_off, sizeof(u64) * (n + 1), cudaMemcpyHostToDevice, cs));
   const int K = m > (u64(1) << 22) ? 8 : 1;
   std::vector<cudaEvent_t> evs;
+  std::vector<std::pair<u32, u32>> ranges;
   u32 vb = 0;
   for (int k = 0; k < K && vb < n; ++k) {
     // vertex range whose edges end near (k+1)/K of m
@@ -447,20 +474,37 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
     GPM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     GPM_CUDA(cudaEventRecord(ev, cs));
     evs.push_back(ev);
-    GPM_CUDA(cudaStreamWaitEvent(s, ev, 0));
-    orient_count_kernel<<<grid_for((u64)(vend - vb) * 32, 256), 256, 0, s>>>(uoff.get(), ucol.get(), n, m, vb, vend, 1,
-                                                                            out.d_off, keep.get(), bad.get());
-    GPM_CUDA(cudaGetLastError());
+    ranges.emplace_back(vb, vend);
     vb = vend;
   }
+  size_t tmp = 0;
+  u32 maxr = 1;
+  for (auto [a, b] : ranges) maxr = std::max(maxr, b - a);
+  GPM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), out.d_off, maxr, s));
+  DBuf<u8> ttmp(std::max<size_t>(1, tmp), s);
+  for (size_t k = 0; k < ranges.size(); ++k) {
+    const auto [rb, re] = ranges[k];
+    GPM_CUDA(cudaStreamWaitEvent(s, evs[k], 0));
+    orient_count_kernel<<<grid_for((u64)(re - rb) * 32, 256), 256, 0, s>>>(uoff.get(), ucol.get(), n, m, rb, re, 1,
+                                                                          cnt.get(), keep.get(), bad.get());
+    GPM_CUDA(cudaGetLastError());
+    GPM_CUDA(cub::DeviceScan::ExclusiveSum(ttmp.get(), tmp, cnt.get() + rb, out.d_off + rb, re - rb, s));
+    add_base_kernel<<<grid_for(re - rb, 256), 256, 0, s>>>(out.d_off, cnt.get(), rb, re);
+    orient_write_kernel<<<grid_for((u64)(re - rb) * 32, 256), 256, 0, s>>>(uoff.get(), ucol.get(), keep.get(), rb, re, m,
+                                                                          out.d_off, out.d_col);
+    GPM_CUDA(cudaGetLastError());
+  }
+  finish_offsets_kernel<<<std::min<unsigned>(grid_for(std::max<u32>(1, n), 256), 1184u), 256, 0, s>>>(out.d_off,
+                                                                                                 cnt.get(), n, md.get());
+  GPM_CUDA(cudaGetLastError());
   if (labels) {
     GPM_CUDA(cudaMallocAsync((void**)&out.d_lab, sizeof(u32) * std::max<u32>(1, n), s));
   }
-  exclusive_scan_u64(out.d_off, n + 1, s);
   u64 dm = 0;
   int hb = 0;
   GPM_CUDA(cudaMemcpyAsync(&dm, out.d_off + n, sizeof(u64), cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaMemcpyAsync(&out.max_deg, md.get(), sizeof(u32), cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaStreamSynchronize(s));
   for (auto e : evs) cudaEventDestroy(e);
   cudaEventDestroy(ready);
@@ -469,13 +513,6 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
   out.n = n;
   out.m = dm;
   out.oriented = true;
-  GPM_CUDA(cudaMallocAsync((void**)&out.d_col, sizeof(u32) * std::max<u64>(1, dm), s));
-  if (n && dm) {
-    orient_write_kernel<<<grid_for((u64)n * 32, 256), 256, 0, s>>>(uoff.get(), ucol.get(), keep.get(), n, out.d_off,
-                                                                  out.d_col);
-    GPM_CUDA(cudaGetLastError());
-  }
-  set_max_degree(out, s);
 }
 
 }  // namespace gpm
