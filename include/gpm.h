@@ -131,7 +131,9 @@ int gpm_result_total(const gpm_result* r, uint64_t* total);
 
 /* PatternMap: n patterns; text in the stable form
  * "k=<n>;L=..;E=(i,j)..".  FSM patterns carry their level
- * (edges) and MNI support; MC patterns carry counts (level = k). */
+ * (edges) and MNI support, ordered by (level, support desc, canonical code),
+ * and their text is formatted on first access (do not read one result from
+ * several threads at once); MC patterns carry counts (level = k). */
 int gpm_result_num_patterns(const gpm_result* r, uint64_t* n);
 int gpm_result_pattern(const gpm_result* r, uint64_t i, char* text, size_t cap, uint64_t* support, int* level);
 

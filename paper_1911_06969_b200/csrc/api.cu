@@ -248,7 +248,8 @@ int gpm_result_pattern(const gpm_result* r, uint64_t i, char* text, size_t cap, 
     set_last_error("pattern index out of range");
     return GPM_EINVAL;
   }
-  const auto& p = r->patterns[i];
+  auto& p = const_cast<gpm_result*>(r)->patterns[i];
+  if (p.text.empty() && p.key) p.text = canon_text(p.key, 0, r->label_bits, &r->label_values);
   if (text && cap) {
     size_t c = std::min(cap - 1, p.text.size());
     std::memcpy(text, p.text.data(), c);

@@ -31,11 +31,14 @@ struct gpm_result {
   int k = 0;
   gpm::u64 total = 0;
   struct Pattern {
-    std::string text;
+    std::string text;   // empty while only the canonical key is known (FSM: formatted on access)
     gpm::u64 support;
     int level;
+    gpm::u64 key = 0;   // packed canonical code (pattern.cuh)
   };
   std::vector<Pattern> patterns;
+  int label_bits = 0;                      // for formatting FSM keys lazily
+  std::vector<gpm::u32> label_values;      // dense label rank -> original label
   gpm_stats stats{};
 };
 

@@ -25,7 +25,6 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
-#include <parallel/algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -489,38 +488,30 @@ __global__ void l1_kernel(FsmArgs a, const u32* __restrict__ idx, const u32* __r
 }
 
 // canonicalize every occupied hash slot once (reduce step 2)
-__global__ void canon_slots_kernel(const unsigned long long* __restrict__ ent, u64 cap, int LB,
-                                   u64* __restrict__ canon, u32* __restrict__ perm, u64* __restrict__ counts,
+// occupied hash slots -> a dense list (any order; everything after is per
+// distinct quick code, so the level's arrays are U-sized instead of cap-sized)
+__global__ void occ_kernel(const unsigned long long* __restrict__ ent, u64 cap, unsigned long long* __restrict__ top,
+                           u32* __restrict__ occ) {
+  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < cap; s += (u64)gridDim.x * blockDim.x)
+    if (ent[2 * s]) occ[atomicAdd(top, 1ull)] = (u32)s;
+}
+
+__global__ void canon_slots_kernel(const unsigned long long* __restrict__ ent, const u32* __restrict__ occ, u64 U,
+                                   int LB, u64* __restrict__ canon, u32* __restrict__ perm, u64* __restrict__ counts,
                                    u32* __restrict__ ids) {
-  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < cap; s += (u64)gridDim.x * blockDim.x) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < U; i += (u64)gridDim.x * blockDim.x) {
+    const u64 s = occ[i];
     const u64 key = ent[2 * s];
-    counts[s] = ent[2 * s + 1] & kCountMask;
-    ids[s] = (u32)(ent[2 * s + 1] >> 40);
-    if (!key) {
-      canon[s] = ~0ull;
-      continue;
-    }
+    counts[i] = ent[2 * s + 1] & kCountMask;
+    ids[i] = (u32)(ent[2 * s + 1] >> 40);
     int nv;
     u32 lab[8], mask;
     pat::decode(key, LB, &nv, lab, &mask);
     u8 p[8];
-    canon[s] = pat::canonicalize(nv, lab, mask, LB, p);
+    canon[i] = pat::canonicalize(nv, lab, mask, LB, p);
     u32 pk = 0;
-    for (int i = 0; i < nv; ++i) pk |= (u32)p[i] << (3 * i);
-    perm[s] = pk;
-  }
-}
-
-// occupied slots -> (canonical key, count) in any order (sorted afterwards)
-__global__ void compact_slots_kernel(const u64* __restrict__ canon, const u64* __restrict__ counts, u64 cap,
-                                     unsigned long long* __restrict__ top, u64* __restrict__ ok,
-                                     u64* __restrict__ oc) {
-  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < cap; s += (u64)gridDim.x * blockDim.x) {
-    const u64 c = canon[s];
-    if (c == ~0ull) continue;
-    const u64 i = atomicAdd(top, 1ull);
-    ok[i] = c;
-    oc[i] = counts[s];
+    for (int j = 0; j < nv; ++j) pk |= (u32)p[j] << (3 * j);
+    perm[i] = pk;
   }
 }
 
@@ -557,18 +548,18 @@ __global__ void merge_qbm_kernel(const u32* __restrict__ qbm, const u64* __restr
   }
 }
 
-__global__ void slot_pid_kernel(const u64* __restrict__ canon, u64 cap, const u64* __restrict__ gkeys, u64 P,
-                                const u32* __restrict__ perm, unsigned long long* __restrict__ ent) {
-  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < cap; s += (u64)gridDim.x * blockDim.x) {
+__global__ void slot_pid_kernel(const u64* __restrict__ canon, const u32* __restrict__ occ, u64 U,
+                                const u64* __restrict__ gkeys, u64 P, const u32* __restrict__ perm,
+                                unsigned long long* __restrict__ ent) {
+  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < U; s += (u64)gridDim.x * blockDim.x) {
     const u64 c = canon[s];
-    if (c == ~0ull) continue;
     u64 lo = 0, hi = P;
     while (lo < hi) {
       u64 mid = (lo + hi) >> 1;
       if (gkeys[mid] < c) lo = mid + 1;
       else hi = mid;
     }
-    ent[2 * s + 1] = ((unsigned long long)lo << 32) | perm[s];
+    ent[2 * (u64)occ[s] + 1] = ((unsigned long long)lo << 32) | perm[s];
   }
 }
 
@@ -703,7 +694,8 @@ struct Fsm {
     DBuf<unsigned long long> ent, used;
     DBuf<int> overflow;
     DBuf<u64> canon;
-    DBuf<u32> perm, bslot, bs_to_pid, ids;
+    DBuf<u32> perm, bslot, bs_to_pid, ids, occ;  // perm / ids / canon / occ: per occupied slot
+    u64 U = 0;
     DBuf<u8> frequent;
     std::vector<u64> gkeys_h, gcount_h, mni_h;
     DBuf<u64> gkeys;
@@ -728,25 +720,26 @@ struct Fsm {
   // After pass A: canonicalize slots, global pattern table (+exchange), pids,
   // count pre-filter, bitmap slots.
   void canon_and_group(Level& R) {
-    R.canon.alloc(R.cap, s);
-    R.perm.alloc(R.cap, s);
-    DBuf<unsigned long long> cc(R.cap, s);
-    R.ids.alloc(R.cap, s);
-    canon_slots_kernel<<<grid1(R.cap), 256, 0, s>>>(R.ent.get(), R.cap, LB, R.canon.get(), R.perm.get(),
-                                                    reinterpret_cast<u64*>(cc.get()), R.ids.get());
-    GPM_CUDA(cudaGetLastError());
-    ++tl.launches;
-    // compact (canon, count) of the U occupied slots, sort by canon, reduce by
-    // key on the device: only the distinct canonical patterns come back
+    // list the U occupied slots, canonicalize each distinct quick code once,
+    // sort by canonical code and reduce by key on the device: only the
+    // distinct canonical patterns come back to the host
     const u64 U = d2h(R.used.get());
-    DBuf<u64> ck(std::max<u64>(1, U), s), ck2(std::max<u64>(1, U), s);
-    DBuf<unsigned long long> cc3(std::max<u64>(1, U), s), cc4(std::max<u64>(1, U), s);
-    DBuf<unsigned long long> top(1, s);
+    R.U = U;
+    const u64 U1 = std::max<u64>(1, U);
+    R.occ.alloc(U1, s);
+    R.canon.alloc(U1, s);
+    R.perm.alloc(U1, s);
+    R.ids.alloc(U1, s);
+    DBuf<u64> ck2(U1, s);
+    DBuf<unsigned long long> cc3(U1, s), cc4(U1, s), top(1, s);
     GPM_CUDA(cudaMemsetAsync(top.get(), 0, sizeof(unsigned long long), s));
-    compact_slots_kernel<<<grid1(R.cap), 256, 0, s>>>(R.canon.get(), reinterpret_cast<const u64*>(cc.get()), R.cap,
-                                                      top.get(), ck.get(), reinterpret_cast<u64*>(cc3.get()));
+    occ_kernel<<<grid1(R.cap), 256, 0, s>>>(R.ent.get(), R.cap, top.get(), R.occ.get());
+    canon_slots_kernel<<<grid1(U1), 256, 0, s>>>(R.ent.get(), R.occ.get(), U, LB, R.canon.get(), R.perm.get(),
+                                                 reinterpret_cast<u64*>(cc3.get()), R.ids.get());
     GPM_CUDA(cudaGetLastError());
-    ++tl.launches;
+    tl.launches += 2;
+    DBuf<u64> ck(U1, s);
+    if (U) GPM_CUDA(cudaMemcpyAsync(ck.get(), R.canon.get(), sizeof(u64) * U, cudaMemcpyDeviceToDevice, s));
     std::vector<u64> keys, cnts;
     if (U) {
       size_t tmp = 0;
@@ -816,7 +809,8 @@ struct Fsm {
     R.gkeys.alloc(std::max<u64>(1, R.P), s);
     if (R.P)
       GPM_CUDA(cudaMemcpyAsync(R.gkeys.get(), R.gkeys_h.data(), sizeof(u64) * R.P, cudaMemcpyHostToDevice, s));
-    slot_pid_kernel<<<grid1(R.cap), 256, 0, s>>>(R.canon.get(), R.cap, R.gkeys.get(), R.P, R.perm.get(), R.ent.get());
+    slot_pid_kernel<<<grid1(std::max<u64>(1, R.U)), 256, 0, s>>>(R.canon.get(), R.occ.get(), R.U, R.gkeys.get(), R.P,
+                                                                 R.perm.get(), R.ent.get());
     GPM_CUDA(cudaGetLastError());
     ++tl.launches;
     // count pre-filter -> bitmap slots (MNI <= count)
@@ -877,11 +871,8 @@ struct Fsm {
     std::vector<u64> sel;
     for (u64 p = 0; p < R.P; ++p)
       if (R.gcount_h[p] >= sigma && R.mni_h[p] >= sigma) sel.push_back(p);
-    const size_t base = res.patterns.size();
-    res.patterns.resize(base + sel.size());
-#pragma omp parallel for schedule(static)
-    for (size_t i = 0; i < sel.size(); ++i)
-      res.patterns[base + i] = {canon_text(R.gkeys_h[sel[i]], 0, LB, &G.label_values), R.mni_h[sel[i]], level};
+    // text is formatted on access (gpm_result_pattern): ~10^6 patterns per call
+    for (u64 p : sel) res.patterns.push_back({std::string(), R.mni_h[p], level, R.gkeys_h[p]});
   }
 
   FsmArgs base_args(Level& R) {
@@ -1044,7 +1035,7 @@ struct Fsm {
     DBuf<int> qover(1, s);
     u64 qcap = 0;
     if (last && nb && !std::getenv("GPM_FSM_TWO_PASS")) {
-      qcap = std::min<u64>(cap / 2, budget / 4 / std::max<u64>(1, per_id));
+      qcap = std::min<u64>(cap / 2, budget / 2 / std::max<u64>(1, per_id));
       if (qcap >= 1024) qbm.alloc(qcap * kposL * wordsL, s);
       else qcap = 0;
     }
@@ -1070,6 +1061,7 @@ struct Fsm {
     }
     const bool fused = qcap && d2h(qover.get()) == 0;
     if (!fused) qbm.release();  // more quick codes than bitmaps: separate domain pass
+    trace(fused ? "pass A fused (qcap, ids)" : "pass A unfused (qcap, ids)", (double)qcap, (double)d2h(R.used.get()));
     u64 acc = d2h(accepted.get());
     prev_unique = d2h(R.used.get());
     trace("pass A (qc)", (double)acc, (double)R.cap);
@@ -1083,7 +1075,7 @@ struct Fsm {
     domains_and_mni(R, LEV + 2, [&](u32* bm, u64 words, int kpos, u32 lo, u32 hi) {
       if (!nb) return;
       if (fused) {
-        merge_qbm_kernel<<<grid1(R.cap * 32), 256, 0, s>>>(qbm.get(), R.canon.get(), R.ids.get(), R.perm.get(), R.cap,
+        merge_qbm_kernel<<<grid1(std::max<u64>(1, R.U) * 32), 256, 0, s>>>(qbm.get(), R.canon.get(), R.ids.get(), R.perm.get(), R.U,
                                                            R.gkeys.get(), R.P, R.bslot.get(), lo, hi, bm, words, kpos);
         GPM_CUDA(cudaGetLastError());
         ++tl.launches;
@@ -1215,11 +1207,14 @@ struct Fsm {
       for (size_t i = 0; i < st.candidates.size(); ++i) st.candidates[i] = v[L2 + i];
       st.balg = (double)v.back();
     }
-    __gnu_parallel::sort(res.patterns.begin(), res.patterns.end(), [](const gpm_result::Pattern& x, const gpm_result::Pattern& y) {
+    // (level, support desc, canonical key): integer compares only
+    std::sort(res.patterns.begin(), res.patterns.end(), [](const gpm_result::Pattern& x, const gpm_result::Pattern& y) {
       if (x.level != y.level) return x.level < y.level;
       if (x.support != y.support) return x.support > y.support;
-      return x.text < y.text;
+      return x.key < y.key;
     });
+    res.label_bits = LB;
+    res.label_values = G.label_values;
   }
 };
 
