@@ -198,7 +198,15 @@ __device__ __forceinline__ u32 hash_add(const Hash& H, u64 key, unsigned long lo
   if (*(volatile int*)H.overflow) return 0;
   u64 h = hash64(key) & H.mask;
   for (int probe = 0; probe < kMaxProbe; ++probe) {
-    unsigned long long cur = H.ent[2 * h];
+    // one 16-byte load returns key and val together: once a key's id is
+    // published it never changes, so a hit needs no atomic round trip — the
+    // count is added with a fire-and-forget reduction
+    const ulonglong2 e = *reinterpret_cast<const ulonglong2*>(H.ent + 2 * h);
+    unsigned long long cur = e.x;
+    if (cur == key && (e.y >> 40) != 0) {
+      atomicAdd(H.ent + 2 * h + 1, c);
+      return (u32)(e.y >> 40);
+    }
     if (cur == 0) {
       unsigned long long prev = atomicCAS(H.ent + 2 * h, 0ull, (unsigned long long)key);
       if (prev == 0ull) {
@@ -263,23 +271,44 @@ struct FsmArgs {
   unsigned long long* accepted;
 };
 
-__device__ __forceinline__ void domain_or(const FsmArgs& a, u64 info, const u32* cv, int cnv) {
+// OR the child's vertices into its pattern's domain bitmaps.  All position
+// words are loaded before any atomic: the loads are independent, so issuing
+// them together overlaps their (mostly DRAM) latencies instead of paying one
+// round trip per position (the atomics would otherwise fence the next load).
+// first = first position this lane must write (lanes whose parent positions are
+// written by a peer lane start at the parent's vertex count).
+template <int NV>
+__device__ __forceinline__ void bitmap_or(u32* base, u64 words, const u32* __restrict__ lrank, u32 perm, bool permute,
+                                          const u32* cv, int cnv, int first) {
+  u32* wp[NV];
+  u32 bit[NV], old[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    wp[i] = nullptr;
+    if (i >= first && i < cnv) {
+      const u32 cp = permute ? (perm >> (3 * i)) & 7u : (u32)i;
+      const u32 lr = ldg(lrank + cv[i]);  // all vertices at one position share its label
+      wp[i] = base + (u64)cp * words + (lr >> 5);
+      bit[i] = 1u << (lr & 31);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) old[i] = wp[i] ? *wp[i] : 0u;
+  // domains saturate quickly: test before the read-modify-write so most
+  // embeddings cost a load instead of an L2 atomic (a stale read only causes a
+  // redundant, still-correct atomicOr)
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    if (wp[i] && !(old[i] & bit[i])) atomicOr(wp[i], bit[i]);
+}
+
+template <int NV>
+__device__ __forceinline__ void domain_or(const FsmArgs& a, u64 info, const u32* cv, int cnv, int first) {
   const u32 pid = (u32)(info >> 32);
   const u32 bs = a.bslot[pid];
   if (bs < a.round_lo || bs >= a.round_hi) return;
-  const u32 perm = (u32)info;
   u32* base = a.bitmaps + (u64)(bs - a.round_lo) * a.kpos * a.words;
-  for (int i = 0; i < cnv; ++i) {
-    const u32 cp = (perm >> (3 * i)) & 7u;
-    const u32 v = cv[i];
-    const u32 lr = ldg(a.lrank + v);  // all vertices at one position share its label
-    u32* wp = base + (u64)cp * a.words + (lr >> 5);
-    const u32 bit = 1u << (lr & 31);
-    // domains saturate quickly: test before the read-modify-write so most
-    // embeddings cost a cached load instead of an L2 atomic (a stale read only
-    // causes a redundant, still-correct atomicOr)
-    if (!(*wp & bit)) atomicOr(wp, bit);
-  }
+  bitmap_or<NV>(base, a.words, a.lrank, (u32)info, true, cv, cnv, first);
 }
 
 // Work per parent: sum of deg over all positions (to_extend default true).
@@ -403,6 +432,10 @@ __global__ void __launch_bounds__(kThreads) eextend_kernel(FsmArgs a) {
           const unsigned long long key = ok ? code : ~0ull;
           const u32 peers = __match_any_sync(0xffffffffu, key);
           const int leader = __ffs(peers) - 1;
+          // lanes with the same quick code AND the same parent set identical
+          // bits for the parent's positions: only the lowest of them writes them
+          const u32 sib = peers & __match_any_sync(0xffffffffu, myp);
+          const int first = (lane == __ffs(sib) - 1) ? 0 : cur.E.nv;
           u32 id = 0;
           if (ok && lane == leader) id = hash_add(a.H, code, __popc(peers));
           if (a.qbm) {
@@ -412,12 +445,7 @@ __global__ void __launch_bounds__(kThreads) eextend_kernel(FsmArgs a) {
             if (ok && id) {
               if (id - 1 < a.qcap) {
                 u32* base = a.qbm + (u64)(id - 1) * a.kpos * a.words;
-                for (int i = 0; i < cnv; ++i) {
-                  const u32 lr = ldg(a.lrank + cv[i]);
-                  u32* wp = base + (u64)i * a.words + (lr >> 5);
-                  const u32 bit = 1u << (lr & 31);
-                  if (!(*wp & bit)) atomicOr(wp, bit);
-                }
+                bitmap_or<LEV + 2>(base, a.words, a.lrank, 0u, false, cv, cnv, first);
               } else {
                 *a.qover = 1;
               }
@@ -425,9 +453,10 @@ __global__ void __launch_bounds__(kThreads) eextend_kernel(FsmArgs a) {
           }
         }
       } else if (MODE == kDomain) {
-        if (ok) {
-          domain_or(a, hash_info(a.H, hash_find(a.H, code)), cv, cnv);
-        }
+        const u32 peers = __match_any_sync(0xffffffffu, ok ? code : ~0ull);
+        const u32 sib = peers & __match_any_sync(0xffffffffu, myp);
+        const int first = (lane == __ffs(sib) - 1) ? 0 : cur.E.nv;
+        if (ok) domain_or<LEV + 2>(a, hash_info(a.H, hash_find(a.H, code)), cv, cnv, first);
       } else {
         bool keep = false;
         if (ok) {
@@ -479,7 +508,7 @@ __global__ void l1_kernel(FsmArgs a, const u32* __restrict__ idx, const u32* __r
     } else if (MODE == kDomain) {
       if (act) {
         u32 cv[2] = {u, v};
-        domain_or(a, hash_info(a.H, hash_find(a.H, code)), cv, 2);
+        domain_or<2>(a, hash_info(a.H, hash_find(a.H, code)), cv, 2, 0);
       }
     } else if (act) {
       keep[i] = a.frequent[hash_info(a.H, hash_find(a.H, code)) >> 32];
