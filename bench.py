@@ -26,7 +26,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -70,33 +69,49 @@ class ClockSampler:
         self.proc = None
         self.lines = []
 
+    # No reader thread: a Python thread waking for every sample competes for
+    # the GIL with the host side of the timed steps (ctypes calls reacquire it
+    # on return).  Samples queue in the pipe (~100 B each, 64 KiB buffer ≈ a
+    # minute of samples) and are drained here, outside the timed steps.
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
         except Exception:
             self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
+    def drain(self, block_s=0.0):
+        """Reads the samples already queued (waits up to block_s for one)."""
+        if not self.proc:
+            return
+        import select
+        t_end = time.time() + block_s
+        while True:
+            r, _, _ = select.select([self.proc.stdout], [], [], max(0.0, t_end - time.time()))
+            if not r:
+                return
+            line = self.proc.stdout.readline()
+            if not line:
+                return
             self.lines.append(line.strip())
+            t_end = time.time()  # got one: only take what is already queued
 
     def wait_samples(self, n, timeout=5.0):
         """Blocks until n samples have arrived (the sampler's first lines lag
         its start; short timed regions would otherwise see none)."""
         t = time.time()
         while self.proc and len(self.lines) < n and time.time() - t < timeout:
-            time.sleep(0.02)
+            self.drain(0.2)
 
     def stop(self, first=0):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.drain()
         self.proc.terminate()
         try:
-            self.proc.wait(timeout=5)
+            rest, _ = self.proc.communicate(timeout=5)
+            self.lines += [ln.strip() for ln in (rest or "").splitlines() if ln.strip()]
         except Exception:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
@@ -257,6 +272,7 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     clocks.wait_samples(1)
+    clocks.drain()
     n_before = len(clocks.lines)
     step_ms = []
     dom_ms, dom_b, launches = [], [], 0
@@ -278,9 +294,11 @@ def main():
     # a short timed region may fall between two 100 ms samples: keep the GPU
     # busy with further (untimed) steps until one sample lands after it began
     t_extra = time.time()
+    clocks.drain()
     while len(clocks.lines) <= n_before + 1 and time.time() - t_extra < 3.0:
         mine_step(g_in, **kw)
         torch.cuda.synchronize()
+        clocks.drain()
     clock_rec = clocks.stop(first=n_before)
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
     if world > 1:

@@ -52,6 +52,14 @@ typedef struct gpm_result gpm_result;
 typedef int (*gpm_exchange_fn)(void* ctx, void* dev_buf, uint64_t count, int elem_bytes, int op, void* stream);
 
 /* EngineConfig + CliConfig knobs. */
+/* Listing sink ("an optional listing mode dumps final-level
+ * embeddings"; PAPER.md:907-910 clique-listing).  Called on the host, in
+ * order, with batches of final-level embeddings: `verts` holds n rows of k
+ * vertex ids (insertion order, i.e. DAG order v0 -> v1 -> ... for TC/CF) in a
+ * pinned staging buffer that is reused once the call returns.  A non-zero
+ * return aborts the job with GPM_EINVAL. */
+typedef int (*gpm_list_fn)(void* ctx, const uint32_t* verts, uint64_t n, int k);
+
 typedef struct gpm_config {
   int app;                  /* gpm_app                                            */
   int k;                    /* MAX_SIZE: vertices (TC/CF/MC); edges+1 (FSM)       */
@@ -71,6 +79,13 @@ typedef struct gpm_config {
    * on the counters (own tail first).  NULL = static split only. */
   void* steal_ctrs;
   uint64_t steal_chunk;     /* level-1 entries per stolen chunk; 0 = auto          */
+  /* Listing mode (TC/CF): the final level is materialised chunk by chunk
+   * (inspection-execution under the memory planner), reconstructed on the
+   * device into k-vertex rows and streamed device -> pinned host through a
+   * double buffer into `list_fn`.  result total = rows listed (summed over
+   * ranks by the exchange when world > 1; each rank lists its own roots). */
+  gpm_list_fn list_fn;      /* NULL = count only                                  */
+  void* list_ctx;
 } gpm_config;
 
 void gpm_config_default(gpm_config* cfg);

@@ -26,11 +26,16 @@ EXPORTS = [
 ]
 
 
+# gpm_list_fn(ctx, const uint32_t* verts, uint64_t n, int k) -> int
+LIST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint32), C.c_uint64, C.c_int)
+
+
 class Config(C.Structure):
     _fields_ = [("app", C.c_int), ("k", C.c_int), ("min_support", C.c_uint64), ("mem_budget", C.c_uint64),
                 ("no_orient", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("root_lo", C.c_uint64),
                 ("root_hi", C.c_uint64), ("stream", C.c_void_p), ("exchange", EXCHANGE_FN),
-                ("exchange_ctx", C.c_void_p), ("steal_ctrs", C.c_void_p), ("steal_chunk", C.c_uint64)]
+                ("exchange_ctx", C.c_void_p), ("steal_ctrs", C.c_void_p), ("steal_chunk", C.c_uint64),
+                ("list_fn", LIST_FN), ("list_ctx", C.c_void_p)]
 
 
 class Stats(C.Structure):

@@ -211,7 +211,7 @@ class MineResult:
 
 def make_config(app: str, k: int = 3, min_support: int = 0, *, mem_budget: int = 0, no_orient: bool = False,
                 rank: int = 0, world: int = 1, root_lo: int = 0, root_hi: int = 0, stream: int = 0,
-                exchange=None, steal_ctrs: int = 0, steal_chunk: int = 0) -> _L.Config:
+                exchange=None, steal_ctrs: int = 0, steal_chunk: int = 0, list_fn=None) -> _L.Config:
     cfg = _L.Config()
     lib().gpm_config_default(C.byref(cfg))
     cfg.app = APP_IDS[app]
@@ -226,6 +226,8 @@ def make_config(app: str, k: int = 3, min_support: int = 0, *, mem_budget: int =
         cfg.exchange = exchange
     cfg.steal_ctrs = steal_ctrs or None
     cfg.steal_chunk = steal_chunk
+    if list_fn is not None:
+        cfg.list_fn = list_fn
     return cfg
 
 
@@ -252,6 +254,29 @@ def mine(g: Graph, app: str, k: int = 3, min_support: int = 0, **kw) -> MineResu
         L.gpm_result_free(r)
         raise
     return MineResult(app, k, total.value, stats, r, npat.value)
+
+
+def list_embeddings(g: Graph, app: str, k: int, **kw):
+    """Listing mode (SPEC.md:458, PAPER.md:907-910 clique-listing): returns
+    (rows, result) where rows is a uint32 array of shape (count, k) holding
+    every final-level embedding in insertion order (DAG order for TC/CF),
+    streamed from the device through gpm_config.list_fn."""
+    chunks = []
+
+    def sink(_ctx, verts, n, kk):
+        try:
+            if n:
+                a = np.ctypeslib.as_array(verts, shape=(n * kk,))
+                chunks.append(a.reshape(n, kk).copy())
+            return 0
+        except Exception:  # never let an exception unwind through C
+            return 1
+
+    cb = _L.LIST_FN(sink)
+    res = mine(g, app, k, list_fn=cb, **kw)
+    kk = res.k
+    rows = np.concatenate(chunks) if chunks else np.zeros((0, kk), dtype=np.uint32)
+    return rows, res
 
 
 def triangle_count(g: Graph, **kw) -> int:

@@ -159,6 +159,8 @@ int gpm_mine(const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
   *out = nullptr;
   return guarded([&] {
     if (cfg->app < GPM_APP_TC || cfg->app > GPM_APP_FSM) throw Error(GPM_EINVAL, "unknown app");
+    if (cfg->list_fn && cfg->app != GPM_APP_TC && cfg->app != GPM_APP_CF)
+      throw Error(GPM_EINVAL, "listing mode: TC/CF only (SPEC.md:458)");
     if (cfg->world < 0 || (cfg->world > 1 && (cfg->rank < 0 || cfg->rank >= cfg->world)))
       throw Error(GPM_EINVAL, "bad rank/world");
     GPM_CUDA(cudaSetDevice(g->device));

@@ -748,7 +748,80 @@ struct Ctx {
   unsigned long long* d_ctr;
   bool siblings_complete;   // every child of each level parent is in this chunk
   bool generic_mc;   // GPM_GENERIC_MC: per-candidate binary-search path for MC
+  // listing mode (gpm_config.list_fn): the last level is materialised and
+  // streamed to the host instead of being counted in the fused kernel
+  gpm_list_fn list_fn;
+  void* list_ctx;
+  u64 listed;
 };
+
+// Listing: final-level entries [i0, i0 + n) -> rows of LEV + 1 vertex ids
+// (insertion order; consecutive threads write consecutive rows).
+template <int LEV>
+__global__ void list_rows_kernel(VLevels L, u64 i0, u64 n, u32* __restrict__ out) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    u32 emb[LEV + 1];
+    reconstruct<LEV>(L, i0 + i, emb);
+#pragma unroll
+    for (int t = 0; t <= LEV; ++t) out[i * (LEV + 1) + t] = emb[t];
+  }
+}
+
+// Streams a materialised final level (n entries at level LEV) to the host sink
+// through two device staging buffers and two pinned host buffers: the rows of
+// piece p are built and copied while the sink consumes piece p - 1.
+template <int LEV>
+void emit_rows(Ctx& c, const VLevels& L, u64 n) {
+  constexpr int K = LEV + 1;
+  const u64 R = std::min<u64>(n, u64(1) << 20);
+  DBuf<u32> d0(R * K, c.s), d1(R * K, c.s);
+  u32* dv[2] = {d0.get(), d1.get()};
+  u32* hv[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  u64 pn[2] = {0, 0};
+  auto cleanup = [&] {
+    for (int b = 0; b < 2; ++b) {
+      if (ev[b]) cudaEventDestroy(ev[b]);
+      if (hv[b]) cudaFreeHost(hv[b]);
+    }
+  };
+  try {
+    for (int b = 0; b < 2; ++b) {
+      GPM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hv[b]), sizeof(u32) * R * K));
+      GPM_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+    }
+    auto deliver = [&](int b) {
+      GPM_CUDA(cudaEventSynchronize(ev[b]));
+      if (c.list_fn(c.list_ctx, hv[b], pn[b], K) != 0) throw Error(GPM_EINVAL, "list_fn aborted the job");
+      c.listed += pn[b];
+    };
+    u64 piece = 0;
+    for (u64 i0 = 0; i0 < n; i0 += R, ++piece) {
+      const int b = (int)(piece & 1);
+      if (piece >= 2) deliver(b);  // buffer b still holds piece - 2
+      pn[b] = std::min<u64>(R, n - i0);
+      list_rows_kernel<LEV><<<(unsigned)std::min<u64>((pn[b] + 255) / 256, (u64)c.sms * 16), 256, 0, c.s>>>(
+          L, i0, pn[b], dv[b]);
+      GPM_CUDA(cudaGetLastError());
+      ++c.tl->launches;
+      GPM_CUDA(cudaMemcpyAsync(hv[b], dv[b], sizeof(u32) * pn[b] * K, cudaMemcpyDeviceToHost, c.s));
+      GPM_CUDA(cudaEventRecord(ev[b], c.s));
+    }
+    if (piece >= 2) deliver((int)(piece & 1));
+    if (piece >= 1) deliver((int)((piece - 1) & 1));
+  } catch (...) {
+    cudaStreamSynchronize(c.s);
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
+template <int LEV>
+void emit_dispatch(Ctx& c, const VLevels& L, u64 n) {
+  if constexpr (LEV + 1 < kMaxLevels) emit_rows<LEV>(c, L, n);
+  else throw Error(GPM_EINVAL, "listing: level out of range");
+}
 
 template <int APP, int LEV, int MODE>
 void launch_extend(Ctx& c, ExtendArgs& a, const char* what, double bytes) {
@@ -814,7 +887,8 @@ void process(Ctx& c, VLevels L, u64 np) {
     }
   }
   if constexpr (APP == kAppCF && LEV >= 2) {
-    if (last && c.g.oriented && c.siblings_complete && c.G->n < (1u << 27) && !std::getenv("GPM_GENERIC_CF")) {
+    if (last && !c.list_fn && c.g.oriented && c.siblings_complete && c.G->n < (1u << 27) &&
+        !std::getenv("GPM_GENERIC_CF")) {
       cf_last_siblings(c, L.idx[LEV - 1], L.vid[LEV - 1], np, LEV);
       return;
     }
@@ -876,7 +950,7 @@ void process(Ctx& c, VLevels L, u64 np) {
   a.b_begin = 0;
   a.b_end = nb;
   a.k = c.k;
-  if (last) {
+  if (last && !c.list_fn) {
     a.hist = c.d_hist;
     a.total = c.d_total;
     launch_extend<APP, LEV, kFused>(c, a, "extend_fused", bytes_in);
@@ -901,7 +975,7 @@ void process(Ctx& c, VLevels L, u64 np) {
   u64 T = 0;
   GPM_CUDA(cudaMemcpyAsync(&T, cnt.get() + nb, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
   GPM_CUDA(cudaStreamSynchronize(c.s));
-  st.level_sizes[LEV] += T;
+  if (!last) st.level_sizes[LEV] += T;  // a listed last level is counted through d_total
   st.balg += 8.0 * T;
   if (T == 0) return;
   // ---- planner: batch ranges whose children fit the budget
@@ -945,7 +1019,8 @@ void process(Ctx& c, VLevels L, u64 np) {
     nl.idx[LEV] = oi.get();
     nl.vid[LEV] = ov.get();
     c.siblings_complete = chunks.size() == 1;  // planner chunks may split a parent's children
-    process_dispatch<APP>(c, LEV + 1, nl, Tc);
+    if (last) emit_dispatch<LEV + 1>(c, nl, Tc);
+    else process_dispatch<APP>(c, LEV + 1, nl, Tc);
   }
 }
 
@@ -1168,6 +1243,10 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   c.st = &st;
   c.sms = sm_count();
   c.generic_mc = std::getenv("GPM_GENERIC_MC") != nullptr;
+  c.list_fn = cfg.list_fn;
+  c.list_ctx = cfg.list_ctx;
+  c.listed = 0;
+  if (c.list_fn && app == GPM_APP_MC) throw Error(GPM_EINVAL, "listing mode: TC/CF only (SPEC.md:458)");
   size_t freeb = 0, totalb = 0;
   freeb = device_free_bytes();
   (void)totalb;
@@ -1199,7 +1278,7 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
       mc3_staged(*G, l1s.get(), slo, shi, c.d_hist, s, tl, st);
     } else if (appk == kAppMC) {
       process_dispatch<kAppMC>(c, 1, L, np);
-    } else if (G->oriented && G->n < (1u << 27) && !std::getenv("GPM_GENERIC_L1")) {  // key = u << 5 | slot
+    } else if (G->oriented && G->n < (1u << 27) && !c.list_fn && !std::getenv("GPM_GENERIC_L1")) {  // key = u << 5 | slot
       process_l1_cf(c, L, l1i.get(), slo, shi);
     } else {
       process_dispatch<kAppCF>(c, 1, L, np);
@@ -1239,6 +1318,11 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   if (k == 2) res.total = nroot;
 
   htrace(s, "levels processed");
+  if (c.list_fn && k > 2) {  // listed rows play the fused kernel's count (exchanged below)
+    const unsigned long long v = c.listed;
+    GPM_CUDA(cudaMemcpyAsync(d_total.get(), &v, sizeof v, cudaMemcpyHostToDevice, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+  }
   // multi-GPU: the only collectives are the per-pattern counts and the
   // per-level size vectors
   if (cfg.world > 1 && cfg.exchange) {

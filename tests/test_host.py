@@ -136,3 +136,26 @@ def test_device_calls_fail_loudly_without_gpu():
     with pytest.raises(P.GpmError) as e:
         P.Graph(g)
     assert e.value.code == 4  # GPM_ECUDA: no silent CPU fallback
+
+
+def test_ctypes_structs_match_header(tmp_path):
+    """The ctypes mirror of gpm_config / gpm_stats has the C layout of
+    include/gpm.h (sizes and the offsets of the trailing fields)."""
+    import shutil
+    import subprocess
+    import ctypes as C
+    from paper_1911_06969_b200 import _lib as L
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "gpm.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(gpm_config),'
+                   ' offsetof(gpm_config, steal_chunk), offsetof(gpm_config, list_fn),'
+                   ' offsetof(gpm_config, list_ctx), sizeof(gpm_stats));return 0;}\n')
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()]
+    want = [C.sizeof(L.Config), L.Config.steal_chunk.offset, L.Config.list_fn.offset, L.Config.list_ctx.offset,
+            C.sizeof(L.Stats)]
+    assert got == want
