@@ -64,8 +64,9 @@ class ClockSampler:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, period_ms="100"):
         self.index = index
+        self.period_ms = str(period_ms)
         self.proc = None
         self.lines = []
 
@@ -76,7 +77,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", self.period_ms],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -269,7 +270,7 @@ def main():
     for _ in range(args.warmup):
         res = mine_step(g_in, **kw)
     barrier()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, os.environ.get("GPM_BENCH_CLOCK_MS", "100"))
     clocks.start()
     clocks.wait_samples(1)
     clocks.drain()

@@ -161,46 +161,107 @@ __device__ __forceinline__ u32 lanemask_lt() {
 }
 
 // Large buffers (level columns, hash tables, bitmaps: 64 MiB .. tens of GB)
-// come from their own per-device stream-ordered pool, in size classes of 1/8
-// of a power of two.  Sharing the default pool with the many small
-// temporaries let those split a cached multi-GB block, so the next call's
-// level buffer missed and the driver had to map (and zero) fresh physical
-// memory: hundreds of ms of jitter on a 0.4 s 4-MC step.
+// come from an explicit per-process cache of cudaMalloc blocks in size
+// classes of 1/8 of a power of two; small temporaries use the default
+// stream-ordered pool.  With stream-ordered pools the driver kept re-mapping
+// multi-GB blocks between calls (0.1-1.4 s stalls inside cudaMallocAsync on a
+// 0.44 s 4-MC step, GPM_TRACE); cached blocks never go back to the driver
+// unless an allocation fails.  A released block carries an event recorded on
+// the releasing stream; the next owner's stream waits on it.
 constexpr size_t kBigAlloc = size_t(64) << 20;
 inline size_t big_size_class(size_t bytes) {
   size_t p = size_t(1) << (63 - __builtin_clzll((unsigned long long)bytes));
   const size_t step = p / 8;
   return (bytes + step - 1) / step * step;
 }
-inline cudaMemPool_t big_pool(int dev) {
-  static std::mutex mu;
-  static cudaMemPool_t pools[64] = {};
-  if (dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lk(mu);
-  if (!pools[dev]) {
-    cudaMemPoolProps props{};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = dev;
-    cudaMemPool_t pl = nullptr;
-    if (cudaMemPoolCreate(&pl, &props) != cudaSuccess) {
+struct BigCache {
+  struct Blk {
+    void* p;
+    size_t bytes;
+    int dev;
+    cudaEvent_t ev;
+  };
+  std::mutex mu;
+  std::vector<Blk> free_;
+  // returns every cached block of `dev` to the driver
+  void trim(int dev) {
+    std::vector<Blk> keep, drop;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      for (auto& b : free_) (b.dev == dev ? drop : keep).push_back(b);
+      free_.swap(keep);
+    }
+    for (auto& b : drop) {
+      cudaEventSynchronize(b.ev);
+      cudaEventDestroy(b.ev);
+      cudaFree(b.p);
+    }
+  }
+  size_t cached(int dev) {
+    std::lock_guard<std::mutex> lk(mu);
+    size_t t = 0;
+    for (auto& b : free_)
+      if (b.dev == dev) t += b.bytes;
+    return t;
+  }
+};
+inline BigCache& big_cache() {
+  static BigCache* c = new BigCache;  // never destroyed: blocks may outlive static destructors
+  return *c;
+}
+inline void* big_alloc(size_t bytes, int dev, cudaStream_t st) {
+  const size_t cls = big_size_class(bytes);
+  BigCache& C = big_cache();
+  {
+    std::lock_guard<std::mutex> lk(C.mu);
+    for (size_t i = 0; i < C.free_.size(); ++i) {
+      if (C.free_[i].dev == dev && C.free_[i].bytes == cls) {
+        BigCache::Blk b = C.free_[i];
+        C.free_[i] = C.free_.back();
+        C.free_.pop_back();
+        cudaStreamWaitEvent(st, b.ev, 0);
+        cudaEventDestroy(b.ev);
+        return b.p;
+      }
+    }
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, cls) != cudaSuccess) {
+    cudaGetLastError();
+    C.trim(dev);  // other size classes (and the default pool's cache): hand them back, retry once
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaDeviceSynchronize();
+      cudaMemPoolTrimTo(pool, 0);
+    }
+    cudaGetLastError();
+    if (cudaMalloc(&p, cls) != cudaSuccess) {
       cudaGetLastError();
       return nullptr;
     }
-    unsigned long long thr = ~0ull;
-    cudaMemPoolSetAttribute(pl, cudaMemPoolAttrReleaseThreshold, &thr);
-    pools[dev] = pl;
   }
-  return pools[dev];
+  return p;
+}
+inline void big_release(void* p, size_t bytes, int dev, cudaStream_t st) {
+  cudaEvent_t ev = nullptr;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(ev, st) != cudaSuccess) {
+    cudaGetLastError();
+    cudaStreamSynchronize(st);
+    if (ev) cudaEventDestroy(ev);
+    cudaFree(p);
+    return;
+  }
+  BigCache& C = big_cache();
+  std::lock_guard<std::mutex> lk(C.mu);
+  C.free_.push_back({p, big_size_class(bytes), dev, ev});
 }
 
-// Stream-ordered device buffer (cudaMallocAsync pools; released memory stays
-// cached across gpm_mine calls).
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
   cudaStream_t s = 0;
+  int dev = -1;  // >= 0: a BigCache block of that device
   DBuf() = default;
   DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
   void alloc(size_t count, cudaStream_t st) {
@@ -209,22 +270,16 @@ struct DBuf {
     n = count;
     if (count) {
       const size_t bytes = count * sizeof(T);
-      cudaError_t e = cudaErrorMemoryAllocation;
-      cudaMemPool_t bp = nullptr;
+      cudaError_t e = cudaSuccess;
       if (bytes >= kBigAlloc) {
-        int dev = 0;
         cudaGetDevice(&dev);
-        bp = big_pool(dev);
-      }
-      if (bp) {
-        e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), big_size_class(bytes), bp, st);
-        if (e != cudaSuccess) {  // cached blocks of other classes: hand them back and retry once
-          cudaGetLastError();
-          cudaStreamSynchronize(st);
-          cudaMemPoolTrimTo(bp, 0);
-          e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), big_size_class(bytes), bp, st);
+        p = static_cast<T*>(big_alloc(bytes, dev, st));
+        if (!p) {
+          e = cudaErrorMemoryAllocation;
+          dev = -1;
         }
       } else {
+        dev = -1;
         e = cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, st);
       }
       if (e != cudaSuccess) {
@@ -236,19 +291,23 @@ struct DBuf {
     }
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) {
+      if (dev >= 0) big_release(p, n * sizeof(T), dev, s);
+      else cudaFreeAsync(p, s);
+    }
     p = nullptr;
     n = 0;
+    dev = -1;
   }
   ~DBuf() { release(); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), dev(o.dev) { o.p = nullptr; o.n = 0; o.dev = -1; }
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; n = o.n; s = o.s;
-      o.p = nullptr; o.n = 0;
+      p = o.p; n = o.n; s = o.s; dev = o.dev;
+      o.p = nullptr; o.n = 0; o.dev = -1;
     }
     return *this;
   }
@@ -315,15 +374,13 @@ inline size_t device_free_bytes() {
   size_t freeb = 0, totalb = 0;
   GPM_CUDA(cudaMemGetInfo(&freeb, &totalb));
   cudaMemPool_t pool;
-  cudaMemPool_t pools[2] = {nullptr, big_pool(dev)};
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) pools[0] = pool;
-  for (cudaMemPool_t pl : pools) {
-    if (!pl) continue;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     unsigned long long reserved = 0, used = 0;
-    if (cudaMemPoolGetAttribute(pl, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
-        cudaMemPoolGetAttribute(pl, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
       freeb += (size_t)(reserved - used);
   }
+  freeb += big_cache().cached(dev);
   cudaGetLastError();
   cache.dev = dev;
   cache.bytes = freeb;

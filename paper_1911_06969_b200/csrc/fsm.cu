@@ -1051,8 +1051,17 @@ struct Fsm {
     // first guess: previous level's distinct quick codes x fan-out, grown x8 on overflow
     // distinct quick codes <= accepted <= candidates W: size for 2 W (capped at
     // 2^26 entries = 1 GB) so the pass rarely has to regrow and re-run
+    // A child's quick code is a function of (parent quick code, extended
+    // position, new vertex label | closing position), so the level has at most
+    // prev_unique x (LEV + 1) x (2^LB + LEV + 1) distinct codes: a table of
+    // twice that never overflows (load <= 1/2) and is 4-250x smaller than the
+    // 2 W guess, i.e. mostly L2-resident probes instead of DRAM ones.
+    const u64 fan = (u64)(LEV + 1) * ((u64(1) << LB) + LEV + 1);
+    const u64 bound = prev_unique > (u64(1) << 40) / fan ? (u64(1) << 40) : prev_unique * fan;
+    u64 want = std::min<u64>(u64(1) << 26, std::max<u64>(2 * W, 64 * prev_unique));
+    want = std::min<u64>(want, 2 * bound + 2);
     u64 cap = 1u << 16;
-    while (cap < std::min<u64>(u64(1) << 26, std::max<u64>(2 * W, 64 * prev_unique))) cap <<= 1;
+    while (cap < want) cap <<= 1;
     // Last level: fuse the domain pass into pass A.  Children OR their vertices
     // into per-quick-code bitmaps (label-local, quick positions); after
     // canonicalisation these are merged into the canonical patterns' bitmaps

@@ -836,6 +836,7 @@ void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u
   DBuf<unsigned long long> ctr(1, s), cand(1, s);
   GPM_CUDA(cudaMemsetAsync(ctr.get(), 0, sizeof(unsigned long long), s));
   GPM_CUDA(cudaMemsetAsync(cand.get(), 0, sizeof(unsigned long long), s));
+  htrace(s, "mc4: scratch");
   Mc4Args a{};
   a.g = G.view();
   a.l1i = l1i;

@@ -899,8 +899,11 @@ void process(Ctx& c, VLevels L, u64 np) {
   DBuf<u64> Wp;
   {
     DBuf<u64> w(np, c.s);
+    htrace(c.s, "generic: alloc w");
     run_work<APP, LEV>(c, L, np, w.get());
+    htrace(c.s, "generic: work kernel");
     pidx.alloc(np, c.s);
+    htrace(c.s, "generic: alloc pidx");
     DBuf<u64> nsel(1, c.s);
     size_t tmp = 0;
     thrust::counting_iterator<u32> it(0);
@@ -909,7 +912,9 @@ void process(Ctx& c, VLevels L, u64 np) {
     GPM_CUDA(cub::DeviceSelect::If(t.get(), tmp, it, pidx.get(), nsel.get(), (int64_t)np, NonZeroW{w.get()}, c.s));
     GPM_CUDA(cudaMemcpyAsync(&nz, nsel.get(), sizeof(u64), cudaMemcpyDeviceToHost, c.s));
     GPM_CUDA(cudaStreamSynchronize(c.s));
+    htrace(c.s, "generic: select");
     Wp.alloc(nz + 1, c.s);
+    htrace(c.s, "generic: alloc Wp");
     GPM_CUDA(cudaMemsetAsync(Wp.get() + nz, 0, sizeof(u64), c.s));
     if (nz) {
       gather_kernel<<<(unsigned)std::min<u64>((nz + 255) / 256, 1u << 20), 256, 0, c.s>>>(w.get(), pidx.get(), nz,
@@ -971,6 +976,7 @@ void process(Ctx& c, VLevels L, u64 np) {
     a.mask_base = 0;
   }
   launch_extend<APP, LEV, kCount>(c, a, "extend_count", bytes_in);
+  htrace(c.s, "generic: count");
   scan_inplace(cnt.get(), nb + 1, c.s);
   u64 T = 0;
   GPM_CUDA(cudaMemcpyAsync(&T, cnt.get() + nb, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
@@ -1004,6 +1010,7 @@ void process(Ctx& c, VLevels L, u64 np) {
     const u64 Tc = end - base;
     if (Tc == 0) continue;
     DBuf<u32> oi(Tc, c.s), ov(Tc, c.s);
+    htrace(c.s, "generic: alloc level");
     ExtendArgs w = a;
     w.b_begin = b0;
     w.b_end = b1;
@@ -1015,6 +1022,7 @@ void process(Ctx& c, VLevels L, u64 np) {
     const double frac = (double)(b1 - b0) / (double)nb;
     const double wbytes = a.masks ? (double)(b1 - b0) * kBatch / 8.0 + 24.0 * Tc : bytes_in * frac;
     launch_extend<APP, LEV, kWrite>(c, w, "extend_write", wbytes + 8.0 * Tc);
+    htrace(c.s, "generic: write");
     VLevels nl = L;
     nl.idx[LEV] = oi.get();
     nl.vid[LEV] = ov.get();
