@@ -267,12 +267,15 @@ def main():
         return P.mine(g, app, k, sigma, **extra, **skw)
 
     res = None
-    for _ in range(args.warmup):
-        res = mine_step(g_in, **kw)
-    barrier()
+    # the sampler starts (and delivers its first line) BEFORE the warm-up, so
+    # the GPU goes straight from the warm-up steps into the timed ones instead
+    # of idling (and dropping clocks) while nvidia-smi comes up
     clocks = ClockSampler(local, os.environ.get("GPM_BENCH_CLOCK_MS", "100"))
     clocks.start()
     clocks.wait_samples(1)
+    for _ in range(args.warmup):
+        res = mine_step(g_in, **kw)
+    barrier()
     clocks.drain()
     n_before = len(clocks.lines)
     step_ms = []
@@ -341,11 +344,22 @@ def main():
     peak, peak_kind = load_peaks()
     dms = statistics.median(dom_ms)
     achieved = (statistics.median(dom_b) / (dms / 1e3) / 1e9) if dms > 0 else 0.0
-    traffic = None
+    traffic = l2_bytes = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{args.app}.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("dram_bytes_per_launch")
+        l2_bytes = tj.get("l2_bytes_per_launch") or None
+    # measured traffic of one ncu-captured launch over this run's live kernel time:
+    # the DRAM rate, and the L2 rate SURVEY §8d asks for on the L2-resident configs
+    mem_rates = {}
+    if dms > 0:
+        if traffic:
+            mem_rates["dram_gbs"] = traffic / (dms / 1e3) / 1e9
+        if l2_bytes:
+            mem_rates["l2_bytes_per_launch"] = l2_bytes
+            mem_rates["l2_gbs"] = l2_bytes / (dms / 1e3) / 1e9
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -361,7 +375,8 @@ def main():
                      "note": ("B_alg counts 4 B for every candidate of every position; staged source "
                               "lists are read on chip once per root/group, and L2-resident CSRs are "
                               "re-read from L2, so B_alg/t can exceed the HBM copy rate. traffic = ncu "
-                              "dram bytes of one captured launch (profiles/traffic_<app>.json)")},
+                              "dram bytes of one captured launch (profiles/traffic_<app>.json)"),
+                     **mem_rates},
         "step_ms": [round(x, 4) for x in step_ms],
         "gpu_launches": launches,
         "clocks": clock_rec,

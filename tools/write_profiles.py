@@ -54,6 +54,9 @@ for rep in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "full_*.ncu-rep")))
         rd = val(h, u, row, "dram__bytes_read.sum") or 0
         wr = val(h, u, row, "dram__bytes_write.sum") or 0
         l2 = val(h, u, row, "lts__t_bytes.sum")
+        if not l2:
+            sec = val(h, u, row, "lts__t_sectors.sum")
+            l2 = 32.0 * sec if sec else None
         lines.append(f"kernel {kname}")
         lines.append(f"  duration_ms {t * 1e3:.4f}" if t else "  duration_ms ?")
         lines.append(f"  dram_read_GB {rd / 1e9:.3f}  dram_write_GB {wr / 1e9:.3f}  dram_GBps {((rd + wr) / t / 1e9) if t else 0:.1f}")
@@ -78,10 +81,11 @@ for rep in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "full_*.ncu-rep")))
                                            for k, v in top))
         app = tag.split("_")[0]
         if app in DOMINANT and any(k in kname for k in DOMINANT[app]) and t:
-            e = traffic.setdefault(app, {"kernels": [], "dram_bytes_per_launch": 0.0, "duration_ms_ncu": 0.0,
-                                         "sources": []})
+            e = traffic.setdefault(app, {"kernels": [], "dram_bytes_per_launch": 0.0, "l2_bytes_per_launch": 0.0,
+                                         "duration_ms_ncu": 0.0, "sources": []})
             e["kernels"].append(kname)
             e["dram_bytes_per_launch"] += rd + wr
+            e["l2_bytes_per_launch"] += l2 or 0.0
             e["duration_ms_ncu"] += t * 1e3
             e["sources"].append(f"profiles/{rnd}/ncu_{tag}.txt")
     src = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_source.py"), rep, tag.split("_", 1)[1], "0", "15"],
