@@ -346,7 +346,8 @@ def main():
     achieved = (statistics.median(dom_b) / (dms / 1e3) / 1e9) if dms > 0 else 0.0
     traffic = l2_bytes = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{args.app}.json")
-    if os.path.exists(tp):
+    # the ncu capture is of the workload's default configuration only
+    if os.path.exists(tp) and (args.sigma is None or args.sigma == WORKLOADS[args.app][2]):
         with open(tp) as f:
             tj = json.load(f)
         traffic = tj.get("dram_bytes_per_launch")

@@ -256,6 +256,23 @@ inline void big_release(void* p, size_t bytes, int dev, cudaStream_t st) {
   C.free_.push_back({p, big_size_class(bytes), dev, ev});
 }
 
+// Raw allocations outside DBuf (graph CSR arrays): same policy as DBuf.
+inline cudaError_t dev_malloc(void** p, size_t bytes, cudaStream_t s) {
+  if (bytes >= kBigAlloc) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    *p = big_alloc(bytes, dev, s);
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+  }
+  return cudaMallocAsync(p, bytes, s);
+}
+inline void dev_free(void* p, size_t bytes, int dev, cudaStream_t s) {
+  if (!p) return;
+  if (bytes >= kBigAlloc) big_release(p, bytes, dev, s);
+  else cudaFreeAsync(p, s);
+}
+
+// Device buffer: >= 64 MiB from BigCache, else the stream-ordered default pool.
 template <class T>
 struct DBuf {
   T* p = nullptr;

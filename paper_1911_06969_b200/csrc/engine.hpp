@@ -17,6 +17,7 @@ struct gpm_graph {
   gpm::u64* d_off = nullptr;
   gpm::u32* d_col = nullptr;
   gpm::u32* d_lab = nullptr;            // dense label ranks (order-preserving)
+  size_t sz_off = 0, sz_col = 0, sz_lab = 0;  // allocation bytes (>= 64 MiB: BigCache blocks)
   std::vector<gpm::u32> label_values;   // rank -> original label value
   int label_bits = 0;
   gpm::u32 max_deg = 0;

@@ -398,7 +398,8 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
   out.label_values = g.label_values;
   out.label_bits = g.label_bits;
   GPM_CUDA(cudaStreamSynchronize(g.stream));  // source graph ordered before our stream
-  GPM_CUDA(cudaMallocAsync((void**)&out.d_off, sizeof(u64) * (g.n + 1), s));
+  out.sz_off = sizeof(u64) * (g.n + 1);
+  GPM_CUDA(dev_malloc((void**)&out.d_off, out.sz_off, s));
   GPM_CUDA(cudaMemsetAsync(out.d_off + g.n, 0, sizeof(u64), s));
   DBuf<u8> keep(std::max<u64>(1, g.m), s);
   DBuf<int> bad(1, s);
@@ -413,14 +414,16 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
   GPM_CUDA(cudaMemcpyAsync(&m, out.d_off + g.n, sizeof(u64), cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaStreamSynchronize(s));
   out.m = m;
-  GPM_CUDA(cudaMallocAsync((void**)&out.d_col, sizeof(u32) * std::max<u64>(1, m), s));
+  out.sz_col = sizeof(u32) * std::max<u64>(1, m);
+  GPM_CUDA(dev_malloc((void**)&out.d_col, out.sz_col, s));
   if (g.n && m) {
     orient_write_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, keep.get(), 0, g.n, g.m,
                                                                     out.d_off, out.d_col);
     GPM_CUDA(cudaGetLastError());
   }
   if (g.labeled) {
-    GPM_CUDA(cudaMallocAsync((void**)&out.d_lab, sizeof(u32) * std::max<u32>(1, g.n), s));
+    out.sz_lab = sizeof(u32) * std::max<u32>(1, g.n);
+    GPM_CUDA(dev_malloc((void**)&out.d_lab, out.sz_lab, s));
     GPM_CUDA(cudaMemcpyAsync(out.d_lab, g.d_lab, sizeof(u32) * g.n, cudaMemcpyDeviceToDevice, s));
   }
   set_max_degree(out, s);
@@ -450,9 +453,11 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
   DBuf<u32> md(1, s);
   GPM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
   GPM_CUDA(cudaMemsetAsync(md.get(), 0, sizeof(u32), s));
-  GPM_CUDA(cudaMallocAsync((void**)&out.d_off, sizeof(u64) * (n + 1), s));
+  out.sz_off = sizeof(u64) * (n + 1);
+  GPM_CUDA(dev_malloc((void**)&out.d_off, out.sz_off, s));
   // a valid undirected CSR keeps exactly m/2 entries; m bounds any input
-  GPM_CUDA(cudaMallocAsync((void**)&out.d_col, sizeof(u32) * std::max<u64>(1, m), s));
+  out.sz_col = sizeof(u32) * std::max<u64>(1, m);
+  GPM_CUDA(dev_malloc((void**)&out.d_col, out.sz_col, s));
   cudaEvent_t ready;
   GPM_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   GPM_CUDA(cudaEventRecord(ready, s));  // allocations visible to the copy stream
@@ -498,7 +503,8 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
                                                                                                  cnt.get(), n, md.get());
   GPM_CUDA(cudaGetLastError());
   if (labels) {
-    GPM_CUDA(cudaMallocAsync((void**)&out.d_lab, sizeof(u32) * std::max<u32>(1, n), s));
+    out.sz_lab = sizeof(u32) * std::max<u32>(1, n);
+    GPM_CUDA(dev_malloc((void**)&out.d_lab, out.sz_lab, s));
   }
   u64 dm = 0;
   int hb = 0;
@@ -523,9 +529,9 @@ using namespace gpm;
 gpm_graph::~gpm_graph() {
   cudaSetDevice(device);
   cudaStream_t s = stream ? stream : 0;
-  if (d_off) cudaFreeAsync(d_off, s);
-  if (d_col) cudaFreeAsync(d_col, s);
-  if (d_lab) cudaFreeAsync(d_lab, s);
+  dev_free(d_off, sz_off, device, s);
+  dev_free(d_col, sz_col, device, s);
+  dev_free(d_lab, sz_lab, device, s);
   if (stream) {
     cudaStreamSynchronize(stream);
     if (owns_stream) cudaStreamDestroy(stream);
@@ -556,8 +562,10 @@ extern "C" int gpm_graph_create_csr(const uint64_t* row_offsets, const uint32_t*
     g->oriented = oriented != 0;
     GPM_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     cudaStream_t s = g->stream;
-    GPM_CUDA(cudaMallocAsync((void**)&g->d_off, sizeof(u64) * (n + 1), s));
-    GPM_CUDA(cudaMallocAsync((void**)&g->d_col, sizeof(u32) * std::max<u64>(1, m), s));
+    g->sz_off = sizeof(u64) * (n + 1);
+    GPM_CUDA(dev_malloc((void**)&g->d_off, g->sz_off, s));
+    g->sz_col = sizeof(u32) * std::max<u64>(1, m);
+    GPM_CUDA(dev_malloc((void**)&g->d_col, g->sz_col, s));
     GPM_CUDA(cudaMemcpyAsync(g->d_off, row_offsets, sizeof(u64) * (n + 1), cudaMemcpyHostToDevice, s));
     if (m) GPM_CUDA(cudaMemcpyAsync(g->d_col, col, sizeof(u32) * m, cudaMemcpyHostToDevice, s));
     if (labels) {
@@ -573,7 +581,8 @@ extern "C" int gpm_graph_create_csr(const uint64_t* row_offsets, const uint32_t*
       for (u32 v = 0; v < n; ++v)
         ranks[v] = (u32)(std::lower_bound(vals.begin(), vals.end(), labels[v]) - vals.begin());
       g->labeled = true;
-      GPM_CUDA(cudaMallocAsync((void**)&g->d_lab, sizeof(u32) * std::max<u32>(1, n), s));
+      g->sz_lab = sizeof(u32) * std::max<u32>(1, n);
+      GPM_CUDA(dev_malloc((void**)&g->d_lab, g->sz_lab, s));
       GPM_CUDA(cudaMemcpyAsync(g->d_lab, ranks.data(), sizeof(u32) * n, cudaMemcpyHostToDevice, s));
       GPM_CUDA(cudaStreamSynchronize(s));  // ranks is a host temporary
     }
