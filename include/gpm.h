@@ -200,6 +200,12 @@ int gpm_generate_rmat(int scale, double edge_factor, double a, double b, double 
                       uint32_t n_labels, uint64_t label_seed, gpm_csr* out);
 void gpm_csr_free(gpm_csr* csr);
 
+/* Returns the device buffers the library keeps cached between gpm_mine calls
+ * (level columns, hash tables, bitmaps >= 64 MiB) to the driver; the next
+ * call re-allocates them.  For callers that share the GPU with other
+ * allocators.  device < 0: every device. */
+int gpm_release_cached(int device);
+
 const char* gpm_last_error(void);
 const char* gpm_version(void);
 

@@ -23,6 +23,7 @@ EXPORTS = [
     "gpm_result_num_patterns", "gpm_result_pattern", "gpm_result_stats", "gpm_result_free",
     "gpm_load_edge_list", "gpm_load_labeled_graph", "gpm_csr_from_edges", "gpm_generate_rmat", "gpm_csr_free",
     "gpm_last_error", "gpm_version", "gpm_steal_create", "gpm_steal_open", "gpm_steal_reset", "gpm_steal_release",
+    "gpm_release_cached",
 ]
 
 
@@ -102,6 +103,7 @@ def lib():
         "gpm_steal_open": (i32, [i32, vp, C.POINTER(vp)]),
         "gpm_steal_reset": (i32, [vp, i32, vp]),
         "gpm_steal_release": (i32, [vp, i32]),
+        "gpm_release_cached": (i32, [i32]),
         "gpm_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():

@@ -279,6 +279,12 @@ def list_embeddings(g: Graph, app: str, k: int, **kw):
     return rows, res
 
 
+def release_cached(device: int = -1) -> None:
+    """Hands the library's cached >= 64 MiB device buffers back to the driver
+    (gpm_release_cached); device < 0: every device."""
+    check(lib().gpm_release_cached(device))
+
+
 def triangle_count(g: Graph, **kw) -> int:
     """SPEC.md:414-422 / PAPER.md:982-984."""
     return mine(g, "tc", 3, **kw).total

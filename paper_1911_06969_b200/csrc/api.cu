@@ -91,6 +91,21 @@ const char* gpm_last_error(void) { return g_last_error.c_str(); }
 
 const char* gpm_version(void) { return "gpm-b200 0.1 (sm_100a)"; }
 
+int gpm_release_cached(int device) {
+  return guarded([&] {
+    int nd = 0;
+    GPM_CUDA(cudaGetDeviceCount(&nd));
+    int cur = 0;
+    GPM_CUDA(cudaGetDevice(&cur));
+    for (int d = 0; d < nd; ++d) {
+      if (device >= 0 && d != device) continue;
+      GPM_CUDA(cudaSetDevice(d));
+      big_cache().trim(d);
+    }
+    GPM_CUDA(cudaSetDevice(cur));
+  });
+}
+
 void gpm_config_default(gpm_config* cfg) {
   if (!cfg) return;
   std::memset(cfg, 0, sizeof(*cfg));

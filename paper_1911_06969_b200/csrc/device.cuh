@@ -298,6 +298,13 @@ struct DBuf {
       } else {
         dev = -1;
         e = cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, st);
+        if (e != cudaSuccess) {  // the big-buffer cache may hold the memory: hand it back, retry
+          cudaGetLastError();
+          int d = 0;
+          cudaGetDevice(&d);
+          big_cache().trim(d);
+          e = cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, st);
+        }
       }
       if (e != cudaSuccess) {
         cudaGetLastError();

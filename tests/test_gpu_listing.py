@@ -133,3 +133,15 @@ def test_list_errors(P):
     # the library stays usable after an aborted listing
     assert P.mine(g, "tc", 3).total == len(P.list_embeddings(g, "tc", 3)[0])
     del C
+
+
+def test_release_cached_between_calls(P):
+    # the big-buffer cache is handed back to the driver and rebuilt transparently
+    hg = P.generate_rmat(14, 16, 0.57, 0.19, 0.19, seed=7)
+    g = P.Graph(hg)
+    a = P.mine(g, "mc", 3)
+    P.release_cached()
+    P.release_cached(0)
+    b = P.mine(g, "mc", 3)
+    assert a.total == b.total and a.patterns == b.patterns
+    assert a.stats["n_explored"] == b.stats["n_explored"]

@@ -136,6 +136,8 @@ def test_device_calls_fail_loudly_without_gpu():
     with pytest.raises(P.GpmError) as e:
         P.Graph(g)
     assert e.value.code == 4  # GPM_ECUDA: no silent CPU fallback
+    with pytest.raises(P.GpmError):
+        P.release_cached()
 
 
 def test_ctypes_structs_match_header(tmp_path):
