@@ -208,6 +208,31 @@ class MineResult:
     def pattern_map(self) -> Dict[str, int]:
         return {t: s for _, t, s in self.patterns}
 
+    def to_tsv(self) -> str:
+        """PatternMap serialisation: `pattern<TAB>support` rows."""
+        return pattern_tsv(self.patterns)
+
+    def to_record(self) -> str:
+        """AppResult as a single-line JSON record."""
+        import json
+        rec = {"app": self.app, "k": self.k, "total_count": self.total,
+               "elapsed_s": self.stats.get("ms_total", 0.0) / 1e3,
+               "n_explored": self.stats.get("n_explored", 0),
+               "patterns": [[t, s] for t, s in _tsv_order(self.patterns)]}
+        return json.dumps(rec, separators=(",", ":"))
+
+
+def _tsv_order(patterns) -> List[Tuple[str, int]]:
+    """Descending support, then pattern text.  Patterns of
+    several levels (FSM) share one table; a canonical text names one level."""
+    return sorted(((t, int(s)) for _, t, s in patterns), key=lambda x: (-x[1], x[0]))
+
+
+def pattern_tsv(patterns) -> str:
+    """`pattern<TAB>support` lines for (level, text, support) tuples, sorted by
+    descending support then pattern text."""
+    return "".join(f"{t}\t{s}\n" for t, s in _tsv_order(patterns))
+
 
 def make_config(app: str, k: int = 3, min_support: int = 0, *, mem_budget: int = 0, no_orient: bool = False,
                 rank: int = 0, world: int = 1, root_lo: int = 0, root_hi: int = 0, stream: int = 0,

@@ -145,3 +145,19 @@ def test_release_cached_between_calls(P):
     b = P.mine(g, "mc", 3)
     assert a.total == b.total and a.patterns == b.patterns
     assert a.stats["n_explored"] == b.stats["n_explored"]
+
+
+def test_pattern_tsv_and_record(P, oracle):
+    # PatternMap TSV and the single-line AppResult record (:463)
+    import json
+    hg = P.generate_rmat(11, 8, 0.45, 0.15, 0.15, seed=3, n_labels=4, label_seed=101)
+    g = P.Graph(hg)
+    oc = oracle.Csr(hg.off, hg.col, hg.labels)
+    for app, k, sigma in (("mc", 4, 0), ("fsm", 3, 40)):
+        r = P.mine(g, app, k, sigma)
+        o = oracle.mine(oc, app, k, sigma)
+        assert r.to_tsv() == P.pattern_tsv([tuple(x) for x in o["patterns"]])
+        rec = json.loads(r.to_record())
+        assert rec["app"] == app and rec["total_count"] == r.total
+        assert [tuple(x) for x in rec["patterns"]] == [tuple(ln.split("\t")[:1]) + (int(ln.split("\t")[1]),)
+                                                      for ln in r.to_tsv().splitlines()]

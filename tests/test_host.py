@@ -161,3 +161,16 @@ def test_ctypes_structs_match_header(tmp_path):
     want = [C.sizeof(L.Config), L.Config.steal_chunk.offset, L.Config.list_fn.offset, L.Config.list_ctx.offset,
             C.sizeof(L.Stats)]
     assert got == want
+
+
+def test_pattern_tsv_order(oracle):
+    """descending support, then pattern text; one row per pattern."""
+    import paper_1911_06969_b200 as P
+    g = oracle.csr_from_edges([(0, 1), (1, 2), (2, 0), (2, 3), (3, 4)], 5)
+    o = oracle.mine(g, "mc", 3)
+    tsv = P.pattern_tsv([tuple(x) for x in o["patterns"]])
+    rows = [ln.split("\t") for ln in tsv.splitlines()]
+    assert len(rows) == len(o["patterns"])
+    keys = [(-int(s), t) for t, s in rows]
+    assert keys == sorted(keys)
+    assert sum(int(s) for _, s in rows) == o["total"]
