@@ -368,6 +368,7 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": config,
         "e2e": {"value": n_explored / (e2e_ms_step / 1e3), "unit": UNIT, "ms_per_step": e2e_ms_step,
+                "step_ms": [round(x, 3) for x in e2e_ms],
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": res.stats["dominant"],

@@ -383,8 +383,10 @@ inline void htrace(cudaStream_t s, const char* what) {
 // ordered pool holds reserved but unused (the pool keeps released blocks,
 // keep_pool_warm), so the planner's budget does not shrink from call to call.
 inline size_t device_free_bytes() {
-  // cudaMemGetInfo costs up to ~1 ms of host time: reuse a reading taken in
-  // the last 50 ms on this device (back-to-back mine calls)
+  // cudaMemGetInfo costs ~1 ms of host time, and tens of ms when an NVML
+  // client (nvidia-smi) is polling the device: reuse a reading taken in the
+  // last 2 s on this device (the planner budgets a fraction of it, and an
+  // allocation that still fails raises GPM_ENOMEM)
   int dev = 0;
   cudaGetDevice(&dev);
   struct Cached {
@@ -394,7 +396,7 @@ inline size_t device_free_bytes() {
   };
   static thread_local Cached cache;
   const auto now = std::chrono::steady_clock::now();
-  if (cache.dev == dev && now - cache.at < std::chrono::milliseconds(50)) return cache.bytes;
+  if (cache.dev == dev && now - cache.at < std::chrono::milliseconds(2000)) return cache.bytes;
   size_t freeb = 0, totalb = 0;
   GPM_CUDA(cudaMemGetInfo(&freeb, &totalb));
   cudaMemPool_t pool;
