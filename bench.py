@@ -21,6 +21,7 @@ over NCCL; time is the max over ranks.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -282,6 +283,8 @@ def main():
     dom_ms, dom_b, launches = [], [], 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed host calls (re-enabled after the e2e steps)
     for _ in range(args.steps):
         flush.zero_()
         if steal is not None:
@@ -334,6 +337,7 @@ def main():
         torch.cuda.synchronize()
         if i > 0:
             e2e_ms.append(1e3 * (time.perf_counter() - t))
+    gc.enable()
     et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
