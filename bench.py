@@ -324,7 +324,8 @@ def main():
     h2d = pinned.off.nbytes + pinned.col.nbytes + (0 if lab_p is None else pinned.labels.nbytes)
     e2e_ms = []
     er = None
-    for i in range(1 + args.steps):
+    ew = max(1, args.warmup)  # untimed e2e warm-up calls (first-touch of pinned pages, caches)
+    for i in range(ew + args.steps):
         if steal is not None:
             steal.reset()
         barrier()
@@ -335,7 +336,7 @@ def main():
                     **({"steal_ctrs": steal.ptr} if steal else {}))
         del g
         torch.cuda.synchronize()
-        if i > 0:
+        if i >= ew:
             e2e_ms.append(1e3 * (time.perf_counter() - t))
     gc.enable()
     et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
