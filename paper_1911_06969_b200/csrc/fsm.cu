@@ -889,11 +889,13 @@ struct Fsm {
     if (R.P)
       GPM_CUDA(cudaMemcpyAsync(R.mni_h.data(), mni.get(), sizeof(u64) * R.P, cudaMemcpyDeviceToHost, s));
     sync();
+    trace("mni kernel + d2h", (double)R.P);
     std::vector<u8> freq(std::max<u64>(1, R.P), 0);
     for (u64 p = 0; p < R.P; ++p) freq[p] = (R.gcount_h[p] >= sigma && R.mni_h[p] >= sigma) ? 1 : 0;
     R.frequent.alloc(freq.size(), s);
     GPM_CUDA(cudaMemcpyAsync(R.frequent.get(), freq.data(), freq.size(), cudaMemcpyHostToDevice, s));
     sync();
+    trace("frequent flags h2d", (double)R.P);
   }
 
   void record(Level& R, int level) {
@@ -901,6 +903,7 @@ struct Fsm {
     for (u64 p = 0; p < R.P; ++p)
       if (R.gcount_h[p] >= sigma && R.mni_h[p] >= sigma) sel.push_back(p);
     // text is formatted on access (gpm_result_pattern): ~10^6 patterns per call
+    res.patterns.reserve(res.patterns.size() + sel.size());
     for (u64 p : sel) res.patterns.push_back({std::string(), R.mni_h[p], level, R.gkeys_h[p]});
   }
 
