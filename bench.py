@@ -385,6 +385,9 @@ def main():
                               "dram bytes of one captured launch (profiles/traffic_<app>.json)"),
                      **mem_rates},
         "step_ms": [round(x, 4) for x in step_ms],
+        # SURVEY §8d asks for best and median as well as the mean (`ms_per_step`)
+        "step_stats": {"best_ms": min(step_ms), "median_ms": statistics.median(step_ms),
+                       "e2e_best_ms": min(e2e_ms), "e2e_median_ms": statistics.median(e2e_ms)},
         "gpu_launches": launches,
         "clocks": clock_rec,
         "result": {"total": res.total, "n_explored": n_explored, "level_sizes": res.stats["level_sizes"],
