@@ -256,14 +256,26 @@ int gpm_result_num_patterns(const gpm_result* r, uint64_t* n) {
     set_last_error("null argument");
     return GPM_EINVAL;
   }
-  *n = r->patterns.size();
+  *n = r->patterns.size() + r->kpatterns.size();
   return GPM_OK;
 }
 
 int gpm_result_pattern(const gpm_result* r, uint64_t i, char* text, size_t cap, uint64_t* support, int* level) {
-  if (!r || i >= r->patterns.size()) {
+  if (!r || i >= r->patterns.size() + r->kpatterns.size()) {
     set_last_error("pattern index out of range");
     return GPM_EINVAL;
+  }
+  if (i >= r->patterns.size()) {  // FSM record: format the canonical key now
+    const auto& q = r->kpatterns[i - r->patterns.size()];
+    if (text && cap) {
+      const std::string t = canon_text(q.key, 0, r->label_bits, &r->label_values);
+      size_t c = std::min(cap - 1, t.size());
+      std::memcpy(text, t.data(), c);
+      text[c] = 0;
+    }
+    if (support) *support = q.support;
+    if (level) *level = q.level;
+    return GPM_OK;
   }
   auto& p = const_cast<gpm_result*>(r)->patterns[i];
   if (p.text.empty() && p.key) p.text = canon_text(p.key, 0, r->label_bits, &r->label_values);

@@ -38,6 +38,14 @@ struct gpm_result {
     gpm::u64 key = 0;   // packed canonical code (pattern.cuh)
   };
   std::vector<Pattern> patterns;
+  // FSM: ~10^6 patterns per call kept as 24-byte (key, support, level)
+  // records; the canonical text is formatted by gpm_result_pattern on access
+  struct KeyPattern {
+    gpm::u64 key;
+    gpm::u64 support;
+    int level;
+  };
+  std::vector<KeyPattern> kpatterns;
   int label_bits = 0;                      // for formatting FSM keys lazily
   std::vector<gpm::u32> label_values;      // dense label rank -> original label
   gpm_stats stats{};

@@ -903,8 +903,8 @@ struct Fsm {
     for (u64 p = 0; p < R.P; ++p)
       if (R.gcount_h[p] >= sigma && R.mni_h[p] >= sigma) sel.push_back(p);
     // text is formatted on access (gpm_result_pattern): ~10^6 patterns per call
-    res.patterns.reserve(res.patterns.size() + sel.size());
-    for (u64 p : sel) res.patterns.push_back({std::string(), R.mni_h[p], level, R.gkeys_h[p]});
+    res.kpatterns.reserve(res.kpatterns.size() + sel.size());
+    for (u64 p : sel) res.kpatterns.push_back({R.gkeys_h[p], R.mni_h[p], level});
   }
 
   FsmArgs base_args(Level& R) {
@@ -1249,7 +1249,8 @@ struct Fsm {
       st.balg = (double)v.back();
     }
     // (level, support desc, canonical key): integer compares only
-    std::sort(res.patterns.begin(), res.patterns.end(), [](const gpm_result::Pattern& x, const gpm_result::Pattern& y) {
+    std::sort(res.kpatterns.begin(), res.kpatterns.end(),
+              [](const gpm_result::KeyPattern& x, const gpm_result::KeyPattern& y) {
       if (x.level != y.level) return x.level < y.level;
       if (x.support != y.support) return x.support > y.support;
       return x.key < y.key;
