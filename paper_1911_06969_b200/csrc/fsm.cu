@@ -21,6 +21,7 @@
 //      whose pattern has MNI >= sigma -> next SoA level (idx, vid, his).
 // The last level is never materialised.  Multi-GPU: pattern keys are
 // all-gathered and bitmaps OR-exchanged through gpm_config.exchange.
+#include <parallel/algorithm>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -1249,8 +1250,9 @@ struct Fsm {
       st.balg = (double)v.back();
     }
     // (level, support desc, canonical key): integer compares only
-    std::sort(res.kpatterns.begin(), res.kpatterns.end(),
-              [](const gpm_result::KeyPattern& x, const gpm_result::KeyPattern& y) {
+    // ~10^6 records: libstdc++'s OpenMP parallel sort on the host cores
+    __gnu_parallel::sort(res.kpatterns.begin(), res.kpatterns.end(),
+                         [](const gpm_result::KeyPattern& x, const gpm_result::KeyPattern& y) {
       if (x.level != y.level) return x.level < y.level;
       if (x.support != y.support) return x.support > y.support;
       return x.key < y.key;
