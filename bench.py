@@ -12,9 +12,15 @@ seed 1), degree-ordered DAG.  A step = one complete mine() of that workload.
 * e2e    = the same metric through the public C ABI from pinned HOST buffers:
            every step uploads the undirected CSR, orients it on the device,
            mines, and reads the result back.
-* roofline = the dominant extend kernel's algorithmic bytes (SURVEY §8d B_alg)
-           / its CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
-* cpu_baseline = the C++/OpenMP oracle (oracle/liboracle.so) on this host.
+* roofline = bytes the dominant extend kernel reads (SURVEY §8d B_alg, or the
+           streamed + staged bytes of the staged MC kernels) / its
+           CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline = the C++/OpenMP oracle (oracle/liboracle.so) on this host,
+           engine time only, on the oracle's own generator restatement.
+* workloads = sub-records (value, e2e, roofline, parity vs the full-size
+           goldens) of the other BASELINE configs: tc, mc3, mc4, fsm.
+* --impl reference = the oracle port on every host thread (never imports
+           paper_1911_06969_b200); same config keys as this arm.
 Multi-GPU (torchrun): root units split by degree weight, counts all-reduced
 over NCCL; time is the max over ranks.
 """
@@ -144,15 +150,37 @@ def _oracle():
     return pyoracle
 
 
-def cpu_sample(hg, app, k, sigma, budget_s, threads):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_graph(name):
+    """The workload's graph from the oracle's own generator restatement (the
+    reference arm and the CPU baseline never load libgpm.so); TC/CF graphs
+    are oriented here, outside every timed region, as on the GPU path."""
+    O = _oracle()
+    app, k, sigma, rmat, _ = WORKLOADS[name]
+    g = O.generate_rmat(rmat["scale"], rmat["edge_factor"], rmat["a"], rmat["b"], rmat["c"], rmat["seed"],
+                        rmat.get("n_labels", 0), rmat.get("label_seed", 101))
+    gin = O.orient_dag(g) if app in ("tc", "cf") else g
+    return g, gin
+
+
+def cpu_sample(gin, app, k, sigma, budget_s, threads):
     """Chooses a bounded sample of the workload for the CPU oracle: a contiguous
     prefix of level-1 root units grown x4 until it costs >= budget_s/4 (or is
     the whole workload).  Returns (root_hi or None for all, description)."""
     O = _oracle()
-    oc = O.Csr(hg.off, hg.col, hg.labels)
     probe = 1 << 14
     while True:
-        r = O.mine(oc, app, k, sigma, threads=threads, root_lo=0, root_hi=probe)
+        r = O.mine(gin, app, k, sigma, threads=threads, root_lo=0, root_hi=probe)
         if r["level_sizes"][0] < probe:
             return None, "full workload"
         if r["ms"] / 1e3 >= budget_s / 4:
@@ -160,10 +188,91 @@ def cpu_sample(hg, app, k, sigma, budget_s, threads):
         probe *= 4
 
 
-def cpu_run(hg, app, k, sigma, root_hi, threads):
+def cpu_run(gin, app, k, sigma, root_hi, threads):
+    """One oracle mine; its "ms" covers the engine only (CSR copy and, for
+    TC/CF, orientation excluded, like the GPU value)."""
     O = _oracle()
-    oc = O.Csr(hg.off, hg.col, hg.labels)
-    return O.mine(oc, app, k, sigma, threads=threads, root_lo=0, root_hi=root_hi if root_hi else 2**64 - 1)
+    return O.mine(gin, app, k, sigma, threads=threads, root_lo=0, root_hi=root_hi if root_hi else 2**64 - 1)
+
+
+def workload_config(name, n, m, sigma):
+    """`config` of a bench line: identical in both arms for the same workload."""
+    app, k, _, _, desc = WORKLOADS[name]
+    cfg = {"workload": desc, "app": app, "k": k, "n": n, "m_half_edges": m,
+           "generator": "SURVEY §8d RMAT (splitmix64 quadrant draws, seeded permutation, load_edge_list cleaning)",
+           "l2": "flushed between timed steps (256 MiB device write, outside the step events)"}
+    if app == "fsm":
+        cfg["min_support"] = sigma
+    return cfg
+
+
+def golden_parity(name, sigma, result):
+    """Compares a run with tests/golden/configs.json (oracle numbers at full
+    size, tests/golden/make_config_goldens.py); None when no golden exists."""
+    gp = os.path.join(ROOT, "tests", "golden", "configs.json")
+    key = {"cf4": "pat_cf4", "tc": "tc16", "mc3": "lj22_mc3", "mc4": "mc4_mc4"}.get(name)
+    if name == "fsm":
+        key = f"fsm17_s{sigma}"
+    if not key or not os.path.exists(gp):
+        return None
+    with open(gp) as f:
+        gold = json.load(f).get(key)
+    if not gold:
+        return None
+    out = {"golden": f"tests/golden/configs.json[{key}]", "source": gold.get("source")}
+    checks = {"n_explored": result["n_explored"] == gold["n_explored"],
+              "level_sizes": list(result["level_sizes"]) == list(gold["level_sizes"])}
+    if "total" in gold:
+        checks["total"] = result["total"] == gold["total"]
+        out["oracle_total"] = gold["total"]
+    if "patterns_digest" in gold:
+        checks["patterns_sha256"] = result.get("patterns_sha256") == gold["patterns_digest"]["sha256"]
+    elif "patterns" in gold:
+        checks["patterns"] = sorted((int(a), str(b), int(c)) for a, b, c in result["patterns"]) == \
+            sorted((int(a), str(b), int(c)) for a, b, c in gold["patterns"])
+    out["checks"] = checks
+    out["match"] = all(checks.values())
+    return out
+
+
+def reference_arm(args, names):
+    """`--impl reference`: the reference's CPU path = the oracle port
+    (oracle/liboracle.so) on every host thread; the reference itself has no
+    engine code.  Never imports paper_1911_06969_b200."""
+    threads = os.cpu_count() or 1
+    line = None
+    subs = {}
+    for i, name in enumerate(names):
+        app, k, sigma, _, _ = WORKLOADS[name]
+        if i == 0 and args.sigma is not None:
+            sigma = args.sigma
+        g, gin = oracle_graph(name)
+        budget = args.cpu_budget if i == 0 else args.cpu_budget / 4
+        steps, warm = (args.steps, args.warmup) if i == 0 else (2, 1)
+        root_hi, sample = cpu_sample(gin, app, k, sigma, budget, threads)
+        times, r = [], None
+        for j in range(warm + steps):
+            r = cpu_run(gin, app, k, sigma, root_hi, threads)
+            if j >= warm:
+                times.append(r["ms"])
+        ms = sum(times) / len(times)
+        v = r["n_explored"] / (ms / 1e3)
+        cb = {"value": v, "unit": UNIT, "cores": threads, "cpu": cpu_model(), "kind": "port",
+              "sample": sample + "; oracle/liboracle.so (C++/OpenMP restatement of SPEC.md engine), "
+                                 "engine time only (graph orientation outside, as in the GPU value)"}
+        rec = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+               "steps": steps, "warmup": warm, "ms_per_step": ms, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+               "config": workload_config(name, g.n, g.m, sigma), "cpu_baseline": cb,
+               "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+               "result": {"total": r.get("total"), "n_explored": r["n_explored"]}}
+        if i == 0:
+            line = rec
+        else:
+            subs[name] = {k_: rec[k_] for k_ in ("value", "ms_per_step", "config", "cpu_baseline", "result")}
+    if subs:
+        line["workloads"] = subs
+    print(json.dumps(line))
 
 
 def main():
@@ -176,57 +285,24 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU oracle work for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sub", action="store_true",
+                    help="headline workload only (default: the cf4 line also carries tc/mc3/mc4/fsm sub-records)")
     ap.add_argument("--no-steal", action="store_true", help="N>1: static split only (no work-stealing tail)")
     args = ap.parse_args()
     rank, world, local = dist_env()
-    app, k, sigma, rmat, desc = WORKLOADS[args.app]
-    if args.sigma is not None:
-        sigma = args.sigma
-
-    import numpy as np
-    import paper_1911_06969_b200 as P
-
-    t0 = time.time()
-    hg = P.generate_rmat(rmat["scale"], rmat["edge_factor"], rmat["a"], rmat["b"], rmat["c"], rmat["seed"],
-                         rmat.get("n_labels", 0), rmat.get("label_seed", 101))
-    gen_s = time.time() - t0
-    config = {"workload": desc, "app": app, "k": k, "n": hg.n, "m_half_edges": hg.m,
-              "generator": "gpm_generate_rmat (splitmix64, seeded permutation, load_edge_list cleaning)",
-              "l2": "flushed between timed steps (256 MiB device write, outside the step events)"}
-    if app == "fsm":
-        config["min_support"] = sigma
+    names = [args.app]
+    if args.app == "cf4" and not args.no_sub and args.sigma is None:
+        names += ["tc", "mc3", "mc4", "fsm"]
 
     if args.impl == "reference":
-        # reference arm: the CPU implementation of the path (oracle restatement of SPEC.md's
-        # engine; the reference's own engine exists only as spec text) on all host threads.
-        if rank != 0:
-            return
-        threads = os.cpu_count() or 1
-        times = []
-        r = None
-        sample = None
-        root_hi, sample = cpu_sample(hg, app, k, sigma, args.cpu_budget, threads)
-        for i in range(args.warmup + args.steps):
-            t = time.time()
-            r = cpu_run(hg, app, k, sigma, root_hi, threads)
-            if i >= args.warmup:
-                times.append(time.time() - t)
-        ms = 1e3 * sum(times) / len(times)
-        v = r["n_explored"] / (ms / 1e3)
-        print(json.dumps({
-            "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": config,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": sample + "; oracle/liboracle.so (C++/OpenMP restatement of SPEC.md engine)"},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "result": {"total": r.get("total"), "n_explored": r["n_explored"]},
-        }))
+        if rank == 0:
+            reference_arm(args, names)
         return
 
+    import numpy as np
     import torch
     import torch.distributed as dist
+    import paper_1911_06969_b200 as P
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -237,171 +313,217 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---------------- device-resident path (value)
-    g_und = P.Graph(hg, device=local)
-    g_in = g_und.orient_dag() if app in ("tc", "cf") else g_und   # preprocessing
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    kw = dict(rank=rank, world=world, stream=sp, exchange=exchange)
     # N > 1: degree-weighted static split + device-side work-stealing tail
     # over counters peer-mapped from rank 0's GPU (FSM levels exchange anyway)
     steal = None
-    if world > 1 and app != "fsm" and not args.no_steal:
+    if world > 1 and not args.no_steal:
         try:
             from paper_1911_06969_b200.dist import StealCounters
             steal = StealCounters()
         except Exception as e:  # static split only
             print(f"[bench] work stealing disabled: {e!r}", file=sys.stderr)
             steal = None
-    config["partition"] = "degree-weighted static split" + (" + device work-stealing tail" if steal else "")
 
-    def mine_step(g, **extra):
-        skw = {}
-        if steal is not None:
-            steal.reset()
-            skw = dict(steal_ctrs=steal.ptr)
-        return P.mine(g, app, k, sigma, **extra, **skw)
+    def run_workload(name, steps, warmup, cpu_budget, headline):
+        app, k, sigma, rmat, desc = WORKLOADS[name]
+        if headline and args.sigma is not None:
+            sigma = args.sigma
+        use_steal = steal if app != "fsm" else None
+        t0 = time.time()
+        hg = P.generate_rmat(rmat["scale"], rmat["edge_factor"], rmat["a"], rmat["b"], rmat["c"], rmat["seed"],
+                             rmat.get("n_labels", 0), rmat.get("label_seed", 101))
+        gen_s = time.time() - t0
+        config = workload_config(name, hg.n, hg.m, sigma)
+        partition = ("degree-weighted static split" + (" + device work-stealing tail" if use_steal else "")
+                     if world > 1 else "single rank")
 
-    res = None
-    # the sampler starts (and delivers its first line) BEFORE the warm-up, so
-    # the GPU goes straight from the warm-up steps into the timed ones instead
-    # of idling (and dropping clocks) while nvidia-smi comes up
-    clocks = ClockSampler(local, os.environ.get("GPM_BENCH_CLOCK_MS", "100"))
-    clocks.start()
-    clocks.wait_samples(1)
-    for _ in range(args.warmup):
-        res = mine_step(g_in, **kw)
-    barrier()
-    clocks.drain()
-    n_before = len(clocks.lines)
-    step_ms = []
-    dom_ms, dom_b, launches = [], [], 0
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    gc.collect()
-    gc.disable()  # no collector pauses inside the timed host calls (re-enabled after the e2e steps)
-    for _ in range(args.steps):
-        flush.zero_()
-        if steal is not None:
-            steal.reset()
-        ev0.record(stream)
-        res = P.mine(g_in, app, k, sigma, **kw, **({"steal_ctrs": steal.ptr} if steal else {}))
-        ev1.record(stream)
-        ev1.synchronize()
-        step_ms.append(ev0.elapsed_time(ev1))
-        dom_ms.append(res.stats["ms_dominant"])
-        dom_b.append(res.stats["b_dominant"])
-        launches += res.stats["launches"]
-    barrier()
-    # a short timed region may fall between two 100 ms samples: keep the GPU
-    # busy with further (untimed) steps until one sample lands after it began
-    t_extra = time.time()
-    clocks.drain()
-    while len(clocks.lines) <= n_before + 1 and time.time() - t_extra < 3.0:
-        mine_step(g_in, **kw)
-        torch.cuda.synchronize()
-        clocks.drain()
-    clock_rec = clocks.stop(first=n_before)
-    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    ms_per_step = tot.item() / args.steps
-    n_explored = res.stats["n_explored"]   # already summed over ranks by the engine's exchange
-    value = n_explored / (ms_per_step / 1e3)
+        # ---------------- device-resident path (value)
+        g_und = P.Graph(hg, device=local)
+        g_in = g_und.orient_dag() if app in ("tc", "cf") else g_und   # preprocessing
+        kw = dict(rank=rank, world=world, stream=sp, exchange=exchange)
 
-    # ---------------- end-to-end through the public C ABI from pinned host buffers
-    off_p = torch.from_numpy(np.ascontiguousarray(hg.off, dtype=np.uint64).view(np.int64)).pin_memory()
-    col_p = torch.from_numpy(np.ascontiguousarray(hg.col, dtype=np.uint32).view(np.int32)).pin_memory()
-    lab_p = (torch.from_numpy(np.ascontiguousarray(hg.labels, dtype=np.uint32).view(np.int32)).pin_memory()
-             if hg.labels is not None else None)
-    pinned = P.HostGraph(off_p.numpy().view(np.uint64), col_p.numpy().view(np.uint32),
-                         None if lab_p is None else lab_p.numpy().view(np.uint32))
-    h2d = pinned.off.nbytes + pinned.col.nbytes + (0 if lab_p is None else pinned.labels.nbytes)
-    e2e_ms = []
-    er = None
-    ew = max(1, args.warmup)  # untimed e2e warm-up calls (first-touch of pinned pages, caches)
-    for i in range(ew + args.steps):
-        if steal is not None:
-            steal.reset()
+        def mine_step():
+            skw = {}
+            if use_steal is not None:
+                use_steal.reset()
+                skw = dict(steal_ctrs=use_steal.ptr)
+            return P.mine(g_in, app, k, sigma, **kw, **skw)
+
+        res = None
+        # the sampler starts (and delivers its first line) BEFORE the warm-up, so
+        # the GPU goes straight from the warm-up steps into the timed ones instead
+        # of idling (and dropping clocks) while nvidia-smi comes up
+        clocks = ClockSampler(local, os.environ.get("GPM_BENCH_CLOCK_MS", "100"))
+        clocks.start()
+        clocks.wait_samples(1)
+        for _ in range(warmup):
+            res = mine_step()
         barrier()
-        t = time.perf_counter()
-        # TC/CF need the degree-ordered DAG: fused pipelined upload + orientation
-        g = P.Graph(pinned, device=local, orient=app in ("tc", "cf"))
-        er = P.mine(g, app, k, sigma, rank=rank, world=world, exchange=exchange,
-                    **({"steal_ctrs": steal.ptr} if steal else {}))
-        del g
-        torch.cuda.synchronize()
-        if i >= ew:
-            e2e_ms.append(1e3 * (time.perf_counter() - t))
-    gc.enable()
-    et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_ms_step = et.item() / args.steps
-    assert er.stats["n_explored"] == n_explored and er.total == res.total, "e2e result differs from device path"
-    d2h = 8 + 8 * len(er.patterns) + 8 * 16 * 3
+        clocks.drain()
+        n_before = len(clocks.lines)
+        step_ms = []
+        dom_ms, dom_b, dom_mv, launches = [], [], [], 0
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        gc.collect()
+        gc.disable()  # no collector pauses inside the timed host calls (re-enabled after the e2e steps)
+        for _ in range(steps):
+            flush.zero_()
+            if use_steal is not None:
+                use_steal.reset()
+            ev0.record(stream)
+            res = P.mine(g_in, app, k, sigma, **kw, **({"steal_ctrs": use_steal.ptr} if use_steal else {}))
+            ev1.record(stream)
+            ev1.synchronize()
+            step_ms.append(ev0.elapsed_time(ev1))
+            dom_ms.append(res.stats["ms_dominant"])
+            dom_b.append(res.stats["b_dominant"])
+            dom_mv.append(res.stats["b_moved_dominant"])
+            launches += res.stats["launches"]
+        barrier()
+        # a short timed region may fall between two 100 ms samples: keep the GPU
+        # busy with further (untimed) steps until one sample lands after it began
+        t_extra = time.time()
+        clocks.drain()
+        while len(clocks.lines) <= n_before + 1 and time.time() - t_extra < 3.0:
+            mine_step()
+            torch.cuda.synchronize()
+            clocks.drain()
+        clock_rec = clocks.stop(first=n_before)
+        tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        ms_per_step = tot.item() / steps
+        n_explored = res.stats["n_explored"]   # already summed over ranks by the engine's exchange
+        value = n_explored / (ms_per_step / 1e3)
 
-    peak, peak_kind = load_peaks()
-    dms = statistics.median(dom_ms)
-    achieved = (statistics.median(dom_b) / (dms / 1e3) / 1e9) if dms > 0 else 0.0
-    traffic = l2_bytes = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{args.app}.json")
-    # the ncu capture is of the workload's default configuration only
-    if os.path.exists(tp) and (args.sigma is None or args.sigma == WORKLOADS[args.app][2]):
-        with open(tp) as f:
-            tj = json.load(f)
-        traffic = tj.get("dram_bytes_per_launch")
-        l2_bytes = tj.get("l2_bytes_per_launch") or None
-    # measured traffic of one ncu-captured launch over this run's live kernel time:
-    # the DRAM rate, and the L2 rate SURVEY §8d asks for on the L2-resident configs
-    mem_rates = {}
-    if dms > 0:
-        if traffic:
-            mem_rates["dram_gbs"] = traffic / (dms / 1e3) / 1e9
-        if l2_bytes:
-            mem_rates["l2_bytes_per_launch"] = l2_bytes
-            mem_rates["l2_gbs"] = l2_bytes / (dms / 1e3) / 1e9
+        # ---------------- end-to-end through the public C ABI from pinned host buffers
+        off_p = torch.from_numpy(np.ascontiguousarray(hg.off, dtype=np.uint64).view(np.int64)).pin_memory()
+        col_p = torch.from_numpy(np.ascontiguousarray(hg.col, dtype=np.uint32).view(np.int32)).pin_memory()
+        lab_p = (torch.from_numpy(np.ascontiguousarray(hg.labels, dtype=np.uint32).view(np.int32)).pin_memory()
+                 if hg.labels is not None else None)
+        pinned = P.HostGraph(off_p.numpy().view(np.uint64), col_p.numpy().view(np.uint32),
+                             None if lab_p is None else lab_p.numpy().view(np.uint32))
+        h2d = pinned.off.nbytes + pinned.col.nbytes + (0 if lab_p is None else pinned.labels.nbytes)
+        e2e_ms = []
+        er = None
+        ew = max(1, warmup)  # untimed e2e warm-up calls (first-touch of pinned pages, caches)
+        for i in range(ew + steps):
+            if use_steal is not None:
+                use_steal.reset()
+            barrier()
+            t = time.perf_counter()
+            # TC/CF need the degree-ordered DAG: fused pipelined upload + orientation
+            g = P.Graph(pinned, device=local, orient=app in ("tc", "cf"))
+            er = P.mine(g, app, k, sigma, rank=rank, world=world, exchange=exchange,
+                        **({"steal_ctrs": use_steal.ptr} if use_steal else {}))
+            del g
+            torch.cuda.synchronize()
+            if i >= ew:
+                e2e_ms.append(1e3 * (time.perf_counter() - t))
+        gc.enable()
+        et = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_ms_step = et.item() / steps
+        assert er.stats["n_explored"] == n_explored and er.total == res.total, "e2e result differs from device path"
+        d2h = 8 + 8 * len(er.patterns) + 8 * 16 * 3
 
-    out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": config,
-        "e2e": {"value": n_explored / (e2e_ms_step / 1e3), "unit": UNIT, "ms_per_step": e2e_ms_step,
-                "step_ms": [round(x, 3) for x in e2e_ms],
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": res.stats["dominant"],
-                     "kernel_ms": dms, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                     "bytes": "SURVEY §8d B_alg of that kernel: 8*l per parent + (16 + 4*deg) per extended position",
-                     "note": ("B_alg counts 4 B for every candidate of every position; staged source "
-                              "lists are read on chip once per root/group, and L2-resident CSRs are "
-                              "re-read from L2, so B_alg/t can exceed the HBM copy rate. traffic = ncu "
-                              "dram bytes of one captured launch (profiles/traffic_<app>.json)"),
-                     **mem_rates},
-        "step_ms": [round(x, 4) for x in step_ms],
-        # SURVEY §8d asks for best and median as well as the mean (`ms_per_step`)
-        "step_stats": {"best_ms": min(step_ms), "median_ms": statistics.median(step_ms),
-                       "e2e_best_ms": min(e2e_ms), "e2e_median_ms": statistics.median(e2e_ms)},
-        "gpu_launches": launches,
-        "clocks": clock_rec,
-        "result": {"total": res.total, "n_explored": n_explored, "level_sizes": res.stats["level_sizes"],
-                   "candidates": res.stats["candidates"], "patterns": len(res.patterns)},
-        "gen_s": round(gen_s, 2),
-    }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        root_hi, sample = cpu_sample(hg, app, k, sigma, args.cpu_budget, threads)
-        r = cpu_run(hg, app, k, sigma, root_hi, threads)
-        out["cpu_baseline"] = {"value": r["n_explored"] / (r["ms"] / 1e3), "unit": UNIT, "cores": threads,
-                               "kind": "port", "sample": sample + " (oracle/liboracle.so, OpenMP)"}
+        peak, peak_kind = load_peaks()
+        dms = statistics.median(dom_ms)
+        b_alg = statistics.median(dom_b)
+        b_mv = statistics.median(dom_mv)
+        achieved = (b_mv / (dms / 1e3) / 1e9) if dms > 0 else 0.0
+        traffic = l2_bytes = None
+        tp = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
+        # the ncu capture is of the workload's default configuration only
+        if os.path.exists(tp) and sigma == WORKLOADS[name][2]:
+            with open(tp) as f:
+                tj = json.load(f)
+            traffic = tj.get("dram_bytes_per_launch")
+            l2_bytes = tj.get("l2_bytes_per_launch") or None
+        # measured traffic of one ncu-captured launch over this run's live kernel time:
+        # the DRAM rate, and the L2 rate SURVEY §8d asks for on the L2-resident configs
+        mem_rates = {}
+        if dms > 0:
+            mem_rates["b_alg_survey"] = b_alg
+            mem_rates["b_alg_survey_gbs"] = b_alg / (dms / 1e3) / 1e9
+            if traffic:
+                mem_rates["dram_gbs"] = traffic / (dms / 1e3) / 1e9
+                mem_rates["dram_frac"] = mem_rates["dram_gbs"] / peak
+            if l2_bytes:
+                mem_rates["l2_bytes_per_launch"] = l2_bytes
+                mem_rates["l2_gbs"] = l2_bytes / (dms / 1e3) / 1e9
+        pats = res.patterns
+        result = {"total": res.total, "n_explored": n_explored, "level_sizes": res.stats["level_sizes"],
+                  "candidates": res.stats["candidates"], "patterns": len(pats),
+                  "n_counted": res.stats["n_counted"]}
+        pres = dict(result, patterns=pats)
+        if app == "fsm":
+            import hashlib
+            rows = sorted((int(l), str(t), int(s_)) for l, t, s_ in pats)
+            pres["patterns_sha256"] = hashlib.sha256(
+                "".join(f"{l}\t{t}\t{s_}\n" for l, t, s_ in rows).encode()).hexdigest()
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": config, "partition": partition,
+            "e2e": {"value": n_explored / (e2e_ms_step / 1e3), "unit": UNIT, "ms_per_step": e2e_ms_step,
+                    "step_ms": [round(x, 3) for x in e2e_ms],
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": res.stats["dominant"],
+                         "kernel_ms": dms, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                         "bytes": ("bytes the dominant kernel reads per launch (b_moved): SURVEY §8d B_alg "
+                                   "(8*l per parent + (16 + 4*deg) per extended position) except for the "
+                                   "staged MC kernels, whose reads are the streamed suffixes + staged sets "
+                                   "(DESIGN.md §5); b_alg_survey keeps the per-candidate figure"),
+                         "note": ("traffic = ncu dram bytes of one captured launch "
+                                  "(profiles/traffic_<app>.json); L2-resident CSRs (cf4, tc, fsm) are "
+                                  "re-read from L2, so their b_moved/t can exceed the HBM rate"),
+                         **mem_rates},
+            "step_ms": [round(x, 4) for x in step_ms],
+            # SURVEY §8d asks for best and median as well as the mean (`ms_per_step`)
+            "step_stats": {"best_ms": min(step_ms), "median_ms": statistics.median(step_ms),
+                           "e2e_best_ms": min(e2e_ms), "e2e_median_ms": statistics.median(e2e_ms)},
+            "gpu_launches": launches,
+            "clocks": clock_rec,
+            "result": result,
+            "parity": golden_parity(name, sigma, pres),
+            "gen_s": round(gen_s, 2),
+        }
+        del g_in, g_und
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            _, gin = oracle_graph(name)
+            root_hi, sample = cpu_sample(gin, app, k, sigma, cpu_budget, threads)
+            r = cpu_run(gin, app, k, sigma, root_hi, threads)
+            out["cpu_baseline"] = {"value": r["n_explored"] / (r["ms"] / 1e3), "unit": UNIT, "cores": threads,
+                                   "cpu": cpu_model(), "kind": "port",
+                                   "sample": sample + " (oracle/liboracle.so, OpenMP; engine time only)"}
+        return out
+
+    line = run_workload(names[0], args.steps, args.warmup, args.cpu_budget, True)
+    subs = {}
+    for name in names[1:]:
+        sub = run_workload(name, args.steps, args.warmup, args.cpu_budget / 4, False)
+        subs[name] = {k_: sub[k_] for k_ in ("value", "ms_per_step", "config", "e2e", "roofline", "step_stats",
+                                              "gpu_launches", "clocks", "result", "parity", "cpu_baseline")
+                      if k_ in sub}
+        line["gpu_launches"] += sub["gpu_launches"]
+    if subs:
+        line["workloads"] = subs
+        line["gpu_launches_note"] = "gpu_launches sums the headline and the sub-record workloads"
     if rank == 0:
-        print(json.dumps(out))
+        print(json.dumps(line))
     if steal is not None:
         steal.close()
     if world > 1:

@@ -169,7 +169,29 @@ typedef struct gpm_stats {
   uint64_t launches;        /* kernels launched by this gpm_mine call            */
   uint64_t chunks;          /* planner chunks used                               */
   char dominant[64];        /* name of the dominant kernel                       */
+  double b_moved_dominant;  /* bytes the dominant kernel actually reads (staged MC
+                               kernels read staged sets once per root/group and
+                               never stream pos-0 candidates; = b_dominant else) */
+  uint64_t n_counted;       /* accepted embeddings whose class was derived from a
+                               count/rank (staged MC pos-0), not a per-candidate
+                               read; included in n_explored                        */
+  uint32_t paths;           /* GPM_PATH_* bits: which kernel paths ran (tests)     */
 } gpm_stats;
+
+/* gpm_stats.paths bits */
+enum {
+  GPM_PATH_GENERIC = 1u << 0,          /* generic inspection-execution extend     */
+  GPM_PATH_CF_EDGE_CHUNK = 1u << 1,    /* TC/CF first extension, edge-chunk kernel */
+  GPM_PATH_CF_SIBLINGS = 1u << 2,      /* CF last level over sibling groups        */
+  GPM_PATH_MC3_WARP = 1u << 3,         /* 3-MC staged, per-warp root sets          */
+  GPM_PATH_MC3_BLOCK = 1u << 4,        /* 3-MC staged, per-CTA root tiles          */
+  GPM_PATH_MC3_MULTITILE = 1u << 5,    /* ... a root needed more than one tile     */
+  GPM_PATH_MC4_STAGED = 1u << 6,       /* 4-MC staged last level                   */
+  GPM_PATH_MC4_HBM_SETS = 1u << 7,     /* ... |S0|+|S1| beyond the on-chip set     */
+  GPM_PATH_PLANNER_CHUNKS = 1u << 8,   /* a level was split by the memory planner  */
+  GPM_PATH_FSM_ROUNDS = 1u << 9,       /* FSM domain bitmaps in several rounds     */
+  GPM_PATH_FSM_FUSED_LAST = 1u << 10   /* FSM last level: domain pass fused        */
+};
 int gpm_result_stats(const gpm_result* r, gpm_stats* out);
 
 void gpm_result_free(gpm_result* r);

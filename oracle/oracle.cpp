@@ -34,6 +34,7 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -978,6 +979,112 @@ int oracle_orient_dag(const std::uint64_t* off, const std::uint32_t* col, std::u
 }
 
 void oracle_free_buf(void* p) { std::free(p); }
+
+// SURVEY.md §8d synthetic input, restated independently of the product's
+// generator so the reference arm of bench.py and the golden scripts never
+// load libgpm.so: splitmix64 quadrant draws per (edge, bit), a seeded
+// Fisher-Yates permutation of [0, 2^scale), self-loops dropped, then
+// graph_io.hpp:83-116 cleaning (ids compacted ascending, symmetrised,
+// deduplicated, ascending lists) done here by sorting packed (u, v) keys.
+// Labels: uniform in [0, n_labels) per dense vertex.  Caller frees the
+// three buffers with oracle_free_buf.
+int oracle_generate_rmat(int scale, double ef, double a, double b, double c, std::uint64_t seed,
+                         std::uint32_t n_labels, std::uint64_t label_seed, std::uint64_t** out_off,
+                         std::uint32_t** out_col, std::uint32_t** out_lab, std::uint32_t* out_n,
+                         std::uint64_t* out_m) {
+  using orc::u32;
+  using orc::u64;
+  try {
+    auto sm = [](u64 x) {
+      x += 0x9E3779B97F4A7C15ull;
+      x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+      x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+      return x ^ (x >> 31);
+    };
+    if (scale < 1 || scale > 31) return 1;
+    const u64 N = u64(1) << scale;
+    const u64 m0 = (u64)std::llround(ef * (double)N);
+    std::vector<u64> perm(N);
+    std::iota(perm.begin(), perm.end(), u64(0));
+    u64 st = sm(seed ^ 0x5EEDC0FFEEull);
+    for (u64 i = N - 1; i > 0; --i) {
+      st = sm(st);
+      std::swap(perm[i], perm[st % (i + 1)]);
+    }
+    // packed undirected pairs (both directions), self-loops dropped
+    std::vector<u64> keys(2 * m0);
+    std::vector<unsigned char> keep(m0);
+#pragma omp parallel for schedule(static)
+    for (long long ii = 0; ii < (long long)m0; ++ii) {
+      u64 x = sm(seed ^ sm((u64)ii + 1)), u = 0, v = 0;
+      for (int bit = 0; bit < scale; ++bit) {
+        x = sm(x);
+        const double r = (double)(x >> 11) * (1.0 / 9007199254740992.0);
+        const int q = r < a ? 0 : r < a + b ? 1 : r < a + b + c ? 2 : 3;
+        u = (u << 1) | (u64)(q >> 1);
+        v = (v << 1) | (u64)(q & 1);
+      }
+      u = perm[u];
+      v = perm[v];
+      keep[ii] = u != v;
+      keys[2 * ii] = (u << 32) | v;
+      keys[2 * ii + 1] = (v << 32) | u;
+    }
+    u64 w = 0;
+    for (u64 i = 0; i < m0; ++i)
+      if (keep[i]) {
+        keys[w++] = keys[2 * i];
+        keys[w++] = keys[2 * i + 1];
+      }
+    keys.resize(w);
+    if (keys.empty()) return 1;
+    // dense ids = rank among the ids that occur (ascending)
+    std::vector<unsigned char> seen(N, 0);
+    for (u64 k : keys) seen[k >> 32] = 1;
+    std::vector<u32> dense(N, 0);
+    u32 n = 0;
+    for (u64 x = 0; x < N; ++x)
+      if (seen[x]) dense[x] = n++;
+#pragma omp parallel for schedule(static)
+    for (long long i = 0; i < (long long)keys.size(); ++i)
+      keys[i] = ((u64)dense[keys[i] >> 32] << 32) | dense[keys[i] & 0xffffffffull];
+    // sort: per-thread std::sort of contiguous blocks, then pairwise merges
+    {
+      const int T = std::max(1, omp_get_max_threads());
+      std::vector<size_t> cut(T + 1);
+      for (int t = 0; t <= T; ++t) cut[t] = keys.size() * (size_t)t / (size_t)T;
+#pragma omp parallel for schedule(static, 1)
+      for (int t = 0; t < T; ++t) std::sort(keys.begin() + cut[t], keys.begin() + cut[t + 1]);
+      for (int width = 1; width < T; width *= 2) {
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int t = 0; t < T; t += 2 * width) {
+          if (t + width >= T) continue;
+          std::inplace_merge(keys.begin() + cut[t], keys.begin() + cut[t + width],
+                             keys.begin() + cut[std::min(T, t + 2 * width)]);
+        }
+      }
+    }
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    u64* off = (u64*)std::calloc(n + 1, sizeof(u64));
+    u32* col = (u32*)std::malloc(sizeof(u32) * keys.size());
+    u32* lab = n_labels ? (u32*)std::malloc(sizeof(u32) * std::max<u32>(1, n)) : nullptr;
+    if (!off || !col || (n_labels && !lab)) return 1;
+    for (size_t i = 0; i < keys.size(); ++i) {
+      ++off[(keys[i] >> 32) + 1];
+      col[i] = (u32)(keys[i] & 0xffffffffull);
+    }
+    for (u32 v = 0; v < n; ++v) off[v + 1] += off[v];
+    for (u32 v = 0; n_labels && v < n; ++v) lab[v] = (u32)(sm(label_seed ^ sm((u64)v + 0x1234567ull)) % n_labels);
+    *out_off = off;
+    *out_col = col;
+    *out_lab = lab;
+    *out_n = n;
+    *out_m = keys.size();
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
 
 // canonicalize restatement exposed for tests: returns "text|p0,p1,..."
 char* oracle_canonicalize(int nv, const std::uint32_t* labels, int ne, const int* edges) {

@@ -44,6 +44,9 @@ def lib():
         L.oracle_orient_dag.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64,
                                         C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]
         L.oracle_free_buf.argtypes = [C.c_void_p]
+        L.oracle_generate_rmat.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                           C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                           C.POINTER(C.c_void_p), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)]
         _lib = L
     return _lib
 
@@ -165,6 +168,25 @@ def orient_dag(g: Csr) -> Csr:
     L.oracle_free_buf(oo)
     L.oracle_free_buf(oc)
     return Csr(o, c, g.labels, True)
+
+
+def generate_rmat(scale: int, edge_factor: float, a: float, b: float, c: float, seed: int = 1,
+                  n_labels: int = 0, label_seed: int = 101) -> Csr:
+    """SURVEY §8d synthetic graph, restated in oracle.cpp (no libgpm.so)."""
+    L = lib()
+    po, pc, pl = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    n, m = C.c_uint32(), C.c_uint64()
+    if L.oracle_generate_rmat(scale, edge_factor, a, b, c, seed, n_labels, label_seed, C.byref(po), C.byref(pc),
+                              C.byref(pl), C.byref(n), C.byref(m)) != 0:
+        raise RuntimeError("oracle_generate_rmat failed")
+    off = np.ctypeslib.as_array(C.cast(po, C.POINTER(C.c_uint64)), shape=(n.value + 1,)).copy()
+    col = np.ctypeslib.as_array(C.cast(pc, C.POINTER(C.c_uint32)), shape=(m.value,)).copy()
+    lab = (np.ctypeslib.as_array(C.cast(pl, C.POINTER(C.c_uint32)), shape=(n.value,)).copy()
+           if pl.value else None)
+    for p_ in (po, pc, pl):
+        if p_.value:
+            L.oracle_free_buf(p_)
+    return Csr(off, col, lab)
 
 
 def _take_ref_csr(r: _RefCsr, oriented=False) -> Csr:

@@ -39,12 +39,19 @@ class Config(C.Structure):
                 ("list_fn", LIST_FN), ("list_ctx", C.c_void_p)]
 
 
+# gpm_stats.paths bits (include/gpm.h)
+PATH_GENERIC, PATH_CF_EDGE_CHUNK, PATH_CF_SIBLINGS, PATH_MC3_WARP, PATH_MC3_BLOCK, PATH_MC3_MULTITILE, \
+    PATH_MC4_STAGED, PATH_MC4_HBM_SETS, PATH_PLANNER_CHUNKS, PATH_FSM_ROUNDS, PATH_FSM_FUSED_LAST = \
+    (1 << i for i in range(11))
+
+
 class Stats(C.Structure):
     _fields_ = [("n_levels", C.c_int), ("level_sizes", C.c_uint64 * 16), ("candidates", C.c_uint64 * 16),
                 ("survivors", C.c_uint64 * 16), ("n_explored", C.c_uint64), ("b_alg", C.c_double),
                 ("ms_total", C.c_double), ("ms_extend", C.c_double), ("ms_dominant", C.c_double),
                 ("b_dominant", C.c_double), ("launches", C.c_uint64), ("chunks", C.c_uint64),
-                ("dominant", C.c_char * 64)]
+                ("dominant", C.c_char * 64), ("b_moved_dominant", C.c_double), ("n_counted", C.c_uint64),
+                ("paths", C.c_uint32)]
 
 
 class CsrStruct(C.Structure):

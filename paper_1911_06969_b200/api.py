@@ -274,7 +274,8 @@ def mine(g: Graph, app: str, k: int = 3, min_support: int = 0, **kw) -> MineResu
                      survivors=list(st.survivors[:nl]), n_explored=st.n_explored, b_alg=st.b_alg,
                      ms_total=st.ms_total, ms_extend=st.ms_extend, ms_dominant=st.ms_dominant,
                      b_dominant=st.b_dominant, launches=st.launches, chunks=st.chunks,
-                     dominant=st.dominant.decode())
+                     dominant=st.dominant.decode(), b_moved_dominant=st.b_moved_dominant,
+                     n_counted=st.n_counted, paths=st.paths)
     except Exception:
         L.gpm_result_free(r)
         raise

@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <array>
 #include <map>
 #include <memory>
 
@@ -75,6 +76,22 @@ void exchange_sum_host(const gpm_config& cfg, std::vector<u64>& v, cudaStream_t 
   GPM_CUDA(cudaStreamSynchronize(s));
 }
 
+// Minimum of a host u64 across ranks (all-gather, op 2): planner sizes that
+// decide how many collectives a level issues must agree on every rank.
+u64 exchange_min_host(const gpm_config& cfg, u64 v, cudaStream_t s) {
+  if (cfg.world <= 1 || !cfg.exchange) return v;
+  const int W = cfg.world;
+  std::vector<u64> h(W, ~0ull);
+  h[cfg.rank] = v;
+  DBuf<u64> d(W, s);
+  GPM_CUDA(cudaMemcpyAsync(d.get(), h.data(), sizeof(u64) * W, cudaMemcpyHostToDevice, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  if (cfg.exchange(cfg.exchange_ctx, d.get(), 1, 8, 2, s) != 0) throw Error(GPM_ENCCL, "exchange(all-gather) failed");
+  GPM_CUDA(cudaMemcpyAsync(h.data(), d.get(), sizeof(u64) * W, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  return *std::min_element(h.begin(), h.end());
+}
+
 void exchange_device(const gpm_config& cfg, void* dev, u64 count, int elem_bytes, int op, cudaStream_t s) {
   if (cfg.world <= 1 || !cfg.exchange || count == 0) return;
   GPM_CUDA(cudaStreamSynchronize(s));
@@ -102,6 +119,7 @@ int gpm_release_cached(int device) {
       GPM_CUDA(cudaSetDevice(d));
       big_cache().trim(d);
     }
+    mem_generation().fetch_add(1, std::memory_order_relaxed);
     GPM_CUDA(cudaSetDevice(cur));
   });
 }
@@ -166,16 +184,47 @@ int gpm_steal_release(void* dev_ptr, int opened) {
   });
 }
 
+static int gpm_mine_once(const gpm_graph* g, const gpm_config* cfg, gpm_result** out);
+
 int gpm_mine(const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
   if (!g || !cfg || !out) {
     set_last_error("gpm_mine: null argument");
     return GPM_EINVAL;
   }
+  int rc = gpm_mine_once(g, cfg, out);
+  // The planner sizes levels from a cached free-memory reading; memory the
+  // caller allocated since (e.g. torch tensors) can make a level allocation
+  // fail.  Re-plan once from a fresh reading with the library's cached
+  // blocks handed back -- unless other ranks already entered collectives
+  // (FSM exchanges per level) or stolen chunks would be lost.
+  const bool solo = cfg->world <= 1 || !cfg->exchange;
+  if (rc == GPM_ENOMEM && !cfg->steal_ctrs && (solo || cfg->app != GPM_APP_FSM)) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    big_cache().trim(dev);
+    mem_generation().fetch_add(1, std::memory_order_relaxed);
+    rc = gpm_mine_once(g, cfg, out);
+  }
+  return rc;
+}
+
+static int gpm_mine_once(const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
   *out = nullptr;
   return guarded([&] {
     if (cfg->app < GPM_APP_TC || cfg->app > GPM_APP_FSM) throw Error(GPM_EINVAL, "unknown app");
+    // config conflicts ("chunking + filter -> error"): the FSM
+    // filter needs every root's embeddings before the next extend, so a
+    // root slice is only legal as one rank's share of an exchanged job;
+    // listing is a TC/CF mode; stealing only applies to the count apps
     if (cfg->list_fn && cfg->app != GPM_APP_TC && cfg->app != GPM_APP_CF)
-      throw Error(GPM_EINVAL, "listing mode: TC/CF only (SPEC.md:458)");
+      throw Error(GPM_ECONFIG, "listing mode: TC/CF only (SPEC.md:458)");
+    if (cfg->app == GPM_APP_FSM && cfg->root_hi > 0 && !(cfg->world > 1 && cfg->exchange))
+      throw Error(GPM_ECONFIG, "fsm: a root slice without a cross-rank exchange would filter on partial supports "
+                               "(SPEC.md:160, :375)");
+    if (cfg->app == GPM_APP_FSM && cfg->steal_ctrs)
+      throw Error(GPM_ECONFIG, "fsm: work stealing conflicts with the per-level exchange (static split only)");
+    if (cfg->steal_ctrs && cfg->root_hi > 0)
+      throw Error(GPM_ECONFIG, "steal_ctrs and an explicit root slice are mutually exclusive");
     if (cfg->world < 0 || (cfg->world > 1 && (cfg->rank < 0 || cfg->rank >= cfg->world)))
       throw Error(GPM_EINVAL, "bad rank/world");
     GPM_CUDA(cudaSetDevice(g->device));
@@ -219,23 +268,27 @@ int gpm_mine(const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
     S.ms_total = ms;
     S.launches = tl.launches;
     S.chunks = st.chunks;
-    std::map<std::string, std::pair<double, double>> per;  // name -> (ms, bytes)
+    S.n_counted = st.counted;
+    S.paths = st.paths | (st.chunks ? (u32)GPM_PATH_PLANNER_CHUNKS : 0u);
+    std::map<std::string, std::array<double, 3>> per;  // name -> (ms, bytes, moved)
     static const bool trace = std::getenv("GPM_TRACE") != nullptr;
     if (trace) std::fprintf(stderr, "[gpm] mine app=%d k=%d total %.3f ms, %zu timed launches\n", cfg->app, cfg->k, ms, tl.recs.size());
     for (auto& r : tl.recs) {
       float t = 0;
       GPM_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
       if (trace) std::fprintf(stderr, "[gpm]   %-28s %10.3f ms  %12.4g B_alg\n", r.name.c_str(), t, r.bytes);
-      per[r.name].first += t;
-      per[r.name].second += r.bytes;
+      per[r.name][0] += t;
+      per[r.name][1] += r.bytes;
+      per[r.name][2] += r.moved >= 0 ? r.moved : r.bytes;
       S.ms_extend += t;
     }
     double best = -1;
     for (auto& [name, v] : per)
-      if (v.first > best) {
-        best = v.first;
-        S.ms_dominant = v.first;
-        S.b_dominant = v.second;
+      if (v[0] > best) {
+        best = v[0];
+        S.ms_dominant = v[0];
+        S.b_dominant = v[1];
+        S.b_moved_dominant = v[2];
         std::snprintf(S.dominant, sizeof S.dominant, "%s", name.c_str());
       }
     *out = res.release();

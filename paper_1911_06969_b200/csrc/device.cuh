@@ -1,9 +1,11 @@
 // device.cuh — device-side graph view, connectivity probes, memory + launch
 // helpers shared by the engine translation units.
 #pragma once
+#include <atomic>
 #include <mutex>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -168,6 +170,23 @@ __device__ __forceinline__ u32 lanemask_lt() {
 // 0.44 s 4-MC step, GPM_TRACE); cached blocks never go back to the driver
 // unless an allocation fails.  A released block carries an event recorded on
 // the releasing stream; the next owner's stream waits on it.
+// Bumped when the library hands memory back to the driver outside a mine
+// call (gpm_release_cached) or after an allocation failure: invalidates the
+// cached free-memory readings of device_free_bytes().
+inline std::atomic<unsigned>& mem_generation() {
+  static std::atomic<unsigned> g{0};
+  return g;
+}
+// Running balance of the library's own >= 64 MiB allocations per device
+// (BigCache blocks handed out: -bytes, handed back: +bytes).  A cached
+// free-memory reading is corrected by the change of this balance since it
+// was taken, so graphs created or freed between two calls are accounted
+// without another cudaMemGetInfo.
+inline std::atomic<long long>& lib_delta(int dev) {
+  static std::atomic<long long> d[64];
+  return d[dev & 63];
+}
+
 constexpr size_t kBigAlloc = size_t(64) << 20;
 inline size_t big_size_class(size_t bytes) {
   size_t p = size_t(1) << (63 - __builtin_clzll((unsigned long long)bytes));
@@ -221,6 +240,7 @@ inline void* big_alloc(size_t bytes, int dev, cudaStream_t st) {
         C.free_.pop_back();
         cudaStreamWaitEvent(st, b.ev, 0);
         cudaEventDestroy(b.ev);
+        lib_delta(dev).fetch_sub((long long)cls, std::memory_order_relaxed);
         return b.p;
       }
     }
@@ -237,9 +257,11 @@ inline void* big_alloc(size_t bytes, int dev, cudaStream_t st) {
     cudaGetLastError();
     if (cudaMalloc(&p, cls) != cudaSuccess) {
       cudaGetLastError();
+      mem_generation().fetch_add(1, std::memory_order_relaxed);
       return nullptr;
     }
   }
+  lib_delta(dev).fetch_sub((long long)cls, std::memory_order_relaxed);
   return p;
 }
 inline void big_release(void* p, size_t bytes, int dev, cudaStream_t st) {
@@ -249,11 +271,13 @@ inline void big_release(void* p, size_t bytes, int dev, cudaStream_t st) {
     cudaStreamSynchronize(st);
     if (ev) cudaEventDestroy(ev);
     cudaFree(p);
+    lib_delta(dev).fetch_add((long long)big_size_class(bytes), std::memory_order_relaxed);
     return;
   }
   BigCache& C = big_cache();
   std::lock_guard<std::mutex> lk(C.mu);
   C.free_.push_back({p, big_size_class(bytes), dev, ev});
+  lib_delta(dev).fetch_add((long long)big_size_class(bytes), std::memory_order_relaxed);
 }
 
 // Raw allocations outside DBuf (graph CSR arrays): same policy as DBuf.
@@ -345,6 +369,7 @@ struct Timeline {
     std::string name;
     cudaEvent_t a, b;
     double bytes;
+    double moved = -1;  // bytes the kernel actually reads when they differ from B_alg (< 0: = bytes)
   };
   cudaStream_t s;
   std::vector<Rec> recs;
@@ -357,7 +382,7 @@ struct Timeline {
     }
   }
   size_t begin(const std::string& name, double bytes) {
-    Rec r{name, nullptr, nullptr, bytes};
+    Rec r{name, nullptr, nullptr, bytes, -1};
     GPM_CUDA(cudaEventCreate(&r.a));
     GPM_CUDA(cudaEventCreate(&r.b));
     GPM_CUDA(cudaEventRecord(r.a, s));
@@ -379,6 +404,18 @@ inline void htrace(cudaStream_t s, const char* what) {
   t0 = t1;
 }
 
+// Occupancy (blocks per SM) of a kernel, computed once per cache slot; the
+// slots are shared by every thread that runs the engine.
+template <class F>
+inline int cached_occupancy(std::atomic<int>& slot, F&& compute) {
+  int v = slot.load(std::memory_order_acquire);
+  if (v == 0) {
+    v = std::max(1, compute());
+    slot.store(v, std::memory_order_release);
+  }
+  return v;
+}
+
 // Device bytes available to the engine: free memory plus what the stream-
 // ordered pool holds reserved but unused (the pool keeps released blocks,
 // keep_pool_warm), so the planner's budget does not shrink from call to call.
@@ -391,12 +428,19 @@ inline size_t device_free_bytes() {
   cudaGetDevice(&dev);
   struct Cached {
     int dev = -1;
+    unsigned gen = 0;
+    long long delta = 0;
     size_t bytes = 0;
     std::chrono::steady_clock::time_point at;
   };
   static thread_local Cached cache;
   const auto now = std::chrono::steady_clock::now();
-  if (cache.dev == dev && now - cache.at < std::chrono::milliseconds(2000)) return cache.bytes;
+  const unsigned gen = mem_generation().load(std::memory_order_relaxed);
+  const long long delta = lib_delta(dev).load(std::memory_order_relaxed);
+  if (cache.dev == dev && cache.gen == gen && now - cache.at < std::chrono::milliseconds(2000)) {
+    const long long v = (long long)cache.bytes + (delta - cache.delta);
+    return v > 0 ? (size_t)v : 0;
+  }
   size_t freeb = 0, totalb = 0;
   GPM_CUDA(cudaMemGetInfo(&freeb, &totalb));
   cudaMemPool_t pool;
@@ -409,6 +453,8 @@ inline size_t device_free_bytes() {
   freeb += big_cache().cached(dev);
   cudaGetLastError();
   cache.dev = dev;
+  cache.gen = gen;
+  cache.delta = delta;
   cache.bytes = freeb;
   cache.at = now;
   return freeb;

@@ -56,7 +56,11 @@ namespace gpm {
 struct Stats {
   std::vector<u64> level_sizes, candidates, survivors;
   double balg = 0;
+  double bmoved = 0;   // bytes read by kernels whose reads differ from B_alg (staged MC)
+  u64 streamed = 0;    // of which: neighbour-list entries read one by one
+  u64 counted = 0;     // accepted embeddings whose class came from a rank/count, not a per-candidate read
   u64 chunks = 0;
+  u32 paths = 0;       // GPM_PATH_* bits
   void ensure(size_t L) {
     if (level_sizes.size() < L) level_sizes.resize(L, 0);
     if (candidates.size() < L) candidates.resize(L, 0);
@@ -106,6 +110,7 @@ void mine_fsm(const gpm_graph& g, const gpm_config& cfg, cudaStream_t s, gpm_res
 // exchange a device buffer in place through gpm_config.exchange.
 void exchange_sum_host(const gpm_config& cfg, std::vector<u64>& v, cudaStream_t s);
 void exchange_device(const gpm_config& cfg, void* dev, u64 count, int elem_bytes, int op, cudaStream_t s);
+u64 exchange_min_host(const gpm_config& cfg, u64 v, cudaStream_t s);
 
 // Canonical pattern text from a packed canonical key (pattern.cuh).
 std::string canon_text(u64 key, int nv, int label_bits, const std::vector<u32>* label_values);

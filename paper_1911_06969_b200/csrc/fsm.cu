@@ -871,6 +871,7 @@ struct Fsm {
     const u64 per_round = std::max<u64>(1, std::min<u64>(R.NB, budget / 2 / std::max<u64>(1, per_pat)));
     DBuf<unsigned long long> mni(std::max<u64>(1, R.P), s);
     GPM_CUDA(cudaMemsetAsync(mni.get(), 0, sizeof(unsigned long long) * std::max<u64>(1, R.P), s));
+    if (per_round < R.NB) st.paths |= GPM_PATH_FSM_ROUNDS;
     if (R.NB) {
       DBuf<u32> bm(per_round * kpos * words, s);
       for (u64 lo = 0; lo < R.NB; lo += per_round) {
@@ -1102,6 +1103,7 @@ struct Fsm {
       cap <<= 3;
     }
     const bool fused = qcap && d2h(qover.get()) == 0;
+    if (fused) st.paths |= GPM_PATH_FSM_FUSED_LAST;
     if (!fused) qbm.release();  // more quick codes than bitmaps: separate domain pass
     trace(fused ? "pass A fused (qcap, ids)" : "pass A unfused (qcap, ids)", (double)qcap, (double)d2h(R.used.get()));
     u64 acc = d2h(accepted.get());
@@ -1176,10 +1178,11 @@ struct Fsm {
     if (k * LB + pat::npairs(k) > 61)
       throw Error(GPM_EINVAL, "fsm: too many distinct labels for a packed pattern code at this k");
     sms = sm_count();
-    size_t freeb = 0, totalb = 0;
-    freeb = device_free_bytes();
-    (void)totalb;
+    const size_t freeb = device_free_bytes();
     budget = cfg.mem_budget ? cfg.mem_budget : (u64)(0.5 * (double)freeb);
+    // the bitmap rounds (one OR collective each) and the fused/two-pass
+    // choice follow from the budget: every rank must plan with the same one
+    budget = exchange_min_host(cfg, budget, s);
     d_ctr.alloc(1, s);
     label_ranks();
     const int levels = k - 1;

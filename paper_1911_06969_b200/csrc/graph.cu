@@ -443,14 +443,23 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
   GPM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   struct StreamGuard {
     cudaStream_t x;
-    ~StreamGuard() { cudaStreamSynchronize(x); cudaStreamDestroy(x); }
-  } guard{cs};
+    ~StreamGuard() {
+      if (!x) return;
+      cudaStreamSynchronize(x);
+      cudaStreamDestroy(x);
+    }
+  };
+  StreamGuard early{cs};  // owns cs until the buffers below exist
   DBuf<u64> uoff(n + 1, s);
   DBuf<u32> ucol(std::max<u64>(1, m), s);
   DBuf<u8> keep(std::max<u64>(1, m), s);
   DBuf<u64> cnt(std::max<u32>(1, n), s);
   DBuf<int> bad(1, s);
   DBuf<u32> md(1, s);
+  // declared after the buffers, so it is destroyed first: on an exception the
+  // copies still in flight on cs finish before the buffers go back to s
+  early.x = nullptr;
+  StreamGuard guard{cs};
   GPM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
   GPM_CUDA(cudaMemsetAsync(md.get(), 0, sizeof(u32), s));
   out.sz_off = sizeof(u64) * (n + 1);

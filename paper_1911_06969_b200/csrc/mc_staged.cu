@@ -69,6 +69,7 @@ struct Mc3Args {
   unsigned long long* ctr;
   unsigned long long* hist;
   unsigned long long* cand;
+  unsigned long long* moved;  // [0] streamed candidates, [1] staged keys, [2] parent visits, [3] pos-0 counted
   u32 codeT, codeW0, codeW1;
 };
 
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(kT, 4) mc3_warp_kernel(Mc3Args a) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   u32* T = s_wtab + wid * kWSlots;
   const DevGraph& g = a.g;
-  unsigned long long aX = 0, aTri = 0, aC0 = 0, aLen = 0, aCand = 0;
+  unsigned long long aX = 0, aTri = 0, aC0 = 0, aLen = 0, aCand = 0, aStg = 0, aVis = 0;
   u32 troot = 0xffffffffu, sh = 0, mask = 0;
   u64 grab = 0, left = 0;
   for (;;) {
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(kT, 4) mc3_warp_kernel(Mc3Args a) {
       for (u32 i = lane * 4; i < cap; i += 128) *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
       __syncwarp();
       for (u32 i = lane; i < ns; i += 32) hb_insert(T, sh, mask, ldg(g.col + sb + i));
+      if (lane == 0) aStg += ns;
       __syncwarp();
     }
     const u64 pa0 = max(s, a.lo);
@@ -263,21 +265,27 @@ __global__ void __launch_bounds__(kT, 4) mc3_warp_kernel(Mc3Args a) {
       aC0 += ns - ip - 1;
       aLen += len;
       aCand += (oe - ob) + (e1 - b1);
+      ++aVis;
     }
     stream_parents(g.col, T, sh, mask, st, len, v1, s_cb[wid], s_ex[wid], s_v1[wid], aX, aTri);
   }
-  // per-lane partials (aC0, aLen, aCand) + warp-uniform (aX, aTri)
+  // per-lane partials (aC0, aLen, aCand, aVis) + warp-uniform (aX, aTri)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     aC0 += __shfl_xor_sync(0xffffffffu, aC0, o);
     aLen += __shfl_xor_sync(0xffffffffu, aLen, o);
     aCand += __shfl_xor_sync(0xffffffffu, aCand, o);
+    aVis += __shfl_xor_sync(0xffffffffu, aVis, o);
   }
   if (lane == 0) {
     if (aTri) atomicAdd(a.hist + a.codeT, aTri);
     if (aC0 - aTri) atomicAdd(a.hist + a.codeW0, aC0 - aTri);
     if (aLen - aX) atomicAdd(a.hist + a.codeW1, aLen - aX);
     if (aCand) atomicAdd(a.cand, aCand);
+    atomicAdd(a.moved + 0, aLen);
+    atomicAdd(a.moved + 1, aStg);
+    atomicAdd(a.moved + 2, aVis);
+    atomicAdd(a.moved + 3, aC0);
   }
 }
 
@@ -293,7 +301,7 @@ __global__ void __launch_bounds__(kT, 4) mc3_block_kernel(Mc3Args a) {
   __shared__ u32 s_next;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const DevGraph& g = a.g;
-  unsigned long long aX = 0, aTri = 0, aC0 = 0, aLen = 0, aCand = 0;
+  unsigned long long aX = 0, aTri = 0, aC0 = 0, aLen = 0, aCand = 0, aStg = 0, aVis = 0;
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -324,7 +332,9 @@ __global__ void __launch_bounds__(kT, 4) mc3_block_kernel(Mc3Args a) {
       *reinterpret_cast<uint4*>(s_btab + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     __syncthreads();
     for (u32 i = k0 + threadIdx.x; i < k1; i += kT) hb_insert(s_btab, sh, mask, ldg(g.col + sb + i));
+    if (threadIdx.x == 0) aStg += k1 - k0;
     __syncthreads();
+    if (threadIdx.x == 0 && ntiles > 1) a.moved[4] = 1;  // path flag (tests)
     const u32 idlo = (t == 0) ? r + 1 : ldg(g.col + sb + k0);
     const bool last_tile = (t + 1 == ntiles);
     const u32 idhi = last_tile ? 0xffffffffu : ldg(g.col + sb + k1);
@@ -346,6 +356,7 @@ __global__ void __launch_bounds__(kT, 4) mc3_block_kernel(Mc3Args a) {
         const u64 en = last_tile ? e1 : lower_bound_col(g.col, st, e1, idhi);
         len = (u32)(en - st);
         aLen += len;
+        ++aVis;
         if (t == 0) {
           aC0 += ns - ip - 1;
           aCand += (oe - ob) + (e1 - b1);
@@ -359,12 +370,17 @@ __global__ void __launch_bounds__(kT, 4) mc3_block_kernel(Mc3Args a) {
     aC0 += __shfl_xor_sync(0xffffffffu, aC0, o);
     aLen += __shfl_xor_sync(0xffffffffu, aLen, o);
     aCand += __shfl_xor_sync(0xffffffffu, aCand, o);
+    aVis += __shfl_xor_sync(0xffffffffu, aVis, o);
   }
   if (lane == 0) {
     if (aTri) atomicAdd(a.hist + a.codeT, aTri);
     if (aC0 - aTri) atomicAdd(a.hist + a.codeW0, aC0 - aTri);  // mod 2^64: partial sums may be negative
     if (aLen - aX) atomicAdd(a.hist + a.codeW1, aLen - aX);
     if (aCand) atomicAdd(a.cand, aCand);
+    atomicAdd(a.moved + 0, aLen);
+    if (aStg) atomicAdd(a.moved + 1, aStg);
+    atomicAdd(a.moved + 2, aVis);
+    atomicAdd(a.moved + 3, aC0);
   }
 }
 
@@ -405,6 +421,7 @@ struct Mc4Args {
   unsigned long long* ctr;
   unsigned long long* hist;   // 64 bins
   unsigned long long* cand;
+  unsigned long long* moved;  // [0] streamed S2 candidates, [1] staged keys, [2] unused, [3] rank-counted
   u32* scratch;               // per warp: max_deg entries for I01
   u64 scratch_stride;
   u32 pm_bits[4];             // pmask value for (v0~v2, v1~v2)
@@ -489,7 +506,10 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
   u32* T = s_tab[wid];
   u32* I01 = a.scratch + (blockIdx.x * (u64)kW4 + wid) * a.scratch_stride;
   s_h[wid][lane] = 0;
+  // per-item u32 counters (streamed, staged, children, rank-counted), folded
+  // into the unused class slot 7 of each parent-mask row of s_h per item
   unsigned long long aCand = 0;
+  u32 aLen = 0, aStg = 0, aRank = 0;
   u32 cur_v0 = 0xffffffffu;
   u64 cur_q = ~0ull;
   UnionSet U{};
@@ -550,6 +570,8 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
           n01 += __popc(bm);
         }
         U.T = fits ? T : nullptr;
+        if (!fits && lane == 0) a.moved[4] = 1;  // path flag (tests)
+        if (lane == 0) aStg += (fits ? U.n0 : 0u) + U.n1;
         __syncwarp();
       }
       // ---- per-child setup: lane c < nstep owns child cur + c
@@ -565,6 +587,7 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
         len = (u32)(e2 - st);
         pmv = U.flags(v2);  // bit 0: v2 ~ v0, bit 1: v2 ~ v1
         aCand += (u64)(ldg(g.off + v0 + 1) - ldg(g.off + v0)) + (ldg(g.off + v1 + 1) - ldg(g.off + v1)) + (e2 - b2);
+        aLen += len;
       }
       // ---- event counts of every child: e2c / e11 / e01 / e12 (see above)
       u32 e2c = 0, e11 = 0, e01 = 0, e12 = 0;
@@ -696,6 +719,7 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
         val[4] = e12;
         val[5] = B1 - I2 - e12;
         val[6] = e2c;
+        aRank += val[1] + val[3] + val[5];
       }
 #pragma unroll
       for (u32 pv = 0; pv < 4; ++pv) {
@@ -710,10 +734,23 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
       __syncwarp();
       cur += nstep;
     }
+    {
+      const u32 l = __reduce_add_sync(0xffffffffu, aLen), rk = __reduce_add_sync(0xffffffffu, aRank);
+      if (lane == 0) {
+        s_h[wid][7] += l;
+        s_h[wid][15] += aStg;
+        s_h[wid][31] += rk;
+      }
+      aLen = aStg = aRank = 0;
+    }
   }
   __syncwarp();
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) aCand += __shfl_xor_sync(0xffffffffu, aCand, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    aCand += __shfl_xor_sync(0xffffffffu, aCand, o);
+  }
+  __syncwarp();
+  if (lane < 4 && s_h[wid][8 * lane + 7]) atomicAdd(a.moved + lane, s_h[wid][8 * lane + 7]);
   {
     const u32 pv = lane >> 3, cl = lane & 7;
     const unsigned long long v = s_h[wid][lane];
@@ -753,9 +790,9 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
   if (NS) mc3_iroot_kernel<<<grid1(nr), 256, 0, s>>>(ismall.get(), nr, rs.get());
   if (NB) mc3_iroot_kernel<<<grid1(nr), 256, 0, s>>>(ibig.get(), nr, rb.get());
   GPM_CUDA(cudaGetLastError());
-  DBuf<unsigned long long> ctr(2, s), cand(1, s);
+  DBuf<unsigned long long> ctr(2, s), cand(6, s);
   GPM_CUDA(cudaMemsetAsync(ctr.get(), 0, 2 * sizeof(unsigned long long), s));
-  GPM_CUDA(cudaMemsetAsync(cand.get(), 0, sizeof(unsigned long long), s));
+  GPM_CUDA(cudaMemsetAsync(cand.get(), 0, 6 * sizeof(unsigned long long), s));
 
   Mc3Args a{};
   a.g = G.view();
@@ -765,6 +802,7 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
   a.vlo = vr[0];
   a.hist = d_hist;
   a.cand = cand.get();
+  a.moved = cand.get() + 1;
   a.codeT = (1u << pat::pair_index(0, 1, 3)) | (1u << pat::pair_index(0, 2, 3)) | (1u << pat::pair_index(1, 2, 3));
   a.codeW0 = (1u << pat::pair_index(0, 1, 3)) | (1u << pat::pair_index(0, 2, 3));
   a.codeW1 = (1u << pat::pair_index(0, 1, 3)) | (1u << pat::pair_index(1, 2, 3));
@@ -772,12 +810,13 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
   size_t rec = tl.recs.size();
   if (NS) {
     const size_t wsmem = (size_t)kWarps * kWSlots * sizeof(u32);
-    static int occ = 0;
-    if (!occ) {
+    static std::atomic<int> occ_slot{0};
+    const int occ = cached_occupancy(occ_slot, [&] {
       GPM_CUDA(cudaFuncSetAttribute(mc3_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
-      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mc3_warp_kernel, kT, wsmem));
-      occ = std::max(1, occ);
-    }
+      int o = 0;
+      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, mc3_warp_kernel, kT, wsmem));
+      return o;
+    });
     const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sms * occ, (NS + kWarps - 1) / kWarps));
     Mc3Args w = a;
     w.istart = ismall.get();
@@ -793,12 +832,13 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
   }
   if (NB) {
     const size_t smem = kBSlots * sizeof(u32);
-    static int occb = 0;
-    if (!occb) {
+    static std::atomic<int> occb_slot{0};
+    const int occb = cached_occupancy(occb_slot, [&] {
       GPM_CUDA(cudaFuncSetAttribute(mc3_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occb, mc3_block_kernel, kT, smem));
-      occb = std::max(1, occb);
-    }
+      int o = 0;
+      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, mc3_block_kernel, kT, smem));
+      return o;
+    });
     const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sms * occb, NB));
     Mc3Args b = a;
     b.istart = ibig.get();
@@ -811,31 +851,46 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
     tl.end(ev);
     ++tl.launches;
   }
-  unsigned long long W = 0;
-  GPM_CUDA(cudaMemcpyAsync(&W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, s));
+  unsigned long long W[6] = {0, 0, 0, 0, 0, 0};
+  GPM_CUDA(cudaMemcpyAsync(W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaStreamSynchronize(s));
   // SURVEY §8d B_alg of the level: 8*l per parent + (16 + 4 deg) per position
-  const double bytes = 8.0 * np + 16.0 * 2 * np + 4.0 * (double)W;
-  if (rec < tl.recs.size()) tl.recs[rec].bytes = bytes;
-  st.candidates[1] += W;
+  const double bytes = 8.0 * np + 16.0 * 2 * np + 4.0 * (double)W[0];
+  // what the kernels actually read: the streamed pos-1 suffixes and staged S0
+  // keys (4 B each) + per parent visit its v1 and offsets pair (20 B);
+  // binary-search probes excluded as in B_alg.  The pos-0 candidates u > v1
+  // are never streamed: their class is the pair predicate decided by the
+  // stream from the other side, so they are counted, not read.
+  const double moved = 4.0 * (double)(W[1] + W[2]) + 20.0 * (double)W[3];
+  if (rec < tl.recs.size()) {  // both launches are named extend_fused_L1: totals on the first
+    tl.recs[rec].bytes = bytes;
+    tl.recs[rec].moved = moved;
+  }
+  st.candidates[1] += W[0];
+  st.streamed += W[1] + W[2];
+  st.counted += W[4];
   st.balg += bytes;
+  st.bmoved += moved;
+  st.paths |= (NS ? (u32)GPM_PATH_MC3_WARP : 0u) | (NB ? (u32)GPM_PATH_MC3_BLOCK : 0u) |
+              (W[5] ? (u32)GPM_PATH_MC3_MULTITILE : 0u);
 }
 
 void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u32* idx2, const u32* vid2, u64 np,
                      unsigned long long* d_hist, cudaStream_t s, Timeline& tl, Stats& st) {
   if (np == 0) return;
-  static int occ = 0;
-  if (!occ) {
-    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mc4_last_kernel, kT4, 0));
-    occ = std::max(1, occ);
-  }
+  static std::atomic<int> occ_slot{0};
+  const int occ = cached_occupancy(occ_slot, [] {
+    int o = 0;
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, mc4_last_kernel, kT4, 0));
+    return o;
+  });
   const u64 nitems = (np + k4Item - 1) / k4Item;
   const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sm_count() * occ, (nitems + kW4 - 1) / kW4));
   const u64 stride = std::max<u64>(32, ((u64)G.max_deg + 31) / 32 * 32);
   DBuf<u32> scratch(blocks * kW4 * stride, s);
-  DBuf<unsigned long long> ctr(1, s), cand(1, s);
+  DBuf<unsigned long long> ctr(1, s), cand(6, s);
   GPM_CUDA(cudaMemsetAsync(ctr.get(), 0, sizeof(unsigned long long), s));
-  GPM_CUDA(cudaMemsetAsync(cand.get(), 0, sizeof(unsigned long long), s));
+  GPM_CUDA(cudaMemsetAsync(cand.get(), 0, 6 * sizeof(unsigned long long), s));
   htrace(s, "mc4: scratch");
   Mc4Args a{};
   a.g = G.view();
@@ -848,6 +903,7 @@ void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u
   a.ctr = ctr.get();
   a.hist = d_hist;
   a.cand = cand.get();
+  a.moved = cand.get() + 1;
   a.scratch = scratch.get();
   a.scratch_stride = stride;
   auto P = [](int i, int j) { return 1u << pat::pair_index(i, j, 4); };
@@ -864,13 +920,21 @@ void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u
   GPM_CUDA(cudaGetLastError());
   tl.end(ev);
   tl.launches += 1;
-  unsigned long long W = 0;
-  GPM_CUDA(cudaMemcpyAsync(&W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, s));
+  unsigned long long W[6] = {0, 0, 0, 0, 0, 0};
+  GPM_CUDA(cudaMemcpyAsync(W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaStreamSynchronize(s));
-  const double bytes = 8.0 * 2 * np + 16.0 * 3 * np + 4.0 * (double)W;
+  const double bytes = 8.0 * 2 * np + 16.0 * 3 * np + 4.0 * (double)W[0];
+  // read by the kernel: streamed S2 suffixes + staged S0/S1 keys (4 B each),
+  // 20 B per child (v2 + offsets pair) and 8 B per child of level-2 index
+  const double moved = 4.0 * (double)(W[1] + W[2]) + 28.0 * (double)np;
   tl.recs[ev].bytes = bytes;
-  st.candidates[2] += W;
+  tl.recs[ev].moved = moved;
+  st.candidates[2] += W[0];
+  st.streamed += W[1] + W[2];
+  st.counted += W[4];
   st.balg += bytes;
+  st.bmoved += moved;
+  st.paths |= GPM_PATH_MC4_STAGED | (W[5] ? (u32)GPM_PATH_MC4_HBM_SETS : 0u);
 }
 
 }  // namespace gpm

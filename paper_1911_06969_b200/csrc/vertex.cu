@@ -827,11 +827,12 @@ template <int APP, int LEV, int MODE>
 void launch_extend(Ctx& c, ExtendArgs& a, const char* what, double bytes) {
   auto kern = extend_kernel<APP, LEV, MODE>;
   size_t smem = (MODE == kFused && APP == kAppMC) ? sizeof(unsigned long long) * (size_t(1) << pat::npairs(c.k)) : 0;
-  static int occ = 0;  // per template instantiation
-  if (occ == 0) {
-    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
-    occ = std::max(1, occ);
-  }
+  static std::atomic<int> occ_slot{0};  // per template instantiation
+  const int occ = cached_occupancy(occ_slot, [&] {
+    int o = 0;
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, smem));
+    return o;
+  });
   const u64 nb = a.b_end - a.b_begin;
   const u64 warps_needed = nb;
   u64 blocks = std::min<u64>((u64)c.sms * occ, (warps_needed * 32 + kThreads - 1) / kThreads);
@@ -839,6 +840,7 @@ void launch_extend(Ctx& c, ExtendArgs& a, const char* what, double bytes) {
   a.grab = std::max<u64>(1, std::min<u64>(kBatchGrab, nb / (blocks * (kThreads / 32) * 64)));
   GPM_CUDA(cudaMemsetAsync(c.d_ctr, 0, sizeof(unsigned long long), c.s));
   a.ctr = c.d_ctr;
+  c.st->paths |= GPM_PATH_GENERIC;
   size_t ev = c.tl->begin(std::string(what) + "_L" + std::to_string(LEV), bytes);
   kern<<<(unsigned)blocks, kThreads, smem, c.s>>>(a);
   GPM_CUDA(cudaGetLastError());
@@ -1041,13 +1043,13 @@ void launch_edge(Ctx& c, EdgeArgs& a, const std::string& what, double bytes) {
   while (hs < 2 * (32 + 2 * std::min<u32>(md, kFilterMax)) && hs < kHashSlots) hs <<= 1;
   a.hstride = hs;
   const size_t smem = (size_t)(kThreads / 32) * hs * sizeof(u32);
-  static int occ_by_hs[16] = {0};
-  int& occ = occ_by_hs[31 - __builtin_clz(hs)];
-  if (occ == 0) {
+  static std::atomic<int> occ_by_hs[16];  // zero-initialised (static storage)
+  const int occ = cached_occupancy(occ_by_hs[31 - __builtin_clz(hs)], [&] {
     GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kThreads / 32 * kHashSlots * 4)));
-    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
-    occ = std::max(1, occ);
-  }
+    int o = 0;
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, smem));
+    return o;
+  });
   const u64 ni = a.iend - a.ibeg;
   u64 blocks = std::max<u64>(1, std::min<u64>((u64)c.sms * occ, (ni * 32 + kThreads - 1) / kThreads));
   // coarse grabs only when every warp gets many items (tail balance first)
@@ -1078,6 +1080,7 @@ void cf_last_siblings(Ctx& c, const u32* idx, const u32* vid, u64 np, int lev) {
   a.total = c.d_total;
   a.cand = cand.get();
   size_t rec = c.tl->recs.size();
+  c.st->paths |= GPM_PATH_CF_SIBLINGS;
   launch_edge<kFused, true>(c, a, "extend_fused_L" + std::to_string(lev), 0.0);
   unsigned long long W = 0;
   GPM_CUDA(cudaMemcpyAsync(&W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, c.s));
@@ -1096,6 +1099,7 @@ void process_l1_cf(Ctx& c, const VLevels& L, const u32* src, u64 lo, u64 hi) {
   if (np == 0) return;
   const bool last = (c.k == 3);
   const u64 NI = (np + 31) / 32;
+  st.paths |= GPM_PATH_CF_EDGE_CHUNK;
   DBuf<unsigned long long> cand(1, c.s);
   GPM_CUDA(cudaMemsetAsync(cand.get(), 0, sizeof(unsigned long long), c.s));
   EdgeArgs a{};
@@ -1255,9 +1259,7 @@ void mine_vertex(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm
   c.list_ctx = cfg.list_ctx;
   c.listed = 0;
   if (c.list_fn && app == GPM_APP_MC) throw Error(GPM_EINVAL, "listing mode: TC/CF only (SPEC.md:458)");
-  size_t freeb = 0, totalb = 0;
-  freeb = device_free_bytes();
-  (void)totalb;
+  const size_t freeb = device_free_bytes();
   u64 budget = cfg.mem_budget ? cfg.mem_budget : (u64)(0.6 * (double)freeb);
   const int mat_levels = std::max(1, k - 3);
   c.cap_entries = std::max<u64>(kBatch, std::min<u64>((u64(1) << 32) - 1, budget / 16 / mat_levels));

@@ -1,0 +1,113 @@
+"""GPU vs the CPU oracle on the code paths that only trigger at BASELINE size
+(ADVICE r1): the tiled 3-MC block kernel (a root with
+|S0| > 1024 keys, several S0 tiles), the 4-MC HBM fallback (|S0|+|S1| > 512),
+the memory planner's chunking, and FSM domain bitmaps in several rounds under
+a small budget.  Each test asserts through gpm_stats.paths that the path ran,
+then compares with the oracle bit for bit."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1911_06969_b200 as P
+    return P
+
+
+def hub_graph(n, p, hubs, seed):
+    """G(n, p) plus `hubs` = [(vertex, degree)] stars to random vertices;
+    hubs get small ids so their upper suffix S0 = N(v) ∩ (>v) is large."""
+    rng = np.random.default_rng(seed)
+    m = int(p * n * (n - 1) / 2)
+    e = rng.integers(0, n, size=(m, 2))
+    parts = [e]
+    for v, d in hubs:
+        nb = rng.choice(np.arange(v + 1, n), size=d, replace=False)
+        parts.append(np.stack([np.full(d, v), nb], 1))
+    return np.concatenate(parts)
+
+
+def host(P, oracle, E, n, labels=None):
+    c = oracle.csr_from_edges(E, n, labels)
+    return P.HostGraph(c.off, c.col, None if labels is None else np.asarray(labels, np.uint32)), c
+
+
+def same_vertex(r, o):
+    assert r.total == o["total"]
+    assert sorted(tuple(x) for x in r.patterns) == sorted(tuple(x) for x in o["patterns"])
+    for key in ("level_sizes", "candidates", "n_explored", "b_alg"):
+        a, b = r.stats[key], o[key]
+        if isinstance(b, list):
+            a = a[:len(b)]
+        assert a == b, (key, a, b)
+
+
+def test_mc3_block_kernel_multitile_vs_oracle(P, oracle):
+    from paper_1911_06969_b200 import _lib
+    n = 6000
+    E = hub_graph(n, 0.002, [(0, 3000), (1, 1500), (5, 700)], seed=1)
+    hg, c = host(P, oracle, E, n)
+    g = P.Graph(hg)
+    r = P.mine(g, "mc", 3)
+    assert r.stats["paths"] & _lib.PATH_MC3_BLOCK and r.stats["paths"] & _lib.PATH_MC3_MULTITILE
+    assert r.stats["paths"] & _lib.PATH_MC3_WARP
+    same_vertex(r, oracle.mine(c, "mc", 3))
+    # the closed form on the same graph
+    d = np.diff(c.off.astype(np.int64))
+    T = oracle.mine(c, "tc", 3)["total"]
+    assert dict((t, s) for _, t, s in r.patterns)["k=3;L=0,0,0;E=(0,1)(0,2)"] == int((d * (d - 1) // 2).sum()) - 3 * T
+
+
+def test_mc4_hbm_union_sets_vs_oracle(P, oracle):
+    from paper_1911_06969_b200 import _lib
+    n = 3000
+    E = hub_graph(n, 0.002, [(0, 600), (2, 450), (3, 300)], seed=2)
+    hg, c = host(P, oracle, E, n)
+    g = P.Graph(hg)
+    r = P.mine(g, "mc", 4)
+    assert r.stats["paths"] & _lib.PATH_MC4_STAGED and r.stats["paths"] & _lib.PATH_MC4_HBM_SETS
+    same_vertex(r, oracle.mine(c, "mc", 4))
+
+
+@pytest.mark.parametrize("app,k", [("cf", 5), ("cf", 6), ("mc", 4)])
+def test_planner_chunks_vs_oracle(P, oracle, app, k):
+    from paper_1911_06969_b200 import _lib
+    # (4-MC's per-candidate oracle is ~100x costlier than k-CL's: smaller graph)
+    hg = P.generate_rmat(12, 12, 0.57, 0.19, 0.19, seed=21) if app == "cf" else \
+        P.generate_rmat(11, 6, 0.57, 0.19, 0.19, seed=21)
+    c = oracle.Csr(hg.off, hg.col)
+    g = P.Graph(hg)
+    r = P.mine(g.orient_dag() if app == "cf" else g, app, k, mem_budget=1 << 16)
+    assert r.stats["chunks"] > 0 and r.stats["paths"] & _lib.PATH_PLANNER_CHUNKS
+    same_vertex(r, oracle.mine(c, app, k))
+
+
+@pytest.mark.parametrize("k,sigma", [(3, 20), (4, 40)])
+def test_fsm_domain_rounds_small_budget_vs_oracle(P, oracle, k, sigma):
+    from paper_1911_06969_b200 import _lib
+    hg = P.generate_rmat(12, 8, 0.45, 0.15, 0.15, seed=3, n_labels=4, label_seed=7)
+    c = oracle.Csr(hg.off, hg.col, hg.labels)
+    r = P.mine(P.Graph(hg), "fsm", k, sigma, mem_budget=1 << 16)
+    assert r.stats["paths"] & _lib.PATH_FSM_ROUNDS
+    assert not r.stats["paths"] & _lib.PATH_FSM_FUSED_LAST  # qcap below the fused minimum
+    o = oracle.mine(c, "fsm", k, sigma)
+    assert sorted(r.patterns) == sorted(tuple(x) for x in o["patterns"])
+    for key in ("level_sizes", "candidates", "n_explored"):
+        assert r.stats[key][:len(o[key])] == o[key], key
+
+
+def test_config_conflicts_return_econfig(P, oracle):
+    from paper_1911_06969_b200 import _lib
+    hg = P.generate_rmat(10, 8, 0.45, 0.15, 0.15, seed=3, n_labels=4, label_seed=7)
+    g = P.Graph(hg)
+    with pytest.raises(_lib.GpmError) as e:
+        P.mine(g, "fsm", 3, 5, root_lo=0, root_hi=100)
+    assert e.value.code == _lib.GPM_ECONFIG
+    with pytest.raises(_lib.GpmError) as e:
+        P.list_embeddings(g, "mc", 3)
+    assert e.value.code == _lib.GPM_ECONFIG

@@ -174,3 +174,40 @@ def test_pattern_tsv_order(oracle):
     keys = [(-int(s), t) for t, s in rows]
     assert keys == sorted(keys)
     assert sum(int(s) for _, s in rows) == o["total"]
+
+
+@pytest.mark.parametrize("args", [(11, 8.0, 0.57, 0.19, 0.19, 1, 0, 101), (13, 11.0, 0.45, 0.15, 0.15, 1, 32, 101),
+                                  (12, 3.35, 0.50, 0.20, 0.20, 7, 4, 5)])
+def test_oracle_generator_restatement_matches_product(oracle, args):
+    """The oracle's own SURVEY §8d generator (used by the reference arm, the
+    CPU baseline and the golden scripts, never libgpm.so) produces the same
+    cleaned CSR and labels as gpm_generate_rmat."""
+    import paper_1911_06969_b200 as P
+    a = oracle.generate_rmat(*args)
+    b = P.generate_rmat(*args)
+    assert np.array_equal(a.off, b.off) and np.array_equal(a.col, b.col)
+    if args[6]:
+        assert np.array_equal(a.labels, b.labels)
+    else:
+        assert a.labels is None and b.labels is None
+
+
+def test_reference_arm_never_loads_the_product(tmp_path):
+    """bench.py --impl reference runs the CPU port only: the product package
+    (and libgpm.so) is never imported, and its config equals the GPU arm's."""
+    import json
+    import subprocess
+    import sys
+    code = ("import runpy, sys, json; sys.argv = ['bench.py', '--impl', 'reference', '--app', 'tc', '--steps', '1',"
+            " '--warmup', '0', '--cpu-budget', '0.2']; runpy.run_path('bench.py', run_name='__main__');"
+            " assert 'paper_1911_06969_b200' not in sys.modules, 'product imported';"
+            " import os; maps = open('/proc/self/maps').read(); assert 'libgpm.so' not in maps, 'libgpm.so mapped'")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["config"]["app"] == "tc"
+    sys.path.insert(0, ROOT)
+    import bench
+    import pyoracle
+    g = pyoracle.generate_rmat(16, 16, 0.57, 0.19, 0.19, 1)
+    assert line["config"] == bench.workload_config("tc", g.n, g.m, 0)
