@@ -259,9 +259,24 @@ def make_config(app: str, k: int = 3, min_support: int = 0, *, mem_budget: int =
 def mine(g: Graph, app: str, k: int = 3, min_support: int = 0, **kw) -> MineResult:
     """mine(g, cfg): extend/reduce/filter level loop."""
     cfg = make_config(app, k, min_support, **kw)
-    L = lib()
     r = C.c_void_p()
-    check(L.gpm_mine(g.handle, C.byref(cfg), C.byref(r)))
+    check(lib().gpm_mine(g.handle, C.byref(cfg), C.byref(r)))
+    return _collect(r, app, k)
+
+
+def mine_custom(entry, g: Graph, k: int, *, name: str = "custom", **kw) -> MineResult:
+    """Runs a user App compiled against include/gpm_engine.cuh: `entry` is a
+    ctypes function with gpm_mine's signature (graph, config, result**) that
+    calls gpm::mine_app<App> (tests/apps/test_apps.cu)."""
+    cfg = make_config("tc", k, 0, **kw)
+    cfg.app = -1  # not a builtin app
+    r = C.c_void_p()
+    check(entry(g.handle, C.byref(cfg), C.byref(r)))
+    return _collect(r, name, k)
+
+
+def _collect(r, app: str, k: int) -> MineResult:
+    L = lib()
     try:
         total = C.c_uint64()
         check(L.gpm_result_total(r, C.byref(total)))

@@ -184,47 +184,34 @@ int gpm_steal_release(void* dev_ptr, int opened) {
   });
 }
 
-static int gpm_mine_once(const gpm_graph* g, const gpm_config* cfg, gpm_result** out);
+}  // extern "C"
 
-int gpm_mine(const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
-  if (!g || !cfg || !out) {
-    set_last_error("gpm_mine: null argument");
-    return GPM_EINVAL;
-  }
-  int rc = gpm_mine_once(g, cfg, out);
-  // The planner sizes levels from a cached free-memory reading; memory the
-  // caller allocated since (e.g. torch tensors) can make a level allocation
-  // fail.  Re-plan once from a fresh reading with the library's cached
-  // blocks handed back -- unless other ranks already entered collectives
-  // (FSM exchanges per level) or stolen chunks would be lost.
-  const bool solo = cfg->world <= 1 || !cfg->exchange;
-  if (rc == GPM_ENOMEM && !cfg->steal_ctrs && (solo || cfg->app != GPM_APP_FSM)) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    big_cache().trim(dev);
-    mem_generation().fetch_add(1, std::memory_order_relaxed);
-    rc = gpm_mine_once(g, cfg, out);
-  }
-  return rc;
+namespace gpm {
+
+// gpm_mine's validation of the builtin apps' config (SPEC.md:375 conflicts).
+static void check_builtin_config(const gpm_config* cfg) {
+  if (cfg->app < GPM_APP_TC || cfg->app > GPM_APP_FSM) throw Error(GPM_EINVAL, "unknown app");
+  // config conflicts ("chunking + filter -> error"): the FSM
+  // filter needs every root's embeddings before the next extend, so a
+  // root slice is only legal as one rank's share of an exchanged job;
+  // listing is a TC/CF mode; stealing only applies to the count apps
+  if (cfg->list_fn && cfg->app != GPM_APP_TC && cfg->app != GPM_APP_CF)
+    throw Error(GPM_ECONFIG, "listing mode: TC/CF only (SPEC.md:458)");
+  if (cfg->app == GPM_APP_FSM && cfg->root_hi > 0 && !(cfg->world > 1 && cfg->exchange))
+    throw Error(GPM_ECONFIG, "fsm: a root slice without a cross-rank exchange would filter on partial supports "
+                             "(SPEC.md:160, :375)");
+  if (cfg->app == GPM_APP_FSM && cfg->steal_ctrs)
+    throw Error(GPM_ECONFIG, "fsm: work stealing conflicts with the per-level exchange (static split only)");
+  if (cfg->steal_ctrs && cfg->root_hi > 0)
+    throw Error(GPM_ECONFIG, "steal_ctrs and an explicit root slice are mutually exclusive");
 }
 
-static int gpm_mine_once(const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
+// Stream, timing events and the stats record around one mine body (a builtin
+// app or a user App instantiated from include/gpm_engine.cuh).
+static int mine_once(const gpm_graph* g, const gpm_config* cfg, gpm_result** out, MineBody body, bool builtin) {
   *out = nullptr;
   return guarded([&] {
-    if (cfg->app < GPM_APP_TC || cfg->app > GPM_APP_FSM) throw Error(GPM_EINVAL, "unknown app");
-    // config conflicts ("chunking + filter -> error"): the FSM
-    // filter needs every root's embeddings before the next extend, so a
-    // root slice is only legal as one rank's share of an exchanged job;
-    // listing is a TC/CF mode; stealing only applies to the count apps
-    if (cfg->list_fn && cfg->app != GPM_APP_TC && cfg->app != GPM_APP_CF)
-      throw Error(GPM_ECONFIG, "listing mode: TC/CF only (SPEC.md:458)");
-    if (cfg->app == GPM_APP_FSM && cfg->root_hi > 0 && !(cfg->world > 1 && cfg->exchange))
-      throw Error(GPM_ECONFIG, "fsm: a root slice without a cross-rank exchange would filter on partial supports "
-                               "(SPEC.md:160, :375)");
-    if (cfg->app == GPM_APP_FSM && cfg->steal_ctrs)
-      throw Error(GPM_ECONFIG, "fsm: work stealing conflicts with the per-level exchange (static split only)");
-    if (cfg->steal_ctrs && cfg->root_hi > 0)
-      throw Error(GPM_ECONFIG, "steal_ctrs and an explicit root slice are mutually exclusive");
+    if (builtin) check_builtin_config(cfg);
     if (cfg->world < 0 || (cfg->world > 1 && (cfg->rank < 0 || cfg->rank >= cfg->world)))
       throw Error(GPM_EINVAL, "bad rank/world");
     GPM_CUDA(cudaSetDevice(g->device));
@@ -240,8 +227,7 @@ static int gpm_mine_once(const gpm_graph* g, const gpm_config* cfg, gpm_result**
     GPM_CUDA(cudaEventCreate(&e1));
     GPM_CUDA(cudaEventRecord(e0, s));
     try {
-      if (cfg->app == GPM_APP_FSM) mine_fsm(*g, *cfg, s, *res, st, tl);
-      else mine_vertex(*g, *cfg, s, *res, st, tl);
+      body(*g, *cfg, s, *res, st, tl);
     } catch (...) {
       cudaStreamSynchronize(s);
       cudaEventDestroy(e0);
@@ -293,6 +279,46 @@ static int gpm_mine_once(const gpm_graph* g, const gpm_config* cfg, gpm_result**
       }
     *out = res.release();
   });
+}
+
+static int mine_with(const gpm_graph* g, const gpm_config* cfg, gpm_result** out, MineBody body, bool builtin) {
+  if (!g || !cfg || !out) {
+    set_last_error("gpm_mine: null argument");
+    return GPM_EINVAL;
+  }
+  int rc = mine_once(g, cfg, out, body, builtin);
+  // The planner sizes levels from a cached free-memory reading; memory the
+  // caller allocated since (e.g. torch tensors) can make a level allocation
+  // fail.  Re-plan once from a fresh reading with the library's cached
+  // blocks handed back -- unless other ranks already entered collectives
+  // (FSM exchanges per level) or stolen chunks would be lost.
+  const bool solo = cfg->world <= 1 || !cfg->exchange;
+  if (rc == GPM_ENOMEM && !cfg->steal_ctrs && (solo || cfg->app != GPM_APP_FSM)) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    big_cache().trim(dev);
+    mem_generation().fetch_add(1, std::memory_order_relaxed);
+    rc = mine_once(g, cfg, out, body, builtin);
+  }
+  return rc;
+}
+
+static void builtin_body(const gpm_graph& g, const gpm_config& cfg, cudaStream_t s, gpm_result& res, Stats& st,
+                         Timeline& tl) {
+  if (cfg.app == GPM_APP_FSM) mine_fsm(g, cfg, s, res, st, tl);
+  else mine_vertex(g, cfg, s, res, st, tl);
+}
+
+int run_custom(const gpm_graph* g, const gpm_config* cfg, gpm_result** out, MineBody body) {
+  return mine_with(g, cfg, out, body, false);
+}
+
+}  // namespace gpm
+
+extern "C" {
+
+int gpm_mine(const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
+  return mine_with(g, cfg, out, builtin_body, true);
 }
 
 int gpm_result_total(const gpm_result* r, uint64_t* total) {

@@ -104,6 +104,12 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out);
 void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels, u32 n, u64 m, gpm_graph& out);
 
 void mine_vertex(const gpm_graph& g, const gpm_config& cfg, cudaStream_t s, gpm_result& res, Stats& st, Timeline& tl);
+
+// One mine body run inside gpm_mine's bookkeeping (stream, events, stats).
+using MineBody = void (*)(const gpm_graph&, const gpm_config&, cudaStream_t, gpm_result&, Stats&, Timeline&);
+// gpm_mine for a user App instantiated from include/gpm_engine.cuh
+// (gpm::mine_app<App>): same bookkeeping, no builtin-app config checks.
+int run_custom(const gpm_graph* g, const gpm_config* cfg, gpm_result** out, MineBody body);
 void mine_fsm(const gpm_graph& g, const gpm_config& cfg, cudaStream_t s, gpm_result& res, Stats& st, Timeline& tl);
 
 // Collective hooks (multi-GPU, one process per GPU): sum a host vector or

@@ -92,7 +92,7 @@ def test_fsm_domain_rounds_small_budget_vs_oracle(P, oracle, k, sigma):
     from paper_1911_06969_b200 import _lib
     hg = P.generate_rmat(12, 8, 0.45, 0.15, 0.15, seed=3, n_labels=4, label_seed=7)
     c = oracle.Csr(hg.off, hg.col, hg.labels)
-    r = P.mine(P.Graph(hg), "fsm", k, sigma, mem_budget=1 << 16)
+    r = P.mine(P.Graph(hg), "fsm", k, sigma, mem_budget=1 << 12)
     assert r.stats["paths"] & _lib.PATH_FSM_ROUNDS
     assert not r.stats["paths"] & _lib.PATH_FSM_FUSED_LAST  # qcap below the fused minimum
     o = oracle.mine(c, "fsm", k, sigma)

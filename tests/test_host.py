@@ -211,3 +211,14 @@ def test_reference_arm_never_loads_the_product(tmp_path):
     import pyoracle
     g = pyoracle.generate_rmat(16, 16, 0.57, 0.19, 0.19, 1)
     assert line["config"] == bench.workload_config("tc", g.n, g.m, 0)
+
+
+def test_engine_header_test_apps_built_and_linked():
+    """tests/apps/libgpm_testapps.so (user apps on include/gpm_engine.cuh)
+    loads against libgpm.so and exports its entry point (no GPU call)."""
+    import ctypes
+    import paper_1911_06969_b200  # noqa: F401  (loads libgpm.so)
+    path = os.path.join(ROOT, "tests", "apps", "libgpm_testapps.so")
+    assert os.path.exists(path), "run __graft_entry__.build()"
+    L = ctypes.CDLL(path)
+    assert hasattr(L, "testapp_mine")
