@@ -31,7 +31,8 @@
 //     template <int S> __device__ static bool to_extend(const Emb<S>&, int pos);
 //     template <int S> __device__ static bool to_add(const Emb<S>&, int pos, u32 u);
 //     template <int S> __device__ static u32  pattern_code(const Emb<S>&, int pos, u32 u);
-//     static bool to_prune(u32 code, u64 support, int level);   // host (kFilter)
+//     static bool to_prune(u32 code, u64 support, int size);    // host (kFilter);
+//                                              // size = vertices of the pattern
 //     static std::string code_text(u32 code, int k);            // host (!kCodesAreMasks)
 //   };
 //
@@ -741,7 +742,8 @@ void process(Ctx& c, VLevels L, u64 np) {
     GPM_CUDA(cudaMemcpyAsync(hh.data(), h.get(), sizeof(unsigned long long) * c.nbins, cudaMemcpyDeviceToHost, c.s));
     GPM_CUDA(cudaStreamSynchronize(c.s));
     std::vector<u8> kh(c.nbins, 0);
-    for (int i = 0; i < c.nbins; ++i) kh[i] = (hh[i] && !App::to_prune((u32)i, hh[i], LEV + 1)) ? 1 : 0;
+    // to_prune(code, support, size): size = vertices of the reduced embeddings
+    for (int i = 0; i < c.nbins; ++i) kh[i] = (hh[i] && !App::to_prune((u32)i, hh[i], LEV + 2)) ? 1 : 0;
     keep.alloc(c.nbins, c.s);
     GPM_CUDA(cudaMemcpyAsync(keep.get(), kh.data(), c.nbins, cudaMemcpyHostToDevice, c.s));
     a.keep = keep.get();

@@ -48,7 +48,7 @@ def exchange_op(t, op: int, group=None):
         for p in parts[1:]:
             acc.bitwise_or_(p)
         t.copy_(acc)
-    elif op == 2:
+    elif op == 2:  # t holds world * n elements, this rank's slot filled
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
         n = t.numel() // world
@@ -60,13 +60,20 @@ def exchange_op(t, op: int, group=None):
         raise ValueError(f"unknown exchange op {op}")
 
 
+def dist_world(group=None) -> int:
+    import torch.distributed as dist
+    return dist.get_world_size(group)
+
+
 def make_exchange(group=None):
     """Returns a ctypes gpm_exchange_fn bound to torch.distributed."""
     import torch
 
     def _cb(ctx, dev_buf, count, elem_bytes, op, stream):
         try:
-            t = torch.as_tensor(_DevArray(dev_buf, count, elem_bytes), device="cuda")
+            # op 2 (all-gather): `count` is per rank, the buffer holds world * count
+            n = count * (dist_world(group) if op == 2 else 1)
+            t = torch.as_tensor(_DevArray(dev_buf, n, elem_bytes), device="cuda")
             if elem_bytes == 8 and op == 0:
                 t = t.view(torch.int64)  # NCCL sums int64 == uint64 modulo 2^64
             elif elem_bytes == 4:

@@ -131,8 +131,8 @@ struct WedgeGrownMotifApp {
       if (t > pos && e.connected(t, u)) code |= engine::Emb<S>::pair_bit(t, S, S + 1);
     return code;
   }
-  // level 3 (3 vertices): prune the triangle code (all three pairs)
-  static bool to_prune(u32 code, u64, int level) { return level == 3 && code == 7u; }
+  // 3-vertex patterns: prune the triangle code (all three pairs)
+  static bool to_prune(u32 code, u64, int size) { return size == 3 && code == 7u; }
   static std::string code_text(u32, int) { return std::string(); }
 };
 

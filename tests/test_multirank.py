@@ -103,7 +103,8 @@ class ThreadedExchange:
 
         def cb(ctx, ptr, count, eb, op, stream):
             try:
-                t = torch.as_tensor(_DevArray(ptr, count, eb), device="cuda")
+                n = count * (self.world if op == 2 else 1)  # op 2: per-rank count, world slots
+                t = torch.as_tensor(_DevArray(ptr, n, eb), device="cuda")
                 t = t.view(torch.int64) if eb == 8 else t.view(torch.int32)
                 self.slots[rank] = t.cpu()
                 self.barrier.wait()
@@ -114,6 +115,8 @@ class ThreadedExchange:
                             acc += s
                         elif op == 1:
                             acc |= s
+                        elif op == 2:  # disjoint slots: sum == all-gather
+                            acc += s
                         else:
                             raise ValueError(op)
                     self.result = acc
@@ -210,7 +213,8 @@ def _ipc_worker(rank, world, port, q):
         from paper_1911_06969_b200.dist import StealCounters, _DevArray, exchange_op
 
         def cb(ctx, ptr, count, eb, op, stream):  # device buffer -> host gloo collective -> device
-            t = torch.as_tensor(_DevArray(ptr, count, eb), device="cuda")
+            n = count * (world if op == 2 else 1)  # op 2: per-rank count, world slots
+            t = torch.as_tensor(_DevArray(ptr, n, eb), device="cuda")
             t = t.view(torch.int64) if eb == 8 else t.view(torch.int32)
             h = t.cpu()
             exchange_op(h, op)
