@@ -482,6 +482,223 @@ __global__ void __launch_bounds__(kThreads) eextend_kernel(FsmArgs a) {
   if (MODE == kQC && lane == 0 && acc) atomicAdd(a.accepted, acc);
 }
 
+// ---------------------------------------------------------------------------
+// Grouped passes.  Parents are sorted by their quick code, so
+// a contiguous candidate range ("item") holds the children of a few parent
+// codes, and a child's quick code is a function of (parent code, extended
+// position, new label | closing position): an item produces at most
+// ~(LEV+1) x (labels + LEV+1) distinct child codes.  One CTA takes an item,
+// aggregates per child code in shared memory -- counts (pass A) or the
+// quick-position domain bitmaps (pass B) -- and flushes once per code: pass
+// A adds each code's count to the global hash (instead of one random hash
+// probe per warp step), pass B ORs each code's bitmap rows into its canonical
+// pattern's rows through the PositionMap (coalesced rows instead of one
+// random DRAM read-modify-write per child and position).
+constexpr int kGT = 512;                       // threads per grouped CTA
+constexpr u32 kSlotPending = 0xffffffffu;      // map entry inserted, slot not yet published
+constexpr u32 kSlotNone = 0xfffffffeu;         // no shared slot: global fallback
+
+struct GroupArgs {
+  const u64* items;     // nitems + 1 candidate-space boundaries
+  u64 nitems;
+  unsigned long long* ctr;
+  u32 mcap;             // shared map entries (power of two)
+  u32 cslots;           // shared per-code slots
+};
+
+template <int LEV>
+__device__ __forceinline__ u64 parent_code(const EEmb<LEV>& E, int LB) {
+  u32 mask = 0;
+#pragma unroll
+  for (int j = 0; j < LEV; ++j) {
+    const int a = min(E.pa[j], E.pb[j]), b = max(E.pa[j], E.pb[j]);
+    mask |= 1u << pat::pair_index(a, b, E.nv);
+  }
+  return pat::make_code(E.nv, E.lab, mask, LB);
+}
+
+// group key of every compacted parent: a 24-bit hash of its quick code
+// (colliding codes merely share a group)
+template <int LEV>
+__global__ void pkey_kernel(DevGraph g, ELevels L, const u32* __restrict__ pidx, u64 nz, int LB,
+                            u32* __restrict__ keys) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nz; i += (u64)gridDim.x * blockDim.x) {
+    EEmb<LEV> E;
+    reconstruct_e<LEV>(L, g, pidx[i], E);
+    keys[i] = (u32)(hash64(parent_code<LEV>(E, LB)) >> 40);
+  }
+}
+
+__global__ void gstart_kernel(const u32* __restrict__ keys, u64 n, u8* __restrict__ flag) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+__global__ void gather_starts_kernel(const u64* __restrict__ Wp, const u32* __restrict__ starts, u64 G,
+                                     u64* __restrict__ out) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < G; i += (u64)gridDim.x * blockDim.x)
+    out[i] = Wp[starts[i]];
+}
+
+// shared-memory map: child quick code -> per-code slot (or kSlotNone)
+template <int MODE>
+__device__ __forceinline__ u32 smap_get(unsigned long long* mkey, u32* mslot, u32 mcap, u32* used, u32 cslots,
+                                        unsigned long long* sinfo, unsigned long long* skey, u64 code,
+                                        const FsmArgs& a) {
+  u32 h = (u32)hash64(code) & (mcap - 1);
+  for (u32 probe = 0; probe < mcap; ++probe) {
+    unsigned long long k = mkey[h];
+    if (k == 0ull) {
+      const unsigned long long prev = atomicCAS(mkey + h, 0ull, (unsigned long long)code);
+      if (prev == 0ull) {
+        const u32 sl = atomicAdd(used, 1u);
+        u32 v = kSlotNone;
+        if (sl < cslots) {
+          v = sl;
+          skey[sl] = code;
+          if (MODE == kDomain) {
+            // the code's canonical pattern and PositionMap; a bitmap only if
+            // the pattern has one in this round
+            const u64 info = hash_info(a.H, hash_find(a.H, code));
+            const u32 bs = a.bslot[(u32)(info >> 32)];
+            sinfo[sl] = (bs >= a.round_lo && bs < a.round_hi) ? (((u64)(bs - a.round_lo) << 32) | (u32)info) : ~0ull;
+          } else {
+            sinfo[sl] = 0ull;
+          }
+        }
+        __threadfence_block();
+        *(volatile u32*)(mslot + h) = v;
+        return v;
+      }
+      k = prev;
+    }
+    if (k == code) {
+      u32 v;
+      while ((v = *(volatile u32*)(mslot + h)) == kSlotPending) {
+      }
+      return v;
+    }
+    h = (h + 1) & (mcap - 1);
+  }
+  return kSlotNone;
+}
+
+template <int LEV, int MODE>
+__global__ void __launch_bounds__(kGT, 1) egroup_kernel(FsmArgs a, GroupArgs ga) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  unsigned long long* mkey = reinterpret_cast<unsigned long long*>(gsm);
+  unsigned long long* sinfo = mkey + ga.mcap;    // kQC: count; kDomain: (bitmap slot << 32 | perm) or ~0
+  unsigned long long* skey = sinfo + ga.cslots;  // code per slot
+  u32* mslot = reinterpret_cast<u32*>(skey + ga.cslots);
+  u32* sbm = mslot + ga.mcap;                    // kDomain: [cslots][kpos][words]
+  __shared__ u64 s_item;
+  __shared__ u32 s_used;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int NW = kGT / 32;
+  const DevGraph& g = a.g;
+  const u64 rowlen = (u64)a.kpos * a.words;
+  unsigned long long acc = 0;
+  for (;;) {
+    __syncthreads();  // the previous item's flush is done
+    if (threadIdx.x == 0) {
+      s_item = atomicAdd(ga.ctr, 1ull);
+      s_used = 0;
+    }
+    for (u32 i = threadIdx.x; i < ga.mcap; i += kGT) {
+      mkey[i] = 0ull;
+      mslot[i] = kSlotPending;
+    }
+    if (MODE == kDomain) {
+      uint4* z = reinterpret_cast<uint4*>(sbm);
+      const u64 n4 = (u64)ga.cslots * rowlen / 4;
+      for (u64 i = threadIdx.x; i < n4; i += kGT) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    const u64 item = s_item;
+    if (item >= ga.nitems) break;
+    const u64 j0 = ldg(ga.items + item), j1 = ldg(ga.items + item + 1);
+    const u64 span = ((j1 - j0 + NW - 1) / NW + 31) & ~31ull;
+    const u64 wj0 = j0 + (u64)wid * span, wj1 = min(j1, wj0 + span);
+    if (wj0 < wj1) {
+      u64 pr = 0;
+      if (lane == 0) pr = upper_bound_prev(a.Wp, 0, a.np + 1, wj0);
+      u64 P0 = __shfl_sync(0xffffffffu, pr, 0);
+      ECursor<LEV> cur;
+      for (u64 jb = wj0; jb < wj1; jb += 32) {
+        const u64 j = jb + lane;
+        const u64 x = (P0 + 1 + lane <= a.np) ? ldg(a.Wp + P0 + 1 + lane) : ~0ull;
+        const u32 bit = (x - jb < 32) ? (1u << (u32)(x - jb)) : 0u;
+        const u32 starts = __reduce_or_sync(0xffffffffu, bit);
+        const u64 myp = P0 + __popc(starts & (lanemask_lt() | (1u << lane)));
+        P0 += __popc(starts);
+        bool ok = false;
+        u64 code = 0;
+        u32 cv[LEV + 2];
+        int cnv = 0;
+        if (j < wj1) {
+          cur.load(a, myp);
+          int q;
+          const u32 w = cur.candidate(g, j, q);
+          int r = cur.E.nv;
+#pragma unroll
+          for (int i = 0; i < LEV + 1; ++i)
+            if (i < cur.E.nv && cur.E.v[i] == w) r = i;
+          ok = edge_to_add<LEV>(cur.E, q, w, r);
+          if (ok) code = child_code<LEV>(cur.E, g, q, w, r, a.LB, cv, cnv);
+        }
+        const u32 mask = __ballot_sync(0xffffffffu, ok);
+        if (!mask) continue;
+        const u32 peers = __match_any_sync(0xffffffffu, ok ? code : ~0ull);
+        const int leader = __ffs(peers) - 1;
+        u32 slot = kSlotNone;
+        if (ok && lane == leader) slot = smap_get<MODE>(mkey, mslot, ga.mcap, &s_used, ga.cslots, sinfo, skey, code, a);
+        slot = __shfl_sync(0xffffffffu, slot, leader);
+        if (MODE == kQC) {
+          acc += __popc(mask);
+          if (ok && lane == leader) {
+            if (slot != kSlotNone) atomicAdd(sinfo + slot, (unsigned long long)__popc(peers));
+            else hash_add(a.H, code, __popc(peers));
+          }
+        } else {
+          // lanes with the same code and parent write the parent's positions once
+          const u32 sib = peers & __match_any_sync(0xffffffffu, myp);
+          const int first = (lane == __ffs(sib) - 1) ? 0 : cur.E.nv;
+          if (ok) {
+            if (slot != kSlotNone) {
+              if (sinfo[slot] != ~0ull)
+                bitmap_or<LEV + 2>(sbm + (u64)slot * rowlen, a.words, a.lrank, 0u, false, cv, cnv, first);
+            } else {
+              domain_or<LEV + 2>(a, hash_info(a.H, hash_find(a.H, code)), cv, cnv, first);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- flush once per code
+    const u32 used = min(s_used, ga.cslots);
+    if (MODE == kQC) {
+      for (u32 sl = threadIdx.x; sl < used; sl += kGT)
+        if (sinfo[sl]) hash_add(a.H, skey[sl], sinfo[sl]);
+    } else {
+      for (u64 row = wid; row < (u64)used * a.kpos; row += NW) {
+        const u32 sl = (u32)(row / a.kpos);
+        const int i = (int)(row % a.kpos);
+        const u64 info = sinfo[sl];
+        if (info == ~0ull || i >= pat::code_nv(skey[sl])) continue;
+        const u32 cp = ((u32)info >> (3 * i)) & 7u;
+        u32* dst = a.bitmaps + ((info >> 32) * a.kpos + cp) * a.words;
+        const u32* src = sbm + (u64)sl * rowlen + (u64)i * a.words;
+        for (u64 w = lane; w < a.words; w += 32) {
+          const u32 v = src[w];
+          if (v) atomicOr(dst + w, v);
+        }
+      }
+    }
+  }
+  if (MODE == kQC && lane == 0 && acc) atomicAdd(a.accepted, acc);  // acc is warp-uniform
+}
+
 // ---- level 1 (single edges): reduce + filter before the loop
 __device__ __forceinline__ u64 l1_code(const DevGraph& g, u32 u, u32 v, int LB) {
   u32 lab[2] = {ldg(g.lab + u), ldg(g.lab + v)};
@@ -999,6 +1216,118 @@ struct Fsm {
     ++tl.launches;
   }
 
+  // ---------------------------------------------------------- grouped passes
+  struct Groups {
+    DBuf<u64> items;
+    u64 nitems = 0;
+    bool on = false;
+  };
+
+  // Sorts the compacted parents by a hash of their quick code (24-bit radix
+  // sort of (key, parent)) so that each item of the candidate space holds the
+  // children of a few parent codes.
+  template <int LEV>
+  void sort_parents(const ELevels& L, DBuf<u32>& pidx, u64 nz, DBuf<u32>& keys) {
+    keys.alloc(nz, s);
+    pkey_kernel<LEV><<<grid1(nz), 256, 0, s>>>(g, L, pidx.get(), nz, LB, keys.get());
+    GPM_CUDA(cudaGetLastError());
+    DBuf<u32> k2(nz, s), p2(nz, s);
+    size_t tmp = 0;
+    GPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys.get(), k2.get(), pidx.get(), p2.get(), (int64_t)nz, 0,
+                                             24, s));
+    DBuf<u8> t(tmp, s);
+    GPM_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, keys.get(), k2.get(), pidx.get(), p2.get(), (int64_t)nz, 0,
+                                             24, s));
+    tl.launches += 5;
+    keys = std::move(k2);
+    pidx = std::move(p2);
+  }
+
+  // Items over the sorted candidate space [0, W): each parent group is one
+  // item, consecutive small groups are merged up to kMinItem candidates and
+  // large groups split into kMaxItem pieces.
+  void build_items(const DBuf<u32>& keys, u64 nz, const DBuf<u64>& Wp, u64 W, Groups& gr) {
+    constexpr u64 kMinItem = u64(1) << 16, kMaxItem = u64(1) << 21;
+    DBuf<u8> flag(nz, s);
+    gstart_kernel<<<grid1(nz), 256, 0, s>>>(keys.get(), nz, flag.get());
+    DBuf<u32> starts(nz, s);
+    DBuf<u64> ng(1, s);
+    size_t tmp = 0;
+    thrust::counting_iterator<u32> it(0);
+    GPM_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, it, flag.get(), starts.get(), ng.get(), (int64_t)nz, s));
+    DBuf<u8> t(tmp, s);
+    GPM_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, it, flag.get(), starts.get(), ng.get(), (int64_t)nz, s));
+    const u64 G = d2h(ng.get());
+    DBuf<u64> gw(G, s);
+    gather_starts_kernel<<<grid1(G), 256, 0, s>>>(Wp.get(), starts.get(), G, gw.get());
+    GPM_CUDA(cudaGetLastError());
+    tl.launches += 4;
+    std::vector<u64> gs(G);
+    GPM_CUDA(cudaMemcpyAsync(gs.data(), gw.get(), sizeof(u64) * G, cudaMemcpyDeviceToHost, s));
+    sync();
+    std::vector<u64> b{0};
+    for (u64 i = 0; i < G; ++i) {
+      const u64 a0 = gs[i], a1 = i + 1 < G ? gs[i + 1] : W;
+      if (a1 - a0 > kMaxItem) {
+        if (b.back() < a0) b.push_back(a0);
+        const u64 np_ = (a1 - a0 + kMaxItem - 1) / kMaxItem;
+        for (u64 q = 1; q < np_; ++q) b.push_back(a0 + (a1 - a0) * q / np_);
+        b.push_back(a1);
+      } else if (a1 - b.back() >= kMinItem) {
+        b.push_back(a1);
+      }
+    }
+    if (b.back() < W) b.push_back(W);
+    gr.nitems = b.size() - 1;
+    gr.items.alloc(b.size(), s);
+    GPM_CUDA(cudaMemcpyAsync(gr.items.get(), b.data(), sizeof(u64) * b.size(), cudaMemcpyHostToDevice, s));
+    sync();
+    trace("groups -> items", (double)G, (double)gr.nitems);
+  }
+
+  // shared-memory geometry of a grouped pass; false = does not fit (the
+  // ungrouped kernels run instead)
+  bool group_geometry(int mode, int kpos, u64 words, GroupArgs& ga, size_t& smem) {
+    int maxs = 0;
+    GPM_CUDA(cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, G.device));
+    const size_t avail = (size_t)maxs - 1024;  // static shared + slack
+    u32 cs = 1024;
+    if (mode == kDomain) {
+      const size_t per = (size_t)kpos * words * 4 + 16 + 24;  // rows + sinfo/skey + 2 map entries
+      cs = (u32)std::min<size_t>(256, avail / per);
+      if (cs < 16) return false;
+    }
+    u32 mc = 64;
+    while (mc < 2 * cs) mc <<= 1;
+    ga.mcap = mc;
+    ga.cslots = cs;
+    smem = (size_t)mc * 12 + (size_t)cs * 16 + (mode == kDomain ? (size_t)cs * kpos * words * 4 : 0);
+    return smem <= avail;
+  }
+
+  template <int LEV>
+  void launch_group(FsmArgs& a, const Groups& gr, int mode, const char* name, double bytes) {
+    GroupArgs ga{};
+    size_t smem = 0;
+    if (!group_geometry(mode, a.kpos, a.words, ga, smem)) throw Error(GPM_EINVAL, "fsm: grouped pass does not fit");
+    ga.items = gr.items.get();
+    ga.nitems = gr.nitems;
+    ga.ctr = d_ctr.get();
+    auto kern = mode == kQC ? egroup_kernel<LEV, kQC> : egroup_kernel<LEV, kDomain>;
+    GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGT, smem));
+    occ = std::max(1, occ);
+    const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sms * occ, gr.nitems));
+    GPM_CUDA(cudaMemsetAsync(d_ctr.get(), 0, sizeof(unsigned long long), s));
+    st.paths |= GPM_PATH_FSM_GROUPED;
+    size_t ev = tl.begin(std::string(name) + "_L" + std::to_string(LEV), bytes);
+    kern<<<(unsigned)blocks, kGT, smem, s>>>(a, ga);
+    GPM_CUDA(cudaGetLastError());
+    tl.end(ev);
+    ++tl.launches;
+  }
+
   // Extends level LEV (np parents) -> reduce (+ filter into out arrays unless last)
   template <int LEV>
   void extend_level(const ELevels& L, u64 np, bool last, DBuf<u32>& oi, DBuf<u32>& ov, DBuf<u8>& oh, u64& nout) {
@@ -1023,6 +1352,16 @@ struct Fsm {
       GPM_CUDA(cub::DeviceSelect::If(t.get(), tmp, it, pidx.get(), nsel.get(), (int64_t)np, NonZeroW{w.get()}, s));
       nz = d2h(nsel.get());
     }
+    // grouped passes: parents sorted by quick code
+    Groups gr;
+    DBuf<u32> gkeys_sorted;
+    {
+      GroupArgs probe{};
+      size_t sm = 0;
+      gr.on = nz && !std::getenv("GPM_FSM_UNGROUPED") &&
+              group_geometry(kDomain, LEV + 2, (max_class + 31) / 32, probe, sm);
+    }
+    if (gr.on) sort_parents<LEV>(L, pidx, nz, gkeys_sorted);
     DBuf<u64> Wp(nz + 1, s);
     GPM_CUDA(cudaMemsetAsync(Wp.get() + nz, 0, sizeof(u64), s));
     if (nz) {
@@ -1033,6 +1372,8 @@ struct Fsm {
     scan_inplace(Wp.get(), nz + 1, s);
     const u64 W = d2h(Wp.get() + nz);
     const u64 nvs = d2h(nvsum.get());
+    if (gr.on && W) build_items(gkeys_sorted, nz, Wp, W, gr);
+    gkeys_sorted.release();
     st.candidates[LEV] += W;
     const double bytes_in = 8.0 * LEV * np + 16.0 * nvs + 4.0 * W;
     st.balg += bytes_in;
@@ -1077,7 +1418,7 @@ struct Fsm {
     DBuf<u32> qbm;
     DBuf<int> qover(1, s);
     u64 qcap = 0;
-    if (last && nb && !std::getenv("GPM_FSM_TWO_PASS")) {
+    if (last && nb && !gr.on && !std::getenv("GPM_FSM_TWO_PASS")) {
       qcap = std::min<u64>(cap / 2, budget / 2 / std::max<u64>(1, per_id));
       if (qcap >= 1024) qbm.alloc(qcap * kposL * wordsL, s);
       else qcap = 0;
@@ -1097,7 +1438,8 @@ struct Fsm {
           a.words = wordsL;
           a.lrank = lrank.get();
         }
-        launch<LEV>(a, kQC, qcap ? "fsm_extend_qc_domain" : "fsm_extend_qc", bytes_in);
+        if (gr.on) launch_group<LEV>(a, gr, kQC, "fsm_group_qc", bytes_in);
+        else launch<LEV>(a, kQC, qcap ? "fsm_extend_qc_domain" : "fsm_extend_qc", bytes_in);
       }
       if (d2h(R.overflow.get()) == 0) break;
       cap <<= 3;
@@ -1133,7 +1475,8 @@ struct Fsm {
       a.kpos = kpos;
       a.round_lo = lo;
       a.round_hi = hi;
-      launch<LEV>(a, kDomain, "fsm_extend_domain", bytes_in);
+      if (gr.on) launch_group<LEV>(a, gr, kDomain, "fsm_group_domain", bytes_in);
+      else launch<LEV>(a, kDomain, "fsm_extend_domain", bytes_in);
     });
     record(R, LEV + 1);
     trace("mni+record", (double)R.P);
