@@ -44,7 +44,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr u64 kBatch = 2048;
 constexpr int kMaxEdges = 5;  // k <= 6
-enum { kQC = 0, kDomain = 1, kSCount = 2, kSWrite = 3 };
+enum { kQC = 0, kDomain = 1, kSCount = 2, kSWrite = 3, kQCD = 4 };
 
 struct ELevels {
   const u32* idx[kMaxEdges + 1];
@@ -540,10 +540,156 @@ __global__ void gather_starts_kernel(const u64* __restrict__ Wp, const u32* __re
     out[i] = Wp[starts[i]];
 }
 
+// Per-lane parent descriptor for the grouped passes: everything the
+// per-candidate test needs, precomputed once when the lane's parent changes,
+// so that is_auto_canonical_edge becomes one packed-pair compare and the
+// child's quick code one OR (new vertex) -- the generic edge_to_add /
+// child_code (above) rebuild position arrays and pattern codes per candidate.
+//   edge_to_add: n = (min, max) of the new edge; accept iff
+//   n is not an edge of the parent, r >= q for a closing edge, and n > e_1
+//   and n > e_s for every s > p, p = step(q) (min with step(r) when closing),
+//   i.e. n > thr[p] with thr[p] = max(e_1, max_{s>p} e_s) (packed pairs
+//   compare lexicographically as integers).
+template <int LEV>
+struct FCur {
+  static constexpr int MV = LEV + 1;
+  u64 cp = ~0ull, cWb = 0, cWe = 0;
+  u32 parent = 0;
+  int nv = 0;
+  u32 v[MV];       // parent vertices (~0 past nv)
+  u32 lr[MV];      // label-local ranks of the parent vertices (domain modes)
+  u32 cend[MV];    // cumulative candidate ends per position (parent-local)
+  u64 cbase[MV];   // col index of candidate `local` at position q = cbase[q] + local
+  u64 dupe[LEV];   // parent edges, packed (min << 32 | max)
+  u64 thr[LEV + 1];
+  u64 newc[MV];    // child code for a new vertex from q (new label bits zero)
+  u32 stp;         // step of position q in bits [4q, 4q+4)
+  u32 pmask;       // parent position-pair mask (nv positions)
+  u32 lshift;      // npairs(nv + 1): new label shift
+  u64 labp;        // parent labels packed (pattern.cuh order)
+
+  __device__ __forceinline__ void load(const FsmArgs& a, u64 p, bool want_lr) {
+    if (p == cp) return;
+    cp = p;
+    cWb = ldg(a.Wp + p);
+    cWe = ldg(a.Wp + p + 1);
+    parent = ldg(a.pidx + p);
+    EEmb<LEV> E;
+    reconstruct_e<LEV>(a.L, a.g, parent, E);
+    nv = E.nv;
+    pmask = 0;
+#pragma unroll
+    for (int j = 0; j < LEV; ++j) {
+      const int x = min(E.pa[j], E.pb[j]), y = max(E.pa[j], E.pb[j]);
+      pmask |= 1u << pat::pair_index(x, y, nv);
+      dupe[j] = ((u64)E.e0[j] << 32) | E.e1[j];
+    }
+#pragma unroll
+    for (int pp = 1; pp <= LEV; ++pp) {
+      u64 t = dupe[0];
+#pragma unroll
+      for (int s2 = 2; s2 <= LEV; ++s2)
+        if (s2 > pp) t = max(t, dupe[s2 - 1]);
+      thr[pp] = t;
+    }
+    thr[0] = thr[1];
+    labp = 0;
+    stp = 0;
+    u32 lab[MV + 1];
+    u32 acc = 0;
+#pragma unroll
+    for (int q = 0; q < MV; ++q) {
+      const bool in = q < nv;
+      v[q] = in ? E.v[q] : 0xffffffffu;
+      lab[q] = in ? E.lab[q] : 0u;
+      if (in) labp = (labp << a.LB) | lab[q];
+      stp |= (u32)(in ? E.step[q] : 0) << (4 * q);
+      u64 b = 0;
+      u32 d = 0;
+      if (in) {
+        b = ldg(a.g.off + v[q]);
+        d = (u32)(ldg(a.g.off + v[q] + 1) - b);
+      }
+      cbase[q] = b - acc;
+      acc += d;
+      cend[q] = acc;
+      lr[q] = (in && want_lr) ? ldg(a.lrank + v[q]) : 0u;
+    }
+    // new-vertex child codes: parent mask re-indexed to nv + 1 positions
+    u32 m1 = 0;
+    for (int x = 0; x < nv; ++x)
+      for (int y = x + 1; y < nv; ++y)
+        if (pmask >> pat::pair_index(x, y, nv) & 1u) m1 |= 1u << pat::pair_index(x, y, nv + 1);
+    u32 lab2[MV + 1];
+#pragma unroll
+    for (int i = 0; i <= MV; ++i) lab2[i] = i < nv ? lab[i] : 0u;
+#pragma unroll
+    for (int q = 0; q < MV; ++q)
+      newc[q] = q < nv ? pat::make_code(nv + 1, lab2, m1 | (1u << pat::pair_index(q, nv, nv + 1)), a.LB) : 0ull;
+    lshift = (u32)pat::npairs(nv + 1);
+  }
+  __device__ __forceinline__ void locate(const FsmArgs& a, u64 j, u64 pa, u64 pb, bool want_lr) {
+    if (cp != ~0ull && j < cWe && j >= cWb) return;
+    const u64 lo = (cp == ~0ull || j < cWb) ? pa : cp + 1;
+    load(a, upper_bound_prev(a.Wp, lo, pb + 1, j), want_lr);
+  }
+
+  // register-resident select (a dynamic index would put the array in local memory)
+  template <class T, int N>
+  __device__ __forceinline__ static T sel(const T (&arr)[N], int i) {
+    T x = arr[0];
+#pragma unroll
+    for (int t = 1; t < N; ++t)
+      if (i == t) x = arr[t];
+    return x;
+  }
+
+  // Candidate j of the loaded parent: accepted?  Fills the child's code and
+  // its new vertex w with w's position r (nv if new).
+  __device__ __forceinline__ bool eval(const FsmArgs& a, u64 j, u64& code, u32& w, int& r) const {
+    const u32 local = (u32)(j - cWb);
+    int q = 0;
+#pragma unroll
+    for (int t = 0; t < MV - 1; ++t) q += local >= cend[t];
+    w = ldg(a.g.col + sel(cbase, q) + local);
+    r = nv;
+#pragma unroll
+    for (int i = 0; i < MV; ++i)
+      if (v[i] == w) r = i;
+    const u32 x = sel(v, q);
+    const u64 n = w < x ? (((u64)w << 32) | x) : (((u64)x << 32) | w);
+    const int sq = (int)((stp >> (4 * q)) & 15u);
+    if (r == nv) {
+      if (!(n > sel(thr, sq))) return false;
+      code = sel(newc, q) | ((u64)ldg(a.g.lab + w) << lshift);
+      return true;
+    }
+    // closing edge (rare): both endpoints in the parent
+    if (r < q) return false;
+#pragma unroll
+    for (int jj = 0; jj < LEV; ++jj)
+      if (dupe[jj] == n) return false;
+    const int sr = (int)((stp >> (4 * r)) & 15u);
+    if (!(n > sel(thr, min(sq, sr)))) return false;
+    u32 lab[MV];
+    u64 lp = labp;
+#pragma unroll
+    for (int i = MV - 1; i >= 0; --i) {
+      lab[i] = 0;
+      if (i < nv) {
+        lab[i] = (u32)(lp & ((u64(1) << a.LB) - 1));
+        lp >>= a.LB;
+      }
+    }
+    code = pat::make_code(nv, lab, pmask | (1u << pat::pair_index(q, r, nv)), a.LB);
+    return true;
+  }
+};
+
 // shared-memory map: child quick code -> per-code slot (or kSlotNone)
 template <int MODE>
 __device__ __forceinline__ u32 smap_get(unsigned long long* mkey, u32* mslot, u32 mcap, u32* used, u32 cslots,
-                                        unsigned long long* sinfo, unsigned long long* skey, u64 code,
+                                        unsigned long long* sinfo, unsigned long long* skey, u32* sid, u64 code,
                                         const FsmArgs& a) {
   u32 h = (u32)hash64(code) & (mcap - 1);
   for (u32 probe = 0; probe < mcap; ++probe) {
@@ -552,50 +698,55 @@ __device__ __forceinline__ u32 smap_get(unsigned long long* mkey, u32* mslot, u3
       const unsigned long long prev = atomicCAS(mkey + h, 0ull, (unsigned long long)code);
       if (prev == 0ull) {
         const u32 sl = atomicAdd(used, 1u);
-        u32 v = kSlotNone;
+        u32 val = kSlotNone;
         if (sl < cslots) {
-          v = sl;
+          val = sl;
           skey[sl] = code;
+          sinfo[sl] = 0ull;
           if (MODE == kDomain) {
             // the code's canonical pattern and PositionMap; a bitmap only if
             // the pattern has one in this round
             const u64 info = hash_info(a.H, hash_find(a.H, code));
             const u32 bs = a.bslot[(u32)(info >> 32)];
             sinfo[sl] = (bs >= a.round_lo && bs < a.round_hi) ? (((u64)(bs - a.round_lo) << 32) | (u32)info) : ~0ull;
-          } else {
-            sinfo[sl] = 0ull;
+          } else if (MODE == kQCD) {
+            sid[sl] = hash_add(a.H, code, 0ull);  // dense quick-code id (0: table overflow)
           }
         }
         __threadfence_block();
-        *(volatile u32*)(mslot + h) = v;
-        return v;
+        *(volatile u32*)(mslot + h) = val;
+        return val;
       }
       k = prev;
     }
     if (k == code) {
-      u32 v;
-      while ((v = *(volatile u32*)(mslot + h)) == kSlotPending) {
+      u32 val;
+      while ((val = *(volatile u32*)(mslot + h)) == kSlotPending) {
       }
-      return v;
+      return val;
     }
     h = (h + 1) & (mcap - 1);
   }
   return kSlotNone;
 }
 
+// MODE kQC: quick-code counts; kQCD: counts + quick-position domain bitmaps
+// per quick-code id (the fused last level); kDomain: canonical-position
+// domain bitmaps of the current round (two-pass levels).
 template <int LEV, int MODE>
 __global__ void __launch_bounds__(kGT, 1) egroup_kernel(FsmArgs a, GroupArgs ga) {
   extern __shared__ __align__(16) unsigned char gsm[];
   unsigned long long* mkey = reinterpret_cast<unsigned long long*>(gsm);
-  unsigned long long* sinfo = mkey + ga.mcap;    // kQC: count; kDomain: (bitmap slot << 32 | perm) or ~0
+  unsigned long long* sinfo = mkey + ga.mcap;    // kQC/kQCD: count; kDomain: (bitmap slot << 32 | perm) or ~0
   unsigned long long* skey = sinfo + ga.cslots;  // code per slot
   u32* mslot = reinterpret_cast<u32*>(skey + ga.cslots);
-  u32* sbm = mslot + ga.mcap;                    // kDomain: [cslots][kpos][words]
+  u32* sid = mslot + ga.mcap;                    // kQCD: dense quick-code id per slot
+  u32* sbm = sid + ga.cslots;                    // kDomain / kQCD: [cslots][kpos][words]
+  constexpr bool kRows = MODE != kQC;
   __shared__ u64 s_item;
   __shared__ u32 s_used;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int NW = kGT / 32;
-  const DevGraph& g = a.g;
   const u64 rowlen = (u64)a.kpos * a.words;
   unsigned long long acc = 0;
   for (;;) {
@@ -608,10 +759,9 @@ __global__ void __launch_bounds__(kGT, 1) egroup_kernel(FsmArgs a, GroupArgs ga)
       mkey[i] = 0ull;
       mslot[i] = kSlotPending;
     }
-    if (MODE == kDomain) {
-      uint4* z = reinterpret_cast<uint4*>(sbm);
-      const u64 n4 = (u64)ga.cslots * rowlen / 4;
-      for (u64 i = threadIdx.x; i < n4; i += kGT) z[i] = make_uint4(0, 0, 0, 0);
+    if (kRows) {
+      const u64 nz = (u64)ga.cslots * rowlen;
+      for (u64 i = threadIdx.x; i < nz; i += kGT) sbm[i] = 0u;
     }
     __syncthreads();
     const u64 item = s_item;
@@ -623,7 +773,7 @@ __global__ void __launch_bounds__(kGT, 1) egroup_kernel(FsmArgs a, GroupArgs ga)
       u64 pr = 0;
       if (lane == 0) pr = upper_bound_prev(a.Wp, 0, a.np + 1, wj0);
       u64 P0 = __shfl_sync(0xffffffffu, pr, 0);
-      ECursor<LEV> cur;
+      FCur<LEV> cur;
       for (u64 jb = wj0; jb < wj1; jb += 32) {
         const u64 j = jb + lane;
         const u64 x = (P0 + 1 + lane <= a.np) ? ldg(a.Wp + P0 + 1 + lane) : ~0ull;
@@ -633,70 +783,114 @@ __global__ void __launch_bounds__(kGT, 1) egroup_kernel(FsmArgs a, GroupArgs ga)
         P0 += __popc(starts);
         bool ok = false;
         u64 code = 0;
-        u32 cv[LEV + 2];
-        int cnv = 0;
+        u32 w = 0;
+        int r = 0;
         if (j < wj1) {
-          cur.load(a, myp);
-          int q;
-          const u32 w = cur.candidate(g, j, q);
-          int r = cur.E.nv;
-#pragma unroll
-          for (int i = 0; i < LEV + 1; ++i)
-            if (i < cur.E.nv && cur.E.v[i] == w) r = i;
-          ok = edge_to_add<LEV>(cur.E, q, w, r);
-          if (ok) code = child_code<LEV>(cur.E, g, q, w, r, a.LB, cv, cnv);
+          cur.load(a, myp, kRows);
+          ok = cur.eval(a, j, code, w, r);
         }
         const u32 mask = __ballot_sync(0xffffffffu, ok);
         if (!mask) continue;
         const u32 peers = __match_any_sync(0xffffffffu, ok ? code : ~0ull);
         const int leader = __ffs(peers) - 1;
         u32 slot = kSlotNone;
-        if (ok && lane == leader) slot = smap_get<MODE>(mkey, mslot, ga.mcap, &s_used, ga.cslots, sinfo, skey, code, a);
+        if (ok && lane == leader)
+          slot = smap_get<MODE>(mkey, mslot, ga.mcap, &s_used, ga.cslots, sinfo, skey, sid, code, a);
         slot = __shfl_sync(0xffffffffu, slot, leader);
-        if (MODE == kQC) {
+        if (MODE != kDomain) {
           acc += __popc(mask);
           if (ok && lane == leader) {
             if (slot != kSlotNone) atomicAdd(sinfo + slot, (unsigned long long)__popc(peers));
-            else hash_add(a.H, code, __popc(peers));
           }
-        } else {
-          // lanes with the same code and parent write the parent's positions once
-          const u32 sib = peers & __match_any_sync(0xffffffffu, myp);
-          const int first = (lane == __ffs(sib) - 1) ? 0 : cur.E.nv;
-          if (ok) {
-            if (slot != kSlotNone) {
-              if (sinfo[slot] != ~0ull)
-                bitmap_or<LEV + 2>(sbm + (u64)slot * rowlen, a.words, a.lrank, 0u, false, cv, cnv, first);
-            } else {
-              domain_or<LEV + 2>(a, hash_info(a.H, hash_find(a.H, code)), cv, cnv, first);
+        }
+        if (MODE == kQC) {
+          if (ok && lane == leader && slot == kSlotNone) hash_add(a.H, code, __popc(peers));
+          continue;
+        }
+        // ---- domains: the child's vertices at its quick positions
+        // (lanes with the same code and parent write the parent's positions once)
+        const u32 sib = peers & __match_any_sync(0xffffffffu, myp);
+        const int first = (lane == __ffs(sib) - 1) ? 0 : cur.nv;
+        u32* row = nullptr;
+        u32 perm = 0;
+        bool permute = false;
+        if (MODE == kQCD && ok && slot == kSlotNone) {
+          // no shared slot: straight into the code's global rows (old path)
+          u32 id = 0;
+          if (lane == leader) id = hash_add(a.H, code, __popc(peers));
+          id = __shfl_sync(peers, id, leader);
+          if (id && id - 1 >= a.qcap) *a.qover = 1;
+          else if (id) row = a.qbm + (u64)(id - 1) * rowlen;
+        } else if (ok && slot != kSlotNone) {
+          if (MODE != kDomain || sinfo[slot] != ~0ull) row = sbm + (u64)slot * rowlen;  // kDomain: bitmap this round?
+        } else if (ok) {  // kDomain without a shared slot
+          const u64 info = hash_info(a.H, hash_find(a.H, code));
+          const u32 bs = a.bslot[(u32)(info >> 32)];
+          if (bs >= a.round_lo && bs < a.round_hi) {
+            row = a.bitmaps + (u64)(bs - a.round_lo) * rowlen;
+            perm = (u32)info;
+            permute = true;
+          }
+        }
+        if (row) {
+          const int cnv = (r == cur.nv) ? cur.nv + 1 : cur.nv;
+          const u32 wl = (r == cur.nv) ? ldg(a.lrank + w) : 0u;
+          u32* wp[LEV + 2];
+          u32 bm[LEV + 2], old[LEV + 2];
+#pragma unroll
+          for (int i = 0; i < LEV + 2; ++i) {
+            wp[i] = nullptr;
+            if (i >= first && i < cnv) {
+              const u32 lri = (i < LEV + 1 && i < cur.nv) ? FCur<LEV>::sel(cur.lr, i < LEV + 1 ? i : 0) : wl;
+              const u32 cp = permute ? (perm >> (3 * i)) & 7u : (u32)i;
+              wp[i] = row + (u64)cp * a.words + (lri >> 5);
+              bm[i] = 1u << (lri & 31);
             }
           }
+#pragma unroll
+          for (int i = 0; i < LEV + 2; ++i) old[i] = wp[i] ? *wp[i] : 0u;
+#pragma unroll
+          for (int i = 0; i < LEV + 2; ++i)
+            if (wp[i] && !(old[i] & bm[i])) atomicOr(wp[i], bm[i]);
         }
       }
     }
     __syncthreads();
     // ---- flush once per code
     const u32 used = min(s_used, ga.cslots);
-    if (MODE == kQC) {
+    if (MODE != kDomain) {
       for (u32 sl = threadIdx.x; sl < used; sl += kGT)
         if (sinfo[sl]) hash_add(a.H, skey[sl], sinfo[sl]);
-    } else {
+    }
+    if (kRows) {
       for (u64 row = wid; row < (u64)used * a.kpos; row += NW) {
         const u32 sl = (u32)(row / a.kpos);
         const int i = (int)(row % a.kpos);
-        const u64 info = sinfo[sl];
-        if (info == ~0ull || i >= pat::code_nv(skey[sl])) continue;
-        const u32 cp = ((u32)info >> (3 * i)) & 7u;
-        u32* dst = a.bitmaps + ((info >> 32) * a.kpos + cp) * a.words;
+        if (i >= pat::code_nv(skey[sl])) continue;
+        u32* dst;
+        if (MODE == kDomain) {
+          const u64 info = sinfo[sl];
+          if (info == ~0ull) continue;
+          const u32 cp = ((u32)info >> (3 * i)) & 7u;
+          dst = a.bitmaps + ((info >> 32) * a.kpos + cp) * a.words;
+        } else {
+          const u32 id = sid[sl];
+          if (!id) continue;
+          if (id - 1 >= a.qcap) {
+            if (lane == 0) *a.qover = 1;
+            continue;
+          }
+          dst = a.qbm + ((u64)(id - 1) * a.kpos + i) * a.words;
+        }
         const u32* src = sbm + (u64)sl * rowlen + (u64)i * a.words;
         for (u64 w = lane; w < a.words; w += 32) {
-          const u32 v = src[w];
-          if (v) atomicOr(dst + w, v);
+          const u32 val = src[w];
+          if (val) atomicOr(dst + w, val);
         }
       }
     }
   }
-  if (MODE == kQC && lane == 0 && acc) atomicAdd(a.accepted, acc);  // acc is warp-uniform
+  if (MODE != kDomain && lane == 0 && acc) atomicAdd(a.accepted, acc);  // acc is warp-uniform
 }
 
 // ---- level 1 (single edges): reduce + filter before the loop
@@ -1292,16 +1486,26 @@ struct Fsm {
     GPM_CUDA(cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, G.device));
     const size_t avail = (size_t)maxs - 1024;  // static shared + slack
     u32 cs = 1024;
-    if (mode == kDomain) {
-      const size_t per = (size_t)kpos * words * 4 + 16 + 24;  // rows + sinfo/skey + 2 map entries
-      cs = (u32)std::min<size_t>(256, avail / per);
+    if (mode != kQC) {
+      const size_t per = (size_t)kpos * words * 4 + 20 + 24;  // rows + sinfo/skey/sid + 2 map entries
+      cs = (u32)std::min<size_t>(256, avail / per) & ~7u;
       if (cs < 16) return false;
     }
     u32 mc = 64;
     while (mc < 2 * cs) mc <<= 1;
     ga.mcap = mc;
     ga.cslots = cs;
-    smem = (size_t)mc * 12 + (size_t)cs * 16 + (mode == kDomain ? (size_t)cs * kpos * words * 4 : 0);
+    auto bytes = [&](u32 c, u32 m) {
+      return (size_t)m * 12 + (size_t)c * 20 + (mode != kQC ? (size_t)c * kpos * words * 4 : 0);
+    };
+    while (bytes(cs, mc) > avail && cs > 16) {
+      cs -= 8;
+      mc = 64;
+      while (mc < 2 * cs) mc <<= 1;
+    }
+    ga.mcap = mc;
+    ga.cslots = cs;
+    smem = bytes(cs, mc);
     return smem <= avail;
   }
 
@@ -1313,7 +1517,7 @@ struct Fsm {
     ga.items = gr.items.get();
     ga.nitems = gr.nitems;
     ga.ctr = d_ctr.get();
-    auto kern = mode == kQC ? egroup_kernel<LEV, kQC> : egroup_kernel<LEV, kDomain>;
+    auto kern = mode == kQC ? egroup_kernel<LEV, kQC> : mode == kQCD ? egroup_kernel<LEV, kQCD> : egroup_kernel<LEV, kDomain>;
     GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGT, smem));
@@ -1418,7 +1622,7 @@ struct Fsm {
     DBuf<u32> qbm;
     DBuf<int> qover(1, s);
     u64 qcap = 0;
-    if (last && nb && !gr.on && !std::getenv("GPM_FSM_TWO_PASS")) {
+    if (last && nb && !std::getenv("GPM_FSM_TWO_PASS")) {
       qcap = std::min<u64>(cap / 2, budget / 2 / std::max<u64>(1, per_id));
       if (qcap >= 1024) qbm.alloc(qcap * kposL * wordsL, s);
       else qcap = 0;
@@ -1438,7 +1642,7 @@ struct Fsm {
           a.words = wordsL;
           a.lrank = lrank.get();
         }
-        if (gr.on) launch_group<LEV>(a, gr, kQC, "fsm_group_qc", bytes_in);
+        if (gr.on) launch_group<LEV>(a, gr, qcap ? kQCD : kQC, qcap ? "fsm_group_qc_domain" : "fsm_group_qc", bytes_in);
         else launch<LEV>(a, kQC, qcap ? "fsm_extend_qc_domain" : "fsm_extend_qc", bytes_in);
       }
       if (d2h(R.overflow.get()) == 0) break;
