@@ -595,14 +595,12 @@ struct FCur {
     thr[0] = thr[1];
     labp = 0;
     stp = 0;
-    u32 lab[MV + 1];
     u32 acc = 0;
 #pragma unroll
     for (int q = 0; q < MV; ++q) {
       const bool in = q < nv;
       v[q] = in ? E.v[q] : 0xffffffffu;
-      lab[q] = in ? E.lab[q] : 0u;
-      if (in) labp = (labp << a.LB) | lab[q];
+      if (in) labp = (labp << a.LB) | E.lab[q];
       stp |= (u32)(in ? E.step[q] : 0) << (4 * q);
       u64 b = 0;
       u32 d = 0;
@@ -616,16 +614,11 @@ struct FCur {
       lr[q] = (in && want_lr) ? ldg(a.lrank + v[q]) : 0u;
     }
     // new-vertex child codes: parent mask re-indexed to nv + 1 positions
-    u32 m1 = 0;
-    for (int x = 0; x < nv; ++x)
-      for (int y = x + 1; y < nv; ++y)
-        if (pmask >> pat::pair_index(x, y, nv) & 1u) m1 |= 1u << pat::pair_index(x, y, nv + 1);
-    u32 lab2[MV + 1];
-#pragma unroll
-    for (int i = 0; i <= MV; ++i) lab2[i] = i < nv ? lab[i] : 0u;
+    const u32 m1 = pat::widen_mask(pmask, nv);
 #pragma unroll
     for (int q = 0; q < MV; ++q)
-      newc[q] = q < nv ? pat::make_code(nv + 1, lab2, m1 | (1u << pat::pair_index(q, nv, nv + 1)), a.LB) : 0ull;
+      newc[q] = q < nv ? pat::make_code_packed(nv + 1, labp << a.LB, m1 | (1u << pat::pair_index(q, nv, nv + 1)))
+                       : 0ull;
     lshift = (u32)pat::npairs(nv + 1);
   }
   __device__ __forceinline__ void locate(const FsmArgs& a, u64 j, u64 pa, u64 pb, bool want_lr) {
@@ -671,17 +664,7 @@ struct FCur {
       if (dupe[jj] == n) return false;
     const int sr = (int)((stp >> (4 * r)) & 15u);
     if (!(n > sel(thr, min(sq, sr)))) return false;
-    u32 lab[MV];
-    u64 lp = labp;
-#pragma unroll
-    for (int i = MV - 1; i >= 0; --i) {
-      lab[i] = 0;
-      if (i < nv) {
-        lab[i] = (u32)(lp & ((u64(1) << a.LB) - 1));
-        lp >>= a.LB;
-      }
-    }
-    code = pat::make_code(nv, lab, pmask | (1u << pat::pair_index(q, r, nv)), a.LB);
+    code = pat::make_code_packed(nv, labp, pmask | (1u << pat::pair_index(q, r, nv)));
     return true;
   }
 };
@@ -743,17 +726,26 @@ __global__ void __launch_bounds__(kGT, 1) egroup_kernel(FsmArgs a, GroupArgs ga)
   u32* sid = mslot + ga.mcap;                    // kQCD: dense quick-code id per slot
   u32* sbm = sid + ga.cslots;                    // kDomain / kQCD: [cslots][kpos][words]
   constexpr bool kRows = MODE != kQC;
-  __shared__ u64 s_item;
+  __shared__ u64 s_item, s_pa, s_pb;
+  __shared__ unsigned long long s_next;
   __shared__ u32 s_used;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int NW = kGT / 32;
+  constexpr u64 kChunk = 4096;  // candidates per warp grab inside an item
   const u64 rowlen = (u64)a.kpos * a.words;
   unsigned long long acc = 0;
   for (;;) {
     __syncthreads();  // the previous item's flush is done
     if (threadIdx.x == 0) {
-      s_item = atomicAdd(ga.ctr, 1ull);
+      const u64 it = atomicAdd(ga.ctr, 1ull);
+      s_item = it;
       s_used = 0;
+      if (it < ga.nitems) {
+        const u64 j0 = ldg(ga.items + it), j1 = ldg(ga.items + it + 1);
+        s_next = j0;
+        s_pa = upper_bound_prev(a.Wp, 0, a.np + 1, j0);
+        s_pb = upper_bound_prev(a.Wp, s_pa, a.np + 1, j1 - 1);
+      }
     }
     for (u32 i = threadIdx.x; i < ga.mcap; i += kGT) {
       mkey[i] = 0ull;
@@ -766,14 +758,18 @@ __global__ void __launch_bounds__(kGT, 1) egroup_kernel(FsmArgs a, GroupArgs ga)
     __syncthreads();
     const u64 item = s_item;
     if (item >= ga.nitems) break;
-    const u64 j0 = ldg(ga.items + item), j1 = ldg(ga.items + item + 1);
-    const u64 span = ((j1 - j0 + NW - 1) / NW + 31) & ~31ull;
-    const u64 wj0 = j0 + (u64)wid * span, wj1 = min(j1, wj0 + span);
-    if (wj0 < wj1) {
+    const u64 j1 = ldg(ga.items + item + 1);
+    const u64 ipa = s_pa, ipb = s_pb;
+    FCur<LEV> cur;
+    for (;;) {  // warps grab kChunk-candidate pieces of the item (balance inside the CTA)
+      unsigned long long c0 = 0;
+      if (lane == 0) c0 = atomicAdd(&s_next, (unsigned long long)kChunk);
+      const u64 wj0 = __shfl_sync(0xffffffffu, c0, 0);
+      if (wj0 >= j1) break;
+      const u64 wj1 = min(j1, wj0 + kChunk);
       u64 pr = 0;
-      if (lane == 0) pr = upper_bound_prev(a.Wp, 0, a.np + 1, wj0);
+      if (lane == 0) pr = upper_bound_prev(a.Wp, ipa, ipb + 1, wj0);
       u64 P0 = __shfl_sync(0xffffffffu, pr, 0);
-      FCur<LEV> cur;
       for (u64 jb = wj0; jb < wj1; jb += 32) {
         const u64 j = jb + lane;
         const u64 x = (P0 + 1 + lane <= a.np) ? ldg(a.Wp + P0 + 1 + lane) : ~0ull;

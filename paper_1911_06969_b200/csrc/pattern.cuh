@@ -49,6 +49,33 @@ __host__ __device__ __forceinline__ uint64_t make_code(int nv, const uint32_t* l
   return ((uint64_t)nv << 61) | (lab_packed << NP) | E;
 }
 
+#ifdef __CUDACC__
+// Device fast paths of the same packing (no per-pair loop): E = complement of
+// the bit-reversed natural mask; labels already packed (L[0] most significant).
+__device__ __forceinline__ uint64_t make_code_packed(int nv, uint64_t lab_packed, uint32_t mask) {
+  const int NP = npairs(nv);
+  const uint32_t full = NP >= 32 ? 0xffffffffu : ((1u << NP) - 1u);
+  const uint32_t M = NP ? (__brev(mask) >> (32 - NP)) : 0u;
+  return ((uint64_t)nv << 61) | (lab_packed << NP) | (uint64_t)(~M & full);
+}
+// natural pair mask over nv positions -> the same pairs over nv + 1 positions
+// (pair (i, j) moves from index p to p + i: row i shifts by i)
+__device__ __forceinline__ uint32_t widen_mask(uint32_t mask, int nv) {
+  uint32_t out = 0;
+  int start = 0;
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+    if (i < nv - 1) {
+      const int len = nv - 1 - i;
+      const uint32_t row = (mask >> start) & ((1u << len) - 1u);
+      out |= row << (start + i);
+      start += len;
+    }
+  }
+  return out;
+}
+#endif
+
 __host__ __device__ __forceinline__ bool next_perm(uint8_t* a, int n) {
   int i = n - 2;
   while (i >= 0 && a[i] >= a[i + 1]) --i;
