@@ -223,6 +223,31 @@ int gpm_generate_rmat(int scale, double edge_factor, double a, double b, double 
                       uint32_t n_labels, uint64_t label_seed, gpm_csr* out);
 void gpm_csr_free(gpm_csr* csr);
 
+/* Binary CSR cache (replaces re-running
+ * load_edge_list / load_labeled_graph, graph_io.hpp:83-211, on every run).
+ * gpm_csr_save writes the cleaned CSR (+ labels, original ids) with a
+ * checksum; src_path (nullable) stamps the source file's size and mtime.
+ * gpm_csr_load reads it back (checksum verified).  gpm_load_cached loads
+ * `path` (labeled != 0: gSpan, else edge list) through the cache at
+ * cache_path (NULL: path + ".gpmcsr"): a cache whose stamp matches the source
+ * is read, otherwise the text is parsed and the cache (re)written;
+ * *cache_hit reports which. */
+int gpm_csr_save(const char* path, const gpm_csr* csr, const char* src_path);
+int gpm_csr_load(const char* path, gpm_csr* out);
+int gpm_load_cached(const char* path, int labeled, const char* cache_path, gpm_csr* out, uint64_t* err_line,
+                    int* cache_hit);
+
+/* canonicalize (the paper's getIsoCanonicalBliss,
+ * PAPER.md:939-954) of `count` patterns of nv <= 8 vertices on `device`, with
+ * the same device canonicaliser the reduce steps use.  labels: count*nv
+ * position labels (NULL = unlabeled); masks: natural pair masks, bit
+ * p(i,j) = i*nv - i*(i+1)/2 + (j-i-1) set iff positions i<j are adjacent.
+ * Outputs: canonical labels (nullable), canonical masks, and the
+ * PositionMap perms[i*nv + q] = canonical position of quick position q
+ * (nullable; first minimiser in next_permutation order). */
+int gpm_canonicalize_batch(int device, int nv, uint64_t count, const uint32_t* labels, const uint32_t* masks,
+                           uint32_t* canon_labels, uint32_t* canon_masks, uint8_t* perms);
+
 /* Returns the device buffers the library keeps cached between gpm_mine calls
  * (level columns, hash tables, bitmaps >= 64 MiB) to the driver; the next
  * call re-allocates them.  For callers that share the GPU with other

@@ -23,7 +23,8 @@ EXPORTS = [
     "gpm_result_num_patterns", "gpm_result_pattern", "gpm_result_stats", "gpm_result_free",
     "gpm_load_edge_list", "gpm_load_labeled_graph", "gpm_csr_from_edges", "gpm_generate_rmat", "gpm_csr_free",
     "gpm_last_error", "gpm_version", "gpm_steal_create", "gpm_steal_open", "gpm_steal_reset", "gpm_steal_release",
-    "gpm_release_cached",
+    "gpm_release_cached", "gpm_csr_save", "gpm_csr_load", "gpm_load_cached",
+    "gpm_canonicalize_batch",
 ]
 
 
@@ -105,6 +106,11 @@ def lib():
         "gpm_generate_rmat": (i32, [i32, C.c_double, C.c_double, C.c_double, C.c_double, u64, u32, u64,
                                     C.POINTER(CsrStruct)]),
         "gpm_csr_free": (None, [C.POINTER(CsrStruct)]),
+        "gpm_canonicalize_batch": (i32, [i32, i32, u64, vp, vp, vp, vp, vp]),
+        "gpm_csr_save": (i32, [C.c_char_p, C.POINTER(CsrStruct), C.c_char_p]),
+        "gpm_csr_load": (i32, [C.c_char_p, C.POINTER(CsrStruct)]),
+        "gpm_load_cached": (i32, [C.c_char_p, i32, C.c_char_p, C.POINTER(CsrStruct), C.POINTER(u64),
+                                  C.POINTER(i32)]),
         "gpm_last_error": (C.c_char_p, []),
         "gpm_steal_create": (i32, [i32, i32, C.POINTER(vp), vp]),
         "gpm_steal_open": (i32, [i32, vp, C.POINTER(vp)]),

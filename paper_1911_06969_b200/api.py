@@ -88,6 +88,42 @@ def load_labeled_graph(path: str) -> HostGraph:
     return _take_csr(cs)
 
 
+def _as_csr(g: HostGraph) -> Tuple[_L.CsrStruct, list]:
+    keep = [np.ascontiguousarray(g.off, dtype=np.uint64), np.ascontiguousarray(g.col, dtype=np.uint32)]
+    cs = _L.CsrStruct(g.n, g.m, keep[0].ctypes.data, keep[1].ctypes.data if g.m else None, None, None)
+    if g.labels is not None:
+        keep.append(np.ascontiguousarray(g.labels, dtype=np.uint32))
+        cs.labels = keep[-1].ctypes.data
+    if g.original_ids is not None:
+        keep.append(np.ascontiguousarray(g.original_ids, dtype=np.uint64))
+        cs.original_ids = keep[-1].ctypes.data
+    return cs, keep
+
+
+def save_csr(path: str, g: HostGraph, src_path: Optional[str] = None) -> None:
+    """Binary CSR cache writer (gpm_csr_save)."""
+    cs, _keep = _as_csr(g)
+    check(lib().gpm_csr_save(str(path).encode(), C.byref(cs), None if src_path is None else str(src_path).encode()))
+
+
+def load_csr(path: str) -> HostGraph:
+    """Binary CSR cache reader (gpm_csr_load; checksum verified)."""
+    cs = _L.CsrStruct()
+    check(lib().gpm_csr_load(str(path).encode(), C.byref(cs)))
+    return _take_csr(cs)
+
+
+def load_cached(path: str, labeled: bool = False, cache_path: Optional[str] = None) -> Tuple[HostGraph, bool]:
+    """load_edge_list / load_labeled_graph through the binary cache
+    (gpm_load_cached): returns (graph, cache_hit)."""
+    cs, line, hit = _L.CsrStruct(), C.c_uint64(0), C.c_int(0)
+    rc = lib().gpm_load_cached(str(path).encode(), int(labeled),
+                               None if cache_path is None else str(cache_path).encode(), C.byref(cs),
+                               C.byref(line), C.byref(hit))
+    check(rc, line.value)
+    return _take_csr(cs), bool(hit.value)
+
+
 def csr_from_edges(src, dst) -> HostGraph:
     s = np.ascontiguousarray(src, dtype=np.uint64)
     d = np.ascontiguousarray(dst, dtype=np.uint64)
@@ -318,6 +354,33 @@ def list_embeddings(g: Graph, app: str, k: int, **kw):
     kk = res.k
     rows = np.concatenate(chunks) if chunks else np.zeros((0, kk), dtype=np.uint32)
     return rows, res
+
+
+def canonicalize(patterns, nv: int, device: int = 0) -> List[Tuple[str, List[int]]]:
+    """Device canonicalize of patterns given as
+    (labels or None, [(i, j), ...]) over nv positions; returns the SPEC.md:252
+    text and the PositionMap (quick -> canonical position) of each."""
+    cnt = len(patterns)
+    labeled = any(l is not None for l, _ in patterns)
+    lab = np.zeros((cnt, nv), np.uint32)
+    masks = np.zeros(cnt, np.uint32)
+    for i, (l, edges) in enumerate(patterns):
+        if l is not None:
+            lab[i] = l
+        for a, b in edges:
+            a, b = min(a, b), max(a, b)
+            masks[i] |= np.uint32(1 << (a * nv - a * (a + 1) // 2 + (b - a - 1)))
+    cl = np.zeros((cnt, nv), np.uint32)
+    cm = np.zeros(cnt, np.uint32)
+    pm = np.zeros((cnt, nv), np.uint8)
+    check(lib().gpm_canonicalize_batch(device, nv, cnt, _p(lab) if labeled else None, _p(masks), _p(cl), _p(cm),
+                                       _p(pm)))
+    out = []
+    pairs = [(a, b) for a in range(nv) for b in range(a + 1, nv)]
+    for i in range(cnt):
+        e = "".join(f"({a},{b})" for p_, (a, b) in enumerate(pairs) if int(cm[i]) >> p_ & 1)
+        out.append((f"k={nv};L=" + ",".join(str(int(x)) for x in cl[i]) + ";E=" + e, [int(x) for x in pm[i]]))
+    return out
 
 
 def release_cached(device: int = -1) -> None:

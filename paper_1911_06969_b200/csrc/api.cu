@@ -27,7 +27,7 @@ std::string canon_text(u64 key, int nv_hint, int label_bits, const std::vector<u
   (void)nv_hint;
   // "k=<n>;L=l0,l1,..;E=(i,j)..", formatted without iostreams:
   // FSM can emit ~10^6 patterns per call
-  char buf[256];
+  char buf[512];
   char* o = buf;
   auto put_u = [&](u32 v) {
     char t[12];
@@ -98,6 +98,21 @@ void exchange_device(const gpm_config& cfg, void* dev, u64 count, int elem_bytes
   if (cfg.exchange(cfg.exchange_ctx, dev, count, elem_bytes, op, s) != 0) throw Error(GPM_ENCCL, "exchange failed");
 }
 
+// One thread per pattern: the device canonicaliser the FSM / MC reduce steps
+// use (pattern.cuh), exposed for batches of arbitrary patterns (tests, tools).
+__global__ void canon_batch_kernel(int nv, u64 count, const u32* __restrict__ lab, const u32* __restrict__ masks,
+                                   int LB, u64* __restrict__ codes, u32* __restrict__ perms) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x) {
+    u32 l[8];
+    for (int j = 0; j < nv; ++j) l[j] = lab[i * nv + j];
+    u8 p[8];
+    codes[i] = pat::canonicalize(nv, l, masks[i], LB, p);
+    u32 pk = 0;
+    for (int j = 0; j < nv; ++j) pk |= (u32)p[j] << (3 * j);
+    perms[i] = pk;
+  }
+}
+
 }  // namespace gpm
 
 using namespace gpm;
@@ -105,6 +120,56 @@ using namespace gpm;
 extern "C" {
 
 const char* gpm_last_error(void) { return g_last_error.c_str(); }
+
+int gpm_canonicalize_batch(int device, int nv, uint64_t count, const uint32_t* labels, const uint32_t* masks,
+                           uint32_t* canon_labels, uint32_t* canon_masks, uint8_t* perms) {
+  return guarded([&] {
+    if (nv < 1 || nv > 8) throw Error(GPM_EINVAL, "canonicalize: 1 <= nv <= 8 (SPEC.md:204)");
+    if (count && (!masks || !canon_masks)) throw Error(GPM_EINVAL, "null argument");
+    const int np = pat::npairs(nv);
+    for (u64 i = 0; i < count; ++i)
+      if (np < 32 && (masks[i] >> np)) throw Error(GPM_EINVAL, "mask has bits beyond the nv*(nv-1)/2 pairs");
+    // dense, order-preserving label ranks (the packed code compares ranks)
+    std::vector<u32> vals;
+    if (labels) vals.assign(labels, labels + count * nv);
+    std::sort(vals.begin(), vals.end());
+    vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+    int LB = 0;
+    while ((u64(1) << LB) < vals.size()) ++LB;
+    if (pat::code_bits(nv, LB) > pat::kCodeBits) throw Error(GPM_EINVAL, "canonicalize: too many distinct labels for a packed code");
+    std::vector<u32> rk(count * nv, 0);
+    if (labels)
+      for (u64 i = 0; i < count * nv; ++i)
+        rk[i] = (u32)(std::lower_bound(vals.begin(), vals.end(), labels[i]) - vals.begin());
+    if (count == 0) return;
+    GPM_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    GPM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG { cudaStream_t s; ~SG() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{st};
+    DBuf<u32> dl(count * nv, st), dm(count, st), dp(count, st);
+    DBuf<u64> dc(count, st);
+    GPM_CUDA(cudaMemcpyAsync(dl.get(), rk.data(), sizeof(u32) * count * nv, cudaMemcpyHostToDevice, st));
+    GPM_CUDA(cudaMemcpyAsync(dm.get(), masks, sizeof(u32) * count, cudaMemcpyHostToDevice, st));
+    canon_batch_kernel<<<(unsigned)std::min<u64>(4096, (count + 127) / 128), 128, 0, st>>>(nv, count, dl.get(), dm.get(),
+                                                                                           LB, dc.get(), dp.get());
+    GPM_CUDA(cudaGetLastError());
+    std::vector<u64> codes(count);
+    std::vector<u32> pk(count);
+    GPM_CUDA(cudaMemcpyAsync(codes.data(), dc.get(), sizeof(u64) * count, cudaMemcpyDeviceToHost, st));
+    GPM_CUDA(cudaMemcpyAsync(pk.data(), dp.get(), sizeof(u32) * count, cudaMemcpyDeviceToHost, st));
+    GPM_CUDA(cudaStreamSynchronize(st));
+    for (u64 i = 0; i < count; ++i) {
+      int cn = 0;
+      u32 cl[8], cm = 0;
+      pat::decode(codes[i], LB, &cn, cl, &cm);
+      canon_masks[i] = cm;
+      for (int j = 0; j < nv; ++j) {
+        if (canon_labels) canon_labels[i * nv + j] = labels ? vals[cl[j]] : 0u;
+        if (perms) perms[i * nv + j] = (u8)((pk[i] >> (3 * j)) & 7u);
+      }
+    }
+  });
+}
 
 const char* gpm_version(void) { return "gpm-b200 0.1 (sm_100a)"; }
 

@@ -1718,7 +1718,7 @@ struct Fsm {
     if (G.oriented) throw Error(GPM_EINVAL, "fsm: graph must be undirected");
     if (k < 2 || k > kMaxEdges + 1) throw Error(GPM_EINVAL, "fsm: k must be in [2,6]");
     LB = std::max(1, G.label_bits);
-    if (k * LB + pat::npairs(k) > 61)
+    if (pat::code_bits(k, LB) > pat::kCodeBits)
       throw Error(GPM_EINVAL, "fsm: too many distinct labels for a packed pattern code at this k");
     sms = sm_count();
     const size_t freeb = device_free_bytes();

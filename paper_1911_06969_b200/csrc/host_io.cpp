@@ -5,6 +5,8 @@
 // digit scanning (no per-line istringstream, the reference's cost centre,
 // SURVEY §3 stack 1); CSR construction is counting-based and OpenMP-parallel.
 #include <omp.h>
+#include <parallel/algorithm>
+#include <sys/stat.h>
 
 #include <algorithm>
 #include <cmath>
@@ -111,11 +113,14 @@ struct Compactor {
 
   void build(std::vector<u64> ids) {
     u64 mx = 0;
-    for (u64 x : ids) mx = std::max(mx, x);
+#pragma omp parallel for reduction(max : mx) schedule(static)
+    for (long long i = 0; i < (long long)ids.size(); ++i) mx = std::max(mx, ids[i]);
     if (!ids.empty() && mx < (u64(1) << 32) && mx <= 4 * ids.size() + 1024) {
       dense_range = true;
       std::vector<u8> seen(mx + 1, 0);
-      for (u64 x : ids) seen[x] = 1;
+      u8* sp = seen.data();
+#pragma omp parallel for schedule(static)
+      for (long long i = 0; i < (long long)ids.size(); ++i) sp[ids[i]] = 1;  // benign same-value writes
       table.assign(mx + 1, UINT32_MAX);
       u32 d = 0;
       for (u64 x = 0; x <= mx; ++x)
@@ -124,7 +129,7 @@ struct Compactor {
           uniq.push_back(x);
         }
     } else {
-      std::sort(ids.begin(), ids.end());
+      __gnu_parallel::sort(ids.begin(), ids.end());
       ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
       uniq = std::move(ids);
       map.reserve(uniq.size() * 2);
@@ -135,21 +140,28 @@ struct Compactor {
   u32 operator()(u64 id) const { return dense_range ? table[id] : map.at(id); }
 };
 
-// Symmetrise, sort, dedup (graph_io.hpp:68-73, :119-126).
+// Symmetrise, sort, dedup (graph_io.hpp:68-73, :119-126).  Degrees and the
+// scatter use relaxed atomics across threads; every list is sorted afterwards,
+// so the result does not depend on the scatter order.
 void build_csr(u32 n, const std::vector<u32>& su, const std::vector<u32>& sv, gpm_csr* out) {
-  const u64 ne = su.size();
+  const long long ne = (long long)su.size();
   std::vector<u64> deg(n + 1, 0);
-  for (u64 i = 0; i < ne; ++i) {
-    ++deg[su[i] + 1];
-    ++deg[sv[i] + 1];
+  u64* dp = deg.data();
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < ne; ++i) {
+    __atomic_fetch_add(dp + su[i] + 1, 1, __ATOMIC_RELAXED);
+    __atomic_fetch_add(dp + sv[i] + 1, 1, __ATOMIC_RELAXED);
   }
   for (u32 v = 0; v < n; ++v) deg[v + 1] += deg[v];
   std::vector<u32> adj(deg[n]);
   {
     std::vector<u64> pos(deg.begin(), deg.end() - 1);
-    for (u64 i = 0; i < ne; ++i) {
-      adj[pos[su[i]]++] = sv[i];
-      adj[pos[sv[i]]++] = su[i];
+    u64* pp = pos.data();
+    u32* ap = adj.data();
+#pragma omp parallel for schedule(static)
+    for (long long i = 0; i < ne; ++i) {
+      ap[__atomic_fetch_add(pp + su[i], 1, __ATOMIC_RELAXED)] = sv[i];
+      ap[__atomic_fetch_add(pp + sv[i], 1, __ATOMIC_RELAXED)] = su[i];
     }
   }
   std::vector<u64> cnt(n + 1, 0);
@@ -208,23 +220,79 @@ inline u64 mix64(u64 x) {
 
 }  // namespace
 
+// Parallel single pass over the file image: the buffer is cut into one
+// range per thread at line starts, each thread parses its lines into local
+// (u, v) vectors, and a parse error reports the globally FIRST bad line (its
+// number = lines of the earlier ranges + its rank inside its own range), as
+// the reference's sequential loop would (graph_io.hpp:88-98).
 void load_edge_list(const char* path, gpm_csr* out) {
   std::string buf = read_file(path);
-  std::vector<u64> a, b;
-  a.reserve(buf.size() / 12);
-  b.reserve(buf.size() / 12);
-  for_each_line(buf, [&](const char* lb, const char* le, u64 lineno) {
-    if (blank_line(lb, le) || comment_line(lb, le)) return;
-    Tok t[3];
-    int nt = tokenize(lb, le, t, 3);
-    u64 u, v;
-    if (nt != 2 || !parse_u64(t[0].b, t[0].e, u) || !parse_u64(t[1].b, t[1].e, v))
+  const char* base = buf.data();
+  const char* end = base + buf.size();
+  const int T = std::max(1, std::min(omp_get_max_threads(), (int)(buf.size() >> 20) + 1));
+  std::vector<const char*> cut(T + 1, end);
+  cut[0] = base;
+  for (int t = 1; t < T; ++t) {
+    const char* p = std::max(base + buf.size() * t / T, cut[t - 1]);
+    const char* nl = p < end ? (const char*)std::memchr(p, '\n', end - p) : nullptr;
+    cut[t] = nl ? nl + 1 : end;
+  }
+  std::vector<std::vector<u64>> A(T), B(T);
+  std::vector<u64> nlines(T, 0), bad(T, 0);  // bad: 1-based line inside the range (0 = none)
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+  for (int t = 0; t < T; ++t) {
+    auto& a = A[t];
+    auto& b = B[t];
+    a.reserve((cut[t + 1] - cut[t]) / 12 + 16);
+    b.reserve((cut[t + 1] - cut[t]) / 12 + 16);
+    const char* p = cut[t];
+    const char* e = cut[t + 1];
+    u64 ln = 0;
+    while (p < e) {
+      const char* nl = (const char*)std::memchr(p, '\n', e - p);
+      const char* le = nl ? nl : e;
+      ++ln;
+      const char* lb = p;
+      const char* ce = le;
+      if (ce > lb && ce[-1] == '\r') --ce;  // chomp (graph_io.hpp:27-29)
+      p = nl ? nl + 1 : e;
+      if (bad[t]) continue;  // keep counting lines only
+      if (blank_line(lb, ce) || comment_line(lb, ce)) continue;
+      Tok tk[3];
+      const int nt = tokenize(lb, ce, tk, 3);
+      u64 u, v;
+      if (nt != 2 || !parse_u64(tk[0].b, tk[0].e, u) || !parse_u64(tk[1].b, tk[1].e, v)) {
+        bad[t] = ln;
+        continue;
+      }
+      if (u == v) continue;  // self-loop
+      a.push_back(u);
+      b.push_back(v);
+    }
+    nlines[t] = ln;
+  }
+  u64 before = 0;
+  for (int t = 0; t < T; ++t) {
+    if (bad[t]) {
+      const u64 lineno = before + bad[t];
       throw Error(GPM_EPARSE, "line " + std::to_string(lineno) + ": expected two non-negative integers", lineno);
-    if (u == v) return;  // self-loop
-    a.push_back(u);
-    b.push_back(v);
-  });
-  if (a.empty()) throw Error(GPM_EINVAL, "edge list is empty after cleaning");
+    }
+    before += nlines[t];
+  }
+  std::string().swap(buf);
+  u64 tot = 0;
+  for (int t = 0; t < T; ++t) tot += A[t].size();
+  if (tot == 0) throw Error(GPM_EINVAL, "edge list is empty after cleaning");
+  std::vector<u64> a(tot), b(tot);
+  std::vector<u64> at(T + 1, 0);
+  for (int t = 0; t < T; ++t) at[t + 1] = at[t] + A[t].size();
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+  for (int t = 0; t < T; ++t) {
+    std::memcpy(a.data() + at[t], A[t].data(), sizeof(u64) * A[t].size());
+    std::memcpy(b.data() + at[t], B[t].data(), sizeof(u64) * B[t].size());
+    std::vector<u64>().swap(A[t]);
+    std::vector<u64>().swap(B[t]);
+  }
   csr_from_pairs(a, b, out);
 }
 
@@ -388,6 +456,136 @@ void generate_rmat(int scale, double ef, double a, double b, double c, u64 seed,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Binary CSR cache: the cleaned CSR of a text input,
+// written once and mapped back with a few large reads instead of re-parsing
+// (the reference re-parses every run, graph_io.hpp:83-116).  Layout, little
+// endian: CacheHeader, row_offsets u64[n+1], col u32[m], labels u32[n] (flag
+// 1), original_ids u64[n] (flag 2).  The header records the source file's
+// size and mtime so a stale cache is detected, and a checksum over the arrays.
+namespace {
+constexpr char kCacheMagic[8] = {'G', 'P', 'M', 'C', 'S', 'R', '0', '1'};
+struct CacheHeader {
+  char magic[8];
+  u32 version;
+  u32 flags;
+  u32 n;
+  u32 pad;
+  u64 m;
+  u64 src_size;
+  u64 src_mtime_ns;
+  u64 checksum;
+};
+static_assert(sizeof(CacheHeader) == 56, "cache header layout");
+
+// word-parallel checksum: mix64 of each 8-byte word (position-salted), summed
+u64 checksum_bytes(const void* p, size_t nbytes, u64 salt) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  const size_t nw = nbytes / 8;
+  u64 s = 0;
+#pragma omp parallel for reduction(+ : s) schedule(static)
+  for (long long i = 0; i < (long long)nw; ++i) {
+    u64 w;
+    std::memcpy(&w, b + 8 * i, 8);
+    s += mix64(w ^ mix64(salt + (u64)i));
+  }
+  u64 tail = 0;
+  std::memcpy(&tail, b + 8 * nw, nbytes - 8 * nw);
+  return s + mix64(tail ^ salt ^ (u64)nbytes);
+}
+
+u64 csr_checksum(const gpm_csr* c) {
+  u64 s = checksum_bytes(c->row_offsets, sizeof(u64) * ((u64)c->n + 1), 1);
+  s += checksum_bytes(c->col, sizeof(u32) * c->m, 2);
+  if (c->labels) s += checksum_bytes(c->labels, sizeof(u32) * (u64)c->n, 3);
+  if (c->original_ids) s += checksum_bytes(c->original_ids, sizeof(u64) * (u64)c->n, 4);
+  return s;
+}
+
+bool file_stamp(const char* path, u64& size, u64& mtime_ns) {
+  struct stat st;
+  if (!path || ::stat(path, &st) != 0) return false;
+  size = (u64)st.st_size;
+  mtime_ns = (u64)st.st_mtim.tv_sec * 1000000000ull + (u64)st.st_mtim.tv_nsec;
+  return true;
+}
+
+void write_all(FILE* f, const void* p, size_t n, const char* path) {
+  if (n && std::fwrite(p, 1, n, f) != n) {
+    std::fclose(f);
+    throw Error(GPM_EINVAL, std::string("short write on ") + path);
+  }
+}
+
+template <class T>
+T* read_array(FILE* f, u64 count, const char* path) {
+  T* p = (T*)std::malloc(sizeof(T) * std::max<u64>(1, count));
+  if (!p) throw Error(GPM_ENOMEM, "cache allocation failed");
+  if (count && std::fread(p, sizeof(T), count, f) != count) {
+    std::free(p);
+    throw Error(GPM_EINVAL, std::string("truncated cache file ") + path);
+  }
+  return p;
+}
+}  // namespace
+
+void csr_save(const char* path, const gpm_csr* c, const char* src_path) {
+  if (!c->row_offsets || (c->m && !c->col)) throw Error(GPM_EINVAL, "csr_save: empty csr");
+  CacheHeader h{};
+  std::memcpy(h.magic, kCacheMagic, 8);
+  h.version = 1;
+  h.flags = (c->labels ? 1u : 0u) | (c->original_ids ? 2u : 0u);
+  h.n = c->n;
+  h.m = c->m;
+  if (src_path && !file_stamp(src_path, h.src_size, h.src_mtime_ns))
+    throw Error(GPM_EINVAL, std::string("cannot stat ") + src_path);
+  h.checksum = csr_checksum(c);
+  const std::string tmp = std::string(path) + ".tmp";
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) throw Error(GPM_EINVAL, std::string("cannot create ") + tmp);
+  write_all(f, &h, sizeof h, path);
+  write_all(f, c->row_offsets, sizeof(u64) * ((u64)c->n + 1), path);
+  write_all(f, c->col, sizeof(u32) * c->m, path);
+  if (c->labels) write_all(f, c->labels, sizeof(u32) * (u64)c->n, path);
+  if (c->original_ids) write_all(f, c->original_ids, sizeof(u64) * (u64)c->n, path);
+  if (std::fclose(f) != 0) throw Error(GPM_EINVAL, std::string("close failed on ") + tmp);
+  if (std::rename(tmp.c_str(), path) != 0) throw Error(GPM_EINVAL, std::string("cannot rename to ") + path);
+}
+
+// Returns false (and leaves `out` empty) when the cache is absent or was
+// written for another version of src_path; a corrupt cache is an error.
+bool csr_load(const char* path, const char* src_path, gpm_csr* out) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) return false;
+  CacheHeader h{};
+  if (std::fread(&h, sizeof h, 1, f) != 1 || std::memcmp(h.magic, kCacheMagic, 8) != 0 || h.version != 1) {
+    std::fclose(f);
+    throw Error(GPM_EINVAL, std::string("not a gpm CSR cache: ") + path);
+  }
+  if (src_path) {
+    u64 sz = 0, mt = 0;
+    if (!file_stamp(src_path, sz, mt) || sz != h.src_size || mt != h.src_mtime_ns) {
+      std::fclose(f);
+      return false;  // stale
+    }
+  }
+  try {
+    out->n = h.n;
+    out->m = h.m;
+    out->row_offsets = read_array<u64>(f, (u64)h.n + 1, path);
+    out->col = read_array<u32>(f, h.m, path);
+    if (h.flags & 1u) out->labels = read_array<u32>(f, h.n, path);
+    if (h.flags & 2u) out->original_ids = read_array<u64>(f, h.n, path);
+  } catch (...) {
+    std::fclose(f);
+    throw;
+  }
+  std::fclose(f);
+  if (csr_checksum(out) != h.checksum) throw Error(GPM_EINVAL, std::string("cache checksum mismatch: ") + path);
+  if (out->row_offsets[0] != 0 || out->row_offsets[h.n] != h.m) throw Error(GPM_EINVAL, "cache offsets inconsistent");
+  return true;
+}
+
 }  // namespace gpm
 
 extern "C" {
@@ -435,6 +633,60 @@ int gpm_generate_rmat(int scale, double edge_factor, double a, double b, double 
   }
   zero_csr(out);
   int rc = gpm::guarded([&] { gpm::generate_rmat(scale, edge_factor, a, b, c, seed, n_labels, label_seed, out); });
+  if (rc != GPM_OK) gpm_csr_free(out);
+  return rc;
+}
+
+int gpm_csr_save(const char* path, const gpm_csr* csr, const char* src_path) {
+  if (!path || !csr) {
+    gpm::set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  return gpm::guarded([&] { gpm::csr_save(path, csr, src_path); });
+}
+
+int gpm_csr_load(const char* path, gpm_csr* out) {
+  if (!path || !out) {
+    gpm::set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  zero_csr(out);
+  int rc = gpm::guarded([&] {
+    if (!gpm::csr_load(path, nullptr, out)) throw gpm::Error(GPM_EINVAL, std::string("cannot open ") + path);
+  });
+  if (rc != GPM_OK) gpm_csr_free(out);
+  return rc;
+}
+
+int gpm_load_cached(const char* path, int labeled, const char* cache_path, gpm_csr* out, uint64_t* err_line,
+                    int* cache_hit) {
+  if (!path || !out) {
+    gpm::set_last_error("null argument");
+    return GPM_EINVAL;
+  }
+  zero_csr(out);
+  if (cache_hit) *cache_hit = 0;
+  const std::string cp = cache_path ? std::string(cache_path) : std::string(path) + ".gpmcsr";
+  int rc = gpm::guarded(
+      [&] {
+        bool hit = false;
+        try {
+          hit = gpm::csr_load(cp.c_str(), path, out);
+        } catch (const gpm::Error&) {
+          gpm_csr_free(out);  // unreadable cache: rebuild it from the text
+          hit = false;
+        }
+        if (hit) {
+          if (cache_hit) *cache_hit = 1;
+          if (labeled && !out->labels) throw gpm::Error(GPM_EINVAL, "cache holds an unlabeled graph");
+          return;
+        }
+        gpm_csr_free(out);
+        if (labeled) gpm::load_labeled_graph(path, out);
+        else gpm::load_edge_list(path, out);
+        gpm::csr_save(cp.c_str(), out, path);
+      },
+      err_line);
   if (rc != GPM_OK) gpm_csr_free(out);
   return rc;
 }

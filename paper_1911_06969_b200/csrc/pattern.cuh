@@ -7,7 +7,7 @@
 // the PositionMap.  We pack a pattern into one u64 whose INTEGER order equals
 // that lexicographic order:
 //
-//   code = nv << 61 | labels << NP | E
+//   code = nv << 60 | labels << NP | E          (nv <= 8; labels + E <= 60 bits)
 //   labels = L[0] << LB*(nv-1) | ... | L[nv-1]        (L[0] most significant)
 //   E      = ~M & (2^NP - 1),  M bit (NP-1-p) set iff pair p is an edge,
 //            pairs p in lexicographic order (0,1),(0,2),..,(nv-2,nv-1)
@@ -46,7 +46,7 @@ __host__ __device__ __forceinline__ uint64_t make_code(int nv, const uint32_t* l
   for (int p = 0; p < NP; ++p)
     if (mask >> p & 1u) M |= (uint64_t)1 << (NP - 1 - p);
   const uint64_t E = (~M) & (((uint64_t)1 << NP) - 1);
-  return ((uint64_t)nv << 61) | (lab_packed << NP) | E;
+  return ((uint64_t)nv << 60) | (lab_packed << NP) | E;
 }
 
 #ifdef __CUDACC__
@@ -56,7 +56,7 @@ __device__ __forceinline__ uint64_t make_code_packed(int nv, uint64_t lab_packed
   const int NP = npairs(nv);
   const uint32_t full = NP >= 32 ? 0xffffffffu : ((1u << NP) - 1u);
   const uint32_t M = NP ? (__brev(mask) >> (32 - NP)) : 0u;
-  return ((uint64_t)nv << 61) | (lab_packed << NP) | (uint64_t)(~M & full);
+  return ((uint64_t)nv << 60) | (lab_packed << NP) | (uint64_t)(~M & full);
 }
 // natural pair mask over nv positions -> the same pairs over nv + 1 positions
 // (pair (i, j) moves from index p to p + i: row i shifts by i)
@@ -95,32 +95,90 @@ __host__ __device__ __forceinline__ bool next_perm(uint8_t* a, int n) {
 
 // canonicalize: returns canonical code; perm[i] = canonical
 // position of quick position i.
+//
+// Labels compare first, so every minimiser sorts the labels: only
+// permutations sending each position into its label's block of the sorted
+// label sequence can win (the exact label-partition pre-filter of
+// SPEC.md:245).  They are enumerated depth-first with increasing slots, i.e.
+// in the lexicographic (next_permutation) order of the full enumeration, so
+// the first minimiser -- the PositionMap tie-break -- is unchanged.  With
+// distinct labels this is one permutation; unlabeled 8-vertex patterns still
+// visit all 40320.
 __host__ __device__ inline uint64_t canonicalize(int nv, const uint32_t* lab, uint32_t mask, int LB, uint8_t* perm_out) {
-  uint8_t p[8];
-  for (int i = 0; i < nv; ++i) p[i] = (uint8_t)i;
+  uint32_t sl[8];
+  for (int i = 0; i < nv; ++i) sl[i] = lab[i];
+  for (int i = 1; i < nv; ++i) {  // insertion sort: the canonical label sequence
+    const uint32_t x = sl[i];
+    int j = i - 1;
+    while (j >= 0 && sl[j] > x) {
+      sl[j + 1] = sl[j];
+      --j;
+    }
+    sl[j + 1] = x;
+  }
+  uint8_t lo[8], hi[8];
+  for (int i = 0; i < nv; ++i) {
+    int a = 0;
+    while (sl[a] != lab[i]) ++a;
+    int b = a;
+    while (b < nv && sl[b] == lab[i]) ++b;
+    lo[i] = (uint8_t)a;
+    hi[i] = (uint8_t)b;
+  }
+  // the pattern's edges as (i, j) position pairs
+  uint8_t ea[28], eb[28];
+  int ne = 0;
+  for (int a = 0; a < nv; ++a)
+    for (int b = a + 1; b < nv; ++b)
+      if (mask >> pair_index(a, b, nv) & 1u) {
+        ea[ne] = (uint8_t)a;
+        eb[ne] = (uint8_t)b;
+        ++ne;
+      }
   uint64_t best = ~(uint64_t)0;
-  uint32_t pl[8];
-  do {
-    for (int i = 0; i < nv; ++i) pl[p[i]] = lab[i];
+  uint8_t p[8], nxt[8];
+  uint32_t used = 0;
+  int i = 0;
+  nxt[0] = lo[0];
+  for (;;) {
+    int sv = nxt[i];
+    while (sv < hi[i] && (used >> sv & 1u)) ++sv;
+    if (sv >= hi[i]) {  // position i exhausted: backtrack
+      if (i == 0) break;
+      --i;
+      used &= ~(1u << p[i]);
+      nxt[i] = (uint8_t)(p[i] + 1);
+      continue;
+    }
+    p[i] = (uint8_t)sv;
+    used |= 1u << sv;
+    if (i + 1 < nv) {
+      ++i;
+      nxt[i] = lo[i];
+      continue;
+    }
     uint32_t pm = 0;
-    for (int a = 0; a < nv; ++a)
-      for (int b = a + 1; b < nv; ++b)
-        if (mask >> pair_index(a, b, nv) & 1u) {
-          int x = p[a], y = p[b];
-          if (x > y) { int t = x; x = y; y = t; }
-          pm |= 1u << pair_index(x, y, nv);
-        }
-    uint64_t c = make_code(nv, pl, pm, LB);
+    for (int e = 0; e < ne; ++e) {
+      int x = p[ea[e]], y = p[eb[e]];
+      if (x > y) { const int t = x; x = y; y = t; }
+      pm |= 1u << pair_index(x, y, nv);
+    }
+    const uint64_t c = make_code(nv, sl, pm, LB);
     if (c < best) {
       best = c;
       if (perm_out)
-        for (int i = 0; i < nv; ++i) perm_out[i] = p[i];
+        for (int j = 0; j < nv; ++j) perm_out[j] = p[j];
     }
-  } while (next_perm(p, nv));
+    used &= ~(1u << sv);
+    nxt[i] = (uint8_t)(sv + 1);
+  }
   return best;
 }
 
-__host__ __device__ __forceinline__ int code_nv(uint64_t code) { return (int)(code >> 61); }
+__host__ __device__ __forceinline__ int code_nv(uint64_t code) { return (int)(code >> 60); }
+// bits a code of nv positions with LB-bit labels needs below the nv field
+__host__ __device__ __forceinline__ int code_bits(int nv, int LB) { return nv * LB + npairs(nv); }
+constexpr int kCodeBits = 60;
 
 // Decode labels and natural-order edge mask from a code.
 __host__ __device__ inline void decode(uint64_t code, int LB, int* nv_out, uint32_t* lab, uint32_t* mask) {
@@ -131,7 +189,7 @@ __host__ __device__ inline void decode(uint64_t code, int LB, int* nv_out, uint3
   uint32_t m = 0;
   for (int p = 0; p < NP; ++p)
     if (M >> (NP - 1 - p) & 1u) m |= 1u << p;
-  uint64_t lp = (code & (((uint64_t)1 << 61) - 1)) >> NP;
+  uint64_t lp = (code & (((uint64_t)1 << 60) - 1)) >> NP;
   for (int i = nv - 1; i >= 0; --i) {
     lab[i] = LB ? (uint32_t)(lp & ((((uint64_t)1) << LB) - 1)) : 0u;
     lp = LB ? (lp >> LB) : 0;

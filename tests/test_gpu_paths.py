@@ -61,8 +61,9 @@ def test_cf_paths(P, scale, ef, abc):
 @pytest.mark.parametrize("scale,ef,abc", [(11, 16, (0.57, 0.19, 0.19)), (13, 8, (0.45, 0.15, 0.15)),
                                           (14, 16, (0.57, 0.19, 0.19))])
 def test_mc_paths(P, scale, ef, abc):
-    # RMAT-14 ef16 has roots with |S0| above the warp-kernel limit: exercises
-    # the tiled block kernel of 3-MC and the HBM fallback of the 4-MC union set
+    # staged vs generic MC (GPU vs GPU); RMAT-14 ef16 has roots with |S0| above
+    # the warp-kernel limit (3-MC block kernel).  The oracle-checked big-root
+    # paths (multi-tile 3-MC, 4-MC HBM union sets) are tests/test_gpu_bigpaths.py
     g = P.Graph(P.generate_rmat(scale, ef, *abc, seed=scale + 1))
     for k in ((3, 4) if scale < 14 else (3,)):
         _same(_run(P, g, "mc", k), _run(P, g, "mc", k, env=["GPM_GENERIC_MC"]))

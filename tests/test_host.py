@@ -84,6 +84,75 @@ def test_parse_errors_match_reference(oracle, tmp_path, text, line):
     assert r.value.line == line
 
 
+@ref_only
+def test_parallel_parse_matches_reference_and_first_error(oracle, tmp_path):
+    """Files of several MiB are parsed in one range per thread: same CSR as the
+    reference loader, and the FIRST bad line is reported even when a later
+    range holds another one."""
+    import paper_1911_06969_b200 as P
+    rng = np.random.default_rng(11)
+    m = 700_000
+    u = rng.integers(0, 50_000, m)
+    v = rng.integers(0, 50_000, m)
+    lines = [f"{a} {b}" if i % 97 else f"# c {i}" for i, (a, b) in enumerate(zip(u, v))]
+    lines[1234] = "  "
+    text = "\n".join(lines) + "\n"
+    path = _write(tmp_path, "big.el", text)
+    mine = P.load_edge_list(path)
+    ref = oracle.ref_load(path)
+    assert np.array_equal(mine.off, ref.off) and np.array_equal(mine.col, ref.col)
+    assert np.array_equal(mine.original_ids, ref.orig)
+    bad = list(lines)
+    bad[450_000] = "1 2 3"
+    bad[650_000] = "x"
+    path = _write(tmp_path, "bad.el", "\n".join(bad) + "\n")
+    with pytest.raises(P.ParseError) as e:
+        P.load_edge_list(path)
+    assert e.value.line == 450_001
+    with pytest.raises(oracle.RefParseError) as r:
+        oracle.ref_load(path)
+    assert r.value.line == 450_001
+
+
+def test_binary_csr_cache(tmp_path):
+    import paper_1911_06969_b200 as P
+    src = _write(tmp_path, "g.el", "".join(f"{a} {b}\n" for a, b in BF.gnp(300, 0.05, 2)))
+    cache = str(tmp_path / "g.el.gpmcsr")
+    g0 = P.load_edge_list(src)
+    g1, hit = P.load_cached(src)
+    assert not hit and os.path.exists(cache)
+    g2, hit = P.load_cached(src)
+    assert hit
+    for g in (g1, g2, P.load_csr(cache)):
+        assert np.array_equal(g.off, g0.off) and np.array_equal(g.col, g0.col)
+        assert np.array_equal(g.original_ids, g0.original_ids)
+    # a changed source invalidates the cache
+    with open(src, "a") as f:
+        f.write("1000 1001\n")
+    g3, hit = P.load_cached(src)
+    assert not hit and g3.n == g0.n + 2
+    assert P.load_cached(src)[1]
+    # a corrupt cache is detected (direct load) and rebuilt (cached load)
+    raw = bytearray(open(cache, "rb").read())
+    raw[-3] ^= 0xFF
+    open(cache, "wb").write(bytes(raw))
+    with pytest.raises(P.GpmError):
+        P.load_csr(cache)
+    g4, hit = P.load_cached(src)
+    assert not hit and np.array_equal(g4.col, g3.col)
+    # labeled graphs keep their labels; save/load of any host graph
+    lg = _write(tmp_path, "l.lg", "v 0 1\nv 1 2\nv 2 1\ne 0 1\ne 1 2\n")
+    a, _ = P.load_cached(lg, labeled=True)
+    b, hit = P.load_cached(lg, labeled=True)
+    assert hit and list(b.labels) == [1, 2, 1] and np.array_equal(a.col, b.col)
+    hg = P.generate_rmat(10, 4, 0.57, 0.19, 0.19, seed=3, n_labels=5)
+    P.save_csr(str(tmp_path / "r.bin"), hg)
+    r = P.load_csr(str(tmp_path / "r.bin"))
+    assert np.array_equal(r.off, hg.off) and np.array_equal(r.col, hg.col) and np.array_equal(r.labels, hg.labels)
+    with pytest.raises(P.GpmError):
+        P.load_csr(str(tmp_path / "missing.bin"))
+
+
 def test_loader_spec_examples(tmp_path):
     import paper_1911_06969_b200 as P
     g = P.load_edge_list(_write(tmp_path, "t.el", "0 1\n1 2\n2 0\n"))   # SPEC.md:43
