@@ -306,8 +306,18 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1911_06969_b200.dist import make_exchange
-    exchange = make_exchange() if world > 1 else None
+    # N > 1: the in-library NCCL exchange (no Python on the exchange path);
+    # the torch.distributed callback only if the native one cannot start
+    exchange, exchange_ctx, native_ex, exchange_kind = None, 0, None, "none (single rank)"
+    if world > 1:
+        try:
+            from paper_1911_06969_b200.dist import NativeExchange
+            native_ex = NativeExchange()
+            exchange, exchange_ctx, exchange_kind = native_ex.fn, native_ex.ctx, "libgpm NCCL (owner-based OR)"
+        except Exception as e:
+            print(f"[bench] native NCCL exchange unavailable ({e!r}); torch.distributed callback", file=sys.stderr)
+            from paper_1911_06969_b200.dist import make_exchange
+            exchange, exchange_kind = make_exchange(), "torch.distributed callback"
     # a dedicated (non-default) stream: the engine launches every kernel on it
     # and the step events are recorded on it, so they bracket the device work
     stream = torch.cuda.Stream()
@@ -347,7 +357,7 @@ def main():
         # ---------------- device-resident path (value)
         g_und = P.Graph(hg, device=local)
         g_in = g_und.orient_dag() if app in ("tc", "cf") else g_und   # preprocessing
-        kw = dict(rank=rank, world=world, stream=sp, exchange=exchange)
+        kw = dict(rank=rank, world=world, stream=sp, exchange=exchange, exchange_ctx=exchange_ctx)
 
         def mine_step():
             skw = {}
@@ -422,7 +432,7 @@ def main():
             t = time.perf_counter()
             # TC/CF need the degree-ordered DAG: fused pipelined upload + orientation
             g = P.Graph(pinned, device=local, orient=app in ("tc", "cf"))
-            er = P.mine(g, app, k, sigma, rank=rank, world=world, exchange=exchange,
+            er = P.mine(g, app, k, sigma, rank=rank, world=world, exchange=exchange, exchange_ctx=exchange_ctx,
                         **({"steal_ctrs": use_steal.ptr} if use_steal else {}))
             del g
             torch.cuda.synchronize()
@@ -475,7 +485,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": config, "partition": partition,
+            "config": config, "partition": partition, "exchange": exchange_kind,
             "e2e": {"value": n_explored / (e2e_ms_step / 1e3), "unit": UNIT, "ms_per_step": e2e_ms_step,
                     "step_ms": [round(x, 3) for x in e2e_ms],
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -526,6 +536,8 @@ def main():
         print(json.dumps(line))
     if steal is not None:
         steal.close()
+    if native_ex is not None:
+        native_ex.close()
     if world > 1:
         dist.destroy_process_group()
 

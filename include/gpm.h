@@ -90,6 +90,23 @@ typedef struct gpm_config {
 
 void gpm_config_default(gpm_config* cfg);
 
+/* In-library NCCL implementation of gpm_exchange_fn (one process per GPU; no
+ * Python on the exchange path).  Rank 0 calls gpm_nccl_unique_id and ships
+ * the GPM_NCCL_ID_BYTES bytes to every rank by any means (MPI, file, socket,
+ * torch.distributed); each rank then calls gpm_exchange_nccl_create, or
+ * wraps a communicator it already owns (ncclComm_t) with
+ * gpm_exchange_nccl_wrap.  Set gpm_config.exchange = gpm_exchange_nccl_fn()
+ * and exchange_ctx = ctx.  Ops: 0 = ncclAllReduce(sum, u64); 1 = bitwise OR
+ * of u32 words, owner-based (grouped ncclSend/ncclRecv all-to-all of 1/N
+ * slices, device OR, ncclAllGather): 2(N-1)/N of the bytes per GPU;
+ * 2 = in-place ncclAllGather. */
+#define GPM_NCCL_ID_BYTES 128
+int gpm_nccl_unique_id(void* id_out);
+int gpm_exchange_nccl_create(const void* unique_id, int rank, int world, int device, void** ctx);
+int gpm_exchange_nccl_wrap(void* nccl_comm, void** ctx);
+gpm_exchange_fn gpm_exchange_nccl_fn(void);
+int gpm_exchange_nccl_destroy(void* ctx);
+
 /* Shared steal counters for gpm_config.steal_ctrs.  One rank creates them on
  * its device and exports a CUDA IPC handle (64 bytes) that the other ranks open
  * (peer mapping over NVLink); ranks in one process may share the pointer.

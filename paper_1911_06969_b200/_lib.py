@@ -24,7 +24,8 @@ EXPORTS = [
     "gpm_load_edge_list", "gpm_load_labeled_graph", "gpm_csr_from_edges", "gpm_generate_rmat", "gpm_csr_free",
     "gpm_last_error", "gpm_version", "gpm_steal_create", "gpm_steal_open", "gpm_steal_reset", "gpm_steal_release",
     "gpm_release_cached", "gpm_csr_save", "gpm_csr_load", "gpm_load_cached",
-    "gpm_canonicalize_batch",
+    "gpm_canonicalize_batch", "gpm_nccl_unique_id", "gpm_exchange_nccl_create", "gpm_exchange_nccl_wrap",
+    "gpm_exchange_nccl_fn", "gpm_exchange_nccl_destroy",
 ]
 
 
@@ -106,6 +107,11 @@ def lib():
         "gpm_generate_rmat": (i32, [i32, C.c_double, C.c_double, C.c_double, C.c_double, u64, u32, u64,
                                     C.POINTER(CsrStruct)]),
         "gpm_csr_free": (None, [C.POINTER(CsrStruct)]),
+        "gpm_nccl_unique_id": (i32, [vp]),
+        "gpm_exchange_nccl_create": (i32, [vp, i32, i32, i32, C.POINTER(vp)]),
+        "gpm_exchange_nccl_wrap": (i32, [vp, C.POINTER(vp)]),
+        "gpm_exchange_nccl_fn": (EXCHANGE_FN, []),
+        "gpm_exchange_nccl_destroy": (i32, [vp]),
         "gpm_canonicalize_batch": (i32, [i32, i32, u64, vp, vp, vp, vp, vp]),
         "gpm_csr_save": (i32, [C.c_char_p, C.POINTER(CsrStruct), C.c_char_p]),
         "gpm_csr_load": (i32, [C.c_char_p, C.POINTER(CsrStruct)]),

@@ -7,8 +7,10 @@ split computed identically on every rank (no communication), so the only
 exchanges are:
   * op 0  sum of u64 per-pattern counters / per-level size vectors (C1)
   * op 1  bitwise OR of u32 domain bitmaps (FSM, C2) — NCCL has no bitwise
-          reduction, so it is an all-gather of the packed words followed by an
-          OR-reduction on the device
+          reduction, so it is owner-based: an all-to-all hands every rank the
+          N copies of its 1/N slice of the words, the rank ORs them on the
+          device, and an all-gather returns the ORed slices (2(N-1)/N of the
+          bitmap bytes per GPU, vs (N-1)x for all-gather + local OR)
   * op 2  all-gather (FSM pattern-key union)
 
 Load balance beyond the static split: ``StealCounters`` creates the shared
@@ -41,13 +43,7 @@ def exchange_op(t, op: int, group=None):
     if op == 0:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     elif op == 1:
-        world = dist.get_world_size(group)
-        parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t, group=group)
-        acc = parts[0].clone()
-        for p in parts[1:]:
-            acc.bitwise_or_(p)
-        t.copy_(acc)
+        owner_or_(t, group)
     elif op == 2:  # t holds world * n elements, this rank's slot filled
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
@@ -58,6 +54,32 @@ def exchange_op(t, op: int, group=None):
         t.copy_(torch.cat(parts))
     else:
         raise ValueError(f"unknown exchange op {op}")
+
+
+def owner_or_(t, group=None):
+    """In-place bitwise OR over ranks, owner-based (the algorithm of the
+    in-library NCCL hook, csrc/nccl_exchange.cu): pad to world * per words,
+    all-to-all the slices to their owners, OR, all-gather."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if world == 1:
+        return t
+    n = t.numel()
+    per = (n + world - 1) // world
+    src = t
+    if per * world != n:
+        src = torch.zeros(per * world, dtype=t.dtype, device=t.device)
+        src[:n] = t
+    parts = torch.empty_like(src)
+    dist.all_to_all_single(parts, src, group=group)
+    own = parts.view(world, per)[0].clone()
+    for q in range(1, world):
+        own.bitwise_or_(parts.view(world, per)[q])
+    out = torch.empty_like(src)
+    dist.all_gather_into_tensor(out, own, group=group)
+    t.copy_(out[:n])
+    return t
 
 
 def dist_world(group=None) -> int:
@@ -86,6 +108,35 @@ def make_exchange(group=None):
             return 1
 
     return EXCHANGE_FN(_cb)
+
+
+class NativeExchange:
+    """The in-library NCCL exchange (gpm_exchange_nccl_*; no Python callback on
+    the exchange path).  Rank 0 draws the NCCL unique id, torch.distributed
+    broadcasts its 128 bytes, every rank creates its communicator on its GPU.
+    Pass ``exchange=ex.fn, exchange_ctx=ex.ctx`` to mine()."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        L = lib()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            check(L.gpm_nccl_unique_id(uid))
+        on_cuda = dist.get_backend(group) == "nccl"
+        h = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device="cuda" if on_cuda else "cpu")
+        dist.broadcast(h, 0, group=group)
+        raw = bytes(h.cpu().tolist())
+        ctx = C.c_void_p()
+        check(L.gpm_exchange_nccl_create(raw, rank, world, torch.cuda.current_device(), C.byref(ctx)))
+        self.ctx = ctx.value
+        self.fn = L.gpm_exchange_nccl_fn()
+
+    def close(self):
+        if self.ctx:
+            check(lib().gpm_exchange_nccl_destroy(self.ctx))
+            self.ctx = None
 
 
 class StealCounters:

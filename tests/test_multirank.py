@@ -47,6 +47,20 @@ def _worker(rank, world, port, q):
         b = torch.tensor([1 << rank, 0x100 << rank], dtype=torch.int32)
         exchange_op(b, 1)
         out["or"] = b.tolist()
+        # owner-based OR (the algorithm of csrc/nccl_exchange.cu): word counts
+        # that do and do not divide by the world size, against a plain OR
+        from paper_1911_06969_b200.dist import owner_or_
+        ok = []
+        for n in (1, 2, 7, 64, 1001):
+            arrs = [torch.from_numpy(np.random.default_rng(100 * q + n).integers(0, 2**31, n).astype(np.int32))
+                    for q in range(world)]
+            want = arrs[0].clone()
+            for a in arrs[1:]:
+                want |= a
+            mine = arrs[rank].clone()
+            owner_or_(mine)
+            ok.append(bool(torch.equal(mine, want)))
+        out["owner_or"] = ok
         g = torch.zeros(2 * world, dtype=torch.int64)
         g[2 * rank:2 * rank + 2] = torch.tensor([rank, rank + 100])
         exchange_op(g, 2)
@@ -66,8 +80,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_gloo_exchange_and_partition(oracle):
-    world = 2
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_exchange_and_partition(oracle, world):
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -79,9 +93,10 @@ def test_gloo_exchange_and_partition(oracle):
         p.join(timeout=60)
         assert p.exitcode == 0
     for r in range(world):
-        assert res[r]["sum"] == [3, 30]
-        assert res[r]["or"] == [3, 0x300]
-        assert res[r]["gather"] == [0, 100, 1, 101]
+        assert res[r]["sum"] == [sum(range(1, world + 1)), 10 * sum(range(1, world + 1))]
+        assert res[r]["or"] == [(1 << world) - 1, ((1 << world) - 1) << 8]
+        assert res[r]["gather"] == sum(([q, q + 100] for q in range(world)), [])
+        assert all(res[r]["owner_or"])
     full = oracle.mine(oracle.csr_from_edges(BF.gnp(160, 0.1, 9), 160), "cf", 4)
     assert res[0]["cf4"] == [full["total"], full["n_explored"]] == res[1]["cf4"]
 
@@ -259,3 +274,38 @@ def test_ipc_steal_counters_two_processes():
         for app, k in (("tc", 3), ("cf", 4), ("mc", 3)):
             base = P.mine(P.Graph(hg), app, k)
             assert res[r][f"{app}{k}"] == (base.total, base.stats["n_explored"], sorted(base.patterns)), (app, k)
+
+
+@pytest.mark.gpu
+def test_native_nccl_exchange_single_rank():
+    """The in-library NCCL hook (gpm_exchange_nccl_*): communicator creation
+    from a unique id, and ops 0/1/2 on device buffers at world 1 (the box has
+    one GPU; the owner-based OR algorithm is covered at world 2/3 on gloo)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import ctypes as C
+    import paper_1911_06969_b200 as P
+    from paper_1911_06969_b200._lib import check, lib
+    L = lib()
+    uid = (C.c_char * 128)()
+    check(L.gpm_nccl_unique_id(uid))
+    ctx = C.c_void_p()
+    check(L.gpm_exchange_nccl_create(bytes(uid), 0, 1, torch.cuda.current_device(), C.byref(ctx)))
+    fn = L.gpm_exchange_nccl_fn()
+    s = torch.cuda.current_stream()
+    a = torch.arange(5, dtype=torch.int64, device="cuda")
+    assert fn(ctx, a.data_ptr(), 5, 8, 0, s.cuda_stream) == 0
+    b = torch.tensor([3, 5, 9], dtype=torch.int32, device="cuda")
+    assert fn(ctx, b.data_ptr(), 3, 4, 1, s.cuda_stream) == 0
+    c = torch.tensor([7, 8], dtype=torch.int64, device="cuda")
+    assert fn(ctx, c.data_ptr(), 2, 8, 2, s.cuda_stream) == 0
+    torch.cuda.synchronize()
+    assert a.tolist() == list(range(5)) and b.tolist() == [3, 5, 9] and c.tolist() == [7, 8]
+    assert fn(ctx, a.data_ptr(), 5, 8, 9, s.cuda_stream) != 0   # unknown op -> error code, no exception
+    # mine() with the native hook bound (world 1)
+    hg = P.generate_rmat(10, 8, 0.45, 0.15, 0.15, seed=3, n_labels=4, label_seed=7)
+    g = P.Graph(hg)
+    base = P.mine(g, "fsm", 3, 20)
+    r = P.mine(g, "fsm", 3, 20, exchange=fn, exchange_ctx=ctx.value)
+    assert r.patterns == base.patterns
+    check(L.gpm_exchange_nccl_destroy(ctx))
