@@ -208,7 +208,8 @@ enum {
   GPM_PATH_PLANNER_CHUNKS = 1u << 8,   /* a level was split by the memory planner  */
   GPM_PATH_FSM_ROUNDS = 1u << 9,       /* FSM domain bitmaps in several rounds     */
   GPM_PATH_FSM_FUSED_LAST = 1u << 10,  /* FSM last level: domain pass fused        */
-  GPM_PATH_FSM_GROUPED = 1u << 11      /* FSM passes over parents grouped by code  */
+  GPM_PATH_FSM_GROUPED = 1u << 11,     /* FSM passes over parents grouped by code  */
+  GPM_PATH_FSM_FAN = 1u << 12          /* FSM last level: fan-out pass (dense slots) */
 };
 int gpm_result_stats(const gpm_result* r, gpm_stats* out);
 

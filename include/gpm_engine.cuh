@@ -878,7 +878,12 @@ void mine(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm_result
   const size_t freeb = device_free_bytes();
   const u64 budget = cfg.mem_budget ? cfg.mem_budget : (u64)(0.6 * (double)freeb);
   const int mat_levels = std::max(1, k - 3);
-  c.cap_entries = std::max<u64>(kBatch, std::min<u64>((u64(1) << 32) - 1, budget / 16 / mat_levels));
+  // bytes per materialised entry: 8 B in its level (idx + vid) for every level
+  // held at once, plus the next level's per-parent temporaries while it is the
+  // parent level (work u64, compacted index u32, offsets u64, k-1 u64
+  // descriptors): a chunk of cap_entries parents always fits the budget
+  const u64 per_entry = 8 * (u64)mat_levels + 20 + 8 * (u64)std::max(1, k - 1);
+  c.cap_entries = std::max<u64>(kBatch, std::min<u64>((u64(1) << 32) - 1, budget / per_entry));
   c.mask_budget = budget / 4;
   c.nbins = App::kReduce == kReduceCodes ? App::num_codes(k) : 1;
   if (App::kReduce == kReduceCodes && App::kFilter && c.nbins <= 0) throw Error(GPM_EINVAL, "num_codes must be > 0");

@@ -889,6 +889,267 @@ __global__ void __launch_bounds__(kGT, 1) egroup_kernel(FsmArgs a, GroupArgs ga)
   if (MODE != kDomain && lane == 0 && acc) atomicAdd(a.accepted, acc);  // acc is warp-uniform
 }
 
+// ---------------------------------------------------------------------------
+// Fan-out pass of the fused last level.  Parents are sorted
+// by their exact quick code; an item is (one parent code P, one extended
+// position q, a range of P's parents).  Every child of the item then has the
+// quick code
+//   new vertex w:   base(P, q) | label(w) << npairs(nv+1)   -> slot label(w)
+//   closing w=v_r:  code(P + edge (q, r))                  -> slot NL + r
+// so the item's codes are DENSE slots of a per-CTA shared table (counts and
+// quick-position domain rows) -- no hashing or code building per child.  A
+// child's new vertex sets one bit of its slot's new-vertex row; the parent
+// positions' bits are the same for all children of one parent with one slot,
+// so each parent ORs its vertices once per slot it produced (a label mask
+// reduced over the warp), not once per child.  At the end of the item every
+// used slot adds its count to the level's quick-code hash (dense id) and ORs
+// its rows into that id's global quick-position bitmaps (qbm) -- the same
+// state the rest of the fused path (canonicalise, merge_qbm) consumes.
+// Lanes map to the candidates N(v_q) of one parent at a time (coalesced);
+// parent descriptors are built 32 at a time, one per lane, into shared memory.
+constexpr int kFT = 512;                 // threads per fan CTA
+constexpr u32 kFanParents = 4096;        // parents per item (large groups split)
+
+struct FanItem {
+  u64 code;    // parent quick code
+  u32 pa, pb;  // parents [pa, pb) of the sorted compacted order
+  u32 q;       // extended position
+  u32 pad;
+};
+
+struct FanArgs {
+  const FanItem* items;
+  u64 nitems;
+  unsigned long long* ctr;
+  u32 nl;      // new-vertex slots (1 << LB <= 32)
+};
+
+template <int LEV>
+struct FanDesc {  // per-warp parent descriptors, struct of arrays over 32 lanes
+  static constexpr int MV = LEV + 1;
+  u64 cb[32];
+  u64 thrq[32];
+  u64 dupe[LEV][32];
+  u64 thr[LEV + 1][32];
+  u32 deg[32];
+  u32 x[32];
+  u32 v[MV][32];
+  u32 lr[MV][32];
+  u32 stp[32];
+};
+
+template <int LEV>
+__global__ void __launch_bounds__(kFT, 1) efan_kernel(FsmArgs a, FanArgs fa) {
+  constexpr int MV = LEV + 1;
+  constexpr int NW = kFT / 32;
+  extern __shared__ __align__(16) unsigned char fsm_fan_smem[];
+  const u32 nslot = fa.nl + MV;
+  const u64 rowlen = (u64)a.kpos * a.words;
+  u32* rows = reinterpret_cast<u32*>(fsm_fan_smem);          // [nslot][kpos][words]
+  u32* cnt = rows + (u64)nslot * rowlen;                      // [nslot]
+  u32* sid = cnt + nslot;                                     // [nslot] quick-code id at flush
+  const u64 doff = (u64)nslot * rowlen + 2 * nslot;
+  FanDesc<LEV>* descs = reinterpret_cast<FanDesc<LEV>*>(rows + doff + (doff & 1));  // 8-byte aligned
+  __shared__ u64 s_item;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  FanDesc<LEV>& D = descs[wid];
+  unsigned long long acc = 0;
+  for (u64 i = threadIdx.x; i < (u64)nslot * rowlen; i += kFT) rows[i] = 0u;
+  for (;;) {
+    for (u32 i = threadIdx.x; i < nslot; i += kFT) cnt[i] = 0u;
+    if (threadIdx.x == 0) s_item = atomicAdd(fa.ctr, 1ull);
+    __syncthreads();
+    const u64 it = s_item;
+    if (it >= fa.nitems) break;
+    const FanItem item = fa.items[it];
+    const int q = (int)item.q;
+    int nv;
+    u32 plab[8], pmask;
+    pat::decode(item.code, a.LB, &nv, plab, &pmask);
+    u64 labp = 0;
+    for (int i = 0; i < nv; ++i) labp = (labp << a.LB) | plab[i];
+    const u32 lshift = (u32)pat::npairs(nv + 1);
+    const u64 newbase = pat::make_code_packed(nv + 1, labp << a.LB,
+                                              pat::widen_mask(pmask, nv) | (1u << pat::pair_index(q, nv, nv + 1)));
+    // ---- warps take 32-parent batches of the item
+    for (u32 b0 = item.pa + 32 * wid; b0 < item.pb; b0 += 32 * NW) {
+      const u32 nb = min(32u, item.pb - b0);
+      __syncwarp();
+      if ((u32)lane < nb) {
+        EEmb<LEV> E;
+        reconstruct_e<LEV>(a.L, a.g, ldg(a.pidx + b0 + lane), E);
+        u64 dupe[LEV];
+#pragma unroll
+        for (int j = 0; j < LEV; ++j) dupe[j] = ((u64)E.e0[j] << 32) | E.e1[j];
+        u64 thr[LEV + 1];
+#pragma unroll
+        for (int pp = 1; pp <= LEV; ++pp) {
+          u64 t = dupe[0];
+#pragma unroll
+          for (int s2 = 2; s2 <= LEV; ++s2)
+            if (s2 > pp) t = max(t, dupe[s2 - 1]);
+          thr[pp] = t;
+        }
+        thr[0] = thr[1];
+        u32 stp = 0, x = 0;
+#pragma unroll
+        for (int i = 0; i < MV; ++i) {
+          const bool in = i < E.nv;
+          D.v[i][lane] = in ? E.v[i] : 0xffffffffu;
+          D.lr[i][lane] = in ? ldg(a.lrank + E.v[i]) : 0u;
+          stp |= (u32)(in ? E.step[i] : 0) << (4 * i);
+          if (i == q) x = E.v[i];
+        }
+#pragma unroll
+        for (int j = 0; j < LEV; ++j) D.dupe[j][lane] = dupe[j];
+        u64 tq = thr[0];
+#pragma unroll
+        for (int pp = 0; pp <= LEV; ++pp) {
+          D.thr[pp][lane] = thr[pp];
+          if (pp == (int)((stp >> (4 * q)) & 15u)) tq = thr[pp];
+        }
+        const u64 cb = ldg(a.g.off + x);
+        D.cb[lane] = cb;
+        D.deg[lane] = (u32)(ldg(a.g.off + x + 1) - cb);
+        D.x[lane] = x;
+        D.thrq[lane] = tq;
+        D.stp[lane] = stp;
+      }
+      __syncwarp();
+      for (u32 j = 0; j < nb; ++j) {
+        const u32 x = D.x[j], deg = D.deg[j];
+        const u64 cb = D.cb[j], thrq = D.thrq[j];
+        u32 pv[MV];
+#pragma unroll
+        for (int i = 0; i < MV; ++i) pv[i] = D.v[i][j];
+        u32 lm = 0, cm = 0;  // labels of new-vertex children / closing positions produced
+        for (u32 jb = 0; jb < deg; jb += 32) {
+          bool ok = false;
+          if (jb + lane < deg) {
+            const u32 w = ldg(a.g.col + cb + jb + lane);
+            int r = nv;
+#pragma unroll
+            for (int i = 0; i < MV; ++i)
+              if (i < nv && pv[i] == w) r = i;
+            const u64 n = w < x ? (((u64)w << 32) | x) : (((u64)x << 32) | w);
+            if (r == nv) {
+              ok = n > thrq;
+              if (ok) {
+                const u32 lw = ldg(a.g.lab + w);
+                const u32 lr = ldg(a.lrank + w);
+                atomicAdd(cnt + lw, 1u);
+                u32* wp = rows + ((u64)lw * a.kpos + nv) * a.words + (lr >> 5);
+                const u32 bit = 1u << (lr & 31);
+                if (!(*wp & bit)) atomicOr(wp, bit);
+                lm |= 1u << lw;
+              }
+            } else if (r > q) {  // closing edge from its earlier-inserted endpoint
+              bool dup = false;
+#pragma unroll
+              for (int jj = 0; jj < LEV; ++jj) dup |= D.dupe[jj][j] == n;
+              const u32 stp = D.stp[j];
+              const int sq = (int)((stp >> (4 * q)) & 15u), sr = (int)((stp >> (4 * r)) & 15u);
+              const int sm = min(sq, sr);
+              u64 t = D.thr[0][j];
+#pragma unroll
+              for (int pp = 1; pp <= LEV; ++pp)
+                if (pp == sm) t = D.thr[pp][j];
+              ok = !dup && n > t;
+              if (ok) cm |= 1u << r;
+            }
+          }
+          acc += __popc(__ballot_sync(0xffffffffu, ok));
+        }
+        // parent positions: once per (parent, slot)
+        lm = __reduce_or_sync(0xffffffffu, lm);
+        cm = __reduce_or_sync(0xffffffffu, cm);
+        if (lm | cm) {
+          u32 plr[MV];
+#pragma unroll
+          for (int i = 0; i < MV; ++i) plr[i] = D.lr[i][j];
+          if (lm >> lane & 1u) {  // lane = new-vertex label (nl <= 32)
+#pragma unroll
+            for (int i = 0; i < MV; ++i)
+              if (i < nv) {
+                u32* wp = rows + ((u64)lane * a.kpos + i) * a.words + (plr[i] >> 5);
+                const u32 bit = 1u << (plr[i] & 31);
+                if (!(*wp & bit)) atomicOr(wp, bit);
+              }
+          }
+          if (lane < MV && (cm >> lane & 1u)) {
+            const u32 sl = fa.nl + lane;
+            atomicAdd(cnt + sl, 1u);  // one closing child per (parent, q, r)
+#pragma unroll
+            for (int i = 0; i < MV; ++i)
+              if (i < nv) {
+                u32* wp = rows + ((u64)sl * a.kpos + i) * a.words + (plr[i] >> 5);
+                atomicOr(wp, 1u << (plr[i] & 31));
+              }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- flush: count -> quick-code hash (dense id), rows -> the id's qbm rows
+    for (u32 sl = threadIdx.x; sl < nslot; sl += kFT) {
+      u32 id = 0;
+      if (cnt[sl]) {
+        u64 code;
+        if (sl < fa.nl) code = newbase | ((u64)sl << lshift);
+        else code = pat::make_code_packed(nv, labp, pmask | (1u << pat::pair_index(q, (int)(sl - fa.nl), nv)));
+        id = hash_add(a.H, code, cnt[sl]);
+        if (id && id - 1 >= a.qcap) {
+          *a.qover = 1;
+          id = 0;
+        }
+      }
+      sid[sl] = id;
+    }
+    __syncthreads();
+    for (u64 rr = wid; rr < (u64)nslot * a.kpos; rr += NW) {
+      const u32 sl = (u32)(rr / a.kpos);
+      const int i = (int)(rr % a.kpos);
+      if (!cnt[sl]) continue;
+      const int cnv = sl < fa.nl ? nv + 1 : nv;
+      if (i >= cnv) continue;
+      u32* src = rows + rr * a.words;
+      const u32 id = sid[sl];
+      u32* dst = id ? a.qbm + ((u64)(id - 1) * a.kpos + i) * a.words : nullptr;
+      for (u64 w = lane; w < a.words; w += 32) {
+        const u32 val = src[w];
+        if (val) {
+          if (dst) atomicOr(dst + w, val);
+          src[w] = 0u;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (lane == 0 && acc) atomicAdd(a.accepted, acc);
+}
+
+// exact quick code of every compacted parent (fan grouping key)
+template <int LEV>
+__global__ void pcode_kernel(DevGraph g, ELevels L, const u32* __restrict__ pidx, u64 nz, int LB,
+                             u64* __restrict__ codes) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nz; i += (u64)gridDim.x * blockDim.x) {
+    EEmb<LEV> E;
+    reconstruct_e<LEV>(L, g, pidx[i], E);
+    codes[i] = parent_code<LEV>(E, LB);
+  }
+}
+
+__global__ void gstart64_kernel(const u64* __restrict__ keys, u64 n, u8* __restrict__ flag) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+__global__ void gather_codes_kernel(const u64* __restrict__ codes, const u32* __restrict__ starts, u64 G,
+                                    u64* __restrict__ out) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < G; i += (u64)gridDim.x * blockDim.x)
+    out[i] = codes[starts[i]];
+}
+
 // ---- level 1 (single edges): reduce + filter before the loop
 __device__ __forceinline__ u64 l1_code(const DevGraph& g, u32 u, u32 v, int LB) {
   u32 lab[2] = {ldg(g.lab + u), ldg(g.lab + v)};
@@ -1528,6 +1789,98 @@ struct Fsm {
     ++tl.launches;
   }
 
+  // ---------------------------------------------------------- fan-out pass (last level)
+  size_t fan_smem(int LEVv, int kpos, u64 words) const {
+    const u64 nslot = (u64(1) << LB) + LEVv + 1;
+    const u64 desc = (u64)(kFT / 32) * (8 * 32 * (2 + 2 * LEVv + 1) + 4 * 32 * (3 + 2 * (LEVv + 1))) + 64;
+    return (size_t)(4 * (nslot * kpos * words + 2 * nslot + 2) + desc);
+  }
+  bool fan_fits(int LEVv, int kpos, u64 words) const {
+    if (LB > 5) return false;  // label slots are lanes of a warp
+    int maxs = 0;
+    GPM_CUDA(cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, G.device));
+    return fan_smem(LEVv, kpos, words) + 1024 <= (size_t)maxs;
+  }
+
+  // compacted parents sorted by their exact quick code; codes sorted alongside
+  template <int LEV>
+  void sort_parents_exact(const ELevels& L, DBuf<u32>& pidx, u64 nz, DBuf<u64>& codes) {
+    codes.alloc(nz, s);
+    pcode_kernel<LEV><<<grid1(nz), 256, 0, s>>>(g, L, pidx.get(), nz, LB, codes.get());
+    GPM_CUDA(cudaGetLastError());
+    DBuf<u64> k2(nz, s);
+    DBuf<u32> p2(nz, s);
+    size_t tmp = 0;
+    GPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, codes.get(), k2.get(), pidx.get(), p2.get(), (int64_t)nz, 0,
+                                             64, s));
+    DBuf<u8> t(tmp, s);
+    GPM_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, codes.get(), k2.get(), pidx.get(), p2.get(), (int64_t)nz, 0,
+                                             64, s));
+    tl.launches += 9;
+    codes = std::move(k2);
+    pidx = std::move(p2);
+  }
+
+  // items: (parent code group, extended position q, <= kFanParents parents)
+  void build_fan_items(const DBuf<u64>& codes, u64 nz, DBuf<FanItem>& items, u64& nitems) {
+    DBuf<u8> flag(nz, s);
+    gstart64_kernel<<<grid1(nz), 256, 0, s>>>(codes.get(), nz, flag.get());
+    DBuf<u32> starts(nz, s);
+    DBuf<u64> ng(1, s);
+    size_t tmp = 0;
+    thrust::counting_iterator<u32> it(0);
+    GPM_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, it, flag.get(), starts.get(), ng.get(), (int64_t)nz, s));
+    DBuf<u8> t(tmp, s);
+    GPM_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, it, flag.get(), starts.get(), ng.get(), (int64_t)nz, s));
+    const u64 G_ = d2h(ng.get());
+    DBuf<u64> gc(std::max<u64>(1, G_), s);
+    gather_codes_kernel<<<grid1(std::max<u64>(1, G_)), 256, 0, s>>>(codes.get(), starts.get(), G_, gc.get());
+    GPM_CUDA(cudaGetLastError());
+    tl.launches += 4;
+    std::vector<u32> hs(G_);
+    std::vector<u64> hc(G_);
+    GPM_CUDA(cudaMemcpyAsync(hs.data(), starts.get(), sizeof(u32) * G_, cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaMemcpyAsync(hc.data(), gc.get(), sizeof(u64) * G_, cudaMemcpyDeviceToHost, s));
+    sync();
+    std::vector<FanItem> v;
+    for (u64 i = 0; i < G_; ++i) {
+      const u32 a0 = hs[i], a1 = i + 1 < G_ ? hs[i + 1] : (u32)nz;
+      const int nvv = pat::code_nv(hc[i]);
+      for (int q = 0; q < nvv; ++q)
+        for (u32 b = a0; b < a1; b += kFanParents) v.push_back(FanItem{hc[i], b, std::min<u32>(a1, b + kFanParents), (u32)q, 0});
+    }
+    // large items first (tail balance)
+    std::stable_sort(v.begin(), v.end(), [](const FanItem& x, const FanItem& y) { return x.pb - x.pa > y.pb - y.pa; });
+    nitems = v.size();
+    items.alloc(std::max<u64>(1, nitems), s);
+    if (nitems) GPM_CUDA(cudaMemcpyAsync(items.get(), v.data(), sizeof(FanItem) * nitems, cudaMemcpyHostToDevice, s));
+    sync();
+    trace("fan groups -> items", (double)G_, (double)nitems);
+  }
+
+  template <int LEV>
+  void launch_fan(FsmArgs& a, const DBuf<FanItem>& items, u64 nitems, const char* name, double bytes) {
+    FanArgs fa{};
+    fa.items = items.get();
+    fa.nitems = nitems;
+    fa.ctr = d_ctr.get();
+    fa.nl = 1u << LB;
+    const size_t smem = fan_smem(LEV, a.kpos, a.words);
+    auto kern = efan_kernel<LEV>;
+    GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFT, smem));
+    occ = std::max(1, occ);
+    const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sms * occ, nitems));
+    GPM_CUDA(cudaMemsetAsync(d_ctr.get(), 0, sizeof(unsigned long long), s));
+    st.paths |= GPM_PATH_FSM_FAN;
+    size_t ev = tl.begin(std::string(name) + "_L" + std::to_string(LEV), bytes);
+    kern<<<(unsigned)blocks, kFT, smem, s>>>(a, fa);
+    GPM_CUDA(cudaGetLastError());
+    tl.end(ev);
+    ++tl.launches;
+  }
+
   // Extends level LEV (np parents) -> reduce (+ filter into out arrays unless last)
   template <int LEV>
   void extend_level(const ELevels& L, u64 np, bool last, DBuf<u32>& oi, DBuf<u32>& ov, DBuf<u8>& oh, u64& nout) {
@@ -1555,10 +1908,13 @@ struct Fsm {
     // grouped passes: parents sorted by quick code
     Groups gr;
     DBuf<u32> gkeys_sorted;
+    // fused last level: the fan-out pass over parents grouped by exact code
+    const bool fan_ok = last && nz && !std::getenv("GPM_FSM_NOFAN") && !std::getenv("GPM_FSM_TWO_PASS") &&
+                        fan_fits(LEV, LEV + 2, (max_class + 31) / 32);
     {
       GroupArgs probe{};
       size_t sm = 0;
-      gr.on = nz && !std::getenv("GPM_FSM_UNGROUPED") &&
+      gr.on = nz && !fan_ok && !std::getenv("GPM_FSM_UNGROUPED") &&
               group_geometry(kDomain, LEV + 2, (max_class + 31) / 32, probe, sm);
     }
     if (gr.on) sort_parents<LEV>(L, pidx, nz, gkeys_sorted);
@@ -1623,6 +1979,20 @@ struct Fsm {
       if (qcap >= 1024) qbm.alloc(qcap * kposL * wordsL, s);
       else qcap = 0;
     }
+    DBuf<FanItem> fitems;
+    u64 nfan = 0;
+    const bool use_fan = fan_ok && qcap && nb;
+    if (use_fan) {
+      DBuf<u64> pcodes;
+      sort_parents_exact<LEV>(L, pidx, nz, pcodes);
+      // Wp in the new parent order (the unfused fallback passes read it)
+      egather_kernel<<<grid1(nz), 256, 0, s>>>(w.get(), pidx.get(), nz, Wp.get());
+      GPM_CUDA(cudaGetLastError());
+      ++tl.launches;
+      GPM_CUDA(cudaMemsetAsync(Wp.get() + nz, 0, sizeof(u64), s));
+      scan_inplace(Wp.get(), nz + 1, s);
+      build_fan_items(pcodes, nz, fitems, nfan);
+    }
     for (;;) {
       alloc_hash(R, cap);
       GPM_CUDA(cudaMemsetAsync(accepted.get(), 0, sizeof(unsigned long long), s));
@@ -1638,7 +2008,8 @@ struct Fsm {
           a.words = wordsL;
           a.lrank = lrank.get();
         }
-        if (gr.on) launch_group<LEV>(a, gr, qcap ? kQCD : kQC, qcap ? "fsm_group_qc_domain" : "fsm_group_qc", bytes_in);
+        if (use_fan) launch_fan<LEV>(a, fitems, nfan, "fsm_fan_qc_domain", bytes_in);
+        else if (gr.on) launch_group<LEV>(a, gr, qcap ? kQCD : kQC, qcap ? "fsm_group_qc_domain" : "fsm_group_qc", bytes_in);
         else launch<LEV>(a, kQC, qcap ? "fsm_extend_qc_domain" : "fsm_extend_qc", bytes_in);
       }
       if (d2h(R.overflow.get()) == 0) break;

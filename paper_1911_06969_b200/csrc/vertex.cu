@@ -62,6 +62,7 @@ struct EdgeArgs {
   unsigned long long* total;  // FUSED
   unsigned long long* cand;   // candidates streamed (stats)
   u32 hstride;                // per-warp hash slots (power of two)
+  u32 long_min;               // lane kernel: lists this long are streamed by the whole warp
   const u32* wv;              // SIB: new vertex per entry (level vid array)
 };
 
@@ -341,17 +342,315 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
 }
 
 
+// Hybrid variant of edge_chunk_kernel for the inspection (COUNT) and fused
+// (FUSED) passes: same items, staging and results.  A parent whose candidate
+// list N+(v1) has at least long_min (default 32) entries is streamed by the
+// whole warp, one parent at a time (no lane -> parent mapping, the probe's
+// root slot is warp-uniform); the shorter lists are packed 32 candidates per
+// step with the OR-reduction mapping of edge_chunk_kernel.  Accepted
+// children are rare (PAT: 1 in 400): COUNT records them as (parent lane,
+// index within the parent) -- the index from a per-parent shared counter
+// plus the rank among same-parent lanes of the step, so it follows u order
+// -- and places them at prefix(parent) + index, i.e. in the sequential
+// (parent, u) order the execution pass copies.  The execution pass (WRITE)
+// stays on edge_chunk_kernel.
+constexpr u32 kLongDefault = 32;
+
+template <int MODE, bool SIB>
+__global__ void __launch_bounds__(kThreads, 5) edge_lane_kernel(EdgeArgs a) {
+  static_assert(MODE != kWrite, "execution runs on edge_chunk_kernel");
+  extern __shared__ __align__(16) u32 s_rhash[];  // [kThreads/32][hstride]
+  __shared__ u64 s_cp[kThreads / 32][32];   // short parent rank: &col[cb] - 4 * exclusive start
+  __shared__ u32 s_ex[kThreads / 32][64];   // short parent rank: exclusive start; ~0 past the last
+  __shared__ u32 s_sl[kThreads / 32][32];   // short parent rank: (lane << 8) | root slot
+  __shared__ u64 s_rb[kThreads / 32][32];   // per root slot: out-list begin
+  __shared__ u32 s_rk[kThreads / 32][64];   // per root slot: exclusive key start; ~0 past the roots
+  __shared__ u32 s_rd[kThreads / 32][32];   // per root slot: out-degree
+  __shared__ u32 s_pc[kThreads / 32][32];   // COUNT: accepted children per parent lane
+  __shared__ __align__(8) u32 s_ac[kThreads / 32][2 * kSparseWords];  // COUNT: (lane << 16 | idx, u)
+  __shared__ __align__(8) u32 s_mw[kThreads / 32][2 * kSparseWords];  // COUNT: ordered (parent, u) pairs
+  __shared__ u32 s_na[kThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const u32 lemask = lanemask_lt() | (1u << lane);
+  u32* T = s_rhash + wid * a.hstride;
+  u64* const scp = s_cp[wid];
+  u32* const sex = s_ex[wid];
+  u32* const ssl = s_sl[wid];
+  u64* const srb = s_rb[wid];
+  u32* const srk = s_rk[wid];
+  u32* const srd = s_rd[wid];
+  u32* const spc = s_pc[wid];
+  u32* const sac = s_ac[wid];
+  u32* const smw = s_mw[wid];
+  srk[32 + lane] = 0xffffffffu;
+  sex[32 + lane] = 0xffffffffu;
+  const DevGraph& g = a.g;
+  unsigned long long acc_total = 0, acc_cand = 0;
+  u32 mbase = 0, mend = 0;
+  u64 grab = 0, grab_left = 0;
+  const u32* const keysrc = SIB ? a.wv : g.col;
+  for (;;) {
+    if (grab_left == 0) {
+      u64 it_ = 0;
+      if (lane == 0) it_ = atomicAdd(a.ctr, (unsigned long long)a.grab) + a.ibeg;
+      grab = __shfl_sync(0xffffffffu, it_, 0);
+      grab_left = a.grab;
+    }
+    const u64 item = grab++;
+    --grab_left;
+    if (item >= a.iend) break;
+    const u64 e = a.lo + item * 32 + lane;
+    const bool valid = e < a.hi;
+    const u32 v0 = valid ? ldg(a.src + e) : 0xffffffffu;
+    const u32 v1 = valid ? ldg(keysrc + e) : 0u;
+    // ---- roots of the item and their staged out-lists (as edge_chunk_kernel)
+    const u32 vprev = __shfl_up_sync(0xffffffffu, v0, 1);
+    const bool lead = valid && (lane == 0 || v0 != vprev);
+    const u32 lmask = __ballot_sync(0xffffffffu, lead);
+    const u32 slot = __popc(lmask & lemask) - 1;
+    u64 rb = 0;
+    u32 rd = 0;
+    if (lead) {
+      if (SIB) {
+        u64 lo_ = 0, hi_ = e;
+        while (lo_ < hi_) {
+          const u64 mid = (lo_ + hi_) >> 1;
+          if (ldg(a.src + mid) < v0) lo_ = mid + 1;
+          else hi_ = mid;
+        }
+        rb = lo_;
+        lo_ = e + 1;
+        hi_ = a.hi;
+        while (lo_ < hi_) {
+          const u64 mid = (lo_ + hi_) >> 1;
+          if (ldg(a.src + mid) <= v0) lo_ = mid + 1;
+          else hi_ = mid;
+        }
+        rd = (u32)(lo_ - rb);
+      } else {
+        rb = ldg(g.off + v0);
+        rd = (u32)(ldg(g.off + v0 + 1) - rb);
+      }
+    }
+    u32 kin = rd;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 t = __shfl_up_sync(0xffffffffu, kin, o);
+      if (lane >= o) kin += t;
+    }
+    const u32 K = __shfl_sync(0xffffffffu, kin, 31);
+    const u32 nr = __popc(lmask);
+    __syncwarp();
+    srk[lane] = 0xffffffffu;
+    sex[lane] = 0xffffffffu;
+    if (MODE == kCount) {
+      spc[lane] = 0;
+      if (lane == 0) s_na[wid] = 0;
+    }
+    __syncwarp();
+    if (lead) {
+      srb[slot] = rb;
+      srk[slot] = kin - rd;
+      srd[slot] = rd;
+    }
+    __syncwarp();
+    const bool use_hash = 2 * K <= a.hstride;
+    u32 sh = 0, hmask = 0;
+    if (use_hash) {
+      u32 cap = 64;
+      while (cap < 8 * K && cap < a.hstride) cap <<= 1;
+      hb_geom(cap, sh, hmask);
+      for (u32 i = lane * 4; i < cap; i += 128)
+        *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+      __syncwarp();
+      u32 R = 0;
+      for (u32 kb = 0; kb < K; kb += 32) {
+        const u32 d = srk[R + 1 + lane] - kb;
+        const u32 starts = __reduce_or_sync(0xffffffffu, d < 32u ? (1u << d) : 0u);
+        const u32 r = min(R + __popc(starts & lemask), nr - 1);
+        R += __popc(starts);
+        const u32 k = kb + lane;
+        if (k < K) hb_insert(T, sh, hmask, (ldg(keysrc + srb[r] + (k - srk[r])) << 5) | r);
+      }
+      __syncwarp();
+    }
+    auto probe = [&](u32 u, u32 sl) -> bool {
+      if (use_hash) return hb_has(T, sh, hmask, (u << 5) | sl);
+      return contains_sorted(keysrc + srb[sl], srd[sl], u);
+    };
+    // record an accepted child of parent lane pl at index idx (COUNT)
+    auto record = [&](u32 pl, u32 idx, u32 u) {
+      const u32 qd = atomicAdd(&s_na[wid], 1u);
+      if (qd < kSparseWords) {
+        sac[2 * qd] = (pl << 16) | idx;
+        sac[2 * qd + 1] = u;
+      }
+    };
+    // ---- this lane's parent: candidates N+(v1)
+    u64 cb = 0;
+    u32 w = 0;
+    if (valid) {
+      cb = ldg(g.off + v1);
+      w = (u32)(ldg(g.off + v1 + 1) - cb);
+    }
+    const u32 total = __reduce_add_sync(0xffffffffu, w);
+    acc_cand += total;
+    if (total == 0) {
+      if (MODE == kCount && lane == 0) {
+        a.cnt[item] = 0;
+        a.moff[item] = ~0ull;
+      }
+      continue;
+    }
+    u32 c = 0;  // accepted children of the item (warp-uniform)
+    // ---- long parents, warp-cooperative
+    for (u32 lm = __ballot_sync(0xffffffffu, w >= a.long_min); lm; lm &= lm - 1) {
+      const int p = __ffs(lm) - 1;
+      const u64 pcb = __shfl_sync(0xffffffffu, cb, p);
+      const u32 pw = __shfl_sync(0xffffffffu, w, p);
+      const u32 psl = __shfl_sync(0xffffffffu, slot, p);
+      const u32* const pl = g.col + pcb;
+      u32 pc = 0;
+      u32 u = lane < pw ? ldg(pl + lane) : 0u;
+      for (u32 jb = 0; jb < pw; jb += 32) {
+        const u32 nu = jb + 32 + lane < pw ? ldg(pl + jb + 32 + lane) : 0u;
+        const bool ok = jb + lane < pw && probe(u, psl);
+        const u32 m = __ballot_sync(0xffffffffu, ok);
+        if (MODE == kCount && ok) record((u32)p, pc + __popc(m & lanemask_lt()), u);
+        pc += __popc(m);
+        u = nu;
+      }
+      if (MODE == kCount && lane == 0) spc[p] = pc;
+      c += pc;
+    }
+    // ---- short parents, packed 32 candidates per step
+    const bool sp = w > 0 && w < a.long_min;
+    const u32 smask = __ballot_sync(0xffffffffu, sp);
+    if (smask) {
+      u32 incl = sp ? w : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const u32 stot = __shfl_sync(0xffffffffu, incl, 31);
+      const u32 rank = __popc(smask & lanemask_lt());
+      if (sp) {
+        scp[rank] = reinterpret_cast<u64>(g.col) + 4 * (cb - (u64)(incl - w));
+        sex[rank] = incl - w;
+        ssl[rank] = ((u32)lane << 8) | slot;
+      }
+      __syncwarp();
+      u32 P = 0;
+      auto map_step = [&](u32 jb) -> u32 {
+        const u32 d = sex[P + 1 + lane] - jb;
+        const u32 starts = __reduce_or_sync(0xffffffffu, d < 32u ? (1u << d) : 0u);
+        const u32 myp = P + __popc(starts & lemask);
+        P += __popc(starts);
+        return myp;
+      };
+      u32 myp = map_step(0);
+      u32 u = lane < stot ? ldg(reinterpret_cast<const u32*>(scp[myp]) + lane) : 0u;
+      for (u32 jb = 0; jb < stot; jb += 32) {
+        const u32 j = jb + lane;
+        u32 nmyp = 0, nu = 0;
+        if (jb + 32 < stot) {
+          nmyp = map_step(jb + 32);
+          if (j + 32 < stot) nu = ldg(reinterpret_cast<const u32*>(scp[nmyp]) + j + 32);
+        }
+        const u32 sl = j < stot ? ssl[myp] : 0u;
+        const bool ok = j < stot && probe(u, sl & 0xffu);
+        const u32 m = __ballot_sync(0xffffffffu, ok);
+        if (MODE == kCount && m) {
+          // index within the parent: its count so far + rank among same-parent lanes
+          const u32 peers = __match_any_sync(0xffffffffu, ok ? myp : 0xffffffffu);
+          if (ok) {
+            const int leader = __ffs(peers) - 1;
+            const u32 pl = sl >> 8;
+            u32 base = 0;
+            if (lane == leader) base = atomicAdd(&spc[pl], (u32)__popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            record(pl, base + __popc(peers & lanemask_lt()), u);
+          }
+        }
+        c += __popc(m);
+        myp = nmyp;
+        u = nu;
+      }
+    }
+    if (MODE == kFused) acc_total += c;
+    if (MODE == kCount) {
+      __syncwarp();
+      u64 mo = ~0ull;
+      if (c && c <= kSparseWords && a.masks) {
+        // order the records: (parent lane, index) -> prefix(parent lane) + index
+        u32 pcnt = spc[lane], pincl = pcnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const u32 t = __shfl_up_sync(0xffffffffu, pincl, o);
+          if (lane >= o) pincl += t;
+        }
+        const u32 pre = pincl - pcnt;
+        for (u32 ib = 0; ib < c; ib += 32) {
+          const u32 i = ib + lane;
+          const u32 key = i < c ? sac[2 * i] : 0u;
+          const u32 pos = __shfl_sync(0xffffffffu, pre, key >> 16) + (key & 0xffffu);
+          if (i < c) {
+            smw[2 * pos] = (u32)(item * 32 + (key >> 16));
+            smw[2 * pos + 1] = sac[2 * i + 1];
+          }
+        }
+        __syncwarp();
+        if (mbase + 2 * c > mend) {
+          unsigned long long t = 0;
+          if (lane == 0) t = atomicAdd(a.mtop, (unsigned long long)kMaskChunk);
+          t = __shfl_sync(0xffffffffu, t, 0);
+          if (t + kMaskChunk <= a.mcap) {
+            mbase = (u32)t;
+            mend = (u32)(t + kMaskChunk);
+          } else {
+            mbase = mend = 0;
+          }
+        }
+        if (mbase + 2 * c <= mend) {
+          for (u32 i = lane; i < 2 * c; i += 32) a.masks[mbase + i] = smw[i];
+          mo = mbase;
+          mbase += 2 * c;
+        }
+      }
+      if (lane == 0) {
+        a.cnt[item] = c;
+        a.moff[item] = mo;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (MODE == kFused && acc_total) atomicAdd(a.total, acc_total);
+    if (acc_cand) atomicAdd(a.cand, acc_cand);
+  }
+}
+
 template <int MODE, bool SIB = false>
 void launch_edge(Ctx& c, EdgeArgs& a, const std::string& what, double bytes) {
-  auto kern = edge_chunk_kernel<MODE, SIB>;
+  // GPM_CF_STREAM=1: the packed-stream kernel (all lanes on the concatenated
+  // candidate lists) instead of the lane-per-parent one
+  static const bool stream_env = std::getenv("GPM_CF_STREAM") != nullptr;
+  const bool stream = stream_env || MODE == kWrite;
+  void (*kern)(EdgeArgs) = edge_chunk_kernel<MODE, SIB>;
+  if constexpr (MODE != kWrite) {
+    if (!stream) kern = edge_lane_kernel<MODE, SIB>;
+  }
   // hash capacity: keys of one item <= 32 + 2 x max out-degree in practice
   const u32 md = c.G->max_deg ? c.G->max_deg : kFilterMax;
   u32 hs = 256;
   while (hs < 2 * (32 + 2 * std::min<u32>(md, kFilterMax)) && hs < kHashSlots) hs <<= 1;
   a.hstride = hs;
+  static const u32 long_min = std::getenv("GPM_CF_LONG") ? (u32)std::atoi(std::getenv("GPM_CF_LONG")) : kLongDefault;
+  a.long_min = long_min;
   const size_t smem = (size_t)(kThreads / 32) * hs * sizeof(u32);
-  static std::atomic<int> occ_by_hs[16];  // zero-initialised (static storage)
-  const int occ = cached_occupancy(occ_by_hs[31 - __builtin_clz(hs)], [&] {
+  static std::atomic<int> occ_by_hs[2][16];  // zero-initialised (static storage)
+  const int occ = cached_occupancy(occ_by_hs[stream][31 - __builtin_clz(hs)], [&] {
     GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kThreads / 32 * kHashSlots * 4)));
     int o = 0;
     GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, smem));

@@ -47,14 +47,18 @@ def test_clique_k6_to_9_vs_oracle(P, oracle, k):
 
 
 def test_clique_k6_to_9_rmat_vs_oracle(P, oracle):
-    hg = P.generate_rmat(13, 16, 0.57, 0.19, 0.19, seed=5)
+    # RMAT-12 ef8: 6.1e6 .. 3.0e7 k-cliques; also under a small memory budget
+    # (planner chunks through every materialised level)
+    hg = P.generate_rmat(12, 8, 0.57, 0.19, 0.19, seed=5)
     c = oracle.Csr(hg.off, hg.col)
     g = P.Graph(hg)
     for k in (6, 7, 8, 9):
-        r = P.mine(g, "cf", k)
         o = oracle.mine(c, "cf", k)
-        assert r.total == o["total"], k
-        assert r.stats["n_explored"] == o["n_explored"], k
+        for kw in ({}, {"mem_budget": 64 << 20}):
+            r = P.mine(g, "cf", k, **kw)
+            assert r.total == o["total"], (k, kw)
+            assert r.stats["n_explored"] == o["n_explored"], (k, kw)
+            assert r.stats["level_sizes"][:len(o["level_sizes"])] == o["level_sizes"], (k, kw)
 
 
 @pytest.mark.parametrize("scale,ef,abc", [(9, 6, (0.57, 0.19, 0.19)), (10, 4, (0.45, 0.15, 0.15))])
