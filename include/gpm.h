@@ -86,7 +86,15 @@ typedef struct gpm_config {
    * ranks by the exchange when world > 1; each rank lists its own roots). */
   gpm_list_fn list_fn;      /* NULL = count only                                  */
   void* list_ctx;
+  /* FSM support measure: GPM_MNI_CANONICAL (default) maps an
+   * embedding's vertex i to domain perm[i] of the canonical pattern only;
+   * GPM_MNI_AUTOMORPHISM also applies every automorphism of the pattern
+   * ("true MNI", open question :318), i.e. each position's domain
+   * is the union over its automorphism orbit. */
+  int mni_mode;
 } gpm_config;
+
+enum { GPM_MNI_CANONICAL = 0, GPM_MNI_AUTOMORPHISM = 1 };
 
 void gpm_config_default(gpm_config* cfg);
 

@@ -593,6 +593,8 @@ struct ReduceState {
   }
 };
 
+static bool g_mni_full = false;  // full-automorphism MNI (oracle_mine_json mni_mode)
+
 // Builds pids from merged quick counts; allocates domain bitsets for
 // count-frequent patterns (count >= sigma is necessary for MNI >= sigma).
 static void reduce_canon(ReduceState& RS, u32 n, u64 sigma) {
@@ -616,7 +618,9 @@ static void reduce_canon(ReduceState& RS, u32 n, u64 sigma) {
   RS.words = (n + 63) / 64;
   RS.slot.assign(RS.pats.size(), -1);
   for (size_t p = 0; p < RS.pats.size(); ++p) {
-    if (RS.pcount[p] >= sigma) {
+    // MNI <= count (one vertex per domain per embedding); the full-automorphism
+    // MNI unions an orbit's domains, so only MNI <= nv * count holds there
+    if (RS.pcount[p] * (g_mni_full ? (u64)RS.pats[p].nv : 1) >= sigma) {
       RS.slot[p] = (int)RS.bits.size();
       auto* b = new std::vector<std::atomic<u64>>(RS.words * RS.pats[p].nv);
       for (auto& x : *b) x.store(0, std::memory_order_relaxed);
@@ -641,17 +645,48 @@ static void reduce_domain(ReduceState& RS, const Graph& g, const EEmb& E) {
   }
 }
 
-// mni
+// Automorphism orbits of a canonical pattern ("true MNI would
+// union over all isomorphic mappings including pattern automorphisms"):
+// brute force over every permutation; orbit id = smallest member.
+static std::vector<int> automorphism_orbits(const Pat& P) {
+  std::vector<int> rep(P.nv), p(P.nv);
+  std::iota(rep.begin(), rep.end(), 0);
+  std::iota(p.begin(), p.end(), 0);
+  do {
+    if (permute(P, p) == P)
+      for (int j = 0; j < P.nv; ++j) {
+        int a = rep[j], b = rep[p[j]];
+        if (a == b) continue;
+        int lo = std::min(a, b), hi = std::max(a, b);
+        for (int& x : rep)
+          if (x == hi) x = lo;
+      }
+  } while (std::next_permutation(p.begin(), p.end()));
+  return rep;
+}
+
+// mni; full-automorphism variant: min over automorphism
+// orbits of the union of the orbit's canonical domains
 static void reduce_mni(ReduceState& RS) {
   RS.mni.assign(RS.pats.size(), 0);
   for (size_t p = 0; p < RS.pats.size(); ++p) {
     int sl = RS.slot[p];
     if (sl < 0) continue;
     auto& b = *RS.bits[sl];
+    const int nv = RS.pats[p].nv;
+    std::vector<int> rep(nv);
+    if (g_mni_full) rep = automorphism_orbits(RS.pats[p]);
+    else std::iota(rep.begin(), rep.end(), 0);
     u64 mn = ~u64(0);
-    for (int pos = 0; pos < RS.pats[p].nv; ++pos) {
+    for (int pos = 0; pos < nv; ++pos) {
+      if (rep[pos] != pos) continue;
       u64 c = 0;
-      for (size_t w = 0; w < RS.words; ++w) c += __builtin_popcountll(b[pos * RS.words + w].load(std::memory_order_relaxed));
+      for (size_t w = 0; w < RS.words; ++w) {
+        u64 x = 0;
+        for (int o = 0; o < nv; ++o)
+          if (rep[o] == pos) x |= b[o * RS.words + w].load(std::memory_order_relaxed);
+        c += __builtin_popcountll(x);
+      }
       mn = std::min(mn, c);
     }
     RS.mni[p] = mn;
@@ -890,8 +925,9 @@ void oracle_free(char* p) { std::free(p); }
 char* oracle_mine_json(const std::uint64_t* off, const std::uint32_t* col, const std::uint32_t* labels,
                        std::uint32_t n, std::uint64_t m, int oriented, int app, int k,
                        std::uint64_t min_support, int threads, std::uint64_t chunk_size,
-                       std::uint64_t root_lo, std::uint64_t root_hi, int no_orient) {
+                       std::uint64_t root_lo, std::uint64_t root_hi, int no_orient, int mni_mode) {
   try {
+    orc::g_mni_full = mni_mode == 1;
     if (threads > 0) omp_set_num_threads(threads);
     orc::Graph g = make_graph(off, col, labels, n, m, oriented);
     std::string out = "{";

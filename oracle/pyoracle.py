@@ -37,7 +37,7 @@ def lib():
         L.oracle_mine_json.restype = C.c_void_p
         L.oracle_mine_json.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64, C.c_int,
                                        C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64,
-                                       C.c_uint64, C.c_int]
+                                       C.c_uint64, C.c_int, C.c_int]
         L.oracle_free.argtypes = [C.c_void_p]
         L.oracle_canonicalize.restype = C.c_void_p
         L.oracle_canonicalize.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p]
@@ -127,13 +127,14 @@ def csr_from_edges(edges, n: Optional[int] = None, labels=None) -> Csr:
 
 
 def mine(g: Csr, app: str, k: int = 3, min_support: int = 0, threads: int = 0, chunk_size: int = 1024,
-         root_lo: int = 0, root_hi: int = 2**64 - 1, no_orient: bool = False) -> dict:
+         root_lo: int = 0, root_hi: int = 2**64 - 1, no_orient: bool = False, mni: str = "canonical") -> dict:
     L = lib()
     off = np.ascontiguousarray(g.off, dtype=np.uint64)
     col = np.ascontiguousarray(g.col, dtype=np.uint32)
     lab = None if g.labels is None else np.ascontiguousarray(g.labels, dtype=np.uint32)
     p = L.oracle_mine_json(_p(off), _p(col), _p(lab), g.n, g.m, int(g.oriented), APPS[app], k, min_support,
-                           threads, chunk_size, root_lo, root_hi, int(no_orient))
+                           threads, chunk_size, root_lo, root_hi, int(no_orient),
+                           {"canonical": 0, "automorphism": 1}[mni])
     s = C.string_at(p).decode()
     L.oracle_free(p)
     d = json.loads(s)

@@ -38,7 +38,7 @@ class Config(C.Structure):
                 ("no_orient", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("root_lo", C.c_uint64),
                 ("root_hi", C.c_uint64), ("stream", C.c_void_p), ("exchange", EXCHANGE_FN),
                 ("exchange_ctx", C.c_void_p), ("steal_ctrs", C.c_void_p), ("steal_chunk", C.c_uint64),
-                ("list_fn", LIST_FN), ("list_ctx", C.c_void_p)]
+                ("list_fn", LIST_FN), ("list_ctx", C.c_void_p), ("mni_mode", C.c_int)]
 
 
 # gpm_stats.paths bits (include/gpm.h)

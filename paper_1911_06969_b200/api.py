@@ -273,7 +273,7 @@ def pattern_tsv(patterns) -> str:
 def make_config(app: str, k: int = 3, min_support: int = 0, *, mem_budget: int = 0, no_orient: bool = False,
                 rank: int = 0, world: int = 1, root_lo: int = 0, root_hi: int = 0, stream: int = 0,
                 exchange=None, exchange_ctx: int = 0, steal_ctrs: int = 0, steal_chunk: int = 0,
-                list_fn=None) -> _L.Config:
+                list_fn=None, mni: str = "canonical") -> _L.Config:
     cfg = _L.Config()
     lib().gpm_config_default(C.byref(cfg))
     cfg.app = APP_IDS[app]
@@ -291,6 +291,7 @@ def make_config(app: str, k: int = 3, min_support: int = 0, *, mem_budget: int =
     cfg.steal_chunk = steal_chunk
     if list_fn is not None:
         cfg.list_fn = list_fn
+    cfg.mni_mode = {"canonical": 0, "automorphism": 1}[mni]
     return cfg
 
 

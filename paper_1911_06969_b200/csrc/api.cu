@@ -129,18 +129,20 @@ int gpm_canonicalize_batch(int device, int nv, uint64_t count, const uint32_t* l
     const int np = pat::npairs(nv);
     for (u64 i = 0; i < count; ++i)
       if (np < 32 && (masks[i] >> np)) throw Error(GPM_EINVAL, "mask has bits beyond the nv*(nv-1)/2 pairs");
-    // dense, order-preserving label ranks (the packed code compares ranks)
-    std::vector<u32> vals;
-    if (labels) vals.assign(labels, labels + count * nv);
-    std::sort(vals.begin(), vals.end());
-    vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
-    int LB = 0;
-    while ((u64(1) << LB) < vals.size()) ++LB;
-    if (pat::code_bits(nv, LB) > pat::kCodeBits) throw Error(GPM_EINVAL, "canonicalize: too many distinct labels for a packed code");
+    // dense, order-preserving label ranks PER PATTERN (the canonical form only
+    // depends on the order of a pattern's own labels): <= nv distinct values,
+    // so 3 label bits always fit the packed code (8 * 3 + 28 <= 60)
+    const int LB = 3;
     std::vector<u32> rk(count * nv, 0);
+    std::vector<u32> vals(count * nv, 0);  // per pattern: rank -> value
     if (labels)
-      for (u64 i = 0; i < count * nv; ++i)
-        rk[i] = (u32)(std::lower_bound(vals.begin(), vals.end(), labels[i]) - vals.begin());
+      for (u64 i = 0; i < count; ++i) {
+        u32* v = vals.data() + i * nv;
+        std::copy(labels + i * nv, labels + (i + 1) * nv, v);
+        std::sort(v, v + nv);
+        const int nu = (int)(std::unique(v, v + nv) - v);
+        for (int j = 0; j < nv; ++j) rk[i * nv + j] = (u32)(std::lower_bound(v, v + nu, labels[i * nv + j]) - v);
+      }
     if (count == 0) return;
     GPM_CUDA(cudaSetDevice(device));
     cudaStream_t st;
@@ -164,7 +166,7 @@ int gpm_canonicalize_batch(int device, int nv, uint64_t count, const uint32_t* l
       pat::decode(codes[i], LB, &cn, cl, &cm);
       canon_masks[i] = cm;
       for (int j = 0; j < nv; ++j) {
-        if (canon_labels) canon_labels[i * nv + j] = labels ? vals[cl[j]] : 0u;
+        if (canon_labels) canon_labels[i * nv + j] = labels ? vals[i * nv + cl[j]] : 0u;
         if (perms) perms[i * nv + j] = (u8)((pk[i] >> (3 * j)) & 7u);
       }
     }
@@ -256,6 +258,8 @@ namespace gpm {
 // gpm_mine's validation of the builtin apps' config (SPEC.md:375 conflicts).
 static void check_builtin_config(const gpm_config* cfg) {
   if (cfg->app < GPM_APP_TC || cfg->app > GPM_APP_FSM) throw Error(GPM_EINVAL, "unknown app");
+  if (cfg->mni_mode != GPM_MNI_CANONICAL && cfg->mni_mode != GPM_MNI_AUTOMORPHISM)
+    throw Error(GPM_EINVAL, "unknown mni_mode");
   // config conflicts ("chunking + filter -> error"): the FSM
   // filter needs every root's embeddings before the next extend, so a
   // root slice is only legal as one rank's share of an exchanged job;

@@ -1262,21 +1262,43 @@ __global__ void slot_pid_kernel(const u64* __restrict__ canon, const u32* __rest
 }
 
 // popcount per (pattern, canonical position); MNI = min over positions
+// MNI per bitmap pattern: min over positions of the domain size
+// (canonical-mapping MNI).  full != 0: full-automorphism
+// MNI -- an embedding's mappings include every automorphism
+// of the pattern, so a position's domain is the union of the canonical
+// domains over its automorphism orbit; min over orbits.
 __global__ void mni_kernel(const u32* __restrict__ bitmaps, u64 words, int kpos, const u64* __restrict__ gkeys,
-                           const u32* __restrict__ bs_to_pid, u32 round_lo, u32 round_n,
+                           const u32* __restrict__ bs_to_pid, u32 round_lo, u32 round_n, int LB, int full,
                            unsigned long long* __restrict__ mni) {
   const u32 r = blockIdx.x;  // bitmap pattern within round
   if (r >= round_n) return;
   const u32 pid = bs_to_pid[round_lo + r];
-  const int nv = pat::code_nv(gkeys[pid]);
+  const u64 key = gkeys[pid];
+  const int nv = pat::code_nv(key);
   __shared__ unsigned long long part[32];
   __shared__ unsigned long long best;
-  if (threadIdx.x == 0) best = ~0ull;
+  __shared__ u8 rep[8];
+  if (threadIdx.x == 0) {
+    best = ~0ull;
+    for (int i = 0; i < 8; ++i) rep[i] = (u8)i;
+    if (full) {
+      int n2;
+      u32 lab[8], mask;
+      pat::decode(key, LB, &n2, lab, &mask);
+      pat::orbits(nv, lab, mask, rep);
+    }
+  }
   __syncthreads();
   for (int pos = 0; pos < nv; ++pos) {
+    if (rep[pos] != pos) continue;  // counted with its orbit's representative
     const u32* bm = bitmaps + ((u64)r * kpos + pos) * words;
     unsigned long long c = 0;
-    for (u64 w = threadIdx.x; w < words; w += blockDim.x) c += __popc(bm[w]);
+    for (u64 w = threadIdx.x; w < words; w += blockDim.x) {
+      u32 v = bm[w];
+      for (int o = pos + 1; o < nv; ++o)
+        if (rep[o] == pos) v |= bitmaps[((u64)r * kpos + o) * words + w];
+      c += __popc(v);
+    }
     c = __reduce_add_sync(0xffffffffu, (unsigned)c);
     if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
     __syncthreads();
@@ -1513,8 +1535,10 @@ struct Fsm {
     ++tl.launches;
     // count pre-filter -> bitmap slots (MNI <= count)
     std::vector<u32> bslot(std::max<u64>(1, R.P), ~0u), bs_to_pid;
+    // MNI <= count; the full-automorphism MNI unions an orbit's domains: <= nv * count
+    const bool full = cfg.mni_mode == GPM_MNI_AUTOMORPHISM;
     for (u64 p = 0; p < R.P; ++p)
-      if (R.gcount_h[p] >= sigma) {
+      if (R.gcount_h[p] * (full ? (u64)pat::code_nv(R.gkeys_h[p]) : 1) >= sigma) {
         bslot[p] = (u32)bs_to_pid.size();
         bs_to_pid.push_back((u32)p);
       }
@@ -1550,7 +1574,7 @@ struct Fsm {
         exchange_device(cfg, bm.get(), n * kpos * words, 4, 1, s);
         trace("domain round", (double)lo, (double)n);
         mni_kernel<<<(unsigned)n, 256, 0, s>>>(bm.get(), words, kpos, R.gkeys.get(), R.bs_to_pid.get(), (u32)lo,
-                                               (u32)n, mni.get());
+                                               (u32)n, LB, cfg.mni_mode == GPM_MNI_AUTOMORPHISM, mni.get());
         GPM_CUDA(cudaGetLastError());
         ++tl.launches;
       }
@@ -1561,17 +1585,23 @@ struct Fsm {
     sync();
     trace("mni kernel + d2h", (double)R.P);
     std::vector<u8> freq(std::max<u64>(1, R.P), 0);
-    for (u64 p = 0; p < R.P; ++p) freq[p] = (R.gcount_h[p] >= sigma && R.mni_h[p] >= sigma) ? 1 : 0;
+    for (u64 p = 0; p < R.P; ++p) freq[p] = frequent_pat(R, p) ? 1 : 0;
     R.frequent.alloc(freq.size(), s);
     GPM_CUDA(cudaMemcpyAsync(R.frequent.get(), freq.data(), freq.size(), cudaMemcpyHostToDevice, s));
     sync();
     trace("frequent flags h2d", (double)R.P);
   }
 
+  // to_prune = MNI < sigma (Listing 5); mni_h is 0 for patterns without a bitmap
+  bool frequent_pat(const Level& R, u64 p) const {
+    if (cfg.mni_mode == GPM_MNI_AUTOMORPHISM) return R.mni_h[p] >= sigma && R.gcount_h[p] > 0;
+    return R.gcount_h[p] >= sigma && R.mni_h[p] >= sigma;
+  }
+
   void record(Level& R, int level) {
     std::vector<u64> sel;
     for (u64 p = 0; p < R.P; ++p)
-      if (R.gcount_h[p] >= sigma && R.mni_h[p] >= sigma) sel.push_back(p);
+      if (frequent_pat(R, p)) sel.push_back(p);
     // text is formatted on access (gpm_result_pattern): ~10^6 patterns per call
     res.kpatterns.reserve(res.kpatterns.size() + sel.size());
     for (u64 p : sel) res.kpatterns.push_back({R.gkeys_h[p], R.mni_h[p], level});

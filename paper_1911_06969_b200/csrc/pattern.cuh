@@ -175,6 +175,63 @@ __host__ __device__ inline uint64_t canonicalize(int nv, const uint32_t* lab, ui
   return best;
 }
 
+// Automorphism orbits of a pattern (full-automorphism MNI):
+// rep[i] = smallest position j such that some automorphism (a label- and
+// edge-preserving permutation) maps i to j.  Label-preserving permutations are
+// enumerated depth-first as in canonicalize (each position stays inside its
+// label block); those that map the edge mask onto itself are automorphisms.
+__host__ __device__ inline void orbits(int nv, const uint32_t* lab, uint32_t mask, uint8_t* rep) {
+  for (int i = 0; i < nv; ++i) rep[i] = (uint8_t)i;
+  uint8_t ea[28], eb[28];
+  int ne = 0;
+  for (int a = 0; a < nv; ++a)
+    for (int b = a + 1; b < nv; ++b)
+      if (mask >> pair_index(a, b, nv) & 1u) {
+        ea[ne] = (uint8_t)a;
+        eb[ne] = (uint8_t)b;
+        ++ne;
+      }
+  uint8_t p[8], nxt[8];
+  uint32_t used = 0;
+  int i = 0;
+  nxt[0] = 0;
+  for (;;) {
+    int sv = nxt[i];
+    while (sv < nv && ((used >> sv & 1u) || lab[sv] != lab[i])) ++sv;
+    if (sv >= nv) {
+      if (i == 0) break;
+      --i;
+      used &= ~(1u << p[i]);
+      nxt[i] = (uint8_t)(p[i] + 1);
+      continue;
+    }
+    p[i] = (uint8_t)sv;
+    used |= 1u << sv;
+    if (i + 1 < nv) {
+      ++i;
+      nxt[i] = 0;
+      continue;
+    }
+    uint32_t pm = 0;
+    for (int e = 0; e < ne; ++e) {
+      int x = p[ea[e]], y = p[eb[e]];
+      if (x > y) { const int t = x; x = y; y = t; }
+      pm |= 1u << pair_index(x, y, nv);
+    }
+    if (pm == mask) {  // automorphism: merge the orbits of j and p[j]
+      for (int j = 0; j < nv; ++j) {
+        const uint8_t a = rep[j], b = rep[p[j]];
+        const uint8_t lo = a < b ? a : b, hi = a < b ? b : a;
+        if (lo != hi)
+          for (int t = 0; t < nv; ++t)
+            if (rep[t] == hi) rep[t] = lo;
+      }
+    }
+    used &= ~(1u << sv);
+    nxt[i] = (uint8_t)(sv + 1);
+  }
+}
+
 __host__ __device__ __forceinline__ int code_nv(uint64_t code) { return (int)(code >> 60); }
 // bits a code of nv positions with LB-bit labels needs below the nv field
 __host__ __device__ __forceinline__ int code_bits(int nv, int LB) { return nv * LB + npairs(nv); }

@@ -62,7 +62,6 @@ struct EdgeArgs {
   unsigned long long* total;  // FUSED
   unsigned long long* cand;   // candidates streamed (stats)
   u32 hstride;                // per-warp hash slots (power of two)
-  u32 long_min;               // lane kernel: lists this long are streamed by the whole warp
   const u32* wv;              // SIB: new vertex per entry (level vid array)
 };
 
@@ -343,18 +342,18 @@ __global__ void __launch_bounds__(kThreads, 5) edge_chunk_kernel(EdgeArgs a) {
 
 
 // Hybrid variant of edge_chunk_kernel for the inspection (COUNT) and fused
-// (FUSED) passes: same items, staging and results.  A parent whose candidate
-// list N+(v1) has at least long_min (default 32) entries is streamed by the
-// whole warp, one parent at a time (no lane -> parent mapping, the probe's
-// root slot is warp-uniform); the shorter lists are packed 32 candidates per
-// step with the OR-reduction mapping of edge_chunk_kernel.  Accepted
+// (FUSED) passes: same items, staging and results.  The whole 32-candidate
+// chunks of a candidate list N+(v1) are streamed by the whole warp, one parent
+// at a time (no lane -> parent mapping, the probe's root slot is
+// warp-uniform); the remaining w mod 32 candidates of every list are packed
+// 32 per step with the OR-reduction mapping of edge_chunk_kernel, so no step
+// is wasted on a partial chunk.  Accepted
 // children are rare (PAT: 1 in 400): COUNT records them as (parent lane,
 // index within the parent) -- the index from a per-parent shared counter
 // plus the rank among same-parent lanes of the step, so it follows u order
 // -- and places them at prefix(parent) + index, i.e. in the sequential
 // (parent, u) order the execution pass copies.  The execution pass (WRITE)
 // stays on edge_chunk_kernel.
-constexpr u32 kLongDefault = 32;
 
 template <int MODE, bool SIB>
 __global__ void __launch_bounds__(kThreads, 5) edge_lane_kernel(EdgeArgs a) {
@@ -503,11 +502,11 @@ __global__ void __launch_bounds__(kThreads, 5) edge_lane_kernel(EdgeArgs a) {
       continue;
     }
     u32 c = 0;  // accepted children of the item (warp-uniform)
-    // ---- long parents, warp-cooperative
-    for (u32 lm = __ballot_sync(0xffffffffu, w >= a.long_min); lm; lm &= lm - 1) {
+    // ---- heads of the long lists (whole 32-candidate chunks), warp-cooperative
+    for (u32 lm = __ballot_sync(0xffffffffu, w >= 32); lm; lm &= lm - 1) {
       const int p = __ffs(lm) - 1;
       const u64 pcb = __shfl_sync(0xffffffffu, cb, p);
-      const u32 pw = __shfl_sync(0xffffffffu, w, p);
+      const u32 pw = __shfl_sync(0xffffffffu, w, p) & ~31u;
       const u32 psl = __shfl_sync(0xffffffffu, slot, p);
       const u32* const pl = g.col + pcb;
       u32 pc = 0;
@@ -523,11 +522,12 @@ __global__ void __launch_bounds__(kThreads, 5) edge_lane_kernel(EdgeArgs a) {
       if (MODE == kCount && lane == 0) spc[p] = pc;
       c += pc;
     }
-    // ---- short parents, packed 32 candidates per step
-    const bool sp = w > 0 && w < a.long_min;
+    // ---- the tails (w mod 32 candidates of every list), packed 32 per step
+    const u32 tw = w & 31u, head = w & ~31u;
+    const bool sp = tw > 0;
     const u32 smask = __ballot_sync(0xffffffffu, sp);
     if (smask) {
-      u32 incl = sp ? w : 0u;
+      u32 incl = tw;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
@@ -536,8 +536,8 @@ __global__ void __launch_bounds__(kThreads, 5) edge_lane_kernel(EdgeArgs a) {
       const u32 stot = __shfl_sync(0xffffffffu, incl, 31);
       const u32 rank = __popc(smask & lanemask_lt());
       if (sp) {
-        scp[rank] = reinterpret_cast<u64>(g.col) + 4 * (cb - (u64)(incl - w));
-        sex[rank] = incl - w;
+        scp[rank] = reinterpret_cast<u64>(g.col) + 4 * (cb + head - (u64)(incl - tw));
+        sex[rank] = incl - tw;
         ssl[rank] = ((u32)lane << 8) | slot;
       }
       __syncwarp();
@@ -646,8 +646,6 @@ void launch_edge(Ctx& c, EdgeArgs& a, const std::string& what, double bytes) {
   u32 hs = 256;
   while (hs < 2 * (32 + 2 * std::min<u32>(md, kFilterMax)) && hs < kHashSlots) hs <<= 1;
   a.hstride = hs;
-  static const u32 long_min = std::getenv("GPM_CF_LONG") ? (u32)std::atoi(std::getenv("GPM_CF_LONG")) : kLongDefault;
-  a.long_min = long_min;
   const size_t smem = (size_t)(kThreads / 32) * hs * sizeof(u32);
   static std::atomic<int> occ_by_hs[2][16];  // zero-initialised (static storage)
   const int occ = cached_occupancy(occ_by_hs[stream][31 - __builtin_clz(hs)], [&] {

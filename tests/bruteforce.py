@@ -40,6 +40,21 @@ def canon(nv, labels, edges):
     return best, list(bperm)
 
 
+def canon_all(nv, labels, edges):
+    """Every permutation achieving the canonical form (all isomorphic mappings
+    of the embedding onto the canonical pattern, automorphisms included)."""
+    best, _ = canon(nv, labels, edges)
+    out = []
+    for perm in itertools.permutations(range(nv)):
+        lab = [0] * nv
+        for i in range(nv):
+            lab[perm[i]] = labels[i]
+        es = sorted((min(perm[a], perm[b]), max(perm[a], perm[b])) for a, b in edges)
+        if (lab, es) == best:
+            out.append(list(perm))
+    return best, out
+
+
 def text(nv, labels, edges):
     return "k=%d;L=%s;E=%s" % (nv, ",".join(str(x) for x in labels), "".join("(%d,%d)" % e for e in edges))
 
@@ -160,8 +175,9 @@ def connected_edge_subsets(adj, size):
         yield canonical_edge_order(S)
 
 
-def fsm(adj, labels, k, sigma):
-    """Level-wise FSM with canonical-mapping MNI and Alg. 1 filter semantics.
+def fsm(adj, labels, k, sigma, full=False):
+    """Level-wise FSM with canonical-mapping MNI (full=True: true MNI over all
+    isomorphic mappings) and Alg. 1 filter semantics.
     Returns ([(level, text, mni)...], level_sizes)."""
     result = []
     level_sizes = []
@@ -177,11 +193,16 @@ def fsm(adj, labels, k, sigma):
         pat_of = {}
         for seq in embs:
             verts, lab, edges = edge_emb_quick(seq, labels)
-            (cl, ce), perm = canon(len(verts), lab, edges)
+            if full:
+                (cl, ce), perms = canon_all(len(verts), lab, edges)
+            else:
+                (cl, ce), perm = canon(len(verts), lab, edges)
+                perms = [perm]
             t = text(len(verts), cl, ce)
             d = dom.setdefault(t, [set() for _ in range(len(verts))])
-            for i, v in enumerate(verts):
-                d[perm[i]].add(v)
+            for perm in perms:
+                for i, v in enumerate(verts):
+                    d[perm[i]].add(v)
             pat_of[frozenset(seq)] = t
         mni = {t: min(len(s) for s in d) for t, d in dom.items()}
         for t, m in mni.items():

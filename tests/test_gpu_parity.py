@@ -239,3 +239,34 @@ def test_fsm_errors_and_sparse_labels(P, oracle):
     r = P.mine(P.Graph(hg), "fsm", 3, 1)
     o = oracle.mine(oracle.Csr(hg.off, hg.col, hg.labels), "fsm", 3, 1)
     assert [tuple(p) for p in r.patterns] == [tuple(p) for p in o["patterns"]]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fsm_full_automorphism_mni_vs_oracle(P, oracle, seed):
+    # full-automorphism MNI: GPU orbit-union domains vs the oracle
+    rng = np.random.default_rng(40 + seed)
+    n = int(rng.integers(40, 120))
+    lab = rng.integers(0, [1, 2, 3, 2][seed], n)
+    hg = host(P, oracle, BF.gnp(n, 0.08, 40 + seed), n, lab)
+    g = P.Graph(hg)
+    oc = oracle.Csr(hg.off, hg.col, hg.labels)
+    for k in (2, 3, 4):
+        for sigma in (2, 5, 9):
+            r = P.mine(g, "fsm", k, sigma, mni="automorphism")
+            o = oracle.mine(oc, "fsm", k, sigma, mni="automorphism")
+            assert [tuple(p) for p in r.patterns] == [tuple(p) for p in o["patterns"]], (k, sigma)
+            same(r, o, ("level_sizes", "candidates", "survivors", "n_explored"))
+
+
+def test_fsm_full_automorphism_rmat(P, oracle):
+    hg = P.generate_rmat(11, 6, 0.45, 0.15, 0.15, seed=2, n_labels=3, label_seed=5)
+    g = P.Graph(hg)
+    oc = oracle.Csr(hg.off, hg.col, hg.labels)
+    for k, sigma in ((3, 40), (4, 80)):
+        r = P.mine(g, "fsm", k, sigma, mni="automorphism")
+        o = oracle.mine(oc, "fsm", k, sigma, mni="automorphism")
+        assert [tuple(p) for p in r.patterns] == [tuple(p) for p in o["patterns"]]
+        same(r, o, ("level_sizes", "candidates", "survivors", "n_explored"))
+        # automorphisms only add mappings: every canonical-MNI frequent pattern stays frequent
+        canon = {t for _, t, _ in P.mine(g, "fsm", k, sigma).patterns}
+        assert canon <= {t for _, t, _ in r.patterns}

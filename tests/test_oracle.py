@@ -58,6 +58,33 @@ def test_fsm_star_canonical_mapping(oracle):
     assert oracle.mine(g, "fsm", 2, 1)["patterns"] == [[1, "k=2;L=0,0;E=(0,1)", 1]]
 
 
+def test_fsm_star_full_automorphism(oracle):
+    # the same star under full-automorphism MNI: both
+    # positions of the edge pattern are one orbit -> domain = all 5 vertices
+    g = csr(oracle, [(0, i) for i in range(1, 5)], labels=np.zeros(5))
+    assert oracle.mine(g, "fsm", 2, 1, mni="automorphism")["patterns"] == [[1, "k=2;L=0,0;E=(0,1)", 5]]
+    # Fig. 2-style chain with distinct end labels: no non-trivial automorphism, both measures agree
+    g = csr(oracle, [(0, 1), (1, 2)], labels=np.array([1, 0, 2]))
+    assert oracle.mine(g, "fsm", 3, 1)["patterns"] == oracle.mine(g, "fsm", 3, 1, mni="automorphism")["patterns"]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fsm_full_automorphism_bruteforce(oracle, seed):
+    # the oracle's orbit-union MNI == brute force over ALL isomorphic mappings
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(10, 24))
+    E = BF.gnp(n, 0.18, 900 + seed)
+    lab = rng.integers(0, 2, n)
+    g = csr(oracle, E, n, lab)
+    adj = BF.adjacency(g.off, g.col)
+    for k in (2, 3, 4):
+        for sigma in (1, 3, 5):
+            r = oracle.mine(g, "fsm", k, sigma, mni="automorphism")
+            want, sizes = BF.fsm(adj, lab, k, sigma, full=True)
+            assert [tuple(x) for x in r["patterns"]] == want, (k, sigma)
+            assert r["level_sizes"] == sizes
+
+
 def test_canonicalize_known(oracle):
     # wedge with centre at position 0 and at position 1 -> identical form
     t0, _ = oracle.canonicalize(3, [0, 0, 0], [(0, 1), (0, 2)])
