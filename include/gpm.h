@@ -217,7 +217,8 @@ enum {
   GPM_PATH_FSM_ROUNDS = 1u << 9,       /* FSM domain bitmaps in several rounds     */
   GPM_PATH_FSM_FUSED_LAST = 1u << 10,  /* FSM last level: domain pass fused        */
   GPM_PATH_FSM_GROUPED = 1u << 11,     /* FSM passes over parents grouped by code  */
-  GPM_PATH_FSM_FAN = 1u << 12          /* FSM last level: fan-out pass (dense slots) */
+  GPM_PATH_FSM_FAN = 1u << 12,         /* FSM last level: fan-out pass (dense slots) */
+  GPM_PATH_FSM_SPARSE = 1u << 13       /* FSM sparse (sorted-key) domains            */
 };
 int gpm_result_stats(const gpm_result* r, gpm_stats* out);
 

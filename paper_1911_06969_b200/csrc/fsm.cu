@@ -44,7 +44,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr u64 kBatch = 2048;
 constexpr int kMaxEdges = 5;  // k <= 6
-enum { kQC = 0, kDomain = 1, kSCount = 2, kSWrite = 3, kQCD = 4 };
+enum { kQC = 0, kDomain = 1, kSCount = 2, kSWrite = 3, kQCD = 4, kSparse = 5 };
 
 struct ELevels {
   const u32* idx[kMaxEdges + 1];
@@ -257,12 +257,21 @@ struct FsmArgs {
   u32* bitmaps;
   u64 words;
   const u32* lrank;       // vertex -> rank within its label class (label-local bitmap index)
+  const u32* labrank;     // vertex -> label << 27 | rank (fan pass; labels < 32, ranks < 2^27)
   u32* qbm;               // fused last level: domain bitmaps per quick-code id (quick positions)
   u64 qcap;               // ids with a bitmap
   int* qover;             // set when an id >= qcap appeared (host falls back to a domain pass)
   int kpos;
   u32 round_lo, round_hi;
   const u8* frequent;     // pattern -> MNI >= sigma
+  // sparse domains: pattern -> sparse slot or ~0, the slot's
+  // packed orbit representatives (3 bits per canonical position), and the
+  // (slot, position, label-local rank) key buffer
+  const u32* sslot;
+  const u32* srep;
+  unsigned long long* skeys;
+  unsigned long long* stop;
+  u64 scap;
   u64* cnt;
   const u64* boffs;
   u64 out_base;
@@ -310,6 +319,36 @@ __device__ __forceinline__ void domain_or(const FsmArgs& a, u64 info, const u32*
   if (bs < a.round_lo || bs >= a.round_hi) return;
   u32* base = a.bitmaps + (u64)(bs - a.round_lo) * a.kpos * a.words;
   bitmap_or<NV>(base, a.words, a.lrank, (u32)info, true, cv, cnv, first);
+}
+
+// Sparse domains: a child of a sparse pattern emits one key per vertex,
+// (slot << 35 | orbit-representative canonical position << 32 | label-local
+// rank); the warp reserves its keys with one atomic.  Sorting + unique then
+// gives the domains exactly (their sizes are the MNI inputs).
+__device__ __forceinline__ void sparse_emit(const FsmArgs& a, bool ok, u64 info, const u32* cv, int cnv) {
+  const int lane = threadIdx.x & 31;
+  u32 sl = ~0u;
+  if (ok) sl = a.sslot[(u32)(info >> 32)];
+  const u32 nk = sl != ~0u ? (u32)cnv : 0u;
+  u32 incl = nk;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const u32 tot = __shfl_sync(0xffffffffu, incl, 31);
+  if (!tot) return;
+  unsigned long long base = 0;
+  if (lane == 31) base = atomicAdd(a.stop, (unsigned long long)tot);
+  base = __shfl_sync(0xffffffffu, base, 31) + (incl - nk);
+  if (!nk) return;
+  const u32 perm = (u32)info, rep = a.srep[sl];
+  for (int i = 0; i < cnv; ++i) {
+    const u32 cp = (perm >> (3 * i)) & 7u;
+    const u32 rp = (rep >> (3 * cp)) & 7u;
+    if (base + i < a.scap)
+      a.skeys[base + i] = ((unsigned long long)sl << 35) | ((unsigned long long)rp << 32) | ldg(a.lrank + cv[i]);
+  }
 }
 
 // Work per parent: sum of deg over all positions (to_extend default true).
@@ -453,6 +492,9 @@ __global__ void __launch_bounds__(kThreads) eextend_kernel(FsmArgs a) {
             }
           }
         }
+      } else if (MODE == kSparse) {
+        const u64 info = ok ? hash_info(a.H, hash_find(a.H, code)) : 0ull;
+        sparse_emit(a, ok, info, cv, cnv);
       } else if (MODE == kDomain) {
         const u32 peers = __match_any_sync(0xffffffffu, ok ? code : ~0ull);
         const u32 sib = peers & __match_any_sync(0xffffffffu, myp);
@@ -907,7 +949,9 @@ __global__ void __launch_bounds__(kGT, 1) egroup_kernel(FsmArgs a, GroupArgs ga)
 // state the rest of the fused path (canonicalise, merge_qbm) consumes.
 // Lanes map to the candidates N(v_q) of one parent at a time (coalesced);
 // parent descriptors are built 32 at a time, one per lane, into shared memory.
-constexpr int kFT = 512;                 // threads per fan CTA
+constexpr int kFT = 256;                 // threads per fan CTA (two CTAs per SM)
+constexpr int kRankBits = 27;            // labrank[v] = label << 27 | rank within the label class
+constexpr u32 kRankMask = (1u << kRankBits) - 1;
 constexpr u32 kFanParents = 4096;        // parents per item (large groups split)
 
 struct FanItem {
@@ -939,7 +983,7 @@ struct FanDesc {  // per-warp parent descriptors, struct of arrays over 32 lanes
 };
 
 template <int LEV>
-__global__ void __launch_bounds__(kFT, 1) efan_kernel(FsmArgs a, FanArgs fa) {
+__global__ void __launch_bounds__(kFT, 2) efan_kernel(FsmArgs a, FanArgs fa) {
   constexpr int MV = LEV + 1;
   constexpr int NW = kFT / 32;
   extern __shared__ __align__(16) unsigned char fsm_fan_smem[];
@@ -951,13 +995,17 @@ __global__ void __launch_bounds__(kFT, 1) efan_kernel(FsmArgs a, FanArgs fa) {
   const u64 doff = (u64)nslot * rowlen + 2 * nslot;
   FanDesc<LEV>* descs = reinterpret_cast<FanDesc<LEV>*>(rows + doff + (doff & 1));  // 8-byte aligned
   __shared__ u64 s_item;
+  __shared__ u32 s_bnext;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   FanDesc<LEV>& D = descs[wid];
   unsigned long long acc = 0;
   for (u64 i = threadIdx.x; i < (u64)nslot * rowlen; i += kFT) rows[i] = 0u;
   for (;;) {
     for (u32 i = threadIdx.x; i < nslot; i += kFT) cnt[i] = 0u;
-    if (threadIdx.x == 0) s_item = atomicAdd(fa.ctr, 1ull);
+    if (threadIdx.x == 0) {
+      s_item = atomicAdd(fa.ctr, 1ull);
+      if (s_item < fa.nitems) s_bnext = fa.items[s_item].pa;
+    }
     __syncthreads();
     const u64 it = s_item;
     if (it >= fa.nitems) break;
@@ -971,8 +1019,12 @@ __global__ void __launch_bounds__(kFT, 1) efan_kernel(FsmArgs a, FanArgs fa) {
     const u32 lshift = (u32)pat::npairs(nv + 1);
     const u64 newbase = pat::make_code_packed(nv + 1, labp << a.LB,
                                               pat::widen_mask(pmask, nv) | (1u << pat::pair_index(q, nv, nv + 1)));
-    // ---- warps take 32-parent batches of the item
-    for (u32 b0 = item.pa + 32 * wid; b0 < item.pb; b0 += 32 * NW) {
+    // ---- warps grab 32-parent batches of the item
+    for (;;) {
+      u32 b0 = 0;
+      if (lane == 0) b0 = atomicAdd(&s_bnext, 32u);
+      b0 = __shfl_sync(0xffffffffu, b0, 0);
+      if (b0 >= item.pb) break;
       const u32 nb = min(32u, item.pb - b0);
       __syncwarp();
       if ((u32)lane < nb) {
@@ -996,7 +1048,7 @@ __global__ void __launch_bounds__(kFT, 1) efan_kernel(FsmArgs a, FanArgs fa) {
         for (int i = 0; i < MV; ++i) {
           const bool in = i < E.nv;
           D.v[i][lane] = in ? E.v[i] : 0xffffffffu;
-          D.lr[i][lane] = in ? ldg(a.lrank + E.v[i]) : 0u;
+          D.lr[i][lane] = in ? ldg(a.labrank + E.v[i]) & kRankMask : 0u;
           stp |= (u32)(in ? E.step[i] : 0) << (4 * i);
           if (i == q) x = E.v[i];
         }
@@ -1010,83 +1062,97 @@ __global__ void __launch_bounds__(kFT, 1) efan_kernel(FsmArgs a, FanArgs fa) {
         }
         const u64 cb = ldg(a.g.off + x);
         D.cb[lane] = cb;
-        D.deg[lane] = (u32)(ldg(a.g.off + x + 1) - cb);
+        D.deg[lane] = (u32)(ldg(a.g.off + x + 1) - cb);  // >= 1: x is an endpoint of a parent edge
         D.x[lane] = x;
         D.thrq[lane] = tq;
         D.stp[lane] = stp;
       }
       __syncwarp();
-      for (u32 j = 0; j < nb; ++j) {
-        const u32 x = D.x[j], deg = D.deg[j];
-        const u64 cb = D.cb[j], thrq = D.thrq[j];
-        u32 pv[MV];
+      // flattened (parent, 32-candidate chunk) stream of the batch, the next
+      // chunk's candidates in flight while the current one is evaluated
+      u32 cj = 0, cjb = 0;
+      u32 cw = (u32)lane < D.deg[0] ? ldg(a.g.col + D.cb[0] + lane) : 0u;
+      u32 lm = 0, cm = 0;  // labels of new-vertex children / closing positions of parent cj
+      while (cj < nb) {
+        const u32 cdeg = D.deg[cj];
+        u32 nj = cj, njb = cjb + 32;
+        if (njb >= cdeg) {
+          nj = cj + 1;
+          njb = 0;
+        }
+        u32 nw = 0;
+        if (nj < nb && njb + lane < D.deg[nj]) nw = ldg(a.g.col + D.cb[nj] + njb + lane);
+        const u32 x = D.x[cj];
+        const u64 thrq = D.thrq[cj];
+        bool ok = false;
+        if (cjb + lane < cdeg) {
+          const u32 w = cw;
+          const u32 lw = ldg(a.labrank + w);  // issued before the position / threshold tests
+          int r = nv;
 #pragma unroll
-        for (int i = 0; i < MV; ++i) pv[i] = D.v[i][j];
-        u32 lm = 0, cm = 0;  // labels of new-vertex children / closing positions produced
-        for (u32 jb = 0; jb < deg; jb += 32) {
-          bool ok = false;
-          if (jb + lane < deg) {
-            const u32 w = ldg(a.g.col + cb + jb + lane);
-            int r = nv;
+          for (int i = 0; i < MV; ++i)
+            if (i < nv && D.v[i][cj] == w) r = i;
+          const u64 n = w < x ? (((u64)w << 32) | x) : (((u64)x << 32) | w);
+          if (r == nv) {
+            ok = n > thrq;
+            if (ok) {
+              const u32 lab = lw >> kRankBits, lr = lw & kRankMask;
+              atomicAdd(cnt + lab, 1u);
+              u32* wp = rows + ((u64)lab * a.kpos + nv) * a.words + (lr >> 5);
+              const u32 bit = 1u << (lr & 31);
+              if (!(*wp & bit)) atomicOr(wp, bit);
+              lm |= 1u << lab;
+            }
+          } else if (r > q) {  // closing edge from its earlier-inserted endpoint
+            bool dup = false;
 #pragma unroll
-            for (int i = 0; i < MV; ++i)
-              if (i < nv && pv[i] == w) r = i;
-            const u64 n = w < x ? (((u64)w << 32) | x) : (((u64)x << 32) | w);
-            if (r == nv) {
-              ok = n > thrq;
-              if (ok) {
-                const u32 lw = ldg(a.g.lab + w);
-                const u32 lr = ldg(a.lrank + w);
-                atomicAdd(cnt + lw, 1u);
-                u32* wp = rows + ((u64)lw * a.kpos + nv) * a.words + (lr >> 5);
-                const u32 bit = 1u << (lr & 31);
-                if (!(*wp & bit)) atomicOr(wp, bit);
-                lm |= 1u << lw;
-              }
-            } else if (r > q) {  // closing edge from its earlier-inserted endpoint
-              bool dup = false;
+            for (int jj = 0; jj < LEV; ++jj) dup |= D.dupe[jj][cj] == n;
+            const u32 stp = D.stp[cj];
+            const int sq = (int)((stp >> (4 * q)) & 15u), sr = (int)((stp >> (4 * r)) & 15u);
+            const int sm = min(sq, sr);
+            u64 t = D.thr[0][cj];
 #pragma unroll
-              for (int jj = 0; jj < LEV; ++jj) dup |= D.dupe[jj][j] == n;
-              const u32 stp = D.stp[j];
-              const int sq = (int)((stp >> (4 * q)) & 15u), sr = (int)((stp >> (4 * r)) & 15u);
-              const int sm = min(sq, sr);
-              u64 t = D.thr[0][j];
+            for (int pp = 1; pp <= LEV; ++pp)
+              if (pp == sm) t = D.thr[pp][cj];
+            ok = !dup && n > t;
+            if (ok) cm |= 1u << r;
+          }
+        }
+        acc += __popc(__ballot_sync(0xffffffffu, ok));
+        if (nj != cj) {
+          // end of parent cj: its vertices once per (parent, slot) produced
+          lm = __reduce_or_sync(0xffffffffu, lm);
+          cm = __reduce_or_sync(0xffffffffu, cm);
+          if (lm | cm) {
+            u32 plr[MV];
 #pragma unroll
-              for (int pp = 1; pp <= LEV; ++pp)
-                if (pp == sm) t = D.thr[pp][j];
-              ok = !dup && n > t;
-              if (ok) cm |= 1u << r;
+            for (int i = 0; i < MV; ++i) plr[i] = D.lr[i][cj];
+            if (lm >> lane & 1u) {  // lane = new-vertex label (nl <= 32)
+#pragma unroll
+              for (int i = 0; i < MV; ++i)
+                if (i < nv) {
+                  u32* wp = rows + ((u64)lane * a.kpos + i) * a.words + (plr[i] >> 5);
+                  const u32 bit = 1u << (plr[i] & 31);
+                  if (!(*wp & bit)) atomicOr(wp, bit);
+                }
+            }
+            if (lane < MV && (cm >> lane & 1u)) {
+              const u32 sl = fa.nl + lane;
+              atomicAdd(cnt + sl, 1u);  // one closing child per (parent, q, r)
+#pragma unroll
+              for (int i = 0; i < MV; ++i)
+                if (i < nv) {
+                  u32* wp = rows + ((u64)sl * a.kpos + i) * a.words + (plr[i] >> 5);
+                  atomicOr(wp, 1u << (plr[i] & 31));
+                }
             }
           }
-          acc += __popc(__ballot_sync(0xffffffffu, ok));
+          lm = 0;
+          cm = 0;
         }
-        // parent positions: once per (parent, slot)
-        lm = __reduce_or_sync(0xffffffffu, lm);
-        cm = __reduce_or_sync(0xffffffffu, cm);
-        if (lm | cm) {
-          u32 plr[MV];
-#pragma unroll
-          for (int i = 0; i < MV; ++i) plr[i] = D.lr[i][j];
-          if (lm >> lane & 1u) {  // lane = new-vertex label (nl <= 32)
-#pragma unroll
-            for (int i = 0; i < MV; ++i)
-              if (i < nv) {
-                u32* wp = rows + ((u64)lane * a.kpos + i) * a.words + (plr[i] >> 5);
-                const u32 bit = 1u << (plr[i] & 31);
-                if (!(*wp & bit)) atomicOr(wp, bit);
-              }
-          }
-          if (lane < MV && (cm >> lane & 1u)) {
-            const u32 sl = fa.nl + lane;
-            atomicAdd(cnt + sl, 1u);  // one closing child per (parent, q, r)
-#pragma unroll
-            for (int i = 0; i < MV; ++i)
-              if (i < nv) {
-                u32* wp = rows + ((u64)sl * a.kpos + i) * a.words + (plr[i] >> 5);
-                atomicOr(wp, 1u << (plr[i] & 31));
-              }
-          }
-        }
+        cj = nj;
+        cjb = njb;
+        cw = nw;
       }
     }
     __syncthreads();
@@ -1179,6 +1245,9 @@ __global__ void l1_kernel(FsmArgs a, const u32* __restrict__ idx, const u32* __r
         u32 cv[2] = {u, v};
         domain_or<2>(a, hash_info(a.H, hash_find(a.H, code)), cv, 2, 0);
       }
+    } else if (MODE == kSparse) {
+      u32 cv[2] = {u, v};
+      sparse_emit(a, act, act ? hash_info(a.H, hash_find(a.H, code)) : 0ull, cv, 2);
     } else if (act) {
       keep[i] = a.frequent[hash_info(a.H, hash_find(a.H, code)) >> 32];
     }
@@ -1312,6 +1381,48 @@ __global__ void mni_kernel(const u32* __restrict__ bitmaps, u64 words, int kpos,
   if (threadIdx.x == 0) mni[pid] = best;
 }
 
+// packed orbit representatives of every sparse slot (identity unless
+// full-automorphism MNI)
+__global__ void srep_kernel(const u64* __restrict__ gkeys, const u32* __restrict__ sp_to_pid, u64 NS, int LB, int full,
+                            u32* __restrict__ srep) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < NS; i += (u64)gridDim.x * blockDim.x) {
+    const u64 key = gkeys[sp_to_pid[i]];
+    const int nv = pat::code_nv(key);
+    u8 rep[8];
+    for (int j = 0; j < 8; ++j) rep[j] = (u8)j;
+    if (full) {
+      int n2;
+      u32 lab[8], mask;
+      pat::decode(key, LB, &n2, lab, &mask);
+      pat::orbits(nv, lab, mask, rep);
+    }
+    u32 pk = 0;
+    for (int j = 0; j < 8; ++j) pk |= (u32)rep[j] << (3 * j);
+    srep[i] = pk;
+  }
+}
+
+// sorted keys -> distinct (slot, position, vertex) per (slot, position)
+__global__ void sparse_count_kernel(const unsigned long long* __restrict__ k, u64 n,
+                                    unsigned long long* __restrict__ dcnt) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    if (k[i] != ~0ull && (i == 0 || k[i] != k[i - 1])) atomicAdd(dcnt + (k[i] >> 32), 1ull);
+}
+
+// MNI of every sparse slot: min over its orbit representatives' domain sizes
+__global__ void sparse_mni_kernel(const unsigned long long* __restrict__ dcnt, const u64* __restrict__ gkeys,
+                                  const u32* __restrict__ sp_to_pid, const u32* __restrict__ srep, u64 NS,
+                                  unsigned long long* __restrict__ mni) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < NS; i += (u64)gridDim.x * blockDim.x) {
+    const u32 pid = sp_to_pid[i];
+    const int nv = pat::code_nv(gkeys[pid]);
+    unsigned long long best = ~0ull;
+    for (int j = 0; j < nv; ++j)
+      if (((srep[i] >> (3 * j)) & 7u) == (u32)j) best = min(best, dcnt[i * 8 + j]);
+    mni[pid] = best;
+  }
+}
+
 struct NonZeroW {
   const u64* w;
   __device__ __forceinline__ bool operator()(const u32& i) const { return w[i] != 0; }
@@ -1329,7 +1440,7 @@ __global__ void iota_kernel(u32* __restrict__ v, u32 n) {
 // sorted (label, vertex) -> rank of each vertex within its label class; the
 // largest class size -> *mx
 __global__ void lrank_kernel(const u32* __restrict__ lab, const u32* __restrict__ vid, u32 n, u32* __restrict__ lrank,
-                             unsigned long long* __restrict__ mx) {
+                             u32* __restrict__ labrank, unsigned long long* __restrict__ mx) {
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     // class start: first index with the same label (binary search)
     u64 lo = 0, hi = i;
@@ -1340,6 +1451,7 @@ __global__ void lrank_kernel(const u32* __restrict__ lab, const u32* __restrict_
       else hi = mid;
     }
     lrank[vid[i]] = (u32)(i - lo);
+    if (labrank) labrank[vid[i]] = (L << kRankBits) | ((u32)(i - lo) & kRankMask);
     if (i + 1 == n || lab[i + 1] != L) atomicMax(mx, (unsigned long long)(i - lo + 1));
   }
 }
@@ -1363,6 +1475,7 @@ struct Fsm {
   u64 prev_unique = 1024;
   DBuf<unsigned long long> d_ctr;
   DBuf<u32> lrank;   // vertex -> rank within its label class
+  DBuf<u32> labrank; // vertex -> label << 27 | rank (fan pass; LB <= 5)
   u64 max_class = 1;
 
   // lrank[v] = #{u < v : lab[u] == lab[v]} via a stable sort of (label, v)
@@ -1381,7 +1494,9 @@ struct Fsm {
                                              std::max(1, LB), s));
     DBuf<unsigned long long> mx(1, s);
     GPM_CUDA(cudaMemsetAsync(mx.get(), 0, sizeof(unsigned long long), s));
-    lrank_kernel<<<grid1(n), 256, 0, s>>>(lab2.get(), vid2.get(), n, lrank.get(), mx.get());
+    if (LB <= 5) labrank.alloc(n, s);
+    lrank_kernel<<<grid1(n), 256, 0, s>>>(lab2.get(), vid2.get(), n, lrank.get(), LB <= 5 ? labrank.get() : nullptr,
+                                          mx.get());
     GPM_CUDA(cudaGetLastError());
     tl.launches += 4;
     max_class = std::max<u64>(1, d2h(mx.get()));
@@ -1421,6 +1536,10 @@ struct Fsm {
     DBuf<u64> gkeys;
     u64 P = 0;
     u64 NB = 0;
+    // sparse domains: pattern -> sparse slot, slot -> pattern, key capacity
+    DBuf<u32> sslot, sp_to_pid;
+    u64 NS = 0;
+    u64 skeys_total = 0;
   };
 
   Hash hash_of(Level& R) {
@@ -1439,7 +1558,7 @@ struct Fsm {
 
   // After pass A: canonicalize slots, global pattern table (+exchange), pids,
   // count pre-filter, bitmap slots.
-  void canon_and_group(Level& R) {
+  void canon_and_group(Level& R, int kpos, bool allow_sparse) {
     // list the U occupied slots, canonicalize each distinct quick code once,
     // sort by canonical code and reduce by key on the device: only the
     // distinct canonical patterns come back to the host
@@ -1537,12 +1656,48 @@ struct Fsm {
     std::vector<u32> bslot(std::max<u64>(1, R.P), ~0u), bs_to_pid;
     // MNI <= count; the full-automorphism MNI unions an orbit's domains: <= nv * count
     const bool full = cfg.mni_mode == GPM_MNI_AUTOMORPHISM;
+    std::vector<u8> need(std::max<u64>(1, R.P), 0);
     for (u64 p = 0; p < R.P; ++p)
-      if (R.gcount_h[p] * (full ? (u64)pat::code_nv(R.gkeys_h[p]) : 1) >= sigma) {
+      need[p] = R.gcount_h[p] * (full ? (u64)pat::code_nv(R.gkeys_h[p]) : 1) >= sigma;
+    // sparse domains: a pattern whose keys (8 B per embedding
+    // vertex, x2 for the sort) cost less than its dense label-local bitmap
+    // rows -- big label classes, few embeddings -- gets sorted key lists
+    // instead, within half the budget (GPM_FSM_SPARSE=1: every pattern).
+    // Counts, words and the budget are rank-invariant, so is the choice.
+    std::vector<u32> sslot(std::max<u64>(1, R.P), ~0u), sp_to_pid;
+    R.skeys_total = 0;
+    if (allow_sparse) {
+      const bool force = std::getenv("GPM_FSM_SPARSE") != nullptr;
+      const u64 words = (max_class + 31) / 32;
+      std::vector<std::pair<u64, u32>> cand;
+      for (u64 p = 0; p < R.P; ++p) {
+        if (!need[p]) continue;
+        const u64 keyb = R.gcount_h[p] * (u64)pat::code_nv(R.gkeys_h[p]) * 16;
+        if (force || keyb < (u64)kpos * words * 4) cand.emplace_back(keyb, (u32)p);
+      }
+      std::sort(cand.begin(), cand.end());
+      u64 used = 0;
+      for (auto [kb, p] : cand) {
+        if (used + kb > budget / 2) break;
+        used += kb;
+        sslot[p] = (u32)sp_to_pid.size();
+        sp_to_pid.push_back(p);
+        R.skeys_total += kb / 16;
+      }
+    }
+    for (u64 p = 0; p < R.P; ++p)
+      if (need[p] && sslot[p] == ~0u) {
         bslot[p] = (u32)bs_to_pid.size();
         bs_to_pid.push_back((u32)p);
       }
     R.NB = bs_to_pid.size();
+    R.NS = sp_to_pid.size();
+    if (R.NS) st.paths |= GPM_PATH_FSM_SPARSE;
+    R.sslot.alloc(sslot.size(), s);
+    GPM_CUDA(cudaMemcpyAsync(R.sslot.get(), sslot.data(), sizeof(u32) * sslot.size(), cudaMemcpyHostToDevice, s));
+    R.sp_to_pid.alloc(std::max<u64>(1, R.NS), s);
+    if (R.NS)
+      GPM_CUDA(cudaMemcpyAsync(R.sp_to_pid.get(), sp_to_pid.data(), sizeof(u32) * R.NS, cudaMemcpyHostToDevice, s));
     R.bslot.alloc(bslot.size(), s);
     GPM_CUDA(cudaMemcpyAsync(R.bslot.get(), bslot.data(), sizeof(u32) * bslot.size(), cudaMemcpyHostToDevice, s));
     R.bs_to_pid.alloc(std::max<u64>(1, R.NB), s);
@@ -1552,9 +1707,60 @@ struct Fsm {
     trace("group", (double)R.P, (double)R.NB);
   }
 
+  // Sparse domains: one extend pass emits (slot, position, rank) keys for the
+  // children of sparse patterns; sort + unique (+ all-gather across ranks)
+  // give every domain exactly; MNI per slot.
+  template <class SparseFn>
+  void sparse_domains(Level& R, unsigned long long* mni, SparseFn&& run_sparse) {
+    DBuf<u32> srep(R.NS, s);
+    srep_kernel<<<grid1(R.NS), 256, 0, s>>>(R.gkeys.get(), R.sp_to_pid.get(), R.NS, LB,
+                                            cfg.mni_mode == GPM_MNI_AUTOMORPHISM, srep.get());
+    GPM_CUDA(cudaGetLastError());
+    const u64 cap = std::max<u64>(1, R.skeys_total);
+    DBuf<unsigned long long> keys(cap, s), top(1, s);
+    GPM_CUDA(cudaMemsetAsync(top.get(), 0, sizeof(unsigned long long), s));
+    run_sparse(keys.get(), top.get(), cap, srep.get());
+    u64 nk = d2h(top.get());
+    if (nk > cap) throw Error(GPM_ENOMEM, "fsm: sparse domain keys exceed the planned capacity");
+    DBuf<unsigned long long> sorted(std::max<u64>(1, nk), s);
+    auto sort_keys = [&](unsigned long long* in, unsigned long long* out, u64 n) {
+      size_t tmp = 0;
+      GPM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, in, out, (int64_t)n, 0, 64, s));
+      DBuf<u8> t(tmp, s);
+      GPM_CUDA(cub::DeviceRadixSort::SortKeys(t.get(), tmp, in, out, (int64_t)n, 0, 64, s));
+      tl.launches += 4;
+    };
+    if (nk) sort_keys(keys.get(), sorted.get(), nk);
+    if (cfg.world > 1 && cfg.exchange) {
+      // union over ranks: all-gather every rank's sorted keys (padded with ~0)
+      const int W = cfg.world;
+      std::vector<u64> lens(W, 0);
+      lens[cfg.rank] = nk;
+      exchange_sum_host(cfg, lens, s);
+      const u64 mx = std::max<u64>(1, *std::max_element(lens.begin(), lens.end()));
+      DBuf<unsigned long long> all(mx * W, s), all2(mx * W, s);
+      GPM_CUDA(cudaMemsetAsync(all.get(), 0xff, sizeof(unsigned long long) * mx * W, s));
+      if (nk)
+        GPM_CUDA(cudaMemcpyAsync(all.get() + (u64)cfg.rank * mx, sorted.get(), sizeof(unsigned long long) * nk,
+                                 cudaMemcpyDeviceToDevice, s));
+      exchange_device(cfg, all.get(), mx, 8, 2, s);
+      sort_keys(all.get(), all2.get(), mx * W);
+      sorted = std::move(all2);
+      nk = 0;
+      for (u64 x : lens) nk += x;  // the ~0 padding sorts last
+    }
+    DBuf<unsigned long long> dcnt(R.NS * 8, s);
+    GPM_CUDA(cudaMemsetAsync(dcnt.get(), 0, sizeof(unsigned long long) * R.NS * 8, s));
+    if (nk) sparse_count_kernel<<<grid1(nk), 256, 0, s>>>(sorted.get(), nk, dcnt.get());
+    sparse_mni_kernel<<<grid1(R.NS), 256, 0, s>>>(dcnt.get(), R.gkeys.get(), R.sp_to_pid.get(), srep.get(), R.NS, mni);
+    GPM_CUDA(cudaGetLastError());
+    tl.launches += 3;
+    trace("sparse domains (slots, keys)", (double)R.NS, (double)nk);
+  }
+
   // Domain pass in rounds that fit the bitmap budget; MNI; frequent flags.
-  template <class DomainFn>
-  void domains_and_mni(Level& R, int kpos, DomainFn&& run_domain) {
+  template <class DomainFn, class SparseFn>
+  void domains_and_mni(Level& R, int kpos, DomainFn&& run_domain, SparseFn&& run_sparse) {
     // label-local domain bitmaps: a position's vertices all carry its label,
     // so bits are indexed by the rank within the label class (n/#labels bits
     // per position instead of n)
@@ -1579,6 +1785,7 @@ struct Fsm {
         ++tl.launches;
       }
     }
+    if (R.NS) sparse_domains(R, mni.get(), run_sparse);
     R.mni_h.assign(R.P, 0);
     if (R.P)
       GPM_CUDA(cudaMemcpyAsync(R.mni_h.data(), mni.get(), sizeof(u64) * R.P, cudaMemcpyDeviceToHost, s));
@@ -1633,22 +1840,38 @@ struct Fsm {
       cap <<= 3;
     }
     prev_unique = d2h(R.used.get());
-    canon_and_group(R);
-    domains_and_mni(R, 2, [&](u32* bm, u64 words, int kpos, u32 lo, u32 hi) {
-      FsmArgs a = base_args(R);
-      a.bslot = R.bslot.get();
-      a.bitmaps = bm;
-      a.words = words;
-      a.lrank = lrank.get();
-      a.kpos = kpos;
-      a.round_lo = lo;
-      a.round_hi = hi;
-      if (n1) {
-        l1_kernel<kDomain><<<grid1(n1), 256, 0, s>>>(a, idx.get(), vid.get(), n1, nullptr);
-        GPM_CUDA(cudaGetLastError());
-        ++tl.launches;
-      }
-    });
+    canon_and_group(R, 2, true);
+    domains_and_mni(
+        R, 2,
+        [&](u32* bm, u64 words, int kpos, u32 lo, u32 hi) {
+          FsmArgs a = base_args(R);
+          a.bslot = R.bslot.get();
+          a.bitmaps = bm;
+          a.words = words;
+          a.lrank = lrank.get();
+          a.kpos = kpos;
+          a.round_lo = lo;
+          a.round_hi = hi;
+          if (n1) {
+            l1_kernel<kDomain><<<grid1(n1), 256, 0, s>>>(a, idx.get(), vid.get(), n1, nullptr);
+            GPM_CUDA(cudaGetLastError());
+            ++tl.launches;
+          }
+        },
+        [&](unsigned long long* keys, unsigned long long* top, u64 scap, const u32* srep) {
+          FsmArgs a = base_args(R);
+          a.lrank = lrank.get();
+          a.sslot = R.sslot.get();
+          a.srep = srep;
+          a.skeys = keys;
+          a.stop = top;
+          a.scap = scap;
+          if (n1) {
+            l1_kernel<kSparse><<<grid1(n1), 256, 0, s>>>(a, idx.get(), vid.get(), n1, nullptr);
+            GPM_CUDA(cudaGetLastError());
+            ++tl.launches;
+          }
+        });
     record(R, 1);
     // filter: keep entries whose pattern is frequent
     if (!n1) return;
@@ -1681,6 +1904,7 @@ struct Fsm {
       case kQC: kern = eextend_kernel<LEV, kQC>; break;
       case kDomain: kern = eextend_kernel<LEV, kDomain>; break;
       case kSCount: kern = eextend_kernel<LEV, kSCount>; break;
+      case kSparse: kern = eextend_kernel<LEV, kSparse>; break;
       default: kern = eextend_kernel<LEV, kSWrite>; break;
     }
     int occ = 0;
@@ -1826,7 +2050,7 @@ struct Fsm {
     return (size_t)(4 * (nslot * kpos * words + 2 * nslot + 2) + desc);
   }
   bool fan_fits(int LEVv, int kpos, u64 words) const {
-    if (LB > 5) return false;  // label slots are lanes of a warp
+    if (LB > 5 || !labrank.get() || max_class >= (u64(1) << kRankBits)) return false;  // label slots = lanes
     int maxs = 0;
     GPM_CUDA(cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, G.device));
     return fan_smem(LEVv, kpos, words) + 1024 <= (size_t)maxs;
@@ -2038,6 +2262,7 @@ struct Fsm {
           a.words = wordsL;
           a.lrank = lrank.get();
         }
+        a.labrank = labrank.get();
         if (use_fan) launch_fan<LEV>(a, fitems, nfan, "fsm_fan_qc_domain", bytes_in);
         else if (gr.on) launch_group<LEV>(a, gr, qcap ? kQCD : kQC, qcap ? "fsm_group_qc_domain" : "fsm_group_qc", bytes_in);
         else launch<LEV>(a, kQC, qcap ? "fsm_extend_qc_domain" : "fsm_extend_qc", bytes_in);
@@ -2058,7 +2283,7 @@ struct Fsm {
       acc = v[0];
     }
     st.level_sizes[LEV] += acc;
-    canon_and_group(R);
+    canon_and_group(R, LEV + 2, !fused);
     domains_and_mni(R, LEV + 2, [&](u32* bm, u64 words, int kpos, u32 lo, u32 hi) {
       if (!nb) return;
       if (fused) {
@@ -2078,6 +2303,16 @@ struct Fsm {
       a.round_hi = hi;
       if (gr.on) launch_group<LEV>(a, gr, kDomain, "fsm_group_domain", bytes_in);
       else launch<LEV>(a, kDomain, "fsm_extend_domain", bytes_in);
+    }, [&](unsigned long long* keys, unsigned long long* top, u64 scap, const u32* srep) {
+      if (!nb) return;
+      FsmArgs a = args(R);
+      a.lrank = lrank.get();
+      a.sslot = R.sslot.get();
+      a.srep = srep;
+      a.skeys = keys;
+      a.stop = top;
+      a.scap = scap;
+      launch<LEV>(a, kSparse, "fsm_extend_sparse", bytes_in);
     });
     record(R, LEV + 1);
     trace("mni+record", (double)R.P);

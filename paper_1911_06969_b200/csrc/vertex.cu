@@ -635,8 +635,14 @@ template <int MODE, bool SIB = false>
 void launch_edge(Ctx& c, EdgeArgs& a, const std::string& what, double bytes) {
   // GPM_CF_STREAM=1: the packed-stream kernel (all lanes on the concatenated
   // candidate lists) instead of the lane-per-parent one
+  // FUSED counts run on the hybrid kernel (whole 32-candidate chunks without
+  // the lane -> parent mapping: TC16 0.264 -> 0.215 ms); the inspection pass
+  // stays on the packed stream, which measured faster on short-list DAGs
+  // (PAT 4-CL: 1.20 vs 1.45 ms; profiles/r02).  GPM_CF_STREAM=1 / GPM_CF_HYBRID=1
+  // force one or the other.
   static const bool stream_env = std::getenv("GPM_CF_STREAM") != nullptr;
-  const bool stream = stream_env || MODE == kWrite;
+  static const bool hybrid_env = std::getenv("GPM_CF_HYBRID") != nullptr;
+  const bool stream = stream_env || MODE == kWrite || (MODE == kCount && !hybrid_env);
   void (*kern)(EdgeArgs) = edge_chunk_kernel<MODE, SIB>;
   if constexpr (MODE != kWrite) {
     if (!stream) kern = edge_lane_kernel<MODE, SIB>;

@@ -112,3 +112,21 @@ def test_config_conflicts_return_econfig(P, oracle):
     with pytest.raises(_lib.GpmError) as e:
         P.list_embeddings(g, "mc", 3)
     assert e.value.code == _lib.GPM_ECONFIG
+
+
+def test_fsm_big_n_sparse_domains_vs_oracle(P, oracle):
+    """Bigger-n FSM: many labels, so most patterns have
+    few embeddings against big label classes; under a tight memory budget the
+    dense label-local rows no longer fit at once (rounds), and the patterns
+    whose sorted keys cost less than their rows take sparse domains (chosen by
+    cost, not forced).  Result = the oracle's."""
+    from paper_1911_06969_b200 import _lib
+    hg = P.generate_rmat(17, 4, 0.45, 0.15, 0.15, seed=8, n_labels=50, label_seed=9)
+    c = oracle.Csr(hg.off, hg.col, hg.labels)
+    g = P.Graph(hg)
+    for k, sigma in ((2, 5), (3, 5)):
+        r = P.mine(g, "fsm", k, sigma, mem_budget=4 << 20)
+        assert r.stats["paths"] & _lib.PATH_FSM_SPARSE, k
+        o = oracle.mine(c, "fsm", k, sigma)
+        assert sorted(r.patterns) == sorted(tuple(x) for x in o["patterns"]), k
+        assert r.stats["n_explored"] == o["n_explored"]

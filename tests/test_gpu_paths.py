@@ -81,3 +81,15 @@ def test_mc_paths_under_planner_chunks(P):
 def test_fsm_paths(P, labels, sigma, k):
     g = P.Graph(P.generate_rmat(12, 8, 0.45, 0.15, 0.15, seed=3, n_labels=labels, label_seed=7))
     _same(_run(P, g, "fsm", k, sigma), _run(P, g, "fsm", k, sigma, env=["GPM_FSM_TWO_PASS"]))
+
+
+@pytest.mark.parametrize("labels,sigma,k", [(4, 30, 4), (8, 20, 3), (6, 40, 5), (1, 50, 3)])
+def test_fsm_sparse_domains_equal_bitmaps(P, labels, sigma, k):
+    # GPM_FSM_SPARSE: every pattern's domains as sorted (slot, position, vertex)
+    # keys instead of bitmaps, with the separate domain pass
+    from paper_1911_06969_b200 import _lib
+    g = P.Graph(P.generate_rmat(12, 8, 0.45, 0.15, 0.15, seed=3, n_labels=labels, label_seed=7))
+    for mni in ("canonical", "automorphism"):
+        sp = _run(P, g, "fsm", k, sigma, env=["GPM_FSM_SPARSE", "GPM_FSM_TWO_PASS"], mni=mni)
+        assert sp.stats["paths"] & _lib.PATH_FSM_SPARSE
+        _same(sp, _run(P, g, "fsm", k, sigma, env=["GPM_FSM_TWO_PASS"], mni=mni))
