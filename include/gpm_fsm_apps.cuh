@@ -1,0 +1,37 @@
+// gpm_fsm_apps.cuh — frequent subgraph mining as the builtin App of the
+// header-only edge-mode engine (include/gpm_fsm_engine.cuh).
+//
+//   FsmApp  fsm(k, sigma)   SPEC.md:441-449, Listing 5:
+//           extend every position (toExtend default true), to_add_edge =
+//           is_auto_canonical_edge + the closing edge from its earlier-inserted
+//           endpoint, reduce = quick -> canonical pattern with
+//           canonical-mapping (or full-automorphism) MNI domains, to_prune =
+//           MNI < sigma.
+// A user edge-mode app defines the same members (kBuiltin = false) and calls
+// gpm::mine_edge_app<App> (tests/apps/test_apps.cu).
+#pragma once
+#include "gpm_fsm_engine.cuh"
+
+namespace gpm {
+
+struct FsmApp {
+  static constexpr bool kBuiltin = true;  // grouped / fan-out passes inline these hooks
+  static constexpr bool kDomains = true;  // MNI support
+  template <int LEV>
+  __device__ static bool to_extend(const fsm_engine::EEmb<LEV>&, int) { return true; }
+  template <int LEV>
+  __device__ static bool to_add_edge(const fsm_engine::EEmb<LEV>& e, const DevGraph&, int q, u32 w, int r) {
+    return fsm_engine::edge_to_add<LEV>(e, q, w, r);
+  }
+  static bool to_prune(const fsm_engine::PatternInfo& p) { return p.count < p.sigma || p.support < p.sigma; }
+};
+
+// gpm_mine for an edge-mode App, inside gpm_mine's bookkeeping (stream,
+// timing, stats); the C-ABI entry a custom edge app's wrapper calls.
+template <class App>
+int mine_edge_app(const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
+  return run_custom(g, cfg, out, [](const gpm_graph& G, const gpm_config& c, cudaStream_t s, gpm_result& r, Stats& st,
+                                    Timeline& tl) { fsm_engine::mine_edges<App>(G, c, s, r, st, tl); });
+}
+
+}  // namespace gpm

@@ -303,11 +303,13 @@ def mine(g: Graph, app: str, k: int = 3, min_support: int = 0, **kw) -> MineResu
     return _collect(r, app, k)
 
 
-def mine_custom(entry, g: Graph, k: int, *, name: str = "custom", **kw) -> MineResult:
-    """Runs a user App compiled against include/gpm_engine.cuh: `entry` is a
-    ctypes function with gpm_mine's signature (graph, config, result**) that
-    calls gpm::mine_app<App> (tests/apps/test_apps.cu)."""
-    cfg = make_config("tc", k, 0, **kw)
+def mine_custom(entry, g: Graph, k: int, *, name: str = "custom", min_support: int = 0, **kw) -> MineResult:
+    """Runs a user App compiled against include/gpm_engine.cuh (vertex mode,
+    gpm::mine_app<App>) or include/gpm_fsm_engine.cuh (edge mode,
+    gpm::mine_edge_app<App>; k = edges + 1, min_support = sigma): `entry` is
+    a ctypes function with gpm_mine's signature (graph, config, result**)
+    (tests/apps/test_apps.cu)."""
+    cfg = make_config("tc", k, min_support, **kw)
     cfg.app = -1  # not a builtin app
     r = C.c_void_p()
     check(entry(g.handle, C.byref(cfg), C.byref(r)))

@@ -5,6 +5,7 @@
 // tests/apps/libgpm_testapps.so (linked against libgpm.so) and checked by
 // tests/test_gpu_apps.py against brute force.
 #include "gpm_engine.cuh"
+#include "gpm_fsm_apps.cuh"
 
 namespace gpm {
 namespace {
@@ -136,8 +137,53 @@ struct WedgeGrownMotifApp {
   static std::string code_text(u32, int) { return std::string(); }
 };
 
+// ---------------------------------------------------------------- edge mode
+// (include/gpm_fsm_engine.cuh; Listing 5's hooks with user changes)
+
+// FSM restricted to vertices with label < 2: toAdd(edge) rejects a new vertex
+// with another label, toPrune drops any pattern carrying one (the level-1
+// single edges include every edge).  = FSM on the induced subgraph.
+struct LabelSubsetFsmApp {
+  static constexpr bool kBuiltin = false, kDomains = true;
+  template <int LEV>
+  __device__ static bool to_extend(const fsm_engine::EEmb<LEV>&, int) { return true; }
+  template <int LEV>
+  __device__ static bool to_add_edge(const fsm_engine::EEmb<LEV>& e, const DevGraph& g, int q, u32 w, int r) {
+    if (r == e.nv && __ldg(g.lab + w) >= 2) return false;
+    return fsm_engine::edge_to_add<LEV>(e, q, w, r);
+  }
+  static bool to_prune(const fsm_engine::PatternInfo& p) {
+    int nv;
+    u32 lab[8], mask;
+    pat::decode(p.key, p.label_bits, &nv, lab, &mask);
+    for (int i = 0; i < nv; ++i)
+      if (lab[i] >= 2) return true;  // dense label ranks: the test graph's labels are 0..L-1
+    return p.count < p.sigma || p.support < p.sigma;
+  }
+};
+
+// Embedding-count support instead of MNI (no domains): toPrune = count < sigma.
+struct CountSupportFsmApp {
+  static constexpr bool kBuiltin = false, kDomains = false;
+  template <int LEV>
+  __device__ static bool to_extend(const fsm_engine::EEmb<LEV>&, int) { return true; }
+  template <int LEV>
+  __device__ static bool to_add_edge(const fsm_engine::EEmb<LEV>& e, const DevGraph&, int q, u32 w, int r) {
+    return fsm_engine::edge_to_add<LEV>(e, q, w, r);
+  }
+  static bool to_prune(const fsm_engine::PatternInfo& p) { return p.count < p.sigma; }
+};
+
 }  // namespace
 }  // namespace gpm
+
+extern "C" int testapp_mine_edges(int which, const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
+  switch (which) {
+    case 0: return gpm::mine_edge_app<gpm::LabelSubsetFsmApp>(g, cfg, out);
+    case 1: return gpm::mine_edge_app<gpm::CountSupportFsmApp>(g, cfg, out);
+    default: return GPM_EINVAL;
+  }
+}
 
 extern "C" int testapp_mine(int which, const gpm_graph* g, const gpm_config* cfg, gpm_result** out) {
   switch (which) {

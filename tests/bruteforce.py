@@ -175,7 +175,7 @@ def connected_edge_subsets(adj, size):
         yield canonical_edge_order(S)
 
 
-def fsm(adj, labels, k, sigma, full=False):
+def fsm(adj, labels, k, sigma, full=False, support="mni"):
     """Level-wise FSM with canonical-mapping MNI (full=True: true MNI over all
     isomorphic mappings) and Alg. 1 filter semantics.
     Returns ([(level, text, mni)...], level_sizes)."""
@@ -204,7 +204,13 @@ def fsm(adj, labels, k, sigma, full=False):
                 for i, v in enumerate(verts):
                     d[perm[i]].add(v)
             pat_of[frozenset(seq)] = t
-        mni = {t: min(len(s) for s in d) for t, d in dom.items()}
+        if support == "count":  # embedding-count support (SPEC.md CountSupport)
+            cnt = defaultdict(int)
+            for S, t in pat_of.items():
+                cnt[t] += 1
+            mni = dict(cnt)
+        else:
+            mni = {t: min(len(s) for s in d) for t, d in dom.items()}
         for t, m in mni.items():
             if m >= sigma:
                 result.append((lev, t, m))

@@ -123,3 +123,50 @@ def test_filter_app_prunes_triangle_prefixes(P, oracle, testapps, n, p, seed):
     # the same hooks without the filter = motif counting (the builtin app)
     full = P.motif_count(g, 4)
     assert sum(full.values()) >= sum(want.values())
+
+
+# ---------------------------------------------------------------- edge mode
+@pytest.fixture(scope="module")
+def edgeapps(P):
+    path = os.path.join(HERE, "apps", "libgpm_testapps.so")
+    from paper_1911_06969_b200 import _lib
+    L = C.CDLL(path)
+    L.testapp_mine_edges.restype = C.c_int
+    L.testapp_mine_edges.argtypes = [C.c_int, C.c_void_p, C.POINTER(_lib.Config), C.POINTER(C.c_void_p)]
+    return {name: (lambda i: (lambda g, cfg, out: L.testapp_mine_edges(i, g, cfg, out)))(i)
+            for name, i in {"label_subset": 0, "count_support": 1}.items()}
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_edge_app_label_subset_equals_induced_fsm(P, oracle, edgeapps, seed):
+    """toAdd(edge) + toPrune restricted to labels {0, 1} == the builtin FSM
+    (the oracle) on the subgraph induced by those vertices."""
+    rng = np.random.default_rng(60 + seed)
+    n = 90
+    lab = rng.integers(0, 4, n)
+    lab[:4] = [0, 1, 2, 3]  # every label present: dense ranks == values
+    E = BF.gnp(n, 0.09, 60 + seed)
+    g, _ = graph(P, oracle, E, n, lab)
+    keep = lab < 2
+    Es = [(a, b) for a, b in E if keep[a] and keep[b]]
+    sub = oracle.csr_from_edges(Es, n, lab)
+    for k, sigma in ((2, 2), (3, 3), (4, 3)):
+        r = P.api.mine_custom(edgeapps["label_subset"], g, k, name="fsm", min_support=sigma)
+        o = oracle.mine(sub, "fsm", k, sigma)
+        assert [tuple(p) for p in r.patterns] == [tuple(p) for p in o["patterns"]], (k, sigma)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_edge_app_count_support_vs_bruteforce(P, oracle, edgeapps, seed):
+    """toPrune on the embedding count (no domains) vs brute force over
+    connected edge subsets with the same filter semantics."""
+    rng = np.random.default_rng(70 + seed)
+    n = int(rng.integers(14, 24))
+    lab = rng.integers(0, 2, n)
+    E = BF.gnp(n, 0.2, 70 + seed)
+    g, adj = graph(P, oracle, E, n, lab)
+    for k, sigma in ((2, 2), (3, 4), (4, 6)):
+        r = P.api.mine_custom(edgeapps["count_support"], g, k, name="fsm", min_support=sigma)
+        want, sizes = BF.fsm(adj, lab, k, sigma, support="count")
+        assert [tuple(p) for p in r.patterns] == want, (k, sigma)
+        assert r.stats["level_sizes"][:len(sizes)] == sizes
