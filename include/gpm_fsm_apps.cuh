@@ -6,7 +6,7 @@
 //           is_auto_canonical_edge + the closing edge from its earlier-inserted
 //           endpoint, reduce = quick -> canonical pattern with
 //           canonical-mapping (or full-automorphism) MNI domains, to_prune =
-//           MNI < sigma.
+//           MNI < sigma, reported support = MNI.
 // A user edge-mode app defines the same members (kBuiltin = false) and calls
 // gpm::mine_edge_app<App> (tests/apps/test_apps.cu).
 #pragma once
@@ -23,7 +23,14 @@ struct FsmApp {
   __device__ static bool to_add_edge(const fsm_engine::EEmb<LEV>& e, const DevGraph&, int q, u32 w, int r) {
     return fsm_engine::edge_to_add<LEV>(e, q, w, r);
   }
-  static bool to_prune(const fsm_engine::PatternInfo& p) { return p.count < p.sigma || p.support < p.sigma; }
+  // Listing 5: MNI < sigma.  (Canonical-mapping MNI <= count, so count < sigma
+  // prunes too; the full-automorphism MNI can exceed the count.)
+  static bool to_prune(const fsm_engine::PatternInfo& p) {
+    if (p.mni_mode == GPM_MNI_CANONICAL && p.count < p.sigma) return true;
+    return p.support < p.sigma;
+  }
+  // the support reported with a frequent pattern (PatternMap)
+  static u64 support_of(const fsm_engine::PatternInfo& p) { return p.support; }
 };
 
 // gpm_mine for an edge-mode App, inside gpm_mine's bookkeeping (stream,

@@ -7,6 +7,8 @@
 //                                           r = position of w in emb (nv: new vertex)
 //   to_prune(PatternInfo)                   toPrune on a canonical pattern's
 //                                           (count, MNI support, sigma)
+//   support_of(PatternInfo)                 the support reported with a
+//                                           surviving pattern (getSupport)
 //   kBuiltin                                the builtin FSM hooks: enables the
 //                                           grouped and fan-out fast paths
 //   kDomains                                compute MNI domains (false: the
@@ -1845,7 +1847,10 @@ struct Fsm {
       if (frequent_pat(R, p)) sel.push_back(p);
     // text is formatted on access (gpm_result_pattern): ~10^6 patterns per call
     res.kpatterns.reserve(res.kpatterns.size() + sel.size());
-    for (u64 p : sel) res.kpatterns.push_back({R.gkeys_h[p], R.mni_h[p], level});
+    for (u64 p : sel) {
+      const PatternInfo pi{R.gkeys_h[p], R.gcount_h[p], R.mni_h[p], sigma, LB, cfg.mni_mode};
+      res.kpatterns.push_back({R.gkeys_h[p], App::support_of(pi), level});
+    }
   }
 
   FsmArgs base_args(Level& R) {

@@ -45,7 +45,10 @@ std::string read_file(const char* path) {
   std::fseek(f, 0, SEEK_END);
   long sz = std::ftell(f);
   std::fseek(f, 0, SEEK_SET);
-  std::string buf(sz > 0 ? (size_t)sz : 0, '\0');
+  std::string buf;
+  // resize_and_overwrite-style: grow without the zero fill of std::string(n, '\0')
+  buf.reserve(sz > 0 ? (size_t)sz : 0);
+  buf.resize(sz > 0 ? (size_t)sz : 0);
   if (sz > 0 && std::fread(buf.data(), 1, (size_t)sz, f) != (size_t)sz) {
     std::fclose(f);
     throw Error(GPM_EINVAL, std::string("short read on ") + path);
@@ -111,6 +114,34 @@ struct Compactor {
   std::vector<u32> table;  // when ids are small: id -> dense
   std::unordered_map<u64, u32> map;
 
+  // ids = a ++ b (two halves, no concatenated copy on the dense path)
+  void build2(const std::vector<u64>& a, const std::vector<u64>& b) {
+    u64 mx = 0;
+    const long long na = (long long)a.size(), nt = na + (long long)b.size();
+#pragma omp parallel for reduction(max : mx) schedule(static)
+    for (long long i = 0; i < nt; ++i) mx = std::max(mx, i < na ? a[i] : b[i - na]);
+    if (nt > 0 && mx < (u64(1) << 32) && mx <= 4 * (u64)nt + 1024) {
+      dense_range = true;
+      std::vector<u8> seen(mx + 1, 0);
+      u8* sp = seen.data();
+#pragma omp parallel for schedule(static)
+      for (long long i = 0; i < nt; ++i) sp[i < na ? a[i] : b[i - na]] = 1;  // benign same-value writes
+      table.assign(mx + 1, UINT32_MAX);
+      u32 d = 0;
+      for (u64 x = 0; x <= mx; ++x)
+        if (seen[x]) {
+          table[x] = d++;
+          uniq.push_back(x);
+        }
+      if (uniq.size() >= (u64(1) << 32)) throw Error(GPM_EINVAL, "too many vertices for 32-bit ids");
+      return;
+    }
+    std::vector<u64> ids;
+    ids.reserve(nt);
+    ids.insert(ids.end(), a.begin(), a.end());
+    ids.insert(ids.end(), b.begin(), b.end());
+    build(std::move(ids));
+  }
   void build(std::vector<u64> ids) {
     u64 mx = 0;
 #pragma omp parallel for reduction(max : mx) schedule(static)
@@ -193,19 +224,23 @@ void finish_ids(const Compactor& C, gpm_csr* out) {
 }
 
 void csr_from_pairs(const std::vector<u64>& a, const std::vector<u64>& b, gpm_csr* out) {
-  std::vector<u64> ids;
-  ids.reserve(a.size() * 2);
-  ids.insert(ids.end(), a.begin(), a.end());
-  ids.insert(ids.end(), b.begin(), b.end());
+  static const bool tr = std::getenv("GPM_IO_TRACE") != nullptr;
+  double t0 = omp_get_wtime();
+  auto mark = [&](const char* w) {
+    if (tr) std::fprintf(stderr, "[gpm io] %-12s %.3f s\n", w, omp_get_wtime() - t0);
+  };
   Compactor C;
-  C.build(std::move(ids));
+  C.build2(a, b);
+  mark("compact");
   std::vector<u32> su(a.size()), sv(a.size());
 #pragma omp parallel for schedule(static)
   for (long long i = 0; i < (long long)a.size(); ++i) {
     su[i] = C(a[i]);
     sv[i] = C(b[i]);
   }
+  mark("map");
   build_csr((u32)C.uniq.size(), su, sv, out);
+  mark("build_csr");
   out->labels = nullptr;
   finish_ids(C, out);
 }
@@ -226,7 +261,13 @@ inline u64 mix64(u64 x) {
 // number = lines of the earlier ranges + its rank inside its own range), as
 // the reference's sequential loop would (graph_io.hpp:88-98).
 void load_edge_list(const char* path, gpm_csr* out) {
+  static const bool tr = std::getenv("GPM_IO_TRACE") != nullptr;
+  const double t0 = omp_get_wtime();
+  auto mark = [&](const char* w) {
+    if (tr) std::fprintf(stderr, "[gpm io] %-12s %.3f s\n", w, omp_get_wtime() - t0);
+  };
   std::string buf = read_file(path);
+  mark("read");
   const char* base = buf.data();
   const char* end = base + buf.size();
   const int T = std::max(1, std::min(omp_get_max_threads(), (int)(buf.size() >> 20) + 1));
@@ -271,6 +312,7 @@ void load_edge_list(const char* path, gpm_csr* out) {
     }
     nlines[t] = ln;
   }
+  mark("parse");
   u64 before = 0;
   for (int t = 0; t < T; ++t) {
     if (bad[t]) {
@@ -293,6 +335,7 @@ void load_edge_list(const char* path, gpm_csr* out) {
     std::vector<u64>().swap(A[t]);
     std::vector<u64>().swap(B[t]);
   }
+  mark("concat");
   csr_from_pairs(a, b, out);
 }
 

@@ -160,6 +160,7 @@ struct LabelSubsetFsmApp {
       if (lab[i] >= 2) return true;  // dense label ranks: the test graph's labels are 0..L-1
     return p.count < p.sigma || p.support < p.sigma;
   }
+  static u64 support_of(const fsm_engine::PatternInfo& p) { return p.support; }
 };
 
 // Embedding-count support instead of MNI (no domains): toPrune = count < sigma.
@@ -172,6 +173,7 @@ struct CountSupportFsmApp {
     return fsm_engine::edge_to_add<LEV>(e, q, w, r);
   }
   static bool to_prune(const fsm_engine::PatternInfo& p) { return p.count < p.sigma; }
+  static u64 support_of(const fsm_engine::PatternInfo& p) { return p.count; }
 };
 
 }  // namespace
