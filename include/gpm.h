@@ -218,7 +218,9 @@ enum {
   GPM_PATH_FSM_FUSED_LAST = 1u << 10,  /* FSM last level: domain pass fused        */
   GPM_PATH_FSM_GROUPED = 1u << 11,     /* FSM passes over parents grouped by code  */
   GPM_PATH_FSM_FAN = 1u << 12,         /* FSM last level: fan-out pass (dense slots) */
-  GPM_PATH_FSM_SPARSE = 1u << 13       /* FSM sparse (sorted-key) domains            */
+  GPM_PATH_FSM_SPARSE = 1u << 13,     /* FSM sparse (sorted-key) domains            */
+  GPM_PATH_CF_LOCAL = 1u << 14,       /* k-CL (k >= 4) counts on per-root local rows */
+  GPM_PATH_CF_LOCAL_BIG = 1u << 15    /* ... CTA-per-root kernel (out-degree > 32)   */
 };
 int gpm_result_stats(const gpm_result* r, gpm_stats* out);
 

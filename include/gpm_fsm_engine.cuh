@@ -773,15 +773,16 @@ __device__ __forceinline__ u32 smap_get(unsigned long long* mkey, u32* mslot, u3
           }
         }
         __threadfence_block();
-        *(volatile u32*)(mslot + h) = val;
+        atomicExch(mslot + h, val);  // publish (atomics: the flag is not a data race)
         return val;
       }
       k = prev;
     }
     if (k == code) {
       u32 val;
-      while ((val = *(volatile u32*)(mslot + h)) == kSlotPending) {
+      while ((val = atomicAdd(mslot + h, 0u)) == kSlotPending) {
       }
+      __threadfence_block();
       return val;
     }
     h = (h + 1) & (mcap - 1);

@@ -44,7 +44,7 @@ class Config(C.Structure):
 # gpm_stats.paths bits (include/gpm.h)
 PATH_GENERIC, PATH_CF_EDGE_CHUNK, PATH_CF_SIBLINGS, PATH_MC3_WARP, PATH_MC3_BLOCK, PATH_MC3_MULTITILE, \
     PATH_MC4_STAGED, PATH_MC4_HBM_SETS, PATH_PLANNER_CHUNKS, PATH_FSM_ROUNDS, PATH_FSM_FUSED_LAST, \
-    PATH_FSM_GROUPED, PATH_FSM_FAN, PATH_FSM_SPARSE = (1 << i for i in range(14))
+    PATH_FSM_GROUPED, PATH_FSM_FAN, PATH_FSM_SPARSE, PATH_CF_LOCAL, PATH_CF_LOCAL_BIG = (1 << i for i in range(16))
 
 
 class Stats(C.Structure):

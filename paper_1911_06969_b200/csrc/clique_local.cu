@@ -1,0 +1,793 @@
+// clique_local.cu — k-CL (k >= 4) counting on the degree-ordered DAG with the
+// levels >= 2 evaluated on per-root local adjacency rows.
+//
+// Reference semantics: Listing 3 under Alg. 1 / Alg. 2
+// (PAPER.md:688-772): parents at level 1 are the DAG edges (v0, v1),
+// candidates at every level are the out-list of the last vertex, and to_add
+// accepts u iff u is an out-neighbour of every earlier vertex.  For a root v0
+// every accepted vertex lies in N+(v0), so the whole subtree of embeddings
+// rooted at v0 lives in the local graph induced on N+(v0):
+//
+//   level 1 (edges -> triangles): every candidate u in N+(v1) is probed
+//     against an on-chip hash of N+(v0) (the same per-candidate probe as the
+//     edge-chunk kernel); an accepted u sets bit j(u) of row[v1], where j is
+//     u's position in N+(v0).  row[v1] is therefore exactly the set of
+//     children of the parent (v0, v1), i.e. {u in N+(v1) : u in N+(v0)}.
+//   level l >= 2: the candidates of a parent (v0, v1, .., x) are N+(x); those
+//     outside N+(v0) were already rejected by the level-1 probe of the edge
+//     (v0, x) (row[x] holds exactly the ones inside), so the children are
+//     S(parent) & row[x], evaluated 32 candidates per AND, where S(parent)
+//     is the parent's own child set (= the common out-neighbours of its
+//     vertices inside N+(v0)).
+//
+// Every level's size, candidate count (sum of out-degrees of the parents'
+// last vertices) and SURVEY §8d algorithmic bytes are the engine's exactly;
+// no level is materialised in HBM, so the inspection / execution passes,
+// the sibling-group last level and their host round trips disappear.
+//
+// Work split: roots with out-degree <= 32 are packed into warp items (the
+// roots whose first out-edge lies in one 32-edge block of the DAG CSR: <= 32
+// roots, <= 63 edges, one 32-bit row per edge); roots with out-degree in
+// (32, kBigMax] and the (at most two) roots cut by the slice bounds go to a
+// CTA-per-root kernel with rows of ceil(d/32) words in shared memory.
+#include <cstdlib>
+
+#include "gpm_apps.cuh"
+
+namespace gpm {
+namespace engine {
+
+namespace {
+
+constexpr u32 kBigMax = 1024;     // largest out-degree handled on chip
+constexpr u32 kMidMax = 128;      // largest out-degree of a warp item
+constexpr int kSmallThreads = 256;
+constexpr int kBigThreads = 128;
+constexpr int kAcc = 2 * kMaxLevels;  // [0, kMaxLevels): children per level; [kMaxLevels, ..): candidates per level
+
+struct LocalArgs {
+  DevGraph g;
+  const u32* src;       // level-1 v0 per DAG edge (absolute edge index)
+  u64 lo, hi;           // level-1 slice = DAG edge range
+  u64 blo, nblk;        // 32-edge blocks [blo, blo + nblk)
+  u32* item_root;       // per block: smallest small root whose first edge lies in the block, or ~0
+  u32* big;             // roots for the CTA kernel
+  unsigned long long* nbig;
+  u32* mid;             // roots of out-degree (32, 64] (one warp item each, after the blocks)
+  unsigned long long* nmid;
+  u32* mid2;            // roots of out-degree (64, 128]
+  unsigned long long* nmid2;
+  unsigned long long* ctr;   // [0] small-item grabs, [1] big-root grabs, [2] medium-root grabs
+  unsigned long long* acc;   // [3][kAcc]: small, medium, big
+  unsigned long long* total; // last-level count (engine d_total)
+  int k;
+};
+
+__device__ __forceinline__ u32 hb_insert_at(u32* T, u32 sh, u32 bmask, u32 v) {
+  u32 b = (v * kHashMul) >> sh;
+  for (;;) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const u32 old = atomicCAS(T + 4 * b + q, kEmpty, v);
+      if (old == kEmpty || old == v) return 4 * b + q;
+    }
+    b = (b + 1) & bmask;
+  }
+}
+
+// slot of v in the bucketised table, or ~0
+__device__ __forceinline__ u32 hb_find(const u32* T, u32 sh, u32 bmask, u32 v) {
+  u32 b = (v * kHashMul) >> sh;
+  for (;;) {
+    const uint4 x = *reinterpret_cast<const uint4*>(T + 4 * b);
+    if (x.x == v || x.y == v || x.z == v || x.w == v)
+      return 4 * b + (x.x == v ? 0u : x.y == v ? 1u : x.z == v ? 2u : 3u);
+    if (x.w == kEmpty) return ~0u;
+    b = (b + 1) & bmask;
+  }
+}
+
+// Classifies the roots of the slice: a root starts at edge e when e is its
+// first out-edge (or e == lo for a root cut by the slice start).
+__global__ void local_prep_kernel(LocalArgs a) {
+  const u64 np = a.hi - a.lo;
+  for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < np; t += (u64)gridDim.x * blockDim.x) {
+    const u64 e = a.lo + t;
+    const u32 v = ldg(a.src + e);
+    if (e != a.lo && ldg(a.src + e - 1) == v) continue;
+    const u64 ob = ldg(a.g.off + v), oe = ldg(a.g.off + v + 1);
+    const u64 d = oe - ob;
+    if (ob < a.lo || oe > a.hi || d > kMidMax) {
+      const unsigned long long i = atomicAdd(a.nbig, 1ull);
+      a.big[i] = v;
+    } else if (d > 64) {
+      const unsigned long long i = atomicAdd(a.nmid2, 1ull);
+      a.mid2[i] = v;
+    } else if (d > 32) {
+      const unsigned long long i = atomicAdd(a.nmid, 1ull);
+      a.mid[i] = v;
+    } else {
+      atomicMin(a.item_root + (e / 32 - a.blo), v);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp items.  An item is either the small roots (out-degree <= 32) whose
+// first out-edge lies in one 32-edge block of the DAG CSR (<= 32 roots,
+// <= 63 edges, 1-word rows), or one medium root (out-degree in (32, 128],
+// rows of <= 4 words).  Per warp in shared memory: a bucketised hash of the
+// item's keys (u << 5 | root slot) -> local position, the rows, and the
+// candidate stream's descriptors.  The stream (the concatenated out-lists of
+// the item's edges) is walked 32 positions per window; a per-window bitmap of
+// entry starts (built once per item) maps lanes to entries with two POPCs,
+// and keys that all sit in their primary bucket are probed with ONE LDS.128
+// (items whose insert overflowed a bucket, or whose stream exceeds the window
+// bitmap, take the general loop: OR-reduction mapping + chained probe).
+constexpr u32 ilog2(u32 x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+
+template <int KMAX, int NB, int WMAX, int WIN = 256, int UNROLL = 4, int MINB = 4>
+struct WarpCfg {
+  static constexpr int kKeys = KMAX;     // edges (keys) per item
+  static constexpr int kBuckets = NB;    // 4 slots each
+  static constexpr int kWords = WMAX;    // row words per edge
+  static constexpr int kWin = WIN;       // stream windows with a start bitmap (32 positions each)
+  static constexpr int kUnroll = UNROLL; // windows per loop step (loads in flight per warp)
+  static constexpr int kMinBlocks = MINB;
+};
+using SmallCfg = WarpCfg<64, 128, 2, 128>;   // small-root blocks (1-word rows) and roots of out-degree <= 64
+using MidCfg = WarpCfg<128, 256, 4, 256, 4, 2>;    // roots of out-degree in (64, 128]
+
+template <class C>
+struct WarpSmem {
+  uint4 T[C::kBuckets];           // keys (kEmpty = free)
+  u32 F[256];                     // 8192-bit filter of the keys (word = hash bits 16..23, bit = 27..31)
+  u8 V[C::kBuckets * 4];          // local position of the key in its root's list
+  u32 rows[C::kKeys * C::kWords];
+  __align__(16) u32 wm[C::kWin + C::kUnroll];  // per window: bit p = an entry starts at window position p
+  uint2 ent[C::kKeys];            // per entry: (cb - exclusive start) mod 2^32, root slot
+  u8 ekk[C::kKeys];               // per entry: its edge kk
+  u32 ex[C::kKeys + 32];          // per entry: exclusive start, ~0 past the entries
+  u32 dp[C::kKeys];               // per edge: out-degree of its v1
+  u8 base[C::kKeys];              // per edge: first edge index of its root
+  u64 rb[32];                     // per root slot: first out-edge
+  u32 rk[64];                     // per root slot: first edge index; ~0 past the roots
+  unsigned long long acc[kAcc];   // levels >= 2 (generic DFS)
+};
+
+// children of the level-1 parent kk: row words R[0..W); levels >= 2 below it
+template <int WMAX>
+__device__ __forceinline__ void count_subtree(const u32* rows, const u32* dp, u32 kbase, u32 kk, u32 W, int last,
+                                              unsigned long long& l2, unsigned long long& c2,
+                                              unsigned long long* sacc) {
+  u32 S[WMAX];
+#pragma unroll
+  for (int w = 0; w < WMAX; ++w) S[w] = w < (int)W ? rows[kk * W + w] : 0u;
+  if (last == 2) {
+    // 4-CL: the children's children are counted, not visited
+#pragma unroll
+    for (int w = 0; w < WMAX; ++w) {
+      u32 m = S[w];
+      while (m) {
+        const u32 j = kbase + w * 32 + __ffs(m) - 1;
+        m &= m - 1;
+        c2 += dp[j];
+        u32 cnt = 0;
+#pragma unroll
+        for (int x = 0; x < WMAX; ++x)
+          if (x < (int)W) cnt += __popc(S[x] & rows[j * W + x]);
+        l2 += cnt;
+      }
+    }
+    return;
+  }
+  // k >= 5: DFS over the child sets (per level W words, local memory)
+  u32 set[kMaxLevels][WMAX], cw[kMaxLevels], cb[kMaxLevels];
+#pragma unroll
+  for (int w = 0; w < WMAX; ++w) set[1][w] = S[w];
+  int lev = 1;
+  cw[1] = 0;
+  cb[1] = S[0];
+  while (lev >= 1) {
+    while (cb[lev] == 0 && cw[lev] + 1 < W) cb[lev] = set[lev][++cw[lev]];
+    if (cb[lev] == 0) {
+      --lev;
+      continue;
+    }
+    const u32 j = kbase + cw[lev] * 32 + __ffs(cb[lev]) - 1;
+    cb[lev] &= cb[lev] - 1;
+    atomicAdd(sacc + kMaxLevels + lev + 1, (unsigned long long)dp[j]);
+    const bool deeper = lev + 1 < last;
+    u32 cnt = 0;
+    for (u32 w = 0; w < W; ++w) {
+      const u32 x = set[lev][w] & rows[j * W + w];
+      cnt += __popc(x);
+      if (deeper) set[lev + 1][w] = x;
+    }
+    if (cnt) atomicAdd(sacc + lev + 1, (unsigned long long)cnt);
+    if (deeper && cnt) {
+      ++lev;
+      cw[lev] = 0;
+      cb[lev] = set[lev][0];
+    }
+  }
+}
+
+// MID = false: items [0, nblk) are small-root blocks, then one item per root
+// of out-degree in (32, 64] (a.mid); MID = true: one item per root of
+// out-degree in (64, 128] (a.mid2).
+template <class C, bool MID>
+__global__ void __launch_bounds__(kSmallThreads, C::kMinBlocks) local_warp_kernel(LocalArgs a) {
+  constexpr int NW = kSmallThreads / 32;
+  extern __shared__ __align__(16) unsigned char wsm[];
+  WarpSmem<C>* const s_w = reinterpret_cast<WarpSmem<C>*>(wsm);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const u32 lt = lanemask_lt(), lemask = lt | (1u << lane);
+  WarpSmem<C>& S = s_w[wid];
+  u32* const Tw = reinterpret_cast<u32*>(S.T);
+  constexpr u32 sh = 32 - ilog2(C::kBuckets);
+  constexpr u32 bmask = C::kBuckets - 1;
+  for (int i = lane; i < kAcc; i += 32) S.acc[i] = 0;
+  for (int i = lane; i < C::kBuckets; i += 32) S.T[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+  for (int i = lane; i < 256; i += 32) S.F[i] = 0;
+  S.rk[32 + lane] = 0xffffffffu;
+  __syncwarp();
+  const DevGraph& g = a.g;
+  const int last = a.k - 2;
+  unsigned long long l1 = 0, c1 = 0, l2 = 0, c2 = 0;
+  const u64 nblk = MID ? 0 : a.nblk;
+  const u64 nitems = nblk + *reinterpret_cast<volatile unsigned long long*>(MID ? a.nmid2 : a.nmid);
+  const u32* const rootlist = MID ? a.mid2 : a.mid;
+  constexpr u64 kGrab = 4;
+  u64 grab = 0, grab_left = 0;
+  for (;;) {
+    if (grab_left == 0) {
+      u64 it_ = 0;
+      if (lane == 0) it_ = atomicAdd(a.ctr + (MID ? 2 : 0), kGrab);
+      grab = __shfl_sync(0xffffffffu, it_, 0);
+      grab_left = kGrab;
+    }
+    const u64 item = grab++;
+    --grab_left;
+    if (item >= nitems) break;
+    // ---- the item's roots -> slots (rb, rk = degree then exclusive start)
+    u32 nr = 0;
+    if (item >= nblk) {
+      if (lane == 0) {
+        const u32 v = rootlist[item - nblk];
+        S.rb[0] = ldg(g.off + v);
+        S.rk[0] = (u32)(ldg(g.off + v + 1) - S.rb[0]);
+      }
+      nr = 1;
+    } else {
+      const u32 ra = a.item_root[item];
+      if (ra == 0xffffffffu) continue;
+      const u64 bend = (a.blo + item + 1) * 32;
+      for (u32 vb = ra;; vb += 32) {
+        const u32 v = vb + lane;
+        u64 ob = ~0ull, oe = 0;
+        if (v < g.n) {
+          ob = ldg(g.off + v);
+          oe = ldg(g.off + v + 1);
+        }
+        const bool q = ob < bend && oe > ob && oe - ob <= 32 && ob >= a.lo && oe <= a.hi;
+        const u32 qm = __ballot_sync(0xffffffffu, q);
+        if (q) {
+          const u32 s = nr + __popc(qm & lt);
+          S.rb[s] = ob;
+          S.rk[s] = (u32)(oe - ob);
+        }
+        nr += __popc(qm);
+        if (__ballot_sync(0xffffffffu, ob >= bend)) break;
+      }
+    }
+    __syncwarp();
+    u32 rd = lane < nr ? S.rk[lane] : 0u, kin = rd;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 t = __shfl_up_sync(0xffffffffu, kin, o);
+      if (lane >= o) kin += t;
+    }
+    const u32 K = __shfl_sync(0xffffffffu, kin, 31);
+    const u32 W = (K + 31) / 32 > 1 && item >= nblk ? (K + 31) / 32 : 1u;  // blocks: 1-word rows
+    __syncwarp();
+    S.rk[lane] = lane < nr ? kin - rd : 0xffffffffu;
+    __syncwarp();
+    // ---- keys (u << 5 | slot) -> local position; per-edge out-lists
+    u32 R = 0, nz = 0, run = 0;
+    bool ovf = false;
+    u32 kpos[C::kKeys / 32], kfw[C::kKeys / 32];
+#pragma unroll
+    for (int rr = 0; rr < C::kKeys / 32; ++rr) {
+      const u32 kb = rr * 32;
+      kpos[rr] = ~0u;
+      kfw[rr] = 0;
+      if (kb >= K) continue;  // warp-uniform
+      u32 r = 0;
+      if (item < nblk) {
+        const u32 dd = S.rk[R + 1 + lane] - kb;
+        const u32 starts = __reduce_or_sync(0xffffffffu, dd < 32u ? (1u << dd) : 0u);
+        r = min(R + __popc(starts & lemask), nr - 1);
+        R += __popc(starts);
+      }
+      const u32 kk = kb + lane;
+      u32 dpv = 0;
+      u64 cb = 0;
+      if (kk < K) {
+        const u32 kbase = S.rk[r], j = kk - kbase;
+        const u32 w = ldg(g.col + S.rb[r] + j);
+        const u32 key = (w << 5) | r;
+        const u32 hv = key * kHashMul;
+        atomicOr(S.F + ((hv >> 16) & 255u), 1u << (hv >> 27));  // filter index: hash bits 16..23, 27..31
+        kfw[rr] = (hv >> 16) & 255u;
+        u32 b = hv >> sh;
+        for (u32 probe = 0;; ++probe) {
+          u32 q = 0;
+          for (; q < 4; ++q) {
+            const u32 old = atomicCAS(Tw + 4 * b + q, kEmpty, key);
+            if (old == kEmpty) break;
+          }
+          if (q < 4) {
+            kpos[rr] = 4 * b + q;
+            break;
+          }
+          ovf = true;
+          b = (b + 1) & bmask;
+        }
+        S.V[kpos[rr]] = (u8)j;
+        S.base[kk] = (u8)kbase;
+        cb = ldg(g.off + w);
+        dpv = (u32)(ldg(g.off + w + 1) - cb);
+        S.dp[kk] = dpv;
+#pragma unroll
+        for (int w2 = 0; w2 < C::kWords; ++w2)
+          if (w2 < (int)W) S.rows[kk * W + w2] = 0;
+      }
+      u32 incl = dpv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const u32 nzm = __ballot_sync(0xffffffffu, dpv > 0);
+      if (dpv > 0) {
+        const u32 qi = nz + __popc(nzm & lt);
+        const u32 ex = run + incl - dpv;
+        S.ex[qi] = ex;
+        S.ent[qi] = make_uint2((u32)(cb - (u64)ex), r);  // col index = (.x + position) mod 2^32 (m < 2^32)
+        S.ekk[qi] = (u8)kk;
+      }
+      nz += __popc(nzm);
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    const u32 total = run;
+    const u32 nwin = (total + 31) >> 5;
+    const bool fast = !__any_sync(0xffffffffu, ovf) && nwin <= (u32)C::kWin;
+    if (fast) {
+      for (u32 i = lane; i < nwin + C::kUnroll; i += 32) S.wm[i] = 0;
+    }
+    S.ex[nz + lane] = 0xffffffffu;
+    __syncwarp();
+    if (fast) {
+      for (u32 i = lane; i < nz; i += 32) {
+        const u32 ex = S.ex[i];
+        atomicOr(S.wm + (ex >> 5), 1u << (ex & 31));
+      }
+    }
+    __syncwarp();
+    // ---- level 1: every candidate u of the stream probes (u, slot)
+    auto hit = [&](u32 key, u32 e) {
+      u32 b = (key * kHashMul) >> sh;
+      for (;;) {
+        const uint4 x = S.T[b];
+        if (x.x == key || x.y == key || x.z == key || x.w == key) {
+          const u32 j = S.V[4 * b + (x.x == key ? 0u : x.y == key ? 1u : x.z == key ? 2u : 3u)], kk = S.ekk[e];
+          atomicOr(S.rows + kk * W + (j >> 5), 1u << (j & 31));
+          return;
+        }
+        if (x.w == kEmpty) return;
+        b = (b + 1) & bmask;
+      }
+    };
+    if (fast) {
+      // a lane past the stream probes key 0xfffffffe (vertex 2^27 - 1, slot
+      // 30): no vertex has that id (n < 2^27) and it is not kEmpty
+      static_assert(C::kUnroll == 4, "one LDS.128 of window masks per step");
+      u32 P = 0xffffffffu;  // entry holding the position before the window
+      const u32* const col = g.col;
+      for (u32 it = 0; it < nwin; it += 4) {
+        const uint4 w4 = *reinterpret_cast<const uint4*>(S.wm + it);
+        const u32 wq[4] = {w4.x, w4.y, w4.z, w4.w};
+        const u32 jl = it * 32 + lane;
+        u32 key[4], eq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          eq[q] = P + __popc(wq[q] & lemask);
+          P += __popc(wq[q]);
+          u32 u = 0x07ffffffu, sl = 30;
+          if (jl + 32 * q < total) {
+            const uint2 d = S.ent[eq[q]];
+            u = ldg(col + (u32)(d.x + jl + 32 * q));
+            sl = d.y;
+          }
+          key[q] = (u << 5) | sl;
+        }
+        // filter bit first (one LDS.32 per window); the bucket (LDS.128,
+        // ~4x the shared-memory wavefronts) only for filter-positive lanes,
+        // which are rare: any positive lane re-probes its 4 keys exactly
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const u32 hv = key[q] * kHashMul;
+          any |= (S.F[__byte_perm(hv, 0, 0x4442)] >> (hv >> 27)) & 1u;
+        }
+        if (any) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) hit(key[q], eq[q]);
+        }
+      }
+    } else {
+      u32 P = 0;
+      for (u32 jb = 0; jb < total; jb += 32) {
+        const u32 d = S.ex[P + 1 + lane] - jb;
+        const u32 st = __reduce_or_sync(0xffffffffu, d < 32u ? (1u << d) : 0u);
+        const u32 myp = P + __popc(st & lemask);
+        P += __popc(st);
+        const u32 jj = jb + lane;
+        if (jj < total) {
+          const uint2 dd = S.ent[myp];
+          const u32 u = ldg(g.col + (u32)(dd.x + jj));
+          hit((u << 5) | dd.y, myp);
+        }
+      }
+    }
+    __syncwarp();
+    // ---- levels >= 2 on the rows
+    for (u32 kk = lane; kk < K; kk += 32) {
+      const u32 kbase = S.base[kk];
+      u32 n1 = 0;
+#pragma unroll
+      for (int w = 0; w < C::kWords; ++w)
+        if (w < (int)W) n1 += __popc(S.rows[kk * W + w]);
+      l1 += n1;
+      c1 += S.dp[kk];
+      if (n1) count_subtree<C::kWords>(S.rows, S.dp, kbase, kk, W, last, l2, c2, S.acc);
+    }
+    __syncwarp();
+    // ---- free the item's keys and filter words
+#pragma unroll
+    for (int rr = 0; rr < C::kKeys / 32; ++rr)
+      if (kpos[rr] != ~0u) {
+        Tw[kpos[rr]] = kEmpty;
+        S.F[kfw[rr]] = 0;
+      }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+    l2 += __shfl_xor_sync(0xffffffffu, l2, o);
+    c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    S.acc[1] += l1;
+    S.acc[kMaxLevels + 1] += c1;
+    S.acc[2] += l2;
+    S.acc[kMaxLevels + 2] += c2;
+  }
+  __syncwarp();
+  unsigned long long* const gacc = a.acc + (MID ? kAcc : 0);  // [1]: the (64, 128] roots
+  for (int i = lane; i < kAcc; i += 32) {
+    const unsigned long long x = S.acc[i];
+    if (!x) continue;
+    if (i == last) atomicAdd(a.total, x);
+    else atomicAdd(gacc + i, x);
+  }
+}
+
+// Dynamic shared-memory layout of local_big_kernel (32-bit word offsets):
+// hash keys (cap), u16 local positions (cap), rows (dmax x ceil(dmax/32)),
+// per-edge out-degrees, stream starts (+33 sentinels), list addresses (u64),
+// stream entry -> edge.
+struct BigLayout {
+  u32 cap, T, V, rows, dp, ex, cp, inf, words;
+  __host__ __device__ explicit BigLayout(u32 dmax) {
+    cap = 128;
+    while (cap < 4 * dmax) cap <<= 1;
+    T = 0;
+    V = cap;
+    rows = V + cap / 2;
+    dp = rows + dmax * ((dmax + 31) / 32);
+    ex = dp + dmax;
+    cp = (ex + dmax + 33 + 1) & ~1u;
+    inf = cp + 2 * dmax;
+    words = inf + dmax;
+  }
+};
+
+// One root per CTA (out-degree in (32, kBigMax], or cut by the slice bounds):
+// hash of N+(v0) (key u -> local position), ceil(d/32)-word rows, the
+// root's candidate stream split evenly over the warps.
+__global__ void __launch_bounds__(kBigThreads) local_big_kernel(LocalArgs a, u32 dmax) {
+  extern __shared__ __align__(16) u32 sm[];
+  constexpr int NW = kBigThreads / 32;
+  const BigLayout L(dmax);
+  u32* const T = sm + L.T;
+  uint16_t* const V = reinterpret_cast<uint16_t*>(sm + L.V);
+  u32* const rows = sm + L.rows;
+  u32* const sdp = sm + L.dp;
+  u32* const sex = sm + L.ex;
+  u64* const scp = reinterpret_cast<u64*>(sm + L.cp);
+  u32* const sinf = sm + L.inf;
+  __shared__ u32 s_wsum[NW + 1];
+  __shared__ u64 s_item;
+  __shared__ unsigned long long s_acc[kAcc];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u32 lt = lanemask_lt(), lemask = lt | (1u << lane);
+  const DevGraph& g = a.g;
+  const int last = a.k - 2;
+  for (int i = tid; i < kAcc; i += kBigThreads) s_acc[i] = 0;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_item = atomicAdd(a.ctr + 1, 1ull);
+    __syncthreads();
+    const u64 item = s_item;
+    if (item >= *reinterpret_cast<volatile unsigned long long*>(a.nbig)) break;
+    const u32 v0 = a.big[item];
+    const u64 ob = ldg(g.off + v0), oe = ldg(g.off + v0 + 1);
+    const u32 d = (u32)(oe - ob);
+    const u32 W = (d + 31) / 32;
+    // counted edges [k0, k1) (a root cut by the slice bounds); every edge's
+    // row is built, since a child's position in N+(v0) (id order) may lie
+    // before or after its parent's
+    const u32 k0 = (u32)(max(ob, a.lo) - ob), k1 = (u32)(min(oe, a.hi) - ob);
+    u32 c = 128;
+    while (c < 4 * d) c <<= 1;
+    const u32 sh = 32 - (31 - __clz(c / 4)), bmask = c / 4 - 1;
+    for (u32 i = tid * 4; i < c; i += 4 * kBigThreads) *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    for (u32 i = tid; i < d * W; i += kBigThreads) rows[i] = 0;
+    __syncthreads();
+    // stage keys, per-edge out-degrees and list starts
+    for (u32 kk = tid; kk < d; kk += kBigThreads) {
+      const u32 w = ldg(g.col + ob + kk);
+      V[hb_insert_at(T, sh, bmask, w)] = (uint16_t)kk;
+      const u64 cb = ldg(g.off + w);
+      sdp[kk] = (u32)(ldg(g.off + w + 1) - cb);
+      scp[kk] = cb;
+    }
+    __syncthreads();
+    // stream entries: edges kk in [0, d) with non-empty lists, in order
+    // (one warp compacts; d <= kBigMax)
+    if (wid == 0) {
+      u32 nz = 0, run = 0;
+      for (u32 kb = 0; kb < d; kb += 32) {
+        const u32 kk = kb + lane;
+        const u32 dp = kk < d ? sdp[kk] : 0u;
+        u32 incl = dp;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const u32 nzm = __ballot_sync(0xffffffffu, dp > 0);
+        // scp is rewritten in place for entries <= kk (nz <= kk)
+        u64 cb = kk < d ? scp[kk] : 0;
+        __syncwarp();
+        if (dp > 0) {
+          const u32 qi = nz + __popc(nzm & lt);
+          const u32 ex = run + incl - dp;
+          sex[qi] = ex;
+          scp[qi] = reinterpret_cast<u64>(g.col) + 4 * (cb - (u64)ex);
+          sinf[qi] = kk;
+        }
+        __syncwarp();
+        nz += __popc(nzm);
+        run += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      for (u32 i = nz + lane; i < nz + 33; i += 32) sex[i] = 0xffffffffu;
+      if (lane == 0) {
+        s_wsum[0] = run;
+        s_wsum[1] = nz;
+      }
+    }
+    __syncthreads();
+    const u32 total = s_wsum[0], nzt = s_wsum[1];
+    // ---- level 1: warp w streams candidates [t0, t1)
+    {
+      const u32 t0 = (u32)((u64)total * wid / NW), t1 = (u32)((u64)total * (wid + 1) / NW);
+      if (t0 < t1) {
+        // P = the entry holding t0: last entry with sex <= t0
+        u32 l_ = 0, h_ = nzt;
+        while (h_ - l_ > 1) {
+          const u32 mid = (l_ + h_) >> 1;
+          if (sex[mid] <= t0) l_ = mid;
+          else h_ = mid;
+        }
+        u32 P = l_;
+        // first map_step may see starts at P (already counted) only via d < 32
+        auto map_step = [&](u32 jb) -> u32 {
+          const u32 dd = sex[P + 1 + lane] - jb;
+          const u32 st = __reduce_or_sync(0xffffffffu, dd < 32u ? (1u << dd) : 0u);
+          const u32 myp = P + __popc(st & lemask);
+          P += __popc(st);
+          return myp;
+        };
+        for (u32 jb = t0; jb < t1; jb += 32) {
+          const u32 myp = map_step(jb);
+          const u32 jj = jb + lane;
+          if (jj < t1) {
+            const u32 u = ldg(reinterpret_cast<const u32*>(scp[myp]) + jj);
+            const u32 pos = hb_find(T, sh, bmask, u);
+            if (pos != ~0u) {
+              const u32 j = V[pos], kk = sinf[myp];
+              atomicOr(rows + (size_t)kk * W + (j >> 5), 1u << (j & 31));
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- levels: counted edges [k0, k1)
+    for (u32 kk = k0 + tid; kk < k1; kk += kBigThreads) {
+      const u32* R0 = rows + (size_t)kk * W;
+      u32 S1 = 0;
+      for (u32 w = 0; w < W; ++w) S1 += __popc(R0[w]);
+      atomicAdd(s_acc + kMaxLevels + 1, (unsigned long long)sdp[kk]);
+      if (S1) atomicAdd(s_acc + 1, (unsigned long long)S1);
+      if (last < 2 || !S1) continue;
+      // DFS over the local rows (sets of W words, in local memory)
+      u32 set[kMaxLevels][kBigMax / 32];
+      u32 cw[kMaxLevels], cb_[kMaxLevels];
+      int lev = 1;
+      for (u32 w = 0; w < W; ++w) set[1][w] = R0[w];
+      cw[1] = 0;
+      cb_[1] = set[1][0];
+      while (lev >= 1) {
+        while (cb_[lev] == 0 && cw[lev] + 1 < W) cb_[lev] = set[lev][++cw[lev]];
+        if (cb_[lev] == 0) {
+          --lev;
+          continue;
+        }
+        const u32 j = cw[lev] * 32 + __ffs(cb_[lev]) - 1;
+        cb_[lev] &= cb_[lev] - 1;
+        atomicAdd(s_acc + kMaxLevels + lev + 1, (unsigned long long)sdp[j]);
+        const u32* Rj = rows + (size_t)j * W;
+        const bool deeper = lev + 1 < last;
+        u32 cnt = 0;
+        for (u32 w = 0; w < W; ++w) {
+          const u32 x = set[lev][w] & Rj[w];
+          cnt += __popc(x);
+          if (deeper) set[lev + 1][w] = x;
+        }
+        if (cnt) atomicAdd(s_acc + lev + 1, (unsigned long long)cnt);
+        if (deeper && cnt) {
+          ++lev;
+          cw[lev] = 0;
+          cb_[lev] = set[lev][0];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < kAcc; i += kBigThreads) {
+    const unsigned long long x = s_acc[i];
+    if (!x) continue;
+    if (i == last) atomicAdd(a.total, x);
+    else atomicAdd(a.acc + 2 * kAcc + i, x);
+  }
+}
+
+
+}  // namespace
+
+template <class C, bool MID>
+size_t launch_warp(Ctx& c, LocalArgs& a, u64 max_items_per8, const char* name) {
+  auto kern = local_warp_kernel<C, MID>;
+  const size_t smem = sizeof(WarpSmem<C>) * (kSmallThreads / 32);
+  static std::atomic<int> occ{0};
+  const int o = cached_occupancy(occ, [&] {
+    GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int r = 0;
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, kSmallThreads, smem));
+    return r;
+  });
+  const u64 blocks = std::max<u64>(1, std::min<u64>((u64)c.sms * o, max_items_per8));
+  size_t rec = c.tl->begin(name, 0.0);
+  kern<<<(unsigned)blocks, kSmallThreads, smem, c.s>>>(a);
+  GPM_CUDA(cudaGetLastError());
+  c.tl->end(rec);
+  return rec;
+}
+
+// k-CL (k >= 4) count of the level-1 slice [slo, shi) on local rows; false
+// when the preconditions do not hold (the caller runs the edge-chunk path).
+bool cf_local_roots(Ctx& c, const u32* l1_src, u64 slo, u64 shi) {
+  if (c.k < 4 || c.list_fn || !c.G->oriented || c.G->max_deg > kBigMax || c.G->n >= (1u << 27) ||
+      c.G->m >= (u64(1) << 32) ||
+      std::getenv("GPM_CF_NOLOCAL"))
+    return false;
+  const u64 np = shi - slo;
+  Stats& st = *c.st;
+  st.paths |= GPM_PATH_CF_LOCAL;
+  const u64 blo = slo / 32, nblk = (shi - 1) / 32 - blo + 1;
+  const u64 bigcap = np / 33 + 3;
+  DBuf<u32> item(nblk, c.s), big(bigcap, c.s), mid(bigcap, c.s), mid2(bigcap, c.s);
+  constexpr int kCtl = 8;
+  DBuf<unsigned long long> ctl(kCtl + 3 * kAcc, c.s);
+  GPM_CUDA(cudaMemsetAsync(item.get(), 0xff, sizeof(u32) * nblk, c.s));
+  GPM_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(unsigned long long) * (kCtl + 3 * kAcc), c.s));
+  LocalArgs a{};
+  a.g = c.g;
+  a.src = l1_src;
+  a.lo = slo;
+  a.hi = shi;
+  a.blo = blo;
+  a.nblk = nblk;
+  a.item_root = item.get();
+  a.big = big.get();
+  a.nbig = ctl.get();
+  a.ctr = ctl.get() + 1;
+  a.mid = mid.get();
+  a.nmid = ctl.get() + 4;
+  a.mid2 = mid2.get();
+  a.nmid2 = ctl.get() + 5;
+  a.acc = ctl.get() + kCtl;
+  a.total = c.d_total;
+  a.k = c.k;
+  const unsigned pg = (unsigned)std::max<u64>(1, std::min<u64>((np + 255) / 256, (u64)c.sms * 8));
+  local_prep_kernel<<<pg, 256, 0, c.s>>>(a);
+  GPM_CUDA(cudaGetLastError());
+  size_t rec[3];
+  rec[0] = launch_warp<SmallCfg, false>(c, a, (nblk + bigcap + 31) / 32, "extend_local_small");
+  rec[1] = launch_warp<MidCfg, true>(c, a, (bigcap + 31) / 32, "extend_local_mid");
+  const u32 dmax = std::max<u32>(kMidMax + 1, c.G->max_deg);
+  const size_t smem = 4 * (size_t)BigLayout(dmax).words;
+  GPM_CUDA(cudaFuncSetAttribute(local_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int ob = 0;
+  GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, local_big_kernel, kBigThreads, smem));
+  const u64 bb = std::max<u64>(1, std::min<u64>((u64)c.sms * std::max(1, ob), bigcap));
+  rec[2] = c.tl->begin("extend_local_big", 0.0);
+  local_big_kernel<<<(unsigned)bb, kBigThreads, smem, c.s>>>(a, dmax);
+  GPM_CUDA(cudaGetLastError());
+  c.tl->end(rec[2]);
+  c.tl->launches += 4;
+  std::vector<unsigned long long> h(kCtl + 3 * kAcc);
+  GPM_CUDA(cudaMemcpyAsync(h.data(), ctl.get(), sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c.s));
+  GPM_CUDA(cudaStreamSynchronize(c.s));
+  if (h[0] > 0 || h[5] > 0) st.paths |= GPM_PATH_CF_LOCAL_BIG;
+  // stats and SURVEY §8d bytes per kernel: level lev parents P_lev (P_1 = the
+  // slice's edges), candidates C_lev, children L_lev (the last level's
+  // children are the engine's total, added from d_total by the caller)
+  const int last = c.k - 2;
+  double bytes[3] = {0, 0, 0};
+  for (int kind = 0; kind < 3; ++kind) {
+    const unsigned long long* A = h.data() + kCtl + kind * kAcc;
+    for (int lev = 1; lev <= last; ++lev) {
+      const u64 C = A[kMaxLevels + lev];
+      st.candidates[lev] += C;
+      bytes[kind] += 4.0 * (double)C;
+      if (lev < last) {
+        st.level_sizes[lev] += A[lev];
+        bytes[kind] += 8.0 * (double)A[lev];  // stored children (engine model)
+      }
+    }
+    // parents per level: P_1 from the level-1 candidates' owners is np in
+    // total; deeper levels' parents are the previous level's children
+    for (int lev = 2; lev <= last; ++lev) bytes[kind] += (8.0 * lev + 16.0) * (double)A[lev - 1];
+  }
+  // level-1 parents: every edge of the slice, (8 + 16) B each; attributed to
+  // the kernels in proportion to their level-1 candidates
+  double c1[3], c1t = 0;
+  for (int kind = 0; kind < 3; ++kind) c1t += (c1[kind] = (double)h[kCtl + kind * kAcc + kMaxLevels + 1]);
+  for (int kind = 0; kind < 3; ++kind) {
+    bytes[kind] += 24.0 * (double)np * (c1t > 0 ? c1[kind] / c1t : (kind == 0 ? 1.0 : 0.0));
+    c.tl->recs[rec[kind]].bytes = bytes[kind];
+    st.balg += bytes[kind];
+  }
+  return true;
+}
+
+}  // namespace engine
+}  // namespace gpm

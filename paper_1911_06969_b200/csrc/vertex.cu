@@ -809,6 +809,8 @@ void process_l1_cf(Ctx& c, const VLevels& L, const u32* src, u64 lo, u64 hi) {
 
 namespace engine {
 
+bool cf_local_roots(Ctx& c, const u32* l1_src, u64 slo, u64 shi);  // clique_local.cu
+
 // Builtin specialisations of a level (gpm_engine.cuh process()).
 bool builtin_level(Ctx& c, int kind, int lev, const VLevels& L, u64 np) {
   const bool last = (lev == c.k - 2);
@@ -833,6 +835,7 @@ bool builtin_roots(Ctx& c, int kind, const VLevels& L, const u32* l1_src, const 
   }
   if (kind == kBuiltinClique && c.G->oriented && c.G->n < (1u << 27) && !c.list_fn &&
       !std::getenv("GPM_GENERIC_L1")) {  // key = u << 5 | slot
+    if (cf_local_roots(c, l1_src, slo, shi)) return true;  // k >= 4 counts on local rows
     process_l1_cf(c, L, l1_src, slo, shi);
     return true;
   }

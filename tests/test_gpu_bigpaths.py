@@ -75,8 +75,11 @@ def test_mc4_hbm_union_sets_vs_oracle(P, oracle):
 
 
 @pytest.mark.parametrize("app,k", [("cf", 5), ("cf", 6), ("mc", 4)])
-def test_planner_chunks_vs_oracle(P, oracle, app, k):
+def test_planner_chunks_vs_oracle(P, oracle, app, k, monkeypatch):
     from paper_1911_06969_b200 import _lib
+    # k-CL counts run on local rows (no materialised levels): force the
+    # level-by-level engine so the planner has levels to chunk
+    monkeypatch.setenv("GPM_CF_NOLOCAL", "1")
     # (4-MC's per-candidate oracle is ~100x costlier than k-CL's: smaller graph)
     hg = P.generate_rmat(12, 12, 0.57, 0.19, 0.19, seed=21) if app == "cf" else \
         P.generate_rmat(11, 6, 0.57, 0.19, 0.19, seed=21)
@@ -130,3 +133,73 @@ def test_fsm_big_n_sparse_domains_vs_oracle(P, oracle):
     o = oracle.mine(c, "fsm", 3, 5)
     assert sorted(r.patterns) == sorted(tuple(x) for x in o["patterns"])
     assert r.stats["n_explored"] == o["n_explored"]
+
+
+# ---------------------------------------------------------------------------
+# k-CL on per-root local rows (csrc/clique_local.cu): small-root warp items
+# (out-degree <= 32), medium roots (<= 128, multi-word rows), the CTA kernel
+# (out-degree > 128 and roots cut by slice bounds), vs the oracle.
+
+def _dense_core(n, p, extra_n, extra_p, seed):
+    """G(n, p) core (DAG out-degrees above 128 for its low-rank vertices) plus
+    a sparse G(extra_n, extra_p) periphery attached to it."""
+    rng = np.random.default_rng(seed)
+    iu = np.triu_indices(n, 1)
+    keep = rng.random(iu[0].size) < p
+    core = np.stack([iu[0][keep], iu[1][keep]], 1)
+    m = int(extra_p * extra_n * extra_n / 2)
+    per = rng.integers(0, n + extra_n, size=(m, 2))
+    return np.concatenate([core, per])
+
+
+@pytest.mark.parametrize("k", [4, 5, 6])
+def test_cf_local_rows_all_classes_vs_oracle(P, oracle, k):
+    from paper_1911_06969_b200 import _lib
+    E = _dense_core(420, 0.38, 20000, 0.0009, seed=k)
+    hg, c = host(P, oracle, E, 420 + 20000)
+    g = P.Graph(hg).orient_dag()
+    r = P.mine(g, "cf", k)
+    assert r.stats["paths"] & _lib.PATH_CF_LOCAL and r.stats["paths"] & _lib.PATH_CF_LOCAL_BIG
+    same_vertex(r, oracle.mine(c, "cf", k))
+
+
+@pytest.mark.parametrize("k", [4, 7])
+def test_cf_local_rows_rmat_vs_oracle(P, oracle, k):
+    from paper_1911_06969_b200 import _lib
+    hg = P.generate_rmat(13, 16, 0.57, 0.19, 0.19, seed=5)
+    c = oracle.Csr(hg.off, hg.col)
+    r = P.mine(P.Graph(hg).orient_dag(), "cf", k)
+    assert r.stats["paths"] & _lib.PATH_CF_LOCAL
+    same_vertex(r, oracle.mine(c, "cf", k))
+
+
+def test_cf_local_rows_slices_vs_oracle(P, oracle):
+    """Root slices cut roots (partial roots go to the CTA kernel): the slices'
+    sums equal the whole, and every slice equals the oracle's slice."""
+    E = _dense_core(300, 0.5, 5000, 0.002, seed=3)
+    hg, c = host(P, oracle, E, 5300)
+    g = P.Graph(hg).orient_dag()
+    whole = P.mine(g, "cf", 4)
+    n1 = whole.stats["level_sizes"][0]
+    cuts = [0, 1, 977, n1 // 3, n1 // 2 + 17, n1 - 5, n1]
+    tot, lv = 0, [0, 0, 0]
+    for lo, hi in zip(cuts, cuts[1:]):
+        r = P.mine(g, "cf", 4, root_lo=lo, root_hi=hi)
+        o = oracle.mine(c, "cf", 4, root_lo=lo, root_hi=hi)
+        assert r.total == o["total"] and r.stats["level_sizes"] == o["level_sizes"], (lo, hi)
+        assert r.stats["candidates"] == o["candidates"] and r.stats["b_alg"] == o["b_alg"], (lo, hi)
+        tot += r.total
+        lv = [x + y for x, y in zip(lv, r.stats["level_sizes"])]
+    assert tot == whole.total and lv == whole.stats["level_sizes"]
+
+
+def test_cf_local_rows_fallback_above_1024(P, oracle):
+    """A DAG out-degree above 1024 (K_{1030,1030}: the smaller ids of one side
+    point at the whole other side) keeps the level-by-level path."""
+    from paper_1911_06969_b200 import _lib
+    a = np.arange(1030)
+    E = np.stack(np.meshgrid(a, a + 1030), -1).reshape(-1, 2)
+    hg, c = host(P, oracle, E, 2060)
+    r = P.mine(P.Graph(hg).orient_dag(), "cf", 4)
+    assert not r.stats["paths"] & _lib.PATH_CF_LOCAL
+    assert r.total == 0 and r.stats["level_sizes"][1] == 0

@@ -119,12 +119,15 @@ def test_wedge_formula_and_tc_consistency(P):
     assert P.clique_find(g, 4) == P.motif_count(g, 4)["k=4;L=0,0,0,0;E=(0,1)(0,2)(0,3)(1,2)(1,3)(2,3)"]
 
 
-def test_planner_chunking_invariance(P, oracle):
+def test_planner_chunking_invariance(P, oracle, monkeypatch):
     hg = P.generate_rmat(12, 8, 0.57, 0.19, 0.19, seed=3)
     g = P.Graph(hg)
     for app, k in (("cf", 4), ("cf", 5), ("mc", 4)):
         base = P.mine(g, app, k)
+        if app == "cf":  # k-CL counts run on local rows: force the level engine to chunk
+            monkeypatch.setenv("GPM_CF_NOLOCAL", "1")
         tiny = P.mine(g, app, k, mem_budget=1 << 16)   # forces many planner chunks
+        monkeypatch.delenv("GPM_CF_NOLOCAL", raising=False)
         assert tiny.stats["chunks"] > 0
         assert tiny.total == base.total and tiny.patterns == base.patterns
         same(tiny, base.stats)

@@ -6,6 +6,7 @@ fallback; environment switches force the fallback so both can be compared on
 the same inputs (totals, pattern maps, per-level sizes, candidates, B_alg):
   GPM_GENERIC_L1   CF/TC first level: generic batches instead of edge chunks
   GPM_GENERIC_CF   CF last level: generic to_add instead of the sibling probe
+  GPM_CF_NOLOCAL   k-CL (k >= 4): level-by-level instead of per-root local rows
   GPM_GENERIC_MC   MC: per-candidate binary search instead of staged sets
   GPM_FSM_TWO_PASS FSM last level: separate domain pass instead of the fused one
 """
@@ -56,6 +57,7 @@ def test_cf_paths(P, scale, ef, abc):
         _same(base, _run(P, g, "cf", k, env=["GPM_GENERIC_L1"]))
         _same(base, _run(P, g, "cf", k, env=["GPM_GENERIC_CF"]))
         _same(base, _run(P, g, "cf", k, env=["GPM_GENERIC_L1", "GPM_GENERIC_CF"]))
+        _same(base, _run(P, g, "cf", k, env=["GPM_CF_NOLOCAL"]))  # local rows vs level by level
 
 
 @pytest.mark.parametrize("scale,ef,abc", [(11, 16, (0.57, 0.19, 0.19)), (13, 8, (0.45, 0.15, 0.15)),
