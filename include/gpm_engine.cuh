@@ -545,6 +545,9 @@ struct Ctx {
 // when they processed the level / root slice.
 bool builtin_level(Ctx& c, int kind, int lev, const VLevels& L, u64 np);
 bool builtin_roots(Ctx& c, int kind, const VLevels& L, const u32* l1_src, const u64* l1_start, u64 slo, u64 shi);
+// k-CL counts on per-root local rows apply (csrc/clique_local.cu): the level-1
+// v0 array is then not needed.
+bool cf_local_applicable(const gpm_graph& G, int k, bool listing);
 
 // Streams a materialised final level (n entries at level LEV) to the host sink
 // through two device staging buffers and two pinned host buffers: the rows of
@@ -845,7 +848,10 @@ void mine(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm_result
   DBuf<u64> l1s;
   u64 n1 = 0;
   const u32* l1vid = nullptr;
-  build_level1(*G, l1i, l1v, n1, s, tl, &l1vid, &l1s);
+  const int world0 = std::max(1, cfg.world);
+  const bool lazy_l1 = builtin<App>::value == kBuiltinClique && world0 == 1 && G->oriented &&
+                       !std::getenv("GPM_GENERIC_L1") && cf_local_applicable(*G, k, cfg.list_fn != nullptr);
+  build_level1(*G, l1i, l1v, n1, s, tl, &l1vid, &l1s, !lazy_l1);
   if (!l1vid) l1vid = l1v.get();
   // root units of this rank: an explicit slice, the degree-weighted static
   // split, or (steal_ctrs set) the split's head + a device-side stealing tail

@@ -332,6 +332,7 @@ static int mine_once(const gpm_graph* g, const gpm_config* cfg, gpm_result** out
       float t = 0;
       GPM_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
       if (trace) std::fprintf(stderr, "[gpm]   %-28s %10.3f ms  %12.4g B_alg\n", r.name.c_str(), t, r.bytes);
+      if (r.side) continue;  // overlapped with the main stream: neither a phase nor the dominant kernel
       per[r.name][0] += t;
       per[r.name][1] += r.bytes;
       per[r.name][2] += r.moved >= 0 ? r.moved : r.bytes;

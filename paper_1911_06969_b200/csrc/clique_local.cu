@@ -47,7 +47,6 @@ constexpr int kAcc = 2 * kMaxLevels;  // [0, kMaxLevels): children per level; [k
 
 struct LocalArgs {
   DevGraph g;
-  const u32* src;       // level-1 v0 per DAG edge (absolute edge index)
   u64 lo, hi;           // level-1 slice = DAG edge range
   u64 blo, nblk;        // 32-edge blocks [blo, blo + nblk)
   u32* item_root;       // per block: smallest small root whose first edge lies in the block, or ~0
@@ -87,27 +86,24 @@ __device__ __forceinline__ u32 hb_find(const u32* T, u32 sh, u32 bmask, u32 v) {
   }
 }
 
-// Classifies the roots of the slice: a root starts at edge e when e is its
-// first out-edge (or e == lo for a root cut by the slice start).
+// Classifies the roots of the slice (thread per vertex: the roots whose
+// out-edge range meets [lo, hi)).
 __global__ void local_prep_kernel(LocalArgs a) {
-  const u64 np = a.hi - a.lo;
-  for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < np; t += (u64)gridDim.x * blockDim.x) {
-    const u64 e = a.lo + t;
-    const u32 v = ldg(a.src + e);
-    if (e != a.lo && ldg(a.src + e - 1) == v) continue;
+  for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < a.g.n; v += (u64)gridDim.x * blockDim.x) {
     const u64 ob = ldg(a.g.off + v), oe = ldg(a.g.off + v + 1);
+    if (oe <= a.lo || ob >= a.hi || ob == oe) continue;
     const u64 d = oe - ob;
     if (ob < a.lo || oe > a.hi || d > kMidMax) {
       const unsigned long long i = atomicAdd(a.nbig, 1ull);
-      a.big[i] = v;
+      a.big[i] = (u32)v;
     } else if (d > 64) {
       const unsigned long long i = atomicAdd(a.nmid2, 1ull);
-      a.mid2[i] = v;
+      a.mid2[i] = (u32)v;
     } else if (d > 32) {
       const unsigned long long i = atomicAdd(a.nmid, 1ull);
-      a.mid[i] = v;
+      a.mid[i] = (u32)v;
     } else {
-      atomicMin(a.item_root + (e / 32 - a.blo), v);
+      atomicMin(a.item_root + (ob / 32 - a.blo), (u32)v);
     }
   }
 }
@@ -682,8 +678,30 @@ __global__ void __launch_bounds__(kBigThreads) local_big_kernel(LocalArgs a, u32
 
 }  // namespace
 
+// Timeline records on a stream other than the timeline's own
+size_t tl_begin_on(Timeline& tl, const char* name, cudaStream_t st) {
+  Timeline::Rec r{name, nullptr, nullptr, 0.0, -1, st != tl.s};
+  GPM_CUDA(cudaEventCreate(&r.a));
+  GPM_CUDA(cudaEventCreate(&r.b));
+  GPM_CUDA(cudaEventRecord(r.a, st));
+  tl.recs.push_back(r);
+  return tl.recs.size() - 1;
+}
+
+// Side stream of the calling thread on the current device: the (64, 1024]
+// out-degree roots run beside the small-root items (their warps are few and
+// long, so serialised they would be a latency-bound tail).
+cudaStream_t side_stream() {
+  int dev = 0;
+  GPM_CUDA(cudaGetDevice(&dev));
+  static thread_local std::vector<cudaStream_t> ss;
+  if ((int)ss.size() <= dev) ss.resize(dev + 1, nullptr);
+  if (!ss[dev]) GPM_CUDA(cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking));
+  return ss[dev];
+}
+
 template <class C, bool MID>
-size_t launch_warp(Ctx& c, LocalArgs& a, u64 max_items_per8, const char* name) {
+size_t launch_warp(Ctx& c, LocalArgs& a, u64 max_blocks, const char* name, cudaStream_t st) {
   auto kern = local_warp_kernel<C, MID>;
   const size_t smem = sizeof(WarpSmem<C>) * (kSmallThreads / 32);
   static std::atomic<int> occ{0};
@@ -693,21 +711,23 @@ size_t launch_warp(Ctx& c, LocalArgs& a, u64 max_items_per8, const char* name) {
     GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, kSmallThreads, smem));
     return r;
   });
-  const u64 blocks = std::max<u64>(1, std::min<u64>((u64)c.sms * o, max_items_per8));
-  size_t rec = c.tl->begin(name, 0.0);
-  kern<<<(unsigned)blocks, kSmallThreads, smem, c.s>>>(a);
+  const u64 blocks = std::max<u64>(1, std::min<u64>((u64)c.sms * o, max_blocks));
+  size_t rec = tl_begin_on(*c.tl, name, st);
+  kern<<<(unsigned)blocks, kSmallThreads, smem, st>>>(a);
   GPM_CUDA(cudaGetLastError());
-  c.tl->end(rec);
+  GPM_CUDA(cudaEventRecord(c.tl->recs[rec].b, st));
   return rec;
 }
 
 // k-CL (k >= 4) count of the level-1 slice [slo, shi) on local rows; false
 // when the preconditions do not hold (the caller runs the edge-chunk path).
-bool cf_local_roots(Ctx& c, const u32* l1_src, u64 slo, u64 shi) {
-  if (c.k < 4 || c.list_fn || !c.G->oriented || c.G->max_deg > kBigMax || c.G->n >= (1u << 27) ||
-      c.G->m >= (u64(1) << 32) ||
-      std::getenv("GPM_CF_NOLOCAL"))
-    return false;
+bool cf_local_applicable(const gpm_graph& G, int k, bool listing) {
+  return k >= 4 && !listing && G.oriented && G.max_deg <= kBigMax && G.n < (1u << 27) && G.m < (u64(1) << 32) &&
+         !std::getenv("GPM_CF_NOLOCAL");
+}
+
+bool cf_local_roots(Ctx& c, const u32*, u64 slo, u64 shi) {
+  if (!cf_local_applicable(*c.G, c.k, c.list_fn != nullptr)) return false;
   const u64 np = shi - slo;
   Stats& st = *c.st;
   st.paths |= GPM_PATH_CF_LOCAL;
@@ -720,7 +740,6 @@ bool cf_local_roots(Ctx& c, const u32* l1_src, u64 slo, u64 shi) {
   GPM_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(unsigned long long) * (kCtl + 3 * kAcc), c.s));
   LocalArgs a{};
   a.g = c.g;
-  a.src = l1_src;
   a.lo = slo;
   a.hi = shi;
   a.blo = blo;
@@ -736,22 +755,38 @@ bool cf_local_roots(Ctx& c, const u32* l1_src, u64 slo, u64 shi) {
   a.acc = ctl.get() + kCtl;
   a.total = c.d_total;
   a.k = c.k;
-  const unsigned pg = (unsigned)std::max<u64>(1, std::min<u64>((np + 255) / 256, (u64)c.sms * 8));
+  const unsigned pg = (unsigned)std::max<u64>(1, std::min<u64>((c.G->n + 255) / 256, (u64)c.sms * 8));
   local_prep_kernel<<<pg, 256, 0, c.s>>>(a);
   GPM_CUDA(cudaGetLastError());
+  // fork: medium-2 and big roots on the side stream, small items here
+  cudaStream_t ss = side_stream();
+  cudaEvent_t fork = nullptr, join = nullptr;
+  GPM_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  GPM_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t* e[2];
+    ~EvGuard() {
+      for (auto* x : e)
+        if (*x) cudaEventDestroy(*x);
+    }
+  } evg{{&fork, &join}};
+  GPM_CUDA(cudaEventRecord(fork, c.s));
+  GPM_CUDA(cudaStreamWaitEvent(ss, fork, 0));
   size_t rec[3];
-  rec[0] = launch_warp<SmallCfg, false>(c, a, (nblk + bigcap + 31) / 32, "extend_local_small");
-  rec[1] = launch_warp<MidCfg, true>(c, a, (bigcap + 31) / 32, "extend_local_mid");
+  rec[1] = launch_warp<MidCfg, true>(c, a, (bigcap + 7) / 8, "extend_local_mid", ss);
   const u32 dmax = std::max<u32>(kMidMax + 1, c.G->max_deg);
   const size_t smem = 4 * (size_t)BigLayout(dmax).words;
   GPM_CUDA(cudaFuncSetAttribute(local_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int ob = 0;
   GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, local_big_kernel, kBigThreads, smem));
   const u64 bb = std::max<u64>(1, std::min<u64>((u64)c.sms * std::max(1, ob), bigcap));
-  rec[2] = c.tl->begin("extend_local_big", 0.0);
-  local_big_kernel<<<(unsigned)bb, kBigThreads, smem, c.s>>>(a, dmax);
+  rec[2] = tl_begin_on(*c.tl, "extend_local_big", ss);
+  local_big_kernel<<<(unsigned)bb, kBigThreads, smem, ss>>>(a, dmax);
   GPM_CUDA(cudaGetLastError());
-  c.tl->end(rec[2]);
+  GPM_CUDA(cudaEventRecord(c.tl->recs[rec[2]].b, ss));
+  GPM_CUDA(cudaEventRecord(join, ss));
+  rec[0] = launch_warp<SmallCfg, false>(c, a, (nblk + bigcap + 7) / 8, "extend_local_small", c.s);
+  GPM_CUDA(cudaStreamWaitEvent(c.s, join, 0));
   c.tl->launches += 4;
   std::vector<unsigned long long> h(kCtl + 3 * kAcc);
   GPM_CUDA(cudaMemcpyAsync(h.data(), ctl.get(), sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c.s));

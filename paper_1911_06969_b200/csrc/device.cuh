@@ -370,6 +370,7 @@ struct Timeline {
     cudaEvent_t a, b;
     double bytes;
     double moved = -1;  // bytes the kernel actually reads when they differ from B_alg (< 0: = bytes)
+    bool side = false;  // ran on a side stream beside the main stream's kernels (not a step phase)
   };
   cudaStream_t s;
   std::vector<Rec> recs;

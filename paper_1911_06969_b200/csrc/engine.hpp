@@ -72,8 +72,10 @@ struct Stats {
 // edge; undirected -> (u,v) with u<v.  idx[i] = first endpoint, vid[i] = second.
 // Undirected graphs: *l1_start (optional) receives the exclusive prefix over
 // vertices of |{v in N(u) : v > u}|, i.e. the first level-1 index of root u.
+// need_idx = false (DAG only): the per-edge v0 array is not built (the k-CL
+// local-row path reads the CSR offsets instead).
 void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl,
-                  const u32** vid_view = nullptr, DBuf<u64>* l1_start = nullptr);
+                  const u32** vid_view = nullptr, DBuf<u64>* l1_start = nullptr, bool need_idx = true);
 
 // Last extension of 3-MC with the root's upper adjacency staged on chip
 // (mc_staged.cu): adds the 3-vertex connectivity-code counts of the level-1

@@ -272,10 +272,14 @@ void keep_pool_warm(int device) {
 }
 
 void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count, cudaStream_t s, Timeline& tl,
-                  const u32** vid_view, DBuf<u64>* l1_start) {
+                  const u32** vid_view, DBuf<u64>* l1_start, bool need_idx) {
   if (g.oriented) {
     // level 1 of a DAG is the CSR edge range itself: vid aliases col (no copy)
     count = g.m;
+    if (!need_idx && vid_view) {
+      *vid_view = g.d_col;
+      return;
+    }
     idx.alloc(std::max<u64>(1, g.m), s);
     if (vid_view) {
       *vid_view = g.d_col;
