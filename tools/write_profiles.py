@@ -18,8 +18,8 @@ out = os.path.join(ROOT, "profiles", rnd)
 os.makedirs(out, exist_ok=True)
 # dominant timeline record per bench workload -> the kernels it is made of
 # (3-MC's "extend_fused_L1" is the warp kernel + the tiled block kernel)
-DOMINANT = {"cf4": ["edge_chunk"], "tc": ["edge_chunk"], "mc3": ["mc3_warp", "mc3_block"], "mc4": ["mc4_last"],
-            "fsm": ["eextend"]}
+DOMINANT = {"cf4": ["local_warp_kernel"], "tc": ["edge_lane_kernel", "edge_chunk"], "mc3": ["mc3_warp", "mc3_block"],
+            "mc4": ["mc4_last"], "fsm": ["efan_kernel"]}
 traffic = {}
 
 
@@ -88,7 +88,7 @@ for rep in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "full_*.ncu-rep")))
             e["l2_bytes_per_launch"] += l2 or 0.0
             e["duration_ms_ncu"] += t * 1e3
             e["sources"].append(f"profiles/{rnd}/ncu_{tag}.txt")
-    src = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_source.py"), rep, tag.split("_", 1)[1], "0", "15"],
+    src = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_source.py"), rep, ".", "0", "15"],
                          capture_output=True, text=True).stdout
     lines.append("top source lines (stall share, instruction share):")
     lines += ["  " + x for x in src.splitlines()]
