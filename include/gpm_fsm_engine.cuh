@@ -39,6 +39,9 @@
 // The last level is never materialised.  Multi-GPU: pattern keys are
 // all-gathered and bitmaps OR-exchanged through gpm_config.exchange.
 #include <parallel/algorithm>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -57,6 +60,23 @@ namespace gpm {
 void scan_inplace(u64* data, u64 n, cudaStream_t s);
 
 namespace fsm_engine {
+
+// host threads for the per-pattern loops (1 when the including translation
+// unit is built without OpenMP)
+inline int host_threads() {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+inline int host_thread() {
+#ifdef _OPENMP
+  return omp_get_thread_num();
+#else
+  return 0;
+#endif
+}
 
 // What App::to_prune sees of a canonical pattern after the level's reduce:
 // its packed canonical code (pattern.cuh; pat::decode with label_bits gives
@@ -760,15 +780,19 @@ __device__ __forceinline__ u32 smap_get(unsigned long long* mkey, u32* mslot, u3
         u32 val = kSlotNone;
         if (sl < cslots) {
           val = sl;
-          skey[sl] = code;
-          sinfo[sl] = 0ull;
+          skey[sl] = code;  // read only after the item's barrier
+          // sinfo is shared with the other warps of the item before any
+          // barrier: written and read with atomics (published through mslot)
+          unsigned long long si = 0ull;
           if (MODE == kDomain) {
             // the code's canonical pattern and PositionMap; a bitmap only if
             // the pattern has one in this round
             const u64 info = hash_info(a.H, hash_find(a.H, code));
             const u32 bs = a.bslot[(u32)(info >> 32)];
-            sinfo[sl] = (bs >= a.round_lo && bs < a.round_hi) ? (((u64)(bs - a.round_lo) << 32) | (u32)info) : ~0ull;
-          } else if (MODE == kQCD) {
+            si = (bs >= a.round_lo && bs < a.round_hi) ? (((u64)(bs - a.round_lo) << 32) | (u32)info) : ~0ull;
+          }
+          atomicExch(sinfo + sl, si);
+          if (MODE == kQCD) {
             sid[sl] = hash_add(a.H, code, 0ull);  // dense quick-code id (0: table overflow)
           }
         }
@@ -895,7 +919,7 @@ __global__ void __launch_bounds__(kGT, 1) egroup_kernel(FsmArgs a, GroupArgs ga)
           if (id && id - 1 >= a.qcap) *a.qover = 1;
           else if (id) row = a.qbm + (u64)(id - 1) * rowlen;
         } else if (ok && slot != kSlotNone) {
-          if (MODE != kDomain || sinfo[slot] != ~0ull) row = sbm + (u64)slot * rowlen;  // kDomain: bitmap this round?
+          if (MODE != kDomain || atomicAdd(sinfo + slot, 0ull) != ~0ull) row = sbm + (u64)slot * rowlen;  // kDomain: bitmap this round?
         } else if (ok) {  // kDomain without a shared slot
           const u64 info = hash_info(a.H, hash_find(a.H, code));
           const u32 bs = a.bslot[(u32)(info >> 32)];
@@ -1569,6 +1593,7 @@ struct Fsm {
     u64 U = 0;
     DBuf<u8> frequent;
     std::vector<u64> gkeys_h, gcount_h, mni_h;
+    std::vector<u8> freq_h;  // frequent (not pruned) flags, host copy
     DBuf<u64> gkeys;
     u64 P = 0;
     u64 NB = 0;
@@ -1670,9 +1695,14 @@ struct Fsm {
       keys.swap(k2);
       cnts.swap(c2);
     }
-    // reduce by canonical key (sorted)
+    // reduce by canonical key (sorted; a single rank's device reduce already
+    // made them unique)
     R.gkeys_h.clear();
     R.gcount_h.clear();
+    if (!(cfg.world > 1 && cfg.exchange)) {
+      R.gkeys_h.swap(keys);
+      R.gcount_h.swap(cnts);
+    }
     for (size_t i = 0; i < keys.size(); ++i) {
       if (R.gkeys_h.empty() || R.gkeys_h.back() != keys[i]) {
         R.gkeys_h.push_back(keys[i]);
@@ -1681,13 +1711,16 @@ struct Fsm {
       R.gcount_h.back() += cnts[i];
     }
     R.P = R.gkeys_h.size();
+    trace("host reduce by key", (double)R.P);
     R.gkeys.alloc(std::max<u64>(1, R.P), s);
     if (R.P)
       GPM_CUDA(cudaMemcpyAsync(R.gkeys.get(), R.gkeys_h.data(), sizeof(u64) * R.P, cudaMemcpyHostToDevice, s));
+    trace("gkeys h2d", (double)R.P);
     slot_pid_kernel<<<grid1(std::max<u64>(1, R.U)), 256, 0, s>>>(R.canon.get(), R.occ.get(), R.U, R.gkeys.get(), R.P,
                                                                  R.perm.get(), R.ent.get());
     GPM_CUDA(cudaGetLastError());
     ++tl.launches;
+    trace("reduce keys + slot pids", (double)R.P, (double)R.U);
     // count pre-filter -> bitmap slots (MNI <= count)
     std::vector<u32> bslot(std::max<u64>(1, R.P), ~0u), bs_to_pid;
     // MNI <= count; the full-automorphism MNI unions an orbit's domains: <= nv * count
@@ -1827,8 +1860,10 @@ struct Fsm {
       GPM_CUDA(cudaMemcpyAsync(R.mni_h.data(), mni.get(), sizeof(u64) * R.P, cudaMemcpyDeviceToHost, s));
     sync();
     trace("mni kernel + d2h", (double)R.P);
-    std::vector<u8> freq(std::max<u64>(1, R.P), 0);
-    for (u64 p = 0; p < R.P; ++p) freq[p] = frequent_pat(R, p) ? 1 : 0;
+    std::vector<u8>& freq = R.freq_h;
+    freq.assign(std::max<u64>(1, R.P), 0);
+#pragma omp parallel for schedule(static)
+    for (long long p = 0; p < (long long)R.P; ++p) freq[p] = frequent_pat(R, (u64)p) ? 1 : 0;
     R.frequent.alloc(freq.size(), s);
     GPM_CUDA(cudaMemcpyAsync(R.frequent.get(), freq.data(), freq.size(), cudaMemcpyHostToDevice, s));
     sync();
@@ -1842,15 +1877,33 @@ struct Fsm {
     return R.gcount_h[p] > 0 && !App::to_prune(pi);
   }
 
+  // text is formatted on access (gpm_result_pattern): ~10^6 patterns per
+  // call, recorded in parallel from the frequent flags (pattern order kept)
   void record(Level& R, int level) {
-    std::vector<u64> sel;
-    for (u64 p = 0; p < R.P; ++p)
-      if (frequent_pat(R, p)) sel.push_back(p);
-    // text is formatted on access (gpm_result_pattern): ~10^6 patterns per call
-    res.kpatterns.reserve(res.kpatterns.size() + sel.size());
-    for (u64 p : sel) {
-      const PatternInfo pi{R.gkeys_h[p], R.gcount_h[p], R.mni_h[p], sigma, LB, cfg.mni_mode};
-      res.kpatterns.push_back({R.gkeys_h[p], App::support_of(pi), level});
+    const long long P = (long long)R.P;
+    const int T = std::max(1, std::min(host_threads(), (int)(P >> 14) + 1));
+    std::vector<u64> part(T + 1, 0);
+#pragma omp parallel num_threads(T)
+    {
+      const int t = host_thread();
+      const long long b = P * t / T, e = P * (t + 1) / T;
+      u64 c = 0;
+      for (long long p = b; p < e; ++p) c += R.freq_h[p];
+      part[t + 1] = c;
+    }
+    for (int t = 0; t < T; ++t) part[t + 1] += part[t];
+    const size_t base = res.kpatterns.size();
+    res.kpatterns.resize(base + part[T]);
+#pragma omp parallel num_threads(T)
+    {
+      const int t = host_thread();
+      const long long b = P * t / T, e = P * (t + 1) / T;
+      size_t o = base + part[t];
+      for (long long p = b; p < e; ++p)
+        if (R.freq_h[p]) {
+          const PatternInfo pi{R.gkeys_h[p], R.gcount_h[p], R.mni_h[p], sigma, LB, cfg.mni_mode};
+          res.kpatterns[o++] = {R.gkeys_h[p], App::support_of(pi), level};
+        }
     }
   }
 
@@ -2140,15 +2193,36 @@ struct Fsm {
     GPM_CUDA(cudaMemcpyAsync(hs.data(), starts.get(), sizeof(u32) * G_, cudaMemcpyDeviceToHost, s));
     GPM_CUDA(cudaMemcpyAsync(hc.data(), gc.get(), sizeof(u64) * G_, cudaMemcpyDeviceToHost, s));
     sync();
-    std::vector<FanItem> v;
+    trace("fan group starts d2h", (double)G_);
+    // items, large first (tail balance): a stable counting sort by size
+    // (sizes are 1..kFanParents), O(items) instead of a comparison sort
+    std::vector<u64> bucket(kFanParents + 2, 0);
+    u64 ntot = 0;
+    for (u64 i = 0; i < G_; ++i) {
+      const u32 a0 = hs[i], a1 = i + 1 < G_ ? hs[i + 1] : (u32)nz;
+      const int nvv = pat::code_nv(hc[i]);
+      for (u32 b = a0; b < a1; b += kFanParents) {
+        bucket[kFanParents - std::min<u32>(a1 - b, kFanParents)] += (u64)nvv;
+        ntot += (u64)nvv;
+      }
+    }
+    u64 acc = 0;
+    for (auto& x : bucket) {
+      const u64 c = x;
+      x = acc;
+      acc += c;
+    }
+    std::vector<FanItem> v(ntot);
     for (u64 i = 0; i < G_; ++i) {
       const u32 a0 = hs[i], a1 = i + 1 < G_ ? hs[i + 1] : (u32)nz;
       const int nvv = pat::code_nv(hc[i]);
       for (int q = 0; q < nvv; ++q)
-        for (u32 b = a0; b < a1; b += kFanParents) v.push_back(FanItem{hc[i], b, std::min<u32>(a1, b + kFanParents), (u32)q, 0});
+        for (u32 b = a0; b < a1; b += kFanParents) {
+          const u32 e = std::min<u32>(a1, b + kFanParents);
+          v[bucket[kFanParents - (e - b)]++] = FanItem{hc[i], b, e, (u32)q, 0};
+        }
     }
-    // large items first (tail balance)
-    std::stable_sort(v.begin(), v.end(), [](const FanItem& x, const FanItem& y) { return x.pb - x.pa > y.pb - y.pa; });
+    trace("fan items host sort", (double)v.size());
     nitems = v.size();
     items.alloc(std::max<u64>(1, nitems), s);
     if (nitems) GPM_CUDA(cudaMemcpyAsync(items.get(), v.data(), sizeof(FanItem) * nitems, cudaMemcpyHostToDevice, s));
@@ -2285,15 +2359,18 @@ struct Fsm {
     DBuf<FanItem> fitems;
     u64 nfan = 0;
     const bool use_fan = fan_ok && qcap && nb;
+    trace("qbm alloc", (double)qcap);
     if (use_fan) {
       DBuf<u64> pcodes;
       sort_parents_exact<LEV>(L, pidx, nz, pcodes);
+      trace("sort parents", (double)nz);
       // Wp in the new parent order (the unfused fallback passes read it)
       egather_kernel<<<grid1(nz), 256, 0, s>>>(w.get(), pidx.get(), nz, Wp.get());
       GPM_CUDA(cudaGetLastError());
       ++tl.launches;
       GPM_CUDA(cudaMemsetAsync(Wp.get() + nz, 0, sizeof(u64), s));
       scan_inplace(Wp.get(), nz + 1, s);
+      trace("egather + scan", (double)nz);
       build_fan_items(pcodes, nz, fitems, nfan);
     }
     for (;;) {
@@ -2363,6 +2440,7 @@ struct Fsm {
       a.scap = scap;
       launch<LEV>(a, kSparse, "fsm_extend_sparse", bytes_in);
     });
+    trace("mni done", (double)R.P);
     record(R, LEV + 1);
     trace("mni+record", (double)R.P);
     if (last || !nb) return;

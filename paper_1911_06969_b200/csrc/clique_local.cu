@@ -129,7 +129,8 @@ struct WarpCfg {
   static constexpr int kWords = WMAX;    // row words per edge
   static constexpr int kWin = WIN;       // stream windows with a start bitmap (32 positions each)
   static constexpr int kUnroll = UNROLL; // windows per loop step (loads in flight per warp)
-  static constexpr int kMinBlocks = MINB;
+  static constexpr int kMinBlocks = MINB;  // (software-pipelining the next step's loads needed 78
+                                          // registers -> 3 CTAs/SM and measured slower: 1.00 vs 0.89 ms)
 };
 using SmallCfg = WarpCfg<64, 128, 2, 128>;   // small-root blocks (1-word rows) and roots of out-degree <= 64
 using MidCfg = WarpCfg<128, 256, 4, 256, 4, 2>;    // roots of out-degree in (64, 128]
@@ -391,35 +392,47 @@ __global__ void __launch_bounds__(kSmallThreads, C::kMinBlocks) local_warp_kerne
       static_assert(C::kUnroll == 4, "one LDS.128 of window masks per step");
       u32 P = 0xffffffffu;  // entry holding the position before the window
       const u32* const col = g.col;
-      for (u32 it = 0; it < nwin; it += 4) {
+      // one step = 4 windows: lane -> entry by the start bitmaps, then the
+      // four candidate loads (raw vertex + slot; the key is formed later)
+      auto issue = [&](u32 it, u32 (&uq)[4], u32 (&sq)[4], u32 (&eq)[4]) {
         const uint4 w4 = *reinterpret_cast<const uint4*>(S.wm + it);
         const u32 wq[4] = {w4.x, w4.y, w4.z, w4.w};
         const u32 jl = it * 32 + lane;
-        u32 key[4], eq[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           eq[q] = P + __popc(wq[q] & lemask);
           P += __popc(wq[q]);
-          u32 u = 0x07ffffffu, sl = 30;
+          uq[q] = 0x07ffffffu;
+          sq[q] = 30;
           if (jl + 32 * q < total) {
             const uint2 d = S.ent[eq[q]];
-            u = ldg(col + (u32)(d.x + jl + 32 * q));
-            sl = d.y;
+            uq[q] = ldg(col + (u32)(d.x + jl + 32 * q));
+            sq[q] = d.y;
           }
-          key[q] = (u << 5) | sl;
         }
-        // filter bit first (one LDS.32 per window); the bucket (LDS.128,
-        // ~4x the shared-memory wavefronts) only for filter-positive lanes,
-        // which are rare: any positive lane re-probes its 4 keys exactly
+      };
+      // filter bit first (one LDS.32 per window); the bucket (LDS.128, ~4x
+      // the shared-memory wavefronts) only for filter-positive lanes, which
+      // are rare: any positive lane re-probes its 4 keys exactly
+      auto probe = [&](const u32 (&uq)[4], const u32 (&sq)[4], const u32 (&eq)[4]) {
+        u32 key[4];
         bool any = false;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
+          key[q] = (uq[q] << 5) | sq[q];
           const u32 hv = key[q] * kHashMul;
           any |= (S.F[__byte_perm(hv, 0, 0x4442)] >> (hv >> 27)) & 1u;
         }
         if (any) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) hit(key[q], eq[q]);
+        }
+      };
+      {
+        for (u32 it = 0; it < nwin; it += 4) {
+          u32 uq[4], sq[4], eq[4];
+          issue(it, uq, sq, eq);
+          probe(uq, sq, eq);
         }
       }
     } else {
