@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <memory>
 
@@ -54,115 +55,76 @@ __global__ void validate_kernel(const u64* __restrict__ off, const u32* __restri
   }
 }
 
-// (deg, id) total order of graph.hpp:124-126
-__device__ __forceinline__ bool precedes(const u64* off, u32 a, u32 b) {
-  u64 da = off[a + 1] - off[a], db = off[b + 1] - off[b];
-  return da != db ? da < db : a < b;
-}
-
-template <bool WRITE>
-__global__ void orient_kernel(const u64* __restrict__ off, const u32* __restrict__ col, u32 n,
-                              u64* __restrict__ cnt_or_off, u32* __restrict__ out_col) {
-  const int lane = threadIdx.x & 31;
-  const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
-  const u64 nwarps = (gridDim.x * (u64)blockDim.x) >> 5;
-  for (u64 u = warp; u < n; u += nwarps) {
-    const u64 b = off[u], e = off[u + 1];
-    u64 w = WRITE ? cnt_or_off[u] : 0;
-    u64 c = 0;
-    for (u64 i0 = b; i0 < e; i0 += 32) {
-      u64 i = i0 + lane;
-      bool keep = false;
-      u32 v = 0;
-      if (i < e) {
-        v = col[i];
-        keep = precedes(off, (u32)u, v);
-      }
-      u32 mask = __ballot_sync(0xffffffffu, keep);
-      if (WRITE && keep) out_col[w + __popc(mask & lanemask_lt())] = v;
-      w += __popc(mask);
-      c += __popc(mask);
-    }
-    if (!WRITE && lane == 0) cnt_or_off[u] = c;
-  }
-}
-
-// Orientation pass 1 over vertices [vb, ve): optional validation (graph.hpp:
-// 29-55), out-degree in the (deg, id) order, and a keep flag per half-edge so
-// pass 2 needs no second degree gather.
-__global__ void orient_count_kernel(const u64* __restrict__ off, const u32* __restrict__ col, u32 n, u64 m, u32 vb,
-                                    u32 ve, int validate, u64* __restrict__ cnt, u8* __restrict__ keep,
-                                    int* __restrict__ bad) {
-  const int lane = threadIdx.x & 31;
-  const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
-  const u64 nwarps = (gridDim.x * (u64)blockDim.x) >> 5;
+// u32 degrees (and the offsets' validity, graph.hpp:29-55) for the
+// orientation's (deg, id) order: one 4-byte random read per edge.
+__global__ void deg32_kernel(const u64* __restrict__ off, u32 vb, u32 ve, u64 m, u32* __restrict__ deg,
+                             int* __restrict__ bad) {
   int mybad = 0;
-  for (u64 uu = vb + warp; uu < ve; uu += nwarps) {
-    const u32 u = (u32)uu;
-    const u64 b = off[u], e = off[u + 1];
-    if (e < b || e > m) {
-      mybad |= 1;
-      if (lane == 0) cnt[u] = 0;
-      continue;
-    }
-    const u64 du = e - b;
-    u64 c = 0;
-    for (u64 i0 = b; i0 < e; i0 += 32) {
-      const u64 i = i0 + lane;
-      bool k = false;
-      if (i < e) {
-        const u32 v = col[i];
-        if (validate && !(v < n && v != u && (i == b || col[i - 1] < v))) mybad |= 2;
-        if (v < n) {
-          const u64 dv = off[v + 1] - off[v];
-          k = du != dv ? du < dv : u < v;
-        }
-        keep[i] = k ? 1 : 0;
-      }
-      c += __popc(__ballot_sync(0xffffffffu, k));
-    }
-    if (lane == 0) cnt[u] = c;
+  for (u64 v = vb + blockIdx.x * (u64)blockDim.x + threadIdx.x; v < ve; v += (u64)gridDim.x * blockDim.x) {
+    const u64 b = off[v], e = off[v + 1];
+    const bool ok = e >= b && e <= m;
+    if (!ok) mybad = 1;
+    deg[v] = ok ? (u32)(e - b) : 0u;
   }
-  mybad = (int)__reduce_or_sync(0xffffffffu, (unsigned)mybad);
-  if (lane == 0 && mybad) atomicOr(bad, mybad);
+  if (mybad) atomicOr(bad, 1);
 }
 
-__global__ void orient_write_kernel(const u64* __restrict__ off, const u32* __restrict__ col,
-                                    const u8* __restrict__ keep, u32 vb, u32 ve, u64 m,
-                                    const u64* __restrict__ doff, u32* __restrict__ dcol) {
-  const int lane = threadIdx.x & 31;
-  const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
-  const u64 nwarps = (gridDim.x * (u64)blockDim.x) >> 5;
-  for (u64 u = vb + warp; u < ve; u += nwarps) {
+// Edge-balanced orientation of a vertex range [vb, ve) whose out-lists are
+// the edge range [eb, ee) (graph.hpp:121-132): the DAG's column array is the
+// kept half-edges in their original order, so every pass is one thread per
+// edge or per vertex -- no warp walks a hub's list alone:
+//   src[i]  = source vertex of edge i (scatter at list starts + max-scan)
+//   keep[i] = (deg u, u) < (deg v, v), plus the graph.hpp:29-55 validation
+//   kpos    = exclusive scan of keep;  dcol[base + kpos[i]] = col[i]
+//   doff[u] = base + kpos[off[u] - eb]; base[k+1] = base[k] + kept in chunk k
+__global__ void src_mark_kernel(const u64* __restrict__ off, u32 vb, u32 ve, u64 eb, u32* __restrict__ src) {
+  for (u64 u = vb + blockIdx.x * (u64)blockDim.x + threadIdx.x; u < ve; u += (u64)gridDim.x * blockDim.x) {
     const u64 b = off[u], e = off[u + 1];
-    if (e < b || e > m) continue;  // invalid offsets: flagged by the count pass
-    u64 w = doff[u];
-    for (u64 i0 = b; i0 < e; i0 += 32) {
-      const u64 i = i0 + lane;
-      const bool k = i < e && keep[i];
-      const u32 mask = __ballot_sync(0xffffffffu, k);
-      if (k) dcol[w + __popc(mask & lanemask_lt())] = col[i];
-      w += __popc(mask);
-    }
+    if (e > b && b >= eb) src[b - eb] = (u32)u;
   }
 }
-
-// chunk [vb, ve) of a running exclusive scan: doff[v] += doff[vb-1] + cnt[vb-1]
-__global__ void add_base_kernel(u64* __restrict__ doff, const u64* __restrict__ cnt, u32 vb, u32 ve) {
-  const u64 base = vb ? doff[vb - 1] + cnt[vb - 1] : 0;
-  for (u64 v = vb + blockIdx.x * (u64)blockDim.x + threadIdx.x; v < ve; v += (u64)gridDim.x * blockDim.x)
-    doff[v] += base;
+__global__ void keep_kernel(const u64* __restrict__ off, const u32* __restrict__ col, const u32* __restrict__ deg,
+                            u32 n, u64 eb, u64 ee, const u32* __restrict__ src, int validate, u32* __restrict__ keep,
+                            int* __restrict__ bad) {
+  int mybad = 0;
+  for (u64 i = eb + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < ee; i += (u64)gridDim.x * blockDim.x) {
+    const u32 u = src[i - eb], v = col[i];
+    if (validate && !(v < n && v != u && (i == off[u] || col[i - 1] < v))) mybad = 2;
+    bool k = false;
+    if (v < n) {
+      const u32 du = deg[u], dv = deg[v];
+      k = du != dv ? du < dv : u < v;
+    }
+    keep[i - eb] = k ? 1u : 0u;
+  }
+  mybad = (int)__reduce_or_sync(__activemask(), (unsigned)mybad);
+  if (mybad && (threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicOr(bad, mybad);
 }
-// doff[n] = total; md = max out-degree
-__global__ void finish_offsets_kernel(u64* __restrict__ doff, const u64* __restrict__ cnt, u32 n,
-                                      u32* __restrict__ md) {
+__global__ void chunk_base_kernel(const u32* __restrict__ keep, const u32* __restrict__ kpos, u64 ne, u64* __restrict__ base,
+                                  int k) {
+  base[k + 1] = base[k] + (ne ? (u64)kpos[ne - 1] + keep[ne - 1] : 0);
+}
+__global__ void dag_write_kernel(const u32* __restrict__ col, const u32* __restrict__ keep, const u32* __restrict__ kpos,
+                                 u64 eb, u64 ee, const u64* __restrict__ base, int k, u32* __restrict__ dcol) {
+  const u64 b0 = base[k];
+  for (u64 i = eb + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < ee; i += (u64)gridDim.x * blockDim.x)
+    if (keep[i - eb]) dcol[b0 + kpos[i - eb]] = col[i];
+}
+__global__ void dag_off_kernel(const u64* __restrict__ off, u32 vb, u32 ve, u64 eb, u64 ee, const u32* __restrict__ kpos,
+                               const u64* __restrict__ base, int k, u64* __restrict__ doff, u32* __restrict__ md) {
+  const u64 b0 = base[k], tot = base[k + 1] - b0;
   u32 best = 0;
-  for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < n; v += (u64)gridDim.x * blockDim.x)
-    best = max(best, (u32)cnt[v]);
-  best = __reduce_max_sync(0xffffffffu, best);
-  if ((threadIdx.x & 31) == 0 && best) atomicMax(md, best);
-  if (blockIdx.x == 0 && threadIdx.x == 0) doff[n] = n ? doff[n - 1] + cnt[n - 1] : 0;
+  for (u64 u = vb + blockIdx.x * (u64)blockDim.x + threadIdx.x; u < ve; u += (u64)gridDim.x * blockDim.x) {
+    const u64 b = off[u], e = off[u + 1];
+    const u64 ks = b < ee ? kpos[b - eb] : tot, ke = e < ee ? kpos[e - eb] : tot;
+    doff[u] = b0 + ks;
+    best = max(best, (u32)(ke - ks));
+  }
+  best = __reduce_max_sync(__activemask(), best);
+  if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && best) atomicMax(md, best);
 }
+
+// doff[n] = total; md = max out-degree
 
 // level 1 of an undirected graph: per vertex, entries v > u (u<v rule).
 // max_v (off[v+1] - off[v]) -> *md (atomicMax per warp)
@@ -394,6 +356,41 @@ void set_max_degree(gpm_graph& out, cudaStream_t s) {
   GPM_CUDA(cudaStreamSynchronize(s));
 }
 
+// Orientation of chunk k = vertices [vb, ve), edges [eb, ee) of (off, col)
+// into (doff, dcol) with the edge-balanced passes above; base[k] must hold
+// the kept half-edges of the earlier chunks (base[0] = 0).
+struct OrientScratch {
+  DBuf<u32> src, keep, kpos;
+  DBuf<u8> tmax, tsum;
+  size_t nmax = 0, nsum = 0;
+  OrientScratch(u64 cap, cudaStream_t s) : src(std::max<u64>(1, cap), s), keep(std::max<u64>(1, cap), s),
+                                           kpos(std::max<u64>(1, cap), s) {
+    GPM_CUDA(cub::DeviceScan::InclusiveScan(nullptr, nmax, src.get(), src.get(), cuda::maximum<u32>{}, (int64_t)std::max<u64>(1, cap), s));
+    GPM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, nsum, keep.get(), kpos.get(), (int64_t)std::max<u64>(1, cap), s));
+    tmax.alloc(std::max<size_t>(1, nmax), s);
+    tsum.alloc(std::max<size_t>(1, nsum), s);
+  }
+};
+void orient_chunk(const u64* off, const u32* col, const u32* deg, u32 n, u32 vb, u32 ve, u64 eb, u64 ee, int validate,
+                  OrientScratch& X, u64* base, int k, u64* doff, u32* dcol, u32* md, int* bad, cudaStream_t s) {
+  const u64 ne = ee - eb;
+  const unsigned gv = std::min<unsigned>(grid_for(std::max<u32>(1, ve - vb), 256), 2368u);
+  const unsigned ge = std::min<unsigned>(grid_for(std::max<u64>(1, ne), 256), 4736u);
+  if (ne) {
+    GPM_CUDA(cudaMemsetAsync(X.src.get(), 0, sizeof(u32) * ne, s));
+    src_mark_kernel<<<gv, 256, 0, s>>>(off, vb, ve, eb, X.src.get());
+    GPM_CUDA(cub::DeviceScan::InclusiveScan(X.tmax.get(), X.nmax, X.src.get(), X.src.get(), cuda::maximum<u32>{},
+                                            (int64_t)ne, s));
+    keep_kernel<<<ge, 256, 0, s>>>(off, col, deg, n, eb, ee, X.src.get(), validate, X.keep.get(), bad);
+    GPM_CUDA(cub::DeviceScan::ExclusiveSum(X.tsum.get(), X.nsum, X.keep.get(), X.kpos.get(), (int64_t)ne, s));
+  }
+  chunk_base_kernel<<<1, 1, 0, s>>>(X.keep.get(), X.kpos.get(), ne, base, k);
+  if (ne) dag_write_kernel<<<ge, 256, 0, s>>>(col, X.keep.get(), X.kpos.get(), eb, ee, base, k, dcol);
+  if (ve > vb) dag_off_kernel<<<gv, 256, 0, s>>>(off, vb, ve, eb, ee, X.kpos.get(), base, k, doff, md);
+  GPM_CUDA(cudaGetLastError());
+}
+__global__ void dag_end_kernel(const u64* __restrict__ base, int k, u64* __restrict__ doff, u32 n) { doff[n] = base[k]; }
+
 void orient_on_device(const gpm_graph& g, gpm_graph& out) {
   cudaStream_t s = out.stream;
   out.n = g.n;
@@ -404,33 +401,34 @@ void orient_on_device(const gpm_graph& g, gpm_graph& out) {
   GPM_CUDA(cudaStreamSynchronize(g.stream));  // source graph ordered before our stream
   out.sz_off = sizeof(u64) * (g.n + 1);
   GPM_CUDA(dev_malloc((void**)&out.d_off, out.sz_off, s));
-  GPM_CUDA(cudaMemsetAsync(out.d_off + g.n, 0, sizeof(u64), s));
-  DBuf<u8> keep(std::max<u64>(1, g.m), s);
+  // the DAG keeps m/2 half-edges of a symmetric CSR; m bounds any input
+  out.sz_col = sizeof(u32) * std::max<u64>(1, g.m);
+  GPM_CUDA(dev_malloc((void**)&out.d_col, out.sz_col, s));
   DBuf<int> bad(1, s);
+  DBuf<u32> md(1, s), deg(std::max<u32>(1, g.n), s);
+  DBuf<u64> base(2, s);
   GPM_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+  GPM_CUDA(cudaMemsetAsync(md.get(), 0, sizeof(u32), s));
+  GPM_CUDA(cudaMemsetAsync(base.get(), 0, sizeof(u64), s));
   if (g.n) {
-    orient_count_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, g.n, g.m, 0, g.n, 0,
-                                                                    out.d_off, keep.get(), bad.get());
+    deg32_kernel<<<std::min<unsigned>(grid_for(g.n, 256), 2368u), 256, 0, s>>>(g.d_off, 0, g.n, g.m, deg.get(), bad.get());
     GPM_CUDA(cudaGetLastError());
   }
-  exclusive_scan_u64(out.d_off, g.n + 1, s);
+  OrientScratch X(g.m, s);
+  orient_chunk(g.d_off, g.d_col, deg.get(), g.n, 0, g.n, 0, g.m, 0, X, base.get(), 0, out.d_off, out.d_col, md.get(),
+               bad.get(), s);
+  dag_end_kernel<<<1, 1, 0, s>>>(base.get(), 1, out.d_off, g.n);
+  GPM_CUDA(cudaGetLastError());
   u64 m = 0;
   GPM_CUDA(cudaMemcpyAsync(&m, out.d_off + g.n, sizeof(u64), cudaMemcpyDeviceToHost, s));
-  GPM_CUDA(cudaStreamSynchronize(s));
-  out.m = m;
-  out.sz_col = sizeof(u32) * std::max<u64>(1, m);
-  GPM_CUDA(dev_malloc((void**)&out.d_col, out.sz_col, s));
-  if (g.n && m) {
-    orient_write_kernel<<<grid_for((u64)g.n * 32, 256), 256, 0, s>>>(g.d_off, g.d_col, keep.get(), 0, g.n, g.m,
-                                                                    out.d_off, out.d_col);
-    GPM_CUDA(cudaGetLastError());
-  }
+  GPM_CUDA(cudaMemcpyAsync(&out.max_deg, md.get(), sizeof(u32), cudaMemcpyDeviceToHost, s));
   if (g.labeled) {
     out.sz_lab = sizeof(u32) * std::max<u32>(1, g.n);
     GPM_CUDA(dev_malloc((void**)&out.d_lab, out.sz_lab, s));
     GPM_CUDA(cudaMemcpyAsync(out.d_lab, g.d_lab, sizeof(u32) * g.n, cudaMemcpyDeviceToDevice, s));
   }
-  set_max_degree(out, s);
+  GPM_CUDA(cudaStreamSynchronize(s));
+  out.m = m;
 }
 
 // Host CSR -> device DAG in one pipelined call: the column array is copied in
@@ -456,8 +454,6 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
   StreamGuard early{cs};  // owns cs until the buffers below exist
   DBuf<u64> uoff(n + 1, s);
   DBuf<u32> ucol(std::max<u64>(1, m), s);
-  DBuf<u8> keep(std::max<u64>(1, m), s);
-  DBuf<u64> cnt(std::max<u32>(1, n), s);
   DBuf<int> bad(1, s);
   DBuf<u32> md(1, s);
   // declared after the buffers, so it is destroyed first: on an exception the
@@ -475,7 +471,28 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
   GPM_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   GPM_CUDA(cudaEventRecord(ready, s));  // allocations visible to the copy stream
   GPM_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+  // GPM_TRACE: device timeline of the copies and the per-chunk orientation
+  static const bool tr = std::getenv("GPM_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto tmark = [&](cudaStream_t st) {
+    if (!tr) return;
+    cudaEvent_t e;
+    GPM_CUDA(cudaEventCreate(&e));
+    GPM_CUDA(cudaEventRecord(e, st));
+    tev.push_back(e);
+  };
+  const auto th0 = std::chrono::steady_clock::now();
+  tmark(cs);
   GPM_CUDA(cudaMemcpyAsync(uoff.get(), h_off, sizeof(u64) * (n + 1), cudaMemcpyHostToDevice, cs));
+  tmark(cs);
+  // degrees (u32) as soon as the offsets have landed
+  DBuf<u32> deg(std::max<u32>(1, n), s);
+  cudaEvent_t offev;
+  GPM_CUDA(cudaEventCreateWithFlags(&offev, cudaEventDisableTiming));
+  GPM_CUDA(cudaEventRecord(offev, cs));
+  GPM_CUDA(cudaStreamWaitEvent(s, offev, 0));
+  if (n) deg32_kernel<<<std::min<unsigned>(grid_for(n, 256), 2368u), 256, 0, s>>>(uoff.get(), 0, n, m, deg.get(), bad.get());
+  GPM_CUDA(cudaGetLastError());
   const int K = m > (u64(1) << 22) ? 8 : 1;
   std::vector<cudaEvent_t> evs;
   std::vector<std::pair<u32, u32>> ranges;
@@ -489,31 +506,25 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
     if (ee > eb)
       GPM_CUDA(cudaMemcpyAsync(ucol.get() + eb, h_col + eb, sizeof(u32) * (ee - eb), cudaMemcpyHostToDevice, cs));
     cudaEvent_t ev;
-    GPM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    GPM_CUDA(cudaEventCreateWithFlags(&ev, tr ? 0 : cudaEventDisableTiming));
     GPM_CUDA(cudaEventRecord(ev, cs));
     evs.push_back(ev);
     ranges.emplace_back(vb, vend);
     vb = vend;
   }
-  size_t tmp = 0;
-  u32 maxr = 1;
-  for (auto [a, b] : ranges) maxr = std::max(maxr, b - a);
-  GPM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), out.d_off, maxr, s));
-  DBuf<u8> ttmp(std::max<size_t>(1, tmp), s);
+  u64 maxe = 1;
+  for (auto [a, b] : ranges) maxe = std::max<u64>(maxe, h_off[b] - h_off[a]);
+  OrientScratch X(maxe, s);
+  DBuf<u64> base(ranges.size() + 1, s);
+  GPM_CUDA(cudaMemsetAsync(base.get(), 0, sizeof(u64), s));
   for (size_t k = 0; k < ranges.size(); ++k) {
     const auto [rb, re] = ranges[k];
     GPM_CUDA(cudaStreamWaitEvent(s, evs[k], 0));
-    orient_count_kernel<<<grid_for((u64)(re - rb) * 32, 256), 256, 0, s>>>(uoff.get(), ucol.get(), n, m, rb, re, 1,
-                                                                          cnt.get(), keep.get(), bad.get());
-    GPM_CUDA(cudaGetLastError());
-    GPM_CUDA(cub::DeviceScan::ExclusiveSum(ttmp.get(), tmp, cnt.get() + rb, out.d_off + rb, re - rb, s));
-    add_base_kernel<<<grid_for(re - rb, 256), 256, 0, s>>>(out.d_off, cnt.get(), rb, re);
-    orient_write_kernel<<<grid_for((u64)(re - rb) * 32, 256), 256, 0, s>>>(uoff.get(), ucol.get(), keep.get(), rb, re, m,
-                                                                          out.d_off, out.d_col);
-    GPM_CUDA(cudaGetLastError());
+    orient_chunk(uoff.get(), ucol.get(), deg.get(), n, rb, re, h_off[rb], h_off[re], 1, X, base.get(), (int)k, out.d_off,
+                 out.d_col, md.get(), bad.get(), s);
+    tmark(s);
   }
-  finish_offsets_kernel<<<std::min<unsigned>(grid_for(std::max<u32>(1, n), 256), 1184u), 256, 0, s>>>(out.d_off,
-                                                                                                 cnt.get(), n, md.get());
+  dag_end_kernel<<<1, 1, 0, s>>>(base.get(), (int)ranges.size(), out.d_off, n);
   GPM_CUDA(cudaGetLastError());
   if (labels) {
     out.sz_lab = sizeof(u32) * std::max<u32>(1, n);
@@ -524,9 +535,28 @@ void create_dag_pipelined(const u64* h_off, const u32* h_col, const u32* labels,
   GPM_CUDA(cudaMemcpyAsync(&dm, out.d_off + n, sizeof(u64), cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaMemcpyAsync(&out.max_deg, md.get(), sizeof(u32), cudaMemcpyDeviceToHost, s));
+  tmark(s);
   GPM_CUDA(cudaStreamSynchronize(s));
+  if (tr) {
+    const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
+    std::fprintf(stderr, "[gpm dag] host %.3f ms; device marks (ms from the first copy):", host_ms);
+    for (size_t i = 1; i < tev.size(); ++i) {
+      float t = 0;
+      cudaEventElapsedTime(&t, tev[0], tev[i]);
+      std::fprintf(stderr, " %.3f", t);
+    }
+    std::fprintf(stderr, "  (off copied, orient chunk 1..K, end); copies done:");
+    for (auto e : evs) {
+      float t = 0;
+      cudaEventElapsedTime(&t, tev[0], e);
+      std::fprintf(stderr, " %.3f", t);
+    }
+    std::fprintf(stderr, "\n");
+    for (auto e : tev) cudaEventDestroy(e);
+  }
   for (auto e : evs) cudaEventDestroy(e);
   cudaEventDestroy(ready);
+  cudaEventDestroy(offev);
   if (hb & 1) throw Error(GPM_EINVAL, "row_offsets not non-decreasing / out of range");
   if (hb & 2) throw Error(GPM_EINVAL, "neighbor list not strictly ascending, self-loop, or id out of range");
   out.n = n;
