@@ -86,11 +86,17 @@ __device__ __forceinline__ u32 hb_find(const u32* T, u32 sh, u32 bmask, u32 v) {
   }
 }
 
-// Classifies the roots of the slice (thread per vertex: the roots whose
-// out-edge range meets [lo, hi)).
+// Classifies the roots of the slice (thread per vertex whose out-edge range
+// meets [lo, hi)): medium / big roots are appended to their lists; every
+// 32-edge block b gets item_root[b] = the first vertex whose list starts at
+// or after 32 b (written by exactly that vertex: no atomics), from which the
+// warp item scans the small roots that start inside the block.
 __global__ void local_prep_kernel(LocalArgs a) {
   for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < a.g.n; v += (u64)gridDim.x * blockDim.x) {
     const u64 ob = ldg(a.g.off + v), oe = ldg(a.g.off + v + 1);
+    // blocks b in [blo, blo + nblk) with prev < 32 b <= ob (prev = start of v - 1)
+    const u64 b0 = max(v ? ldg(a.g.off + v - 1) / 32 + 1 : 0, a.blo), b1 = ob / 32 + 1;  // b in [b0, b1)
+    for (u64 b = b0; b < b1 && b < a.blo + a.nblk; ++b) a.item_root[b - a.blo] = (u32)v;
     if (oe <= a.lo || ob >= a.hi || ob == oe) continue;
     const u64 d = oe - ob;
     if (ob < a.lo || oe > a.hi || d > kMidMax) {
@@ -102,8 +108,6 @@ __global__ void local_prep_kernel(LocalArgs a) {
     } else if (d > 32) {
       const unsigned long long i = atomicAdd(a.nmid, 1ull);
       a.mid[i] = (u32)v;
-    } else {
-      atomicMin(a.item_root + (ob / 32 - a.blo), (u32)v);
     }
   }
 }
@@ -138,7 +142,7 @@ using MidCfg = WarpCfg<128, 256, 4, 256, 4, 2>;    // roots of out-degree in (64
 template <class C>
 struct WarpSmem {
   uint4 T[C::kBuckets];           // keys (kEmpty = free)
-  u32 F[256];                     // 8192-bit filter of the keys (word = hash bits 16..23, bit = 27..31)
+  u32 F[256];                     // 8192-bit blocked Bloom filter of the keys (2 bits per key)
   u8 V[C::kBuckets * 4];          // local position of the key in its root's list
   u32 rows[C::kKeys * C::kWords];
   __align__(16) u32 wm[C::kWin + C::kUnroll];  // per window: bit p = an entry starts at window position p
@@ -315,7 +319,9 @@ __global__ void __launch_bounds__(kSmallThreads, C::kMinBlocks) local_warp_kerne
         const u32 w = ldg(g.col + S.rb[r] + j);
         const u32 key = (w << 5) | r;
         const u32 hv = key * kHashMul;
-        atomicOr(S.F + ((hv >> 16) & 255u), 1u << (hv >> 27));  // filter index: hash bits 16..23, 27..31
+        // filter: word = hash bits 16..23, two bits = bits 27..31 and 11..15
+        // (a blocked Bloom filter: ~0.03 % false positives at 64 keys)
+        atomicOr(S.F + ((hv >> 16) & 255u), (1u << (hv >> 27)) | (1u << ((hv >> 11) & 31u)));
         kfw[rr] = (hv >> 16) & 255u;
         u32 b = hv >> sh;
         for (u32 probe = 0;; ++probe) {
@@ -415,17 +421,19 @@ __global__ void __launch_bounds__(kSmallThreads, C::kMinBlocks) local_warp_kerne
       // the shared-memory wavefronts) only for filter-positive lanes, which
       // are rare: any positive lane re-probes its 4 keys exactly
       auto probe = [&](const u32 (&uq)[4], const u32 (&sq)[4], const u32 (&eq)[4]) {
-        u32 key[4];
-        bool any = false;
+        u32 key[4], pm = 0;  // pm: windows whose key passed the filter
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           key[q] = (uq[q] << 5) | sq[q];
           const u32 hv = key[q] * kHashMul;
-          any |= (S.F[__byte_perm(hv, 0, 0x4442)] >> (hv >> 27)) & 1u;
+          const u32 f = S.F[__byte_perm(hv, 0, 0x4442)];
+          const u32 m2 = (1u << (hv >> 27)) | (1u << ((hv >> 11) & 31u));
+          pm |= (u32)((f & m2) == m2) << q;
         }
-        if (any) {
+        if (pm) {  // rare: true hits (~0.3 % of candidates) and filter false positives
 #pragma unroll
-          for (int q = 0; q < 4; ++q) hit(key[q], eq[q]);
+          for (int q = 0; q < 4; ++q)
+            if (pm & (1u << q)) hit(key[q], eq[q]);  // static indices: key / eq stay in registers
         }
       };
       {
@@ -789,9 +797,16 @@ bool cf_local_roots(Ctx& c, const u32*, u64 slo, u64 shi) {
   rec[1] = launch_warp<MidCfg, true>(c, a, (bigcap + 7) / 8, "extend_local_mid", ss);
   const u32 dmax = std::max<u32>(kMidMax + 1, c.G->max_deg);
   const size_t smem = 4 * (size_t)BigLayout(dmax).words;
-  GPM_CUDA(cudaFuncSetAttribute(local_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int ob = 0;
-  GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, local_big_kernel, kBigThreads, smem));
+  // attribute + occupancy once per shared-memory size (per thread: the
+  // attribute is per device and threads may run on different devices)
+  static thread_local std::pair<size_t, int> big_occ{0, 0};
+  if (big_occ.first != smem) {
+    GPM_CUDA(cudaFuncSetAttribute(local_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int o = 0;
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, local_big_kernel, kBigThreads, smem));
+    big_occ = {smem, o};
+  }
+  const int ob = big_occ.second;
   const u64 bb = std::max<u64>(1, std::min<u64>((u64)c.sms * std::max(1, ob), bigcap));
   rec[2] = tl_begin_on(*c.tl, "extend_local_big", ss);
   local_big_kernel<<<(unsigned)bb, kBigThreads, smem, ss>>>(a, dmax);
