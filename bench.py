@@ -56,6 +56,19 @@ METRIC = "embeddings explored/sec (N_explored = |L1| + accepted per extend level
 UNIT = "embeddings/s"
 
 
+L2_RESIDENT = ("cf4", "tc", "fsm")
+_L2_PEAK = []
+
+
+def l2_read_peak():
+    """L2 read GB/s, measured once per process on cuda:0 (64 MiB working set)."""
+    if not _L2_PEAK:
+        import torch
+        import paper_1911_06969_b200 as P
+        _L2_PEAK.append(P.probe_read_bandwidth(64 << 20, torch.cuda.current_device(), 10))
+    return _L2_PEAK[0]
+
+
 def load_peaks():
     for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
         if os.path.exists(p):
@@ -471,6 +484,14 @@ def main():
             if l2_bytes:
                 mem_rates["l2_bytes_per_launch"] = l2_bytes
                 mem_rates["l2_gbs"] = l2_bytes / (dms / 1e3) / 1e9
+        # L2-resident CSRs (the PAT DAG is 76 MB, TC16 / FSM17 smaller; L2 is
+        # 126 MB): their kernels stream the CSR from L2, so the L2 read rate is
+        # the roofline that bounds them (measured, stated)
+        if name in L2_RESIDENT and dms > 0:
+            l2_peak = l2_read_peak()
+            mem_rates["l2"] = {"achieved_gbs": achieved, "peak_gbs": l2_peak, "frac": achieved / l2_peak,
+                               "peak_kind": ("builder-measured in this run: gpm_probe_read_bandwidth over a 64 MiB "
+                                             "device buffer (16-byte __ldcg loads, persistent grid, best of 10)")}
         pats = res.patterns
         result = {"total": res.total, "n_explored": n_explored, "level_sizes": res.stats["level_sizes"],
                   "candidates": res.stats["candidates"], "patterns": len(pats),

@@ -283,6 +283,12 @@ int gpm_canonicalize_batch(int device, int nv, uint64_t count, const uint32_t* l
  * allocators.  device < 0: every device. */
 int gpm_release_cached(int device);
 
+/* Diagnostic: best-of-`reps` read bandwidth (GB/s) of one persistent grid of
+ * 16-byte loads over a `bytes` device buffer -- 64 MiB measures the L2 read
+ * rate the L2-resident workloads' roofline uses (bench.py roofline.l2), a few
+ * GiB the HBM read rate.  Not on the mining path. */
+int gpm_probe_read_bandwidth(int device, uint64_t bytes, int reps, double* gbs);
+
 const char* gpm_last_error(void);
 const char* gpm_version(void);
 

@@ -25,7 +25,7 @@ EXPORTS = [
     "gpm_last_error", "gpm_version", "gpm_steal_create", "gpm_steal_open", "gpm_steal_reset", "gpm_steal_release",
     "gpm_release_cached", "gpm_csr_save", "gpm_csr_load", "gpm_load_cached",
     "gpm_canonicalize_batch", "gpm_nccl_unique_id", "gpm_exchange_nccl_create", "gpm_exchange_nccl_wrap",
-    "gpm_exchange_nccl_fn", "gpm_exchange_nccl_destroy",
+    "gpm_exchange_nccl_fn", "gpm_exchange_nccl_destroy", "gpm_probe_read_bandwidth",
 ]
 
 
@@ -123,6 +123,7 @@ def lib():
         "gpm_steal_reset": (i32, [vp, i32, vp]),
         "gpm_steal_release": (i32, [vp, i32]),
         "gpm_release_cached": (i32, [i32]),
+        "gpm_probe_read_bandwidth": (i32, [i32, u64, i32, C.POINTER(C.c_double)]),
         "gpm_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():

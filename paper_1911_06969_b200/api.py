@@ -388,6 +388,14 @@ def canonicalize(patterns, nv: int, device: int = 0) -> List[Tuple[str, List[int
     return out
 
 
+def probe_read_bandwidth(nbytes: int, device: int = 0, reps: int = 10) -> float:
+    """Best-of-reps read GB/s over an nbytes device buffer (64 MiB: the L2
+    read rate; GiBs: HBM) -- the L2 roofline denominator of bench.py."""
+    v = C.c_double()
+    check(lib().gpm_probe_read_bandwidth(device, nbytes, reps, C.byref(v)))
+    return v.value
+
+
 def release_cached(device: int = -1) -> None:
     """Hands the library's cached >= 64 MiB device buffers back to the driver
     (gpm_release_cached); device < 0: every device."""
