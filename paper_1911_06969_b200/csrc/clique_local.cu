@@ -219,7 +219,6 @@ __device__ __forceinline__ void count_subtree(const u32* rows, const u32* dp, u3
 // out-degree in (64, 128] (a.mid2).
 template <class C, bool MID>
 __global__ void __launch_bounds__(kSmallThreads, C::kMinBlocks) local_warp_kernel(LocalArgs a) {
-  constexpr int NW = kSmallThreads / 32;
   extern __shared__ __align__(16) unsigned char wsm[];
   WarpSmem<C>* const s_w = reinterpret_cast<WarpSmem<C>*>(wsm);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

@@ -43,8 +43,8 @@ constexpr int kT = 256;
 constexpr int kWarps = kT / 32;
 constexpr u32 kWSlots = 1024;   // per-warp hash slots (4 KB): load <= 1/8 up to kWKeys
 constexpr u32 kWKeys = 256;     // roots with |S0| <= this use the warp kernel (load <= 1/4)
-constexpr u32 kBSlots = 8192;   // per-CTA hash slots (32 KB)
-constexpr u32 kBKeys = 1024;    // S0 tile of the block kernel (load 1/8)
+constexpr u32 kBSlots = 8192;   // default per-CTA hash slots (32 KB)
+constexpr u32 kBKeys = 1024;    // default S0 tile of the block kernel (load 1/8)
 constexpr u32 kPB = 4096;       // parents per block item (warps grab 32 at a time)
 
 // first index i in [b, e) with col[i] >= key
@@ -71,11 +71,12 @@ struct Mc3Args {
   unsigned long long* cand;
   unsigned long long* moved;  // [0] streamed candidates, [1] staged keys, [2] parent visits, [3] pos-0 counted
   u32 codeT, codeW0, codeW1;
+  u32 bkeys, bslots;          // block kernel: S0 tile keys, hash slots (shared memory)
 };
 
 // Per-root item counts.  small: |S0| <= kWKeys -> ceil(npar/32) warp items;
 // big: ntiles * ceil(npar/kPB) block items.
-__global__ void mc3_items_kernel(const u64* __restrict__ l1s, u64 lo, u64 hi, u32 vlo, u32 nr,
+__global__ void mc3_items_kernel(const u64* __restrict__ l1s, u64 lo, u64 hi, u32 vlo, u32 nr, u32 bkeys,
                                  u64* __restrict__ small, u64* __restrict__ big) {
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nr; i += (u64)gridDim.x * blockDim.x) {
     const u32 r = vlo + (u32)i;
@@ -86,7 +87,7 @@ __global__ void mc3_items_kernel(const u64* __restrict__ l1s, u64 lo, u64 hi, u3
     u64 cs = 0, cb = 0;
     if (np) {
       if (ns <= kWKeys) cs = (np + 31) / 32;
-      else cb = ((ns + kBKeys - 1) / kBKeys) * ((np + kPB - 1) / kPB);
+      else cb = ((ns + bkeys - 1) / bkeys) * ((np + kPB - 1) / kPB);
     }
     small[i] = cs;
     big[i] = cb;
@@ -319,13 +320,13 @@ __global__ void __launch_bounds__(kT, 4) mc3_block_kernel(Mc3Args a) {
     const u64 sb = oe - ns;
     const u64 pa0 = max(s, a.lo), pe = min(e, a.hi);
     const u64 nch = (pe - pa0 + kPB - 1) / kPB;
-    const u32 ntiles = (ns + kBKeys - 1) / kBKeys;
+    const u32 ntiles = (ns + a.bkeys - 1) / a.bkeys;
     const u64 q = item - ldg(a.istart + rr);
     const u32 t = (u32)(q / nch);
     const u64 c = q % nch;
-    const u32 k0 = t * kBKeys, k1 = min(ns, k0 + kBKeys);
+    const u32 k0 = t * a.bkeys, k1 = min(ns, k0 + a.bkeys);
     u32 cap = 1024;  // table sized to the tile: load <= 1/8, cleared in O(cap)
-    while (cap < 8 * (k1 - k0) && cap < kBSlots) cap <<= 1;
+    while (cap < 8 * (k1 - k0) && cap < a.bslots) cap <<= 1;
     u32 sh, mask;
     hb_geom(cap, sh, mask);
     for (u32 i = threadIdx.x * 4; i < cap; i += kT * 4)
@@ -777,7 +778,11 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
   DBuf<u64> ismall(nr + 1, s), ibig(nr + 1, s);
   GPM_CUDA(cudaMemsetAsync(ismall.get() + nr, 0, sizeof(u64), s));
   GPM_CUDA(cudaMemsetAsync(ibig.get() + nr, 0, sizeof(u64), s));
-  mc3_items_kernel<<<grid1(nr), 256, 0, s>>>(l1s, lo, hi, vr[0], nr, ismall.get(), ibig.get());
+  // block-kernel tile: GPM_MC3_TILE keys (default kBKeys) at load <= 1/4..1/8
+  static const u32 tile_env = std::getenv("GPM_MC3_TILE") ? (u32)std::atoi(std::getenv("GPM_MC3_TILE")) : 0u;
+  const u32 bkeys = tile_env ? tile_env : kBKeys;
+  const u32 bslots = std::max<u32>(kBSlots, bkeys * 4 > kBSlots ? (bkeys * 4 + 1023) & ~1023u : kBSlots);
+  mc3_items_kernel<<<grid1(nr), 256, 0, s>>>(l1s, lo, hi, vr[0], nr, bkeys, ismall.get(), ibig.get());
   GPM_CUDA(cudaGetLastError());
   scan_inplace(ismall.get(), nr + 1, s);
   scan_inplace(ibig.get(), nr + 1, s);
@@ -806,6 +811,8 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
   a.codeT = (1u << pat::pair_index(0, 1, 3)) | (1u << pat::pair_index(0, 2, 3)) | (1u << pat::pair_index(1, 2, 3));
   a.codeW0 = (1u << pat::pair_index(0, 1, 3)) | (1u << pat::pair_index(0, 2, 3));
   a.codeW1 = (1u << pat::pair_index(0, 1, 3)) | (1u << pat::pair_index(1, 2, 3));
+  a.bkeys = bkeys;
+  a.bslots = bslots;
   const int sms = sm_count();
   size_t rec = tl.recs.size();
   if (NS) {
@@ -831,14 +838,15 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
     ++tl.launches;
   }
   if (NB) {
-    const size_t smem = kBSlots * sizeof(u32);
-    static std::atomic<int> occb_slot{0};
-    const int occb = cached_occupancy(occb_slot, [&] {
+    const size_t smem = (size_t)bslots * sizeof(u32);
+    static thread_local std::pair<size_t, int> occb_c{0, 0};
+    if (occb_c.first != smem) {
       GPM_CUDA(cudaFuncSetAttribute(mc3_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int o = 0;
       GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, mc3_block_kernel, kT, smem));
-      return o;
-    });
+      occb_c = {smem, std::max(1, o)};
+    }
+    const int occb = occb_c.second;
     const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sms * occb, NB));
     Mc3Args b = a;
     b.istart = ibig.get();
