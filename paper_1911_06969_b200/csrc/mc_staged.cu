@@ -44,7 +44,7 @@ constexpr int kWarps = kT / 32;
 constexpr u32 kWSlots = 1024;   // per-warp hash slots (4 KB): load <= 1/8 up to kWKeys
 constexpr u32 kWKeys = 256;     // roots with |S0| <= this use the warp kernel (load <= 1/4)
 constexpr u32 kBSlots = 8192;   // default per-CTA hash slots (32 KB)
-constexpr u32 kBKeys = 1024;    // default S0 tile of the block kernel (load 1/8)
+constexpr u32 kBKeys = 2048;    // default S0 tile of the block kernel (load 1/4; 1024: 130.8 ms, 2048: 127.5 ms on LJ22)
 constexpr u32 kPB = 4096;       // parents per block item (warps grab 32 at a time)
 
 // first index i in [b, e) with col[i] >= key
