@@ -86,30 +86,34 @@ __device__ __forceinline__ u32 hb_find(const u32* T, u32 sh, u32 bmask, u32 v) {
   }
 }
 
+// warp-aggregated append of v to list (one atomic per warp and list)
+__device__ __forceinline__ void warp_append(bool take, u32 v, u32* list, unsigned long long* n) {
+  const u32 m = __ballot_sync(__activemask(), take);
+  if (!m) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(n, (unsigned long long)__popc(m));
+  base = __shfl_sync(__activemask(), base, leader);
+  if (take) list[base + __popc(m & lanemask_lt())] = v;
+}
+
 // Classifies the roots of the slice (thread per vertex whose out-edge range
 // meets [lo, hi)): medium / big roots are appended to their lists; every
 // 32-edge block b gets item_root[b] = the first vertex whose list starts at
 // or after 32 b (written by exactly that vertex: no atomics), from which the
 // warp item scans the small roots that start inside the block.
 __global__ void local_prep_kernel(LocalArgs a) {
-  for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < a.g.n; v += (u64)gridDim.x * blockDim.x) {
-    const u64 ob = ldg(a.g.off + v), oe = ldg(a.g.off + v + 1);
-    // blocks b in [blo, blo + nblk) with prev < 32 b <= ob (prev = start of v - 1)
-    const u64 b0 = max(v ? ldg(a.g.off + v - 1) / 32 + 1 : 0, a.blo), b1 = ob / 32 + 1;  // b in [b0, b1)
-    for (u64 b = b0; b < b1 && b < a.blo + a.nblk; ++b) a.item_root[b - a.blo] = (u32)v;
-    if (oe <= a.lo || ob >= a.hi || ob == oe) continue;
-    const u64 d = oe - ob;
-    if (ob < a.lo || oe > a.hi || d > kMidMax) {
-      const unsigned long long i = atomicAdd(a.nbig, 1ull);
-      a.big[i] = (u32)v;
-    } else if (d > 64) {
-      const unsigned long long i = atomicAdd(a.nmid2, 1ull);
-      a.mid2[i] = (u32)v;
-    } else if (d > 32) {
-      const unsigned long long i = atomicAdd(a.nmid, 1ull);
-      a.mid[i] = (u32)v;
-    }
-  }
+  const u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x;  // one vertex per thread
+  if (v >= a.g.n) return;
+  const u64 ob = ldg(a.g.off + v), oe = ldg(a.g.off + v + 1);
+  const u64 b0 = max(v ? ldg(a.g.off + v - 1) / 32 + 1 : 0, a.blo), b1 = ob / 32 + 1;  // b in [b0, b1)
+  for (u64 b = b0; b < b1 && b < a.blo + a.nblk; ++b) a.item_root[b - a.blo] = (u32)v;
+  const bool in = !(oe <= a.lo || ob >= a.hi || ob == oe);
+  const u64 d = oe - ob;
+  const bool big = in && (ob < a.lo || oe > a.hi || d > kMidMax);
+  warp_append(big, (u32)v, a.big, a.nbig);
+  warp_append(in && !big && d > 64, (u32)v, a.mid2, a.nmid2);
+  warp_append(in && !big && d > 32 && d <= 64, (u32)v, a.mid, a.nmid);
 }
 
 // ---------------------------------------------------------------------------
@@ -775,7 +779,7 @@ bool cf_local_roots(Ctx& c, const u32*, u64 slo, u64 shi) {
   a.acc = ctl.get() + kCtl;
   a.total = c.d_total;
   a.k = c.k;
-  const unsigned pg = (unsigned)std::max<u64>(1, std::min<u64>((c.G->n + 255) / 256, (u64)c.sms * 8));
+  const unsigned pg = (unsigned)std::max<u64>(1, (c.G->n + 255) / 256);
   local_prep_kernel<<<pg, 256, 0, c.s>>>(a);
   GPM_CUDA(cudaGetLastError());
   // fork: medium-2 and big roots on the side stream, small items here
