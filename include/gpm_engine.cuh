@@ -932,7 +932,11 @@ void mine(const gpm_graph& G0, const gpm_config& cfg, cudaStream_t s, gpm_result
       tsum += thi[r] - tlo[r];
     }
     run_slice(lo, tlo[cfg.rank]);
-    const u64 chunk = cfg.steal_chunk ? cfg.steal_chunk : std::max<u64>(1024, tsum / ((u64)world * 32));
+    // k-CL on local rows pays a fixed ~50 us per slice (prep, launches, one
+    // host sync): coarser tail chunks there
+    const bool local_rows = builtin<App>::value == kBuiltinClique && cf_local_applicable(*G, k, c.list_fn != nullptr);
+    const u64 chunk = cfg.steal_chunk ? cfg.steal_chunk
+                                      : std::max<u64>(local_rows ? 65536 : 1024, tsum / ((u64)world * (local_rows ? 4 : 32)));
     DBuf<u64> d_t(2 * world, s), d_out(2, s);
     GPM_CUDA(cudaMemcpyAsync(d_t.get(), tlo.data(), sizeof(u64) * world, cudaMemcpyHostToDevice, s));
     GPM_CUDA(cudaMemcpyAsync(d_t.get() + world, thi.data(), sizeof(u64) * world, cudaMemcpyHostToDevice, s));

@@ -59,6 +59,7 @@ struct LocalArgs {
   unsigned long long* ctr;   // [0] small-item grabs, [1] big-root grabs, [2] medium-root grabs
   unsigned long long* acc;   // [3][kAcc]: small, medium, big
   unsigned long long* total; // last-level count (engine d_total)
+  u32* vr;                   // vertex range of the slice (device)
   int k;
 };
 
@@ -102,18 +103,52 @@ __device__ __forceinline__ void warp_append(bool take, u32 v, u32* list, unsigne
 // 32-edge block b gets item_root[b] = the first vertex whose list starts at
 // or after 32 b (written by exactly that vertex: no atomics), from which the
 // warp item scans the small roots that start inside the block.
+__global__ void local_vrange_kernel(LocalArgs a) {
+  // vr[0] = root of edge lo (last v with off[v] <= lo); vr[1] = first v with off[v] >= hi
+  if (threadIdx.x > 1) return;
+  const u64 key = threadIdx.x == 0 ? a.lo : a.hi;
+  u64 l = 0, h = a.g.n;
+  if (threadIdx.x == 0) {
+    while (l < h) {  // last v in [0, n) with off[v] <= lo
+      const u64 mid = (l + h + 1) >> 1;
+      if (ldg(a.g.off + mid) <= key) l = mid;
+      else h = mid - 1;
+    }
+  } else {
+    while (l < h) {  // first v with off[v] >= hi
+      const u64 mid = (l + h) >> 1;
+      if (ldg(a.g.off + mid) < key) l = mid + 1;
+      else h = mid;
+    }
+  }
+  a.vr[threadIdx.x] = (u32)l;
+  // block blo's lower-bound vertex may precede the slice (its list starts
+  // before lo): scanning block blo from the root of edge lo finds every
+  // small root that starts inside the slice (the prep may lower it no further)
+  if (threadIdx.x == 0 && a.nblk) a.item_root[0] = (u32)l;
+}
+
 __global__ void local_prep_kernel(LocalArgs a) {
-  const u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x;  // one vertex per thread
-  if (v >= a.g.n) return;
-  const u64 ob = ldg(a.g.off + v), oe = ldg(a.g.off + v + 1);
-  const u64 b0 = max(v ? ldg(a.g.off + v - 1) / 32 + 1 : 0, a.blo), b1 = ob / 32 + 1;  // b in [b0, b1)
-  for (u64 b = b0; b < b1 && b < a.blo + a.nblk; ++b) a.item_root[b - a.blo] = (u32)v;
-  const bool in = !(oe <= a.lo || ob >= a.hi || ob == oe);
-  const u64 d = oe - ob;
-  const bool big = in && (ob < a.lo || oe > a.hi || d > kMidMax);
-  warp_append(big, (u32)v, a.big, a.nbig);
-  warp_append(in && !big && d > 64, (u32)v, a.mid2, a.nmid2);
-  warp_append(in && !big && d > 32 && d <= 64, (u32)v, a.mid, a.nmid);
+  // the slice's vertex range [vr[0], vr[1]] (grid-stride: any grid covers it)
+  const u64 vend = ((u64)a.vr[1] + 1 < (u64)a.g.n) ? (u64)a.vr[1] + 1 : (u64)a.g.n;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 vb = a.vr[0] + blockIdx.x * (u64)blockDim.x; vb < vend; vb += stride) {
+    const u64 v = vb + threadIdx.x;
+    const bool valid = v < vend;
+    u64 ob = 0, oe = 0;
+    if (valid) {
+      ob = ldg(a.g.off + v);
+      oe = ldg(a.g.off + v + 1);
+      const u64 b0 = max(v ? ldg(a.g.off + v - 1) / 32 + 1 : 0, a.blo), b1 = ob / 32 + 1;  // b in [b0, b1)
+      for (u64 b = b0; b < b1 && b < a.blo + a.nblk; ++b) a.item_root[b - a.blo] = (u32)v;
+    }
+    const bool in = valid && !(oe <= a.lo || ob >= a.hi || ob == oe);
+    const u64 d = oe - ob;
+    const bool big = in && (ob < a.lo || oe > a.hi || d > kMidMax);
+    warp_append(big, (u32)v, a.big, a.nbig);
+    warp_append(in && !big && d > 64, (u32)v, a.mid2, a.nmid2);
+    warp_append(in && !big && d > 32 && d <= 64, (u32)v, a.mid, a.nmid);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -779,7 +814,13 @@ bool cf_local_roots(Ctx& c, const u32*, u64 slo, u64 shi) {
   a.acc = ctl.get() + kCtl;
   a.total = c.d_total;
   a.k = c.k;
-  const unsigned pg = (unsigned)std::max<u64>(1, (c.G->n + 255) / 256);
+  // the slice's vertices: at most (hi - lo) non-empty ones plus the empty
+  // vertices between them; whole-graph bound when that is smaller
+  DBuf<u32> vr(2, c.s);
+  a.vr = vr.get();
+  local_vrange_kernel<<<1, 32, 0, c.s>>>(a);
+  const u64 vcap = std::min<u64>(c.G->n, np + (u64(1) << 20));  // grid size only: the kernel strides
+  const unsigned pg = (unsigned)std::max<u64>(1, (vcap + 255) / 256);
   local_prep_kernel<<<pg, 256, 0, c.s>>>(a);
   GPM_CUDA(cudaGetLastError());
   // fork: medium-2 and big roots on the side stream, small items here
