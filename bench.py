@@ -386,7 +386,12 @@ def main():
         clocks = ClockSampler(local, os.environ.get("GPM_BENCH_CLOCK_MS", "100"))
         clocks.start()
         clocks.wait_samples(1)
-        for _ in range(warmup):
+        # collect before the warm-up, not between it and the timed steps (an
+        # idle GPU during a collection made the first timed step the slowest)
+        gc.collect()
+        gc.disable()  # no collector pauses inside the timed host calls (re-enabled after the e2e steps)
+        for _ in range(warmup):  # the same as a timed step (L2 flush + step), untimed
+            flush.zero_()
             res = mine_step()
         barrier()
         clocks.drain()
@@ -395,8 +400,6 @@ def main():
         dom_ms, dom_b, dom_mv, launches = [], [], [], 0
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
-        gc.collect()
-        gc.disable()  # no collector pauses inside the timed host calls (re-enabled after the e2e steps)
         for _ in range(steps):
             flush.zero_()
             if use_steal is not None:

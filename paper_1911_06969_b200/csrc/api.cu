@@ -307,8 +307,13 @@ static int mine_once(const gpm_graph* g, const gpm_config* cfg, gpm_result** out
     GPM_CUDA(cudaStreamSynchronize(s));
     float ms = 0;
     GPM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    struct EvDrop {
+      cudaEvent_t a, b;
+      ~EvDrop() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
+    } ev_drop{e0, e1};  // kept for the trace's per-kernel start offsets
 
     gpm_stats& S = res->stats;
     std::memset(&S, 0, sizeof S);
@@ -331,7 +336,12 @@ static int mine_once(const gpm_graph* g, const gpm_config* cfg, gpm_result** out
     for (auto& r : tl.recs) {
       float t = 0;
       GPM_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
-      if (trace) std::fprintf(stderr, "[gpm]   %-28s %10.3f ms  %12.4g B_alg\n", r.name.c_str(), t, r.bytes);
+      if (trace) {
+        float t0 = 0;
+        GPM_CUDA(cudaEventElapsedTime(&t0, e0, r.a));
+        std::fprintf(stderr, "[gpm]   %-28s %10.3f ms  %12.4g B_alg  (starts at %.3f ms%s)\n", r.name.c_str(), t, r.bytes,
+                     t0, r.side ? ", side stream" : "");
+      }
       if (r.side) continue;  // overlapped with the main stream: neither a phase nor the dominant kernel
       per[r.name][0] += t;
       per[r.name][1] += r.bytes;

@@ -27,9 +27,11 @@
 //
 // Work split: roots with out-degree <= 32 are packed into warp items (the
 // roots whose first out-edge lies in one 32-edge block of the DAG CSR: <= 32
-// roots, <= 63 edges, one 32-bit row per edge); roots with out-degree in
-// (32, kBigMax] and the (at most two) roots cut by the slice bounds go to a
-// CTA-per-root kernel with rows of ceil(d/32) words in shared memory.
+// roots, <= 63 edges, one 32-bit row per edge); a root with out-degree in
+// (32, 64] is one warp item (2-word rows); roots with out-degree in
+// (64, kBigMax] and the (at most two) roots cut by the slice bounds go to a
+// CTA-per-root kernel (run first) with rows of ceil(d/32) words in shared
+// memory.
 #include <cstdlib>
 
 #include "gpm_apps.cuh"
@@ -40,7 +42,7 @@ namespace engine {
 namespace {
 
 constexpr u32 kBigMax = 1024;     // largest out-degree handled on chip
-constexpr u32 kMidMax = 128;      // largest out-degree of a warp item
+constexpr u32 kMidMax = 64;       // largest out-degree of a warp item
 constexpr int kSmallThreads = 256;
 constexpr int kBigThreads = 128;
 constexpr int kAcc = 2 * kMaxLevels;  // [0, kMaxLevels): children per level; [kMaxLevels, ..): candidates per level
@@ -54,9 +56,7 @@ struct LocalArgs {
   unsigned long long* nbig;
   u32* mid;             // roots of out-degree (32, 64] (one warp item each, after the blocks)
   unsigned long long* nmid;
-  u32* mid2;            // roots of out-degree (64, 128]
-  unsigned long long* nmid2;
-  unsigned long long* ctr;   // [0] small-item grabs, [1] big-root grabs, [2] medium-root grabs
+  unsigned long long* ctr;   // [0] warp-item grabs, [1] big-root grabs
   unsigned long long* acc;   // [3][kAcc]: small, medium, big
   unsigned long long* total; // last-level count (engine d_total)
   u32* vr;                   // vertex range of the slice (device)
@@ -146,16 +146,15 @@ __global__ void local_prep_kernel(LocalArgs a) {
     const u64 d = oe - ob;
     const bool big = in && (ob < a.lo || oe > a.hi || d > kMidMax);
     warp_append(big, (u32)v, a.big, a.nbig);
-    warp_append(in && !big && d > 64, (u32)v, a.mid2, a.nmid2);
-    warp_append(in && !big && d > 32 && d <= 64, (u32)v, a.mid, a.nmid);
+    warp_append(in && !big && d > 32, (u32)v, a.mid, a.nmid);
   }
 }
 
 // ---------------------------------------------------------------------------
 // Warp items.  An item is either the small roots (out-degree <= 32) whose
 // first out-edge lies in one 32-edge block of the DAG CSR (<= 32 roots,
-// <= 63 edges, 1-word rows), or one medium root (out-degree in (32, 128],
-// rows of <= 4 words).  Per warp in shared memory: a bucketised hash of the
+// <= 63 edges, 1-word rows), or one medium root (out-degree in (32, 64],
+// rows of 2 words).  Per warp in shared memory: a bucketised hash of the
 // item's keys (u << 5 | root slot) -> local position, the rows, and the
 // candidate stream's descriptors.  The stream (the concatenated out-lists of
 // the item's edges) is walked 32 positions per window; a per-window bitmap of
@@ -176,7 +175,6 @@ struct WarpCfg {
                                           // registers -> 3 CTAs/SM and measured slower: 1.00 vs 0.89 ms)
 };
 using SmallCfg = WarpCfg<64, 128, 2, 128>;   // small-root blocks (1-word rows) and roots of out-degree <= 64
-using MidCfg = WarpCfg<128, 256, 4, 256, 4, 2>;    // roots of out-degree in (64, 128]
 
 template <class C>
 struct WarpSmem {
@@ -253,10 +251,9 @@ __device__ __forceinline__ void count_subtree(const u32* rows, const u32* dp, u3
   }
 }
 
-// MID = false: items [0, nblk) are small-root blocks, then one item per root
-// of out-degree in (32, 64] (a.mid); MID = true: one item per root of
-// out-degree in (64, 128] (a.mid2).
-template <class C, bool MID>
+// Items [0, nblk) are small-root blocks, then one item per root of out-degree
+// in (32, 64] (a.mid).
+template <class C>
 __global__ void __launch_bounds__(kSmallThreads, C::kMinBlocks) local_warp_kernel(LocalArgs a) {
   extern __shared__ __align__(16) unsigned char wsm[];
   WarpSmem<C>* const s_w = reinterpret_cast<WarpSmem<C>*>(wsm);
@@ -274,15 +271,15 @@ __global__ void __launch_bounds__(kSmallThreads, C::kMinBlocks) local_warp_kerne
   const DevGraph& g = a.g;
   const int last = a.k - 2;
   unsigned long long l1 = 0, c1 = 0, l2 = 0, c2 = 0;
-  const u64 nblk = MID ? 0 : a.nblk;
-  const u64 nitems = nblk + *reinterpret_cast<volatile unsigned long long*>(MID ? a.nmid2 : a.nmid);
-  const u32* const rootlist = MID ? a.mid2 : a.mid;
+  const u64 nblk = a.nblk;
+  const u64 nitems = nblk + *reinterpret_cast<volatile unsigned long long*>(a.nmid);
+  const u32* const rootlist = a.mid;
   constexpr u64 kGrab = 4;
   u64 grab = 0, grab_left = 0;
   for (;;) {
     if (grab_left == 0) {
       u64 it_ = 0;
-      if (lane == 0) it_ = atomicAdd(a.ctr + (MID ? 2 : 0), kGrab);
+      if (lane == 0) it_ = atomicAdd(a.ctr, kGrab);
       grab = __shfl_sync(0xffffffffu, it_, 0);
       grab_left = kGrab;
     }
@@ -533,7 +530,7 @@ __global__ void __launch_bounds__(kSmallThreads, C::kMinBlocks) local_warp_kerne
     S.acc[kMaxLevels + 2] += c2;
   }
   __syncwarp();
-  unsigned long long* const gacc = a.acc + (MID ? kAcc : 0);  // [1]: the (64, 128] roots
+  unsigned long long* const gacc = a.acc;
   for (int i = lane; i < kAcc; i += 32) {
     const unsigned long long x = S.acc[i];
     if (!x) continue;
@@ -737,7 +734,8 @@ __global__ void __launch_bounds__(kBigThreads) local_big_kernel(LocalArgs a, u32
 
 }  // namespace
 
-// Timeline records on a stream other than the timeline's own
+// Timeline record on a stream other than the timeline's own (marked side:
+// overlapped, not a phase of the step)
 size_t tl_begin_on(Timeline& tl, const char* name, cudaStream_t st) {
   Timeline::Rec r{name, nullptr, nullptr, 0.0, -1, st != tl.s};
   GPM_CUDA(cudaEventCreate(&r.a));
@@ -747,9 +745,7 @@ size_t tl_begin_on(Timeline& tl, const char* name, cudaStream_t st) {
   return tl.recs.size() - 1;
 }
 
-// Side stream of the calling thread on the current device: the (64, 1024]
-// out-degree roots run beside the small-root items (their warps are few and
-// long, so serialised they would be a latency-bound tail).
+// Side stream of the calling thread on the current device
 cudaStream_t side_stream() {
   int dev = 0;
   GPM_CUDA(cudaGetDevice(&dev));
@@ -759,9 +755,9 @@ cudaStream_t side_stream() {
   return ss[dev];
 }
 
-template <class C, bool MID>
+template <class C>
 size_t launch_warp(Ctx& c, LocalArgs& a, u64 max_blocks, const char* name, cudaStream_t st) {
-  auto kern = local_warp_kernel<C, MID>;
+  auto kern = local_warp_kernel<C>;
   const size_t smem = sizeof(WarpSmem<C>) * (kSmallThreads / 32);
   static std::atomic<int> occ{0};
   const int o = cached_occupancy(occ, [&] {
@@ -771,10 +767,10 @@ size_t launch_warp(Ctx& c, LocalArgs& a, u64 max_blocks, const char* name, cudaS
     return r;
   });
   const u64 blocks = std::max<u64>(1, std::min<u64>((u64)c.sms * o, max_blocks));
-  size_t rec = tl_begin_on(*c.tl, name, st);
+  size_t rec = c.tl->begin(name, 0.0);
   kern<<<(unsigned)blocks, kSmallThreads, smem, st>>>(a);
   GPM_CUDA(cudaGetLastError());
-  GPM_CUDA(cudaEventRecord(c.tl->recs[rec].b, st));
+  c.tl->end(rec);
   return rec;
 }
 
@@ -792,7 +788,7 @@ bool cf_local_roots(Ctx& c, const u32*, u64 slo, u64 shi) {
   st.paths |= GPM_PATH_CF_LOCAL;
   const u64 blo = slo / 32, nblk = (shi - 1) / 32 - blo + 1;
   const u64 bigcap = np / 33 + 3;
-  DBuf<u32> item(nblk, c.s), big(bigcap, c.s), mid(bigcap, c.s), mid2(bigcap, c.s);
+  DBuf<u32> item(nblk, c.s), big(bigcap, c.s), mid(bigcap, c.s);
   constexpr int kCtl = 8;
   DBuf<unsigned long long> ctl(kCtl + 3 * kAcc, c.s);
   GPM_CUDA(cudaMemsetAsync(item.get(), 0xff, sizeof(u32) * nblk, c.s));
@@ -809,8 +805,6 @@ bool cf_local_roots(Ctx& c, const u32*, u64 slo, u64 shi) {
   a.ctr = ctl.get() + 1;
   a.mid = mid.get();
   a.nmid = ctl.get() + 4;
-  a.mid2 = mid2.get();
-  a.nmid2 = ctl.get() + 5;
   a.acc = ctl.get() + kCtl;
   a.total = c.d_total;
   a.k = c.k;
@@ -823,22 +817,11 @@ bool cf_local_roots(Ctx& c, const u32*, u64 slo, u64 shi) {
   const unsigned pg = (unsigned)std::max<u64>(1, (vcap + 255) / 256);
   local_prep_kernel<<<pg, 256, 0, c.s>>>(a);
   GPM_CUDA(cudaGetLastError());
-  // fork: medium-2 and big roots on the side stream, small items here
-  cudaStream_t ss = side_stream();
-  cudaEvent_t fork = nullptr, join = nullptr;
-  GPM_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-  GPM_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-  struct EvGuard {
-    cudaEvent_t* e[2];
-    ~EvGuard() {
-      for (auto* x : e)
-        if (*x) cudaEventDestroy(*x);
-    }
-  } evg{{&fork, &join}};
-  GPM_CUDA(cudaEventRecord(fork, c.s));
-  GPM_CUDA(cudaStreamWaitEvent(ss, fork, 0));
-  size_t rec[3];
-  rec[1] = launch_warp<MidCfg, true>(c, a, (bigcap + 7) / 8, "extend_local_mid", ss);
+  // roots of out-degree > 64 (and slice-cut roots): one CTA each, ~50 us on
+  // PAT.  (Heavy medium-root warp CTAs -- 94 KB of shared memory -- launched
+  // beside the persistent small-item grid only got SMs once it drained, i.e.
+  // ran as a tail; light CTAs dispatched first co-reside with it.)
+  size_t rec[3] = {0, 0, 0};
   const u32 dmax = std::max<u32>(kMidMax + 1, c.G->max_deg);
   const size_t smem = 4 * (size_t)BigLayout(dmax).words;
   // attribute + occupancy once per shared-memory size (per thread: the
@@ -852,18 +835,34 @@ bool cf_local_roots(Ctx& c, const u32*, u64 slo, u64 shi) {
   }
   const int ob = big_occ.second;
   const u64 bb = std::max<u64>(1, std::min<u64>((u64)c.sms * std::max(1, ob), bigcap));
+  // the CTA kernel (few, light CTAs: 128 threads, ~12 KB) is dispatched
+  // first on a side stream, the small-item grid right after on the main one:
+  // they share the SMs while the big roots run instead of serialising
+  cudaStream_t ss = side_stream();
+  cudaEvent_t fork = nullptr, join = nullptr;
+  GPM_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  GPM_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t* e[2];
+    ~EvGuard() {
+      for (auto* x : e)
+        if (*x) cudaEventDestroy(*x);
+    }
+  } evg{{&fork, &join}};
+  GPM_CUDA(cudaEventRecord(fork, c.s));
+  GPM_CUDA(cudaStreamWaitEvent(ss, fork, 0));
   rec[2] = tl_begin_on(*c.tl, "extend_local_big", ss);
   local_big_kernel<<<(unsigned)bb, kBigThreads, smem, ss>>>(a, dmax);
   GPM_CUDA(cudaGetLastError());
   GPM_CUDA(cudaEventRecord(c.tl->recs[rec[2]].b, ss));
   GPM_CUDA(cudaEventRecord(join, ss));
-  rec[0] = launch_warp<SmallCfg, false>(c, a, (nblk + bigcap + 7) / 8, "extend_local_small", c.s);
+  rec[0] = launch_warp<SmallCfg>(c, a, (nblk + bigcap + 7) / 8, "extend_local_small", c.s);
   GPM_CUDA(cudaStreamWaitEvent(c.s, join, 0));
   c.tl->launches += 4;
   std::vector<unsigned long long> h(kCtl + 3 * kAcc);
   GPM_CUDA(cudaMemcpyAsync(h.data(), ctl.get(), sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c.s));
   GPM_CUDA(cudaStreamSynchronize(c.s));
-  if (h[0] > 0 || h[5] > 0) st.paths |= GPM_PATH_CF_LOCAL_BIG;
+  if (h[0] > 0) st.paths |= GPM_PATH_CF_LOCAL_BIG;
   // stats and SURVEY §8d bytes per kernel: level lev parents P_lev (P_1 = the
   // slice's edges), candidates C_lev, children L_lev (the last level's
   // children are the engine's total, added from d_total by the caller)
@@ -888,7 +887,7 @@ bool cf_local_roots(Ctx& c, const u32*, u64 slo, u64 shi) {
   // the kernels in proportion to their level-1 candidates
   double c1[3], c1t = 0;
   for (int kind = 0; kind < 3; ++kind) c1t += (c1[kind] = (double)h[kCtl + kind * kAcc + kMaxLevels + 1]);
-  for (int kind = 0; kind < 3; ++kind) {
+  for (int kind = 0; kind < 3; kind += 2) {  // kind 1 (the old medium-root kernel) is unused
     bytes[kind] += 24.0 * (double)np * (c1t > 0 ? c1[kind] / c1t : (kind == 0 ? 1.0 : 0.0));
     c.tl->recs[rec[kind]].bytes = bytes[kind];
     st.balg += bytes[kind];
