@@ -135,15 +135,18 @@ __global__ void local_prep_kernel(LocalArgs a) {
   for (u64 vb = a.vr[0] + blockIdx.x * (u64)blockDim.x; vb < vend; vb += stride) {
     const u64 v = vb + threadIdx.x;
     const bool valid = v < vend;
-    u64 ob = 0, oe = 0;
+    // one offset load per lane; the neighbours' from the adjacent lanes
+    const int lane = threadIdx.x & 31;
+    const u64 ob = v <= a.g.n ? ldg(a.g.off + v) : 0;
+    u64 oe = __shfl_down_sync(0xffffffffu, ob, 1), prev = __shfl_up_sync(0xffffffffu, ob, 1);
+    if (lane == 31 && valid) oe = ldg(a.g.off + v + 1);
+    if (lane == 0 && v) prev = ldg(a.g.off + v - 1);
     if (valid) {
-      ob = ldg(a.g.off + v);
-      oe = ldg(a.g.off + v + 1);
-      const u64 b0 = max(v ? ldg(a.g.off + v - 1) / 32 + 1 : 0, a.blo), b1 = ob / 32 + 1;  // b in [b0, b1)
+      const u64 b0 = max(v ? prev / 32 + 1 : 0, a.blo), b1 = ob / 32 + 1;  // b in [b0, b1)
       for (u64 b = b0; b < b1 && b < a.blo + a.nblk; ++b) a.item_root[b - a.blo] = (u32)v;
     }
     const bool in = valid && !(oe <= a.lo || ob >= a.hi || ob == oe);
-    const u64 d = oe - ob;
+    const u64 d = valid ? oe - ob : 0;
     const bool big = in && (ob < a.lo || oe > a.hi || d > kMidMax);
     warp_append(big, (u32)v, a.big, a.nbig);
     warp_append(in && !big && d > 32, (u32)v, a.mid, a.nmid);
