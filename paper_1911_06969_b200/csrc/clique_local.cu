@@ -754,7 +754,12 @@ cudaStream_t side_stream() {
   GPM_CUDA(cudaGetDevice(&dev));
   static thread_local std::vector<cudaStream_t> ss;
   if ((int)ss.size() <= dev) ss.resize(dev + 1, nullptr);
-  if (!ss[dev]) GPM_CUDA(cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking));
+  if (!ss[dev]) {
+    // highest priority: its CTAs are dispatched before the small-item grid's
+    int lo = 0, hi = 0;
+    GPM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GPM_CUDA(cudaStreamCreateWithPriority(&ss[dev], cudaStreamNonBlocking, hi));
+  }
   return ss[dev];
 }
 
