@@ -61,6 +61,35 @@ void scan_inplace(u64* data, u64 n, cudaStream_t s);
 
 namespace fsm_engine {
 
+// Per-thread host scratch vectors that keep their capacity across calls: the
+// per-level host arrays (10^5..10^6 entries) would otherwise be fresh
+// allocations whose first-touch page faults cost ~1 ms per MB on these hosts.
+// One slot per (type, use); every use is a temporary of one function.
+template <class T, int SLOT>
+std::vector<T>& host_scratch() {
+  static thread_local std::vector<T> v;
+  return v;
+}
+
+// Pool of u64 host vectors (capacity kept across levels and calls) for the
+// per-level pattern arrays that outlive one function (keys, counts, MNI).
+inline std::vector<std::vector<u64>>& u64_pool() {
+  static thread_local std::vector<std::vector<u64>> p;
+  return p;
+}
+inline std::vector<u64> take_u64() {
+  auto& p = u64_pool();
+  if (p.empty()) return {};
+  std::vector<u64> v = std::move(p.back());
+  p.pop_back();
+  v.clear();
+  return v;
+}
+inline void give_u64(std::vector<u64>& v) {
+  if (v.capacity() && u64_pool().size() < 8) u64_pool().push_back(std::move(v));
+  v = std::vector<u64>();
+}
+
 // host threads for the per-pattern loops (1 when the including translation
 // unit is built without OpenMP)
 inline int host_threads() {
@@ -1592,8 +1621,16 @@ struct Fsm {
     DBuf<u32> perm, bslot, bs_to_pid, ids, occ;  // perm / ids / canon / occ: per occupied slot
     u64 U = 0;
     DBuf<u8> frequent;
-    std::vector<u64> gkeys_h, gcount_h, mni_h;
+    std::vector<u64> gkeys_h, gcount_h, mni_h;  // from / back to the host pool (u64_pool)
     std::vector<u8> freq_h;  // frequent (not pruned) flags, host copy
+    Level() = default;
+    Level(const Level&) = delete;
+    Level& operator=(const Level&) = delete;
+    ~Level() {
+      give_u64(gkeys_h);
+      give_u64(gcount_h);
+      give_u64(mni_h);
+    }
     DBuf<u64> gkeys;
     u64 P = 0;
     u64 NB = 0;
@@ -1640,7 +1677,7 @@ struct Fsm {
     tl.launches += 2;
     DBuf<u64> ck(U1, s);
     if (U) GPM_CUDA(cudaMemcpyAsync(ck.get(), R.canon.get(), sizeof(u64) * U, cudaMemcpyDeviceToDevice, s));
-    std::vector<u64> keys, cnts;
+    std::vector<u64> keys = take_u64(), cnts = take_u64();
     if (U) {
       size_t tmp = 0;
       GPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ck.get(), ck2.get(), cc3.get(), cc4.get(), (int64_t)U, 0,
@@ -1711,6 +1748,8 @@ struct Fsm {
       R.gcount_h.back() += cnts[i];
     }
     R.P = R.gkeys_h.size();
+    give_u64(keys);
+    give_u64(cnts);
     trace("host reduce by key", (double)R.P);
     R.gkeys.alloc(std::max<u64>(1, R.P), s);
     if (R.P)
@@ -1722,10 +1761,14 @@ struct Fsm {
     ++tl.launches;
     trace("reduce keys + slot pids", (double)R.P, (double)R.U);
     // count pre-filter -> bitmap slots (MNI <= count)
-    std::vector<u32> bslot(std::max<u64>(1, R.P), ~0u), bs_to_pid;
+    std::vector<u32>& bslot = host_scratch<u32, 0>();
+    std::vector<u32>& bs_to_pid = host_scratch<u32, 1>();
+    bslot.assign(std::max<u64>(1, R.P), ~0u);
+    bs_to_pid.clear();
     // MNI <= count; the full-automorphism MNI unions an orbit's domains: <= nv * count
     const bool full = cfg.mni_mode == GPM_MNI_AUTOMORPHISM;
-    std::vector<u8> need(std::max<u64>(1, R.P), 0);
+    std::vector<u8>& need = host_scratch<u8, 0>();
+    need.assign(std::max<u64>(1, R.P), 0);
     for (u64 p = 0; p < R.P; ++p)
       need[p] = App::kDomains && R.gcount_h[p] * (full ? (u64)pat::code_nv(R.gkeys_h[p]) : 1) >= sigma;
     // sparse domains: a pattern whose keys (8 B per embedding
@@ -1733,7 +1776,10 @@ struct Fsm {
     // rows -- big label classes, few embeddings -- gets sorted key lists
     // instead, within half the budget (GPM_FSM_SPARSE=1: every pattern).
     // Counts, words and the budget are rank-invariant, so is the choice.
-    std::vector<u32> sslot(std::max<u64>(1, R.P), ~0u), sp_to_pid;
+    std::vector<u32>& sslot = host_scratch<u32, 2>();
+    std::vector<u32>& sp_to_pid = host_scratch<u32, 3>();
+    sslot.assign(std::max<u64>(1, R.P), ~0u);
+    sp_to_pid.clear();
     R.skeys_total = 0;
     if (allow_sparse) {
       const bool force = std::getenv("GPM_FSM_SPARSE") != nullptr;
@@ -1855,6 +1901,8 @@ struct Fsm {
       }
     }
     if (R.NS) sparse_domains(R, mni.get(), run_sparse);
+    give_u64(R.mni_h);
+    R.mni_h = take_u64();
     R.mni_h.assign(R.P, 0);
     if (R.P)
       GPM_CUDA(cudaMemcpyAsync(R.mni_h.data(), mni.get(), sizeof(u64) * R.P, cudaMemcpyDeviceToHost, s));
@@ -2212,7 +2260,8 @@ struct Fsm {
       x = acc;
       acc += c;
     }
-    std::vector<FanItem> v(ntot);
+    std::vector<FanItem>& v = host_scratch<FanItem, 0>();
+    v.resize(ntot);  // every element is written below
     for (u64 i = 0; i < G_; ++i) {
       const u32 a0 = hs[i], a1 = i + 1 < G_ ? hs[i + 1] : (u32)nz;
       const int nvv = pat::code_nv(hc[i]);
