@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgpm.so")
+LIB_PATH = os.path.join(HERE, os.environ.get("GPM_LIB_VARIANT", "libgpm.so"))  # variant: A/B builds in-tree
 
 GPM_OK, GPM_EINVAL, GPM_EPARSE, GPM_ENOMEM, GPM_ECUDA, GPM_ENCCL, GPM_ECONFIG = range(7)
 APP_TC, APP_CF, APP_MC, APP_FSM = range(4)

@@ -82,10 +82,12 @@ void build_level1(const gpm_graph& g, DBuf<u32>& idx, DBuf<u32>& vid, u64& count
 // slice [lo, hi) into d_hist (8 bins) and the candidates / B_alg to st.
 void mc3_staged(const gpm_graph& g, const u64* l1_start, u64 lo, u64 hi, unsigned long long* d_hist, cudaStream_t s,
                 Timeline& tl, Stats& st);
-// Last extension of 4-MC over a materialised level 2 (idx2 -> level-1 index,
-// vid2 = v2) with S0 / S1 staged on chip; adds 6-pair code counts to d_hist.
-void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u32* idx2, const u32* vid2, u64 np,
-                     unsigned long long* d_hist, cudaStream_t s, Timeline& tl, Stats& st);
+// Levels 2 and 3 of 4-MC fused over the level-1 slice (l1i = v0, l1v = v1,
+// nq parents): S0 / S1 staged on chip per parent, the parent's level-2
+// children walked in place (never materialised); adds 6-pair code counts to
+// d_hist and both levels' candidates / level size / B_alg to st.
+void mc4_roots_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, u64 nq, unsigned long long* d_hist,
+                      cudaStream_t s, Timeline& tl, Stats& st);
 
 // Degree-weighted static split of [0, n1) root units into `world` parts
 // (SURVEY §8e); weight = candidate count of each level-1 entry.

@@ -408,21 +408,18 @@ constexpr int kT4 = 256;
 constexpr int kW4 = kT4 / 32;
 constexpr u32 k4Slots = 1024;  // per-warp union table S0 ∪ S1 (4 KB)
 constexpr u32 k4Keys = 512;    // |S0| + |S1| above this -> binary search in HBM
-constexpr u64 k4Item = 512;    // level-2 entries per warp work item
-constexpr u64 kShortList = 0;  // lists up to this length skip the lower-bound search (64 measured slower on MC4)
+constexpr u64 k4Q = 8;         // level-1 parents per warp work item
 
 struct Mc4Args {
   DevGraph g;
   const u32* l1i;   // level-1 v0 (slice-relative)
   const u32* l1v;   // level-1 v1
-  const u32* idx2;  // level-2 -> level-1 index
-  const u32* vid2;  // level-2 v2
-  u64 np;
+  u64 nq;           // level-1 parents in the slice
   u64 nitems;
   unsigned long long* ctr;
   unsigned long long* hist;   // 64 bins
-  unsigned long long* cand;
-  unsigned long long* moved;  // [0] streamed S2 candidates, [1] staged keys, [2] unused, [3] rank-counted
+  unsigned long long* cand;   // [0] level-2 candidates, [1] level-3 candidates
+  unsigned long long* moved;  // [0] streamed S2 candidates, [1] staged keys, [2] level-2 children, [3] rank-counted, [4] path flag
   u32* scratch;               // per warp: max_deg entries for I01
   u64 scratch_stride;
   u32 pm_bits[4];             // pmask value for (v0~v2, v1~v2)
@@ -484,6 +481,12 @@ __device__ __forceinline__ u32 count_gt_plain(const u32* a, u32 n, u32 key) {
   return n - lo;
 }
 
+// The HBM fallback is out of line: the kernels inline flags() at ~10 sites
+// and their loop bodies are instruction-cache sensitive (a second inlined
+// copy of the 4-MC step body measured 2x slower).
+__device__ __forceinline__ u32 us_flags_sorted(const u32* s0, u32 n0, const u32* s1, u32 n1, u32 v) {
+  return (contains_sorted(s0, n0, v) ? 1u : 0u) | (contains_sorted(s1, n1, v) ? 2u : 0u);
+}
 struct UnionSet {
   const u32* T;      // nullptr -> probe the sorted lists in HBM
   const u32* s0;
@@ -491,249 +494,281 @@ struct UnionSet {
   u32 n0, n1, sh, mask;
   __device__ __forceinline__ u32 flags(u32 v) const {
     if (T) return us_flags(T, sh, mask, v);
-    return (contains_sorted(s0, n0, v) ? 1u : 0u) | (contains_sorted(s1, n1, v) ? 2u : 0u);
+    return us_flags_sorted(s0, n0, s1, n1, v);
   }
 };
 
-__global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
+// Fused level 2 + last level of 4-MC: items are ranges of level-1 parents
+// q = (v0, v1); per q the warp stages S0 ∪ S1 once and walks q's level-2
+// children in place -- {u in S0 : u > v1} (pos 0, the contiguous suffix of
+// the sorted S0 above v1) then {u in S1 : u !in S0} (pos 1, first-adjacent
+// rule) -- so level 2 is never materialised (no inspection / execution
+// passes, no idx2 / vid2 round trip through HBM).  The children are exactly
+// is_auto_canonical_vertex's accepted candidates of (v0, v1)
+// (gpm_engine.cuh).
+__global__ void __launch_bounds__(kT4, 4) mc4_roots_kernel(Mc4Args a) {
   __shared__ __align__(16) u32 s_tab[kW4][k4Slots];
   __shared__ u64 s_cb[kW4][32];
   __shared__ u32 s_ex[kW4][32];
   __shared__ u32 s_v2[kW4][32];
-  __shared__ u32 s_ev[kW4][4][32];
   __shared__ unsigned long long s_h[kW4][32];
+  __shared__ unsigned long long s_kids[kW4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const DevGraph& g = a.g;
   u32* T = s_tab[wid];
   u32* I01 = a.scratch + (blockIdx.x * (u64)kW4 + wid) * a.scratch_stride;
   s_h[wid][lane] = 0;
-  // per-item u32 counters (streamed, staged, children, rank-counted), folded
-  // into the unused class slot 7 of each parent-mask row of s_h per item
+  if (lane == 0) s_kids[wid] = 0;
+  // per-item counters (streamed, staged, rank-counted), folded into the
+  // unused class slot 7 of each parent-mask row of s_h per item
   unsigned long long aCand = 0;
   u32 aLen = 0, aStg = 0, aRank = 0;
-  u32 cur_v0 = 0xffffffffu;
-  u64 cur_q = ~0ull;
   UnionSet U{};
-  u64 s0b = 0;
   u32 v0 = 0, v1 = 0, n01 = 0;
+  u32 deg01 = 0, deg0 = 0;  // degrees < 2^32
+  u32 cur_v0 = 0xffffffffu;
+
+  // one warp step over up to 32 children (lane-owned v2 where valid).  The
+  // classes only matter summed per parent-mask value pv, so event counts go
+  // straight into s_h (val[1] = Im - e11 etc.: +e into one class, -e into
+  // its rank partner; the u64 sums wrap back to the exact totals).
+  // a0 / b1: #S0 > max(v1, v2) / #S1 > v2 when known from the child's index
+  // in the staged list (~0u: binary search).
+  auto step = [&](bool valid, u32 v2, u32 a0, u32 b1) {
+    u32 len = 0, pmv = 0;
+    u64 st = 0;
+    if (valid) {
+      const u64 b2 = ldg(g.off + v2), e2 = ldg(g.off + v2 + 1);
+      st = lower_bound_col(g.col, b2, e2, v0 + 1);
+      len = (u32)(e2 - st);
+      pmv = U.flags(v2);  // bit 0: v2 ~ v0, bit 1: v2 ~ v1
+      aCand += (u64)deg01 + (e2 - b2);
+      aLen += len;
+    }
+    // long S2 ranges (>= 32 candidates): one child at a time, warp-uniform
+    // thresholds, coalesced loads, four in flight, per-lane event counters
+    u32 todo = __ballot_sync(0xffffffffu, len >= 32);
+    while (todo) {
+      const int i = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const u64 b = __shfl_sync(0xffffffffu, st, i);
+      const u32 L = __shfl_sync(0xffffffffu, len, i);
+      const u32 cv2 = __shfl_sync(0xffffffffu, v2, i);
+      const u32 cpv = __shfl_sync(0xffffffffu, pmv, i);
+      const u32 cm = max(v1, cv2);
+      u32 c2 = 0, c11 = 0, c01 = 0, c12 = 0;
+      u32 j = 0;
+      for (; j + 128 <= L; j += 128) {
+        u32 u[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u[q] = ldg(g.col + b + j + 32 * q + lane);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const u32 f = U.flags(u[q]);
+          c2 += (f == 0 && u[q] > v0);
+          c11 += (f == 3 && u[q] > cm);
+          c01 += (f == 1 && u[q] > cm);
+          c12 += (f == 2 && u[q] > cv2);
+        }
+      }
+      for (; j < L; j += 32) {
+        const bool ok = j + lane < L;
+        const u32 u0 = ok ? ldg(g.col + b + j + lane) : 0u;
+        const u32 f0 = ok ? U.flags(u0) : 4u;
+        c2 += (f0 == 0 && u0 > v0);
+        c11 += (f0 == 3 && u0 > cm);
+        c01 += (f0 == 1 && u0 > cm);
+        c12 += (f0 == 2 && u0 > cv2);
+      }
+      c2 = __reduce_add_sync(0xffffffffu, c2);
+      c11 = __reduce_add_sync(0xffffffffu, c11);
+      c01 = __reduce_add_sync(0xffffffffu, c01);
+      c12 = __reduce_add_sync(0xffffffffu, c12);
+      if (lane == 0) {
+        unsigned long long* h = s_h[wid] + cpv * 8;
+        h[0] += c11;
+        h[1] -= c11;
+        h[2] += c01;
+        h[3] -= c01;
+        h[4] += c12;
+        h[5] -= c12;
+        h[6] += c2;
+        aRank -= c11 + c01 + c12;
+      }
+    }
+    // short S2 ranges: packed 32 candidates per step (OR-reduction lane ->
+    // child map); each candidate adds one to a packed per-lane counter of its
+    // (child pv, event) bin -- 8-bit fields, a lane sees < 32 candidates here
+    const u32 sl = len < 32 ? len : 0u;
+    u32 incl = sl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total) {
+      const u32 nz = __ballot_sync(0xffffffffu, sl > 0);
+      const u32 rank = __popc(nz & lanemask_lt());
+      const u32 nnz = __popc(nz);
+      if (sl > 0) {
+        s_cb[wid][rank] = st;
+        s_ex[wid][rank] = incl - sl;
+        s_v2[wid][rank] = v2 | (pmv << 30);  // ids < 2^30
+      }
+      __syncwarp();
+      u32 acc0 = 0, acc1 = 0, acc2 = 0;  // pv 1, 2, 3 (pv 0 never occurs); 8-bit field per event
+      u32 P = 0;
+      for (u32 jb = 0; jb < total; jb += 32) {
+        const u32 j = jb + lane;
+        const u32 x = (P + 1 + lane < nnz) ? s_ex[wid][P + 1 + lane] : 0xffffffffu;
+        const u32 bit = (x - jb < 32u) ? (1u << (x - jb)) : 0u;
+        const u32 starts = __reduce_or_sync(0xffffffffu, bit);
+        const u32 c = P + __popc(starts & (lanemask_lt() | (1u << lane)));
+        P += __popc(starts);
+        if (j < total) {
+          const u32 u = ldg(g.col + s_cb[wid][c] + (j - s_ex[wid][c]));
+          const u32 w = s_v2[wid][c];
+          const u32 cv2 = w & 0x3fffffffu;
+          const u32 f = U.flags(u);
+          // event field: 0 e11, 1 e01, 2 e12, 3 e2
+          const bool hit = f == 0 ? u > v0 : (f == 2 ? u > cv2 : u > max(v1, cv2));
+          const u32 ev = f == 0 ? 3u : (f == 3 ? 0u : f);
+          const u32 inc = hit ? 1u << (8 * ev) : 0u;
+          const u32 k = w >> 30;
+          acc0 += k == 1 ? inc : 0u;
+          acc1 += k == 2 ? inc : 0u;
+          acc2 += k == 3 ? inc : 0u;
+        }
+      }
+      // fields summed over the warp as 16-bit lanes (< 32 x 32 per field)
+#pragma unroll
+      for (int pv = 1; pv <= 3; ++pv) {
+        const u32 A = pv == 1 ? acc0 : (pv == 2 ? acc1 : acc2);
+        const u32 lo = __reduce_add_sync(0xffffffffu, A & 0x00ff00ffu);         // events 0, 2
+        const u32 hi = __reduce_add_sync(0xffffffffu, (A >> 8) & 0x00ff00ffu);  // events 1, 3
+        if (lane == 0 && (lo | hi)) {
+          const u32 e11 = lo & 0xffffu, e12 = lo >> 16, e01 = hi & 0xffffu, e2 = hi >> 16;
+          unsigned long long* h = s_h[wid] + pv * 8;
+          h[0] += e11;
+          h[1] -= e11;
+          h[2] += e01;
+          h[3] -= e01;
+          h[4] += e12;
+          h[5] -= e12;
+          h[6] += e2;
+          aRank -= e11 + e01 + e12;
+        }
+      }
+      __syncwarp();
+    }
+    // ---- per-child rank terms, reduced per parent-mask value
+    u32 r1 = 0, r3 = 0, r5 = 0;
+    if (valid) {
+      const u32 m = max(v1, v2);
+      const u32 A0 = a0 != ~0u ? a0 : count_gt_global(U.s0, U.n0, m);
+      const u32 B1 = b1 != ~0u ? b1 : count_gt_global(U.s1, U.n1, v2);
+      const u32 Im = count_gt_plain(I01, n01, m);
+      const u32 I2 = count_gt_plain(I01, n01, v2);
+      r1 = Im;
+      r3 = A0 - Im;
+      r5 = B1 - I2;
+      aRank += r1 + r3 + r5;
+    }
+#pragma unroll
+    for (u32 pv = 1; pv < 4; ++pv) {
+      const bool mine = valid && pmv == pv;
+      if (__ballot_sync(0xffffffffu, mine) == 0) continue;
+      const u32 s1_ = __reduce_add_sync(0xffffffffu, mine ? r1 : 0u);
+      const u32 s3_ = __reduce_add_sync(0xffffffffu, mine ? r3 : 0u);
+      const u32 s5_ = __reduce_add_sync(0xffffffffu, mine ? r5 : 0u);
+      if (lane == 0) {
+        s_h[wid][pv * 8 + 1] += s1_;
+        s_h[wid][pv * 8 + 3] += s3_;
+        s_h[wid][pv * 8 + 5] += s5_;
+      }
+    }
+    __syncwarp();
+  };
+
   for (;;) {
     u64 it_ = 0;
     if (lane == 0) it_ = atomicAdd(a.ctr, 1ull);
     const u64 item = __shfl_sync(0xffffffffu, it_, 0);
     if (item >= a.nitems) break;
-    u64 cur = item * k4Item;
-    const u64 iend = min(a.np, cur + k4Item);
-    while (cur < iend) {
-      // children of one level-1 parent q among the next 32 entries
-      const u64 e = cur + lane;
-      const u64 qi = e < iend ? (u64)ldg(a.idx2 + e) : ~0ull;
-      const u64 q = __shfl_sync(0xffffffffu, qi, 0);
-      const u32 nstep = __popc(__ballot_sync(0xffffffffu, qi == q));  // a prefix: idx2 is sorted
-      if (q != cur_q) {
-        // ---- stage S0 ∪ S1 (flags) and I01 = S0 ∩ S1 in ascending order
-        cur_q = q;
-        const u32 nv0 = ldg(a.l1i + q);
-        v1 = ldg(a.l1v + q);
-        if (nv0 != cur_v0) {
-          cur_v0 = v0 = nv0;
-          const u64 b0 = ldg(g.off + v0), e0 = ldg(g.off + v0 + 1);
-          s0b = lower_bound_col(g.col, b0, e0, v0 + 1);
-          U.s0 = g.col + s0b;
-          U.n0 = (u32)(e0 - s0b);
-        }
-        const u64 b1 = ldg(g.off + v1), e1 = ldg(g.off + v1 + 1);
-        const u64 s1b = lower_bound_col(g.col, b1, e1, v0 + 1);
-        U.s1 = g.col + s1b;
-        U.n1 = (u32)(e1 - s1b);
-        const bool fits = U.n0 + U.n1 <= k4Keys;
-        if (fits) {
-          u32 cap = 64;
-          while (cap < 8 * (U.n0 + U.n1) && cap < k4Slots) cap <<= 1;  // load <= 1/8 while it fits
-          hb_geom(cap, U.sh, U.mask);
-          __syncwarp();
-          for (u32 i = lane * 4; i < cap; i += 128)
-            *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-          __syncwarp();
-          for (u32 i = lane; i < U.n0; i += 32) us_add(T, U.sh, U.mask, ldg(U.s0 + i), 1u);
-          __syncwarp();
-        }
-        n01 = 0;
-        for (u32 jb = 0; jb < U.n1; jb += 32) {
-          const u32 j = jb + lane;
-          u32 u = 0;
-          bool hit = false;
-          if (j < U.n1) {
-            u = ldg(U.s1 + j);
-            hit = fits ? us_add(T, U.sh, U.mask, u, 2u) : contains_sorted(U.s0, U.n0, u);
-          }
-          const u32 bm = __ballot_sync(0xffffffffu, hit);
-          if (hit) I01[n01 + __popc(bm & lanemask_lt())] = u;
-          n01 += __popc(bm);
-        }
-        U.T = fits ? T : nullptr;
-        if (!fits && lane == 0) a.moved[4] = 1;  // path flag (tests)
-        if (lane == 0) aStg += (fits ? U.n0 : 0u) + U.n1;
+    const u64 qend = min(a.nq, (item + 1) * k4Q);
+    for (u64 q = item * k4Q; q < qend; ++q) {
+      // ---- stage S0 ∪ S1 (flags) and I01 = S0 ∩ S1 in ascending order
+      const u32 nv0 = ldg(a.l1i + q);
+      v1 = ldg(a.l1v + q);
+      if (nv0 != cur_v0) {  // level 1 is in v0 order: S0 is found once per root
+        cur_v0 = v0 = nv0;
+        const u64 b0 = ldg(g.off + v0), e0 = ldg(g.off + v0 + 1);
+        const u64 s0b = lower_bound_col(g.col, b0, e0, v0 + 1);
+        U.s0 = g.col + s0b;
+        U.n0 = (u32)(e0 - s0b);
+        deg0 = (u32)(e0 - b0);
+      }
+      const u64 b1 = ldg(g.off + v1), e1 = ldg(g.off + v1 + 1);
+      const u64 s1b = lower_bound_col(g.col, b1, e1, v0 + 1);
+      U.s1 = g.col + s1b;
+      U.n1 = (u32)(e1 - s1b);
+      deg01 = deg0 + (u32)(e1 - b1);
+      const bool fits = U.n0 + U.n1 <= k4Keys;
+      if (fits) {
+        u32 cap = 64;
+        while (cap < 8 * (U.n0 + U.n1) && cap < k4Slots) cap <<= 1;  // load <= 1/8 while it fits
+        hb_geom(cap, U.sh, U.mask);
+        __syncwarp();
+        for (u32 i = lane * 4; i < cap; i += 128)
+          *reinterpret_cast<uint4*>(T + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        __syncwarp();
+        for (u32 i = lane; i < U.n0; i += 32) us_add(T, U.sh, U.mask, ldg(U.s0 + i), 1u);
         __syncwarp();
       }
-      // ---- per-child setup: lane c < nstep owns child cur + c
-      u32 v2 = 0, len = 0, pmv = 0;
-      u64 st = 0;
-      const bool valid = lane < (int)nstep;
-      if (valid) {
-        v2 = ldg(a.vid2 + cur + lane);
-        const u64 b2 = ldg(g.off + v2), e2 = ldg(g.off + v2 + 1);
-        // short lists are streamed whole (the u > v0 test is applied per
-        // candidate below) instead of paying a dependent binary search
-        st = (e2 - b2 <= kShortList) ? b2 : lower_bound_col(g.col, b2, e2, v0 + 1);
-        len = (u32)(e2 - st);
-        pmv = U.flags(v2);  // bit 0: v2 ~ v0, bit 1: v2 ~ v1
-        aCand += (u64)(ldg(g.off + v0 + 1) - ldg(g.off + v0)) + (ldg(g.off + v1 + 1) - ldg(g.off + v1)) + (e2 - b2);
-        aLen += len;
+      n01 = 0;
+      for (u32 jb = 0; jb < U.n1; jb += 32) {
+        const u32 j = jb + lane;
+        u32 u = 0;
+        bool hit = false;
+        if (j < U.n1) {
+          u = ldg(U.s1 + j);
+          hit = fits ? us_add(T, U.sh, U.mask, u, 2u) : contains_sorted(U.s0, U.n0, u);
+        }
+        const u32 bm = __ballot_sync(0xffffffffu, hit);
+        if (hit) I01[n01 + __popc(bm & lanemask_lt())] = u;
+        n01 += __popc(bm);
       }
-      // ---- event counts of every child: e2c / e11 / e01 / e12 (see above)
-      u32 e2c = 0, e11 = 0, e01 = 0, e12 = 0;
-      // long S2 ranges (>= 32 candidates): one child at a time, warp-uniform
-      // thresholds, coalesced loads, two in flight
-      u32 todo = __ballot_sync(0xffffffffu, len >= 32);
-      while (todo) {
-        const int i = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const u64 b = __shfl_sync(0xffffffffu, st, i);
-        const u32 L = __shfl_sync(0xffffffffu, len, i);
-        const u32 cv2 = __shfl_sync(0xffffffffu, v2, i);
-        const u32 cm = max(v1, cv2);
-        u32 c2 = 0, c11 = 0, c01 = 0, c12 = 0;
-        u32 j = 0;
-        for (; j + 128 <= L; j += 128) {  // four loads in flight per lane
-          u32 u[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) u[q] = ldg(g.col + b + j + 32 * q + lane);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const u32 f = U.flags(u[q]);
-            c2 += __popc(__ballot_sync(0xffffffffu, f == 0 && u[q] > v0));
-            c11 += __popc(__ballot_sync(0xffffffffu, f == 3 && u[q] > cm));
-            c01 += __popc(__ballot_sync(0xffffffffu, f == 1 && u[q] > cm));
-            c12 += __popc(__ballot_sync(0xffffffffu, f == 2 && u[q] > cv2));
-          }
-        }
-        for (; j + 64 <= L; j += 64) {
-          const u32 u0 = ldg(g.col + b + j + lane);
-          const u32 u1 = ldg(g.col + b + j + 32 + lane);
-          const u32 f0 = U.flags(u0), f1 = U.flags(u1);
-          c2 += __popc(__ballot_sync(0xffffffffu, f0 == 0 && u0 > v0)) + __popc(__ballot_sync(0xffffffffu, f1 == 0 && u1 > v0));
-          c11 += __popc(__ballot_sync(0xffffffffu, f0 == 3 && u0 > cm)) + __popc(__ballot_sync(0xffffffffu, f1 == 3 && u1 > cm));
-          c01 += __popc(__ballot_sync(0xffffffffu, f0 == 1 && u0 > cm)) + __popc(__ballot_sync(0xffffffffu, f1 == 1 && u1 > cm));
-          c12 += __popc(__ballot_sync(0xffffffffu, f0 == 2 && u0 > cv2)) + __popc(__ballot_sync(0xffffffffu, f1 == 2 && u1 > cv2));
-        }
-        for (; j < L; j += 32) {
-          const bool ok = j + lane < L;
-          const u32 u0 = ok ? ldg(g.col + b + j + lane) : 0u;
-          const u32 f0 = ok ? U.flags(u0) : 4u;
-          c2 += __popc(__ballot_sync(0xffffffffu, f0 == 0 && u0 > v0));
-          c11 += __popc(__ballot_sync(0xffffffffu, f0 == 3 && u0 > cm));
-          c01 += __popc(__ballot_sync(0xffffffffu, f0 == 1 && u0 > cm));
-          c12 += __popc(__ballot_sync(0xffffffffu, f0 == 2 && u0 > cv2));
-        }
-        if (lane == i) {
-          e2c = c2;
-          e11 = c11;
-          e01 = c01;
-          e12 = c12;
-        }
-      }
-      // short S2 ranges: packed 32 candidates per step (OR-reduction lane ->
-      // child map), per-child counts by the first lane of each segment
-      const u32 sl = len < 32 ? len : 0u;
-      u32 incl = sl;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const u32 total = __shfl_sync(0xffffffffu, incl, 31);
-      const u32 nz = __ballot_sync(0xffffffffu, sl > 0);
-      const u32 rank = __popc(nz & lanemask_lt());
-      const u32 nnz = __popc(nz);
-      if (total) {
-        if (sl > 0) {
-          s_cb[wid][rank] = st;
-          s_ex[wid][rank] = incl - sl;
-          s_v2[wid][rank] = v2;
-        }
-#pragma unroll
-        for (int ev = 0; ev < 4; ++ev) s_ev[wid][ev][lane] = 0;
-        __syncwarp();
-        u32 P = 0;
-        for (u32 jb = 0; jb < total; jb += 32) {
-          const u32 j = jb + lane;
-          const u32 x = (P + 1 + lane < nnz) ? s_ex[wid][P + 1 + lane] : 0xffffffffu;
-          const u32 bit = (x - jb < 32u) ? (1u << (x - jb)) : 0u;
-          const u32 starts = __reduce_or_sync(0xffffffffu, bit);
-          const u32 c = P + __popc(starts & (lanemask_lt() | (1u << lane)));
-          P += __popc(starts);
-          bool f2 = false, f11 = false, f01 = false, f12 = false;
-          if (j < total) {
-            const u32 u = ldg(g.col + s_cb[wid][c] + (j - s_ex[wid][c]));
-            const u32 cv2 = s_v2[wid][c];
-            const u32 cm = max(v1, cv2);
-            const u32 f = U.flags(u);
-            f2 = f == 0 && u > v0;
-            f11 = f == 3 && u > cm;
-            f01 = f == 1 && u > cm;
-            f12 = f == 2 && u > cv2;
-          }
-          const u32 b2_ = __ballot_sync(0xffffffffu, f2), b11 = __ballot_sync(0xffffffffu, f11);
-          const u32 b01 = __ballot_sync(0xffffffffu, f01), b12 = __ballot_sync(0xffffffffu, f12);
-          const u32 heads = starts | 1u;
-          if ((heads >> lane & 1u) && j < total) {
-            const u32 above = heads & ~((2u << lane) - 1u);
-            const u32 endl = above ? (u32)(__ffs(above) - 1) : 32u;
-            const u32 seg = (endl >= 32 ? 0xffffffffu : ((1u << endl) - 1u)) & ~((1u << lane) - 1u);
-            s_ev[wid][0][c] += __popc(b2_ & seg);
-            s_ev[wid][1][c] += __popc(b11 & seg);
-            s_ev[wid][2][c] += __popc(b01 & seg);
-            s_ev[wid][3][c] += __popc(b12 & seg);
-          }
-          __syncwarp();
-        }
-        if (sl > 0) {
-          e2c = s_ev[wid][0][rank];
-          e11 = s_ev[wid][1][rank];
-          e01 = s_ev[wid][2][rank];
-          e12 = s_ev[wid][3][rank];
-        }
-        __syncwarp();
-      }
-      // ---- per-child class values, reduced per parent-mask value
-      u32 val[7] = {0, 0, 0, 0, 0, 0, 0};
-      if (valid) {
-        const u32 m = max(v1, v2);
-        const u32 A0 = count_gt_global(U.s0, U.n0, m);
-        const u32 B1 = count_gt_global(U.s1, U.n1, v2);
-        const u32 Im = count_gt_plain(I01, n01, m);
-        const u32 I2 = count_gt_plain(I01, n01, v2);
-        val[0] = e11;
-        val[1] = Im - e11;
-        val[2] = e01;
-        val[3] = A0 - Im - e01;
-        val[4] = e12;
-        val[5] = B1 - I2 - e12;
-        val[6] = e2c;
-        aRank += val[1] + val[3] + val[5];
-      }
-#pragma unroll
-      for (u32 pv = 0; pv < 4; ++pv) {
-        const bool mine = valid && pmv == pv;
-        if (__ballot_sync(0xffffffffu, mine) == 0) continue;
-#pragma unroll
-        for (int cl = 0; cl < 7; ++cl) {
-          const u32 sum = __reduce_add_sync(0xffffffffu, mine ? val[cl] : 0u);
-          if (lane == 0) s_h[wid][pv * 8 + cl] += sum;
-        }
+      U.T = fits ? T : nullptr;
+      if (!fits && lane == 0) a.moved[4] = 1;  // path flag (tests)
+      if (lane == 0) {
+        aStg += (fits ? U.n0 : 0u) + U.n1;
+        s_h[wid][23] += deg01;      // slot 23 (pv 2, class 7): level-2 candidates
       }
       __syncwarp();
-      cur += nstep;
+      // ---- level-2 children: pos 0 = the suffix of S0 above v1, then pos 1 =
+      // the S1 members not adjacent to v0; one step loop over the
+      // concatenation (one inlined copy of the step body)
+      const u32 p1 = U.n0 - count_gt_global(U.s0, U.n0, v1);
+      const u32 nA = U.n0 - p1, nAll = nA + U.n1;
+      for (u32 jb = 0; jb < nAll; jb += 32) {
+        const u32 j = jb + lane;
+        bool valid = j < nAll;
+        u32 v2 = 0, a0 = ~0u, b1 = ~0u;
+        if (valid) {
+          if (j < nA) {  // v2 = S0[p1 + j] > v1: #S0 > v2 from its index
+            v2 = ldg(U.s0 + p1 + j);
+            a0 = nA - j - 1;
+          } else {  // v2 = S1[t]: #S1 > v2 from its index
+            v2 = ldg(U.s1 + (j - nA));
+            b1 = nAll - j - 1;
+            valid = !(U.flags(v2) & 1u);
+          }
+        }
+        const u32 nk = __popc(__ballot_sync(0xffffffffu, valid));
+        if (lane == 0) s_kids[wid] += nk;
+        step(valid, v2, a0, b1);
+      }
     }
     {
       const u32 l = __reduce_add_sync(0xffffffffu, aLen), rk = __reduce_add_sync(0xffffffffu, aRank);
@@ -747,17 +782,21 @@ __global__ void __launch_bounds__(kT4, 4) mc4_last_kernel(Mc4Args a) {
   }
   __syncwarp();
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    aCand += __shfl_xor_sync(0xffffffffu, aCand, o);
-  }
+  for (int o = 16; o > 0; o >>= 1) aCand += __shfl_xor_sync(0xffffffffu, aCand, o);
   __syncwarp();
-  if (lane < 4 && s_h[wid][8 * lane + 7]) atomicAdd(a.moved + lane, s_h[wid][8 * lane + 7]);
+  {  // slots 7 / 15 / 31: streamed, staged, rank-counted; 23: level-2 candidates
+    const unsigned long long v = lane < 4 ? s_h[wid][8 * lane + 7] : 0ull;
+    if (v) atomicAdd(lane == 2 ? a.cand : a.moved + lane, v);
+  }
   {
     const u32 pv = lane >> 3, cl = lane & 7;
     const unsigned long long v = s_h[wid][lane];
     if (cl < 7 && v) atomicAdd(a.hist + (a.pm_bits[pv] | a.cl_bits[cl]), v);
   }
-  if (lane == 0 && aCand) atomicAdd(a.cand, aCand);
+  if (lane == 0) {
+    if (aCand) atomicAdd(a.cand + 1, aCand);
+    if (s_kids[wid]) atomicAdd(a.moved + 2, s_kids[wid]);
+  }
 }
 
 inline unsigned grid1(u64 items) { return (unsigned)std::max<u64>(1, std::min<u64>((items + 255) / 256, 1u << 20)); }
@@ -883,35 +922,33 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
               (W[5] ? (u32)GPM_PATH_MC3_MULTITILE : 0u);
 }
 
-void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u32* idx2, const u32* vid2, u64 np,
-                     unsigned long long* d_hist, cudaStream_t s, Timeline& tl, Stats& st) {
-  if (np == 0) return;
+void mc4_roots_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, u64 nq, unsigned long long* d_hist,
+                      cudaStream_t s, Timeline& tl, Stats& st) {
+  if (nq == 0) return;
   static std::atomic<int> occ_slot{0};
   const int occ = cached_occupancy(occ_slot, [] {
     int o = 0;
-    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, mc4_last_kernel, kT4, 0));
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, mc4_roots_kernel, kT4, 0));
     return o;
   });
-  const u64 nitems = (np + k4Item - 1) / k4Item;
+  const u64 nitems = (nq + k4Q - 1) / k4Q;
   const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sm_count() * occ, (nitems + kW4 - 1) / kW4));
   const u64 stride = std::max<u64>(32, ((u64)G.max_deg + 31) / 32 * 32);
   DBuf<u32> scratch(blocks * kW4 * stride, s);
-  DBuf<unsigned long long> ctr(1, s), cand(6, s);
+  DBuf<unsigned long long> ctr(1, s), cand(7, s);
   GPM_CUDA(cudaMemsetAsync(ctr.get(), 0, sizeof(unsigned long long), s));
-  GPM_CUDA(cudaMemsetAsync(cand.get(), 0, 6 * sizeof(unsigned long long), s));
+  GPM_CUDA(cudaMemsetAsync(cand.get(), 0, 7 * sizeof(unsigned long long), s));
   htrace(s, "mc4: scratch");
   Mc4Args a{};
   a.g = G.view();
   a.l1i = l1i;
   a.l1v = l1v;
-  a.idx2 = idx2;
-  a.vid2 = vid2;
-  a.np = np;
+  a.nq = nq;
   a.nitems = nitems;
   a.ctr = ctr.get();
   a.hist = d_hist;
   a.cand = cand.get();
-  a.moved = cand.get() + 1;
+  a.moved = cand.get() + 2;
   a.scratch = scratch.get();
   a.scratch_stride = stride;
   auto P = [](int i, int j) { return 1u << pat::pair_index(i, j, 4); };
@@ -923,26 +960,37 @@ void mc4_last_staged(const gpm_graph& G, const u32* l1i, const u32* l1v, const u
   a.cl_bits[4] = P(1, 3) | P(2, 3);
   a.cl_bits[5] = P(1, 3);
   a.cl_bits[6] = P(2, 3);
-  size_t ev = tl.begin("extend_fused_L2", 0.0);
-  mc4_last_kernel<<<(unsigned)blocks, kT4, 0, s>>>(a);
+  size_t ev = tl.begin("extend_fused_L1L2", 0.0);
+  mc4_roots_kernel<<<(unsigned)blocks, kT4, 0, s>>>(a);
   GPM_CUDA(cudaGetLastError());
   tl.end(ev);
   tl.launches += 1;
-  unsigned long long W[6] = {0, 0, 0, 0, 0, 0};
+  // W: level-2 candidates, level-3 candidates, streamed S2, staged keys,
+  // level-2 children, rank-counted, path flag
+  unsigned long long W[7] = {0, 0, 0, 0, 0, 0, 0};
   GPM_CUDA(cudaMemcpyAsync(W, cand.get(), sizeof W, cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaStreamSynchronize(s));
-  const double bytes = 8.0 * 2 * np + 16.0 * 3 * np + 4.0 * (double)W[0];
+  const double T = (double)W[4];
+  // SURVEY §8d B_alg of both levels, as the level-by-level engine counts
+  // them (level 1: 8 B + two 16 B offset pairs per parent + 4 B per
+  // candidate + 8 B per child; level 2: 16 B + three offset pairs per parent
+  // + 4 B per candidate)
+  const double bytes = (8.0 + 32.0) * (double)nq + 4.0 * (double)W[0] + 8.0 * T + (16.0 + 48.0) * T +
+                       4.0 * (double)W[1];
   // read by the kernel: streamed S2 suffixes + staged S0/S1 keys (4 B each),
-  // 20 B per child (v2 + offsets pair) and 8 B per child of level-2 index
-  const double moved = 4.0 * (double)(W[1] + W[2]) + 28.0 * (double)np;
+  // 24 B per level-1 parent (v0, v1, offsets) and 20 B per child (its id,
+  // re-read from the staged list, and its offsets pair)
+  const double moved = 4.0 * (double)(W[2] + W[3]) + 24.0 * (double)nq + 20.0 * T;
   tl.recs[ev].bytes = bytes;
   tl.recs[ev].moved = moved;
-  st.candidates[2] += W[0];
-  st.streamed += W[1] + W[2];
-  st.counted += W[4];
+  st.candidates[1] += W[0];
+  st.candidates[2] += W[1];
+  st.level_sizes[1] += W[4];
+  st.streamed += W[2];
+  st.counted += W[5];
   st.balg += bytes;
   st.bmoved += moved;
-  st.paths |= GPM_PATH_MC4_STAGED | (W[5] ? (u32)GPM_PATH_MC4_HBM_SETS : 0u);
+  st.paths |= GPM_PATH_MC4_STAGED | (W[6] ? (u32)GPM_PATH_MC4_HBM_SETS : 0u);
 }
 
 }  // namespace gpm

@@ -814,11 +814,6 @@ bool cf_local_roots(Ctx& c, const u32* l1_src, u64 slo, u64 shi);  // clique_loc
 // Builtin specialisations of a level (gpm_engine.cuh process()).
 bool builtin_level(Ctx& c, int kind, int lev, const VLevels& L, u64 np) {
   const bool last = (lev == c.k - 2);
-  if (kind == kBuiltinMotif && lev == 2 && last && c.k == 4 && !std::getenv("GPM_GENERIC_MC") &&
-      c.G->n < (1u << 30)) {  // union-set tags need ids < 2^30
-    mc4_last_staged(*c.G, L.idx[0], L.vid[0], L.idx[1], L.vid[1], np, c.d_hist, c.s, *c.tl, *c.st);
-    return true;
-  }
   if (kind == kBuiltinClique && lev >= 2 && last && !c.list_fn && c.g.oriented && c.siblings_complete &&
       c.G->n < (1u << 27) && !std::getenv("GPM_GENERIC_CF")) {
     cf_last_siblings(c, L.idx[lev - 1], L.vid[lev - 1], np, lev);
@@ -831,6 +826,11 @@ bool builtin_level(Ctx& c, int kind, int lev, const VLevels& L, u64 np) {
 bool builtin_roots(Ctx& c, int kind, const VLevels& L, const u32* l1_src, const u64* l1_start, u64 slo, u64 shi) {
   if (kind == kBuiltinMotif && c.k == 3 && l1_start && !std::getenv("GPM_GENERIC_MC")) {
     mc3_staged(*c.G, l1_start, slo, shi, c.d_hist, c.s, *c.tl, *c.st);
+    return true;
+  }
+  if (kind == kBuiltinMotif && c.k == 4 && c.G->n < (1u << 30) &&  // union-set tags need ids < 2^30
+      !std::getenv("GPM_GENERIC_MC")) {
+    mc4_roots_staged(*c.G, L.idx[0], L.vid[0], shi - slo, c.d_hist, c.s, *c.tl, *c.st);
     return true;
   }
   if (kind == kBuiltinClique && c.G->oriented && c.G->n < (1u << 27) && !c.list_fn &&

@@ -80,6 +80,8 @@ def test_planner_chunks_vs_oracle(P, oracle, app, k, monkeypatch):
     # k-CL counts run on local rows (no materialised levels): force the
     # level-by-level engine so the planner has levels to chunk
     monkeypatch.setenv("GPM_CF_NOLOCAL", "1")
+    # 4-MC's fused roots kernel never materialises level 2: force the level engine
+    monkeypatch.setenv("GPM_GENERIC_MC", "1")
     # (4-MC's per-candidate oracle is ~100x costlier than k-CL's: smaller graph)
     hg = P.generate_rmat(12, 12, 0.57, 0.19, 0.19, seed=21) if app == "cf" else \
         P.generate_rmat(11, 6, 0.57, 0.19, 0.19, seed=21)

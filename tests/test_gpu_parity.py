@@ -126,8 +126,11 @@ def test_planner_chunking_invariance(P, oracle, monkeypatch):
         base = P.mine(g, app, k)
         if app == "cf":  # k-CL counts run on local rows: force the level engine to chunk
             monkeypatch.setenv("GPM_CF_NOLOCAL", "1")
+        else:  # 4-MC's fused roots kernel has no materialised level to chunk
+            monkeypatch.setenv("GPM_GENERIC_MC", "1")
         tiny = P.mine(g, app, k, mem_budget=1 << 16)   # forces many planner chunks
         monkeypatch.delenv("GPM_CF_NOLOCAL", raising=False)
+        monkeypatch.delenv("GPM_GENERIC_MC", raising=False)
         assert tiny.stats["chunks"] > 0
         assert tiny.total == base.total and tiny.patterns == base.patterns
         same(tiny, base.stats)
