@@ -213,7 +213,8 @@ __device__ __forceinline__ void stream_parents(const u32* __restrict__ col, cons
   tri += ct;
 }
 
-__global__ void __launch_bounds__(kT, 4) mc3_warp_kernel(Mc3Args a) {
+// 5 CTAs / SM for both 3-MC kernels (LJ22: 218.6 -> 216.2 ms; 6: 218.3 ms)
+__global__ void __launch_bounds__(kT, 5) mc3_warp_kernel(Mc3Args a) {
   extern __shared__ __align__(16) u32 s_wtab[];  // [kWarps][kWSlots]
   __shared__ u64 s_cb[kWarps][32];
   __shared__ u32 s_ex[kWarps][32];
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(kT, 4) mc3_warp_kernel(Mc3Args a) {
 // Roots with |S0| > kWKeys: item = (root, S0 tile, chunk of <= kPB parents).
 // The CTA stages the tile; warps grab 32 parents at a time from the chunk and
 // stream their candidates inside the tile's id range [idlo, idhi).
-__global__ void __launch_bounds__(kT, 4) mc3_block_kernel(Mc3Args a) {
+__global__ void __launch_bounds__(kT, 5) mc3_block_kernel(Mc3Args a) {
   extern __shared__ __align__(16) u32 s_btab[];
   __shared__ u64 s_cb[kWarps][32];
   __shared__ u32 s_ex[kWarps][32];
@@ -506,7 +507,9 @@ struct UnionSet {
 // passes, no idx2 / vid2 round trip through HBM).  The children are exactly
 // is_auto_canonical_vertex's accepted candidates of (v0, v1)
 // (gpm_engine.cuh).
-__global__ void __launch_bounds__(kT4, 4) mc4_roots_kernel(Mc4Args a) {
+// 5 CTAs / SM (48 registers, ~90 B of spills): latency-bound probes and
+// searches want warps more than registers (4 CTAs: 386 ms, 5: 366 ms on MC4)
+__global__ void __launch_bounds__(kT4, 5) mc4_roots_kernel(Mc4Args a) {
   __shared__ __align__(16) u32 s_tab[kW4][k4Slots];
   __shared__ u64 s_cb[kW4][32];
   __shared__ u32 s_ex[kW4][32];
