@@ -1763,23 +1763,31 @@ struct Fsm {
     // count pre-filter -> bitmap slots (MNI <= count)
     std::vector<u32>& bslot = host_scratch<u32, 0>();
     std::vector<u32>& bs_to_pid = host_scratch<u32, 1>();
-    bslot.assign(std::max<u64>(1, R.P), ~0u);
-    bs_to_pid.clear();
-    // MNI <= count; the full-automorphism MNI unions an orbit's domains: <= nv * count
-    const bool full = cfg.mni_mode == GPM_MNI_AUTOMORPHISM;
+    std::vector<u32>& sslot = host_scratch<u32, 2>();
+    std::vector<u32>& sp_to_pid = host_scratch<u32, 3>();
     std::vector<u8>& need = host_scratch<u8, 0>();
-    need.assign(std::max<u64>(1, R.P), 0);
-    for (u64 p = 0; p < R.P; ++p)
-      need[p] = App::kDomains && R.gcount_h[p] * (full ? (u64)pat::code_nv(R.gkeys_h[p]) : 1) >= sigma;
+    const long long PP = (long long)std::max<u64>(1, R.P);
+    bslot.resize(PP);
+    sslot.resize(PP);
+    need.resize(PP);
+    bs_to_pid.clear();
+    sp_to_pid.clear();
+    // MNI <= count; the full-automorphism MNI unions an orbit's domains: <= nv * count
+    // (~10^6 patterns on the last level: the per-pattern host loops run on
+    // the host cores, ~9 ms single-threaded on the GPU box)
+    const bool full = cfg.mni_mode == GPM_MNI_AUTOMORPHISM;
+    const int HT = std::max(1, std::min(host_threads(), (int)(PP >> 14) + 1));
+#pragma omp parallel for num_threads(HT) schedule(static)
+    for (long long p = 0; p < PP; ++p) {
+      need[p] = p < (long long)R.P && App::kDomains &&
+                R.gcount_h[p] * (full ? (u64)pat::code_nv(R.gkeys_h[p]) : 1) >= sigma;
+      sslot[p] = ~0u;
+    }
     // sparse domains: a pattern whose keys (8 B per embedding
     // vertex, x2 for the sort) cost less than its dense label-local bitmap
     // rows -- big label classes, few embeddings -- gets sorted key lists
     // instead, within half the budget (GPM_FSM_SPARSE=1: every pattern).
     // Counts, words and the budget are rank-invariant, so is the choice.
-    std::vector<u32>& sslot = host_scratch<u32, 2>();
-    std::vector<u32>& sp_to_pid = host_scratch<u32, 3>();
-    sslot.assign(std::max<u64>(1, R.P), ~0u);
-    sp_to_pid.clear();
     R.skeys_total = 0;
     if (allow_sparse) {
       const bool force = std::getenv("GPM_FSM_SPARSE") != nullptr;
@@ -1800,11 +1808,35 @@ struct Fsm {
         R.skeys_total += kb / 16;
       }
     }
-    for (u64 p = 0; p < R.P; ++p)
-      if (need[p] && sslot[p] == ~0u) {
-        bslot[p] = (u32)bs_to_pid.size();
-        bs_to_pid.push_back((u32)p);
+    // dense bitmap slots in pattern order: per-thread counts, prefix, write
+    {
+      std::vector<u64> part(HT + 1, 0);
+#pragma omp parallel num_threads(HT)
+      {
+        const int t = host_thread();
+        const long long b = PP * t / HT, e = PP * (t + 1) / HT;
+        u64 c = 0;
+        for (long long p = b; p < e; ++p) c += need[p] && sslot[p] == ~0u;
+        part[t + 1] = c;
       }
+      for (int t = 0; t < HT; ++t) part[t + 1] += part[t];
+      bs_to_pid.resize(part[HT]);
+#pragma omp parallel num_threads(HT)
+      {
+        const int t = host_thread();
+        const long long b = PP * t / HT, e = PP * (t + 1) / HT;
+        u64 o = part[t];
+        for (long long p = b; p < e; ++p) {
+          if (need[p] && sslot[p] == ~0u) {
+            bslot[p] = (u32)o;
+            bs_to_pid[o++] = (u32)p;
+          } else {
+            bslot[p] = ~0u;
+          }
+        }
+      }
+    }
+    trace("group: host slots", (double)R.P);
     R.NB = bs_to_pid.size();
     R.NS = sp_to_pid.size();
     if (R.NS) st.paths |= GPM_PATH_FSM_SPARSE;
@@ -1890,6 +1922,7 @@ struct Fsm {
       for (u64 lo = 0; lo < R.NB; lo += per_round) {
         const u64 n = std::min(per_round, R.NB - lo);
         GPM_CUDA(cudaMemsetAsync(bm.get(), 0, sizeof(u32) * n * kpos * words, s));
+        trace("domain memset", (double)n * kpos * words * 4);
         run_domain(bm.get(), words, kpos, (u32)lo, (u32)(lo + n));
         // multi-GPU: OR the packed domain bitmaps across ranks (SURVEY §5 route ii)
         exchange_device(cfg, bm.get(), n * kpos * words, 4, 1, s);

@@ -44,6 +44,10 @@ struct gpm_result {
     gpm::u64 key;
     gpm::u64 support;
     int level;
+    // no zero-fill on resize(): the ~17 MB of records are first touched by
+    // the parallel writers in record() (host page faults cost ~1 ms per MB)
+    KeyPattern() {}
+    KeyPattern(gpm::u64 k, gpm::u64 s, int l) : key(k), support(s), level(l) {}
   };
   std::vector<KeyPattern> kpatterns;
   int label_bits = 0;                      // for formatting FSM keys lazily

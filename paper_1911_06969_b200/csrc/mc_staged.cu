@@ -549,7 +549,8 @@ __global__ void __launch_bounds__(kT4, 5) mc4_roots_kernel(Mc4Args a) {
       aLen += len;
     }
     // long S2 ranges (>= 32 candidates): one child at a time, warp-uniform
-    // thresholds, coalesced loads, four in flight, per-lane event counters
+    // thresholds, coalesced loads, two in flight (4: 366 ms, 2: 361, 1: 365),
+    // per-lane event counters
     u32 todo = __ballot_sync(0xffffffffu, len >= 32);
     while (todo) {
       const int i = __ffs(todo) - 1;
@@ -561,12 +562,12 @@ __global__ void __launch_bounds__(kT4, 5) mc4_roots_kernel(Mc4Args a) {
       const u32 cm = max(v1, cv2);
       u32 c2 = 0, c11 = 0, c01 = 0, c12 = 0;
       u32 j = 0;
-      for (; j + 128 <= L; j += 128) {
-        u32 u[4];
+      for (; j + 64 <= L; j += 64) {
+        u32 u[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) u[q] = ldg(g.col + b + j + 32 * q + lane);
+        for (int q = 0; q < 2; ++q) u[q] = ldg(g.col + b + j + 32 * q + lane);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 2; ++q) {
           const u32 f = U.flags(u[q]);
           c2 += (f == 0 && u[q] > v0);
           c11 += (f == 3 && u[q] > cm);
