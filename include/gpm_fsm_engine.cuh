@@ -1374,20 +1374,19 @@ __global__ void canon_slots_kernel(const unsigned long long* __restrict__ ent, c
 // pattern's bitmaps through the PositionMap (one warp per quick code).
 __global__ void merge_qbm_kernel(const u32* __restrict__ qbm, const u64* __restrict__ canon,
                                  const u32* __restrict__ ids, const u32* __restrict__ perm, u64 cap,
-                                 const u64* __restrict__ gkeys, u64 P, const u32* __restrict__ bslot, u32 round_lo,
-                                 u32 round_hi, u32* __restrict__ bitmaps, u64 words, int kpos) {
+                                 const unsigned long long* __restrict__ ent, const u32* __restrict__ occ,
+                                 const u32* __restrict__ bslot, u32 round_lo, u32 round_hi, u32* __restrict__ bitmaps,
+                                 u64 words, int kpos) {
   const int lane = threadIdx.x & 31;
   for (u64 sl = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; sl < cap;
        sl += ((u64)gridDim.x * blockDim.x) >> 5) {
     const u64 c = canon[sl];
     if (c == ~0ull) continue;
-    u64 lo = 0, hi = P;  // pattern id of the canonical key
-    while (lo < hi) {
-      const u64 mid = (lo + hi) >> 1;
-      if (gkeys[mid] < c) lo = mid + 1;
-      else hi = mid;
-    }
-    const u32 bs = bslot[lo];
+    // pattern id of the canonical key: slot_pid_kernel published it in the
+    // slot's value (a per-warp binary search over ~10^6 keys was ~20
+    // dependent loads per quick code, most of this kernel's time)
+    const u32 pid = (u32)(ent[2 * (u64)occ[sl] + 1] >> 32);
+    const u32 bs = bslot[pid];
     if (bs < round_lo || bs >= round_hi) continue;
     const int nv = pat::code_nv(c);
     const u32 pm = perm[sl];
@@ -1424,49 +1423,47 @@ __global__ void slot_pid_kernel(const u64* __restrict__ canon, const u32* __rest
 // MNI -- an embedding's mappings include every automorphism
 // of the pattern, so a position's domain is the union of the canonical
 // domains over its automorphism orbit; min over orbits.
+// One warp per bitmap pattern (8 per CTA): ~10^6 patterns of a few KB each
+// (a CTA per pattern was ~5 us of scheduling per pattern, 4 ms a level)
 __global__ void mni_kernel(const u32* __restrict__ bitmaps, u64 words, int kpos, const u64* __restrict__ gkeys,
                            const u32* __restrict__ bs_to_pid, u32 round_lo, u32 round_n, int LB, int full,
                            unsigned long long* __restrict__ mni) {
-  const u32 r = blockIdx.x;  // bitmap pattern within round
+  const u32 lane = threadIdx.x & 31;
+  const u32 r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // bitmap pattern within round
   if (r >= round_n) return;
   const u32 pid = bs_to_pid[round_lo + r];
   const u64 key = gkeys[pid];
   const int nv = pat::code_nv(key);
-  __shared__ unsigned long long part[32];
-  __shared__ unsigned long long best;
-  __shared__ u8 rep[8];
-  if (threadIdx.x == 0) {
-    best = ~0ull;
-    for (int i = 0; i < 8; ++i) rep[i] = (u8)i;
-    if (full) {
+  // orbit representative of each position, 4 bits each (identity unless full)
+  u32 reps = 0x76543210u;
+  if (full) {
+    if (lane == 0) {
       int n2;
       u32 lab[8], mask;
+      u8 rep[8];
+      for (int i = 0; i < 8; ++i) rep[i] = (u8)i;
       pat::decode(key, LB, &n2, lab, &mask);
       pat::orbits(nv, lab, mask, rep);
+      reps = 0;
+      for (int i = 0; i < 8; ++i) reps |= (u32)rep[i] << (4 * i);
     }
+    reps = __shfl_sync(0xffffffffu, reps, 0);
   }
-  __syncthreads();
+  unsigned long long best = ~0ull;
   for (int pos = 0; pos < nv; ++pos) {
-    if (rep[pos] != pos) continue;  // counted with its orbit's representative
+    if (((reps >> (4 * pos)) & 15u) != (u32)pos) continue;  // counted with its orbit's representative
     const u32* bm = bitmaps + ((u64)r * kpos + pos) * words;
-    unsigned long long c = 0;
-    for (u64 w = threadIdx.x; w < words; w += blockDim.x) {
+    u32 c = 0;
+    for (u64 w = lane; w < words; w += 32) {
       u32 v = bm[w];
       for (int o = pos + 1; o < nv; ++o)
-        if (rep[o] == pos) v |= bitmaps[((u64)r * kpos + o) * words + w];
+        if (((reps >> (4 * o)) & 15u) == (u32)pos) v |= bitmaps[((u64)r * kpos + o) * words + w];
       c += __popc(v);
     }
-    c = __reduce_add_sync(0xffffffffu, (unsigned)c);
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long t = 0;
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
-      best = min(best, t);
-    }
-    __syncthreads();
+    c = __reduce_add_sync(0xffffffffu, c);  // <= n / labels bits per position
+    best = min(best, (unsigned long long)c);
   }
-  if (threadIdx.x == 0) mni[pid] = best;
+  if (lane == 0) mni[pid] = best;
 }
 
 // packed orbit representatives of every sparse slot (identity unless
@@ -1566,6 +1563,10 @@ struct Fsm {
   DBuf<u32> lrank;   // vertex -> rank within its label class
   DBuf<u32> labrank; // vertex -> label << 27 | rank (fan pass; LB <= 5)
   u64 max_class = 1;
+  // words of one label-local domain row (padding rows to 16 bytes for
+  // vector loads in merge_qbm measured slower: 5.7 -> 11.3 ms, the lanes'
+  // ORs no longer coalesce)
+  u64 dom_words() const { return (max_class + 31) / 32; }
 
   // lrank[v] = #{u < v : lab[u] == lab[v]} via a stable sort of (label, v)
   void label_ranks() {
@@ -1791,7 +1792,7 @@ struct Fsm {
     R.skeys_total = 0;
     if (allow_sparse) {
       const bool force = std::getenv("GPM_FSM_SPARSE") != nullptr;
-      const u64 words = (max_class + 31) / 32;
+      const u64 words = dom_words();
       std::vector<std::pair<u64, u32>> cand;
       for (u64 p = 0; p < R.P; ++p) {
         if (!need[p]) continue;
@@ -1911,7 +1912,7 @@ struct Fsm {
     // label-local domain bitmaps: a position's vertices all carry its label,
     // so bits are indexed by the rank within the label class (n/#labels bits
     // per position instead of n)
-    const u64 words = (max_class + 31) / 32;
+    const u64 words = dom_words();
     const u64 per_pat = (u64)kpos * words * 4;
     const u64 per_round = std::max<u64>(1, std::min<u64>(R.NB, budget / 2 / std::max<u64>(1, per_pat)));
     DBuf<unsigned long long> mni(std::max<u64>(1, R.P), s);
@@ -1927,7 +1928,7 @@ struct Fsm {
         // multi-GPU: OR the packed domain bitmaps across ranks (SURVEY §5 route ii)
         exchange_device(cfg, bm.get(), n * kpos * words, 4, 1, s);
         trace("domain round", (double)lo, (double)n);
-        mni_kernel<<<(unsigned)n, 256, 0, s>>>(bm.get(), words, kpos, R.gkeys.get(), R.bs_to_pid.get(), (u32)lo,
+        mni_kernel<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(bm.get(), words, kpos, R.gkeys.get(), R.bs_to_pid.get(), (u32)lo,
                                                (u32)n, LB, cfg.mni_mode == GPM_MNI_AUTOMORPHISM, mni.get());
         GPM_CUDA(cudaGetLastError());
         ++tl.launches;
@@ -2369,12 +2370,12 @@ struct Fsm {
     // fused last level: the fan-out pass over parents grouped by exact code
     // (the grouped and fan passes inline the builtin to_add_edge: builtin FSM only)
     const bool fan_ok = App::kBuiltin && last && nz && !std::getenv("GPM_FSM_NOFAN") &&
-                        !std::getenv("GPM_FSM_TWO_PASS") && fan_fits(LEV, LEV + 2, (max_class + 31) / 32);
+                        !std::getenv("GPM_FSM_TWO_PASS") && fan_fits(LEV, LEV + 2, dom_words());
     {
       GroupArgs probe{};
       size_t sm = 0;
       gr.on = App::kBuiltin && nz && !fan_ok && !std::getenv("GPM_FSM_UNGROUPED") &&
-              group_geometry(kDomain, LEV + 2, (max_class + 31) / 32, probe, sm);
+              group_geometry(kDomain, LEV + 2, dom_words(), probe, sm);
     }
     if (gr.on) sort_parents<LEV>(L, pidx, nz, gkeys_sorted);
     DBuf<u64> Wp(nz + 1, s);
@@ -2428,7 +2429,7 @@ struct Fsm {
     // canonicalisation these are merged into the canonical patterns' bitmaps
     // through the PositionMaps, so the level is extended once, not twice.
     const int kposL = LEV + 2;
-    const u64 wordsL = (max_class + 31) / 32;
+    const u64 wordsL = dom_words();
     const u64 per_id = (u64)kposL * wordsL * 4;
     DBuf<u32> qbm;
     DBuf<int> qover(1, s);
@@ -2496,7 +2497,7 @@ struct Fsm {
       if (!nb) return;
       if (fused) {
         merge_qbm_kernel<<<grid1(std::max<u64>(1, R.U) * 32), 256, 0, s>>>(qbm.get(), R.canon.get(), R.ids.get(), R.perm.get(), R.U,
-                                                           R.gkeys.get(), R.P, R.bslot.get(), lo, hi, bm, words, kpos);
+                                                           R.ent.get(), R.occ.get(), R.bslot.get(), lo, hi, bm, words, kpos);
         GPM_CUDA(cudaGetLastError());
         ++tl.launches;
         return;
