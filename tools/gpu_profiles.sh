@@ -6,7 +6,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --app cf4 --steps 2 --warmup 3 --no-cpu-baseline --no-sub > /dev/null 2>&1
 # target : kernel regex (demangled name) : launches to skip : count
 for spec in "cf4:local_warp_kernel.*int.64:1:1" "tc:edge_lane_kernel:0:1" "mc3:mc3_warp:0:1" "mc3:mc3_block:0:1" \
-            "mc4:mc4_last:0:1" "fsm:efan_kernel:0:1"; do
+            "mc4:mc4_roots:0:1" "fsm:efan_kernel:0:1"; do
   IFS=: read t rx sk ct <<< "$spec"
   tag=$(echo "$rx" | sed 's/[^A-Za-z0-9_]//g' | cut -c1-24)
   timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$rx" \

@@ -19,7 +19,7 @@ os.makedirs(out, exist_ok=True)
 # dominant timeline record per bench workload -> the kernels it is made of
 # (3-MC's "extend_fused_L1" is the warp kernel + the tiled block kernel)
 DOMINANT = {"cf4": ["local_warp_kernel"], "tc": ["edge_lane_kernel", "edge_chunk"], "mc3": ["mc3_warp", "mc3_block"],
-            "mc4": ["mc4_last"], "fsm": ["efan_kernel"]}
+            "mc4": ["mc4_roots"], "fsm": ["efan_kernel"]}
 traffic = {}
 
 
