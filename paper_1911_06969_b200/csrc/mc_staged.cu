@@ -430,13 +430,16 @@ struct Mc4Args {
 // Union hash set of S0 and S1: slot = (id << 2) | (in S0) | (in S1) << 1
 // (ids < 2^30).  One probe answers both memberships.
 __device__ __forceinline__ u32 us_flags(const u32* T, u32 sh, u32 bmask, u32 v) {
+  // slot = id << 2 | flags: (slot ^ v << 2) < 4 <=> same id; the empty slot
+  // ~0u never matches (ids < 2^30 - 1)
+  const u32 vk = v << 2;
   u32 b = (v * kHashMul) >> sh;  // bucketised (4 slots, one LDS.128), see hb_has
   for (;;) {
     const uint4 x = *reinterpret_cast<const uint4*>(T + 4 * b);
-    if ((x.x >> 2) == v && x.x != kEmpty) return x.x & 3u;
-    if ((x.y >> 2) == v && x.y != kEmpty) return x.y & 3u;
-    if ((x.z >> 2) == v && x.z != kEmpty) return x.z & 3u;
-    if ((x.w >> 2) == v && x.w != kEmpty) return x.w & 3u;
+    if ((x.x ^ vk) < 4u) return x.x & 3u;
+    if ((x.y ^ vk) < 4u) return x.y & 3u;
+    if ((x.z ^ vk) < 4u) return x.z & 3u;
+    if ((x.w ^ vk) < 4u) return x.w & 3u;
     if (x.w == kEmpty) return 0;
     b = (b + 1) & bmask;
   }
@@ -515,16 +518,15 @@ __global__ void __launch_bounds__(kT4, 5) mc4_roots_kernel(Mc4Args a) {
   __shared__ u32 s_ex[kW4][32];
   __shared__ u32 s_v2[kW4][32];
   __shared__ unsigned long long s_h[kW4][32];
-  __shared__ unsigned long long s_kids[kW4];
+  __shared__ unsigned long long s_kids[kW4], s_cand[kW4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const DevGraph& g = a.g;
   u32* T = s_tab[wid];
   u32* I01 = a.scratch + (blockIdx.x * (u64)kW4 + wid) * a.scratch_stride;
   s_h[wid][lane] = 0;
-  if (lane == 0) s_kids[wid] = 0;
+  if (lane == 0) s_kids[wid] = s_cand[wid] = 0;
   // per-item counters (streamed, staged, rank-counted), folded into the
   // unused class slot 7 of each parent-mask row of s_h per item
-  unsigned long long aCand = 0;
   u32 aLen = 0, aStg = 0, aRank = 0;
   UnionSet U{};
   u32 v0 = 0, v1 = 0, n01 = 0;
@@ -545,8 +547,13 @@ __global__ void __launch_bounds__(kT4, 5) mc4_roots_kernel(Mc4Args a) {
       st = lower_bound_col(g.col, b2, e2, v0 + 1);
       len = (u32)(e2 - st);
       pmv = U.flags(v2);  // bit 0: v2 ~ v0, bit 1: v2 ~ v1
-      aCand += (u64)deg01 + (e2 - b2);
       aLen += len;
+    }
+    {  // level-3 candidates of the step's children (deg v0 + deg v1 + deg v2),
+       // summed in 16-bit halves so the warp sums fit 32 bits
+      const u32 cc = valid ? deg01 + (u32)(ldg(g.off + v2 + 1) - ldg(g.off + v2)) : 0u;
+      const u32 lo = __reduce_add_sync(0xffffffffu, cc & 0xffffu), hi = __reduce_add_sync(0xffffffffu, cc >> 16);
+      if (lane == 0) s_cand[wid] += (unsigned long long)lo + ((unsigned long long)hi << 16);
     }
     // long S2 ranges (>= 32 candidates): one child at a time, warp-uniform
     // thresholds, coalesced loads, two in flight (4: 366 ms, 2: 361, 1: 365),
@@ -785,9 +792,6 @@ __global__ void __launch_bounds__(kT4, 5) mc4_roots_kernel(Mc4Args a) {
     }
   }
   __syncwarp();
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) aCand += __shfl_xor_sync(0xffffffffu, aCand, o);
-  __syncwarp();
   {  // slots 7 / 15 / 31: streamed, staged, rank-counted; 23: level-2 candidates
     const unsigned long long v = lane < 4 ? s_h[wid][8 * lane + 7] : 0ull;
     if (v) atomicAdd(lane == 2 ? a.cand : a.moved + lane, v);
@@ -798,7 +802,7 @@ __global__ void __launch_bounds__(kT4, 5) mc4_roots_kernel(Mc4Args a) {
     if (cl < 7 && v) atomicAdd(a.hist + (a.pm_bits[pv] | a.cl_bits[cl]), v);
   }
   if (lane == 0) {
-    if (aCand) atomicAdd(a.cand + 1, aCand);
+    if (s_cand[wid]) atomicAdd(a.cand + 1, s_cand[wid]);
     if (s_kids[wid]) atomicAdd(a.moved + 2, s_kids[wid]);
   }
 }
