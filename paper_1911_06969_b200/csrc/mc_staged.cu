@@ -826,7 +826,16 @@ void mc3_staged(const gpm_graph& G, const u64* l1s, u64 lo, u64 hi, unsigned lon
   GPM_CUDA(cudaMemsetAsync(ismall.get() + nr, 0, sizeof(u64), s));
   GPM_CUDA(cudaMemsetAsync(ibig.get() + nr, 0, sizeof(u64), s));
   // block-kernel tile: GPM_MC3_TILE keys (default kBKeys) at load <= 1/4..1/8
-  static const u32 tile_env = std::getenv("GPM_MC3_TILE") ? (u32)std::atoi(std::getenv("GPM_MC3_TILE")) : 0u;
+  // (the tile's hash has a power-of-two capacity: the knob is rounded up to
+  // a power of two in [256, 8192]; 3072 used to overrun the table)
+  static const u32 tile_env = [] {
+    const char* e = std::getenv("GPM_MC3_TILE");
+    const long t = e ? std::atol(e) : 0;
+    if (t <= 0) return 0u;
+    u32 p = 256;
+    while (p < (u32)std::min<long>(t, 8192)) p <<= 1;
+    return p;
+  }();
   const u32 bkeys = tile_env ? tile_env : kBKeys;
   const u32 bslots = std::max<u32>(kBSlots, bkeys * 4 > kBSlots ? (bkeys * 4 + 1023) & ~1023u : kBSlots);
   mc3_items_kernel<<<grid1(nr), 256, 0, s>>>(l1s, lo, hi, vr[0], nr, bkeys, ismall.get(), ibig.get());
