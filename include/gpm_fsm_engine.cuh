@@ -1037,7 +1037,11 @@ __global__ void __launch_bounds__(kGT, 1) egroup_kernel(FsmArgs a, GroupArgs ga)
 // state the rest of the fused path (canonicalise, merge_qbm) consumes.
 // Lanes map to the candidates N(v_q) of one parent at a time (coalesced);
 // parent descriptors are built 32 at a time, one per lane, into shared memory.
-constexpr int kFT = 256;                 // threads per fan CTA (two CTAs per SM)
+// threads per fan CTA: 14 warps when two such CTAs fit an SM (the fan pass is
+// latency-bound at 2 CTAs/SM: FSM17 256 -> 122.4 ms, 320 -> 110.7, 384 ->
+// 102.9, 448 -> 97.5; one CTA of 512-704 threads: 123-145 ms), else 8
+constexpr int kFT = 256;
+constexpr int kFTWide = 448;
 constexpr int kRankBits = 27;            // labrank[v] = label << 27 | rank within the label class
 constexpr u32 kRankMask = (1u << kRankBits) - 1;
 constexpr u32 kFanParents = 4096;        // parents per item (large groups split)
@@ -1070,10 +1074,10 @@ struct FanDesc {  // per-warp parent descriptors, struct of arrays over 32 lanes
   u32 stp[32];
 };
 
-template <int LEV>
-__global__ void __launch_bounds__(kFT, 2) efan_kernel(FsmArgs a, FanArgs fa) {
+template <int LEV, int FT>
+__global__ void __launch_bounds__(FT, 2) efan_kernel(FsmArgs a, FanArgs fa) {
   constexpr int MV = LEV + 1;
-  constexpr int NW = kFT / 32;
+  constexpr int NW = FT / 32;
   extern __shared__ __align__(16) unsigned char fsm_fan_smem[];
   const u32 nslot = fa.nl + MV;
   const u64 rowlen = (u64)a.kpos * a.words;
@@ -1087,9 +1091,9 @@ __global__ void __launch_bounds__(kFT, 2) efan_kernel(FsmArgs a, FanArgs fa) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   FanDesc<LEV>& D = descs[wid];
   unsigned long long acc = 0;
-  for (u64 i = threadIdx.x; i < (u64)nslot * rowlen; i += kFT) rows[i] = 0u;
+  for (u64 i = threadIdx.x; i < (u64)nslot * rowlen; i += FT) rows[i] = 0u;
   for (;;) {
-    for (u32 i = threadIdx.x; i < nslot; i += kFT) cnt[i] = 0u;
+    for (u32 i = threadIdx.x; i < nslot; i += FT) cnt[i] = 0u;
     if (threadIdx.x == 0) {
       s_item = atomicAdd(fa.ctr, 1ull);
       if (s_item < fa.nitems) s_bnext = fa.items[s_item].pa;
@@ -1245,7 +1249,7 @@ __global__ void __launch_bounds__(kFT, 2) efan_kernel(FsmArgs a, FanArgs fa) {
     }
     __syncthreads();
     // ---- flush: count -> quick-code hash (dense id), rows -> the id's qbm rows
-    for (u32 sl = threadIdx.x; sl < nslot; sl += kFT) {
+    for (u32 sl = threadIdx.x; sl < nslot; sl += FT) {
       u32 id = 0;
       if (cnt[sl]) {
         u64 code;
@@ -2223,9 +2227,9 @@ struct Fsm {
   }
 
   // ---------------------------------------------------------- fan-out pass (last level)
-  size_t fan_smem(int LEVv, int kpos, u64 words) const {
+  size_t fan_smem(int LEVv, int kpos, u64 words, int ft = kFT) const {
     const u64 nslot = (u64(1) << LB) + LEVv + 1;
-    const u64 desc = (u64)(kFT / 32) * (8 * 32 * (2 + 2 * LEVv + 1) + 4 * 32 * (3 + 2 * (LEVv + 1))) + 64;
+    const u64 desc = (u64)(ft / 32) * (8 * 32 * (2 + 2 * LEVv + 1) + 4 * 32 * (3 + 2 * (LEVv + 1))) + 64;
     return (size_t)(4 * (nslot * kpos * words + 2 * nslot + 2) + desc);
   }
   bool fan_fits(int LEVv, int kpos, u64 words) const {
@@ -2323,17 +2327,28 @@ struct Fsm {
     fa.nitems = nitems;
     fa.ctr = d_ctr.get();
     fa.nl = 1u << LB;
-    const size_t smem = fan_smem(LEV, a.kpos, a.words);
-    auto kern = efan_kernel<LEV>;
-    GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFT, smem));
+    // wide CTAs when two of them fit an SM, else the 8-warp CTA
+    size_t smem = fan_smem(LEV, a.kpos, a.words, kFTWide);
+    auto kern = efan_kernel<LEV, kFTWide>;
+    int ft = kFTWide, occ = 0, maxs = 0;
+    GPM_CUDA(cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, G.device));
+    if (smem + 1024 <= (size_t)maxs && !std::getenv("GPM_FSM_FAN_NARROW")) {
+      GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFTWide, smem));
+    }
+    if (occ < 2) {
+      smem = fan_smem(LEV, a.kpos, a.words, kFT);
+      kern = efan_kernel<LEV, kFT>;
+      ft = kFT;
+      GPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFT, smem));
+    }
     occ = std::max(1, occ);
     const u64 blocks = std::max<u64>(1, std::min<u64>((u64)sms * occ, nitems));
     GPM_CUDA(cudaMemsetAsync(d_ctr.get(), 0, sizeof(unsigned long long), s));
     st.paths |= GPM_PATH_FSM_FAN;
     size_t ev = tl.begin(std::string(name) + "_L" + std::to_string(LEV), bytes);
-    kern<<<(unsigned)blocks, kFT, smem, s>>>(a, fa);
+    kern<<<(unsigned)blocks, ft, smem, s>>>(a, fa);
     GPM_CUDA(cudaGetLastError());
     tl.end(ev);
     ++tl.launches;

@@ -9,6 +9,7 @@ the same inputs (totals, pattern maps, per-level sizes, candidates, B_alg):
   GPM_CF_NOLOCAL   k-CL (k >= 4): level-by-level instead of per-root local rows
   GPM_GENERIC_MC   MC: per-candidate binary search instead of staged sets
   GPM_FSM_TWO_PASS FSM last level: separate domain pass instead of the fused one
+  GPM_FSM_FAN_NARROW FSM fan pass: 8-warp CTAs instead of 14-warp ones
 """
 import os
 
@@ -97,3 +98,12 @@ def test_fsm_sparse_domains_equal_bitmaps(P, labels, sigma, k):
         sp = _run(P, g, "fsm", k, sigma, env=["GPM_FSM_SPARSE", "GPM_FSM_TWO_PASS"], mni=mni)
         assert sp.stats["paths"] & _lib.PATH_FSM_SPARSE
         _same(sp, _run(P, g, "fsm", k, sigma, env=["GPM_FSM_TWO_PASS"], mni=mni))
+
+
+@pytest.mark.parametrize("labels,sigma,k", [(8, 20, 3), (16, 10, 4)])
+def test_fsm_fan_narrow_ctas(P, labels, sigma, k):
+    # the fan pass runs 14-warp CTAs when two fit an SM, else 8-warp CTAs
+    # (GPM_FSM_FAN_NARROW forces the latter): same patterns and supports
+    g = P.Graph(P.generate_rmat(12, 8, 0.45, 0.15, 0.15, seed=5, n_labels=labels, label_seed=9))
+    _same(_run(P, g, "fsm", k, sigma), _run(P, g, "fsm", k, sigma, env=["GPM_FSM_FAN_NARROW"]))
+
