@@ -1299,6 +1299,15 @@ __global__ void pcode_kernel(DevGraph g, ELevels L, const u32* __restrict__ pidx
   }
 }
 
+// codes <-> sort keys: rotate the vertex-count nibble (bits 60-63) to the
+// bottom so the occupied bits are contiguous from bit 0 (fewer radix passes)
+__global__ void rotl4_kernel(u64* __restrict__ c, u64 n, int left) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const u64 x = c[i];
+    c[i] = left ? (x << 4) | (x >> 60) : (x >> 4) | (x << 60);
+  }
+}
+
 __global__ void gstart64_kernel(const u64* __restrict__ keys, u64 n, u8* __restrict__ flag) {
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
     flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
@@ -2247,15 +2256,23 @@ struct Fsm {
     codes.alloc(nz, s);
     pcode_kernel<LEV><<<grid1(nz), 256, 0, s>>>(g, L, pidx.get(), nz, LB, codes.get());
     GPM_CUDA(cudaGetLastError());
+    // a parent has LEV edges, so <= LEV + 1 vertices: its code below bit 60
+    // fits npairs + nv x LB bits; with the nv nibble rotated to the bottom the
+    // sort needs 4 + that many bits (FSM17 level 2: 22 instead of 64)
+    const int nvmax = LEV + 1;
+    const int bits = std::min(64, 4 + pat::npairs(nvmax) + nvmax * LB);
+    rotl4_kernel<<<grid1(nz), 256, 0, s>>>(codes.get(), nz, 1);
     DBuf<u64> k2(nz, s);
     DBuf<u32> p2(nz, s);
     size_t tmp = 0;
     GPM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, codes.get(), k2.get(), pidx.get(), p2.get(), (int64_t)nz, 0,
-                                             64, s));
+                                             bits, s));
     DBuf<u8> t(tmp, s);
     GPM_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, codes.get(), k2.get(), pidx.get(), p2.get(), (int64_t)nz, 0,
-                                             64, s));
-    tl.launches += 9;
+                                             bits, s));
+    rotl4_kernel<<<grid1(nz), 256, 0, s>>>(k2.get(), nz, 0);
+    GPM_CUDA(cudaGetLastError());
+    tl.launches += 11;
     codes = std::move(k2);
     pidx = std::move(p2);
   }
